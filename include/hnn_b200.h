@@ -1,0 +1,254 @@
+/*
+ * hnn_b200.h — C-ABI of the B200 hybrid-training hot path.
+ *
+ * Replaces, for all N merged models at once, the per-model numpy work the
+ * reference does inside train.run_batch (pkg/src/hybridnn/train.py:223-256):
+ *
+ *   entry point                 replaces (reference file:line)
+ *   --------------------------  -------------------------------------------------------
+ *   hnn_step_begin              per-batch schedule: store.batches / lr_at_epoch / opt step
+ *                               (store.py:68-81, optim.py:22-30, optim.py:57,73-76)
+ *   hnn_gather_rows             Batch(x=train_x[idx], y=train_y[idx])   (store.py:77-80)
+ *   hnn_grouped_gemm            dense fwd / bwd  _dense_fwd, _dense_bwd (ops.py:46-55) with
+ *                               relu fwd/bwd fused (ops.py:62-67)
+ *   hnn_grouped_conv            conv2d fwd / bwd _conv2d_fwd, _conv2d_bwd (ops.py:100-130)
+ *   hnn_conv_wgrad_reduce       the fixed-order finish of the conv weight/bias gradient
+ *   hnn_grouped_maxpool         maxpool2d fwd / bwd (ops.py:149-174), relu mask fused
+ *   hnn_grouped_relu            stand-alone relu fwd / bwd (ops.py:62-67)
+ *   hnn_sce_fused               softmax_cross_entropy + argmax accuracy + non-finite abort
+ *                               (ops.py:220-251, train.py:239-243,252-255)
+ *   hnn_multi_tensor_sgd        optim.apply_update, SGD / momentum branch (optim.py:59-71)
+ *   hnn_multi_tensor_adam       optim.apply_update, Adam branch (optim.py:73-87)
+ *   hnn_last_error              error text for the last nonzero status on this thread
+ *
+ * Conventions (every entry point):
+ *   - all pointers are caller-owned DEVICE memory except where noted; the
+ *     problem tables themselves live in device memory;
+ *   - every call is asynchronous and stream-ordered on `stream`
+ *     (a cudaStream_t passed as void*); no allocation, no host sync;
+ *   - return 0 on success, a nonzero HNN_ERR_* otherwise (no C++ exception
+ *     crosses the ABI); hnn_last_error() describes the failure;
+ *   - a model takes part in a launch only if its current schedule row has
+ *     active != 0 and (when a status array is passed) its status.alive != 0;
+ *   - results per model never depend on which other models share a launch:
+ *     tiling is a fixed function of each problem's own shape, there are no
+ *     atomics and no data-dependent split-K, so isolation is bit-exact.
+ */
+#ifndef HNN_B200_H
+#define HNN_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define HNN_OK 0
+#define HNN_ERR_INVALID 1     /* bad argument / unsupported shape */
+#define HNN_ERR_CUDA 2        /* a CUDA runtime call failed */
+#define HNN_ERR_UNSUPPORTED 3 /* feature not built into this library */
+
+/* hnn_grouped_gemm / hnn_grouped_conv `op` */
+#define HNN_FWD 0
+#define HNN_DGRAD 1
+#define HNN_WGRAD 2
+
+/* hnn_grouped_gemm `prec` */
+#define HNN_PREC_F32_SIMT 0   /* fp32 FFMA, CUDA cores */
+#define HNN_PREC_F32_3XTF32 1 /* tcgen05 kind::tf32, hi/lo split, fp32 accumulate in TMEM */
+
+/* optimizer segment kinds */
+#define HNN_OPT_SGD 0
+#define HNN_OPT_SGD_MOMENTUM 1
+#define HNN_OPT_ADAM 2
+
+/* One model's schedule for the current step (device array, one row per model). */
+typedef struct hnn_step_row {
+  int32_t active;    /* model trains (or evaluates) at this step */
+  int32_t rows;      /* real rows in this batch (<= the model's batch capacity) */
+  int32_t perm_base; /* index into the model's permutation of the batch's first row */
+  int32_t epoch;     /* zero-based epoch of this batch */
+  int32_t batch;     /* zero-based batch index within the epoch */
+  int32_t opt_step;  /* optimizer step count t after this update (1-based) */
+  float lr;          /* F32(lr_at_epoch(...)) */
+  float bias1;       /* F32(1 - 0.9^t)   (Adam) */
+  float bias2;       /* F32(1 - 0.999^t) (Adam) */
+  int32_t reserved[3];
+} hnn_step_row; /* 48 bytes */
+
+/* Persistent per-model device status, updated by hnn_sce_fused. */
+typedef struct hnn_model_status {
+  int32_t alive;       /* 0 once a non-finite loss was seen (the job aborts) */
+  int32_t abort_epoch; /* epoch / batch of the first non-finite loss, -1 if none */
+  int32_t abort_batch;
+  int32_t last_correct;
+  float last_loss;
+  int32_t reserved;
+  double loss_sum;     /* sum of F64(loss) * rows since the host last reset it */
+  int64_t correct_sum; /* argmax hits since the last reset */
+  int64_t seen;        /* rows since the last reset */
+} hnn_model_status; /* 48 bytes */
+
+/* Copy sched[*counter] (n_models rows) into cur and advance *counter. 1 block. */
+int hnn_step_begin(const hnn_step_row* sched, int32_t* counter, hnn_step_row* cur, int n_models, void* stream);
+
+typedef struct hnn_gather_problem {
+  const float* src_x;     /* dataset samples [n, sample] */
+  const int32_t* src_y;   /* dataset labels as int32 class ids [n] */
+  const int32_t* perm;    /* this model's epoch permutation [n] (identity for evaluation) */
+  float* dst_x;           /* batch [cap, ld_dst]; rows >= rows are zero-filled */
+  int32_t* dst_y;         /* batch labels [cap]; rows >= rows get 0 */
+  int32_t sample;         /* floats per sample */
+  int32_t ld_dst;         /* row stride of dst_x in floats */
+  int32_t cap;            /* batch capacity (the job's batch_size) */
+  int32_t model;
+} hnn_gather_problem;
+
+int hnn_gather_rows(const hnn_gather_problem* probs, int nprob, int max_cap, const hnn_step_row* cur,
+                    void* stream);
+
+/*
+ * Row-major grouped GEMM problem.  Let R = cur[model].rows.
+ *  FWD:   C[i,j] = sum_k A[i*lda+k] * B[j*ldb+k] + bias[j]; relu if `relu`;   i < m (= cap), rows >= R -> 0
+ *  DGRAD: C[i,j] = sum_k A[i*lda+k] * B[k*ldb+j]; times (mask[i*ldc+j] > 0) if mask; rows >= R -> 0
+ *  WGRAD: C[i,j] = sum_{r<R} A[r*lda+i] * B[r*ldb+j]; dbias[i] = sum_{r<R} A[r*lda+i] (row order)
+ * tile_base / tiles_n are filled by the planner (tiles of the chosen kernel, see hnn_gemm_tiles).
+ */
+typedef struct hnn_gemm_problem {
+  const float* a;
+  const float* b;
+  float* c;
+  const float* bias;
+  const float* mask;
+  float* dbias;
+  int32_t m, n, k;
+  int32_t lda, ldb, ldc;
+  int32_t model;
+  int32_t relu;
+  int32_t tile_base;
+  int32_t tiles_n;
+} hnn_gemm_problem;
+
+/* Tile edge (m, n) used by (op, prec); lets the host lay out tile_base / tiles_n. */
+int hnn_gemm_tile_shape(int op, int prec, int32_t* tile_m, int32_t* tile_n);
+
+int hnn_grouped_gemm(int op, int prec, const hnn_gemm_problem* probs, int nprob, int total_tiles,
+                     const hnn_step_row* cur, const hnn_model_status* status, void* stream);
+
+/*
+ * Implicit-GEMM convolution on NCHW, zero padding `pad`, square kernel k.
+ *  FWD:   y = conv(x, w) + bias (relu if `relu`), rows >= R zero        GEMM M=cap*OH*OW, N=F, K=C*k*k
+ *  DGRAD: dx = conv_transpose(dy, w), times (mask > 0) if mask          GEMM M=cap*H*W,   N=C, K=F*k*k
+ *  WGRAD: partial[s] = sum over the s-th fixed chunk of (rows x OH x OW) of dy (x) im2col(x),
+ *         column C*k*k of each partial holding the bias-gradient chunk; then hnn_conv_wgrad_reduce.
+ */
+typedef struct hnn_conv_problem {
+  const float* x;
+  const float* weight; /* [F, C, k, k] */
+  const float* bias;
+  float* y;
+  const float* dy;
+  float* dx;
+  const float* mask;
+  float* partial; /* WGRAD workspace [splits, F, C*k*k + 1] */
+  float* dw;      /* [F, C, k, k] */
+  float* db;      /* [F] */
+  int32_t cap, c, h, w, f, k, stride, pad, oh, ow;
+  int32_t model;
+  int32_t relu;
+  int32_t tile_base;
+  int32_t tiles_n;
+  int32_t splits;     /* WGRAD: number of fixed K chunks */
+  int32_t split_len;  /* WGRAD: GEMM-K elements per chunk (multiple of OH*OW not required) */
+} hnn_conv_problem;
+
+int hnn_conv_tile_shape(int op, int32_t* tile_m, int32_t* tile_n);
+
+int hnn_grouped_conv(int op, const hnn_conv_problem* probs, int nprob, int total_tiles, const hnn_step_row* cur,
+                     const hnn_model_status* status, void* stream);
+
+/* dw[f,:] = sum_s partial[s,f,:C*k*k] and db[f] = sum_s partial[s,f,C*k*k] in split order. */
+int hnn_conv_wgrad_reduce(const hnn_conv_problem* probs, int nprob, int total_blocks, const hnn_step_row* cur,
+                          const hnn_model_status* status, void* stream);
+
+typedef struct hnn_pool_problem {
+  const float* x;
+  float* y;
+  uint8_t* idx;       /* argmax within each k*k window, first max wins (numpy argmax) */
+  const float* dy;
+  float* dx;
+  const float* mask;  /* BWD: multiply by (mask > 0) (fused relu backward), may be NULL */
+  int32_t cap, c, h, w, k, stride, oh, ow;
+  int32_t model;
+  int32_t block_base;
+  int32_t blocks;
+  int32_t reserved;
+} hnn_pool_problem;
+
+int hnn_grouped_maxpool(int op, const hnn_pool_problem* probs, int nprob, int total_blocks,
+                        const hnn_step_row* cur, const hnn_model_status* status, void* stream);
+
+typedef struct hnn_relu_problem {
+  const float* x; /* relu input */
+  float* y;
+  const float* dy;
+  float* dx;
+  int32_t cap, row; /* row = floats per sample */
+  int32_t model;
+  int32_t block_base;
+  int32_t blocks;
+  int32_t reserved;
+} hnn_relu_problem;
+
+int hnn_grouped_relu(int op, const hnn_relu_problem* probs, int nprob, int total_blocks, const hnn_step_row* cur,
+                     const hnn_model_status* status, void* stream);
+
+typedef struct hnn_sce_problem {
+  const float* logits; /* [cap, ld] */
+  const int32_t* labels;
+  float* dlogits;      /* [cap, ld]; NULL for evaluation */
+  int32_t ld;
+  int32_t classes;
+  int32_t cap;
+  int32_t model;
+} hnn_sce_problem;
+
+/*
+ * One block per problem (max_cap / max_classes size its shared memory).  train != 0: non-finite loss -> status.alive = 0 and abort_epoch/batch
+ * recorded, nothing accumulated; otherwise loss_sum += F64(loss)*R, correct_sum, seen updated.
+ * train == 0 (evaluation): always accumulates (train.py:274-276), never aborts.
+ * loss_out[model] / correct_out[model] receive the step's loss and hit count when not NULL.
+ */
+int hnn_sce_fused(const hnn_sce_problem* probs, int nprob, int max_cap, int max_classes, const hnn_step_row* cur,
+                  hnn_model_status* status, int train, float* loss_out, int32_t* correct_out, void* stream);
+
+typedef struct hnn_opt_segment {
+  float* param;
+  const float* grad;
+  float* m;           /* Adam first moment / SGD velocity */
+  float* v;           /* Adam second moment */
+  int64_t count;      /* floats in the segment (param/grad/m/v are 16-byte aligned) */
+  int32_t model;
+  int32_t kind;       /* HNN_OPT_* */
+  float momentum;
+  int32_t chunk_base; /* first 4096-float chunk of this segment in the launch */
+  int32_t chunks;
+  int32_t reserved;
+} hnn_opt_segment;
+
+int hnn_multi_tensor_sgd(const hnn_opt_segment* segs, int nseg, int total_chunks, const hnn_step_row* cur,
+                         const hnn_model_status* status, void* stream);
+int hnn_multi_tensor_adam(const hnn_opt_segment* segs, int nseg, int total_chunks, const hnn_step_row* cur,
+                          const hnn_model_status* status, void* stream);
+
+/* Sizes of the ABI structs, so bindings can assert their layouts. */
+int hnn_struct_size(const char* name);
+
+const char* hnn_last_error(void);
+const char* hnn_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* HNN_B200_H */

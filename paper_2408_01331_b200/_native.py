@@ -1,0 +1,144 @@
+"""ctypes binding of the C-ABI library (include/hnn_b200.h).
+
+The library is the product: if it is missing, cannot be loaded, or no CUDA
+device is present, every device entry point raises — there is no CPU
+fallback anywhere in this package.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from pathlib import Path
+
+from .errors import DeviceError
+
+LIB_PATH = Path(__file__).resolve().parent / "_lib" / "libhnn_b200.so"
+
+HNN_FWD, HNN_DGRAD, HNN_WGRAD = 0, 1, 2
+PREC_SIMT, PREC_3XTF32 = 0, 1
+OPT_SGD, OPT_SGD_MOMENTUM, OPT_ADAM = 0, 1, 2
+
+P = C.c_uint64  # device pointers travel as integers
+I = C.c_int32
+
+
+class StepRow(C.Structure):
+    _fields_ = [("active", I), ("rows", I), ("perm_base", I), ("epoch", I), ("batch", I), ("opt_step", I),
+                ("lr", C.c_float), ("bias1", C.c_float), ("bias2", C.c_float), ("reserved", I * 3)]
+
+
+class ModelStatus(C.Structure):
+    _fields_ = [("alive", I), ("abort_epoch", I), ("abort_batch", I), ("last_correct", I),
+                ("last_loss", C.c_float), ("reserved", I), ("loss_sum", C.c_double),
+                ("correct_sum", C.c_int64), ("seen", C.c_int64)]
+
+
+class GatherProblem(C.Structure):
+    _fields_ = [("src_x", P), ("src_y", P), ("perm", P), ("dst_x", P), ("dst_y", P),
+                ("sample", I), ("ld_dst", I), ("cap", I), ("model", I)]
+
+
+class GemmProblem(C.Structure):
+    _fields_ = [("a", P), ("b", P), ("c", P), ("bias", P), ("mask", P), ("dbias", P),
+                ("m", I), ("n", I), ("k", I), ("lda", I), ("ldb", I), ("ldc", I),
+                ("model", I), ("relu", I), ("tile_base", I), ("tiles_n", I)]
+
+
+class ConvProblem(C.Structure):
+    _fields_ = [("x", P), ("weight", P), ("bias", P), ("y", P), ("dy", P), ("dx", P), ("mask", P),
+                ("partial", P), ("dw", P), ("db", P),
+                ("cap", I), ("c", I), ("h", I), ("w", I), ("f", I), ("k", I), ("stride", I), ("pad", I),
+                ("oh", I), ("ow", I), ("model", I), ("relu", I), ("tile_base", I), ("tiles_n", I),
+                ("splits", I), ("split_len", I)]
+
+
+class PoolProblem(C.Structure):
+    _fields_ = [("x", P), ("y", P), ("idx", P), ("dy", P), ("dx", P), ("mask", P),
+                ("cap", I), ("c", I), ("h", I), ("w", I), ("k", I), ("stride", I), ("oh", I), ("ow", I),
+                ("model", I), ("block_base", I), ("blocks", I), ("reserved", I)]
+
+
+class ReluProblem(C.Structure):
+    _fields_ = [("x", P), ("y", P), ("dy", P), ("dx", P), ("cap", I), ("row", I), ("model", I),
+                ("block_base", I), ("blocks", I), ("reserved", I)]
+
+
+class SceProblem(C.Structure):
+    _fields_ = [("logits", P), ("labels", P), ("dlogits", P), ("ld", I), ("classes", I), ("cap", I), ("model", I)]
+
+
+class OptSegment(C.Structure):
+    _fields_ = [("param", P), ("grad", P), ("m", P), ("v", P), ("count", C.c_int64), ("model", I), ("kind", I),
+                ("momentum", C.c_float), ("chunk_base", I), ("chunks", I), ("reserved", I)]
+
+
+STRUCTS = {
+    "hnn_step_row": StepRow, "hnn_model_status": ModelStatus, "hnn_gather_problem": GatherProblem,
+    "hnn_gemm_problem": GemmProblem, "hnn_conv_problem": ConvProblem, "hnn_pool_problem": PoolProblem,
+    "hnn_relu_problem": ReluProblem, "hnn_sce_problem": SceProblem, "hnn_opt_segment": OptSegment,
+}
+
+# every symbol include/hnn_b200.h declares, with its ctypes signature
+VP = C.c_void_p
+SIGNATURES = {
+    "hnn_step_begin": [P, P, P, C.c_int, VP],
+    "hnn_gather_rows": [P, C.c_int, C.c_int, P, VP],
+    "hnn_gemm_tile_shape": [C.c_int, C.c_int, C.POINTER(I), C.POINTER(I)],
+    "hnn_grouped_gemm": [C.c_int, C.c_int, P, C.c_int, C.c_int, P, P, VP],
+    "hnn_conv_tile_shape": [C.c_int, C.POINTER(I), C.POINTER(I)],
+    "hnn_grouped_conv": [C.c_int, P, C.c_int, C.c_int, P, P, VP],
+    "hnn_conv_wgrad_reduce": [P, C.c_int, C.c_int, P, P, VP],
+    "hnn_grouped_maxpool": [C.c_int, P, C.c_int, C.c_int, P, P, VP],
+    "hnn_grouped_relu": [C.c_int, P, C.c_int, C.c_int, P, P, VP],
+    "hnn_sce_fused": [P, C.c_int, C.c_int, C.c_int, P, P, C.c_int, P, P, VP],
+    "hnn_multi_tensor_sgd": [P, C.c_int, C.c_int, P, P, VP],
+    "hnn_multi_tensor_adam": [P, C.c_int, C.c_int, P, P, VP],
+    "hnn_struct_size": [C.c_char_p],
+    "hnn_last_error": [],
+    "hnn_version": [],
+}
+
+_lib = None
+
+
+def load(path: Path = LIB_PATH):
+    """Load (once) and type the library; raises if it is not built."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not path.exists():
+        raise DeviceError("load", -1, f"{path} is missing — run __graft_entry__.build() (no CPU fallback exists)")
+    lib = C.CDLL(str(path))
+    for name, args in SIGNATURES.items():
+        fn = getattr(lib, name)
+        fn.argtypes = args
+        fn.restype = C.c_char_p if name in ("hnn_last_error", "hnn_version") else C.c_int
+    for name, cls in STRUCTS.items():
+        got = lib.hnn_struct_size(name.encode())
+        if got != C.sizeof(cls):
+            raise DeviceError("load", -1, f"ABI mismatch for {name}: library {got} bytes, binding {C.sizeof(cls)}")
+    _lib = lib
+    return lib
+
+
+def call(name: str, *args) -> None:
+    lib = load()
+    status = getattr(lib, name)(*args)
+    if status != 0:
+        raise DeviceError(name, status, lib.hnn_last_error().decode(errors="replace"))
+
+
+def tile_shape(op: int, prec: int) -> tuple:
+    tm, tn = I(), I()
+    call("hnn_gemm_tile_shape", op, prec, C.byref(tm), C.byref(tn))
+    return tm.value, tn.value
+
+
+def conv_tile_shape(op: int) -> tuple:
+    tm, tn = I(), I()
+    call("hnn_conv_tile_shape", op, C.byref(tm), C.byref(tn))
+    return tm.value, tn.value
+
+
+def table_bytes(cls, rows: list) -> bytes:
+    arr = (cls * len(rows))(*rows)
+    return bytes(arr)

@@ -1,0 +1,99 @@
+// C-ABI plumbing: error state, the per-step schedule prologue and the batch gather.
+#include <cstring>
+
+#include "common.cuh"
+
+namespace hnn {
+
+static thread_local std::string g_last_error;
+
+void set_error(const char* where, const char* what) {
+  g_last_error = std::string(where) + ": " + what;
+}
+
+int check_launch(const char* where) {
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) {
+    set_error(where, cudaGetErrorString(e));
+    return HNN_ERR_CUDA;
+  }
+  return HNN_OK;
+}
+
+// sched row block `*counter` -> cur, then advance.  One block; n_models*12 words.
+__global__ void step_begin_kernel(const hnn_step_row* __restrict__ sched, int32_t* counter,
+                                  hnn_step_row* __restrict__ cur, int n_models) {
+  const int step = *counter;
+  const int words = n_models * int(sizeof(hnn_step_row) / 4);
+  const int32_t* src = reinterpret_cast<const int32_t*>(sched + size_t(step) * n_models);
+  int32_t* dst = reinterpret_cast<int32_t*>(cur);
+  for (int i = threadIdx.x; i < words; i += blockDim.x) dst[i] = src[i];
+  __syncthreads();
+  if (threadIdx.x == 0) *counter = step + 1;
+}
+
+// One block per (row, problem): dst row r <- src row perm[perm_base + r]; rows >= R zero-filled.
+__global__ void gather_rows_kernel(const hnn_gather_problem* __restrict__ probs, const hnn_step_row* __restrict__ cur) {
+  const hnn_gather_problem p = probs[blockIdx.y];
+  const int r = blockIdx.x;
+  if (r >= p.cap || !cur[p.model].active) return;
+  const hnn_step_row s = cur[p.model];
+  float* dst = p.dst_x + size_t(r) * p.ld_dst;
+  if (r >= s.rows) {
+    for (int i = threadIdx.x; i < p.ld_dst; i += blockDim.x) dst[i] = 0.0f;
+    if (threadIdx.x == 0) p.dst_y[r] = 0;
+    return;
+  }
+  const int src_row = p.perm[s.perm_base + r];
+  const float* src = p.src_x + size_t(src_row) * p.sample;
+  const bool vec = ((p.sample & 3) == 0) && ((p.ld_dst & 3) == 0) &&
+                   ((reinterpret_cast<uintptr_t>(p.src_x) & 15) == 0) && ((reinterpret_cast<uintptr_t>(p.dst_x) & 15) == 0);
+  if (vec) {
+    const float4* s4 = reinterpret_cast<const float4*>(src);
+    float4* d4 = reinterpret_cast<float4*>(dst);
+    for (int i = threadIdx.x; i < p.sample / 4; i += blockDim.x) d4[i] = __ldg(s4 + i);
+  } else {
+    for (int i = threadIdx.x; i < p.sample; i += blockDim.x) dst[i] = __ldg(src + i);
+  }
+  for (int i = p.sample + threadIdx.x; i < p.ld_dst; i += blockDim.x) dst[i] = 0.0f;
+  if (threadIdx.x == 0) p.dst_y[r] = p.src_y[src_row];
+}
+
+}  // namespace hnn
+
+extern "C" {
+
+const char* hnn_last_error(void) { return hnn::g_last_error.c_str(); }
+
+const char* hnn_version(void) { return "hnn_b200 1.0 sm_100a"; }
+
+int hnn_struct_size(const char* name) {
+  if (!name) return -1;
+  if (!strcmp(name, "hnn_step_row")) return sizeof(hnn_step_row);
+  if (!strcmp(name, "hnn_model_status")) return sizeof(hnn_model_status);
+  if (!strcmp(name, "hnn_gather_problem")) return sizeof(hnn_gather_problem);
+  if (!strcmp(name, "hnn_gemm_problem")) return sizeof(hnn_gemm_problem);
+  if (!strcmp(name, "hnn_conv_problem")) return sizeof(hnn_conv_problem);
+  if (!strcmp(name, "hnn_pool_problem")) return sizeof(hnn_pool_problem);
+  if (!strcmp(name, "hnn_relu_problem")) return sizeof(hnn_relu_problem);
+  if (!strcmp(name, "hnn_sce_problem")) return sizeof(hnn_sce_problem);
+  if (!strcmp(name, "hnn_opt_segment")) return sizeof(hnn_opt_segment);
+  return -1;
+}
+
+int hnn_step_begin(const hnn_step_row* sched, int32_t* counter, hnn_step_row* cur, int n_models, void* stream) {
+  HNN_REQUIRE(sched && counter && cur && n_models > 0, "hnn_step_begin", "null pointer or empty model set");
+  hnn::step_begin_kernel<<<1, 256, 0, hnn::as_stream(stream)>>>(sched, counter, cur, n_models);
+  return hnn::check_launch("hnn_step_begin");
+}
+
+int hnn_gather_rows(const hnn_gather_problem* probs, int nprob, int max_cap, const hnn_step_row* cur,
+                    void* stream) {
+  HNN_REQUIRE(probs && cur && nprob > 0 && max_cap > 0, "hnn_gather_rows", "bad arguments");
+  HNN_REQUIRE(nprob <= 65535, "hnn_gather_rows", "too many problems");
+  dim3 grid(max_cap, nprob);
+  hnn::gather_rows_kernel<<<grid, 128, 0, hnn::as_stream(stream)>>>(probs, cur);
+  return hnn::check_launch("hnn_gather_rows");
+}
+
+}  // extern "C"

@@ -1,0 +1,116 @@
+// Grouped max-pool (fwd/bwd, relu mask fused into bwd) and stand-alone relu
+// (pkg/src/hybridnn/ops.py:62-67, 149-174).  HBM-bound elementwise kernels:
+// one thread per output (fwd) or per input element (bwd, gather form, so the
+// reference's np.add.at scatter becomes a fixed-order sum with no atomics).
+#include "common.cuh"
+
+namespace hnn {
+
+constexpr int PTHREADS = 256;
+
+__global__ void __launch_bounds__(PTHREADS) maxpool_fwd_kernel(const hnn_pool_problem* __restrict__ probs, int nprob,
+                                                               const hnn_step_row* __restrict__ cur,
+                                                               const hnn_model_status* __restrict__ status) {
+  const int pi = find_problem(probs, nprob, blockIdx.x, [](const hnn_pool_problem& q) { return q.block_base; });
+  const hnn_pool_problem p = probs[pi];
+  if (!live(cur, status, p.model)) return;
+  const long long e = (long long)(blockIdx.x - p.block_base) * PTHREADS + threadIdx.x;
+  const long long total = (long long)p.cap * p.c * p.oh * p.ow;
+  if (e >= total) return;
+  const int ox = int(e % p.ow);
+  const int oy = int((e / p.ow) % p.oh);
+  const long long plane = e / ((long long)p.oh * p.ow);  // b*C + c
+  const int b = int(plane / p.c);
+  if (b >= cur[p.model].rows) {
+    p.y[e] = 0.0f;
+    p.idx[e] = 0;
+    return;
+  }
+  const float* src = p.x + plane * p.h * p.w;
+  // numpy argmax over the window flattened (i, j): first max wins, first NaN wins outright
+  float best = src[(oy * p.stride) * p.w + ox * p.stride];
+  int best_i = 0;
+  if (best == best) {
+    for (int q = 1; q < p.k * p.k; ++q) {
+      const int i = q / p.k, j = q - i * p.k;
+      const float v = src[(oy * p.stride + i) * p.w + ox * p.stride + j];
+      if (!(v <= best)) {
+        best = v;
+        best_i = q;
+        if (v != v) break;
+      }
+    }
+  }
+  p.y[e] = best;
+  p.idx[e] = (uint8_t)best_i;
+}
+
+__global__ void __launch_bounds__(PTHREADS) maxpool_bwd_kernel(const hnn_pool_problem* __restrict__ probs, int nprob,
+                                                               const hnn_step_row* __restrict__ cur,
+                                                               const hnn_model_status* __restrict__ status) {
+  const int pi = find_problem(probs, nprob, blockIdx.x, [](const hnn_pool_problem& q) { return q.block_base; });
+  const hnn_pool_problem p = probs[pi];
+  if (!live(cur, status, p.model)) return;
+  const long long e = (long long)(blockIdx.x - p.block_base) * PTHREADS + threadIdx.x;
+  const long long total = (long long)p.cap * p.c * p.h * p.w;
+  if (e >= total) return;
+  const int x = int(e % p.w);
+  const int y = int((e / p.w) % p.h);
+  const long long plane = e / ((long long)p.h * p.w);
+  const int b = int(plane / p.c);
+  float acc = 0.0f;
+  if (b < cur[p.model].rows) {
+    // windows (oy, ox) covering (y, x), visited in ascending (oy, ox) like np.add.at's index order
+    const int oy_lo = max(0, (y - p.k + p.stride) / p.stride), oy_hi = min(p.oh - 1, y / p.stride);
+    const int ox_lo = max(0, (x - p.k + p.stride) / p.stride), ox_hi = min(p.ow - 1, x / p.stride);
+    const size_t obase = size_t(plane) * p.oh * p.ow;
+    for (int oy = oy_lo; oy <= oy_hi; ++oy) {
+      const int i = y - oy * p.stride;
+      if (i < 0 || i >= p.k) continue;
+      for (int ox = ox_lo; ox <= ox_hi; ++ox) {
+        const int j = x - ox * p.stride;
+        if (j < 0 || j >= p.k) continue;
+        const size_t o = obase + size_t(oy) * p.ow + ox;
+        if (p.idx[o] == i * p.k + j) acc = __fadd_rn(acc, p.dy[o]);
+      }
+    }
+    if (p.mask) acc = np_mask(acc, p.mask[e]);
+  }
+  p.dx[e] = acc;
+}
+
+__global__ void __launch_bounds__(PTHREADS) relu_kernel(int op, const hnn_relu_problem* __restrict__ probs, int nprob,
+                                                        const hnn_step_row* __restrict__ cur,
+                                                        const hnn_model_status* __restrict__ status) {
+  const int pi = find_problem(probs, nprob, blockIdx.x, [](const hnn_relu_problem& q) { return q.block_base; });
+  const hnn_relu_problem p = probs[pi];
+  if (!live(cur, status, p.model)) return;
+  const long long e = (long long)(blockIdx.x - p.block_base) * PTHREADS + threadIdx.x;
+  if (e >= (long long)p.cap * p.row) return;
+  const bool real = (e / p.row) < cur[p.model].rows;
+  if (op == HNN_FWD) p.y[e] = real ? np_relu(p.x[e]) : 0.0f;
+  else p.dx[e] = real ? np_mask(p.dy[e], p.x[e]) : 0.0f;
+}
+
+}  // namespace hnn
+
+extern "C" int hnn_grouped_maxpool(int op, const hnn_pool_problem* probs, int nprob, int total_blocks,
+                                   const hnn_step_row* cur, const hnn_model_status* status, void* stream) {
+  HNN_REQUIRE(probs && cur && nprob > 0 && total_blocks > 0, "hnn_grouped_maxpool", "bad arguments");
+  cudaStream_t s = hnn::as_stream(stream);
+  if (op == HNN_FWD) hnn::maxpool_fwd_kernel<<<total_blocks, hnn::PTHREADS, 0, s>>>(probs, nprob, cur, status);
+  else if (op == HNN_DGRAD) hnn::maxpool_bwd_kernel<<<total_blocks, hnn::PTHREADS, 0, s>>>(probs, nprob, cur, status);
+  else {
+    hnn::set_error("hnn_grouped_maxpool", "op must be HNN_FWD or HNN_DGRAD");
+    return HNN_ERR_INVALID;
+  }
+  return hnn::check_launch("hnn_grouped_maxpool");
+}
+
+extern "C" int hnn_grouped_relu(int op, const hnn_relu_problem* probs, int nprob, int total_blocks,
+                                const hnn_step_row* cur, const hnn_model_status* status, void* stream) {
+  HNN_REQUIRE(probs && cur && nprob > 0 && total_blocks > 0, "hnn_grouped_relu", "bad arguments");
+  HNN_REQUIRE(op == HNN_FWD || op == HNN_DGRAD, "hnn_grouped_relu", "op must be HNN_FWD or HNN_DGRAD");
+  hnn::relu_kernel<<<total_blocks, hnn::PTHREADS, 0, hnn::as_stream(stream)>>>(op, probs, nprob, cur, status);
+  return hnn::check_launch("hnn_grouped_relu");
+}

@@ -1,0 +1,640 @@
+"""Device runtime for a merged hybrid: packing, launch plans, lockstep steps.
+
+A :class:`DeviceHybrid` owns, for the models of one rank:
+
+* packed HBM arenas — params / grads / moment-1 / moment-2, one contiguous
+  16-byte-aligned segment per model, tensors inside in the reference's
+  param_specs order (src/engine.py:42-52);
+* per-model activation buffers ([batch, features], NCHW for images) and two
+  ping-pong gradient buffers;
+* compiled launch plans: every model's op chain is lowered to *stages*
+  (dense / conv with relu fused into the producer, max-pool, stand-alone
+  relu; flatten is a view) and stage ``w`` of every model runs in the same
+  grouped launch per kind ("wave");
+* the per-step schedule (``hnn_step_row`` per model) in device memory, read
+  by every kernel through the ``cur`` row block that ``hnn_step_begin``
+  refreshes, so a whole step is a fixed launch sequence that can be replayed
+  as a CUDA graph.
+
+Everything here calls the C-ABI (``_native``); nothing computes on the CPU.
+"""
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _native as N
+from .errors import HybridnnError, ShapeMismatchError
+from .ops import OP_KINDS, conv_extent
+
+STEP_DTYPE = np.dtype([("active", "<i4"), ("rows", "<i4"), ("perm_base", "<i4"), ("epoch", "<i4"),
+                       ("batch", "<i4"), ("opt_step", "<i4"), ("lr", "<f4"), ("bias1", "<f4"),
+                       ("bias2", "<f4"), ("reserved", "<i4", (3,))])
+STATUS_DTYPE = np.dtype([("alive", "<i4"), ("abort_epoch", "<i4"), ("abort_batch", "<i4"),
+                         ("last_correct", "<i4"), ("last_loss", "<f4"), ("reserved", "<i4"),
+                         ("loss_sum", "<f8"), ("correct_sum", "<i8"), ("seen", "<i8")])
+assert STEP_DTYPE.itemsize == 48 and STATUS_DTYPE.itemsize == 48
+
+OPT_CHUNK = 4096
+CONV_SPLIT_LEN = 2048
+TC_MIN_DIM = 64  # smallest M/N/K worth a tcgen05 tile; smaller problems stay on CUDA cores
+
+
+class UnsupportedGraphError(HybridnnError):
+    """The graph uses something the device path does not implement."""
+
+
+def _torch():
+    import torch
+
+    return torch
+
+
+def _align4(n: int) -> int:
+    return (n + 3) // 4 * 4
+
+
+# --------------------------------------------------------------------------- stages
+
+
+@dataclass
+class Stage:
+    kind: str                  # dense | conv | pool | relu
+    node_id: str
+    attrs: dict
+    in_shape: tuple
+    out_shape: tuple
+    relu: bool = False         # relu fused into this producer's epilogue
+    mask_input: bool = False   # grad wrt input is multiplied by (input > 0) (producer had a fused relu)
+    needs_dx: bool = False     # some parameter lives upstream
+    params: tuple = ()         # pids (weight, bias) in the model namespace
+    # filled when buffers are bound
+    ld_in: int = 0
+    ld_out: int = 0
+    x = None
+    y = None
+    dy = None
+    dx = None
+    idx = None
+    partial = None
+    splits: int = 0
+
+
+def lower_graph(graph) -> tuple:
+    """Chain of nodes -> (stages, logits_features, loss_head).  Raises for unsupported graphs."""
+    from .engine import chain, infer_shapes
+
+    nodes = chain(graph)
+    shapes = infer_shapes(graph)
+    loss_head = OP_KINDS[nodes[-1].op].loss_head
+    body = nodes[:-1] if loss_head else nodes
+    stages: list = []
+    i = 0
+    while i < len(body):
+        n = body[i]
+        ins = shapes[n.inputs[0]]
+        outs = shapes[n.node_id]
+        if n.op in ("dense", "conv2d"):
+            st = Stage("dense" if n.op == "dense" else "conv", n.node_id, dict(n.attrs), ins, outs,
+                       params=(f"{n.node_id}.weight", f"{n.node_id}.bias"))
+            # fuse a following relu when its consumer's backward can apply the mask
+            if i + 1 < len(body) and body[i + 1].op == "relu":
+                j = i + 2
+                while j < len(body) and body[j].op == "flatten":
+                    j += 1
+                if j < len(body) and body[j].op in ("dense", "conv2d", "maxpool2d"):
+                    st.relu = True
+                    i += 1
+            stages.append(st)
+        elif n.op == "maxpool2d":
+            if n.attrs["kernel"] ** 2 > 256:
+                raise UnsupportedGraphError(f"node {n.node_id!r}: pool windows above 16x16 are not supported")
+            stages.append(Stage("pool", n.node_id, dict(n.attrs), ins, outs))
+        elif n.op == "relu":
+            stages.append(Stage("relu", n.node_id, {}, ins, outs))
+        elif n.op == "flatten":
+            if stages:
+                stages[-1].out_shape = outs  # a view: same memory, flat per-sample shape
+        elif n.op == "embedding-lookup":
+            raise UnsupportedGraphError(f"node {n.node_id!r}: embedding-lookup has no device kernel yet")
+        else:
+            raise UnsupportedGraphError(f"node {n.node_id!r}: op {n.op!r} cannot appear here")
+        i += 1
+    if not stages:
+        raise UnsupportedGraphError("graph has no parameterised or elementwise stage")
+    final = shapes[body[-1].node_id]
+    if len(final) != 1:
+        raise ShapeMismatchError(body[-1].node_id, f"softmax-cross-entropy needs flat logits, got {final}")
+    seen_param = False
+    for k, st in enumerate(stages):
+        st.needs_dx = seen_param
+        if st.kind in ("dense", "conv"):
+            seen_param = True
+        if k > 0 and stages[k - 1].relu:
+            st.mask_input = True
+    return stages, final[0], loss_head
+
+
+# --------------------------------------------------------------------------- models / datasets
+
+
+@dataclass
+class ModelSlot:
+    """One model on this rank: graph, hyper-parameters and arena placement."""
+
+    index: int
+    job_id: str
+    graph: object
+    batch_size: int
+    optimizer: str
+    momentum: float
+    specs: dict                  # pid -> shape (param_specs order)
+    stages: list = field(default_factory=list)
+    classes: int = 0
+    offsets: dict = field(default_factory=dict)  # pid -> float offset in the arena
+    seg_off: int = 0
+    seg_len: int = 0
+    sample_shape: tuple = ()
+    batch_x = None
+    batch_y = None
+    grads_buf: list = field(default_factory=list)
+
+    @property
+    def opt_kind(self) -> int:
+        if self.optimizer == "adam":
+            return N.OPT_ADAM
+        return N.OPT_SGD_MOMENTUM if self.momentum else N.OPT_SGD
+
+
+class DeviceDataset:
+    """A dataset resident in HBM once: samples as f32, labels as int32 class ids."""
+
+    def __init__(self, ds, device, classes: int | None = None, src=None):
+        torch = _torch()
+        from .ops import check_class_indices
+
+        self.content_hash = ds.content_hash
+        self.sample_shape = tuple(ds.train_x.shape[1:])
+        self.n_train, self.n_test = int(ds.train_x.shape[0]), int(ds.test_x.shape[0])
+        k = classes if classes is not None else 1 << 30
+        ytr = check_class_indices(ds.train_y, k).astype(np.int32)
+        yte = check_class_indices(ds.test_y, k).astype(np.int32) if self.n_test else np.zeros(0, np.int32)
+        if src is not None:  # tensors already on the device (e.g. received by broadcast)
+            self.train_x, self.train_y, self.test_x, self.test_y = src
+        else:
+            self.train_x = torch.from_numpy(np.ascontiguousarray(ds.train_x, dtype=np.float32)).to(device)
+            self.test_x = torch.from_numpy(np.ascontiguousarray(ds.test_x, dtype=np.float32)).to(device)
+            self.train_y = torch.from_numpy(ytr).to(device)
+            self.test_y = torch.from_numpy(yte).to(device)
+        self.identity = torch.arange(max(self.n_test, 1), dtype=torch.int32, device=device)
+        self.max_label = int(max(ytr.max(initial=0), yte.max(initial=0)))
+        self.nbytes = int(sum(t.numel() * t.element_size() for t in (self.train_x, self.train_y, self.test_x,
+                                                                          self.test_y)))
+
+
+# --------------------------------------------------------------------------- launches
+
+
+class Launch:
+    """One C-ABI call with its device-resident problem table."""
+
+    def __init__(self, entry: str, args: tuple, table=None, label: str = ""):
+        self.entry, self.args, self.table, self.label = entry, args, table, label
+
+    def run(self, stream) -> None:
+        N.call(self.entry, *self.args, stream)
+
+
+def _dev_table(cls, rows, device):
+    torch = _torch()
+    raw = N.table_bytes(cls, rows)
+    t = torch.frombuffer(bytearray(raw), dtype=torch.uint8).to(device)
+    return t
+
+
+def _ptr(t) -> int:
+    return 0 if t is None else int(t.data_ptr())
+
+
+class DeviceHybrid:
+    """Packed device state + launch plans for the models of one rank."""
+
+    def __init__(self, slots: list, device=None, use_tensor_cores: bool = True):
+        torch = _torch()
+        N.load()
+        if not torch.cuda.is_available():
+            raise HybridnnError("no CUDA device: the hybrid trainer has no CPU fallback")
+        self.device = torch.device(device or "cuda")
+        self.slots = slots
+        self.n = len(slots)
+        self.use_tc = use_tensor_cores
+        off = 0
+        for s in slots:
+            s.stages, s.classes, _ = lower_graph(s.graph)
+            s.sample_shape = tuple(s.graph.input_shape)
+            s.seg_off = off
+            for pid, shp in s.specs.items():
+                s.offsets[pid] = off
+                off += _align4(int(np.prod(shp)))
+            s.seg_len = off - s.seg_off
+        self.arena_len = max(off, 4)
+        f32 = dict(dtype=torch.float32, device=self.device)
+        self.params = torch.zeros(self.arena_len, **f32)
+        self.grads = torch.zeros(self.arena_len, **f32)
+        need_m = any(s.opt_kind != N.OPT_SGD for s in slots)
+        need_v = any(s.opt_kind == N.OPT_ADAM for s in slots)
+        self.m1 = torch.zeros(self.arena_len, **f32) if need_m else None
+        self.m2 = torch.zeros(self.arena_len, **f32) if need_v else None
+        self.cur = torch.zeros(self.n * 48, dtype=torch.uint8, device=self.device)
+        self.counter = torch.zeros(1, dtype=torch.int32, device=self.device)
+        self.status = torch.zeros(self.n * 48, dtype=torch.uint8, device=self.device)
+        self.eval_status = torch.zeros(self.n * 48, dtype=torch.uint8, device=self.device)
+        self.loss_out = torch.zeros(self.n, **f32)
+        self.correct_out = torch.zeros(self.n, dtype=torch.int32, device=self.device)
+        self.sched = None
+        self.reset_status()
+        self._bind_buffers()
+        self.train_plan: list = []
+        self.eval_plan: list = []
+        self.forward_plan: list = []
+        self.graph = None
+        self.datasets = {}
+
+    # ------------------------------------------------------------------ buffers
+    def _bind_buffers(self):
+        torch = _torch()
+        dev = self.device
+        for s in self.slots:
+            cap = s.batch_size
+            first = s.stages[0]
+            sample = int(np.prod(s.sample_shape))
+            ld0 = _align4(sample) if first.kind == "dense" else sample
+            s.batch_x = torch.zeros(cap, ld0, dtype=torch.float32, device=dev)
+            s.batch_y = torch.zeros(cap, dtype=torch.int32, device=dev)
+            prev_out, prev_ld = s.batch_x, ld0
+            widest = ld0
+            for st in s.stages:
+                st.x, st.ld_in = prev_out, prev_ld
+                feats = int(np.prod(st.out_shape))
+                if st.kind == "dense":
+                    st.ld_out = _align4(feats)
+                elif st.kind == "relu":
+                    st.ld_out = st.ld_in
+                else:
+                    st.ld_out = feats
+                st.y = torch.zeros(cap, st.ld_out, dtype=torch.float32, device=dev)
+                if st.kind == "pool":
+                    st.idx = torch.zeros(cap * feats, dtype=torch.uint8, device=dev)
+                if st.kind == "conv":
+                    c, h, w = st.in_shape
+                    f, oh, ow = self._conv_out(st)
+                    k = st.attrs["kernel"]
+                    st.splits = -(-cap * oh * ow // CONV_SPLIT_LEN)
+                    st.partial = torch.zeros(st.splits * f * (c * k * k + 1), dtype=torch.float32, device=dev)
+                widest = max(widest, st.ld_out, st.ld_in)
+                prev_out, prev_ld = st.y, st.ld_out
+            s.grads_buf = [torch.zeros(cap * widest, dtype=torch.float32, device=dev) for _ in range(2)]
+            for k, st in enumerate(s.stages):
+                st.dy = s.grads_buf[k % 2][: cap * st.ld_out].view(cap, st.ld_out)
+                st.dx = s.grads_buf[(k + 1) % 2][: cap * st.ld_in].view(cap, st.ld_in)
+
+    @staticmethod
+    def _conv_out(st):
+        c, h, w = st.in_shape
+        k, s_, p = st.attrs["kernel"], st.attrs.get("stride", 1), st.attrs.get("padding", 0)
+        return st.attrs["filters"], conv_extent(h, k, s_, p), conv_extent(w, k, s_, p)
+
+    def reset_status(self, which=None):
+        st = np.zeros(self.n, dtype=STATUS_DTYPE)
+        st["alive"] = 1
+        st["abort_epoch"] = -1
+        st["abort_batch"] = -1
+        torch = _torch()
+        target = self.status if which is None else which
+        target.copy_(torch.from_numpy(st.view(np.uint8)).to(self.device))
+
+    def read_status(self, which=None) -> np.ndarray:
+        src = self.status if which is None else which
+        return src.cpu().numpy().view(STATUS_DTYPE).copy()
+
+    def reset_accumulators(self, models: list):
+        """Zero loss_sum / correct_sum / seen of the given models (alive flags untouched)."""
+        if not models:
+            return
+        st = self.read_status()
+        for m in models:
+            st["loss_sum"][m] = 0.0
+            st["correct_sum"][m] = 0
+            st["seen"][m] = 0
+        self.status.copy_(_torch().from_numpy(st.view(np.uint8)).to(self.device))
+
+    # ------------------------------------------------------------------ params
+    def upload_params(self, m: int, params: dict):
+        s = self.slots[m]
+        host = np.zeros(s.seg_len, dtype=np.float32)
+        for pid, shp in s.specs.items():
+            a = np.ascontiguousarray(params[pid], dtype=np.float32)
+            if a.shape != tuple(shp):
+                raise ShapeMismatchError(pid, f"shape {a.shape} != {tuple(shp)}")
+            o = s.offsets[pid] - s.seg_off
+            host[o:o + a.size] = a.reshape(-1)
+        self.params[s.seg_off:s.seg_off + s.seg_len].copy_(_torch().from_numpy(host))
+
+    def _download(self, arena, m: int) -> dict:
+        s = self.slots[m]
+        host = arena[s.seg_off:s.seg_off + s.seg_len].cpu().numpy()
+        out = {}
+        for pid, shp in s.specs.items():
+            o = s.offsets[pid] - s.seg_off
+            out[pid] = host[o:o + int(np.prod(shp))].reshape(shp).copy()
+        return out
+
+    def download_params(self, m: int) -> dict:
+        return self._download(self.params, m)
+
+    def download_grads(self, m: int) -> dict:
+        return self._download(self.grads, m)
+
+    def download_moments(self, m: int) -> tuple:
+        s = self.slots[m]
+        m1 = self._download(self.m1, m) if s.opt_kind != N.OPT_SGD else {}
+        m2 = self._download(self.m2, m) if s.opt_kind == N.OPT_ADAM else {}
+        return m1, m2
+
+    def upload_moments(self, m: int, m1: dict, m2: dict):
+        s = self.slots[m]
+        for arena, src in ((self.m1, m1), (self.m2, m2)):
+            if arena is None or not src:
+                continue
+            host = np.zeros(s.seg_len, dtype=np.float32)
+            for pid, a in src.items():
+                o = s.offsets[pid] - s.seg_off
+                host[o:o + a.size] = np.asarray(a, dtype=np.float32).reshape(-1)
+            arena[s.seg_off:s.seg_off + s.seg_len].copy_(_torch().from_numpy(host))
+
+    def pview(self, arena, m: int, pid: str):
+        s = self.slots[m]
+        o = s.offsets[pid]
+        return arena[o:o + int(np.prod(s.specs[pid]))]
+
+    # ------------------------------------------------------------------ datasets
+    def bind_datasets(self, by_model: list, perm_capacity: int):
+        """by_model[m] = DeviceDataset of model m.  Builds the gather tables."""
+        torch = _torch()
+        self.model_data = by_model
+        self.perm = torch.zeros(self.n, max(perm_capacity, 1), dtype=torch.int32, device=self.device)
+        for s, d in zip(self.slots, by_model):
+            if tuple(d.sample_shape) != tuple(s.sample_shape):
+                raise ShapeMismatchError("input", f"job {s.job_id!r}: dataset samples {d.sample_shape} "
+                                                  f"!= graph input {s.sample_shape}")
+            if d.max_label >= s.classes:
+                raise ValueError(f"target class out of range [0, {s.classes})")
+        self._gather_train = self._gather_launch(train=True)
+        self._gather_eval = self._gather_launch(train=False)
+
+    def _gather_launch(self, train: bool):
+        rows = []
+        for s, d in zip(self.slots, self.model_data):
+            rows.append(N.GatherProblem(
+                _ptr(d.train_x if train else d.test_x), _ptr(d.train_y if train else d.test_y),
+                _ptr(self.perm[s.index]) if train else _ptr(d.identity),
+                _ptr(s.batch_x), _ptr(s.batch_y), int(np.prod(s.sample_shape)), s.batch_x.shape[1],
+                s.batch_size, s.index))
+        t = _dev_table(N.GatherProblem, rows, self.device)
+        cap = max(s.batch_size for s in self.slots)
+        return Launch("hnn_gather_rows", (_ptr(t), len(rows), cap, _ptr(self.cur)), t, "gather")
+
+    # ------------------------------------------------------------------ plans
+    def _stage_waves(self):
+        depth = max(len(s.stages) for s in self.slots)
+        return [[(s, s.stages[w]) for s in self.slots if w < len(s.stages)] for w in range(depth)]
+
+    def _route_tc(self, op, d) -> bool:
+        """Whether a dense problem goes to the tcgen05 3xTF32 kernel (set by gemm_tc support)."""
+        return False
+
+    def _gemm_launch(self, op, items, label):
+        """items: list of (slot, stage).  Splits into SIMT / 3xTF32 launches."""
+        groups = {N.PREC_SIMT: [], N.PREC_3XTF32: []}
+        for s, st in items:
+            cap = s.batch_size
+            K, U = int(np.prod(st.in_shape)), st.out_shape[0]
+            w = self.pview(self.params, s.index, st.params[0])
+            b = self.pview(self.params, s.index, st.params[1])
+            if op == N.HNN_FWD:
+                d = dict(a=_ptr(st.x), b=_ptr(w), c=_ptr(st.y), bias=_ptr(b), mask=0, dbias=0, m=cap, n=U, k=K,
+                         lda=st.ld_in, ldb=K, ldc=st.ld_out, relu=int(st.relu))
+            elif op == N.HNN_DGRAD:
+                d = dict(a=_ptr(st.dy), b=_ptr(w), c=_ptr(st.dx), bias=0, mask=_ptr(st.x) if st.mask_input else 0,
+                         dbias=0, m=cap, n=K, k=U, lda=st.ld_out, ldb=K, ldc=st.ld_in, relu=0)
+            else:
+                gw = self.pview(self.grads, s.index, st.params[0])
+                gb = self.pview(self.grads, s.index, st.params[1])
+                d = dict(a=_ptr(st.dy), b=_ptr(st.x), c=_ptr(gw), bias=0, mask=0, dbias=_ptr(gb), m=U, n=K, k=cap,
+                         lda=st.ld_out, ldb=st.ld_in, ldc=K, relu=0)
+            prec = N.PREC_3XTF32 if (self.use_tc and self._route_tc(op, d)) else N.PREC_SIMT
+            groups[prec].append((s, d))
+        out = []
+        for prec, rows in groups.items():
+            if not rows:
+                continue
+            tm, tn = N.tile_shape(op, prec)
+            probs, base = [], 0
+            for s, d in rows:
+                tiles_m, tiles_n = -(-d["m"] // tm), -(-d["n"] // tn)
+                probs.append(N.GemmProblem(tile_base=base, tiles_n=tiles_n, model=s.index, **d))
+                base += tiles_m * tiles_n
+            t = _dev_table(N.GemmProblem, probs, self.device)
+            out.append(Launch("hnn_grouped_gemm", (op, prec, _ptr(t), len(probs), base, _ptr(self.cur),
+                                                   _ptr(self.status)), t, f"{label}/{'tc' if prec else 'simt'}"))
+        return out
+
+    def _conv_launch(self, op, items, label):
+        tm, tn = N.conv_tile_shape(op)
+        probs, base, red, rbase = [], 0, [], 0
+        for s, st in items:
+            c, h, w = st.in_shape
+            f, oh, ow = self._conv_out(st)
+            k = st.attrs["kernel"]
+            W = self.pview(self.params, s.index, st.params[0])
+            B = self.pview(self.params, s.index, st.params[1])
+            common = dict(x=_ptr(st.x), weight=_ptr(W), bias=_ptr(B), y=_ptr(st.y), dy=_ptr(st.dy),
+                          dx=_ptr(st.dx), mask=_ptr(st.x) if (op == N.HNN_DGRAD and st.mask_input) else 0,
+                          partial=_ptr(st.partial), dw=_ptr(self.pview(self.grads, s.index, st.params[0])),
+                          db=_ptr(self.pview(self.grads, s.index, st.params[1])), cap=s.batch_size, c=c, h=h, w=w,
+                          f=f, k=k, stride=st.attrs.get("stride", 1), pad=st.attrs.get("padding", 0), oh=oh, ow=ow,
+                          model=s.index, relu=int(st.relu), splits=st.splits, split_len=CONV_SPLIT_LEN)
+            if op == N.HNN_FWD:
+                M, Nn = s.batch_size * oh * ow, f
+                tiles = -(-M // tm) * -(-Nn // tn)
+                tiles_n = -(-Nn // tn)
+            elif op == N.HNN_DGRAD:
+                M, Nn = s.batch_size * h * w, c
+                tiles = -(-M // tm) * -(-Nn // tn)
+                tiles_n = -(-Nn // tn)
+            else:
+                tiles_n = -(-(c * k * k + 1) // tn)
+                tiles = st.splits * -(-f // tm) * tiles_n
+                nblk = -(-(f * (c * k * k + 1)) // 256)
+                red.append(N.ConvProblem(tile_base=rbase, tiles_n=tiles_n, **common))
+                rbase += nblk
+            probs.append(N.ConvProblem(tile_base=base, tiles_n=tiles_n, **common))
+            base += tiles
+        t = _dev_table(N.ConvProblem, probs, self.device)
+        out = [Launch("hnn_grouped_conv", (op, _ptr(t), len(probs), base, _ptr(self.cur), _ptr(self.status)), t,
+                      label)]
+        if op == N.HNN_WGRAD:
+            rt = _dev_table(N.ConvProblem, red, self.device)
+            out.append(Launch("hnn_conv_wgrad_reduce", (_ptr(rt), len(red), rbase, _ptr(self.cur),
+                                                        _ptr(self.status)), rt, label + "/reduce"))
+        return out
+
+    def _pool_launch(self, op, items, label):
+        probs, base = [], 0
+        for s, st in items:
+            c, h, w = st.in_shape
+            k = st.attrs["kernel"]
+            stride = st.attrs.get("stride", k)
+            oh, ow = conv_extent(h, k, stride, 0), conv_extent(w, k, stride, 0)
+            total = s.batch_size * c * (oh * ow if op == N.HNN_FWD else h * w)
+            blocks = -(-total // 256)
+            probs.append(N.PoolProblem(_ptr(st.x), _ptr(st.y), _ptr(st.idx), _ptr(st.dy), _ptr(st.dx),
+                                       _ptr(st.x) if st.mask_input else 0, s.batch_size, c, h, w, k, stride, oh,
+                                       ow, s.index, base, blocks, 0))
+            base += blocks
+        t = _dev_table(N.PoolProblem, probs, self.device)
+        return [Launch("hnn_grouped_maxpool", (op, _ptr(t), len(probs), base, _ptr(self.cur), _ptr(self.status)),
+                       t, label)]
+
+    def _relu_launch(self, op, items, label):
+        probs, base = [], 0
+        for s, st in items:
+            blocks = -(-(s.batch_size * st.ld_in) // 256)
+            probs.append(N.ReluProblem(_ptr(st.x), _ptr(st.y), _ptr(st.dy), _ptr(st.dx), s.batch_size, st.ld_in,
+                                       s.index, base, blocks, 0))
+            base += blocks
+        t = _dev_table(N.ReluProblem, probs, self.device)
+        return [Launch("hnn_grouped_relu", (op, _ptr(t), len(probs), base, _ptr(self.cur), _ptr(self.status)), t,
+                       label)]
+
+    def _wave_launches(self, op, items, label):
+        by_kind: dict = {}
+        for s, st in items:
+            by_kind.setdefault(st.kind, []).append((s, st))
+        out = []
+        for kind, group in by_kind.items():
+            if kind == "dense":
+                out += self._gemm_launch(op, group, f"{label}/dense")
+            elif kind == "conv":
+                out += self._conv_launch(op, group, f"{label}/conv")
+            elif kind == "pool":
+                out += self._pool_launch(N.HNN_FWD if op == N.HNN_FWD else N.HNN_DGRAD, group, f"{label}/pool")
+            else:
+                out += self._relu_launch(N.HNN_FWD if op == N.HNN_FWD else N.HNN_DGRAD, group, f"{label}/relu")
+        return out
+
+    def _sce_launch(self, train: bool):
+        probs = []
+        for s in self.slots:
+            last = s.stages[-1]
+            probs.append(N.SceProblem(_ptr(last.y), _ptr(s.batch_y), _ptr(last.dy) if train else 0, last.ld_out,
+                                      s.classes, s.batch_size, s.index))
+        t = _dev_table(N.SceProblem, probs, self.device)
+        cap = max(s.batch_size for s in self.slots)
+        ncls = max(s.classes for s in self.slots)
+        status = self.status if train else self.eval_status
+        return Launch("hnn_sce_fused", (_ptr(t), len(probs), cap, ncls, _ptr(self.cur), _ptr(status), int(train),
+                                        _ptr(self.loss_out), _ptr(self.correct_out)), t,
+                      "sce" if train else "sce/eval")
+
+    def _optimizer_launch(self):
+        segs, base = [], 0
+        for s in self.slots:
+            if s.seg_len == 0:
+                continue
+            chunks = -(-s.seg_len // OPT_CHUNK)
+            kind = s.opt_kind
+            segs.append(N.OptSegment(
+                _ptr(self.params) + 4 * s.seg_off, _ptr(self.grads) + 4 * s.seg_off,
+                (_ptr(self.m1) + 4 * s.seg_off) if kind != N.OPT_SGD else 0,
+                (_ptr(self.m2) + 4 * s.seg_off) if kind == N.OPT_ADAM else 0,
+                s.seg_len, s.index, kind, float(np.float32(s.momentum)), base, chunks, 0))
+            base += chunks
+        if not segs:
+            return []
+        t = _dev_table(N.OptSegment, segs, self.device)
+        entry = "hnn_multi_tensor_adam" if any(s.kind == N.OPT_ADAM for s in segs) else "hnn_multi_tensor_sgd"
+        return [Launch(entry, (_ptr(t), len(segs), base, _ptr(self.cur), _ptr(self.status)), t, "optimizer")]
+
+    def build_plans(self):
+        waves = self._stage_waves()
+        fwd = []
+        for w, items in enumerate(waves):
+            fwd += self._wave_launches(N.HNN_FWD, items, f"fwd{w}")
+        bwd = []
+        for w in range(len(waves) - 1, -1, -1):
+            items = waves[w]
+            wg = [(s, st) for s, st in items if st.kind in ("dense", "conv")]
+            if wg:
+                for kind in ("dense", "conv"):
+                    grp = [(s, st) for s, st in wg if st.kind == kind]
+                    if grp:
+                        bwd += (self._gemm_launch(N.HNN_WGRAD, grp, f"bwd{w}/dense/wgrad") if kind == "dense"
+                                else self._conv_launch(N.HNN_WGRAD, grp, f"bwd{w}/conv/wgrad"))
+            dg = [(s, st) for s, st in items if st.needs_dx]
+            if dg:
+                bwd += self._wave_launches(N.HNN_DGRAD, dg, f"bwd{w}")
+        self.forward_plan = fwd
+        self.train_plan = [self._gather_train] + fwd + [self._sce_launch(True)] + bwd + self._optimizer_launch()
+        self.eval_plan = [self._gather_eval] + fwd + [self._sce_launch(False)]
+        self.graph = None
+
+    # ------------------------------------------------------------------ running
+    def load_schedule(self, rows: np.ndarray):
+        """rows: [T, n] STEP_DTYPE.  Uploads and rewinds the step counter."""
+        torch = _torch()
+        flat = np.ascontiguousarray(rows).view(np.uint8).reshape(-1)
+        need = flat.size
+        if self.sched is None or self.sched.numel() < need:
+            self.sched = torch.zeros(max(need, 48 * self.n * 64), dtype=torch.uint8, device=self.device)
+            self.graph = None  # the graph captured the old schedule pointer
+        self.sched[:need].copy_(torch.from_numpy(flat))
+        self.counter.zero_()
+
+    def _stream(self):
+        torch = _torch()
+        return torch.cuda.current_stream(self.device).cuda_stream
+
+    def run_plan(self, plan: list, stream=None):
+        stream = self._stream() if stream is None else stream
+        N.call("hnn_step_begin", _ptr(self.sched), _ptr(self.counter), _ptr(self.cur), self.n, stream)
+        for launch in plan:
+            launch.run(stream)
+
+    def train_steps(self, count: int, use_graph: bool = False):
+        """Run `count` scheduled training steps (stream-ordered, asynchronous)."""
+        if not use_graph:
+            for _ in range(count):
+                self.run_plan(self.train_plan)
+            return
+        torch = _torch()
+        if self.graph is None:
+            side = torch.cuda.Stream(self.device)
+            side.wait_stream(torch.cuda.current_stream(self.device))
+            g = torch.cuda.CUDAGraph()
+            saved = self.counter.clone()
+            with torch.cuda.graph(g, stream=side):
+                self.run_plan(self.train_plan, side.cuda_stream)
+            torch.cuda.current_stream(self.device).wait_stream(side)
+            self.counter.copy_(saved)  # capture did not execute anything, but keep it explicit
+            self.graph = g
+        for _ in range(count):
+            self.graph.replay()
+
+    def launch_count(self, train: bool = True) -> int:
+        return 1 + len(self.train_plan if train else self.eval_plan)
+
+    def perm_upload(self, m: int, perm: np.ndarray):
+        self.perm[m, : perm.size].copy_(_torch().from_numpy(perm.astype(np.int32)))

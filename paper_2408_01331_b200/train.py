@@ -1,0 +1,514 @@
+"""Lockstep training of a merged hybrid on the GPU — the hot path's host side.
+
+Mirrors hybridnn.train (src/train.py:42-476): ``Trainer(hybrid, plan, jobs,
+datasets, ...)`` with the same hooks and report types, ``evaluate``,
+``train_standalone`` and checkpoints.  The difference is the schedule: the
+reference runs one (job, epoch) slice at a time; here every live job steps
+in lockstep, one grouped launch sequence per step for all of them
+(SURVEY.md finding 3 — a job's trajectory does not depend on the order).
+
+Per job the arithmetic is the reference's: the same keyed initial values and
+epoch permutations, ``lr_at_epoch``, the optimizer step counter t, a
+non-finite loss aborting only that job before its update
+(src/train.py:239-243, 408-418), sample-weighted epoch curves accumulated in
+float64 (:419-426) and the test split evaluated in order at completion
+(:259-279, 429-446).  Schedule-dependent outputs (``completion_index``,
+``executed``) follow the lockstep order instead of the plan's slice order.
+"""
+from __future__ import annotations
+
+import time
+from dataclasses import dataclass, field
+from functools import lru_cache
+
+import numpy as np
+
+from .errors import StateError, UnknownJobError
+from .model import TrainingJob
+from .optim import ADAM_BETA1, ADAM_BETA2, OptimizerState, lr_at_epoch
+from .runtime import STEP_DTYPE, DeviceDataset
+from .unify import HybridModel, merge, qualify, unqualify
+
+F32 = np.float32
+
+
+@lru_cache(maxsize=None)
+def _bias(t: int) -> tuple:
+    """Adam corrections for 1-based step t, evaluated like src/optim.py:75-76."""
+    return float(F32(1.0 - ADAM_BETA1 ** t)), float(F32(1.0 - ADAM_BETA2 ** t))
+
+
+# --------------------------------------------------------------------------- checkpoints
+
+
+@dataclass
+class Checkpoint:
+    """One job's resumable state at an epoch boundary (src/train.py:42-99)."""
+
+    job_id: str
+    completed_epochs: int
+    data_cursor: int
+    optimizer_kind: str
+    optimizer_step: int
+    momentum: float
+    params: dict
+    slot_m: dict = field(default_factory=dict)
+    slot_v: dict = field(default_factory=dict)
+    slot_momentum: dict = field(default_factory=dict)
+
+
+def make_checkpoint(hybrid: HybridModel, job_id: str) -> Checkpoint:
+    sub = hybrid.sub(job_id)
+    params = {unqualify(job_id, k): v.copy() for k, v in hybrid.sub_params(job_id).items()}
+    m1 = m2 = {}
+    if hybrid.device is not None:
+        m1, m2 = hybrid.device.download_moments(sub.slot)
+    else:
+        opt = sub.optimizer
+        m1 = {unqualify(job_id, k): v.copy() for k, v in (opt.m1 or opt.velocity).items()}
+        m2 = {unqualify(job_id, k): v.copy() for k, v in opt.m2.items()}
+    opt = sub.optimizer
+    adam = opt.kind == "adam"
+    return Checkpoint(job_id, sub.completed_epochs, sub.completed_epochs, opt.kind, opt.step, opt.momentum, params,
+                      slot_m=m1 if adam else {}, slot_v=m2 if adam else {},
+                      slot_momentum=m1 if (not adam and opt.momentum) else {})
+
+
+def restore_checkpoint(hybrid: HybridModel, ckpt: Checkpoint) -> None:
+    """Load a checkpoint into the matching sub-model (src/train.py:102-149)."""
+    sub = hybrid.sub(ckpt.job_id)
+    expect = {unqualify(ckpt.job_id, pid) for pid in sub.param_ids()}
+    if sorted(expect) != sorted(ckpt.params):
+        raise StateError(f"checkpoint for {ckpt.job_id!r} does not match the submitted model: parameter sets differ")
+    current = {unqualify(ckpt.job_id, k): v for k, v in hybrid.sub_params(ckpt.job_id).items()}
+    for pid, arr in ckpt.params.items():
+        if current[pid].shape != arr.shape:
+            raise StateError(f"checkpoint shape {arr.shape} != model shape {current[pid].shape} for parameter {pid!r}")
+    if sub.optimizer.kind != ckpt.optimizer_kind:
+        raise StateError(f"checkpoint optimizer {ckpt.optimizer_kind!r} != job optimizer {sub.optimizer.kind!r}")
+    hybrid.set_sub_params(ckpt.job_id, ckpt.params)
+    opt = sub.optimizer
+    opt.step, opt.momentum = ckpt.optimizer_step, ckpt.momentum
+    q = lambda d: {qualify(ckpt.job_id, k): np.array(v, copy=True) for k, v in d.items()}
+    opt.m1, opt.m2, opt.velocity = q(ckpt.slot_m), q(ckpt.slot_v), q(ckpt.slot_momentum)
+    if hybrid.device is not None:
+        hybrid.device.upload_moments(sub.slot, ckpt.slot_m or ckpt.slot_momentum, ckpt.slot_v)
+    sub.completed_epochs = ckpt.completed_epochs
+
+
+# --------------------------------------------------------------------------- reports
+
+
+@dataclass
+class JobResult:
+    job_id: str
+    status: str = "training"
+    slices_executed: int = 0
+    completion_index: int | None = None
+    epochs_completed: int = 0
+    curve: list = field(default_factory=list)
+    final_train_loss: float | None = None
+    final_train_accuracy: float | None = None
+    final_test_loss: float | None = None
+    final_test_accuracy: float | None = None
+    abort_reason: str | None = None
+    wall_time: float = 0.0
+
+    def to_dict(self, with_wall: bool = False) -> dict:
+        out = {
+            "job_id": self.job_id, "status": self.status, "slices_executed": self.slices_executed,
+            "completion_index": self.completion_index, "epochs_completed": self.epochs_completed,
+            "curve": [[e, l, a] for e, l, a in self.curve], "final_train_loss": self.final_train_loss,
+            "final_train_accuracy": self.final_train_accuracy, "final_test_loss": self.final_test_loss,
+            "final_test_accuracy": self.final_test_accuracy, "abort_reason": self.abort_reason,
+        }
+        if with_wall:
+            out["wall_time"] = self.wall_time
+        return out
+
+
+@dataclass
+class TrainReport:
+    policy: str
+    jobs: dict
+    executed: list = field(default_factory=list)
+    simulated_unified_time: float = 0.0
+    simulated_baseline_time: float = 0.0
+    memory_trace_ref: str | None = None
+    wall_time: float = 0.0
+    steps: int = 0             # lockstep device steps executed
+    samples: int = 0           # training rows consumed across all jobs
+
+    def to_dict(self, with_wall: bool = False) -> dict:
+        out = {
+            "policy": self.policy, "jobs": {j: r.to_dict(with_wall) for j, r in sorted(self.jobs.items())},
+            "executed": [[j, e] for j, e in self.executed], "simulated_unified_time": self.simulated_unified_time,
+            "simulated_baseline_time": self.simulated_baseline_time, "memory_trace_ref": self.memory_trace_ref,
+        }
+        if with_wall:
+            out["wall_time"] = self.wall_time
+        return out
+
+
+# --------------------------------------------------------------------------- the trainer
+
+
+class _Track:
+    """Lockstep bookkeeping of one job."""
+
+    def __init__(self, job, slot, dataset, epochs):
+        self.job, self.slot, self.dataset, self.epochs = job, slot, dataset, list(epochs)
+        hp = job.hypers
+        self.batch = hp.batch_size
+        self.n = dataset.sample_count
+        self.spe = -(-self.n // self.batch)
+        self.total = self.spe * len(self.epochs)
+        self.opt_base = 0
+        self.done = False
+
+    def epoch_index(self, t):
+        return t // self.spe
+
+
+class Trainer:
+    """Runs a plan over a hybrid, all live jobs in lockstep on the GPU.
+
+    Hooks are the reference's (src/train.py:294-325).  Extra keyword options:
+    ``use_graph`` (replay each step as a CUDA graph), ``use_tensor_cores``,
+    ``device``, ``comm`` (a :class:`paper_2408_01331_b200.parallel.RankGroup`
+    for multi-GPU dataset broadcast / metric gather).
+    """
+
+    def __init__(self, hybrid: HybridModel, plan, jobs: list, datasets: dict, completion_sink=None,
+                 pause_sink=None, pause_poll=None, step_observer=None, slice_observer=None, *,
+                 use_graph: bool = True, use_tensor_cores: bool = True, device=None, comm=None,
+                 loss_observer=None):
+        self.hybrid = hybrid
+        self.plan = plan
+        jobs = [TrainingJob.coerce(j) for j in jobs]
+        self.jobs = {j.job_id: j for j in jobs}
+        self.datasets = datasets
+        self.completion_sink, self.pause_sink, self.pause_poll = completion_sink, pause_sink, pause_poll
+        self.step_observer, self.slice_observer = step_observer, slice_observer
+        # loss_observer(job_id, step, loss, correct): per-step device losses (forces one-step windows)
+        self.loss_observer = loss_observer
+        self.use_graph, self.use_tc, self.device_name, self.comm = use_graph, use_tensor_cores, device, comm
+        self._pause_requests: set = set()
+        self.results = {j.job_id: JobResult(job_id=j.job_id, epochs_completed=j.completed_epochs) for j in jobs}
+        self.checkpoints: dict = {}
+        self._executed: list = []
+        self._device_data: dict = {}
+        for job_id in self.jobs:
+            if job_id not in hybrid.sub_models:
+                raise UnknownJobError(job_id)
+            if job_id not in datasets:
+                raise StateError(f"job {job_id!r}: dataset not resolved")
+
+    def request_pause(self, job_id: str) -> None:
+        if job_id not in self.jobs:
+            raise UnknownJobError(job_id)
+        status = self.results[job_id].status
+        if status in ("complete", "aborted"):
+            raise StateError(f"job {job_id!r} is already {status}")
+        self._pause_requests.add(job_id)
+
+    # ------------------------------------------------------------------ setup
+    def _epochs_from_plan(self) -> dict:
+        out = {jid: [] for jid in self.jobs}
+        for s in self.plan.slices:
+            if s.job_id in out:
+                out[s.job_id].append(s.epoch)
+        return out
+
+    def _device(self):
+        dev = self.hybrid.materialize(self.device_name, use_tensor_cores=self.use_tc)
+        for jid, sub in self.hybrid.sub_models.items():
+            opt = sub.optimizer
+            if opt.m1 or opt.m2 or opt.velocity:
+                strip = lambda d: {unqualify(jid, k): v for k, v in d.items()}
+                dev.upload_moments(sub.slot, strip(opt.m1 or opt.velocity), strip(opt.m2))
+        return dev
+
+    def _upload_datasets(self, dev) -> list:
+        by_model = [None] * dev.n
+        cache = self._device_data
+        for jid, sub in self.hybrid.sub_models.items():
+            if jid not in self.jobs:
+                ds = None
+            else:
+                ds = self.datasets[jid]
+            if ds is None:
+                continue
+            key = ds.content_hash
+            if key not in cache:
+                cache[key] = (self.comm.share_dataset(ds, dev.device) if self.comm is not None
+                              else DeviceDataset(ds, dev.device))
+            by_model[sub.slot] = cache[key]
+        # models of the hybrid not trained by this Trainer borrow any dataset of the right shape
+        for i, d in enumerate(by_model):
+            if d is None:
+                slot = dev.slots[i]
+                match = [v for v in cache.values() if tuple(v.sample_shape) == tuple(slot.sample_shape)]
+                if not match:
+                    raise StateError(f"job {slot.job_id!r}: dataset not resolved")
+                by_model[i] = match[0]
+        return by_model
+
+    # ------------------------------------------------------------------ run
+    def run(self) -> TrainReport:
+        started = time.perf_counter()
+        for job in self.jobs.values():
+            if job.completed_epochs >= job.hypers.epochs:
+                self._complete(job.job_id)
+        epochs = self._epochs_from_plan()
+        live = [jid for jid in self.jobs if self.results[jid].status == "training" and epochs[jid]]
+        steps_run, samples = 0, 0
+        if live:
+            dev = self._device()
+            by_model = self._upload_datasets(dev)
+            dev.bind_datasets(by_model, max(d.n_train for d in by_model))
+            dev.build_plans()
+            dev.reset_status()
+            self.device = dev
+            tracks = {}
+            for jid in live:
+                sub = self.hybrid.sub(jid)
+                tr = _Track(self.jobs[jid], sub.slot, self.datasets[jid], epochs[jid])
+                tr.opt_base = sub.optimizer.step
+                tracks[jid] = tr
+            steps_run, samples = self._lockstep(dev, tracks)
+        self._apply_pauses(force_all=True)
+        report = TrainReport(self.plan.policy, self.results, executed=list(self._executed),
+                             wall_time=time.perf_counter() - started, steps=steps_run, samples=samples)
+        return report
+
+    def _boundaries(self, tracks) -> list:
+        pts = {0}
+        for tr in tracks.values():
+            pts.update(range(tr.spe, tr.total + 1, tr.spe))
+        if self.step_observer is not None or self.loss_observer is not None:
+            pts.update(range(0, max(tr.total for tr in tracks.values()) + 1))
+        return sorted(pts)
+
+    def _window_rows(self, tracks, t0, t1) -> np.ndarray:
+        rows = np.zeros((t1 - t0, len(self.hybrid.sub_models)), dtype=STEP_DTYPE)
+        for tr in tracks.values():
+            if tr.done:
+                continue
+            lo, hi = t0, min(t1, tr.total)
+            if hi <= lo:
+                continue
+            hp = tr.job.hypers
+            for t in range(lo, hi):
+                i, b = divmod(t, tr.spe)
+                e = tr.epochs[i]
+                step = tr.opt_base + t + 1
+                b1, b2 = _bias(step)
+                rows[t - t0, tr.slot] = (1, min(tr.batch, tr.n - b * tr.batch), b * tr.batch, e, b, step,
+                                         float(F32(lr_at_epoch(hp.learning_rate, hp.lr_milestones, e))), b1, b2,
+                                         (0, 0, 0))
+        return rows
+
+    def _lockstep(self, dev, tracks) -> tuple:
+        from . import rng
+
+        bounds = self._boundaries(tracks)
+        horizon = max(tr.total for tr in tracks.values())
+        steps_run, samples = 0, 0
+        for t0, t1 in zip(bounds[:-1], bounds[1:]):
+            if t0 >= horizon or all(tr.done for tr in tracks.values()):
+                break
+            starting = []
+            for tr in tracks.values():
+                if not tr.done and t0 < tr.total and t0 % tr.spe == 0:
+                    e = tr.epochs[t0 // tr.spe]
+                    perm = rng.permutation(tr.n, "shuffle", tr.dataset.content_hash, tr.job.hypers.seed, e)
+                    dev.perm_upload(tr.slot, perm)
+                    starting.append(tr.slot)
+            dev.reset_accumulators(starting)
+            rows = self._window_rows(tracks, t0, t1)
+            samples += int(rows["rows"][rows["active"] == 1].sum())
+            dev.load_schedule(rows)
+            wall0 = time.perf_counter()
+            dev.train_steps(t1 - t0, use_graph=self.use_graph)
+            steps_run += t1 - t0
+            if self.loss_observer is not None:
+                losses = dev.loss_out.cpu().numpy()
+                hits = dev.correct_out.cpu().numpy()
+                for tr in tracks.values():
+                    if not tr.done and t0 < tr.total:
+                        self.loss_observer(tr.job.job_id, t0, float(losses[tr.slot]), int(hits[tr.slot]))
+            if self.step_observer is not None:
+                alive = dev.read_status()["alive"]
+                for tr in tracks.values():
+                    if not tr.done and t0 < tr.total and alive[tr.slot]:
+                        self.step_observer(tr.job.job_id, self.hybrid.sub_params(tr.job.job_id))
+            st = dev.read_status()  # synchronises the stream
+            elapsed = time.perf_counter() - wall0
+            for tr in tracks.values():
+                if tr.done or t0 >= tr.total:
+                    continue
+                res = self.results[tr.job.job_id]
+                res.wall_time += elapsed
+                row = st[tr.slot]
+                if not row["alive"]:
+                    res.status = "aborted"
+                    res.abort_reason = (f"non-finite loss in job {tr.job.job_id} at epoch {int(row['abort_epoch'])}"
+                                        f", batch {int(row['abort_batch'])}")
+                    tr.done = True
+                    continue
+                if t1 % tr.spe == 0 and t1 <= tr.total:
+                    i = t1 // tr.spe - 1
+                    e = tr.epochs[i]
+                    seen = int(row["seen"])
+                    loss, acc = float(row["loss_sum"]) / seen, int(row["correct_sum"]) / seen
+                    res.curve.append((e, loss, acc))
+                    res.final_train_loss, res.final_train_accuracy = loss, acc
+                    res.slices_executed += 1
+                    res.epochs_completed = e + 1
+                    sub = self.hybrid.sub(tr.job.job_id)
+                    sub.completed_epochs = e + 1
+                    sub.optimizer.step = tr.opt_base + t1
+                    self._executed.append((tr.job.job_id, e))
+                    if self.slice_observer is not None:
+                        self.slice_observer(tr.job.job_id, e)
+                    if e == tr.job.hypers.epochs - 1:
+                        tr.done = True
+                        self._complete(tr.job.job_id)
+                    elif self._pause_wanted(tr.job.job_id):
+                        tr.done = True
+                        self._pause(tr.job.job_id)
+        return steps_run, samples
+
+    # ------------------------------------------------------------------ completion / pause
+    def _pause_wanted(self, job_id) -> bool:
+        if job_id in self._pause_requests:
+            return True
+        if self.pause_poll is not None:
+            return job_id in set(self.pause_poll())
+        return False
+
+    def _pause(self, job_id):
+        self._pause_requests.discard(job_id)
+        ckpt = make_checkpoint(self.hybrid, job_id)
+        self.checkpoints[job_id] = ckpt
+        self.results[job_id].status = "paused"
+        if self.pause_sink is not None:
+            self.pause_sink(job_id, ckpt)
+
+    def _apply_pauses(self, force_all=False):
+        wanted = set(self._pause_requests)
+        if self.pause_poll is not None:
+            wanted |= {j for j in self.pause_poll() if j in self.jobs and self.results[j].status == "training"}
+        self._pause_requests.clear()
+        for jid in sorted(wanted):
+            if self.results[jid].status == "training":
+                self._pause(jid)
+
+    def _complete(self, job_id: str) -> None:
+        result = self.results[job_id]
+        sub = self.hybrid.sub(job_id)
+        ds = self.datasets[job_id]
+        loss, acc = evaluate_hybrid(self.hybrid, [job_id], {job_id: ds}, trainer=self)[job_id]
+        result.status = "complete"
+        result.completion_index = len(self._executed)
+        result.final_test_loss, result.final_test_accuracy = loss, acc
+        if self.completion_sink is not None:
+            self.completion_sink(job_id, self.hybrid.snapshot(), result)
+
+
+# --------------------------------------------------------------------------- evaluation
+
+
+def evaluate_hybrid(hybrid: HybridModel, job_ids: list, datasets: dict, trainer=None) -> dict:
+    """Test-split loss/accuracy of several sub-models in one lockstep forward pass (src/train.py:259-279)."""
+    dev = hybrid.device
+    if dev is None or not dev.eval_plan:
+        t = Trainer(hybrid, _NoPlan(), [], {}, use_graph=False)
+        dev = hybrid.materialize()
+        by_model = []
+        cache = {}
+        for jid, sub in hybrid.sub_models.items():
+            ds = datasets.get(jid) or next(iter(datasets.values()))
+            if ds.content_hash not in cache:
+                cache[ds.content_hash] = DeviceDataset(ds, dev.device)
+            by_model.append(cache[ds.content_hash])
+        dev.bind_datasets(by_model, max(d.n_train for d in by_model))
+        dev.build_plans()
+        del t
+    out = {}
+    todo = []
+    for jid in job_ids:
+        n_test = datasets[jid].test_x.shape[0]
+        if n_test == 0:
+            out[jid] = (0.0, 0.0)
+        else:
+            todo.append(jid)
+    if not todo:
+        return out
+    slots = {jid: hybrid.sub(jid).slot for jid in todo}
+    for jid in todo:
+        if dev.model_data[slots[jid]].content_hash != datasets[jid].content_hash:
+            raise StateError(f"job {jid!r}: evaluation dataset differs from the bound one")
+    steps = {jid: -(-datasets[jid].test_x.shape[0] // dev.slots[slots[jid]].batch_size) for jid in todo}
+    T = max(steps.values())
+    rows = np.zeros((T, dev.n), dtype=STEP_DTYPE)
+    for jid in todo:
+        m, B, n = slots[jid], dev.slots[slots[jid]].batch_size, datasets[jid].test_x.shape[0]
+        for t in range(steps[jid]):
+            rows[t, m]["active"] = 1
+            rows[t, m]["rows"] = min(B, n - t * B)
+            rows[t, m]["perm_base"] = t * B
+    dev.reset_status(dev.eval_status)
+    dev.load_schedule(rows)
+    for _ in range(T):
+        dev.run_plan(dev.eval_plan)
+    st = dev.read_status(dev.eval_status)
+    for jid in todo:
+        row = st[slots[jid]]
+        total = int(row["seen"])
+        out[jid] = (float(row["loss_sum"]) / total, int(row["correct_sum"]) / total)
+    return out
+
+
+class _NoPlan:
+    policy = "lockstep"
+    slices = ()
+
+
+def evaluate(graph, params, order, x, y, batch_size: int) -> tuple:
+    """Reference-signature evaluate (src/train.py:259-279) for one model, on the GPU."""
+    from . import store
+    from .model import HyperParams
+
+    job = TrainingJob("eval", graph, "eval", HyperParams(1, batch_size, 1.0), 0, 0)
+    h = merge([job])
+    h.set_sub_params("eval", {k.split("/", 1)[-1]: v for k, v in params.items()})
+    ds = store.Dataset("eval", x[:1].astype(np.float32), np.zeros(1, np.float32),
+                       np.ascontiguousarray(x, dtype=np.float32), np.asarray(y, dtype=np.float32))
+    return evaluate_hybrid(h, ["eval"], {"eval": ds})["eval"]
+
+
+# --------------------------------------------------------------------------- standalone
+
+
+def train_standalone(job, dataset, step_observer=None, **options) -> tuple:
+    """Train one model alone (src/train.py:453-476) — the same device path with one slot."""
+    job = TrainingJob.coerce(job)
+    hybrid = merge([job])
+    from .schedule import make_plan
+
+    observer = None
+    if step_observer is not None:
+        observer = lambda jid, p: step_observer(jid, {unqualify(jid, k): v for k, v in p.items()})
+    trainer = Trainer(hybrid, make_plan("fcfs", [job]), [job], {job.job_id: dataset}, step_observer=observer,
+                      **options)
+    report = trainer.run()
+    res = report.jobs[job.job_id]
+    if res.status == "aborted":
+        raise StateError(f"non-finite loss in standalone run of {job.job_id} at epoch "
+                         f"{res.abort_reason.split('epoch ')[1].split(',')[0]}")
+    params = {unqualify(job.job_id, k): v for k, v in hybrid.sub_params(job.job_id).items()}
+    sub = hybrid.sub(job.job_id)
+    opt = OptimizerState(sub.optimizer.kind, sub.optimizer.momentum, sub.optimizer.step)
+    return params, opt

@@ -1,0 +1,139 @@
+"""Host-side logic and the C-ABI library surface (no GPU needed)."""
+import re
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+import oracle
+from conftest import REPO, load_case
+
+import paper_2408_01331_b200 as h
+from paper_2408_01331_b200 import _native, store, zoo
+from paper_2408_01331_b200.runtime import lower_graph
+
+
+def header_symbols():
+    text = (REPO / "include" / "hnn_b200.h").read_text()
+    return sorted(set(re.findall(r"^(?:int|const char\*)\s+(hnn_\w+)\(", text, flags=re.M)))
+
+
+def test_library_exports_every_declared_symbol():
+    lib = _native.load()
+    syms = header_symbols()
+    assert len(syms) >= 14
+    for name in syms:
+        assert hasattr(lib, name), name
+        assert name in _native.SIGNATURES, f"binding misses {name}"
+    assert lib.hnn_version().startswith(b"hnn_b200")
+
+
+def test_abi_struct_layouts_match_binding():
+    lib = _native.load()
+    for name, cls in _native.STRUCTS.items():
+        import ctypes
+
+        assert lib.hnn_struct_size(name.encode()) == ctypes.sizeof(cls), name
+
+
+def test_library_is_sm100a_cubin():
+    import subprocess
+
+    out = subprocess.run(["/usr/local/cuda/bin/cuobjdump", "-lelf", str(_native.LIB_PATH)], capture_output=True,
+                         text=True).stdout
+    assert "sm_100a" in out
+
+
+def test_merge_validation_mirrors_reference():
+    with pytest.raises(h.StateError, match="empty"):
+        h.merge([])
+    ds = store.from_splits(oracle.blob_splits("t", "v", 2, 8, 16, 4))
+    good = zoo.job("a", zoo.mlp(8, (16,), 2), ds, 0)
+    bad = zoo.job("b", zoo.mlp(8, (16,), 2), ds, 1)
+    del bad.graph.nodes[0].attrs["units"]
+    bad2 = zoo.job("c", zoo.mlp(8, (16,), 2), ds, 2)
+    bad2.graph.nodes[1].inputs = ["ghost"]
+    with pytest.raises(h.MergeError) as info:
+        h.merge([good, bad, bad2])
+    assert set(info.value.per_job) == {"b", "c"}
+    assert any("missing attr" in p for p in info.value.per_job["b"])
+    assert any("unknown input" in p for p in info.value.per_job["c"])
+    with pytest.raises(h.MergeError) as info:
+        h.merge([good, zoo.job("a", zoo.mlp(8, (16,), 2), ds, 3)])
+    assert any("duplicate" in p for p in info.value.per_job["a"])
+
+
+def test_init_is_bit_exact_and_merge_order_free():
+    g1, g2 = zoo.mlp(784, (256,), 10), zoo.lenet5()
+    ds = store.from_splits(oracle.blob_splits("t", "w", 2, 8, 16, 4))
+    j1, j2 = zoo.job("x", g1, ds, 0, seed=3), zoo.job("y", g2, ds, 1, seed=4)
+    a, b = h.merge([j1, j2]), h.merge([j2, j1])
+    for pid in a.params:
+        assert np.array_equal(a.params[pid], b.params[pid])
+    for job in (j1, j2):
+        ref = oracle.init_model(job.graph, job.hypers.seed)
+        assert list(h.param_specs(job.graph)) == list(oracle.param_layout(job.graph))
+        for pid, v in ref.items():
+            assert np.array_equal(a.params[f"{job.job_id}/{pid}"], v)
+
+
+def test_namespacing_and_routing_nodes():
+    ds = store.from_splits(oracle.blob_splits("t", "w", 2, 8, 16, 4))
+    hy = h.merge([zoo.job("a", zoo.mlp(8, (16,), 2), ds, 0), zoo.job("b", zoo.lenet5(), ds, 1)])
+    assert hy.job_ids() == ["a", "b"]
+    assert hy.global_input.node_id == "hybrid/input" and hy.global_output.routes["a"] == "a/fc2"
+    assert hy.node_count() == 3 + 12 + 2
+    assert hy.sub("a").graph.nodes[0].inputs == ["input"]
+    with pytest.raises(h.UnknownJobError):
+        hy.sub("zzz")
+    snap = hy.snapshot()
+    snap.params["a/fc1.weight"][0, 0] = 99.0
+    assert hy.params["a/fc1.weight"][0, 0] != 99.0
+
+
+def test_batches_and_hash_match_oracle():
+    splits = oracle.blob_splits("t", "b", 3, 5, 23, 4)
+    ds = store.from_splits(splits)
+    assert ds.content_hash == oracle.dataset_digest(splits)
+    got = store.batches(ds, 4, 7, 2)
+    ref = oracle.epoch_batches(splits["train_x"], splits["train_y"], ds.content_hash, 4, 7, 2)
+    assert [b.x.shape[0] for b in got] == [4, 4, 4, 4, 4, 3]
+    for b, (x, y, _) in zip(got, ref):
+        assert np.array_equal(b.x, x) and np.array_equal(b.y, y)
+    assert store.batch_count(60000, 256) == 235
+
+
+def test_lowering_fuses_relu_and_marks_masks():
+    st, classes, head = lower_graph(zoo.lenet5())
+    assert [s.kind for s in st] == ["conv", "pool", "conv", "pool", "dense", "dense", "dense"]
+    assert [s.relu for s in st] == [True, False, True, False, True, True, False]
+    assert [s.mask_input for s in st] == [False, True, False, True, False, True, True]
+    assert [s.needs_dx for s in st] == [False, True, True, True, True, True, True]
+    assert classes == 10 and not head
+    # a relu that ends the graph stays a stand-alone stage
+    g = zoo.mlp(8, (4,), 3)
+    g.nodes.append(h.OpNode("act_out", "relu", [g.output]))
+    g.output = "act_out"
+    st, _, _ = lower_graph(g)
+    assert [s.kind for s in st] == ["dense", "dense", "relu"]
+
+
+def test_schedule_rows_follow_reference_batches_and_adam_steps():
+    from paper_2408_01331_b200.train import Trainer, _Track
+
+    splits = oracle.blob_splits("t", "s", 2, 8, 70, 4)
+    ds = store.from_splits(splits)
+    job = zoo.job("a", zoo.mlp(8, (16,), 2), ds, 0, epochs=3, batch_size=32, lr=0.1, optimizer="adam",
+                  milestones=(2,))
+    hy = h.merge([job])
+    tr = Trainer(hy, h.make_plan("fcfs", [job]), [job], {"a": ds})
+    track = _Track(job, 0, ds, [0, 1, 2])
+    rows = tr._window_rows({"a": track}, 0, track.total)
+    assert track.spe == 3 and track.total == 9
+    assert rows["rows"][:, 0].tolist() == [32, 32, 6] * 3
+    assert rows["perm_base"][:, 0].tolist() == [0, 32, 64] * 3
+    assert rows["epoch"][:, 0].tolist() == [0, 0, 0, 1, 1, 1, 2, 2, 2]
+    assert rows["opt_step"][:, 0].tolist() == list(range(1, 10))
+    # milestone 2 (one-based) decays from zero-based epoch 1 on (src/optim.py:22-30)
+    assert np.all(rows["lr"][:3, 0] == np.float32(0.1)) and np.all(rows["lr"][3:, 0] == np.float32(0.1 * 0.1))
+    assert rows["bias1"][0, 0] == np.float32(1.0 - 0.9) and rows["bias2"][4, 0] == np.float32(1.0 - 0.999 ** 5)
