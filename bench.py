@@ -1,0 +1,393 @@
+"""Benchmark: aggregate train samples/s of N merged models on B200 (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload c3|c2|c5|c1] [--impl reference]
+
+Default workload: C3 — 32 heterogeneous MLPs 784-h-h-10, h_i = 128*(1 + i mod 16), Adam lr 1e-3,
+batch 256, synthetic MNIST-shaped blob data (60,000 x 784).  It is the config BASELINE.json
+quotes at 1/2/4/8 GPUs; at N GPUs each rank trains its own 32 models (model-identity sharding,
+weak scaling, no gradient collective; NCCL broadcasts the dataset once).
+
+One "step" = one lockstep optimizer step of every model on its next batch.
+  value   device-resident throughput: inputs already in HBM, CUDA events around K steps
+          (CUDA-graph replay), max over ranks.
+  e2e     the public host-fed API (paper_2408_01331_b200.train.HostFedStepper): every step
+          copies that step's batches from pinned host memory to the device and reads the
+          per-model losses back; CUDA events around K steps.
+  roofline the dominant kernel of the step, timed per launch with CUDA events on its stream.
+  cpu_baseline the reference algorithm (the numpy oracle port) on the host cores, bounded sample.
+--impl reference runs only that CPU arm (rank 0) and prints its own line.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import time
+from pathlib import Path
+
+REPO = Path(__file__).resolve().parent
+sys.path.insert(0, str(REPO))
+
+import numpy as np  # noqa: E402
+
+METRIC = "Aggregate train samples/s over N merged models"
+UNIT = "samples/s"
+WORKLOADS = {
+    "c3": "C3: 32 heterogeneous MLPs 784-h-h-10 (h=128*(1+i%16)) per GPU, Adam lr 1e-3, batch 256, "
+          "synthetic MNIST-shaped blob 60000x784",
+    "c2": "C2: 8 LeNet-5 per GPU, SGD lr 0.01, batch 128, synthetic CIFAR-shaped 50000x3x32x32",
+    "c5": "C5: 32 MLP 784-256-10 per GPU (256 over 8), SGD lr 10^(-3+2i/255), batch 64, MNIST-shaped blob",
+    "c1": "C1: 2 MLP 784-256-10, SGD lr 0.01/0.05, batch 64, MNIST-shaped blob",
+}
+MODELS_PER_GPU = {"c3": 32, "c2": 8, "c5": 32, "c1": 2}
+
+
+def peaks():
+    p = REPO / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return d["hbm_gbs"], d["bf16_tflops"], d.get("bf16_tflops_sustained", d["bf16_tflops"]), "measured"
+    return 6650.0, 1590.0, 1400.0, "fallback"
+
+
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+def make_dataset(workload):
+    from paper_2408_01331_b200 import zoo
+
+    if workload == "c2":
+        return zoo.image_dataset()
+    return zoo.blob_dataset()
+
+
+# ----------------------------------------------------------------------------- CPU arm
+
+
+_CPU_DATA = {}
+
+
+def _cpu_worker(args):
+    """Reference algorithm (oracle port) for one model: `steps` batches from its epoch-0 order.
+
+    The dataset is inherited through fork (module global), never pickled."""
+    os.environ["OPENBLAS_NUM_THREADS"] = "1"
+    from threadpoolctl import threadpool_limits
+
+    import oracle
+
+    graph, seed, lr, opt, batch, steps = args
+    xs, ys, digest = _CPU_DATA["x"], _CPU_DATA["y"], _CPU_DATA["digest"]
+    with threadpool_limits(1):
+        params = oracle.init_model(graph, seed)
+        o = oracle.OracleOptimizer(opt)
+        perm = oracle.keyed_permutation(xs.shape[0], "shuffle", digest, seed, 0)
+        t0 = time.perf_counter()
+        done = 0
+        for b in range(steps):
+            idx = perm[b * batch:(b + 1) * batch]
+            oracle.train_step(graph, params, xs[idx], ys[idx], o, lr)
+            done += idx.size
+        return done, time.perf_counter() - t0
+
+
+def cpu_baseline(jobs, ds, steps_per_model):
+    """Aggregate samples/s of the reference algorithm over all host cores (one process per core).
+
+    Each worker times only its training steps (init excluded); the aggregate assumes the
+    per-model work packs perfectly onto the cores: samples / (sum of step times / processes)."""
+    import multiprocessing as mp
+
+    cores = len(os.sched_getaffinity(0))
+    procs = min(cores, len(jobs))
+    _CPU_DATA.update(x=ds.train_x, y=ds.train_y, digest=ds.content_hash)
+    work = [(j.graph, j.hypers.seed, j.hypers.learning_rate, j.hypers.optimizer, j.hypers.batch_size,
+             steps_per_model) for j in jobs]
+    ctx = mp.get_context("fork")
+    t0 = time.perf_counter()
+    with ctx.Pool(procs) as pool:
+        res = pool.map(_cpu_worker, work, chunksize=1)
+    wall = time.perf_counter() - t0
+    samples = sum(r[0] for r in res)
+    busy = sum(r[1] for r in res)
+    return {"value": samples / (busy / procs), "unit": UNIT, "cores": procs, "kind": "port",
+            "sample": f"{steps_per_model} steps x {len(jobs)} models of the workload (the oracle's numpy "
+                      f"restatement of hybridnn run_batch, 1 BLAS thread per process); {samples} samples, "
+                      f"{busy:.1f} core-seconds of steps, {wall:.1f}s wall incl. init"}
+
+
+# ----------------------------------------------------------------------------- clocks
+
+
+class ClockSampler:
+    def __init__(self, index=0):
+        self.index, self.proc, self.path = index, None, Path(f"/tmp/hnn_clocks_{os.getpid()}.csv")
+
+    def __enter__(self):
+        q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.index}", f"--query-gpu={q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except FileNotFoundError:
+            self.proc = None
+        time.sleep(0.3)
+        return self
+
+    def __exit__(self, *a):
+        if self.proc is not None:
+            self.proc.terminate()
+            self.proc.wait()
+
+    def summary(self):
+        if not self.path.exists():
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        rows = [r.split(", ") for r in self.path.read_text().strip().splitlines() if r.count(",") >= 8]
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(r[1]) for r in rows]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4) if r[5 + i].strip() == "Active"})
+        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": float(rows[0][2]), "reasons": reasons,
+                "samples": len(rows)}
+
+
+# ----------------------------------------------------------------------------- GPU arm
+
+
+def build_rank(workload, rank, world, device):
+    """Jobs of this rank (model-identity shard), hybrid, device dataset, plans, epoch-0 perms."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2408_01331_b200 import merge, store, zoo
+    from paper_2408_01331_b200.parallel import RankGroup
+
+    comm = RankGroup(rank, world, device) if world > 1 else None
+    # every rank keeps a host copy for the host-fed (e2e) arm; HBM copies come from rank 0's broadcast
+    ds = make_dataset(workload)
+    if comm is not None:
+        ddev, _ = comm.share_dataset(ds if rank == 0 else None, device)
+        meta = ds
+    else:
+        from paper_2408_01331_b200.runtime import DeviceDataset
+
+        ddev, meta = DeviceDataset(ds, device), ds
+    per = MODELS_PER_GPU[workload]
+    jobs = zoo.config_jobs(workload, meta, first_model=per * rank, count=per)
+    hy = merge(jobs)
+    dev = hy.materialize(device)
+    dev.bind_datasets([ddev] * dev.n, ddev.n_train)
+    dev.build_plans()
+    return jobs, hy, dev, ddev, meta, ds, comm
+
+
+def schedule(jobs, meta, steps):
+    """Rows for `steps` lockstep steps from epoch 0 (wrapping the epoch-0 order past its end)."""
+    from paper_2408_01331_b200.runtime import STEP_DTYPE
+    from paper_2408_01331_b200.train import _bias
+    from paper_2408_01331_b200.optim import lr_at_epoch
+
+    rows = np.zeros((steps, len(jobs)), dtype=STEP_DTYPE)
+    n = meta.sample_count
+    for m, j in enumerate(jobs):
+        B = j.hypers.batch_size
+        spe = -(-n // B)
+        lr = float(np.float32(lr_at_epoch(j.hypers.learning_rate, (), 0)))
+        for t in range(steps):
+            b = t % spe
+            b1, b2 = _bias(t + 1)
+            rows[t, m] = (1, min(B, n - b * B), b * B, t // spe, b, t + 1, lr, b1, b2, (0, 0, 0))
+    return rows
+
+
+def upload_perms(dev, jobs, meta):
+    from paper_2408_01331_b200 import rng
+
+    for m, j in enumerate(jobs):
+        dev.perm_upload(m, rng.permutation(meta.sample_count, "shuffle", meta.content_hash, j.hypers.seed, 0))
+
+
+def kernel_profile(dev, steps):
+    """Average duration of every launch of an eager step (CUDA events on the launch stream)."""
+    import torch
+
+    from paper_2408_01331_b200 import _native as N
+
+    stream = torch.cuda.current_stream()
+    plan = dev.train_plan
+    totals = np.zeros(len(plan))
+    for _ in range(steps):
+        evs = [torch.cuda.Event(enable_timing=True) for _ in range(len(plan) + 1)]
+        N.call("hnn_step_begin", int(dev.sched.data_ptr()), int(dev.counter.data_ptr()), int(dev.cur.data_ptr()),
+               dev.n, stream.cuda_stream)
+        evs[0].record(stream)
+        for i, launch in enumerate(plan):
+            launch.run(stream.cuda_stream)
+            evs[i + 1].record(stream)
+        torch.cuda.synchronize()
+        totals += [evs[i].elapsed_time(evs[i + 1]) for i in range(len(plan))]
+    return totals / steps  # ms
+
+
+def roofline(dev, per_launch_ms, hbm, tf_burst, tf_sus, peak_kind):
+    i = int(np.argmax(per_launch_ms))
+    launch = dev.train_plan[i]
+    sec = per_launch_ms[i] / 1e3
+    share = float(per_launch_ms[i] / per_launch_ms.sum())
+    if launch.flops:
+        achieved = launch.flops / sec / 1e12
+        peak = tf_sus
+        return {"kernel": launch.label, "bound": "tensor", "achieved": round(achieved, 3), "peak": peak,
+                "unit": "TFLOP/s", "frac": round(achieved / peak, 5), "traffic": None,
+                "share_of_step": round(share, 4), "avg_ms": round(per_launch_ms[i], 4),
+                "peak_source": f"{peak_kind} bf16 sustained (MEASURED_PEAKS.json); kernel computes fp32"}
+    achieved = launch.nbytes / sec / 1e9
+    return {"kernel": launch.label, "bound": "hbm", "achieved": round(achieved, 1), "peak": hbm, "unit": "GB/s",
+            "frac": round(achieved / hbm, 4), "traffic": None, "share_of_step": round(share, 4),
+            "avg_ms": round(per_launch_ms[i], 4), "peak_source": f"{peak_kind} HBM copy (MEASURED_PEAKS.json)"}
+
+
+def gpu_arm(args):
+    import torch
+    import torch.distributed as dist
+
+    world, rank, local = dist_env()
+    torch.cuda.set_device(local)
+    device = torch.device("cuda", local)
+    if world > 1 and not dist.is_initialized():
+        dist.init_process_group("nccl", device_id=device)
+    jobs, hy, dev, ddev, meta, ds, comm = build_rank(args.workload, rank, world, device)
+    total = args.warmup + args.steps
+    rows = schedule(jobs, meta, total + 8)
+    upload_perms(dev, jobs, meta)
+    samples_per_step = int(rows["rows"][: args.steps].sum()) / args.steps
+
+    # ---- device-resident timed run (CUDA graph replay)
+    dev.load_schedule(rows)
+    dev.train_steps(args.warmup, use_graph=True)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    start, stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clocks:
+        torch.cuda.synchronize()
+        start.record()
+        dev.train_steps(args.steps, use_graph=True)
+        stop.record()
+        torch.cuda.synchronize()
+    ms = start.elapsed_time(stop)
+    if world > 1:
+        dist.barrier()
+        t = torch.tensor([ms], device=device)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    value = samples_per_step * world * args.steps / (ms / 1e3)
+
+    # ---- per-kernel timing for the roofline (eager, same schedule)
+    dev.load_schedule(rows)
+    per_launch = kernel_profile(dev, min(5, args.steps))
+    hbm, tfb, tfs, kind = peaks()
+    roof = roofline(dev, per_launch, hbm, tfb, tfs, kind)
+
+    # ---- e2e through the host-fed public API
+    from paper_2408_01331_b200.train import HostFedStepper
+
+    stepper = HostFedStepper(hy, {j.job_id: meta for j in jobs})
+    host_batches = stepper.stage_epoch_batches(ds if ds is not None else None, rows, count=2,
+                                               comm=comm)
+    dev.load_schedule(rows)
+    for i in range(args.warmup):
+        stepper.step(host_batches[i % len(host_batches)])
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for i in range(args.steps):
+        stepper.step(host_batches[i % len(host_batches)])
+    stepper.finish()
+    e1.record()
+    torch.cuda.synchronize()
+    ems = e0.elapsed_time(e1)
+    if world > 1:
+        t = torch.tensor([ems], device=device)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ems = float(t.item())
+    e2e = {"value": round(samples_per_step * world * args.steps / (ems / 1e3), 1), "unit": UNIT,
+           "h2d_bytes_per_step": stepper.h2d_bytes_per_step, "d2h_bytes_per_step": stepper.d2h_bytes_per_step,
+           "api": "paper_2408_01331_b200.train.HostFedStepper.step (pinned host batches -> HBM, losses -> host)"}
+
+    peak_alloc = torch.cuda.max_memory_allocated(device)
+    n_models = len(jobs)
+    line = {
+        "metric": METRIC, "value": round(value, 1), "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": round(ms / args.steps, 4), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic (keyed-Philox blob/image "
+        "generators of the reference), random-init weights from the reference's keyed init",
+        "config": {"workload": WORKLOADS[args.workload], "models_per_gpu": n_models,
+                   "global_batch": int(samples_per_step * world), "parallelism": f"model-identity sharding x{world}",
+                   "l2": "per-step working set (params+grads+Adam moments) exceeds the 126 MB L2; no flush"},
+        "hbm_bytes_per_model": int((peak_alloc - ddev.nbytes) / n_models + ddev.nbytes / n_models),
+        "gpu_launches": dev.launch_count() * args.steps,
+        "e2e": e2e, "roofline": roof, "clocks": clocks.summary(),
+    }
+    if rank == 0 and world == 1 and not args.no_cpu:
+        line["cpu_baseline"] = cpu_baseline(jobs, ds, args.cpu_steps)
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def reference_arm(args):
+    world, rank, _ = dist_env()
+    if rank != 0:
+        return
+    from paper_2408_01331_b200 import zoo
+
+    ds = make_dataset(args.workload)
+    jobs = zoo.config_jobs(args.workload, ds, count=MODELS_PER_GPU[args.workload])
+    # warmup: one short pass so page-ins / pool start-up are not timed
+    if args.warmup:
+        cpu_baseline(jobs[:2], ds, 1)
+    base = cpu_baseline(jobs, ds, max(1, args.steps // 4))
+    line = {"metric": METRIC, "value": round(base["value"], 2), "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f32", "data": "synthetic", "impl": "reference",
+            "config": {"workload": WORKLOADS[args.workload], "models_per_gpu": MODELS_PER_GPU[args.workload],
+                       "parallelism": "host processes, one model per core"},
+            "cpu_baseline": base,
+            "e2e": {"value": round(base["value"], 2), "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--workload", default="c3", choices=sorted(WORKLOADS))
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--cpu-steps", type=int, default=3)
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.impl == "reference":
+        reference_arm(args)
+    else:
+        gpu_arm(args)
+
+
+if __name__ == "__main__":
+    main()

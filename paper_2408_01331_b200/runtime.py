@@ -171,25 +171,37 @@ class ModelSlot:
 class DeviceDataset:
     """A dataset resident in HBM once: samples as f32, labels as int32 class ids."""
 
-    def __init__(self, ds, device, classes: int | None = None, src=None):
+    def __init__(self, ds, device):
         torch = _torch()
         from .ops import check_class_indices
 
         self.content_hash = ds.content_hash
         self.sample_shape = tuple(ds.train_x.shape[1:])
         self.n_train, self.n_test = int(ds.train_x.shape[0]), int(ds.test_x.shape[0])
-        k = classes if classes is not None else 1 << 30
-        ytr = check_class_indices(ds.train_y, k).astype(np.int32)
-        yte = check_class_indices(ds.test_y, k).astype(np.int32) if self.n_test else np.zeros(0, np.int32)
-        if src is not None:  # tensors already on the device (e.g. received by broadcast)
-            self.train_x, self.train_y, self.test_x, self.test_y = src
-        else:
-            self.train_x = torch.from_numpy(np.ascontiguousarray(ds.train_x, dtype=np.float32)).to(device)
-            self.test_x = torch.from_numpy(np.ascontiguousarray(ds.test_x, dtype=np.float32)).to(device)
-            self.train_y = torch.from_numpy(ytr).to(device)
-            self.test_y = torch.from_numpy(yte).to(device)
-        self.identity = torch.arange(max(self.n_test, 1), dtype=torch.int32, device=device)
+        ytr = check_class_indices(ds.train_y, 1 << 30).astype(np.int32)
+        yte = check_class_indices(ds.test_y, 1 << 30).astype(np.int32) if self.n_test else np.zeros(0, np.int32)
+        self.train_x = torch.from_numpy(np.ascontiguousarray(ds.train_x, dtype=np.float32)).to(device)
+        self.test_x = torch.from_numpy(np.ascontiguousarray(ds.test_x, dtype=np.float32)).to(device)
+        self.train_y = torch.from_numpy(ytr).to(device)
+        self.test_y = torch.from_numpy(yte).to(device)
         self.max_label = int(max(ytr.max(initial=0), yte.max(initial=0)))
+        self._finish(device)
+
+    @classmethod
+    def from_tensors(cls, content_hash, train_x, train_y, test_x, test_y, max_label, device):
+        """Wrap tensors already on the device (e.g. received through an NCCL broadcast)."""
+        self = cls.__new__(cls)
+        self.content_hash = content_hash
+        self.sample_shape = tuple(train_x.shape[1:])
+        self.n_train, self.n_test = int(train_x.shape[0]), int(test_x.shape[0])
+        self.train_x, self.train_y, self.test_x, self.test_y = train_x, train_y, test_x, test_y
+        self.max_label = int(max_label)
+        self._finish(device)
+        return self
+
+    def _finish(self, device):
+        torch = _torch()
+        self.identity = torch.arange(max(self.n_test, 1), dtype=torch.int32, device=device)
         self.nbytes = int(sum(t.numel() * t.element_size() for t in (self.train_x, self.train_y, self.test_x,
                                                                           self.test_y)))
 
@@ -200,8 +212,10 @@ class DeviceDataset:
 class Launch:
     """One C-ABI call with its device-resident problem table."""
 
-    def __init__(self, entry: str, args: tuple, table=None, label: str = ""):
+    def __init__(self, entry: str, args: tuple, table=None, label: str = "", flops: int = 0, nbytes: int = 0):
         self.entry, self.args, self.table, self.label = entry, args, table, label
+        # algorithmic work of one launch (all problems, full batches): the roofline numerators
+        self.flops, self.nbytes = flops, nbytes
 
     def run(self, stream) -> None:
         N.call(self.entry, *self.args, stream)
@@ -266,13 +280,24 @@ class DeviceHybrid:
     def _bind_buffers(self):
         torch = _torch()
         dev = self.device
+        # every model's input batch lives in one arena so a host-fed step is a single H2D copy
+        lds, xo, yo = [], [], []
+        xoff = yoff = 0
         for s in self.slots:
-            cap = s.batch_size
-            first = s.stages[0]
             sample = int(np.prod(s.sample_shape))
-            ld0 = _align4(sample) if first.kind == "dense" else sample
-            s.batch_x = torch.zeros(cap, ld0, dtype=torch.float32, device=dev)
-            s.batch_y = torch.zeros(cap, dtype=torch.int32, device=dev)
+            ld0 = _align4(sample) if s.stages[0].kind == "dense" else sample
+            lds.append(ld0)
+            xo.append(xoff)
+            yo.append(yoff)
+            xoff += _align4(s.batch_size * ld0)
+            yoff += _align4(s.batch_size)
+        self.batch_arena = torch.zeros(max(xoff, 4), dtype=torch.float32, device=dev)
+        self.label_arena = torch.zeros(max(yoff, 4), dtype=torch.int32, device=dev)
+        self.batch_layout = list(zip(xo, yo, lds))
+        for s, ld0, a, b in zip(self.slots, lds, xo, yo):
+            cap = s.batch_size
+            s.batch_x = self.batch_arena[a:a + cap * ld0].view(cap, ld0)
+            s.batch_y = self.label_arena[b:b + cap]
             prev_out, prev_ld = s.batch_x, ld0
             widest = ld0
             for st in s.stages:
@@ -404,7 +429,8 @@ class DeviceHybrid:
                 s.batch_size, s.index))
         t = _dev_table(N.GatherProblem, rows, self.device)
         cap = max(s.batch_size for s in self.slots)
-        return Launch("hnn_gather_rows", (_ptr(t), len(rows), cap, _ptr(self.cur)), t, "gather")
+        nbytes = sum(r.cap * (8 * r.sample + 8) for r in rows)
+        return Launch("hnn_gather_rows", (_ptr(t), len(rows), cap, _ptr(self.cur)), t, "gather", nbytes=nbytes)
 
     # ------------------------------------------------------------------ plans
     def _stage_waves(self):
@@ -447,13 +473,18 @@ class DeviceHybrid:
                 probs.append(N.GemmProblem(tile_base=base, tiles_n=tiles_n, model=s.index, **d))
                 base += tiles_m * tiles_n
             t = _dev_table(N.GemmProblem, probs, self.device)
+            flops = sum(2 * d["m"] * d["n"] * d["k"] for _, d in rows)
+            # bytes: A + B read once, C written once (fp32)
+            nbytes = sum(4 * (d["m"] * d["k"] + d["k"] * d["n"] + d["m"] * d["n"]) for _, d in rows)
             out.append(Launch("hnn_grouped_gemm", (op, prec, _ptr(t), len(probs), base, _ptr(self.cur),
-                                                   _ptr(self.status)), t, f"{label}/{'tc' if prec else 'simt'}"))
+                                                   _ptr(self.status)), t, f"{label}/{'tc' if prec else 'simt'}",
+                              flops=flops, nbytes=nbytes))
         return out
 
     def _conv_launch(self, op, items, label):
         tm, tn = N.conv_tile_shape(op)
         probs, base, red, rbase = [], 0, [], 0
+        flops = 0
         for s, st in items:
             c, h, w = st.in_shape
             f, oh, ow = self._conv_out(st)
@@ -482,9 +513,10 @@ class DeviceHybrid:
                 rbase += nblk
             probs.append(N.ConvProblem(tile_base=base, tiles_n=tiles_n, **common))
             base += tiles
+            flops += 2 * s.batch_size * oh * ow * f * c * k * k
         t = _dev_table(N.ConvProblem, probs, self.device)
         out = [Launch("hnn_grouped_conv", (op, _ptr(t), len(probs), base, _ptr(self.cur), _ptr(self.status)), t,
-                      label)]
+                      label, flops=flops)]
         if op == N.HNN_WGRAD:
             rt = _dev_table(N.ConvProblem, red, self.device)
             out.append(Launch("hnn_conv_wgrad_reduce", (_ptr(rt), len(red), rbase, _ptr(self.cur),
@@ -504,9 +536,10 @@ class DeviceHybrid:
                                        _ptr(st.x) if st.mask_input else 0, s.batch_size, c, h, w, k, stride, oh,
                                        ow, s.index, base, blocks, 0))
             base += blocks
+        nbytes = sum(4 * p.cap * p.c * (p.h * p.w + p.oh * p.ow) + p.cap * p.c * p.oh * p.ow for p in probs)
         t = _dev_table(N.PoolProblem, probs, self.device)
         return [Launch("hnn_grouped_maxpool", (op, _ptr(t), len(probs), base, _ptr(self.cur), _ptr(self.status)),
-                       t, label)]
+                       t, label, nbytes=nbytes)]
 
     def _relu_launch(self, op, items, label):
         probs, base = [], 0
@@ -516,8 +549,9 @@ class DeviceHybrid:
                                        s.index, base, blocks, 0))
             base += blocks
         t = _dev_table(N.ReluProblem, probs, self.device)
+        nbytes = sum((8 if op == N.HNN_FWD else 12) * p.cap * p.row for p in probs)
         return [Launch("hnn_grouped_relu", (op, _ptr(t), len(probs), base, _ptr(self.cur), _ptr(self.status)), t,
-                       label)]
+                       label, nbytes=nbytes)]
 
     def _wave_launches(self, op, items, label):
         by_kind: dict = {}
@@ -545,9 +579,10 @@ class DeviceHybrid:
         cap = max(s.batch_size for s in self.slots)
         ncls = max(s.classes for s in self.slots)
         status = self.status if train else self.eval_status
+        nbytes = sum(p.cap * (4 * p.classes * (2 if train else 1) + 4) for p in probs)
         return Launch("hnn_sce_fused", (_ptr(t), len(probs), cap, ncls, _ptr(self.cur), _ptr(status), int(train),
                                         _ptr(self.loss_out), _ptr(self.correct_out)), t,
-                      "sce" if train else "sce/eval")
+                      "sce" if train else "sce/eval", nbytes=nbytes)
 
     def _optimizer_launch(self):
         segs, base = [], 0
@@ -566,7 +601,10 @@ class DeviceHybrid:
             return []
         t = _dev_table(N.OptSegment, segs, self.device)
         entry = "hnn_multi_tensor_adam" if any(s.kind == N.OPT_ADAM for s in segs) else "hnn_multi_tensor_sgd"
-        return [Launch(entry, (_ptr(t), len(segs), base, _ptr(self.cur), _ptr(self.status)), t, "optimizer")]
+        per = {N.OPT_SGD: 12, N.OPT_SGD_MOMENTUM: 20, N.OPT_ADAM: 28}
+        nbytes = sum(per[s.kind] * s.count for s in segs)
+        return [Launch(entry, (_ptr(t), len(segs), base, _ptr(self.cur), _ptr(self.status)), t, "optimizer",
+                       nbytes=nbytes)]
 
     def build_plans(self):
         waves = self._stage_waves()
@@ -613,25 +651,32 @@ class DeviceHybrid:
         for launch in plan:
             launch.run(stream)
 
-    def train_steps(self, count: int, use_graph: bool = False):
-        """Run `count` scheduled training steps (stream-ordered, asynchronous)."""
+    def train_steps(self, count: int, use_graph: bool = False, host_fed: bool = False):
+        """Run `count` scheduled training steps (stream-ordered, asynchronous).
+
+        host_fed: the batch arenas were filled by the caller (H2D), so the gather is skipped.
+        """
+        plan = self.train_plan[1:] if host_fed else self.train_plan
         if not use_graph:
             for _ in range(count):
-                self.run_plan(self.train_plan)
+                self.run_plan(plan)
             return
         torch = _torch()
+        graphs = self.__dict__.setdefault("_graphs", {})
         if self.graph is None:
+            graphs.clear()
+            self.graph = True
+        g = graphs.get(host_fed)
+        if g is None:
             side = torch.cuda.Stream(self.device)
             side.wait_stream(torch.cuda.current_stream(self.device))
             g = torch.cuda.CUDAGraph()
-            saved = self.counter.clone()
             with torch.cuda.graph(g, stream=side):
-                self.run_plan(self.train_plan, side.cuda_stream)
+                self.run_plan(plan, side.cuda_stream)
             torch.cuda.current_stream(self.device).wait_stream(side)
-            self.counter.copy_(saved)  # capture did not execute anything, but keep it explicit
-            self.graph = g
+            graphs[host_fed] = g
         for _ in range(count):
-            self.graph.replay()
+            g.replay()
 
     def launch_count(self, train: bool = True) -> int:
         return 1 + len(self.train_plan if train else self.eval_plan)

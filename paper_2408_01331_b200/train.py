@@ -241,7 +241,7 @@ class Trainer:
                 continue
             key = ds.content_hash
             if key not in cache:
-                cache[key] = (self.comm.share_dataset(ds, dev.device) if self.comm is not None
+                cache[key] = (self.comm.share_dataset(ds, dev.device)[0] if self.comm is not None
                               else DeviceDataset(ds, dev.device))
             by_model[sub.slot] = cache[key]
         # models of the hybrid not trained by this Trainer borrow any dataset of the right shape
@@ -415,6 +415,73 @@ class Trainer:
         result.final_test_loss, result.final_test_accuracy = loss, acc
         if self.completion_sink is not None:
             self.completion_sink(job_id, self.hybrid.snapshot(), result)
+
+
+# --------------------------------------------------------------------------- host-fed steps
+
+
+class HostFedStepper:
+    """Step a materialised hybrid from HOST batches (the reference's run_batch contract, all jobs at once).
+
+    Each :meth:`step` copies one lockstep step's batches — every job's ``x`` and integer
+    labels, laid out like the device batch arena — from pinned host memory into HBM with
+    one H2D copy per arena, runs the step's kernels (no device gather), and copies the
+    per-job loss and correct count back to pinned host memory.  The schedule rows
+    (rows / lr / optimizer step) come from :meth:`DeviceHybrid.load_schedule` as usual.
+    """
+
+    def __init__(self, hybrid: HybridModel, datasets: dict, use_graph: bool = True):
+        import torch
+
+        self.hybrid, self.dev, self.use_graph = hybrid, hybrid.device, use_graph
+        if self.dev is None or not self.dev.train_plan:
+            raise StateError("materialise the hybrid and build its plans before host-fed stepping")
+        self.datasets = datasets
+        self.loss_host = torch.zeros(self.dev.n, dtype=torch.float32).pin_memory()
+        self.hits_host = torch.zeros(self.dev.n, dtype=torch.int32).pin_memory()
+        self.h2d_bytes_per_step = int(self.dev.batch_arena.numel() * 4 + self.dev.label_arena.numel() * 4)
+        self.d2h_bytes_per_step = int(self.dev.n * 8)
+
+    def stage_epoch_batches(self, ds, rows, count: int = 2, comm=None) -> list:
+        """Pinned host copies of the first `count` steps' batches (store.batches order, src/store.py:68-81)."""
+        import torch
+
+        from . import rng
+
+        dev = self.dev
+        staged = []
+        perms = {}
+        for t in range(count):
+            x = torch.zeros(dev.batch_arena.numel(), dtype=torch.float32).pin_memory()
+            y = torch.zeros(dev.label_arena.numel(), dtype=torch.int32).pin_memory()
+            xn, yn = x.numpy(), y.numpy()
+            for slot, (xo, yo, ld) in zip(dev.slots, dev.batch_layout):
+                d = self.datasets[slot.job_id]
+                if slot.index not in perms:
+                    perms[slot.index] = rng.permutation(d.sample_count, "shuffle", d.content_hash,
+                                                        self.hybrid.sub(slot.job_id).hypers.seed, 0)
+                r = rows[t, slot.index]
+                idx = perms[slot.index][r["perm_base"]:r["perm_base"] + r["rows"]]
+                sample = int(np.prod(slot.sample_shape))
+                blk = xn[xo:xo + slot.batch_size * ld].reshape(slot.batch_size, ld)
+                blk[: idx.size, :sample] = ds.train_x[idx].reshape(idx.size, sample)
+                yn[yo:yo + idx.size] = ds.train_y[idx].astype(np.int32)
+            staged.append((x, y))
+        return staged
+
+    def step(self, host_batch) -> None:
+        x, y = host_batch
+        self.dev.batch_arena.copy_(x, non_blocking=True)
+        self.dev.label_arena.copy_(y, non_blocking=True)
+        self.dev.train_steps(1, use_graph=self.use_graph, host_fed=True)
+        self.loss_host.copy_(self.dev.loss_out, non_blocking=True)
+        self.hits_host.copy_(self.dev.correct_out, non_blocking=True)
+
+    def finish(self) -> dict:
+        import torch
+
+        torch.cuda.current_stream().synchronize()
+        return {s.job_id: (float(self.loss_host[s.index]), int(self.hits_host[s.index])) for s in self.dev.slots}
 
 
 # --------------------------------------------------------------------------- evaluation
