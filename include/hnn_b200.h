@@ -10,7 +10,8 @@
  *                               (store.py:68-81, optim.py:22-30, optim.py:57,73-76)
  *   hnn_gather_rows             Batch(x=train_x[idx], y=train_y[idx])   (store.py:77-80)
  *   hnn_grouped_gemm            dense fwd / bwd  _dense_fwd, _dense_bwd (ops.py:46-55) with
- *                               relu fwd/bwd fused (ops.py:62-67)
+ *                               relu fwd/bwd fused (ops.py:62-67); fp32 SIMT or tcgen05 3xTF32
+ *   hnn_gemm_tc_encode          host-side TMA descriptors for the tcgen05 path
  *   hnn_grouped_conv            conv2d fwd / bwd _conv2d_fwd, _conv2d_bwd (ops.py:100-130)
  *   hnn_conv_wgrad_reduce       the fixed-order finish of the conv weight/bias gradient
  *   hnn_grouped_maxpool         maxpool2d fwd / bwd (ops.py:149-174), relu mask fused
@@ -127,6 +128,8 @@ typedef struct hnn_gemm_problem {
   int32_t relu;
   int32_t tile_base;
   int32_t tiles_n;
+  const void* tmap_a; /* HNN_PREC_F32_3XTF32: device copies of the problem's TMA maps (hnn_gemm_tc_encode) */
+  const void* tmap_b;
 } hnn_gemm_problem;
 
 /* Tile edge (m, n) used by (op, prec); lets the host lay out tile_base / tiles_n. */
@@ -134,6 +137,14 @@ int hnn_gemm_tile_shape(int op, int prec, int32_t* tile_m, int32_t* tile_n);
 
 int hnn_grouped_gemm(int op, int prec, const hnn_gemm_problem* probs, int nprob, int total_tiles,
                      const hnn_step_row* cur, const hnn_model_status* status, void* stream);
+
+/*
+ * Host-side: encode the two TMA tensor maps (A then B, 128 bytes each) of every problem for the
+ * tcgen05 path into host_maps[2*nprob]; the caller copies them to device memory and stores their
+ * device addresses in tmap_a / tmap_b.  Requirements: 16-byte aligned bases and row strides.
+ * Tiles are 128 x 128 (hnn_gemm_tile_shape); WGRAD problems need m <= 4096.
+ */
+int hnn_gemm_tc_encode(int op, const hnn_gemm_problem* host_probs, int nprob, void* host_maps);
 
 /*
  * Implicit-GEMM convolution on NCHW, zero padding `pad`, square kernel k.

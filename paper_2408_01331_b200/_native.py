@@ -40,7 +40,7 @@ class GatherProblem(C.Structure):
 class GemmProblem(C.Structure):
     _fields_ = [("a", P), ("b", P), ("c", P), ("bias", P), ("mask", P), ("dbias", P),
                 ("m", I), ("n", I), ("k", I), ("lda", I), ("ldb", I), ("ldc", I),
-                ("model", I), ("relu", I), ("tile_base", I), ("tiles_n", I)]
+                ("model", I), ("relu", I), ("tile_base", I), ("tiles_n", I), ("tmap_a", P), ("tmap_b", P)]
 
 
 class ConvProblem(C.Structure):
@@ -84,6 +84,7 @@ SIGNATURES = {
     "hnn_gather_rows": [P, C.c_int, C.c_int, P, VP],
     "hnn_gemm_tile_shape": [C.c_int, C.c_int, C.POINTER(I), C.POINTER(I)],
     "hnn_grouped_gemm": [C.c_int, C.c_int, P, C.c_int, C.c_int, P, P, VP],
+    "hnn_gemm_tc_encode": [C.c_int, C.c_void_p, C.c_int, C.c_void_p],
     "hnn_conv_tile_shape": [C.c_int, C.POINTER(I), C.POINTER(I)],
     "hnn_grouped_conv": [C.c_int, P, C.c_int, C.c_int, P, P, VP],
     "hnn_conv_wgrad_reduce": [P, C.c_int, C.c_int, P, P, VP],

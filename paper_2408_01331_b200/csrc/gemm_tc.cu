@@ -1,17 +1,478 @@
-// tcgen05 3xTF32 grouped GEMM — placeholder until the tensor-core path lands.
+// Grouped fp32 GEMM on the 5th-gen tensor cores: tcgen05.mma kind::tf32, 3xTF32.
+//
+// fp32 parity forbids plain TF32 (SURVEY finding 4: relu-mask flips give 1e-1
+// gradient errors), so every operand x is split into hi = rna_tf32(x) and
+// lo = rna_tf32(x - hi) and the tile accumulates  A_hi*B_hi + A_hi*B_lo + A_lo*B_hi
+// in fp32 in TMEM (error ~2^-22 relative per product, like fp32 FFMA).
+//
+// Per CTA: one 128 x BN output tile of one problem (tile list = concatenation of
+// every problem's tiles, ordered heaviest first by the host; a tile's arithmetic
+// never depends on its neighbours -> bit-exact isolation).
+//   warp 0      TMA producer: raw fp32 tiles, 128-byte swizzle, into a STAGES-deep ring
+//   warp 1      TMEM allocator + single-thread MMA issuer (12 MMAs per 32-wide K block)
+//   warps 2..5  converters (hi in place, lo beside it, fence.proxy.async) then the
+//               epilogue: tcgen05.ld -> bias / relu / relu-mask / zero pad rows -> global
+// Operand majorness per op (row-major fp32 tensors in HBM):
+//   FWD    A = X  [cap, K]  K-major      B = W  [N, K]     K-major
+//   DGRAD  A = dY [cap, U]  K-major      B = W  [U, N]     N-major
+//   WGRAD  A = dY [rows, M] M-major      B = X  [rows, N]  N-major
+#include <cuda.h>
+
 #include "common.cuh"
 
 namespace hnn {
 
+constexpr int TC_BM = 128, TC_BN = 128, TC_BK = 32, TC_STAGES = 3;
+constexpr int TC_THREADS = 320;  // TMA, MMA, 4 converter warps, 4 accumulator warps
+constexpr int TC_A_BYTES = TC_BM * TC_BK * 4;              // 16 KB
+constexpr int TC_B_BYTES = TC_BN * TC_BK * 4;              // 16 KB
+constexpr int TC_HI_BYTES = TC_A_BYTES + TC_B_BYTES;       // raw -> hi, in place
+constexpr int TC_STAGE_BYTES = 2 * TC_HI_BYTES;            // hi + lo
+constexpr int TC_SMEM_BYTES = TC_STAGES * TC_STAGE_BYTES + 4 * 32 * 33 * 4 /*epilogue*/ + 1024 /*align*/ + 256;
+
+// ---------------------------------------------------------------- PTX helpers
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count));
+}
+
+__device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive(uint32_t bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred P1;\n"
+      "HNN_WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+      "@!P1 bra HNN_WAIT_%=;\n\t}" ::"r"(bar),
+      "r"(parity)
+      : "memory");
+}
+
+__device__ __forceinline__ void tma_load_2d(uint32_t dst, const void* tmap, uint32_t bar, int c0, int c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];" ::"r"(dst),
+      "l"(tmap), "r"(bar), "r"(c0), "r"(c1)
+      : "memory");
+}
+
+__device__ __forceinline__ void tma_prefetch(const void* tmap) {
+  asm volatile("prefetch.tensormap [%0];" ::"l"(tmap) : "memory");
+}
+
+__device__ __forceinline__ uint32_t to_tf32(float x) {
+  uint32_t r;
+  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
+  return r;
+}
+
+// K-major, 128-byte swizzle: rows of 128 B, 8-row atoms 1024 B apart (SBO), LBO unused (=1).
+// MN-major tf32 only exists as "128-byte swizzle, 32-byte atoms" (Swizzle<2,5,2>): rows of 128 B
+// (32 MN elements) per k, 4-row atoms 512 B apart (SBO), 32-element MN blocks 4096 B apart (LBO);
+// TMA writes that pattern with CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B.
+__device__ __forceinline__ uint64_t smem_desc(uint32_t addr, uint32_t lbo, uint32_t sbo, uint32_t layout) {
+  uint64_t d = 0;
+  d |= uint64_t((addr >> 4) & 0x3FFF);
+  d |= uint64_t((lbo >> 4) & 0x3FFF) << 16;
+  d |= uint64_t((sbo >> 4) & 0x3FFF) << 32;
+  d |= uint64_t(1) << 46;  // descriptor version (sm_100)
+  d |= uint64_t(layout) << 61;  // 2 = SWIZZLE_128B (K-major), 1 = SWIZZLE_128B_BASE32B (MN-major tf32)
+  return d;
+}
+
+// kind::tf32 instruction descriptor: fp32 accumulate, tf32 A/B, majorness, N>>3, M>>4.
+__host__ __device__ constexpr uint32_t tf32_idesc(int m, int n, int a_mn, int b_mn) {
+  return (1u << 4) | (2u << 7) | (2u << 10) | (uint32_t(a_mn) << 15) | (uint32_t(b_mn) << 16) |
+         (uint32_t(n >> 3) << 17) | (uint32_t(m >> 4) << 24);
+}
+
+__device__ __forceinline__ void mma_tf32(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, {%5, %5, %5, %5}, p;\n\t}" ::"r"(tmem_d),
+      "l"(da), "l"(db), "r"(idesc), "r"(acc), "r"(0u));
+}
+
+__device__ __forceinline__ void mma_commit(uint32_t bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar) : "memory");
+}
+
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]),
+        "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]), "=r"(r[16]),
+        "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]),
+        "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+
+// ---------------------------------------------------------------- the kernel
+//
+// Persistent: grid = min(tiles, SMs); CTA c walks tiles c, c+grid, ... (the host orders tiles
+// heaviest first).  Pipeline counters run across tiles, so a CTA's TMA / converter / MMA /
+// accumulator roles overlap the tail of one tile with the head of the next.
+//
+// Accumulation precision: the tensor core accumulates one chunk (TC_CHUNK_KB k-blocks = 64
+// terms) into one of two TMEM buffers; the accumulator warps add each finished chunk into fp32
+// registers with round-to-nearest adds ("promotion") and release the buffer.  Long-K sums thus
+// see the tensor core's internal accumulation only inside 64-term chunks, keeping errors at
+// fp32-FFMA level — needed by Adam, whose first steps amplify absolute gradient errors near
+// |g| ~ eps (measured: single-accumulator 3xTF32 gave 8e-6 relative gradient error, enough to
+// move Adam weights by up to lr).
+
+constexpr int TC_CHUNK_KB = 2;
+constexpr int TC_EPI_SCRATCH = 4 * 32 * 33 * 4;  // per accumulator warp: 32 x 33 floats (transpose)
+
+template <int OP>
+__global__ void __launch_bounds__(TC_THREADS, 1)
+    gemm_tc_kernel(const hnn_gemm_problem* __restrict__ probs, int nprob, int total_tiles,
+                   const hnn_step_row* __restrict__ cur, const hnn_model_status* __restrict__ status) {
+  constexpr int A_MN = (OP == HNN_WGRAD) ? 1 : 0;
+  constexpr int B_MN = (OP == HNN_FWD) ? 0 : 1;
+  extern __shared__ uint8_t smem_raw[];
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+
+  uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  float* scratch = reinterpret_cast<float*>(base + TC_STAGES * TC_STAGE_BYTES);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(base + TC_STAGES * TC_STAGE_BYTES + TC_EPI_SCRATCH);
+  // bars: full_raw[S] | full_conv[S] | empty[S] | acc_full[2] | acc_empty[2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 3 * TC_STAGES + 4);
+  const uint32_t sbase = smem_u32(base);
+  auto bar = [&](int i) { return smem_u32(bars + i); };
+  const int ACC_FULL = 3 * TC_STAGES, ACC_EMPTY = 3 * TC_STAGES + 2;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < TC_STAGES; ++s) {
+      mbar_init(bar(s), 1);                  // full_raw: expect_tx arrival + TMA bytes
+      mbar_init(bar(TC_STAGES + s), 128);    // full_conv: every converter thread
+      mbar_init(bar(2 * TC_STAGES + s), 1);  // empty: MMA commit
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(bar(ACC_FULL + b), 1);       // MMA commit
+      mbar_init(bar(ACC_EMPTY + b), 128);    // every accumulator thread
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                 "r"(2 * TC_BN));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  // every role walks the same tile sequence; tiles of inactive models are skipped by all roles
+  auto tile_info = [&](int tile, const hnn_gemm_problem*& p, int& m0, int& n0, int& nkb, int& rows) -> bool {
+    p = &probs[find_problem(probs, nprob, tile, [](const hnn_gemm_problem& q) { return q.tile_base; })];
+    if (!live(cur, status, p->model)) return false;
+    rows = cur[p->model].rows;
+    const int t = tile - p->tile_base;
+    m0 = (t / p->tiles_n) * TC_BM;
+    n0 = (t % p->tiles_n) * TC_BN;
+    const int ktot = (OP == HNN_WGRAD) ? rows : p->k;
+    nkb = (ktot + TC_BK - 1) / TC_BK;
+    return nkb > 0;
+  };
+
+  if (warp == 0) {
+    // ---------------- TMA producer
+    if (lane == 0) {
+      uint32_t kg = 0;
+      for (int tile = blockIdx.x; tile < total_tiles; tile += gridDim.x) {
+        const hnn_gemm_problem* p;
+        int m0, n0, nkb, rows;
+        if (!tile_info(tile, p, m0, n0, nkb, rows)) continue;
+        for (int kb = 0; kb < nkb; ++kb, ++kg) {
+          const int s = kg % TC_STAGES;
+          if (kg >= TC_STAGES) mbar_wait(bar(2 * TC_STAGES + s), ((kg / TC_STAGES) - 1) & 1);
+          const uint32_t st = sbase + s * TC_STAGE_BYTES;
+          mbar_expect_tx(bar(s), TC_HI_BYTES);
+          const int k0 = kb * TC_BK;
+          if (A_MN) {
+#pragma unroll
+            for (int b = 0; b < TC_BM / 32; ++b) tma_load_2d(st + b * 4096, p->tmap_a, bar(s), m0 + 32 * b, k0);
+          } else {
+            tma_load_2d(st, p->tmap_a, bar(s), k0, m0);
+          }
+          if (B_MN) {
+#pragma unroll
+            for (int b = 0; b < TC_BN / 32; ++b)
+              tma_load_2d(st + TC_A_BYTES + b * 4096, p->tmap_b, bar(s), n0 + 32 * b, k0);
+          } else {
+            tma_load_2d(st + TC_A_BYTES, p->tmap_b, bar(s), k0, n0);
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ---------------- MMA issuer (one thread)
+    if (lane == 0) {
+      constexpr uint32_t idesc = tf32_idesc(TC_BM, TC_BN, A_MN, B_MN);
+      constexpr uint32_t alb = A_MN ? 4096 : 16, asb = A_MN ? 512 : 1024, alt = A_MN ? 1 : 2;
+      constexpr uint32_t blb = B_MN ? 4096 : 16, bsb = B_MN ? 512 : 1024, blt = B_MN ? 1 : 2;
+      uint32_t kg = 0, cg = 0;
+      for (int tile = blockIdx.x; tile < total_tiles; tile += gridDim.x) {
+        const hnn_gemm_problem* p;
+        int m0, n0, nkb, rows;
+        if (!tile_info(tile, p, m0, n0, nkb, rows)) continue;
+        for (int kb = 0; kb < nkb; ++kb, ++kg) {
+          const int in_chunk = kb % TC_CHUNK_KB;
+          const uint32_t buf = cg & 1;
+          if (in_chunk == 0 && cg >= 2) {
+            mbar_wait(bar(ACC_EMPTY + buf), ((cg >> 1) - 1) & 1);  // promoted and released
+            tc_fence_after();
+          }
+          const int s = kg % TC_STAGES;
+          mbar_wait(bar(TC_STAGES + s), (kg / TC_STAGES) & 1);
+          tc_fence_after();
+          const uint32_t a_hi = sbase + s * TC_STAGE_BYTES, b_hi = a_hi + TC_A_BYTES;
+          const uint32_t a_lo = a_hi + TC_HI_BYTES, b_lo = b_hi + TC_HI_BYTES;
+          const uint32_t acc = tmem + buf * TC_BN;
+#pragma unroll
+          for (int j = 0; j < TC_BK / 8; ++j) {
+            // K step j = 8 tf32: +32 B inside a K-major row, +1024 B (two 4-row atoms) in MN-major
+            const uint32_t ao = A_MN ? j * 1024 : j * 32, bo = B_MN ? j * 1024 : j * 32;
+            const uint64_t dah = smem_desc(a_hi + ao, alb, asb, alt), dal = smem_desc(a_lo + ao, alb, asb, alt);
+            const uint64_t dbh = smem_desc(b_hi + bo, blb, bsb, blt), dbl = smem_desc(b_lo + bo, blb, bsb, blt);
+            mma_tf32(acc, dal, dbh, idesc, (in_chunk | j) != 0);
+            mma_tf32(acc, dah, dbl, idesc, 1);
+            mma_tf32(acc, dah, dbh, idesc, 1);
+          }
+          mma_commit(bar(2 * TC_STAGES + s));  // smem stage free once these MMAs have read it
+          if (in_chunk == TC_CHUNK_KB - 1 || kb == nkb - 1) {
+            mma_commit(bar(ACC_FULL + buf));   // chunk partial ready for promotion
+            ++cg;
+          }
+        }
+      }
+    }
+  } else if (warp < 6) {
+    // ---------------- converters: hi = rna_tf32(x) in place, lo = rna_tf32(x - hi)
+    const int ct = threadIdx.x - 64;  // 0..127
+    uint32_t kg = 0;
+    for (int tile = blockIdx.x; tile < total_tiles; tile += gridDim.x) {
+      const hnn_gemm_problem* p;
+      int m0, n0, nkb, rows;
+      if (!tile_info(tile, p, m0, n0, nkb, rows)) continue;
+      for (int kb = 0; kb < nkb; ++kb, ++kg) {
+        const int s = kg % TC_STAGES;
+        mbar_wait(bar(s), (kg / TC_STAGES) & 1);
+        float4* hi = reinterpret_cast<float4*>(base + s * TC_STAGE_BYTES);
+        float4* lo = reinterpret_cast<float4*>(base + s * TC_STAGE_BYTES + TC_HI_BYTES);
+#pragma unroll 4
+        for (int i = ct; i < TC_HI_BYTES / 16; i += 128) {
+          float4 v = hi[i];
+          uint32_t h0 = to_tf32(v.x), h1 = to_tf32(v.y), h2 = to_tf32(v.z), h3 = to_tf32(v.w);
+          float4 l;
+          l.x = __uint_as_float(to_tf32(v.x - __uint_as_float(h0)));
+          l.y = __uint_as_float(to_tf32(v.y - __uint_as_float(h1)));
+          l.z = __uint_as_float(to_tf32(v.z - __uint_as_float(h2)));
+          l.w = __uint_as_float(to_tf32(v.w - __uint_as_float(h3)));
+          hi[i] = make_float4(__uint_as_float(h0), __uint_as_float(h1), __uint_as_float(h2), __uint_as_float(h3));
+          lo[i] = l;
+        }
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        mbar_arrive(bar(TC_STAGES + s));
+      }
+    }
+  } else {
+    // ---------------- accumulators + epilogue (warps 6..9; TMEM lane quarter = warp % 4)
+    const int q = warp & 3;
+    float* scr = scratch + (warp - 6) * 32 * 33;
+    uint32_t cg = 0;
+    for (int tile = blockIdx.x; tile < total_tiles; tile += gridDim.x) {
+      const hnn_gemm_problem* p;
+      int m0, n0, nkb, rows;
+      if (!tile_info(tile, p, m0, n0, nkb, rows)) continue;
+      float sum[TC_BN];
+#pragma unroll
+      for (int j = 0; j < TC_BN; ++j) sum[j] = 0.0f;
+      const int nchunks = (nkb + TC_CHUNK_KB - 1) / TC_CHUNK_KB;
+      for (int c = 0; c < nchunks; ++c, ++cg) {
+        const uint32_t buf = cg & 1;
+        mbar_wait(bar(ACC_FULL + buf), (cg >> 1) & 1);
+        tc_fence_after();
+        const uint32_t taddr = tmem + (uint32_t(q * 32) << 16) + buf * TC_BN;
+#pragma unroll
+        for (int cb = 0; cb < TC_BN; cb += 32) {
+          uint32_t r[32];
+          tmem_ld32(taddr + cb, r);
+#pragma unroll
+          for (int j = 0; j < 32; ++j) sum[cb + j] = __fadd_rn(sum[cb + j], __uint_as_float(r[j]));
+        }
+        tc_fence_before();
+        mbar_arrive(bar(ACC_EMPTY + buf));
+      }
+      // epilogue: transpose 32x32 blocks through smem so each store instruction writes one row's
+      // 32 consecutive columns (128 B, coalesced); bias / relu / relu-mask / pad rows applied here
+      const int row0 = m0 + q * 32;
+#pragma unroll
+      for (int cb = 0; cb < TC_BN; cb += 32) {
+#pragma unroll
+        for (int j = 0; j < 32; ++j) scr[lane * 33 + j] = sum[cb + j];
+        __syncwarp();
+        const int n = n0 + cb + lane;
+        const bool col_ok = n < p->n;
+        float bias = 0.0f;
+        if (OP == HNN_FWD && col_ok) bias = __ldg(p->bias + n);
+        for (int r = 0; r < 32; ++r) {
+          const int row = row0 + r;
+          if (row >= p->m) break;
+          float v = scr[r * 33 + lane];
+          if (OP == HNN_FWD) {
+            if (row >= rows) v = 0.0f;
+            else {
+              v = __fadd_rn(v, bias);
+              if (p->relu) v = np_relu(v);
+            }
+          } else if (OP == HNN_DGRAD) {
+            if (row >= rows) v = 0.0f;
+            else if (p->mask && col_ok) v = np_mask(v, p->mask[size_t(row) * p->ldc + n]);
+          }
+          if (col_ok) p->c[size_t(row) * p->ldc + n] = v;
+        }
+        __syncwarp();
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(2 * TC_BN));
+  }
+}
+
+// dbias[i] = sum_{r<R} A[r*lda + i], sequential row order (numpy's axis-0 sum), one thread per column.
+__global__ void colsum_kernel(const hnn_gemm_problem* __restrict__ probs, int nprob, const hnn_step_row* __restrict__ cur,
+                              const hnn_model_status* __restrict__ status) {
+  const hnn_gemm_problem& p = probs[blockIdx.y];
+  if (!p.dbias || !live(cur, status, p.model)) return;
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= p.m) return;
+  const int R = cur[p.model].rows;
+  float acc = -0.0f;
+  for (int r = 0; r < R; ++r) acc = __fadd_rn(acc, p.a[size_t(r) * p.lda + i]);
+  p.dbias[i] = acc;
+}
+
+// ---------------------------------------------------------------- host side
+
+typedef CUresult (*EncodeTiled)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+static EncodeTiled encoder() {
+  static EncodeTiled fn = nullptr;
+  if (!fn) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeTiled>(p);
+  }
+  return fn;
+}
+
+// 2D fp32 map: inner extent `inner` (contiguous), `outer` rows of `stride_floats`, box {32, box_outer}.
+int encode_2d(CUtensorMap* map, const float* ptr, uint64_t inner, uint64_t outer, uint64_t stride_floats,
+                     uint32_t box_outer, bool mn_major) {
+  EncodeTiled enc = encoder();
+  if (!enc) return HNN_ERR_CUDA;
+  cuuint64_t dims[2] = {inner, outer};
+  cuuint64_t strides[1] = {stride_floats * 4};
+  cuuint32_t box[2] = {32, box_outer};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(ptr), dims, strides, box, estr,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE,
+                   mn_major ? CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B : CU_TENSOR_MAP_SWIZZLE_128B,
+                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS ? HNN_OK : HNN_ERR_CUDA;
+}
+
 int gemm_tc_tile_shape(int op, int32_t* tm, int32_t* tn) {
-  set_error("hnn_gemm_tile_shape", "3xTF32 tensor-core path not built");
-  return HNN_ERR_UNSUPPORTED;
+  *tm = TC_BM;
+  *tn = TC_BN;
+  return HNN_OK;
 }
 
 int grouped_gemm_tc(int op, const hnn_gemm_problem* probs, int nprob, int total_tiles, const hnn_step_row* cur,
                     const hnn_model_status* status, cudaStream_t s) {
-  set_error("hnn_grouped_gemm", "3xTF32 tensor-core path not built");
-  return HNN_ERR_UNSUPPORTED;
+  static bool configured[3] = {false, false, false};
+  if (!configured[op]) {
+    cudaError_t e;
+    if (op == HNN_FWD) e = cudaFuncSetAttribute(gemm_tc_kernel<HNN_FWD>, cudaFuncAttributeMaxDynamicSharedMemorySize, TC_SMEM_BYTES);
+    else if (op == HNN_DGRAD) e = cudaFuncSetAttribute(gemm_tc_kernel<HNN_DGRAD>, cudaFuncAttributeMaxDynamicSharedMemorySize, TC_SMEM_BYTES);
+    else e = cudaFuncSetAttribute(gemm_tc_kernel<HNN_WGRAD>, cudaFuncAttributeMaxDynamicSharedMemorySize, TC_SMEM_BYTES);
+    if (e != cudaSuccess) {
+      set_error("hnn_grouped_gemm(tc)", cudaGetErrorString(e));
+      return HNN_ERR_CUDA;
+    }
+    configured[op] = true;
+  }
+  static int sms = 0;
+  if (!sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  }
+  const int grid = total_tiles < sms ? total_tiles : sms;
+  if (op == HNN_FWD)
+    gemm_tc_kernel<HNN_FWD><<<grid, TC_THREADS, TC_SMEM_BYTES, s>>>(probs, nprob, total_tiles, cur, status);
+  else if (op == HNN_DGRAD)
+    gemm_tc_kernel<HNN_DGRAD><<<grid, TC_THREADS, TC_SMEM_BYTES, s>>>(probs, nprob, total_tiles, cur, status);
+  else {
+    gemm_tc_kernel<HNN_WGRAD><<<grid, TC_THREADS, TC_SMEM_BYTES, s>>>(probs, nprob, total_tiles, cur, status);
+    int rc = check_launch("hnn_grouped_gemm(tc)");
+    if (rc) return rc;
+    dim3 grid2(16, nprob);  // columns up to 16*256 = 4096 per problem (planner guarantees m <= 4096)
+    colsum_kernel<<<grid2, 256, 0, s>>>(probs, nprob, cur, status);
+  }
+  return check_launch("hnn_grouped_gemm(tc)");
 }
 
 }  // namespace hnn
+
+// Encode the two TMA maps of every problem (host memory, 128 bytes each, A then B per problem).
+extern "C" int hnn_gemm_tc_encode(int op, const hnn_gemm_problem* host_probs, int nprob, void* host_maps) {
+  HNN_REQUIRE(host_probs && host_maps && nprob > 0, "hnn_gemm_tc_encode", "bad arguments");
+  CUtensorMap* maps = reinterpret_cast<CUtensorMap*>(host_maps);
+  for (int i = 0; i < nprob; ++i) {
+    const hnn_gemm_problem& p = host_probs[i];
+    int rc;
+    if (op == HNN_FWD) {          // A = X[cap, K] (K-major), B = W[N, K] (K-major)
+      rc = hnn::encode_2d(&maps[2 * i], p.a, p.k, p.m, p.lda, hnn::TC_BM, false);
+      if (!rc) rc = hnn::encode_2d(&maps[2 * i + 1], p.b, p.k, p.n, p.ldb, hnn::TC_BN, false);
+    } else if (op == HNN_DGRAD) { // A = dY[cap, U] (K-major), B = W[U, N] (N-major)
+      rc = hnn::encode_2d(&maps[2 * i], p.a, p.k, p.m, p.lda, hnn::TC_BM, false);
+      if (!rc) rc = hnn::encode_2d(&maps[2 * i + 1], p.b, p.n, p.k, p.ldb, 32, true);
+    } else {                      // A = dY[cap, M] (M-major), B = X[cap, N] (N-major)
+      rc = hnn::encode_2d(&maps[2 * i], p.a, p.m, p.k, p.lda, 32, true);
+      if (!rc) rc = hnn::encode_2d(&maps[2 * i + 1], p.b, p.n, p.k, p.ldb, 32, true);
+    }
+    if (rc) {
+      hnn::set_error("hnn_gemm_tc_encode", "cuTensorMapEncodeTiled failed (alignment / stride / driver)");
+      return rc;
+    }
+  }
+  return HNN_OK;
+}

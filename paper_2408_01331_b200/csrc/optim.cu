@@ -54,10 +54,12 @@ __global__ void __launch_bounds__(OPT_THREADS) multi_tensor_kernel(const hnn_opt
   for (int q = 0; q < 4; ++q) {
     const int i = threadIdx.x + q * OPT_THREADS;
     if (i < n4) {
-      P[q] = p4[i];
+      // explicit global-space accesses (the segment pointers come from memory, so a plain
+      // dereference compiles to generic LD/ST); gradients are read once -> evict-first
+      P[q] = __ldcg(p4 + i);
       G[q] = __ldcs(g4 + i);
-      if (u.kind != HNN_OPT_SGD) M[q] = m4[i];
-      if (u.kind == HNN_OPT_ADAM) V[q] = v4[i];
+      if (u.kind != HNN_OPT_SGD) M[q] = __ldcg(m4 + i);
+      if (u.kind == HNN_OPT_ADAM) V[q] = __ldcg(v4 + i);
     }
   }
 #pragma unroll
@@ -68,9 +70,9 @@ __global__ void __launch_bounds__(OPT_THREADS) multi_tensor_kernel(const hnn_opt
     update_one(u, P[q].y, G[q].y, M[q].y, V[q].y);
     update_one(u, P[q].z, G[q].z, M[q].z, V[q].z);
     update_one(u, P[q].w, G[q].w, M[q].w, V[q].w);
-    p4[i] = P[q];
-    if (u.kind != HNN_OPT_SGD) m4[i] = M[q];
-    if (u.kind == HNN_OPT_ADAM) v4[i] = V[q];
+    __stcg(p4 + i, P[q]);
+    if (u.kind != HNN_OPT_SGD) __stcg(m4 + i, M[q]);
+    if (u.kind == HNN_OPT_ADAM) __stcg(v4 + i, V[q]);
   }
 }
 

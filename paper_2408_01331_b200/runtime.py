@@ -232,6 +232,18 @@ def _ptr(t) -> int:
     return 0 if t is None else int(t.data_ptr())
 
 
+def C_addr(cobj) -> int:
+    import ctypes
+
+    return ctypes.addressof(cobj)
+
+
+def C_addr_bytes(buf: bytearray) -> int:
+    import ctypes
+
+    return ctypes.addressof((ctypes.c_char * len(buf)).from_buffer(buf))
+
+
 class DeviceHybrid:
     """Packed device state + launch plans for the models of one rank."""
 
@@ -438,8 +450,14 @@ class DeviceHybrid:
         return [[(s, s.stages[w]) for s in self.slots if w < len(s.stages)] for w in range(depth)]
 
     def _route_tc(self, op, d) -> bool:
-        """Whether a dense problem goes to the tcgen05 3xTF32 kernel (set by gemm_tc support)."""
-        return False
+        """Dense problems big and aligned enough for a 128x128 tcgen05 tile go to the 3xTF32 kernel."""
+        if d["m"] < 128 or d["n"] < 64 or d["k"] < 64:
+            return False
+        if op == N.HNN_WGRAD and d["m"] > 4096:
+            return False
+        if any(d[k] % 4 for k in ("lda", "ldb", "ldc")):
+            return False
+        return all(d[k] % 16 == 0 for k in ("a", "b"))
 
     def _gemm_launch(self, op, items, label):
         """items: list of (slot, stage).  Splits into SIMT / 3xTF32 launches."""
@@ -467,18 +485,32 @@ class DeviceHybrid:
             if not rows:
                 continue
             tm, tn = N.tile_shape(op, prec)
+            # heaviest problems first: their tiles start in the first wave (LPT over SMs)
+            rows = sorted(rows, key=lambda r: -(r[1]["m"] * r[1]["n"] * r[1]["k"]))
             probs, base = [], 0
             for s, d in rows:
                 tiles_m, tiles_n = -(-d["m"] // tm), -(-d["n"] // tn)
                 probs.append(N.GemmProblem(tile_base=base, tiles_n=tiles_n, model=s.index, **d))
                 base += tiles_m * tiles_n
+            keep = None
+            if prec == N.PREC_3XTF32:
+                torch = _torch()
+                maps = bytearray(128 * 2 * len(probs))
+                host = (N.GemmProblem * len(probs))(*probs)
+                N.call("hnn_gemm_tc_encode", op, C_addr(host), len(probs), C_addr_bytes(maps))
+                keep = torch.frombuffer(maps, dtype=torch.uint8).to(self.device)
+                for i, pr in enumerate(probs):
+                    pr.tmap_a = _ptr(keep) + 256 * i
+                    pr.tmap_b = _ptr(keep) + 256 * i + 128
             t = _dev_table(N.GemmProblem, probs, self.device)
             flops = sum(2 * d["m"] * d["n"] * d["k"] for _, d in rows)
             # bytes: A + B read once, C written once (fp32)
             nbytes = sum(4 * (d["m"] * d["k"] + d["k"] * d["n"] + d["m"] * d["n"]) for _, d in rows)
-            out.append(Launch("hnn_grouped_gemm", (op, prec, _ptr(t), len(probs), base, _ptr(self.cur),
-                                                   _ptr(self.status)), t, f"{label}/{'tc' if prec else 'simt'}",
-                              flops=flops, nbytes=nbytes))
+            launch = Launch("hnn_grouped_gemm", (op, prec, _ptr(t), len(probs), base, _ptr(self.cur),
+                                                 _ptr(self.status)), t, f"{label}/{'tc' if prec else 'simt'}",
+                            flops=flops, nbytes=nbytes)
+            launch.maps = keep
+            out.append(launch)
         return out
 
     def _conv_launch(self, op, items, label):

@@ -145,9 +145,13 @@ def test_trajectory_matches_reference(pkg, name):
     step_err = np.max(np.abs(np.asarray(losses) - ref_losses) / np.abs(ref_losses))
     assert step_err <= REL_STEP * 10, step_err  # whole-trajectory drift after many steps
     assert abs(losses[0] - ref_losses[0]) / abs(ref_losses[0]) <= REL_STEP
-    # step 0 weights (one update from identical init): the per-step criterion
+    # step 0 weights (one update from identical init): the per-step criterion.  Adam's first
+    # update lr*g/(|g|+eps) amplifies absolute gradient noise where |g| ~ eps: the reference
+    # itself moves fc2.weight of c3_mlp by 6.3e-5 (rel) between 1 and 2 BLAS threads, so Adam
+    # weights get 3x that allowance; gradients are checked at 1e-5 in test_step_gradients_match_oracle
+    tol = REL_STEP if c["opt"] == "sgd" else 3 * REL_STEP
     for pid in graph_pids(arr, "step0"):
-        assert rel(step0[pid], arr[f"step0/{pid}"]) <= REL_STEP, pid
+        assert rel(step0[pid], arr[f"step0/{pid}"]) <= tol, (pid, rel(step0[pid], arr[f"step0/{pid}"]))
     _, params = pkg.separate(h, name)
     for pid in graph_pids(arr, "final"):
         assert rel(params[pid], arr[f"final/{pid}"]) <= REL_STEP * 10, (pid, rel(params[pid], arr[f"final/{pid}"]))
@@ -313,3 +317,55 @@ def test_separation_layout_and_roundtrip(pkg):
         assert not np.array_equal(pkg.separate(h, job.job_id)[1][next(iter(params))], params[next(iter(params))])
     with pytest.raises(pkg.UnknownJobError):
         pkg.separate(h, "nope")
+
+
+def _first_step_grads(pkg, name, tc):
+    arr, c, graph, splits, digest = load_case(name)
+    from paper_2408_01331_b200 import store
+
+    ds = store.from_splits(splits)
+    job = pkg.TrainingJob(name, graph, digest, pkg.HyperParams(1, c["batch"], c["lr"], c["opt"], (), c["seed"]), 0, 0)
+    h = pkg.merge([job])
+    grabbed = {}
+    tr = pkg.Trainer(h, pkg.make_plan("fcfs", [job]), [job], {name: ds}, use_tensor_cores=tc)
+    tr.step_observer = lambda j, p: grabbed or grabbed.update(
+        grads=tr.device.download_grads(0), params={k.split("/", 1)[1]: v for k, v in p.items()})
+    tr.run()
+    return grabbed, [l.label for l in tr.device.train_plan], (arr, c, graph, splits, digest)
+
+
+@pytest.mark.parametrize("name", ["c3_mlp", "c1_mlp", "lenet"])
+def test_step_gradients_match_oracle(pkg, name):
+    """Gradients of the first step (tensor-core path where routed) vs the oracle: rel <= 1e-5."""
+    got, labels, (arr, c, graph, splits, digest) = _first_step_grads(pkg, name, True)
+    params = oracle.init_model(graph, c["seed"])
+    bx, by, _ = oracle.epoch_batches(splits["train_x"], splits["train_y"], digest, c["batch"], c["seed"], 0)[0]
+    logits, tape = oracle.model_forward(graph, params, bx)
+    _, dl = oracle.sce_loss_and_grad(logits, by)
+    ref = oracle.model_backward(tape, dl)
+    for pid, g in ref.items():
+        assert rel(got["grads"][pid], g) <= 1e-5, (name, pid, rel(got["grads"][pid], g))
+    if name == "c3_mlp":
+        assert any(l.endswith("/tc") for l in labels)
+
+
+@pytest.mark.parametrize("name", ["c3_mlp", "c1_mlp", "deep_adam"])
+def test_optimizer_is_bit_exact_given_gradients(pkg, name):
+    """The multi-tensor SGD/Adam kernel reproduces apply_update bit for bit (src/optim.py:52-87)."""
+    got, _, (arr, c, graph, splits, digest) = _first_step_grads(pkg, name, True)
+    params = oracle.init_model(graph, c["seed"])
+    opt = oracle.OracleOptimizer(c["opt"])
+    opt.apply(params, {k: v.copy() for k, v in got["grads"].items()}, c["lr"])
+    for pid, v in params.items():
+        assert np.array_equal(v, got["params"][pid]), pid
+
+
+@pytest.mark.parametrize("name", ["c3_mlp", "c1_mlp"])
+def test_tensor_core_path_matches_cuda_core_path(pkg, name):
+    """3xTF32 tcgen05 GEMMs vs the fp32 FFMA kernels: first-step gradients agree to fp32 noise."""
+    tc, tc_labels, _ = _first_step_grads(pkg, name, True)
+    simt, simt_labels, _ = _first_step_grads(pkg, name, False)
+    assert any(l.endswith("/tc") for l in tc_labels)
+    assert not any(l.endswith("/tc") for l in simt_labels)
+    for pid in tc["grads"]:
+        assert rel(tc["grads"][pid], simt["grads"][pid]) <= 5e-6, pid
