@@ -57,6 +57,7 @@ extern "C" {
 /* hnn_grouped_gemm `prec` */
 #define HNN_PREC_F32_SIMT 0   /* fp32 FFMA, CUDA cores */
 #define HNN_PREC_F32_3XTF32 1 /* tcgen05 kind::tf32, hi/lo split, fp32 accumulate in TMEM */
+#define HNN_PREC_F32_SIMT_SKINNY 2 /* fp32 FFMA, 128 x 16 tiles for N <= 16 (e.g. logits layers) */
 
 /* optimizer segment kinds */
 #define HNN_OPT_SGD 0

@@ -69,10 +69,39 @@ __device__ __forceinline__ void tma_prefetch(const void* tmap) {
   asm volatile("prefetch.tensormap [%0];" ::"l"(tmap) : "memory");
 }
 
-__device__ __forceinline__ uint32_t to_tf32(float x) {
-  uint32_t r;
-  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
-  return r;
+// Round-to-nearest (ties away) to tf32 on the bit pattern: 2 integer ops instead of the
+// 4-instruction cvt.rna emulation.  Finite training values only (a NaN payload confined to the
+// low 13 bits would turn into inf — such a step aborts on its non-finite loss anyway).
+__device__ __forceinline__ uint32_t tf32_bits(uint32_t x) { return (x + 0x1000u) & 0xFFFFE000u; }
+
+__device__ __forceinline__ uint4 lds128(uint32_t addr) {
+  uint4 v;
+  asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(addr));
+  return v;
+}
+
+__device__ __forceinline__ void sts128(uint32_t addr, uint4 v) {
+  asm volatile("st.shared.v4.u32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w)
+               : "memory");
+}
+
+__device__ __forceinline__ void sts32(uint32_t addr, float v) {
+  asm volatile("st.shared.f32 [%0], %1;" ::"r"(addr), "f"(v) : "memory");
+}
+
+__device__ __forceinline__ float lds32(uint32_t addr) {
+  float v;
+  asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(addr));
+  return v;
+}
+
+// hi = rna_tf32(x), lo = rna_tf32(x - hi), elementwise on 4 lanes
+__device__ __forceinline__ void split4(uint4 v, uint4& hi, uint4& lo) {
+  hi.x = tf32_bits(v.x); hi.y = tf32_bits(v.y); hi.z = tf32_bits(v.z); hi.w = tf32_bits(v.w);
+  lo.x = tf32_bits(__float_as_uint(__uint_as_float(v.x) - __uint_as_float(hi.x)));
+  lo.y = tf32_bits(__float_as_uint(__uint_as_float(v.y) - __uint_as_float(hi.y)));
+  lo.z = tf32_bits(__float_as_uint(__uint_as_float(v.z) - __uint_as_float(hi.z)));
+  lo.w = tf32_bits(__float_as_uint(__uint_as_float(v.w) - __uint_as_float(hi.w)));
 }
 
 // K-major, 128-byte swizzle: rows of 128 B, 8-row atoms 1024 B apart (SBO), LBO unused (=1).
@@ -275,19 +304,13 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       for (int kb = 0; kb < nkb; ++kb, ++kg) {
         const int s = kg % TC_STAGES;
         mbar_wait(bar(s), (kg / TC_STAGES) & 1);
-        float4* hi = reinterpret_cast<float4*>(base + s * TC_STAGE_BYTES);
-        float4* lo = reinterpret_cast<float4*>(base + s * TC_STAGE_BYTES + TC_HI_BYTES);
+        const uint32_t hi = sbase + s * TC_STAGE_BYTES, lo = hi + TC_HI_BYTES;
 #pragma unroll 4
         for (int i = ct; i < TC_HI_BYTES / 16; i += 128) {
-          float4 v = hi[i];
-          uint32_t h0 = to_tf32(v.x), h1 = to_tf32(v.y), h2 = to_tf32(v.z), h3 = to_tf32(v.w);
-          float4 l;
-          l.x = __uint_as_float(to_tf32(v.x - __uint_as_float(h0)));
-          l.y = __uint_as_float(to_tf32(v.y - __uint_as_float(h1)));
-          l.z = __uint_as_float(to_tf32(v.z - __uint_as_float(h2)));
-          l.w = __uint_as_float(to_tf32(v.w - __uint_as_float(h3)));
-          hi[i] = make_float4(__uint_as_float(h0), __uint_as_float(h1), __uint_as_float(h2), __uint_as_float(h3));
-          lo[i] = l;
+          uint4 h, l;
+          split4(lds128(hi + 16 * i), h, l);
+          sts128(hi + 16 * i, h);
+          sts128(lo + 16 * i, l);
         }
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         mbar_arrive(bar(TC_STAGES + s));
@@ -296,7 +319,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   } else {
     // ---------------- accumulators + epilogue (warps 6..9; TMEM lane quarter = warp % 4)
     const int q = warp & 3;
-    float* scr = scratch + (warp - 6) * 32 * 33;
+    const uint32_t scr = smem_u32(scratch) + (warp - 6) * 32 * 33 * 4;
     uint32_t cg = 0;
     for (int tile = blockIdx.x; tile < total_tiles; tile += gridDim.x) {
       const hnn_gemm_problem* p;
@@ -327,7 +350,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
 #pragma unroll
       for (int cb = 0; cb < TC_BN; cb += 32) {
 #pragma unroll
-        for (int j = 0; j < 32; ++j) scr[lane * 33 + j] = sum[cb + j];
+        for (int j = 0; j < 32; ++j) sts32(scr + 4 * (lane * 33 + j), sum[cb + j]);
         __syncwarp();
         const int n = n0 + cb + lane;
         const bool col_ok = n < p->n;
@@ -336,7 +359,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         for (int r = 0; r < 32; ++r) {
           const int row = row0 + r;
           if (row >= p->m) break;
-          float v = scr[r * 33 + lane];
+          float v = lds32(scr + 4 * (r * 33 + lane));
           if (OP == HNN_FWD) {
             if (row >= rows) v = 0.0f;
             else {
@@ -347,7 +370,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
             if (row >= rows) v = 0.0f;
             else if (p->mask && col_ok) v = np_mask(v, p->mask[size_t(row) * p->ldc + n]);
           }
-          if (col_ok) p->c[size_t(row) * p->ldc + n] = v;
+          if (col_ok) __stcg(p->c + size_t(row) * p->ldc + n, v);
         }
         __syncwarp();
       }

@@ -10,7 +10,7 @@
 
 namespace hnn {
 
-constexpr int SCE_THREADS = 256, SCE_WARPS = SCE_THREADS / 32;
+constexpr int SCE_THREADS = 1024, SCE_WARPS = SCE_THREADS / 32;
 
 // numpy @TYPE@_pairwise_sum for float32, contiguous (reduce starts from +0.0).
 __device__ float np_pairwise_sum(const float* a, int n) {

@@ -461,7 +461,7 @@ class DeviceHybrid:
 
     def _gemm_launch(self, op, items, label):
         """items: list of (slot, stage).  Splits into SIMT / 3xTF32 launches."""
-        groups = {N.PREC_SIMT: [], N.PREC_3XTF32: []}
+        groups = {N.PREC_SIMT: [], N.PREC_SIMT_SKINNY: [], N.PREC_3XTF32: []}
         for s, st in items:
             cap = s.batch_size
             K, U = int(np.prod(st.in_shape)), st.out_shape[0]
@@ -478,7 +478,10 @@ class DeviceHybrid:
                 gb = self.pview(self.grads, s.index, st.params[1])
                 d = dict(a=_ptr(st.dy), b=_ptr(st.x), c=_ptr(gw), bias=0, mask=0, dbias=_ptr(gb), m=U, n=K, k=cap,
                          lda=st.ld_out, ldb=st.ld_in, ldc=K, relu=0)
-            prec = N.PREC_3XTF32 if (self.use_tc and self._route_tc(op, d)) else N.PREC_SIMT
+            if self.use_tc and self._route_tc(op, d):
+                prec = N.PREC_3XTF32
+            else:
+                prec = N.PREC_SIMT_SKINNY if d["n"] <= 16 else N.PREC_SIMT
             groups[prec].append((s, d))
         out = []
         for prec, rows in groups.items():
@@ -507,7 +510,8 @@ class DeviceHybrid:
             # bytes: A + B read once, C written once (fp32)
             nbytes = sum(4 * (d["m"] * d["k"] + d["k"] * d["n"] + d["m"] * d["n"]) for _, d in rows)
             launch = Launch("hnn_grouped_gemm", (op, prec, _ptr(t), len(probs), base, _ptr(self.cur),
-                                                 _ptr(self.status)), t, f"{label}/{'tc' if prec else 'simt'}",
+                                                 _ptr(self.status)), t,
+                            f"{label}/{ {N.PREC_SIMT: 'simt', N.PREC_SIMT_SKINNY: 'simt16', N.PREC_3XTF32: 'tc'}[prec] }",
                             flops=flops, nbytes=nbytes)
             launch.maps = keep
             out.append(launch)

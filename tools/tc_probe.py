@@ -12,6 +12,9 @@ from paper_2408_01331_b200 import _native as N
 from paper_2408_01331_b200.runtime import STEP_DTYPE, _dev_table, _ptr
 
 
+TIME = False
+
+
 def run(op, prec, M, Nn, K, rows=None, seed=0, dbg=0):
     g = np.random.default_rng(seed)
     dev = torch.device("cuda")
@@ -56,10 +59,27 @@ def run(op, prec, M, Nn, K, rows=None, seed=0, dbg=0):
     N.call("hnn_grouped_gemm", op, prec, _ptr(t), 1, -(-d["m"] // tm) * tiles_n, _ptr(cur), 0,
            torch.cuda.current_stream().cuda_stream)
     torch.cuda.synchronize()
+    if TIME:
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(20):
+            N.call("hnn_grouped_gemm", op, prec, _ptr(t), 1, -(-d["m"] // tm) * tiles_n, _ptr(cur), 0,
+                   torch.cuda.current_stream().cuda_stream)
+        e1.record()
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1) / 20
+        print(f"  time op={op} prec={prec} {M}x{Nn}x{K}: {ms*1e3:.1f} us  {2*M*Nn*K/ms/1e9:.1f} TF/s")
     got = c.cpu().numpy().astype(np.float64)
     err = np.abs(got - ref) / (np.abs(ref).max() + 1e-30)
     return float(err.max()), got, ref
 
+
+if __name__ == "__main__" and len(sys.argv) > 1 and sys.argv[1] == "time":
+    TIME = True
+    for shape in ((256, 2048, 2048), (2048, 2048, 256), (256, 1024, 784), (4096, 4096, 256)):
+        for op in (0, 1, 2):
+            run(op, 1, *shape)
+    sys.exit(0)
 
 if __name__ == "__main__" and len(sys.argv) > 1 and sys.argv[1] == "variants":
     for op in (1, 2):
