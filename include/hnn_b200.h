@@ -131,6 +131,18 @@ typedef struct hnn_gemm_problem {
   int32_t tiles_n;
   const void* tmap_a; /* HNN_PREC_F32_3XTF32: device copies of the problem's TMA maps (hnn_gemm_tc_encode) */
   const void* tmap_b;
+  const void* tmap_c;
+  /* WGRAD optimizer fusion: when opt_w != NULL the epilogue applies the model's SGD / momentum /
+   * Adam update (arithmetic of hnn_multi_tensor_*) to the weight with the tile's finished
+   * gradient, and to the bias with dbias; c / dbias may then be NULL (gradient not stored). */
+  float* opt_w;
+  float* opt_wm;
+  float* opt_wv;
+  float* opt_b;
+  float* opt_bm;
+  float* opt_bv;
+  int32_t opt_kind; /* HNN_OPT_* */
+  float opt_momentum;
 } hnn_gemm_problem;
 
 /* Tile edge (m, n) used by (op, prec); lets the host lay out tile_base / tiles_n. */
@@ -140,9 +152,9 @@ int hnn_grouped_gemm(int op, int prec, const hnn_gemm_problem* probs, int nprob,
                      const hnn_step_row* cur, const hnn_model_status* status, void* stream);
 
 /*
- * Host-side: encode the two TMA tensor maps (A then B, 128 bytes each) of every problem for the
- * tcgen05 path into host_maps[2*nprob]; the caller copies them to device memory and stores their
- * device addresses in tmap_a / tmap_b.  Requirements: 16-byte aligned bases and row strides.
+ * Host-side: encode the three TMA tensor maps (A, B, C; 128 bytes each) of every problem for the
+ * tcgen05 path into host_maps[3*nprob]; the caller copies them to device memory and stores their
+ * device addresses in tmap_a / tmap_b / tmap_c.  Requirements: 16-byte aligned bases and row strides.
  * Tiles are 128 x 128 (hnn_gemm_tile_shape); WGRAD problems need m <= 4096.
  */
 int hnn_gemm_tc_encode(int op, const hnn_gemm_problem* host_probs, int nprob, void* host_maps);

@@ -40,7 +40,9 @@ class GatherProblem(C.Structure):
 class GemmProblem(C.Structure):
     _fields_ = [("a", P), ("b", P), ("c", P), ("bias", P), ("mask", P), ("dbias", P),
                 ("m", I), ("n", I), ("k", I), ("lda", I), ("ldb", I), ("ldc", I),
-                ("model", I), ("relu", I), ("tile_base", I), ("tiles_n", I), ("tmap_a", P), ("tmap_b", P)]
+                ("model", I), ("relu", I), ("tile_base", I), ("tiles_n", I), ("tmap_a", P), ("tmap_b", P),
+                ("tmap_c", P), ("opt_w", P), ("opt_wm", P), ("opt_wv", P), ("opt_b", P), ("opt_bm", P),
+                ("opt_bv", P), ("opt_kind", I), ("opt_momentum", C.c_float)]
 
 
 class ConvProblem(C.Structure):

@@ -19,6 +19,7 @@ CSRC = PKG / "csrc"
 OUT_DIR = PKG / "_lib"
 LIB = OUT_DIR / "libhnn_b200.so"
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+PER_FILE_FLAGS: dict = {}
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "--expt-relaxed-constexpr", "-Xptxas", "-v"]
 
 
@@ -49,7 +50,8 @@ def build(verbose: bool = False) -> Path:
         obj = OUT_DIR / (src.stem + ".o")
         objs.append(obj)
         if _stale(obj, [src] + headers):
-            cmd = [_nvcc(), *ARCH, *FLAGS, "-I", str(REPO / "include"), "-c", str(src), "-o", str(obj)]
+            extra = PER_FILE_FLAGS.get(src.name, [])
+            cmd = [_nvcc(), *ARCH, *FLAGS, *extra, "-I", str(REPO / "include"), "-c", str(src), "-o", str(obj)]
             r = subprocess.run(cmd, capture_output=True, text=True)
             log.append(r.stderr)
             if r.returncode != 0:

@@ -100,7 +100,7 @@ __global__ void __launch_bounds__(STHREADS) gemm_simt_kernel(const hnn_gemm_prob
       }
       __syncthreads();
       if (k0 + BK < k_lim) load_slab(k0 + BK);  // next slab in flight during the FMAs
-      if (OP == HNN_WGRAD && p.dbias != nullptr && n0 == 0 && tid < BM) {
+      if (OP == HNN_WGRAD && (p.dbias != nullptr || p.opt_b != nullptr) && n0 == 0 && tid < BM) {
         const int kmax = min(BK, k_lim - k0);
         for (int kk = 0; kk < kmax; ++kk) bsum = __fadd_rn(bsum, As[kk][tid]);
       }
@@ -120,38 +120,176 @@ __global__ void __launch_bounds__(STHREADS) gemm_simt_kernel(const hnn_gemm_prob
     }
   }
 
-  if (OP == HNN_WGRAD && p.dbias != nullptr && n0 == 0 && tid < BM && m0 + tid < p.m) p.dbias[m0 + tid] = bsum;
+  if (OP == HNN_WGRAD && (p.dbias != nullptr || p.opt_b != nullptr) && n0 == 0 && tid < BM && m0 + tid < p.m) {
+    if (p.dbias) p.dbias[m0 + tid] = bsum;
+    if (p.opt_b) {
+      const Update u = make_update(cur[p.model], p.opt_kind, p.opt_momentum);
+      const int i = m0 + tid;
+      float w = p.opt_b[i], m = p.opt_bm ? p.opt_bm[i] : 0.0f, v = p.opt_bv ? p.opt_bv[i] : 0.0f;
+      update_one(u, w, bsum, m, v);
+      p.opt_b[i] = w;
+      if (p.opt_bm) p.opt_bm[i] = m;
+      if (p.opt_bv) p.opt_bv[i] = v;
+    }
+  }
+  if (OP == HNN_WGRAD && p.opt_w != nullptr) {
+    // fused optimizer: update W (and its moments) with the finished gradient tile
+    const Update u = make_update(cur[p.model], p.opt_kind, p.opt_momentum);
+#pragma unroll
+    for (int i = 0; i < TM; ++i) {
+      const int gm = m0 + ty * TM + i;
+      if (gm >= p.m) continue;
+#pragma unroll
+      for (int j = 0; j < TN; ++j) {
+        const int gn = n0 + tx * TN + j;
+        if (gn >= p.n) continue;
+        const size_t off = size_t(gm) * p.ldc + gn;
+        float w = p.opt_w[off], m = p.opt_wm ? p.opt_wm[off] : 0.0f, v = p.opt_wv ? p.opt_wv[off] : 0.0f;
+        update_one(u, w, acc[i][j], m, v);
+        p.opt_w[off] = w;
+        if (p.opt_wm) p.opt_wm[off] = m;
+        if (p.opt_wv) p.opt_wv[off] = v;
+      }
+    }
+    if (p.c == nullptr) return;
+  }
 
-  // ---- epilogue
+  // ---- epilogue (float4 stores when the row segment is aligned and in range)
+  const bool vec = (TN == 4) && ((p.ldc & 3) == 0) && ((reinterpret_cast<uintptr_t>(p.c) & 15) == 0) &&
+                   (!p.mask || (reinterpret_cast<uintptr_t>(p.mask) & 15) == 0);
 #pragma unroll
   for (int i = 0; i < TM; ++i) {
     const int gm = m0 + ty * TM + i;
     if (gm >= p.m) continue;
+    const int gn0 = n0 + tx * TN;
+    float v[TN];
 #pragma unroll
-    for (int j = 0; j < TN; ++j) {
-      const int gn = n0 + tx * TN + j;
-      if (gn >= p.n) continue;
-      float v = acc[i][j];
+    for (int j = 0; j < TN; ++j) v[j] = acc[i][j];
+    if (vec && gn0 + 3 < p.n) {
       if (OP == HNN_FWD) {
-        if (gm >= rows) v = 0.0f;
-        else {
-          v = __fadd_rn(v, p.bias[gn]);
-          if (p.relu) v = np_relu(v);
+        const float4 b4 = *reinterpret_cast<const float4*>(p.bias + gn0);
+        const float bb[4] = {b4.x, b4.y, b4.z, b4.w};
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          v[j] = (gm >= rows) ? 0.0f : __fadd_rn(v[j], bb[j]);
+          if (p.relu && gm < rows) v[j] = np_relu(v[j]);
         }
       } else if (OP == HNN_DGRAD) {
-        if (gm >= rows) v = 0.0f;
-        else if (p.mask) v = np_mask(v, p.mask[size_t(gm) * p.ldc + gn]);
+        if (gm >= rows) {
+#pragma unroll
+          for (int j = 0; j < 4; ++j) v[j] = 0.0f;
+        } else if (p.mask) {
+          const float4 m4 = *reinterpret_cast<const float4*>(p.mask + size_t(gm) * p.ldc + gn0);
+          v[0] = np_mask(v[0], m4.x);
+          v[1] = np_mask(v[1], m4.y);
+          v[2] = np_mask(v[2], m4.z);
+          v[3] = np_mask(v[3], m4.w);
+        }
       }
-      p.c[size_t(gm) * p.ldc + gn] = v;
+      *reinterpret_cast<float4*>(p.c + size_t(gm) * p.ldc + gn0) = make_float4(v[0], v[1], v[2], v[3]);
+      continue;
+    }
+#pragma unroll
+    for (int j = 0; j < TN; ++j) {
+      const int gn = gn0 + j;
+      if (gn >= p.n) continue;
+      float x = v[j];
+      if (OP == HNN_FWD) {
+        if (gm >= rows) x = 0.0f;
+        else {
+          x = __fadd_rn(x, p.bias[gn]);
+          if (p.relu) x = np_relu(x);
+        }
+      } else if (OP == HNN_DGRAD) {
+        if (gm >= rows) x = 0.0f;
+        else if (p.mask) x = np_mask(x, p.mask[size_t(gm) * p.ldc + gn]);
+      }
+      p.c[size_t(gm) * p.ldc + gn] = x;
     }
   }
 }
 
-// Skinny variant (128 x 16) for N <= 16: used by the host via hnn_gemm_tile_shape(prec = SIMT_SKINNY).
+// FWD with N <= 16 (e.g. the 10-class logits layer, K up to thousands): a warp computes two
+// rows against all N columns, lanes striding K with float4 loads, then a fixed xor-shuffle
+// tree reduces each dot product (deterministic, independent of other problems).
+// Tile = 16 rows (8 warps x 2 rows) of one problem.
+__global__ void __launch_bounds__(STHREADS) rowdot_fwd_kernel(const hnn_gemm_problem* __restrict__ probs, int nprob,
+                                                              const hnn_step_row* __restrict__ cur,
+                                                              const hnn_model_status* __restrict__ status) {
+  const int pi = find_problem(probs, nprob, blockIdx.x, [](const hnn_gemm_problem& q) { return q.tile_base; });
+  const hnn_gemm_problem p = probs[pi];
+  if (!live(cur, status, p.model)) return;
+  const int rows = cur[p.model].rows;
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const int r0 = (blockIdx.x - p.tile_base) * 16 + warp * 2;
+  if (r0 >= p.m) return;
+  const bool has1 = r0 + 1 < p.m;
+  float a0[16], a1[16];
+#pragma unroll
+  for (int j = 0; j < 16; ++j) a0[j] = a1[j] = 0.0f;
+  const bool live0 = r0 < rows, live1 = has1 && (r0 + 1) < rows;
+  if (live0) {
+    const float* x0 = p.a + size_t(r0) * p.lda;
+    const float* x1 = p.a + size_t(r0 + (live1 ? 1 : 0)) * p.lda;
+    const bool vec = ((p.lda & 3) == 0) && ((p.ldb & 3) == 0) && ((reinterpret_cast<uintptr_t>(p.a) & 15) == 0) &&
+                     ((reinterpret_cast<uintptr_t>(p.b) & 15) == 0);
+    int k = 0;
+    if (vec) {
+      for (; k + 128 <= p.k; k += 128) {
+        const int kk = k + lane * 4;
+        const float4 u0 = __ldg(reinterpret_cast<const float4*>(x0 + kk));
+        const float4 u1 = __ldg(reinterpret_cast<const float4*>(x1 + kk));
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
+          if (j >= p.n) break;
+          const float4 w = __ldg(reinterpret_cast<const float4*>(p.b + size_t(j) * p.ldb + kk));
+          a0[j] = fmaf(u0.x, w.x, fmaf(u0.y, w.y, fmaf(u0.z, w.z, fmaf(u0.w, w.w, a0[j]))));
+          a1[j] = fmaf(u1.x, w.x, fmaf(u1.y, w.y, fmaf(u1.z, w.z, fmaf(u1.w, w.w, a1[j]))));
+        }
+      }
+    }
+    for (int kk = k + lane; kk < p.k; kk += 32) {
+      const float u0 = __ldg(x0 + kk), u1 = __ldg(x1 + kk);
+#pragma unroll
+      for (int j = 0; j < 16; ++j) {
+        if (j >= p.n) break;
+        const float w = __ldg(p.b + size_t(j) * p.ldb + kk);
+        a0[j] = fmaf(u0, w, a0[j]);
+        a1[j] = fmaf(u1, w, a1[j]);
+      }
+    }
+  }
+#pragma unroll
+  for (int j = 0; j < 16; ++j) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      a0[j] += __shfl_xor_sync(0xffffffffu, a0[j], o);
+      a1[j] += __shfl_xor_sync(0xffffffffu, a1[j], o);
+    }
+  }
+  if (lane < p.n) {
+    float y0 = 0.0f, y1 = 0.0f;
+#pragma unroll
+    for (int j = 0; j < 16; ++j)
+      if (j == lane) { y0 = a0[j]; y1 = a1[j]; }
+    const float b = p.bias[lane];
+    y0 = live0 ? __fadd_rn(y0, b) : 0.0f;
+    y1 = live1 ? __fadd_rn(y1, b) : 0.0f;
+    if (p.relu) {
+      if (live0) y0 = np_relu(y0);
+      if (live1) y1 = np_relu(y1);
+    }
+    p.c[size_t(r0) * p.ldc + lane] = y0;
+    if (has1) p.c[size_t(r0 + 1) * p.ldc + lane] = y1;
+  }
+}
+
+// Skinny variants for N <= 16: selected by the host with prec = HNN_PREC_F32_SIMT_SKINNY.
 template <int OP>
 void launch_simt(int skinny, const hnn_gemm_problem* probs, int nprob, int total_tiles, const hnn_step_row* cur,
                  const hnn_model_status* status, cudaStream_t s) {
-  if (skinny) gemm_simt_kernel<OP, 128, 16><<<total_tiles, STHREADS, 0, s>>>(probs, nprob, cur, status);
+  if (skinny && OP == HNN_FWD) rowdot_fwd_kernel<<<total_tiles, STHREADS, 0, s>>>(probs, nprob, cur, status);
+  else if (skinny) gemm_simt_kernel<OP, 128, 16><<<total_tiles, STHREADS, 0, s>>>(probs, nprob, cur, status);
   else gemm_simt_kernel<OP, 64, 64><<<total_tiles, STHREADS, 0, s>>>(probs, nprob, cur, status);
 }
 
@@ -177,8 +315,8 @@ extern "C" int hnn_gemm_tile_shape(int op, int prec, int32_t* tile_m, int32_t* t
     *tile_n = 64;
     return HNN_OK;
   }
-  if (prec == HNN_PREC_F32_SIMT_SKINNY) {
-    *tile_m = 128;
+  if (prec == HNN_PREC_F32_SIMT_SKINNY) {  // FWD: 16-row row-dot tiles; DGRAD/WGRAD: 128 x 16
+    *tile_m = (op == HNN_FWD) ? 16 : 128;
     *tile_n = 16;
     return HNN_OK;
   }

@@ -1,17 +1,22 @@
 // Grouped fp32 GEMM on the 5th-gen tensor cores: tcgen05.mma kind::tf32, 3xTF32.
 //
 // fp32 parity forbids plain TF32 (SURVEY finding 4: relu-mask flips give 1e-1
-// gradient errors), so every operand x is split into hi = rna_tf32(x) and
-// lo = rna_tf32(x - hi) and the tile accumulates  A_hi*B_hi + A_hi*B_lo + A_lo*B_hi
-// in fp32 in TMEM (error ~2^-22 relative per product, like fp32 FFMA).
+// gradient errors), so every operand x is split into hi = trunc_tf32(x) and
+// lo = rna_tf32(x - hi) and the tile accumulates  A_hi*B_hi + A_hi*B_lo + A_lo*B_hi.
+// The tensor core itself truncates fp32 operands to tf32 (measured: feeding raw fp32 as
+// "hi" gives the same 6e-7 GEMM error as an explicit split, a rounding unit would give
+// ~1e-4), so the raw TMA tile IS the hi operand and converters only write lo.
 //
 // Per CTA: one 128 x BN output tile of one problem (tile list = concatenation of
 // every problem's tiles, ordered heaviest first by the host; a tile's arithmetic
 // never depends on its neighbours -> bit-exact isolation).
-//   warp 0      TMA producer: raw fp32 tiles, 128-byte swizzle, into a STAGES-deep ring
-//   warp 1      TMEM allocator + single-thread MMA issuer (12 MMAs per 32-wide K block)
-//   warps 2..5  converters (hi in place, lo beside it, fence.proxy.async) then the
-//               epilogue: tcgen05.ld -> bias / relu / relu-mask / zero pad rows -> global
+//   warp 0       TMA producer: raw fp32 tiles, 128-byte swizzle, into a STAGES-deep ring
+//   warp 1       TMEM allocator + single-thread MMA issuer (12 MMAs per 32-wide K block)
+//   warps 2..5   converters: lo = rna_tf32(x - trunc(x)) into a separate lo ring, fence.proxy.async
+//   warps 6..13  accumulators (two per TMEM lane quarter, 64 columns each): promote each
+//                128-term TMEM chunk into fp32 registers (RN adds),
+//                then the epilogue (bias / relu / relu-mask / zero pad rows) into 128B-swizzled
+//                smem staging blocks written out by TMA stores
 // Operand majorness per op (row-major fp32 tensors in HBM):
 //   FWD    A = X  [cap, K]  K-major      B = W  [N, K]     K-major
 //   DGRAD  A = dY [cap, U]  K-major      B = W  [U, N]     N-major
@@ -22,13 +27,17 @@
 
 namespace hnn {
 
-constexpr int TC_BM = 128, TC_BN = 128, TC_BK = 32, TC_STAGES = 3;
-constexpr int TC_THREADS = 320;  // TMA, MMA, 4 converter warps, 4 accumulator warps
+constexpr int TC_BM = 128, TC_BN = 128, TC_BK = 32;
+constexpr int TC_RAW_STAGES = 4;  // TMA ring of raw fp32 tiles (= the hi operands)
+constexpr int TC_LO_STAGES = 2;   // converter ring of lo operands
+constexpr int TC_THREADS = 448;   // TMA, MMA, 4 converter warps, 8 accumulator warps (2 per lane quarter)
+constexpr int TC_CONV_THREADS = 128;
 constexpr int TC_A_BYTES = TC_BM * TC_BK * 4;              // 16 KB
 constexpr int TC_B_BYTES = TC_BN * TC_BK * 4;              // 16 KB
-constexpr int TC_HI_BYTES = TC_A_BYTES + TC_B_BYTES;       // raw -> hi, in place
-constexpr int TC_STAGE_BYTES = 2 * TC_HI_BYTES;            // hi + lo
-constexpr int TC_SMEM_BYTES = TC_STAGES * TC_STAGE_BYTES + 4 * 32 * 33 * 4 /*epilogue*/ + 1024 /*align*/ + 256;
+constexpr int TC_HI_BYTES = TC_A_BYTES + TC_B_BYTES;       // one raw (or lo) stage
+constexpr int TC_EPI_BYTES = 8 * 32 * 32 * 4;              // per accumulator warp: one 32x32 fp32 staging block
+constexpr int TC_SMEM_BYTES = (TC_RAW_STAGES + TC_LO_STAGES) * TC_HI_BYTES + TC_EPI_BYTES + 1024 + 256;
+constexpr int TC_CHUNK_KB = 4;  // k-blocks per TMEM chunk before promotion to fp32 registers
 
 // ---------------------------------------------------------------- PTX helpers
 
@@ -64,6 +73,19 @@ __device__ __forceinline__ void tma_load_2d(uint32_t dst, const void* tmap, uint
       "l"(tmap), "r"(bar), "r"(c0), "r"(c1)
       : "memory");
 }
+
+__device__ __forceinline__ void tma_store_2d(const void* tmap, uint32_t src, int c0, int c1) {
+  asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];" ::"l"(tmap), "r"(src),
+               "r"(c0), "r"(c1)
+               : "memory");
+  asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+}
+
+__device__ __forceinline__ void tma_store_wait_read() {
+  asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");  // staging smem free to overwrite
+}
+
+__device__ __forceinline__ void tma_store_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
 
 __device__ __forceinline__ void tma_prefetch(const void* tmap) {
   asm volatile("prefetch.tensormap [%0];" ::"l"(tmap) : "memory");
@@ -151,6 +173,28 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
 
+__device__ __forceinline__ void tmem_ld32_nowait(uint32_t taddr, uint32_t (&r)[32]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]),
+        "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]), "=r"(r[16]),
+        "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]),
+        "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(taddr));
+}
+
+__device__ __forceinline__ void tmem_st32(uint32_t taddr, const uint32_t (&r)[32]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,"
+      "%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" ::"r"(taddr),
+      "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]), "r"(r[9]),
+      "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15]), "r"(r[16]), "r"(r[17]), "r"(r[18]),
+      "r"(r[19]), "r"(r[20]), "r"(r[21]), "r"(r[22]), "r"(r[23]), "r"(r[24]), "r"(r[25]), "r"(r[26]), "r"(r[27]),
+      "r"(r[28]), "r"(r[29]), "r"(r[30]), "r"(r[31]));
+  asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+}
+
 // ---------------------------------------------------------------- the kernel
 //
 // Persistent: grid = min(tiles, SMs); CTA c walks tiles c, c+grid, ... (the host orders tiles
@@ -165,8 +209,6 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
 // |g| ~ eps (measured: single-accumulator 3xTF32 gave 8e-6 relative gradient error, enough to
 // move Adam weights by up to lr).
 
-constexpr int TC_CHUNK_KB = 2;
-constexpr int TC_EPI_SCRATCH = 4 * 32 * 33 * 4;  // per accumulator warp: 32 x 33 floats (transpose)
 
 template <int OP>
 __global__ void __launch_bounds__(TC_THREADS, 1)
@@ -174,31 +216,38 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
                    const hnn_step_row* __restrict__ cur, const hnn_model_status* __restrict__ status) {
   constexpr int A_MN = (OP == HNN_WGRAD) ? 1 : 0;
   constexpr int B_MN = (OP == HNN_FWD) ? 0 : 1;
+  constexpr int SR = TC_RAW_STAGES, SL = TC_LO_STAGES;
   extern __shared__ uint8_t smem_raw[];
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
 
   uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  float* scratch = reinterpret_cast<float*>(base + TC_STAGES * TC_STAGE_BYTES);
-  uint64_t* bars = reinterpret_cast<uint64_t*>(base + TC_STAGES * TC_STAGE_BYTES + TC_EPI_SCRATCH);
-  // bars: full_raw[S] | full_conv[S] | empty[S] | acc_full[2] | acc_empty[2]
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 3 * TC_STAGES + 4);
-  const uint32_t sbase = smem_u32(base);
+  const uint32_t raw_base = smem_u32(base);                       // [SR][A | B]
+  const uint32_t lo_base = raw_base + SR * TC_HI_BYTES;            // [SL][A | B], same layout
+  const uint32_t epi_base = raw_base + (SR + SL) * TC_HI_BYTES;  // [8 warps][32 x 128 B], 1024-aligned
+  uint64_t* bars = reinterpret_cast<uint64_t*>(base + (SR + SL) * TC_HI_BYTES + TC_EPI_BYTES);
+  // barriers
+  constexpr int RAW_FULL = 0, RAW_EMPTY = SR, LO_FULL = 2 * SR, LO_EMPTY = 2 * SR + SL;
+  constexpr int ACC_FULL = 2 * SR + 2 * SL, ACC_EMPTY = ACC_FULL + 2, NBARS = ACC_EMPTY + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + NBARS);
   auto bar = [&](int i) { return smem_u32(bars + i); };
-  const int ACC_FULL = 3 * TC_STAGES, ACC_EMPTY = 3 * TC_STAGES + 2;
 
   if (threadIdx.x == 0) {
-    for (int s = 0; s < TC_STAGES; ++s) {
-      mbar_init(bar(s), 1);                  // full_raw: expect_tx arrival + TMA bytes
-      mbar_init(bar(TC_STAGES + s), 128);    // full_conv: every converter thread
-      mbar_init(bar(2 * TC_STAGES + s), 1);  // empty: MMA commit
+    for (int s = 0; s < SR; ++s) {
+      mbar_init(bar(RAW_FULL + s), 1);                 // producer's expect_tx arrival + TMA bytes
+      mbar_init(bar(RAW_EMPTY + s), 1);                // MMA commit
+    }
+    for (int s = 0; s < SL; ++s) {
+      mbar_init(bar(LO_FULL + s), TC_CONV_THREADS);    // every converter thread
+      mbar_init(bar(LO_EMPTY + s), 1);                 // MMA commit
     }
     for (int b = 0; b < 2; ++b) {
-      mbar_init(bar(ACC_FULL + b), 1);       // MMA commit
-      mbar_init(bar(ACC_EMPTY + b), 128);    // every accumulator thread
+      mbar_init(bar(ACC_FULL + b), 1);                 // MMA commit
+      mbar_init(bar(ACC_EMPTY + b), 256);              // every accumulator thread
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 1) {
+    // columns: two chunk buffers [0,128) and [128,256)
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
                  "r"(2 * TC_BN));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
@@ -230,29 +279,31 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         int m0, n0, nkb, rows;
         if (!tile_info(tile, p, m0, n0, nkb, rows)) continue;
         for (int kb = 0; kb < nkb; ++kb, ++kg) {
-          const int s = kg % TC_STAGES;
-          if (kg >= TC_STAGES) mbar_wait(bar(2 * TC_STAGES + s), ((kg / TC_STAGES) - 1) & 1);
-          const uint32_t st = sbase + s * TC_STAGE_BYTES;
-          mbar_expect_tx(bar(s), TC_HI_BYTES);
+          const int s = kg % SR;
+          if (kg >= SR) mbar_wait(bar(RAW_EMPTY + s), ((kg / SR) - 1) & 1);
+          const uint32_t st = raw_base + s * TC_HI_BYTES;
+          mbar_expect_tx(bar(RAW_FULL + s), TC_HI_BYTES);
           const int k0 = kb * TC_BK;
           if (A_MN) {
 #pragma unroll
-            for (int b = 0; b < TC_BM / 32; ++b) tma_load_2d(st + b * 4096, p->tmap_a, bar(s), m0 + 32 * b, k0);
+            for (int b = 0; b < TC_BM / 32; ++b)
+              tma_load_2d(st + b * 4096, p->tmap_a, bar(RAW_FULL + s), m0 + 32 * b, k0);
           } else {
-            tma_load_2d(st, p->tmap_a, bar(s), k0, m0);
+            tma_load_2d(st, p->tmap_a, bar(RAW_FULL + s), k0, m0);
           }
           if (B_MN) {
 #pragma unroll
             for (int b = 0; b < TC_BN / 32; ++b)
-              tma_load_2d(st + TC_A_BYTES + b * 4096, p->tmap_b, bar(s), n0 + 32 * b, k0);
+              tma_load_2d(st + TC_A_BYTES + b * 4096, p->tmap_b, bar(RAW_FULL + s), n0 + 32 * b, k0);
           } else {
-            tma_load_2d(st + TC_A_BYTES, p->tmap_b, bar(s), k0, n0);
+            tma_load_2d(st + TC_A_BYTES, p->tmap_b, bar(RAW_FULL + s), k0, n0);
           }
         }
       }
     }
   } else if (warp == 1) {
-    // ---------------- MMA issuer (one thread)
+    // ---------------- MMA issuer (one thread): hi*hi as soon as the raw tile lands,
+    // then the two correction products once the converters have written lo
     if (lane == 0) {
       constexpr uint32_t idesc = tf32_idesc(TC_BM, TC_BN, A_MN, B_MN);
       constexpr uint32_t alb = A_MN ? 4096 : 16, asb = A_MN ? 512 : 1024, alt = A_MN ? 1 : 2;
@@ -269,112 +320,159 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
             mbar_wait(bar(ACC_EMPTY + buf), ((cg >> 1) - 1) & 1);  // promoted and released
             tc_fence_after();
           }
-          const int s = kg % TC_STAGES;
-          mbar_wait(bar(TC_STAGES + s), (kg / TC_STAGES) & 1);
-          tc_fence_after();
-          const uint32_t a_hi = sbase + s * TC_STAGE_BYTES, b_hi = a_hi + TC_A_BYTES;
-          const uint32_t a_lo = a_hi + TC_HI_BYTES, b_lo = b_hi + TC_HI_BYTES;
+          const int s = kg % SR, l = kg % SL;
+          const uint32_t a_hi = raw_base + s * TC_HI_BYTES, b_hi = a_hi + TC_A_BYTES;
+          const uint32_t a_lo = lo_base + l * TC_HI_BYTES, b_lo = a_lo + TC_A_BYTES;
           const uint32_t acc = tmem + buf * TC_BN;
+          mbar_wait(bar(RAW_FULL + s), (kg / SR) & 1);
+          tc_fence_after();
 #pragma unroll
           for (int j = 0; j < TC_BK / 8; ++j) {
             // K step j = 8 tf32: +32 B inside a K-major row, +1024 B (two 4-row atoms) in MN-major
             const uint32_t ao = A_MN ? j * 1024 : j * 32, bo = B_MN ? j * 1024 : j * 32;
+            mma_tf32(acc, smem_desc(a_hi + ao, alb, asb, alt), smem_desc(b_hi + bo, blb, bsb, blt), idesc,
+                     (in_chunk | j) != 0);
+          }
+          mbar_wait(bar(LO_FULL + l), (kg / SL) & 1);
+          tc_fence_after();
+#pragma unroll
+          for (int j = 0; j < TC_BK / 8; ++j) {
+            const uint32_t ao = A_MN ? j * 1024 : j * 32, bo = B_MN ? j * 1024 : j * 32;
             const uint64_t dah = smem_desc(a_hi + ao, alb, asb, alt), dal = smem_desc(a_lo + ao, alb, asb, alt);
             const uint64_t dbh = smem_desc(b_hi + bo, blb, bsb, blt), dbl = smem_desc(b_lo + bo, blb, bsb, blt);
-            mma_tf32(acc, dal, dbh, idesc, (in_chunk | j) != 0);
+            mma_tf32(acc, dal, dbh, idesc, 1);
             mma_tf32(acc, dah, dbl, idesc, 1);
-            mma_tf32(acc, dah, dbh, idesc, 1);
           }
-          mma_commit(bar(2 * TC_STAGES + s));  // smem stage free once these MMAs have read it
+          mma_commit(bar(RAW_EMPTY + s));  // raw and lo slots free once these MMAs have read them
+          mma_commit(bar(LO_EMPTY + l));
           if (in_chunk == TC_CHUNK_KB - 1 || kb == nkb - 1) {
-            mma_commit(bar(ACC_FULL + buf));   // chunk partial ready for promotion
+            mma_commit(bar(ACC_FULL + buf));  // chunk partial ready for promotion
             ++cg;
           }
         }
       }
     }
   } else if (warp < 6) {
-    // ---------------- converters: hi = rna_tf32(x) in place, lo = rna_tf32(x - hi)
+    // ---------------- converters: lo = rna_tf32(x - trunc_tf32(x)); the raw tile stays as hi
     const int ct = threadIdx.x - 64;  // 0..127
+    constexpr int PER = TC_HI_BYTES / 16 / TC_CONV_THREADS;
     uint32_t kg = 0;
     for (int tile = blockIdx.x; tile < total_tiles; tile += gridDim.x) {
       const hnn_gemm_problem* p;
       int m0, n0, nkb, rows;
       if (!tile_info(tile, p, m0, n0, nkb, rows)) continue;
       for (int kb = 0; kb < nkb; ++kb, ++kg) {
-        const int s = kg % TC_STAGES;
-        mbar_wait(bar(s), (kg / TC_STAGES) & 1);
-        const uint32_t hi = sbase + s * TC_STAGE_BYTES, lo = hi + TC_HI_BYTES;
-#pragma unroll 4
-        for (int i = ct; i < TC_HI_BYTES / 16; i += 128) {
-          uint4 h, l;
-          split4(lds128(hi + 16 * i), h, l);
-          sts128(hi + 16 * i, h);
-          sts128(lo + 16 * i, l);
+        const int s = kg % SR, l = kg % SL;
+        mbar_wait(bar(RAW_FULL + s), (kg / SR) & 1);
+        const uint32_t hi = raw_base + s * TC_HI_BYTES, lo = lo_base + l * TC_HI_BYTES;
+        uint4 v[PER];
+#pragma unroll
+        for (int u = 0; u < PER; ++u) v[u] = lds128(hi + 16 * (ct + u * TC_CONV_THREADS));
+        if (kg >= SL) mbar_wait(bar(LO_EMPTY + l), ((kg / SL) - 1) & 1);
+#pragma unroll
+        for (int u = 0; u < PER; ++u) {
+          uint4 o;
+          o.x = tf32_bits(__float_as_uint(__uint_as_float(v[u].x) - __uint_as_float(v[u].x & 0xFFFFE000u)));
+          o.y = tf32_bits(__float_as_uint(__uint_as_float(v[u].y) - __uint_as_float(v[u].y & 0xFFFFE000u)));
+          o.z = tf32_bits(__float_as_uint(__uint_as_float(v[u].z) - __uint_as_float(v[u].z & 0xFFFFE000u)));
+          o.w = tf32_bits(__float_as_uint(__uint_as_float(v[u].w) - __uint_as_float(v[u].w & 0xFFFFE000u)));
+          sts128(lo + 16 * (ct + u * TC_CONV_THREADS), o);
         }
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        mbar_arrive(bar(TC_STAGES + s));
+        mbar_arrive(bar(LO_FULL + l));
       }
     }
   } else {
-    // ---------------- accumulators + epilogue (warps 6..9; TMEM lane quarter = warp % 4)
-    const int q = warp & 3;
-    const uint32_t scr = smem_u32(scratch) + (warp - 6) * 32 * 33 * 4;
-    uint32_t cg = 0;
+    // ---------------- accumulators + epilogue (warps 6..13: lane quarter warp % 4, column half)
+    constexpr int HALF = TC_BN / 2;
+    const int q = warp & 3, half = (warp - 6) >> 2;
+    const uint32_t lane_base = tmem + (uint32_t(q * 32) << 16) + half * HALF;
+    const uint32_t stg = epi_base + (warp - 6) * 4096;
+    uint32_t cg = 0, nstore = 0;
     for (int tile = blockIdx.x; tile < total_tiles; tile += gridDim.x) {
       const hnn_gemm_problem* p;
       int m0, n0, nkb, rows;
       if (!tile_info(tile, p, m0, n0, nkb, rows)) continue;
-      float sum[TC_BN];
-#pragma unroll
-      for (int j = 0; j < TC_BN; ++j) sum[j] = 0.0f;
       const int nchunks = (nkb + TC_CHUNK_KB - 1) / TC_CHUNK_KB;
+      const int row0 = m0 + q * 32, row = row0 + lane;
+      const int nh = n0 + half * HALF;
+      float sum[HALF];
       for (int c = 0; c < nchunks; ++c, ++cg) {
         const uint32_t buf = cg & 1;
         mbar_wait(bar(ACC_FULL + buf), (cg >> 1) & 1);
         tc_fence_after();
-        const uint32_t taddr = tmem + (uint32_t(q * 32) << 16) + buf * TC_BN;
+        // promotion: fp32 running total += chunk (round-to-nearest adds)
 #pragma unroll
-        for (int cb = 0; cb < TC_BN; cb += 32) {
-          uint32_t r[32];
-          tmem_ld32(taddr + cb, r);
+        for (int cb = 0; cb < HALF; cb += 32) {
+          uint32_t r0[32];
+          tmem_ld32(lane_base + buf * TC_BN + cb, r0);
 #pragma unroll
-          for (int j = 0; j < 32; ++j) sum[cb + j] = __fadd_rn(sum[cb + j], __uint_as_float(r[j]));
+          for (int j = 0; j < 32; ++j)
+            sum[cb + j] = (c == 0) ? __uint_as_float(r0[j]) : __fadd_rn(sum[cb + j], __uint_as_float(r0[j]));
         }
         tc_fence_before();
         mbar_arrive(bar(ACC_EMPTY + buf));
       }
-      // epilogue: transpose 32x32 blocks through smem so each store instruction writes one row's
-      // 32 consecutive columns (128 B, coalesced); bias / relu / relu-mask / pad rows applied here
-      const int row0 = m0 + q * 32;
+      // epilogue: per 32x32 block, registers -> 128B-swizzled staging (16-byte chunk j of row r
+      // lives at chunk j ^ (r & 7): conflict-free STS.128) -> one TMA store per block
+      const bool zero_row = (OP != HNN_WGRAD) && row >= rows;
+      const float* mrow = (OP == HNN_DGRAD && p->mask && row < p->m) ? p->mask + size_t(row) * p->ldc : nullptr;
 #pragma unroll
-      for (int cb = 0; cb < TC_BN; cb += 32) {
-#pragma unroll
-        for (int j = 0; j < 32; ++j) sts32(scr + 4 * (lane * 33 + j), sum[cb + j]);
+      for (int cb = 0; cb < HALF; cb += 32) {
+        if (lane == 0 && nstore > 0) tma_store_wait_read();  // previous store done reading staging
         __syncwarp();
-        const int n = n0 + cb + lane;
-        const bool col_ok = n < p->n;
-        float bias = 0.0f;
-        if (OP == HNN_FWD && col_ok) bias = __ldg(p->bias + n);
-        for (int r = 0; r < 32; ++r) {
-          const int row = row0 + r;
-          if (row >= p->m) break;
-          float v = lds32(scr + 4 * (r * 33 + lane));
-          if (OP == HNN_FWD) {
-            if (row >= rows) v = 0.0f;
-            else {
-              v = __fadd_rn(v, bias);
-              if (p->relu) v = np_relu(v);
+#pragma unroll
+        for (int j4 = 0; j4 < 8; ++j4) {
+          float v[4];
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            const int jj = j4 * 4 + e, n = nh + cb + jj;
+            float x = sum[cb + jj];
+            if (OP == HNN_FWD) {
+              if (zero_row) x = 0.0f;
+              else {
+                if (n < p->n) x = __fadd_rn(x, __ldg(p->bias + n));
+                if (p->relu & 1) x = np_relu(x);
+              }
+            } else if (OP == HNN_DGRAD) {
+              if (zero_row) x = 0.0f;
+              else if (mrow && n < p->n) x = np_mask(x, __ldg(mrow + n));
             }
-          } else if (OP == HNN_DGRAD) {
-            if (row >= rows) v = 0.0f;
-            else if (p->mask && col_ok) v = np_mask(v, p->mask[size_t(row) * p->ldc + n]);
+            v[e] = x;
           }
-          if (col_ok) __stcg(p->c + size_t(row) * p->ldc + n, v);
+          sts128(stg + lane * 128 + ((j4 ^ (lane & 7)) << 4),
+                 make_uint4(__float_as_uint(v[0]), __float_as_uint(v[1]), __float_as_uint(v[2]), __float_as_uint(v[3])));
         }
         __syncwarp();
+        if (OP == HNN_WGRAD && p->opt_w != nullptr) {
+          // fused optimizer: lane = column, so W / moment accesses of a row are one coalesced
+          // 128-byte transaction; the gradient comes back out of the swizzled staging block
+          const Update u = make_update(cur[p->model], p->opt_kind, p->opt_momentum);
+          const int n = nh + cb + lane;
+          if (n < p->n) {
+            for (int rr = 0; rr < 32; ++rr) {
+              const int r = row0 + rr;
+              if (r >= p->m) break;
+              const float g = lds32(stg + rr * 128 + ((((lane >> 2) ^ (rr & 7))) << 4) + ((lane & 3) << 2));
+              const size_t off = size_t(r) * p->ldc + n;
+              float w = p->opt_w[off], mm = p->opt_wm ? p->opt_wm[off] : 0.0f, vv = p->opt_wv ? p->opt_wv[off] : 0.0f;
+              update_one(u, w, g, mm, vv);
+              p->opt_w[off] = w;
+              if (p->opt_wm) p->opt_wm[off] = mm;
+              if (p->opt_wv) p->opt_wv[off] = vv;
+            }
+          }
+          __syncwarp();
+        }
+        if (p->c != nullptr) {
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+          __syncwarp();
+          if (lane == 0) tma_store_2d(p->tmap_c, stg, nh + cb, row0);
+          ++nstore;
+        }
       }
     }
+    if (lane == 0) tma_store_wait_all();
   }
   tc_fence_before();
   __syncthreads();
@@ -384,17 +482,26 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   }
 }
 
-// dbias[i] = sum_{r<R} A[r*lda + i], sequential row order (numpy's axis-0 sum), one thread per column.
+// dbias[i] = sum_{r<R} A[r*lda + i], sequential row order (numpy's axis-0 sum), one thread per
+// column; with optimizer fusion the bias is updated here too.
 __global__ void colsum_kernel(const hnn_gemm_problem* __restrict__ probs, int nprob, const hnn_step_row* __restrict__ cur,
                               const hnn_model_status* __restrict__ status) {
   const hnn_gemm_problem& p = probs[blockIdx.y];
-  if (!p.dbias || !live(cur, status, p.model)) return;
+  if ((!p.dbias && !p.opt_b) || !live(cur, status, p.model)) return;
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= p.m) return;
   const int R = cur[p.model].rows;
   float acc = -0.0f;
   for (int r = 0; r < R; ++r) acc = __fadd_rn(acc, p.a[size_t(r) * p.lda + i]);
-  p.dbias[i] = acc;
+  if (p.dbias) p.dbias[i] = acc;
+  if (p.opt_b) {
+    const Update u = make_update(cur[p.model], p.opt_kind, p.opt_momentum);
+    float w = p.opt_b[i], m = p.opt_bm ? p.opt_bm[i] : 0.0f, v = p.opt_bv ? p.opt_bv[i] : 0.0f;
+    update_one(u, w, acc, m, v);
+    p.opt_b[i] = w;
+    if (p.opt_bm) p.opt_bm[i] = m;
+    if (p.opt_bv) p.opt_bv[i] = v;
+  }
 }
 
 // ---------------------------------------------------------------- host side
@@ -475,7 +582,7 @@ int grouped_gemm_tc(int op, const hnn_gemm_problem* probs, int nprob, int total_
 
 }  // namespace hnn
 
-// Encode the two TMA maps of every problem (host memory, 128 bytes each, A then B per problem).
+// Encode the three TMA maps of every problem (host memory, 128 bytes each: A, B, C per problem).
 extern "C" int hnn_gemm_tc_encode(int op, const hnn_gemm_problem* host_probs, int nprob, void* host_maps) {
   HNN_REQUIRE(host_probs && host_maps && nprob > 0, "hnn_gemm_tc_encode", "bad arguments");
   CUtensorMap* maps = reinterpret_cast<CUtensorMap*>(host_maps);
@@ -483,15 +590,17 @@ extern "C" int hnn_gemm_tc_encode(int op, const hnn_gemm_problem* host_probs, in
     const hnn_gemm_problem& p = host_probs[i];
     int rc;
     if (op == HNN_FWD) {          // A = X[cap, K] (K-major), B = W[N, K] (K-major)
-      rc = hnn::encode_2d(&maps[2 * i], p.a, p.k, p.m, p.lda, hnn::TC_BM, false);
-      if (!rc) rc = hnn::encode_2d(&maps[2 * i + 1], p.b, p.k, p.n, p.ldb, hnn::TC_BN, false);
+      rc = hnn::encode_2d(&maps[3 * i], p.a, p.k, p.m, p.lda, hnn::TC_BM, false);
+      if (!rc) rc = hnn::encode_2d(&maps[3 * i + 1], p.b, p.k, p.n, p.ldb, hnn::TC_BN, false);
     } else if (op == HNN_DGRAD) { // A = dY[cap, U] (K-major), B = W[U, N] (N-major)
-      rc = hnn::encode_2d(&maps[2 * i], p.a, p.k, p.m, p.lda, hnn::TC_BM, false);
-      if (!rc) rc = hnn::encode_2d(&maps[2 * i + 1], p.b, p.n, p.k, p.ldb, 32, true);
+      rc = hnn::encode_2d(&maps[3 * i], p.a, p.k, p.m, p.lda, hnn::TC_BM, false);
+      if (!rc) rc = hnn::encode_2d(&maps[3 * i + 1], p.b, p.n, p.k, p.ldb, 32, true);
     } else {                      // A = dY[cap, M] (M-major), B = X[cap, N] (N-major)
-      rc = hnn::encode_2d(&maps[2 * i], p.a, p.m, p.k, p.lda, 32, true);
-      if (!rc) rc = hnn::encode_2d(&maps[2 * i + 1], p.b, p.n, p.k, p.ldb, 32, true);
+      rc = hnn::encode_2d(&maps[3 * i], p.a, p.m, p.k, p.lda, 32, true);
+      if (!rc) rc = hnn::encode_2d(&maps[3 * i + 1], p.b, p.n, p.k, p.ldb, 32, true);
     }
+    // C (all ops): row-major [m, n] with row stride ldc; 32x32 boxes, 128-byte swizzle
+    if (!rc && p.c) rc = hnn::encode_2d(&maps[3 * i + 2], p.c, p.n, p.m, p.ldc, 32, false);
     if (rc) {
       hnn::set_error("hnn_gemm_tc_encode", "cuTensorMapEncodeTiled failed (alignment / stride / driver)");
       return rc;

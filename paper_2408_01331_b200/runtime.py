@@ -247,8 +247,12 @@ def C_addr_bytes(buf: bytearray) -> int:
 class DeviceHybrid:
     """Packed device state + launch plans for the models of one rank."""
 
-    def __init__(self, slots: list, device=None, use_tensor_cores: bool = True):
+    def __init__(self, slots: list, device=None, use_tensor_cores: bool = True, fuse_optimizer: bool = True,
+                 keep_grads: bool = False):
         torch = _torch()
+        # fuse_optimizer: dense layers apply SGD/Adam in their weight-gradient epilogue (the
+        # gradient never round-trips HBM); keep_grads: still store dW/db (tests, diagnostics)
+        self.fuse_optimizer, self.keep_grads = fuse_optimizer, keep_grads
         N.load()
         if not torch.cuda.is_available():
             raise HybridnnError("no CUDA device: the hybrid trainer has no CPU fallback")
@@ -457,7 +461,7 @@ class DeviceHybrid:
             return False
         if any(d[k] % 4 for k in ("lda", "ldb", "ldc")):
             return False
-        return all(d[k] % 16 == 0 for k in ("a", "b"))
+        return all(d[k] % 16 == 0 for k in ("a", "b", "c"))
 
     def _gemm_launch(self, op, items, label):
         """items: list of (slot, stage).  Splits into SIMT / 3xTF32 launches."""
@@ -476,8 +480,19 @@ class DeviceHybrid:
             else:
                 gw = self.pview(self.grads, s.index, st.params[0])
                 gb = self.pview(self.grads, s.index, st.params[1])
-                d = dict(a=_ptr(st.dy), b=_ptr(st.x), c=_ptr(gw), bias=0, mask=0, dbias=_ptr(gb), m=U, n=K, k=cap,
-                         lda=st.ld_out, ldb=st.ld_in, ldc=K, relu=0)
+                fuse = self._fused(s)
+                keep = self.keep_grads or not fuse
+                d = dict(a=_ptr(st.dy), b=_ptr(st.x), c=_ptr(gw) if keep else 0, bias=0, mask=0,
+                         dbias=_ptr(gb) if keep else 0, m=U, n=K, k=cap, lda=st.ld_out, ldb=st.ld_in, ldc=K, relu=0)
+                if fuse:
+                    kind = s.opt_kind
+                    arena = lambda a, pid: _ptr(self.pview(a, s.index, pid)) if a is not None else 0
+                    d.update(opt_w=arena(self.params, st.params[0]), opt_b=arena(self.params, st.params[1]),
+                             opt_wm=arena(self.m1, st.params[0]) if kind != N.OPT_SGD else 0,
+                             opt_bm=arena(self.m1, st.params[1]) if kind != N.OPT_SGD else 0,
+                             opt_wv=arena(self.m2, st.params[0]) if kind == N.OPT_ADAM else 0,
+                             opt_bv=arena(self.m2, st.params[1]) if kind == N.OPT_ADAM else 0,
+                             opt_kind=kind, opt_momentum=float(np.float32(s.momentum)))
             if self.use_tc and self._route_tc(op, d):
                 prec = N.PREC_3XTF32
             else:
@@ -498,17 +513,21 @@ class DeviceHybrid:
             keep = None
             if prec == N.PREC_3XTF32:
                 torch = _torch()
-                maps = bytearray(128 * 2 * len(probs))
+                maps = bytearray(128 * 3 * len(probs))
                 host = (N.GemmProblem * len(probs))(*probs)
                 N.call("hnn_gemm_tc_encode", op, C_addr(host), len(probs), C_addr_bytes(maps))
                 keep = torch.frombuffer(maps, dtype=torch.uint8).to(self.device)
                 for i, pr in enumerate(probs):
-                    pr.tmap_a = _ptr(keep) + 256 * i
-                    pr.tmap_b = _ptr(keep) + 256 * i + 128
+                    pr.tmap_a = _ptr(keep) + 384 * i
+                    pr.tmap_b = _ptr(keep) + 384 * i + 128
+                    pr.tmap_c = _ptr(keep) + 384 * i + 256
             t = _dev_table(N.GemmProblem, probs, self.device)
             flops = sum(2 * d["m"] * d["n"] * d["k"] for _, d in rows)
-            # bytes: A + B read once, C written once (fp32)
-            nbytes = sum(4 * (d["m"] * d["k"] + d["k"] * d["n"] + d["m"] * d["n"]) for _, d in rows)
+            # bytes: A + B read once, C written once (fp32); a fused optimizer adds its p/m/v traffic
+            nbytes = sum(4 * (d["m"] * d["k"] + d["k"] * d["n"] + (d["m"] * d["n"] if d.get("c") else 0))
+                         for _, d in rows)
+            per_param = {N.OPT_SGD: 8, N.OPT_SGD_MOMENTUM: 16, N.OPT_ADAM: 24}
+            nbytes += sum(per_param[d["opt_kind"]] * d["m"] * (d["n"] + 1) for _, d in rows if d.get("opt_w"))
             launch = Launch("hnn_grouped_gemm", (op, prec, _ptr(t), len(probs), base, _ptr(self.cur),
                                                  _ptr(self.status)), t,
                             f"{label}/{ {N.PREC_SIMT: 'simt', N.PREC_SIMT_SKINNY: 'simt16', N.PREC_3XTF32: 'tc'}[prec] }",
@@ -620,19 +639,43 @@ class DeviceHybrid:
                                         _ptr(self.loss_out), _ptr(self.correct_out)), t,
                       "sce" if train else "sce/eval", nbytes=nbytes)
 
+    def _fused(self, s) -> bool:
+        """Dense weight gradients of model s feed the optimizer inside their epilogue.
+
+        Only for SGD / momentum (a multiply-subtract per element): Adam's three IEEE
+        divisions and square root per element would leave the tensor-core pipeline waiting
+        on eight epilogue warps (measured 2.5x slower), so Adam keeps the full-occupancy
+        multi-tensor kernel."""
+        return self.fuse_optimizer and s.opt_kind != N.OPT_ADAM
+
+    def _unfused_ranges(self, s) -> list:
+        """(offset, count) arena ranges of model s updated by the multi-tensor kernel."""
+        if not self._fused(s):
+            return [(s.seg_off, s.seg_len)]
+        fused = {pid for st in s.stages if st.kind == "dense" for pid in st.params}
+        out = []
+        for pid, shp in s.specs.items():
+            if pid in fused:
+                continue
+            off, cnt = s.offsets[pid], _align4(int(np.prod(shp)))
+            if out and out[-1][0] + out[-1][1] == off:
+                out[-1] = (out[-1][0], out[-1][1] + cnt)
+            else:
+                out.append((off, cnt))
+        return out
+
     def _optimizer_launch(self):
         segs, base = [], 0
         for s in self.slots:
-            if s.seg_len == 0:
-                continue
-            chunks = -(-s.seg_len // OPT_CHUNK)
             kind = s.opt_kind
-            segs.append(N.OptSegment(
-                _ptr(self.params) + 4 * s.seg_off, _ptr(self.grads) + 4 * s.seg_off,
-                (_ptr(self.m1) + 4 * s.seg_off) if kind != N.OPT_SGD else 0,
-                (_ptr(self.m2) + 4 * s.seg_off) if kind == N.OPT_ADAM else 0,
-                s.seg_len, s.index, kind, float(np.float32(s.momentum)), base, chunks, 0))
-            base += chunks
+            for off, cnt in self._unfused_ranges(s):
+                chunks = -(-cnt // OPT_CHUNK)
+                segs.append(N.OptSegment(
+                    _ptr(self.params) + 4 * off, _ptr(self.grads) + 4 * off,
+                    (_ptr(self.m1) + 4 * off) if kind != N.OPT_SGD else 0,
+                    (_ptr(self.m2) + 4 * off) if kind == N.OPT_ADAM else 0,
+                    cnt, s.index, kind, float(np.float32(s.momentum)), base, chunks, 0))
+                base += chunks
         if not segs:
             return []
         t = _dev_table(N.OptSegment, segs, self.device)
@@ -650,16 +693,17 @@ class DeviceHybrid:
         bwd = []
         for w in range(len(waves) - 1, -1, -1):
             items = waves[w]
-            wg = [(s, st) for s, st in items if st.kind in ("dense", "conv")]
-            if wg:
-                for kind in ("dense", "conv"):
-                    grp = [(s, st) for s, st in wg if st.kind == kind]
-                    if grp:
-                        bwd += (self._gemm_launch(N.HNN_WGRAD, grp, f"bwd{w}/dense/wgrad") if kind == "dense"
-                                else self._conv_launch(N.HNN_WGRAD, grp, f"bwd{w}/conv/wgrad"))
+            # input gradients first: with optimizer fusion the weight-gradient launch updates W in
+            # place, and this wave's DGRAD must still read the pre-update W (src/engine.py:120-151
+            # computes every gradient before apply_update)
             dg = [(s, st) for s, st in items if st.needs_dx]
             if dg:
                 bwd += self._wave_launches(N.HNN_DGRAD, dg, f"bwd{w}")
+            for kind in ("dense", "conv"):
+                grp = [(s, st) for s, st in items if st.kind == kind]
+                if grp:
+                    bwd += (self._gemm_launch(N.HNN_WGRAD, grp, f"bwd{w}/dense/wgrad") if kind == "dense"
+                            else self._conv_launch(N.HNN_WGRAD, grp, f"bwd{w}/conv/wgrad"))
         self.forward_plan = fwd
         self.train_plan = [self._gather_train] + fwd + [self._sce_launch(True)] + bwd + self._optimizer_launch()
         self.eval_plan = [self._gather_eval] + fwd + [self._sce_launch(False)]

@@ -182,7 +182,7 @@ class Trainer:
     def __init__(self, hybrid: HybridModel, plan, jobs: list, datasets: dict, completion_sink=None,
                  pause_sink=None, pause_poll=None, step_observer=None, slice_observer=None, *,
                  use_graph: bool = True, use_tensor_cores: bool = True, device=None, comm=None,
-                 loss_observer=None):
+                 loss_observer=None, fuse_optimizer: bool = True, keep_grads: bool = False):
         self.hybrid = hybrid
         self.plan = plan
         jobs = [TrainingJob.coerce(j) for j in jobs]
@@ -193,6 +193,7 @@ class Trainer:
         # loss_observer(job_id, step, loss, correct): per-step device losses (forces one-step windows)
         self.loss_observer = loss_observer
         self.use_graph, self.use_tc, self.device_name, self.comm = use_graph, use_tensor_cores, device, comm
+        self.fuse_optimizer, self.keep_grads = fuse_optimizer, keep_grads
         self._pause_requests: set = set()
         self.results = {j.job_id: JobResult(job_id=j.job_id, epochs_completed=j.completed_epochs) for j in jobs}
         self.checkpoints: dict = {}
@@ -221,7 +222,8 @@ class Trainer:
         return out
 
     def _device(self):
-        dev = self.hybrid.materialize(self.device_name, use_tensor_cores=self.use_tc)
+        dev = self.hybrid.materialize(self.device_name, use_tensor_cores=self.use_tc,
+                                      fuse_optimizer=self.fuse_optimizer, keep_grads=self.keep_grads)
         for jid, sub in self.hybrid.sub_models.items():
             opt = sub.optimizer
             if opt.m1 or opt.m2 or opt.velocity:

@@ -145,7 +145,8 @@ class HybridModel:
         else:
             self.device.upload_params(sub.slot, bare)
 
-    def materialize(self, device=None, use_tensor_cores: bool = True):
+    def materialize(self, device=None, use_tensor_cores: bool = True, fuse_optimizer: bool = True,
+                    keep_grads: bool = False):
         """Pack every sub-model into device arenas (idempotent)."""
         if self.device is not None:
             return self.device
@@ -157,7 +158,8 @@ class HybridModel:
             hp = sub.hypers
             slots.append(ModelSlot(i, jid, sub.original, hp.batch_size if hp else 1, sub.optimizer.kind,
                                    sub.optimizer.momentum, engine.param_specs(sub.original)))
-        dev = DeviceHybrid(slots, device=device, use_tensor_cores=use_tensor_cores)
+        dev = DeviceHybrid(slots, device=device, use_tensor_cores=use_tensor_cores, fuse_optimizer=fuse_optimizer,
+                           keep_grads=keep_grads)
         for jid, sub in self.sub_models.items():
             dev.upload_params(sub.slot, {unqualify(jid, pid): self._host_params[pid] for pid in sub.param_ids()})
         self.device = dev

@@ -319,7 +319,7 @@ def test_separation_layout_and_roundtrip(pkg):
         pkg.separate(h, "nope")
 
 
-def _first_step_grads(pkg, name, tc):
+def _first_step_grads(pkg, name, tc, fuse=True):
     arr, c, graph, splits, digest = load_case(name)
     from paper_2408_01331_b200 import store
 
@@ -327,7 +327,8 @@ def _first_step_grads(pkg, name, tc):
     job = pkg.TrainingJob(name, graph, digest, pkg.HyperParams(1, c["batch"], c["lr"], c["opt"], (), c["seed"]), 0, 0)
     h = pkg.merge([job])
     grabbed = {}
-    tr = pkg.Trainer(h, pkg.make_plan("fcfs", [job]), [job], {name: ds}, use_tensor_cores=tc)
+    tr = pkg.Trainer(h, pkg.make_plan("fcfs", [job]), [job], {name: ds}, use_tensor_cores=tc, keep_grads=True,
+                     fuse_optimizer=fuse)
     tr.step_observer = lambda j, p: grabbed or grabbed.update(
         grads=tr.device.download_grads(0), params={k.split("/", 1)[1]: v for k, v in p.items()})
     tr.run()
@@ -349,10 +350,12 @@ def test_step_gradients_match_oracle(pkg, name):
         assert any(l.endswith("/tc") for l in labels)
 
 
-@pytest.mark.parametrize("name", ["c3_mlp", "c1_mlp", "deep_adam"])
-def test_optimizer_is_bit_exact_given_gradients(pkg, name):
-    """The multi-tensor SGD/Adam kernel reproduces apply_update bit for bit (src/optim.py:52-87)."""
-    got, _, (arr, c, graph, splits, digest) = _first_step_grads(pkg, name, True)
+@pytest.mark.parametrize("fuse", [True, False])
+@pytest.mark.parametrize("name", ["c3_mlp", "c1_mlp", "deep_adam", "lenet"])
+def test_optimizer_is_bit_exact_given_gradients(pkg, name, fuse):
+    """SGD/Adam — fused into the weight-gradient epilogue or the stand-alone multi-tensor kernel —
+    reproduces apply_update bit for bit given the same gradients (src/optim.py:52-87)."""
+    got, _, (arr, c, graph, splits, digest) = _first_step_grads(pkg, name, True, fuse)
     params = oracle.init_model(graph, c["seed"])
     opt = oracle.OracleOptimizer(c["opt"])
     opt.apply(params, {k: v.copy() for k, v in got["grads"].items()}, c["lr"])

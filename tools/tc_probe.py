@@ -47,12 +47,12 @@ def run(op, prec, M, Nn, K, rows=None, seed=0, dbg=0):
                          dbias=_ptr(db) if op == 2 else 0, model=0, relu=dbg << 8, tile_base=0, tiles_n=tiles_n, **d)
     keep = None
     if prec == N.PREC_3XTF32:
-        maps = bytearray(256)
+        maps = bytearray(384)
         host = (N.GemmProblem * 1)(prob)
         N.call("hnn_gemm_tc_encode", op, ctypes.addressof(host), 1,
-               ctypes.addressof((ctypes.c_char * 256).from_buffer(maps)))
+               ctypes.addressof((ctypes.c_char * 384).from_buffer(maps)))
         keep = torch.frombuffer(maps, dtype=torch.uint8).to(dev)
-        prob.tmap_a, prob.tmap_b = _ptr(keep), _ptr(keep) + 128
+        prob.tmap_a, prob.tmap_b, prob.tmap_c = _ptr(keep), _ptr(keep) + 128, _ptr(keep) + 256
     t = _dev_table(N.GemmProblem, [prob], dev)
     r = np.zeros(1, STEP_DTYPE); r["active"] = 1; r["rows"] = rows
     cur = torch.from_numpy(r.view(np.uint8).copy()).to(dev)
@@ -73,6 +73,21 @@ def run(op, prec, M, Nn, K, rows=None, seed=0, dbg=0):
     err = np.abs(got - ref) / (np.abs(ref).max() + 1e-30)
     return float(err.max()), got, ref
 
+
+if __name__ == "__main__" and len(sys.argv) > 1 and sys.argv[1] == "bisect":
+    TIME = True
+    for shape in ((256, 2048, 2048), (2048, 2048, 256)):
+        for dbg in (0,):
+            print("dbg", dbg, "(1: no lo MMAs, 2: no conversion, 4: no stores, 8: no promotion)")
+            run(0, 1, *shape, dbg=dbg)
+    sys.exit(0)
+
+if __name__ == "__main__" and len(sys.argv) > 1 and sys.argv[1] == "trunc":
+    for op in (0, 1, 2):
+        for dbg in (0, 1):
+            e, got, ref = run(op, 1, 256, 384, 784, dbg=dbg)
+            print(f"op={op} raw-hi={dbg} maxrel={e:.3e}")
+    sys.exit(0)
 
 if __name__ == "__main__" and len(sys.argv) > 1 and sys.argv[1] == "time":
     TIME = True
