@@ -12,7 +12,8 @@
  *   hnn_grouped_gemm            dense fwd / bwd  _dense_fwd, _dense_bwd (ops.py:46-55) with
  *                               relu fwd/bwd fused (ops.py:62-67); fp32 SIMT or tcgen05 3xTF32
  *   hnn_gemm_tc_encode          host-side TMA descriptors for the tcgen05 path
- *   hnn_grouped_conv            conv2d fwd / bwd _conv2d_fwd, _conv2d_bwd (ops.py:100-130)
+ *   hnn_grouped_conv            conv2d fwd / bwd _conv2d_fwd, _conv2d_bwd (ops.py:100-130), implicit GEMM
+ *   hnn_grouped_conv_direct     the same for small channel counts, direct (one thread per output)
  *   hnn_conv_wgrad_reduce       the fixed-order finish of the conv weight/bias gradient
  *   hnn_grouped_maxpool         maxpool2d fwd / bwd (ops.py:149-174), relu mask fused
  *   hnn_grouped_relu            stand-alone relu fwd / bwd (ops.py:62-67)
@@ -190,6 +191,18 @@ int hnn_conv_tile_shape(int op, int32_t* tile_m, int32_t* tile_n);
 
 int hnn_grouped_conv(int op, const hnn_conv_problem* probs, int nprob, int total_tiles, const hnn_step_row* cur,
                      const hnn_model_status* status, void* stream);
+
+/*
+ * Direct (non-GEMM) convolution for small layers (LeNet-class: one sample's activations and the
+ * filters fit in shared memory; at most 16*256 weights): one CTA per sample (FWD, DGRAD) or per
+ * chunk of HNN_CONV_DIRECT_BCHUNK samples (WGRAD partials, splits = ceil(cap / chunk), reduced by
+ * hnn_conv_wgrad_reduce).  tile_base counts CTAs; `smem` = max over the launch's problems of
+ * hnn_conv_direct_smem(op, ...).
+ */
+#define HNN_CONV_DIRECT_BCHUNK 4
+int hnn_conv_direct_smem(int op, int c, int h, int w, int f, int k, int oh, int ow);
+int hnn_grouped_conv_direct(int op, const hnn_conv_problem* probs, int nprob, int total_blocks, int smem,
+                            const hnn_step_row* cur, const hnn_model_status* status, void* stream);
 
 /* dw[f,:] = sum_s partial[s,f,:C*k*k] and db[f] = sum_s partial[s,f,C*k*k] in split order. */
 int hnn_conv_wgrad_reduce(const hnn_conv_problem* probs, int nprob, int total_blocks, const hnn_step_row* cur,

@@ -16,6 +16,7 @@ LIB_PATH = Path(__file__).resolve().parent / "_lib" / "libhnn_b200.so"
 HNN_FWD, HNN_DGRAD, HNN_WGRAD = 0, 1, 2
 PREC_SIMT, PREC_3XTF32, PREC_SIMT_SKINNY = 0, 1, 2
 OPT_SGD, OPT_SGD_MOMENTUM, OPT_ADAM = 0, 1, 2
+CONV_DIRECT_BCHUNK = 4
 
 P = C.c_uint64  # device pointers travel as integers
 I = C.c_int32
@@ -90,6 +91,8 @@ SIGNATURES = {
     "hnn_conv_tile_shape": [C.c_int, C.POINTER(I), C.POINTER(I)],
     "hnn_grouped_conv": [C.c_int, P, C.c_int, C.c_int, P, P, VP],
     "hnn_conv_wgrad_reduce": [P, C.c_int, C.c_int, P, P, VP],
+    "hnn_grouped_conv_direct": [C.c_int, P, C.c_int, C.c_int, C.c_int, P, P, VP],
+    "hnn_conv_direct_smem": [C.c_int] * 8,
     "hnn_grouped_maxpool": [C.c_int, P, C.c_int, C.c_int, P, P, VP],
     "hnn_grouped_relu": [C.c_int, P, C.c_int, C.c_int, P, P, VP],
     "hnn_sce_fused": [P, C.c_int, C.c_int, C.c_int, P, P, C.c_int, P, P, VP],
@@ -140,6 +143,17 @@ def conv_tile_shape(op: int) -> tuple:
     tm, tn = I(), I()
     call("hnn_conv_tile_shape", op, C.byref(tm), C.byref(tn))
     return tm.value, tn.value
+
+
+def conv_direct_smem(op, c, h, w, f, k, oh, ow) -> int:
+    return int(load().hnn_conv_direct_smem(op, c, h, w, f, k, oh, ow))
+
+
+def conv_direct_ok(c, h, w, f, k, oh, ow) -> bool:
+    """Whether a conv layer fits the direct (shared-memory, per-sample) kernels."""
+    if f * (c * k * k + 1) > 16 * 256:
+        return False
+    return all(conv_direct_smem(op, c, h, w, f, k, oh, ow) <= 200 * 1024 for op in (HNN_FWD, HNN_DGRAD, HNN_WGRAD))
 
 
 def table_bytes(cls, rows: list) -> bytes:

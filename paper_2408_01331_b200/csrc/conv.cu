@@ -213,3 +213,207 @@ extern "C" int hnn_conv_wgrad_reduce(const hnn_conv_problem* probs, int nprob, i
   hnn::conv_wgrad_reduce_kernel<<<total_blocks, 256, 0, hnn::as_stream(stream)>>>(probs, nprob, cur, status);
   return hnn::check_launch("hnn_conv_wgrad_reduce");
 }
+
+// ---------------------------------------------------------------------------------------------
+// Direct convolution for small layers (LeNet-class: one sample's activations plus the whole
+// filter bank fit in shared memory), where a 64x32 implicit-GEMM tile would be mostly padding.
+// One CTA per (problem, sample) for FWD / DGRAD and per (problem, batch chunk of
+// HNN_CONV_DIRECT_BCHUNK samples) for WGRAD; the sample's input (or output gradient) and the
+// filters are staged in shared memory and every thread sweeps outputs with fixed-order FMAs.
+// WGRAD writes per-chunk partials that hnn_conv_wgrad_reduce sums in chunk order (no atomics).
+// probs[i].tile_base counts CTAs.
+namespace hnn {
+
+constexpr int DTHREADS = 256;
+
+__device__ __forceinline__ void stage(float* dst, const float* __restrict__ src, int n) {
+  for (int i = threadIdx.x; i < n; i += blockDim.x) dst[i] = __ldg(src + i);
+}
+
+template <int OP>
+__global__ void __launch_bounds__(DTHREADS) conv_direct_kernel(const hnn_conv_problem* __restrict__ probs, int nprob,
+                                                               const hnn_step_row* __restrict__ cur,
+                                                               const hnn_model_status* __restrict__ status) {
+  extern __shared__ float sm[];
+  const int pi = find_problem(probs, nprob, blockIdx.x, [](const hnn_conv_problem& q) { return q.tile_base; });
+  const hnn_conv_problem& p = probs[pi];
+  if (!live(cur, status, p.model)) return;
+  const ConvGeom g(p);
+  const int rows = cur[p.model].rows;
+  const int unit = blockIdx.x - p.tile_base;  // sample (FWD/DGRAD) or batch chunk (WGRAD)
+  if (OP == HNN_FWD) {
+    const int b = unit;
+    float* yb = p.y + size_t(b) * g.f * g.ohw;
+    if (b >= rows) {
+      for (int e = threadIdx.x; e < g.f * g.ohw; e += blockDim.x) yb[e] = 0.0f;
+      return;
+    }
+    float* xs = sm;                 // [C][H][W]
+    float* ws = sm + g.c * g.hw;    // [F][C*k*k]
+    stage(xs, p.x + size_t(b) * g.c * g.hw, g.c * g.hw);
+    stage(ws, p.weight, g.f * g.ckk);
+    __syncthreads();
+    for (int e = threadIdx.x; e < g.f * g.ohw; e += blockDim.x) {
+      const int f = e / g.ohw, opix = e - f * g.ohw;
+      const int oy = opix / g.ow, ox = opix - oy * g.ow;
+      const int y0 = oy * g.s - g.pad, x0 = ox * g.s - g.pad;
+      const int i0 = max(0, -y0), i1 = min(g.k, g.h - y0), j0 = max(0, -x0), j1 = min(g.k, g.w - x0);
+      const float* wf = ws + f * g.ckk;
+      float acc = 0.0f;
+      for (int c = 0; c < g.c; ++c) {
+        const float* xc = xs + c * g.hw + y0 * g.w + x0;
+        const float* wc = wf + c * g.kk2;
+        for (int i = i0; i < i1; ++i)
+          for (int j = j0; j < j1; ++j) acc = fmaf(xc[i * g.w + j], wc[i * g.k + j], acc);
+      }
+      float v = __fadd_rn(acc, __ldg(p.bias + f));
+      if (p.relu) v = np_relu(v);
+      yb[e] = v;
+    }
+  } else if (OP == HNN_DGRAD) {
+    const int b = unit;
+    float* dxb = p.dx + size_t(b) * g.c * g.hw;
+    if (b >= rows) {
+      for (int e = threadIdx.x; e < g.c * g.hw; e += blockDim.x) dxb[e] = 0.0f;
+      return;
+    }
+    float* ds = sm;                  // [F][OH][OW]
+    float* ws = sm + g.f * g.ohw;    // [F][C][k][k]
+    stage(ds, p.dy + size_t(b) * g.f * g.ohw, g.f * g.ohw);
+    stage(ws, p.weight, g.f * g.ckk);
+    __syncthreads();
+    const float* mb = p.mask ? p.mask + size_t(b) * g.c * g.hw : nullptr;
+    for (int e = threadIdx.x; e < g.c * g.hw; e += blockDim.x) {
+      const int c = e / g.hw, pix = e - c * g.hw;
+      const int y = pix / g.w, x = pix - y * g.w;
+      // taps i with (y + pad - i) divisible by s and 0 <= (y + pad - i)/s < OH, ascending i;
+      // oy steps down by one per tap (no division in the loop)
+      const int ry = (y + g.pad) % g.s, rx = (x + g.pad) % g.s;
+      const int oy_first = (y + g.pad - ry) / g.s, ox_first = (x + g.pad - rx) / g.s;
+      float acc = 0.0f;
+      for (int f = 0; f < g.f; ++f) {
+        const float* df = ds + f * g.ohw;
+        const float* wfc = ws + (f * g.c + c) * g.kk2;
+        for (int i = ry, oy = oy_first; i < g.k && oy >= 0; i += g.s, --oy) {
+          if (oy >= g.oh) continue;
+          const float* drow = df + oy * g.ow;
+          const float* wrow = wfc + i * g.k;
+          for (int j = rx, ox = ox_first; j < g.k && ox >= 0; j += g.s, --ox) {
+            if (ox >= g.ow) continue;
+            acc = fmaf(drow[ox], wrow[j], acc);
+          }
+        }
+      }
+      dxb[e] = mb ? np_mask(acc, mb[e]) : acc;
+    }
+  } else {
+    // WGRAD: the CTA stages its chunk of samples (inputs with a padded, bank-conflict-free
+    // layout: row stride W+1, channel stride H*(W+1)+1); thread t owns weights t, t+256, ...
+    // and sweeps the valid output window of each staged sample in order.
+    constexpr int MAXW = 16;
+    const int cols = g.ckk + 1, nw = g.f * cols;
+    const int rs = g.w + 1, cs = g.h * rs + 1;
+    const int b0 = unit * HNN_CONV_DIRECT_BCHUNK, nb = max(0, min(HNN_CONV_DIRECT_BCHUNK, rows - b0));
+    float* xs = sm;                                            // [nb][C] x (H x rs), channel stride cs
+    float* ds = sm + HNN_CONV_DIRECT_BCHUNK * g.c * cs;        // [nb][F][OH][OW]
+    for (int e = threadIdx.x; e < nb * g.c * g.hw; e += blockDim.x) {
+      const int pc = e / g.hw, pix = e - pc * g.hw, y = pix / g.w, x = pix - y * g.w;
+      xs[pc * cs + y * rs + x] = __ldg(p.x + size_t(b0) * g.c * g.hw + e);
+    }
+    stage(ds, p.dy + size_t(b0) * g.f * g.ohw, nb * g.f * g.ohw);
+    __syncthreads();
+    float acc[MAXW];
+#pragma unroll
+    for (int q = 0; q < MAXW; ++q) acc[q] = 0.0f;
+#pragma unroll
+    for (int q = 0; q < MAXW; ++q) {
+      const int wi = threadIdx.x + q * DTHREADS;
+      if (wi >= nw) break;
+      const int f = wi / cols, col = wi - f * cols;
+      float a = 0.0f;
+      if (col == g.ckk) {
+        for (int sb = 0; sb < nb; ++sb) {
+          const float* df = ds + (sb * g.f + f) * g.ohw;
+          for (int t = 0; t < g.ohw; ++t) a = __fadd_rn(a, df[t]);
+        }
+      } else {
+        const int c = col / g.kk2, r = col - c * g.kk2, i = r / g.k, j = r - i * g.k;
+        const int ny = g.h - 1 + g.pad - i, nx = g.w - 1 + g.pad - j;
+        const int oy0 = max(0, (g.pad - i + g.s - 1) / g.s), oy1 = ny < 0 ? 0 : min(g.oh, ny / g.s + 1);
+        const int ox0 = max(0, (g.pad - j + g.s - 1) / g.s), ox1 = nx < 0 ? 0 : min(g.ow, nx / g.s + 1);
+        // four interleaved partial sums (ox residues mod 4) hide the shared-memory latency of
+        // the dependent FMA chain; they are combined in a fixed order, so results stay deterministic
+        float a4[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+        for (int sb = 0; sb < nb; ++sb) {
+          const float* df = ds + (sb * g.f + f) * g.ohw;
+          const float* xc = xs + (sb * g.c + c) * cs + (i - g.pad) * rs + (j - g.pad);
+          for (int oy = oy0; oy < oy1; ++oy) {
+            const float* xr = xc + oy * g.s * rs;
+            const float* dr = df + oy * g.ow;
+            int ox = ox0;
+            for (; ox + 3 < ox1; ox += 4) {
+              a4[0] = fmaf(dr[ox], xr[ox * g.s], a4[0]);
+              a4[1] = fmaf(dr[ox + 1], xr[(ox + 1) * g.s], a4[1]);
+              a4[2] = fmaf(dr[ox + 2], xr[(ox + 2) * g.s], a4[2]);
+              a4[3] = fmaf(dr[ox + 3], xr[(ox + 3) * g.s], a4[3]);
+            }
+            for (; ox < ox1; ++ox) a4[ox & 3] = fmaf(dr[ox], xr[ox * g.s], a4[ox & 3]);
+          }
+        }
+        a = __fadd_rn(__fadd_rn(a4[0], a4[1]), __fadd_rn(a4[2], a4[3]));
+      }
+      acc[q] = a;
+    }
+#pragma unroll
+    for (int q = 0; q < MAXW; ++q) {
+      const int wi = threadIdx.x + q * DTHREADS;
+      if (wi >= nw) break;
+      p.partial[size_t(unit) * nw + wi] = acc[q];  // == partial[(split * F + f) * cols + col]
+    }
+  }
+}
+
+// Shared-memory bytes a problem needs on the direct path (host and device agree on this).
+__host__ __device__ inline int conv_direct_smem(int op, int c, int h, int w, int f, int k, int oh, int ow) {
+  const int ckk = c * k * k;
+  if (op == HNN_FWD) return 4 * (c * h * w + f * ckk);
+  if (op == HNN_DGRAD) return 4 * (f * oh * ow + f * ckk);
+  return 4 * HNN_CONV_DIRECT_BCHUNK * (c * (h * (w + 1) + 1) + f * oh * ow);
+}
+
+}  // namespace hnn
+
+extern "C" int hnn_conv_direct_smem(int op, int c, int h, int w, int f, int k, int oh, int ow) {
+  return hnn::conv_direct_smem(op, c, h, w, f, k, oh, ow);
+}
+
+extern "C" int hnn_grouped_conv_direct(int op, const hnn_conv_problem* probs, int nprob, int total_blocks, int smem,
+                                       const hnn_step_row* cur, const hnn_model_status* status, void* stream) {
+  HNN_REQUIRE(probs && cur && nprob > 0 && total_blocks > 0, "hnn_grouped_conv_direct", "bad arguments");
+  HNN_REQUIRE(smem > 0 && smem <= 200 * 1024, "hnn_grouped_conv_direct", "layer too large for the direct path");
+  cudaStream_t s = hnn::as_stream(stream);
+  static int configured[3] = {0, 0, 0};
+  if (op == HNN_FWD) {
+    if (smem > configured[0]) {
+      cudaFuncSetAttribute(hnn::conv_direct_kernel<HNN_FWD>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+      configured[0] = 200 * 1024;
+    }
+    hnn::conv_direct_kernel<HNN_FWD><<<total_blocks, hnn::DTHREADS, smem, s>>>(probs, nprob, cur, status);
+  } else if (op == HNN_DGRAD) {
+    if (smem > configured[1]) {
+      cudaFuncSetAttribute(hnn::conv_direct_kernel<HNN_DGRAD>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+      configured[1] = 200 * 1024;
+    }
+    hnn::conv_direct_kernel<HNN_DGRAD><<<total_blocks, hnn::DTHREADS, smem, s>>>(probs, nprob, cur, status);
+  } else if (op == HNN_WGRAD) {
+    if (smem > configured[2]) {
+      cudaFuncSetAttribute(hnn::conv_direct_kernel<HNN_WGRAD>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+      configured[2] = 200 * 1024;
+    }
+    hnn::conv_direct_kernel<HNN_WGRAD><<<total_blocks, hnn::DTHREADS, smem, s>>>(probs, nprob, cur, status);
+  } else {
+    hnn::set_error("hnn_grouped_conv_direct", "unknown op");
+    return HNN_ERR_INVALID;
+  }
+  return hnn::check_launch("hnn_grouped_conv_direct");
+}

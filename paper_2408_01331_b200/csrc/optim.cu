@@ -10,6 +10,21 @@
 
 namespace hnn {
 
+// weak, non-coherent 16-byte loads (every element is read then written by the same thread, and
+// nothing else touches the arenas during the launch) and evict-first streaming stores
+__device__ __forceinline__ float4 ld_nc4(const float4* p) {
+  float4 v;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.f32 {%0, %1, %2, %3}, [%4];"
+               : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+               : "l"(p));
+  return v;
+}
+
+__device__ __forceinline__ void st_cs4(float4* p, float4 v) {
+  asm volatile("st.global.cs.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(p), "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w)
+               : "memory");
+}
+
 constexpr int OPT_THREADS = 256, OPT_CHUNK = 4096;  // 4 float4 per thread
 
 // Persistent grid-stride walk over the 4096-float chunks of all segments (chunk ids are
@@ -36,11 +51,11 @@ __global__ void __launch_bounds__(OPT_THREADS) multi_tensor_kernel(const hnn_opt
       const int i = threadIdx.x + q * OPT_THREADS;
       if (i < n4) {
         // explicit global-space accesses (the segment pointers come from memory, so a plain
-        // dereference compiles to generic LD/ST); gradients are read once -> evict-first
-        P[q] = __ldcg(p4 + i);
-        G[q] = __ldcs(g4 + i);
-        if (u.kind != HNN_OPT_SGD) M[q] = __ldcg(m4 + i);
-        if (u.kind == HNN_OPT_ADAM) V[q] = __ldcg(v4 + i);
+        // dereference would compile to generic LD/ST)
+        P[q] = ld_nc4(p4 + i);
+        G[q] = ld_nc4(g4 + i);
+        if (u.kind != HNN_OPT_SGD) M[q] = ld_nc4(m4 + i);
+        if (u.kind == HNN_OPT_ADAM) V[q] = ld_nc4(v4 + i);
       }
     }
 #pragma unroll
@@ -51,9 +66,9 @@ __global__ void __launch_bounds__(OPT_THREADS) multi_tensor_kernel(const hnn_opt
       update_one(u, P[q].y, G[q].y, M[q].y, V[q].y);
       update_one(u, P[q].z, G[q].z, M[q].z, V[q].z);
       update_one(u, P[q].w, G[q].w, M[q].w, V[q].w);
-      __stcg(p4 + i, P[q]);
-      if (u.kind != HNN_OPT_SGD) __stcg(m4 + i, M[q]);
-      if (u.kind == HNN_OPT_ADAM) __stcg(v4 + i, V[q]);
+      st_cs4(p4 + i, P[q]);
+      if (u.kind != HNN_OPT_SGD) st_cs4(m4 + i, M[q]);
+      if (u.kind == HNN_OPT_ADAM) st_cs4(v4 + i, V[q]);
     }
   }
 }

@@ -69,25 +69,35 @@ def _conv(op, x, w, b, y, dy, dx, attrs, rows, dw=None, db=None):
     f, _, k, _ = w.shape
     s, p = attrs.get("stride", 1), attrs.get("padding", 0)
     oh, ow = conv_extent(h, k, s, p), conv_extent(wd, k, s, p)
+    direct = N.conv_direct_ok(c, h, wd, f, k, oh, ow)
     split_len = 2048
-    splits = -(-n * oh * ow // split_len)
+    splits = -(-n // N.CONV_DIRECT_BCHUNK) if direct else -(-n * oh * ow // split_len)
     partial = torch.zeros(splits * f * (c * k * k + 1), dtype=torch.float32, device=x.device)
     common = dict(x=_ptr(x), weight=_ptr(w), bias=_ptr(b), y=_ptr(y), dy=_ptr(dy), dx=_ptr(dx), mask=0,
                   partial=_ptr(partial), dw=_ptr(dw), db=_ptr(db), cap=n, c=c, h=h, w=wd, f=f, k=k, stride=s,
                   pad=p, oh=oh, ow=ow, model=0, relu=0, splits=splits, split_len=split_len)
-    tm, tn = N.conv_tile_shape(op)
-    if op == N.HNN_FWD:
-        tiles_n, tiles = -(-f // tn), -(-(n * oh * ow) // tm) * -(-f // tn)
-    elif op == N.HNN_DGRAD:
-        tiles_n, tiles = -(-c // tn), -(-(n * h * wd) // tm) * -(-c // tn)
+    cols = c * k * k + 1
+    if direct:
+        tiles_n = 1
+        tiles = splits if op == N.HNN_WGRAD else n
     else:
-        tiles_n = -(-(c * k * k + 1) // tn)
-        tiles = splits * -(-f // tm) * tiles_n
+        tm, tn = N.conv_tile_shape(op)
+        if op == N.HNN_FWD:
+            tiles_n, tiles = -(-f // tn), -(-(n * oh * ow) // tm) * -(-f // tn)
+        elif op == N.HNN_DGRAD:
+            tiles_n, tiles = -(-c // tn), -(-(n * h * wd) // tm) * -(-c // tn)
+        else:
+            tiles_n = -(-cols // tn)
+            tiles = splits * -(-f // tm) * tiles_n
     t = _dev_table(N.ConvProblem, [N.ConvProblem(tile_base=0, tiles_n=tiles_n, **common)], x.device)
     cur = _cur(rows)
-    N.call("hnn_grouped_conv", op, _ptr(t), 1, tiles, _ptr(cur), 0, _stream())
+    if direct:
+        N.call("hnn_grouped_conv_direct", op, _ptr(t), 1, tiles, N.conv_direct_smem(op, c, h, wd, f, k, oh, ow),
+               _ptr(cur), 0, _stream())
+    else:
+        N.call("hnn_grouped_conv", op, _ptr(t), 1, tiles, _ptr(cur), 0, _stream())
     if op == N.HNN_WGRAD:
-        nblk = -(-(f * (c * k * k + 1)) // 256)
+        nblk = -(-(f * cols) // 256)
         N.call("hnn_conv_wgrad_reduce", _ptr(t), 1, nblk, _ptr(cur), 0, _stream())
     torch.cuda.current_stream().synchronize()
 

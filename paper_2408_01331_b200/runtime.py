@@ -332,7 +332,10 @@ class DeviceHybrid:
                     c, h, w = st.in_shape
                     f, oh, ow = self._conv_out(st)
                     k = st.attrs["kernel"]
-                    st.splits = -(-cap * oh * ow // CONV_SPLIT_LEN)
+                    # small layers (LeNet-class) use the direct shared-memory kernels
+                    st.direct = N.conv_direct_ok(c, h, w, f, k, oh, ow)
+                    st.splits = (-(-cap // N.CONV_DIRECT_BCHUNK) if st.direct
+                                 else -(-cap * oh * ow // CONV_SPLIT_LEN))
                     st.partial = torch.zeros(st.splits * f * (c * k * k + 1), dtype=torch.float32, device=dev)
                 widest = max(widest, st.ld_out, st.ld_in)
                 prev_out, prev_ld = st.y, st.ld_out
@@ -537,9 +540,17 @@ class DeviceHybrid:
         return out
 
     def _conv_launch(self, op, items, label):
+        out = []
+        for direct in (False, True):
+            group = [(s, st) for s, st in items if getattr(st, "direct", False) == direct]
+            if group:
+                out += self._conv_group(op, group, label + ("/direct" if direct else ""), direct)
+        return out
+
+    def _conv_group(self, op, items, label, direct):
         tm, tn = N.conv_tile_shape(op)
         probs, base, red, rbase = [], 0, [], 0
-        flops = 0
+        flops = smem = 0
         for s, st in items:
             c, h, w = st.in_shape
             f, oh, ow = self._conv_out(st)
@@ -552,26 +563,33 @@ class DeviceHybrid:
                           db=_ptr(self.pview(self.grads, s.index, st.params[1])), cap=s.batch_size, c=c, h=h, w=w,
                           f=f, k=k, stride=st.attrs.get("stride", 1), pad=st.attrs.get("padding", 0), oh=oh, ow=ow,
                           model=s.index, relu=int(st.relu), splits=st.splits, split_len=CONV_SPLIT_LEN)
-            if op == N.HNN_FWD:
-                M, Nn = s.batch_size * oh * ow, f
-                tiles = -(-M // tm) * -(-Nn // tn)
-                tiles_n = -(-Nn // tn)
+            cols = c * k * k + 1
+            if direct:
+                tiles_n = 1
+                tiles = st.splits if op == N.HNN_WGRAD else s.batch_size
+                smem = max(smem, N.conv_direct_smem(op, c, h, w, f, k, oh, ow))
+            elif op == N.HNN_FWD:
+                tiles_n = -(-f // tn)
+                tiles = -(-(s.batch_size * oh * ow) // tm) * tiles_n
             elif op == N.HNN_DGRAD:
-                M, Nn = s.batch_size * h * w, c
-                tiles = -(-M // tm) * -(-Nn // tn)
-                tiles_n = -(-Nn // tn)
+                tiles_n = -(-c // tn)
+                tiles = -(-(s.batch_size * h * w) // tm) * tiles_n
             else:
-                tiles_n = -(-(c * k * k + 1) // tn)
+                tiles_n = -(-cols // tn)
                 tiles = st.splits * -(-f // tm) * tiles_n
-                nblk = -(-(f * (c * k * k + 1)) // 256)
+            if op == N.HNN_WGRAD:
                 red.append(N.ConvProblem(tile_base=rbase, tiles_n=tiles_n, **common))
-                rbase += nblk
+                rbase += -(-(f * cols) // 256)
             probs.append(N.ConvProblem(tile_base=base, tiles_n=tiles_n, **common))
             base += tiles
             flops += 2 * s.batch_size * oh * ow * f * c * k * k
         t = _dev_table(N.ConvProblem, probs, self.device)
-        out = [Launch("hnn_grouped_conv", (op, _ptr(t), len(probs), base, _ptr(self.cur), _ptr(self.status)), t,
-                      label, flops=flops)]
+        if direct:
+            args = (op, _ptr(t), len(probs), base, smem, _ptr(self.cur), _ptr(self.status))
+            out = [Launch("hnn_grouped_conv_direct", args, t, label, flops=flops)]
+        else:
+            out = [Launch("hnn_grouped_conv", (op, _ptr(t), len(probs), base, _ptr(self.cur), _ptr(self.status)), t,
+                          label, flops=flops)]
         if op == N.HNN_WGRAD:
             rt = _dev_table(N.ConvProblem, red, self.device)
             out.append(Launch("hnn_conv_wgrad_reduce", (_ptr(rt), len(red), rbase, _ptr(self.cur),

@@ -262,6 +262,8 @@ class Trainer:
         for job in self.jobs.values():
             if job.completed_epochs >= job.hypers.epochs:
                 self._complete(job.job_id)
+        # pause requests pending before the first slice apply immediately (src/train.py:341-342)
+        self._apply_pauses()
         epochs = self._epochs_from_plan()
         live = [jid for jid in self.jobs if self.results[jid].status == "training" and epochs[jid]]
         steps_run, samples = 0, 0
@@ -399,6 +401,7 @@ class Trainer:
             self.pause_sink(job_id, ckpt)
 
     def _apply_pauses(self, force_all=False):
+        """Checkpoint and stop every job with a pending pause request (reference _apply_pauses)."""
         wanted = set(self._pause_requests)
         if self.pause_poll is not None:
             wanted |= {j for j in self.pause_poll() if j in self.jobs and self.results[j].status == "training"}

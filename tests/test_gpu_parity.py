@@ -372,3 +372,74 @@ def test_tensor_core_path_matches_cuda_core_path(pkg, name):
     assert not any(l.endswith("/tc") for l in simt_labels)
     for pid in tc["grads"]:
         assert rel(tc["grads"][pid], simt["grads"][pid]) <= 5e-6, pid
+
+
+@pytest.mark.parametrize("c,f,k,s,p,side", [(32, 16, 3, 1, 1, 9), (3, 6, 5, 1, 0, 9), (16, 96, 3, 2, 1, 9),
+                                            (64, 8, 3, 1, 0, 9), (2, 3, 4, 1, 1, 3), (3, 4, 3, 2, 2, 7),
+                                            (4, 5, 2, 3, 1, 8)])
+def test_conv_paths_match_oracle(pkg, c, f, k, s, p, side):
+    """Implicit-GEMM (large layers) and direct conv kernels vs the numpy restatement, incl. taps that
+    fall entirely in the padding and strides larger than the kernel."""
+    g = oracle.keyed_generator("conv-path", c, f, k, s, p)
+    x = g.normal(size=(3, c, side, side)).astype(np.float32)
+    w = (g.normal(size=(f, c, k, k)) / np.sqrt(c * k * k)).astype(np.float32)
+    b = g.normal(size=f).astype(np.float32)
+    attrs = {"filters": f, "kernel": k, "stride": s, "padding": p}
+    y_ref, saved = oracle.op_forward("conv2d", x, {"weight": w, "bias": b}, attrs)
+    dy = g.normal(size=y_ref.shape).astype(np.float32)
+    dx_ref, dp_ref = oracle.op_backward("conv2d", dy, saved, {"weight": w, "bias": b}, attrs)
+    kind = pkg.OP_KINDS["conv2d"]
+    y, aux = kind.forward(x, {"weight": w, "bias": b}, attrs)
+    dx, dp = kind.backward(dy, aux, {"weight": w, "bias": b}, attrs)
+    assert rel(y, y_ref) <= 1e-5 and rel(dx, dx_ref) <= 1e-5
+    assert rel(dp["weight"], dp_ref["weight"]) <= 1e-5 and rel(dp["bias"], dp_ref["bias"]) <= 1e-5
+
+
+def test_pause_before_run_checkpoints_immediately(pkg):
+    from paper_2408_01331_b200 import store, zoo
+
+    ds = store.from_splits(oracle.blob_splits("golden", "two", 2, 8, 64, 32))
+    job = zoo.job("a", zoo.mlp(8, (16,), 2), ds, 0, epochs=3, batch_size=16, lr=0.05, seed=1)
+    h = pkg.merge([job])
+    t = pkg.Trainer(h, pkg.make_plan("fcfs", [job]), [job], {"a": ds})
+    t.request_pause("a")
+    r = t.run()
+    assert r.jobs["a"].status == "paused" and t.checkpoints["a"].completed_epochs == 0
+    init = pkg.init_params(job.graph, 1)
+    for pid, v in t.checkpoints["a"].params.items():
+        assert np.array_equal(v, init[pid])
+
+
+def test_pause_and_resume_is_bit_identical_to_a_straight_run(pkg):
+    """Checkpoint at an epoch boundary, restore into a fresh hybrid, finish: same bits as no pause
+    (mirrors pkg/tests/test_trainer.py:288-372 on the device path)."""
+    from paper_2408_01331_b200 import store, zoo
+
+    splits = oracle.blob_splits("golden", "four", 4, 12, 96, 32)
+    ds = store.from_splits(splits)
+    mk = lambda: [zoo.job("a", zoo.mlp(12, (24, 16), 4), ds, 0, epochs=4, batch_size=16, lr=0.01,
+                          optimizer="adam", seed=2),
+                  zoo.job("b", zoo.mlp(12, (8,), 4), ds, 1, epochs=3, batch_size=32, lr=0.05, seed=3)]
+    jobs = mk()
+    h = pkg.merge(jobs)
+    pkg.Trainer(h, pkg.make_plan("rr", jobs), jobs, {"a": ds, "b": ds}).run()
+    straight = {j: pkg.separate(h, j)[1] for j in ("a", "b")}
+
+    jobs = mk()
+    h1 = pkg.merge(jobs)
+    t1 = pkg.Trainer(h1, pkg.make_plan("rr", jobs), jobs, {"a": ds, "b": ds})
+    t1.slice_observer = lambda j, e: t1.request_pause("a") if (j, e) == ("a", 0) else None
+    r1 = t1.run()
+    assert r1.jobs["a"].status == "paused" and r1.jobs["b"].status == "complete"
+    ckpt = t1.checkpoints["a"]
+    assert ckpt.completed_epochs == 1 and ckpt.optimizer_step == 6 and ckpt.slot_m and ckpt.slot_v
+
+    resumed = mk()[0]
+    resumed.completed_epochs = ckpt.completed_epochs
+    h2 = pkg.merge([resumed])
+    pkg.restore_checkpoint(h2, ckpt)
+    r2 = pkg.Trainer(h2, pkg.make_plan("fcfs", [resumed]), [resumed], {"a": ds}).run()
+    assert r2.jobs["a"].status == "complete" and r2.jobs["a"].epochs_completed == 4
+    got = pkg.separate(h2, "a")[1]
+    for pid, v in straight["a"].items():
+        assert np.array_equal(got[pid], v), pid
