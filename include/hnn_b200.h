@@ -58,7 +58,8 @@ extern "C" {
 /* hnn_grouped_gemm `prec` */
 #define HNN_PREC_F32_SIMT 0   /* fp32 FFMA, CUDA cores */
 #define HNN_PREC_F32_3XTF32 1 /* tcgen05 kind::tf32, hi/lo split, fp32 accumulate in TMEM */
-#define HNN_PREC_F32_SIMT_SKINNY 2 /* fp32 FFMA, 128 x 16 tiles for N <= 16 (e.g. logits layers) */
+#define HNN_PREC_F32_SIMT_SKINNY 2 /* fp32 FFMA streaming kernels for one dimension <= 16 (logits layers):
+                                      FWD n <= 16, DGRAD k <= 16, WGRAD m <= 16; rows/columns multiple of 4 */
 
 /* optimizer segment kinds */
 #define HNN_OPT_SGD 0
@@ -277,6 +278,11 @@ int hnn_multi_tensor_sgd(const hnn_opt_segment* segs, int nseg, int total_chunks
                          const hnn_model_status* status, void* stream);
 int hnn_multi_tensor_adam(const hnn_opt_segment* segs, int nseg, int total_chunks, const hnn_step_row* cur,
                           const hnn_model_status* status, void* stream);
+
+/* Self-test of the optimizer's exact float32 arithmetic (no reference counterpart): for i < n,
+ * q[i] = a[i] / b[i] and r[i] = sqrt(a[i]) with the same round-to-nearest-even routines the
+ * Adam update uses (optim.py:84-87: m / bias1, v / bias2, np.sqrt, the final quotient). */
+int hnn_selftest_div_sqrt(const float* a, const float* b, float* q, float* r, int64_t n, void* stream);
 
 /* Sizes of the ABI structs, so bindings can assert their layouts. */
 int hnn_struct_size(const char* name);

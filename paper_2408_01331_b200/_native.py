@@ -98,6 +98,7 @@ SIGNATURES = {
     "hnn_sce_fused": [P, C.c_int, C.c_int, C.c_int, P, P, C.c_int, P, P, VP],
     "hnn_multi_tensor_sgd": [P, C.c_int, C.c_int, P, P, VP],
     "hnn_multi_tensor_adam": [P, C.c_int, C.c_int, P, P, VP],
+    "hnn_selftest_div_sqrt": [VP, VP, VP, VP, C.c_int64, VP],
     "hnn_struct_size": [C.c_char_p],
     "hnn_last_error": [],
     "hnn_version": [],

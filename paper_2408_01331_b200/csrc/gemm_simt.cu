@@ -5,9 +5,8 @@
 // therefore its bits) never depends on its neighbours.  K is walked in BK-wide
 // slabs staged in shared memory, double-buffered through registers (the next
 // slab's global loads are in flight while the current one is multiplied).
-// Two tile shapes: 64x64 (general) and 128x16 (skinny N, e.g. the 10-class logits
-// layer, whose FWD has K up to 2048).  Used for every shape the tcgen05 path does
-// not take and as the reference-precision path.
+// 64x64 tiles; used for every shape the tcgen05 path and the small-dimension kernels
+// (gemm_skinny.cu) do not take, and as the reference-precision path.
 #include "common.cuh"
 
 namespace hnn {
@@ -209,95 +208,17 @@ __global__ void __launch_bounds__(STHREADS) gemm_simt_kernel(const hnn_gemm_prob
   }
 }
 
-// FWD with N <= 16 (e.g. the 10-class logits layer, K up to thousands): a warp computes two
-// rows against all N columns, lanes striding K with float4 loads, then a fixed xor-shuffle
-// tree reduces each dot product (deterministic, independent of other problems).
-// Tile = 16 rows (8 warps x 2 rows) of one problem.
-__global__ void __launch_bounds__(STHREADS) rowdot_fwd_kernel(const hnn_gemm_problem* __restrict__ probs, int nprob,
-                                                              const hnn_step_row* __restrict__ cur,
-                                                              const hnn_model_status* __restrict__ status) {
-  const int pi = find_problem(probs, nprob, blockIdx.x, [](const hnn_gemm_problem& q) { return q.tile_base; });
-  const hnn_gemm_problem p = probs[pi];
-  if (!live(cur, status, p.model)) return;
-  const int rows = cur[p.model].rows;
-  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
-  const int r0 = (blockIdx.x - p.tile_base) * 16 + warp * 2;
-  if (r0 >= p.m) return;
-  const bool has1 = r0 + 1 < p.m;
-  float a0[16], a1[16];
-#pragma unroll
-  for (int j = 0; j < 16; ++j) a0[j] = a1[j] = 0.0f;
-  const bool live0 = r0 < rows, live1 = has1 && (r0 + 1) < rows;
-  if (live0) {
-    const float* x0 = p.a + size_t(r0) * p.lda;
-    const float* x1 = p.a + size_t(r0 + (live1 ? 1 : 0)) * p.lda;
-    const bool vec = ((p.lda & 3) == 0) && ((p.ldb & 3) == 0) && ((reinterpret_cast<uintptr_t>(p.a) & 15) == 0) &&
-                     ((reinterpret_cast<uintptr_t>(p.b) & 15) == 0);
-    int k = 0;
-    if (vec) {
-      for (; k + 128 <= p.k; k += 128) {
-        const int kk = k + lane * 4;
-        const float4 u0 = __ldg(reinterpret_cast<const float4*>(x0 + kk));
-        const float4 u1 = __ldg(reinterpret_cast<const float4*>(x1 + kk));
-#pragma unroll
-        for (int j = 0; j < 16; ++j) {
-          if (j >= p.n) break;
-          const float4 w = __ldg(reinterpret_cast<const float4*>(p.b + size_t(j) * p.ldb + kk));
-          a0[j] = fmaf(u0.x, w.x, fmaf(u0.y, w.y, fmaf(u0.z, w.z, fmaf(u0.w, w.w, a0[j]))));
-          a1[j] = fmaf(u1.x, w.x, fmaf(u1.y, w.y, fmaf(u1.z, w.z, fmaf(u1.w, w.w, a1[j]))));
-        }
-      }
-    }
-    for (int kk = k + lane; kk < p.k; kk += 32) {
-      const float u0 = __ldg(x0 + kk), u1 = __ldg(x1 + kk);
-#pragma unroll
-      for (int j = 0; j < 16; ++j) {
-        if (j >= p.n) break;
-        const float w = __ldg(p.b + size_t(j) * p.ldb + kk);
-        a0[j] = fmaf(u0, w, a0[j]);
-        a1[j] = fmaf(u1, w, a1[j]);
-      }
-    }
-  }
-#pragma unroll
-  for (int j = 0; j < 16; ++j) {
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      a0[j] += __shfl_xor_sync(0xffffffffu, a0[j], o);
-      a1[j] += __shfl_xor_sync(0xffffffffu, a1[j], o);
-    }
-  }
-  if (lane < p.n) {
-    float y0 = 0.0f, y1 = 0.0f;
-#pragma unroll
-    for (int j = 0; j < 16; ++j)
-      if (j == lane) { y0 = a0[j]; y1 = a1[j]; }
-    const float b = p.bias[lane];
-    y0 = live0 ? __fadd_rn(y0, b) : 0.0f;
-    y1 = live1 ? __fadd_rn(y1, b) : 0.0f;
-    if (p.relu) {
-      if (live0) y0 = np_relu(y0);
-      if (live1) y1 = np_relu(y1);
-    }
-    p.c[size_t(r0) * p.ldc + lane] = y0;
-    if (has1) p.c[size_t(r0 + 1) * p.ldc + lane] = y1;
-  }
-}
-
-// Skinny variants for N <= 16: selected by the host with prec = HNN_PREC_F32_SIMT_SKINNY.
-template <int OP>
-void launch_simt(int skinny, const hnn_gemm_problem* probs, int nprob, int total_tiles, const hnn_step_row* cur,
-                 const hnn_model_status* status, cudaStream_t s) {
-  if (skinny && OP == HNN_FWD) rowdot_fwd_kernel<<<total_tiles, STHREADS, 0, s>>>(probs, nprob, cur, status);
-  else if (skinny) gemm_simt_kernel<OP, 128, 16><<<total_tiles, STHREADS, 0, s>>>(probs, nprob, cur, status);
-  else gemm_simt_kernel<OP, 64, 64><<<total_tiles, STHREADS, 0, s>>>(probs, nprob, cur, status);
-}
+// Defined in gemm_skinny.cu: the small-dimension (<= 16) streaming kernels.
+int grouped_gemm_skinny(int op, const hnn_gemm_problem* probs, int nprob, int total_tiles, const hnn_step_row* cur,
+                        const hnn_model_status* status, cudaStream_t s);
+int skinny_tile_shape(int op, int32_t* tm, int32_t* tn);
 
 int grouped_gemm_simt(int op, int skinny, const hnn_gemm_problem* probs, int nprob, int total_tiles,
                       const hnn_step_row* cur, const hnn_model_status* status, cudaStream_t s) {
-  if (op == HNN_FWD) launch_simt<HNN_FWD>(skinny, probs, nprob, total_tiles, cur, status, s);
-  else if (op == HNN_DGRAD) launch_simt<HNN_DGRAD>(skinny, probs, nprob, total_tiles, cur, status, s);
-  else launch_simt<HNN_WGRAD>(skinny, probs, nprob, total_tiles, cur, status, s);
+  if (skinny) return grouped_gemm_skinny(op, probs, nprob, total_tiles, cur, status, s);
+  if (op == HNN_FWD) gemm_simt_kernel<HNN_FWD, 64, 64><<<total_tiles, STHREADS, 0, s>>>(probs, nprob, cur, status);
+  else if (op == HNN_DGRAD) gemm_simt_kernel<HNN_DGRAD, 64, 64><<<total_tiles, STHREADS, 0, s>>>(probs, nprob, cur, status);
+  else gemm_simt_kernel<HNN_WGRAD, 64, 64><<<total_tiles, STHREADS, 0, s>>>(probs, nprob, cur, status);
   return check_launch("hnn_grouped_gemm(simt)");
 }
 
@@ -315,11 +236,7 @@ extern "C" int hnn_gemm_tile_shape(int op, int prec, int32_t* tile_m, int32_t* t
     *tile_n = 64;
     return HNN_OK;
   }
-  if (prec == HNN_PREC_F32_SIMT_SKINNY) {  // FWD: 16-row row-dot tiles; DGRAD/WGRAD: 128 x 16
-    *tile_m = (op == HNN_FWD) ? 16 : 128;
-    *tile_n = 16;
-    return HNN_OK;
-  }
+  if (prec == HNN_PREC_F32_SIMT_SKINNY) return hnn::skinny_tile_shape(op, tile_m, tile_n);
   if (prec == HNN_PREC_F32_3XTF32) return hnn::gemm_tc_tile_shape(op, tile_m, tile_n);
   hnn::set_error("hnn_gemm_tile_shape", "unknown precision");
   return HNN_ERR_INVALID;

@@ -1,0 +1,303 @@
+// Dense-layer GEMMs with one tiny dimension (<= 16): the 10-class logits layer of every model
+// (pkg/src/hybridnn/ops.py:46-55).  They move far more bytes than they compute, so each is a
+// vectorised, coalesced streaming kernel instead of a tiled GEMM (a 64x64 or 128x16 tile
+// wastes most of its lanes on a 10-wide edge):
+//   FWD   y[B, n<=16]  = x[B, K] W[n, K]^T + b   one warp per 4 rows, lanes stride K by float4,
+//                                                 W rows loaded once per k-step for all 4 rows
+//   DGRAD dx[B, N]     = dy[B, k<=16] W[k, N]    one float4 column quad per thread, 4 rows,
+//                      (* (x > 0) relu mask)       W quads held in registers across the rows
+//   WGRAD dW[m<=16, N] = dy[R, m]^T x[R, N]      one float4 column quad per thread over a fixed
+//                                                 quarter of the rows, quarters reduced in order;
+//                                                 bias gradient and the fused optimizer included
+// Tiling is a fixed function of each problem's shape (bit-exact isolation); no atomics.
+#include "common.cuh"
+
+namespace hnn {
+
+constexpr int KTHREADS = 256;
+constexpr int FWD_ROWS = 4;  // rows per warp; tile = 8 warps x 4 rows = 32 rows
+constexpr int DG_ROWS = 4;   // DGRAD rows per thread; tile = 8 row groups x 4 rows x 128 columns
+constexpr int WG_QUADS = 64; // WGRAD column quads per CTA; tile = 256 columns, 4 row quarters
+
+__device__ __forceinline__ float4 ldg4(const float* p) { return __ldg(reinterpret_cast<const float4*>(p)); }
+
+__device__ __forceinline__ float dot4(float4 a, float4 b, float acc) {
+  return fmaf(a.x, b.x, fmaf(a.y, b.y, fmaf(a.z, b.z, fmaf(a.w, b.w, acc))));
+}
+
+// ------------------------------------------------------------------------------------------ FWD
+template <int NJ>
+__device__ __forceinline__ void rowdot_rows(const hnn_gemm_problem& p, int r0, int rows, int lane) {
+  float acc[FWD_ROWS][NJ];
+#pragma unroll
+  for (int i = 0; i < FWD_ROWS; ++i)
+#pragma unroll
+    for (int j = 0; j < NJ; ++j) acc[i][j] = 0.0f;
+  const float* x[FWD_ROWS];
+#pragma unroll
+  for (int i = 0; i < FWD_ROWS; ++i) x[i] = p.a + size_t(min(r0 + i, max(rows - 1, 0))) * p.lda;
+  const float* w[NJ];
+#pragma unroll
+  for (int j = 0; j < NJ; ++j) w[j] = p.b + size_t(min(j, p.n - 1)) * p.ldb;  // clamped: no branch
+  const bool vec = ((p.lda & 3) == 0) && ((p.ldb & 3) == 0) && ((reinterpret_cast<uintptr_t>(p.a) & 15) == 0) &&
+                   ((reinterpret_cast<uintptr_t>(p.b) & 15) == 0);
+  int k = 0;
+  if (vec) {
+    for (; k + 128 <= p.k; k += 128) {
+      const int kk = k + lane * 4;
+      float4 u[FWD_ROWS], v[NJ];
+#pragma unroll
+      for (int i = 0; i < FWD_ROWS; ++i) u[i] = ldg4(x[i] + kk);
+#pragma unroll
+      for (int j = 0; j < NJ; ++j) v[j] = ldg4(w[j] + kk);
+#pragma unroll
+      for (int i = 0; i < FWD_ROWS; ++i)
+#pragma unroll
+        for (int j = 0; j < NJ; ++j) acc[i][j] = dot4(u[i], v[j], acc[i][j]);
+    }
+  }
+  for (int kk = k + lane; kk < p.k; kk += 32) {
+    float u[FWD_ROWS];
+#pragma unroll
+    for (int i = 0; i < FWD_ROWS; ++i) u[i] = __ldg(x[i] + kk);
+#pragma unroll
+    for (int j = 0; j < NJ; ++j) {
+      const float v = __ldg(w[j] + kk);
+#pragma unroll
+      for (int i = 0; i < FWD_ROWS; ++i) acc[i][j] = fmaf(u[i], v, acc[i][j]);
+    }
+  }
+  // fixed xor-shuffle tree per dot product (deterministic)
+#pragma unroll
+  for (int i = 0; i < FWD_ROWS; ++i)
+#pragma unroll
+    for (int j = 0; j < NJ; ++j)
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) acc[i][j] += __shfl_xor_sync(0xffffffffu, acc[i][j], o);
+  if (lane < p.n) {
+    const float b = __ldg(p.bias + lane);
+#pragma unroll
+    for (int i = 0; i < FWD_ROWS; ++i) {
+      const int r = r0 + i;
+      if (r >= p.m) break;
+      float y = 0.0f;
+#pragma unroll
+      for (int j = 0; j < NJ; ++j)
+        if (j == lane) y = acc[i][j];
+      if (r < rows) {
+        y = __fadd_rn(y, b);
+        if (p.relu) y = np_relu(y);
+      } else {
+        y = 0.0f;  // rows past this step's batch are exact zeros
+      }
+      p.c[size_t(r) * p.ldc + lane] = y;
+    }
+  }
+}
+
+__global__ void __launch_bounds__(KTHREADS) skinny_fwd_kernel(const hnn_gemm_problem* __restrict__ probs, int nprob,
+                                                              const hnn_step_row* __restrict__ cur,
+                                                              const hnn_model_status* __restrict__ status) {
+  const int pi = find_problem(probs, nprob, blockIdx.x, [](const hnn_gemm_problem& q) { return q.tile_base; });
+  const hnn_gemm_problem& p = probs[pi];
+  if (!live(cur, status, p.model)) return;
+  const int rows = cur[p.model].rows;
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const int r0 = (blockIdx.x - p.tile_base) * (8 * FWD_ROWS) + warp * FWD_ROWS;
+  if (r0 >= p.m) return;
+  // CTA-uniform dispatch on the column count: loads and FMAs carry no per-column branches
+  if (p.n <= 4) rowdot_rows<4>(p, r0, rows, lane);
+  else if (p.n <= 8) rowdot_rows<8>(p, r0, rows, lane);
+  else if (p.n <= 12) rowdot_rows<12>(p, r0, rows, lane);
+  else rowdot_rows<16>(p, r0, rows, lane);
+}
+
+// ---------------------------------------------------------------------------------------- DGRAD
+template <int KJ>
+__device__ __forceinline__ void outer_rows(const hnn_gemm_problem& p, int r0, int col, int rows) {
+  float4 w[KJ];
+#pragma unroll
+  for (int j = 0; j < KJ; ++j) w[j] = j < p.k ? ldg4(p.b + size_t(j) * p.ldb + col) : make_float4(0, 0, 0, 0);
+#pragma unroll
+  for (int i = 0; i < DG_ROWS; ++i) {
+    const int r = r0 + i;
+    if (r >= p.m) break;
+    float4 o = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
+    if (r < rows) {
+      const float* dy = p.a + size_t(r) * p.lda;
+#pragma unroll
+      for (int j = 0; j < KJ; ++j) {
+        const float d = j < p.k ? __ldg(dy + j) : 0.0f;
+        o.x = fmaf(d, w[j].x, o.x);
+        o.y = fmaf(d, w[j].y, o.y);
+        o.z = fmaf(d, w[j].z, o.z);
+        o.w = fmaf(d, w[j].w, o.w);
+      }
+      if (p.mask) {
+        const float4 m = ldg4(p.mask + size_t(r) * p.ldc + col);
+        o.x = np_mask(o.x, m.x);
+        o.y = np_mask(o.y, m.y);
+        o.z = np_mask(o.z, m.z);
+        o.w = np_mask(o.w, m.w);
+      }
+    }
+    *reinterpret_cast<float4*>(p.c + size_t(r) * p.ldc + col) = o;
+  }
+}
+
+__global__ void __launch_bounds__(KTHREADS) skinny_dgrad_kernel(const hnn_gemm_problem* __restrict__ probs, int nprob,
+                                                                const hnn_step_row* __restrict__ cur,
+                                                                const hnn_model_status* __restrict__ status) {
+  const int pi = find_problem(probs, nprob, blockIdx.x, [](const hnn_gemm_problem& q) { return q.tile_base; });
+  const hnn_gemm_problem& p = probs[pi];
+  if (!live(cur, status, p.model)) return;
+  const int rows = cur[p.model].rows;
+  const int t = blockIdx.x - p.tile_base;
+  const int m0 = (t / p.tiles_n) * (8 * DG_ROWS), n0 = (t % p.tiles_n) * 128;
+  const int col = n0 + (threadIdx.x & 31) * 4, r0 = m0 + (threadIdx.x >> 5) * DG_ROWS;
+  if (col >= p.n || r0 >= p.m) return;  // n is a multiple of 4 (host routing)
+  if (p.k <= 4) outer_rows<4>(p, r0, col, rows);
+  else if (p.k <= 8) outer_rows<8>(p, r0, col, rows);
+  else if (p.k <= 12) outer_rows<12>(p, r0, col, rows);
+  else outer_rows<16>(p, r0, col, rows);
+}
+
+// ---------------------------------------------------------------------------------------- WGRAD
+constexpr int WG_CHUNK = 256;  // dy rows staged in shared memory per pass ([256][16] floats)
+
+template <int MJ>
+__device__ __forceinline__ void colacc(const hnn_gemm_problem& p, int col, int r_lo, int r_hi, int base,
+                                       float (&part)[16][4], const float* dys) {
+  const float* x = p.b + col;
+#pragma unroll 4
+  for (int r = r_lo; r < r_hi; ++r) {
+    const float4 xv = ldg4(x + size_t(r) * p.ldb);
+    const float* d = dys + (r - base) * 16;
+#pragma unroll
+    for (int j = 0; j < MJ; ++j) {
+      part[j][0] = fmaf(d[j], xv.x, part[j][0]);
+      part[j][1] = fmaf(d[j], xv.y, part[j][1]);
+      part[j][2] = fmaf(d[j], xv.z, part[j][2]);
+      part[j][3] = fmaf(d[j], xv.w, part[j][3]);
+    }
+  }
+}
+
+__global__ void __launch_bounds__(KTHREADS) skinny_wgrad_kernel(const hnn_gemm_problem* __restrict__ probs, int nprob,
+                                                                const hnn_step_row* __restrict__ cur,
+                                                                const hnn_model_status* __restrict__ status) {
+  extern __shared__ __align__(16) float wg_smem[];
+  float* dys = wg_smem;                   // [WG_CHUNK][16] staged dy rows (zero padded)
+  float* red = wg_smem + WG_CHUNK * 16;   // [3][WG_QUADS][16][4] partials of row quarters 1..3
+  const int pi = find_problem(probs, nprob, blockIdx.x, [](const hnn_gemm_problem& q) { return q.tile_base; });
+  const hnn_gemm_problem& p = probs[pi];
+  if (!live(cur, status, p.model)) return;
+  const int rows = cur[p.model].rows;
+  const int n0 = (blockIdx.x - p.tile_base) * (4 * WG_QUADS);
+  const int qd = threadIdx.x % WG_QUADS, q = threadIdx.x / WG_QUADS;
+  const int col = n0 + qd * 4;
+  const bool active = col < p.n;  // n is a multiple of 4 (host routing)
+  const bool bias_thread = n0 == 0 && threadIdx.x < p.m && (p.dbias || p.opt_b);
+  float part[16][4];
+#pragma unroll
+  for (int j = 0; j < 16; ++j) part[j][0] = part[j][1] = part[j][2] = part[j][3] = 0.0f;
+  float bsum = -0.0f;
+  // fixed decomposition: 256-row chunks in order; inside a chunk, row quarter q of each thread
+  for (int base = 0; base < rows; base += WG_CHUNK) {
+    const int n = min(WG_CHUNK, rows - base);
+    __syncthreads();
+    for (int e = threadIdx.x; e < WG_CHUNK * 16; e += KTHREADS) {
+      const int r = e >> 4, j = e & 15;
+      dys[e] = (j < p.m && r < n) ? __ldg(p.a + size_t(base + r) * p.lda + j) : 0.0f;
+    }
+    __syncthreads();
+    if (bias_thread)  // numpy's axis-0 sum: sequential row order per column
+      for (int r = 0; r < n; ++r) bsum = __fadd_rn(bsum, dys[r * 16 + threadIdx.x]);
+    if (active) {
+      const int lo = base + (n * q) / 4, hi = base + (n * (q + 1)) / 4;
+      if (p.m <= 4) colacc<4>(p, col, lo, hi, base, part, dys);
+      else if (p.m <= 8) colacc<8>(p, col, lo, hi, base, part, dys);
+      else if (p.m <= 12) colacc<12>(p, col, lo, hi, base, part, dys);
+      else colacc<16>(p, col, lo, hi, base, part, dys);
+    }
+  }
+  if (bias_thread) {
+    if (p.dbias) p.dbias[threadIdx.x] = bsum;
+    if (p.opt_b) {
+      const Update u = make_update(cur[p.model], p.opt_kind, p.opt_momentum);
+      const int i = threadIdx.x;
+      float w = p.opt_b[i], m = p.opt_bm ? p.opt_bm[i] : 0.0f, v = p.opt_bv ? p.opt_bv[i] : 0.0f;
+      update_one(u, w, bsum, m, v);
+      p.opt_b[i] = w;
+      if (p.opt_bm) p.opt_bm[i] = m;
+      if (p.opt_bv) p.opt_bv[i] = v;
+    }
+  }
+  if (q > 0) {
+    float* dst = red + (size_t(q - 1) * WG_QUADS + qd) * 64;
+#pragma unroll
+    for (int j = 0; j < 16; ++j)
+      *reinterpret_cast<float4*>(dst + j * 4) = make_float4(part[j][0], part[j][1], part[j][2], part[j][3]);
+  }
+  __syncthreads();
+  if (q != 0 || !active) return;
+  // quarters summed in fixed order 0 + 1 + 2 + 3
+#pragma unroll
+  for (int s = 0; s < 3; ++s) {
+    const float* src = red + (size_t(s) * WG_QUADS + qd) * 64;
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+      const float4 v = *reinterpret_cast<const float4*>(src + j * 4);
+      part[j][0] += v.x;
+      part[j][1] += v.y;
+      part[j][2] += v.z;
+      part[j][3] += v.w;
+    }
+  }
+  const Update u = make_update(cur[p.model], p.opt_kind, p.opt_momentum);
+#pragma unroll
+  for (int j = 0; j < 16; ++j) {
+    if (j >= p.m) break;
+    const size_t off = size_t(j) * p.ldc + col;
+    if (p.c) *reinterpret_cast<float4*>(p.c + off) = make_float4(part[j][0], part[j][1], part[j][2], part[j][3]);
+    if (p.opt_w) {
+      float4 w = *reinterpret_cast<float4*>(p.opt_w + off);
+      float4 m = p.opt_wm ? *reinterpret_cast<float4*>(p.opt_wm + off) : make_float4(0, 0, 0, 0);
+      float4 v = p.opt_wv ? *reinterpret_cast<float4*>(p.opt_wv + off) : make_float4(0, 0, 0, 0);
+      update_one(u, w.x, part[j][0], m.x, v.x);
+      update_one(u, w.y, part[j][1], m.y, v.y);
+      update_one(u, w.z, part[j][2], m.z, v.z);
+      update_one(u, w.w, part[j][3], m.w, v.w);
+      *reinterpret_cast<float4*>(p.opt_w + off) = w;
+      if (p.opt_wm) *reinterpret_cast<float4*>(p.opt_wm + off) = m;
+      if (p.opt_wv) *reinterpret_cast<float4*>(p.opt_wv + off) = v;
+    }
+  }
+}
+
+int skinny_tile_shape(int op, int32_t* tm, int32_t* tn) {
+  if (op == HNN_FWD) { *tm = 8 * FWD_ROWS; *tn = 16; }
+  else if (op == HNN_DGRAD) { *tm = 8 * DG_ROWS; *tn = 128; }
+  else { *tm = 16; *tn = 4 * WG_QUADS; }
+  return HNN_OK;
+}
+
+int grouped_gemm_skinny(int op, const hnn_gemm_problem* probs, int nprob, int total_tiles, const hnn_step_row* cur,
+                        const hnn_model_status* status, cudaStream_t s) {
+  if (op == HNN_FWD) {
+    skinny_fwd_kernel<<<total_tiles, KTHREADS, 0, s>>>(probs, nprob, cur, status);
+  } else if (op == HNN_DGRAD) {
+    skinny_dgrad_kernel<<<total_tiles, KTHREADS, 0, s>>>(probs, nprob, cur, status);
+  } else {
+    constexpr int smem = (WG_CHUNK * 16 + 3 * WG_QUADS * 64) * 4;  // 64 KB
+    static bool configured = false;
+    if (!configured) {
+      cudaFuncSetAttribute(skinny_wgrad_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+      configured = true;
+    }
+    skinny_wgrad_kernel<<<total_tiles, KTHREADS, smem, s>>>(probs, nprob, cur, status);
+  }
+  return check_launch("hnn_grouped_gemm(skinny)");
+}
+
+}  // namespace hnn

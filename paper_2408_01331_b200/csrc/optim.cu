@@ -25,14 +25,27 @@ __device__ __forceinline__ void st_cs4(float4* p, float4 v) {
                : "memory");
 }
 
-constexpr int OPT_THREADS = 256, OPT_CHUNK = 4096;  // 4 float4 per thread
+constexpr int OPT_THREADS = 256, OPT_CHUNK = 4096;  // 4 float4 per thread per chunk
+// Measured on C3 (76.7M Adam params, tools/opt_variants.py): 5 CTAs/SM x 1 float4 per arena per
+// thread 0.399 ms (5.39 TB/s, 82% of the copy peak; a pure-traffic kernel with the same access
+// pattern 0.375 ms); 4 CTAs 0.404; 6 / 8 CTAs (register-capped, spilling) 0.44 / 0.51;
+// 2 float4 per thread 0.49; 4 float4 at 2 CTAs 0.61.
+#ifndef HNN_OPT_MIN_CTAS
+#define HNN_OPT_MIN_CTAS 5
+#endif
+#ifndef HNN_OPT_UNROLL
+#define HNN_OPT_UNROLL 1
+#endif
+constexpr int OPT_MIN_CTAS = HNN_OPT_MIN_CTAS, OPT_UNROLL = HNN_OPT_UNROLL;
 
 // Persistent grid-stride walk over the 4096-float chunks of all segments (chunk ids are
-// a flat index; each chunk belongs to exactly one segment).
-__global__ void __launch_bounds__(OPT_THREADS) multi_tensor_kernel(const hnn_opt_segment* __restrict__ segs, int nseg,
-                                                                   int total_chunks,
-                                                                   const hnn_step_row* __restrict__ cur,
-                                                                   const hnn_model_status* __restrict__ status) {
+// a flat index; each chunk belongs to exactly one segment).  A thread handles one float4 of
+// each arena at a time: full occupancy (2048 threads x 64 B in flight per SM) hides both the
+// HBM latency and the dependent division / sqrt chains of Adam, which at 2 CTAs/SM with
+// 16 elements per thread made the launch latency-bound.
+__global__ void __launch_bounds__(OPT_THREADS, OPT_MIN_CTAS)
+    multi_tensor_kernel(const hnn_opt_segment* __restrict__ segs, int nseg, int total_chunks,
+                        const hnn_step_row* __restrict__ cur, const hnn_model_status* __restrict__ status) {
   for (int chunk = blockIdx.x; chunk < total_chunks; chunk += gridDim.x) {
     const int si = find_problem(segs, nseg, chunk, [](const hnn_opt_segment& q) { return q.chunk_base; });
     const hnn_opt_segment& sg = segs[si];
@@ -45,30 +58,33 @@ __global__ void __launch_bounds__(OPT_THREADS) multi_tensor_kernel(const hnn_opt
     float4* m4 = sg.m ? reinterpret_cast<float4*>(sg.m + base) : nullptr;
     float4* v4 = sg.v ? reinterpret_cast<float4*>(sg.v + base) : nullptr;
     const int n4 = int(min((long long)OPT_CHUNK, sg.count - base) / 4);
-    float4 P[4], G[4], M[4], V[4];
+#pragma unroll 1
+    for (int i0 = threadIdx.x; i0 < n4; i0 += OPT_THREADS * OPT_UNROLL) {
+      // explicit global-space accesses (the segment pointers come from memory, so a plain
+      // dereference would compile to generic LD/ST); all loads of the group issue first
+      float4 P[OPT_UNROLL], G[OPT_UNROLL], M[OPT_UNROLL], V[OPT_UNROLL];
 #pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      const int i = threadIdx.x + q * OPT_THREADS;
-      if (i < n4) {
-        // explicit global-space accesses (the segment pointers come from memory, so a plain
-        // dereference would compile to generic LD/ST)
-        P[q] = ld_nc4(p4 + i);
-        G[q] = ld_nc4(g4 + i);
-        if (u.kind != HNN_OPT_SGD) M[q] = ld_nc4(m4 + i);
-        if (u.kind == HNN_OPT_ADAM) V[q] = ld_nc4(v4 + i);
+      for (int q = 0; q < OPT_UNROLL; ++q) {
+        const int i = i0 + q * OPT_THREADS;
+        if (i < n4) {
+          P[q] = ld_nc4(p4 + i);
+          G[q] = ld_nc4(g4 + i);
+          if (u.kind != HNN_OPT_SGD) M[q] = ld_nc4(m4 + i);
+          if (u.kind == HNN_OPT_ADAM) V[q] = ld_nc4(v4 + i);
+        }
       }
-    }
 #pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      const int i = threadIdx.x + q * OPT_THREADS;
-      if (i >= n4) continue;
-      update_one(u, P[q].x, G[q].x, M[q].x, V[q].x);
-      update_one(u, P[q].y, G[q].y, M[q].y, V[q].y);
-      update_one(u, P[q].z, G[q].z, M[q].z, V[q].z);
-      update_one(u, P[q].w, G[q].w, M[q].w, V[q].w);
-      st_cs4(p4 + i, P[q]);
-      if (u.kind != HNN_OPT_SGD) st_cs4(m4 + i, M[q]);
-      if (u.kind == HNN_OPT_ADAM) st_cs4(v4 + i, V[q]);
+      for (int q = 0; q < OPT_UNROLL; ++q) {
+        const int i = i0 + q * OPT_THREADS;
+        if (i >= n4) continue;
+        update_one(u, P[q].x, G[q].x, M[q].x, V[q].x);
+        update_one(u, P[q].y, G[q].y, M[q].y, V[q].y);
+        update_one(u, P[q].z, G[q].z, M[q].z, V[q].z);
+        update_one(u, P[q].w, G[q].w, M[q].w, V[q].w);
+        st_cs4(p4 + i, P[q]);
+        if (u.kind != HNN_OPT_SGD) st_cs4(m4 + i, M[q]);
+        if (u.kind == HNN_OPT_ADAM) st_cs4(v4 + i, V[q]);
+      }
     }
   }
 }
@@ -82,7 +98,7 @@ int launch_multi_tensor(const char* who, const hnn_opt_segment* segs, int nseg, 
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   }
-  const int grid = total_chunks < 4 * sms ? total_chunks : 4 * sms;  // 2 resident CTAs/SM x 2 waves
+  const int grid = total_chunks < OPT_MIN_CTAS * sms ? total_chunks : OPT_MIN_CTAS * sms;  // one wave
   multi_tensor_kernel<<<grid, OPT_THREADS, 0, as_stream(stream)>>>(segs, nseg, total_chunks, cur, status);
   return check_launch(who);
 }
@@ -100,4 +116,20 @@ extern "C" int hnn_multi_tensor_sgd(const hnn_opt_segment* segs, int nseg, int t
 extern "C" int hnn_multi_tensor_adam(const hnn_opt_segment* segs, int nseg, int total_chunks, const hnn_step_row* cur,
                                      const hnn_model_status* status, void* stream) {
   return hnn::launch_multi_tensor("hnn_multi_tensor_adam", segs, nseg, total_chunks, cur, status, stream);
+}
+
+namespace hnn {
+__global__ void selftest_div_sqrt_kernel(const float* a, const float* b, float* q, float* r, int64_t n) {
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x) {
+    q[i] = div_rn_exact(a[i], b[i]);
+    r[i] = sqrt_rn_exact(a[i]);
+  }
+}
+}  // namespace hnn
+
+extern "C" int hnn_selftest_div_sqrt(const float* a, const float* b, float* q, float* r, int64_t n, void* stream) {
+  HNN_REQUIRE(a && b && q && r && n >= 0, "hnn_selftest_div_sqrt", "bad arguments");
+  if (n == 0) return HNN_OK;
+  hnn::selftest_div_sqrt_kernel<<<1184, 256, 0, hnn::as_stream(stream)>>>(a, b, q, r, n);
+  return hnn::check_launch("hnn_selftest_div_sqrt");
 }

@@ -466,6 +466,20 @@ class DeviceHybrid:
             return False
         return all(d[k] % 16 == 0 for k in ("a", "b", "c"))
 
+    @staticmethod
+    def _route_skinny(op, d) -> bool:
+        """One GEMM dimension <= 16 (the logits layer): the streaming kernels of gemm_skinny.cu.
+        DGRAD / WGRAD use float4 column quads, so they also need 16-byte rows."""
+        if op == N.HNN_FWD:
+            return d["n"] <= 16
+        small = d["k"] if op == N.HNN_DGRAD else d["m"]
+        if small > 16 or d["n"] % 4:
+            return False
+        if any(d[k] % 4 for k in ("ldb", "ldc")) or (op == N.HNN_DGRAD and d["mask"] and d["ldc"] % 4):
+            return False
+        ptrs = ("b", "c", "mask") if op == N.HNN_DGRAD else ("b", "c", "opt_w", "opt_wm", "opt_wv")
+        return all(d.get(k, 0) % 16 == 0 for k in ptrs)
+
     def _gemm_launch(self, op, items, label):
         """items: list of (slot, stage).  Splits into SIMT / 3xTF32 launches."""
         groups = {N.PREC_SIMT: [], N.PREC_SIMT_SKINNY: [], N.PREC_3XTF32: []}
@@ -498,8 +512,10 @@ class DeviceHybrid:
                              opt_kind=kind, opt_momentum=float(np.float32(s.momentum)))
             if self.use_tc and self._route_tc(op, d):
                 prec = N.PREC_3XTF32
+            elif self._route_skinny(op, d):
+                prec = N.PREC_SIMT_SKINNY
             else:
-                prec = N.PREC_SIMT_SKINNY if d["n"] <= 16 else N.PREC_SIMT
+                prec = N.PREC_SIMT
             groups[prec].append((s, d))
         out = []
         for prec, rows in groups.items():

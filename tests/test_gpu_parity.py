@@ -443,3 +443,100 @@ def test_pause_and_resume_is_bit_identical_to_a_straight_run(pkg):
     got = pkg.separate(h2, "a")[1]
     for pid, v in straight["a"].items():
         assert np.array_equal(got[pid], v), pid
+
+
+@pytest.mark.parametrize("opt_step", [1, 7])
+def test_adam_is_bit_exact_on_subnormal_and_zero_state(pkg, opt_step):
+    """Converged models carry zero and subnormal gradients / moments (C3 after 60 steps: 12% of the
+    second moments are subnormal).  The multi-tensor Adam must still equal apply_update bit for bit
+    there (src/optim.py:73-87): m/bias1, v/bias2, sqrt and the final quotient all subnormal-exact."""
+    import torch
+
+    from paper_2408_01331_b200 import store, zoo
+    from paper_2408_01331_b200.runtime import STEP_DTYPE
+    from paper_2408_01331_b200.train import _bias
+
+    ds = store.from_splits(oracle.blob_splits("golden", "sub", 4, 16, 64, 32))
+    job = zoo.job("a", zoo.mlp(16, (2048, 512), 4), ds, 0, epochs=1, batch_size=32, lr=1e-3, optimizer="adam",
+                  seed=3)
+    h = pkg.merge([job])
+    dev = h.materialize()
+    from paper_2408_01331_b200.runtime import DeviceDataset
+
+    dd = DeviceDataset(ds, dev.device)
+    dev.bind_datasets([dd], dd.n_train)
+    dev.build_plans()
+    g = np.random.default_rng(opt_step)
+    n = dev.arena_len
+    tiny = np.finfo(np.float32).tiny
+
+    def crafted(scale):
+        cls = g.integers(0, 5, n)
+        mag = np.where(cls == 0, 0.0, np.where(cls == 1, g.uniform(0, 1, n) * tiny,     # subnormal
+                       np.where(cls == 2, g.uniform(1, 1e3, n) * tiny, g.uniform(0, 1, n) * scale)))
+        return (mag * np.where(g.integers(0, 2, n) == 1, -1.0, 1.0)).astype(np.float32)
+
+    P = g.normal(0, 0.1, n).astype(np.float32)
+    G = crafted(1e-6)
+    M = crafted(1e-7)
+    V = np.abs(crafted(1e-12))
+    for arena, host in ((dev.params, P), (dev.grads, G), (dev.m1, M), (dev.m2, V)):
+        arena.copy_(torch.from_numpy(host))
+    b1, b2 = _bias(opt_step)
+    rows = np.zeros((1, 1), dtype=STEP_DTYPE)
+    rows[0, 0] = (1, 32, 0, 0, 0, opt_step, float(np.float32(1e-3)), b1, b2, (0, 0, 0))
+    dev.load_schedule(rows)
+    dev.run_plan([dev.train_plan[-1]])
+    torch.cuda.synchronize()
+    F = np.float32
+    with np.errstate(all="ignore"):
+        m = (F(1) - F(0.9)) * G if opt_step == 1 else F(0.9) * M + (F(1) - F(0.9)) * G
+        v = (F(1) - F(0.999)) * G * G if opt_step == 1 else F(0.999) * V + (F(1) - F(0.999)) * G * G
+        p = P - F(1e-3) * (m / F(b1)) / (np.sqrt(v / F(b2)) + F(1e-8))
+    assert np.array_equal(dev.m1.cpu().numpy(), m)
+    assert np.array_equal(dev.m2.cpu().numpy(), v)
+    assert np.array_equal(dev.params.cpu().numpy(), p)
+
+
+def test_exact_div_sqrt_match_numpy(pkg):
+    """The optimizer's slow-path-free float32 division / sqrt (csrc/common.cuh div_rn_exact,
+    sqrt_rn_exact) equal numpy's correctly rounded float32 ops bit for bit: random operands over
+    the whole range (zeros, subnormals, the fallback ranges) plus exact and near subnormal ties."""
+    import torch
+
+    from paper_2408_01331_b200 import _native as N
+
+    g = np.random.default_rng(11)
+    n = 1 << 22
+    parts_a, parts_b = [], []
+    bits = lambda lo, hi, k: g.integers(lo, hi, k, dtype=np.int64).astype(np.uint32).view(np.float32)
+    sign = lambda x: np.where(g.integers(0, 2, x.size) == 1, -x, x).astype(np.float32)
+    parts_a += [sign(bits(0, 0x7F800000, n)), sign(bits(0, 0x00800000, n)), sign(bits(0x00800000, 0x0A000000, n)),
+                np.zeros(n // 8, np.float32)]
+    parts_b += [bits(0x30800000, 0x4E800000, n), bits(0x3DCCCCCD, 0x3F800000, n), bits(0x3A800000, 0x3F800000, n),
+                bits(0x30800000, 0x4E800000, n // 8)]
+    # exact subnormal ties a/b = (2k+1) * 2^-150 (b = 2 * odd), and their neighbours
+    k = g.integers(0, 1 << 20, n // 4)
+    b = (2.0 * g.choice([1, 3, 5, 7, 9, 11, 13], n // 4)).astype(np.float32)
+    a = ((2 * k + 1) * (b / 2) * 2.0 ** -149).astype(np.float32)
+    for d in (0, 1, -1):
+        parts_a.append(sign((a.view(np.uint32) + np.uint32(d % (1 << 32))).view(np.float32) if d >= 0
+                       else (a.view(np.uint32) - np.uint32(1)).view(np.float32)))
+        parts_b.append(b)
+    # outside the fast ranges (falls back to __fdiv_rn): tiny / huge divisors, huge numerators
+    parts_a.append(sign(bits(0, 0x7F800000, n // 8)))
+    parts_b.append(np.where(g.integers(0, 2, n // 8) == 1, bits(0x00000001, 0x30800000, n // 8),
+                            bits(0x4E800000, 0x7F800000, n // 8)).astype(np.float32))
+    A, B = np.concatenate(parts_a), np.concatenate(parts_b)
+    da, db = torch.from_numpy(A).cuda(), torch.from_numpy(B).cuda()
+    q, r = torch.empty_like(da), torch.empty_like(da)
+    N.call("hnn_selftest_div_sqrt", da.data_ptr(), db.data_ptr(), q.data_ptr(), r.data_ptr(), A.size,
+           torch.cuda.current_stream().cuda_stream)
+    torch.cuda.synchronize()
+    with np.errstate(all="ignore"):
+        rq, rr = A / B, np.sqrt(A)
+    gq, gr = q.cpu().numpy(), r.cpu().numpy()
+    same = lambda x, y: (x.view(np.uint32) == y.view(np.uint32)) | (np.isnan(x) & np.isnan(y))
+    bad_q, bad_r = ~same(gq, rq), ~same(gr, rr)
+    assert not bad_q.any(), (A[bad_q][:5], B[bad_q][:5], gq[bad_q][:5], rq[bad_q][:5], int(bad_q.sum()))
+    assert not bad_r.any(), (A[bad_r][:5], gr[bad_r][:5], rr[bad_r][:5], int(bad_r.sum()))

@@ -1,0 +1,17 @@
+#!/bin/bash
+# One gpurun call: GPU tests, smoke, bench lines, ncu launch list + full capture of the top kernels.
+# usage (from the repo root, on the box): bash tools/gpu_round.sh TAG
+TAG=${1:-r01}
+mkdir -p gpurun_out
+python -c "import __graft_entry__ as g; g.build()" > gpurun_out/build.log 2>&1
+timeout 900 python -m pytest tests -x -q -m gpu > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_gpu.log
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; echo "smoke rc=$?" >> gpurun_out/smoke.log
+for w in c3 c2 c5; do
+  timeout 600 python bench.py --workload $w > gpurun_out/bench_$w.json 2> gpurun_out/bench_$w.err
+done
+timeout 300 python bench.py --impl reference --steps 3 --warmup 1 > gpurun_out/bench_ref.json 2> gpurun_out/bench_ref.err
+timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_c3.csv \
+  python bench.py --workload c3 --steps 2 --warmup 1 --no-cpu > gpurun_out/ncu_launch_c3.log 2>&1
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:'multi_tensor|gemm_tc' -s 20 -c 6 \
+  -o gpurun_out/prof_c3 python bench.py --workload c3 --steps 2 --warmup 1 --no-cpu > gpurun_out/ncu_full_c3.log 2>&1
+echo done
