@@ -58,6 +58,11 @@ extern "C" {
 /* hnn_grouped_gemm `prec` */
 #define HNN_PREC_F32_SIMT 0   /* fp32 FFMA, CUDA cores */
 #define HNN_PREC_F32_3XTF32 1 /* tcgen05 kind::tf32, hi/lo split, fp32 accumulate in TMEM */
+#define HNN_PREC_F32_3XTF32_PAIR 3 /* as HNN_PREC_F32_3XTF32 on CTA pairs (tcgen05 cta_group::2), 256 x 256
+                                      tiles; same TMA maps (hnn_gemm_tc_encode).  The problem table MUST be
+                                      followed by a tile schedule: int32 npairs, offsets[npairs + 1], tile
+                                      ids[total_tiles]; when npairs != min(total_tiles, SMs/2) (or npairs is
+                                      0) the pairs take tiles round-robin instead */
 #define HNN_PREC_F32_SIMT_SKINNY 2 /* fp32 FFMA streaming kernels for one dimension <= 16 (logits layers):
                                       FWD n <= 16, DGRAD k <= 16, WGRAD m <= 16; rows/columns multiple of 4 */
 

@@ -14,7 +14,7 @@ from .errors import DeviceError
 LIB_PATH = Path(__file__).resolve().parent / "_lib" / "libhnn_b200.so"
 
 HNN_FWD, HNN_DGRAD, HNN_WGRAD = 0, 1, 2
-PREC_SIMT, PREC_3XTF32, PREC_SIMT_SKINNY = 0, 1, 2
+PREC_SIMT, PREC_3XTF32, PREC_SIMT_SKINNY, PREC_3XTF32_PAIR = 0, 1, 2, 3
 OPT_SGD, OPT_SGD_MOMENTUM, OPT_ADAM = 0, 1, 2
 CONV_DIRECT_BCHUNK = 4
 

@@ -226,6 +226,10 @@ int grouped_gemm_simt(int op, int skinny, const hnn_gemm_problem* probs, int npr
 int grouped_gemm_tc(int op, const hnn_gemm_problem* probs, int nprob, int total_tiles, const hnn_step_row* cur,
                     const hnn_model_status* status, cudaStream_t s);
 int gemm_tc_tile_shape(int op, int32_t* tm, int32_t* tn);
+// Defined in gemm_tc2.cu (CTA-pair tcgen05 kernel).
+int grouped_gemm_tc2(int op, const hnn_gemm_problem* probs, int nprob, int total_tiles, const hnn_step_row* cur,
+                     const hnn_model_status* status, cudaStream_t s);
+int gemm_tc2_tile_shape(int op, int32_t* tm, int32_t* tn);
 
 }  // namespace hnn
 
@@ -238,6 +242,7 @@ extern "C" int hnn_gemm_tile_shape(int op, int prec, int32_t* tile_m, int32_t* t
   }
   if (prec == HNN_PREC_F32_SIMT_SKINNY) return hnn::skinny_tile_shape(op, tile_m, tile_n);
   if (prec == HNN_PREC_F32_3XTF32) return hnn::gemm_tc_tile_shape(op, tile_m, tile_n);
+  if (prec == HNN_PREC_F32_3XTF32_PAIR) return hnn::gemm_tc2_tile_shape(op, tile_m, tile_n);
   hnn::set_error("hnn_gemm_tile_shape", "unknown precision");
   return HNN_ERR_INVALID;
 }
@@ -250,6 +255,7 @@ extern "C" int hnn_grouped_gemm(int op, int prec, const hnn_gemm_problem* probs,
   if (prec == HNN_PREC_F32_SIMT || prec == HNN_PREC_F32_SIMT_SKINNY)
     return hnn::grouped_gemm_simt(op, prec == HNN_PREC_F32_SIMT_SKINNY, probs, nprob, total_tiles, cur, status, s);
   if (prec == HNN_PREC_F32_3XTF32) return hnn::grouped_gemm_tc(op, probs, nprob, total_tiles, cur, status, s);
+  if (prec == HNN_PREC_F32_3XTF32_PAIR) return hnn::grouped_gemm_tc2(op, probs, nprob, total_tiles, cur, status, s);
   hnn::set_error("hnn_grouped_gemm", "unknown precision");
   return HNN_ERR_INVALID;
 }

@@ -1,0 +1,441 @@
+// Grouped fp32 GEMM on CTA pairs: tcgen05.mma.cta_group::2 kind::tf32, 3xTF32, 256 x 256 tiles.
+//
+// Why pairs: the single-CTA kernel (gemm_tc.cu, 128 x 128 tiles) is shared-memory-bandwidth
+// bound — per 32-wide K block its 12 tf32 MMAs read 96 KB of operands out of smem and TMA +
+// the lo converters move another 96 KB, ~250 B/clk against ~128 B/clk (ncu: tensor pipe 24-35%,
+// profiles/r01/ncu_c3_v4.txt).  With cta_group::2 one MMA covers a 256 x 256 tile across the
+// two SMs of a TPC: each CTA stages half of A (its 128 rows) and half of B (128 of the 256
+// columns), the tensor cores exchange the B halves, and per CTA the operand reads drop to
+// 64 B/clk with the converter traffic at 62 B/clk.
+//
+// Arithmetic is the single-CTA kernel's: every operand x is used as hi = x (the tensor core
+// truncates fp32 to tf32) and lo = rna_tf32(x - trunc_tf32(x)); the tile accumulates
+// A_hi*B_hi + A_lo*B_hi + A_hi*B_lo.  Accumulation precision ("promotion"): the tensor core
+// sums one chunk of TC2_CHUNK_KB K blocks into one of two 256-column TMEM buffers; the
+// accumulator warps add each finished chunk into fp32 registers (IEEE adds) and release the
+// buffer, so the MMAs of the next chunk never wait for a promotion (double buffering).  Each
+// CTA's 128 x 256 running sum lives in registers: 8 accumulator warps x 128 columns (384
+// threads per CTA leave 168 registers per thread).
+//
+// Roles (384 threads per CTA, 1 CTA per SM, persistent over a heaviest-first tile list; both
+// CTAs of a pair walk the same tiles):
+//   warp 0       TMA producer: this CTA's A half and B half, raw fp32, into a 3-stage ring
+//   warp 1       TMEM allocator (pair) + single-thread MMA issuer (leader CTA only)
+//   warps 2,3    converters: lo ring from the raw ring, then arrive on the leader
+//   warps 4..11  accumulators: promotion + epilogue (bias / relu / relu-mask / zero rows) of
+//                this CTA's 128 rows, TMA stores; WGRAD optimizer fusion as in gemm_tc.cu
+// Each ring stage holds a K block's raw tiles and their lo tiles, so a converter can work as
+// soon as its raw tiles land (up to two K blocks ahead of the MMAs).
+// Barriers: raw full/empty, acc full: per CTA (the leader's commits multicast to both);
+// lo full and acc empty: in the leader, arrived on by both CTAs.
+#include "tc_common.cuh"
+
+namespace hnn {
+
+constexpr int TC2_BM = 128;                // rows per CTA (pair tile: 256)
+constexpr int TC2_BN = 256;                // pair tile columns (each CTA stages 128 of B)
+constexpr int TC2_BK = 32;
+constexpr int TC2_STAGES = 3;  // each stage: raw A | raw B | lo A | lo B (64 KB)
+constexpr int TC2_THREADS = 384;
+constexpr int TC2_CONV_WARPS = 2;
+constexpr int TC2_CHUNK_KB = 4;
+constexpr int TC2_A_BYTES = TC2_BM * TC2_BK * 4;        // 16 KB
+constexpr int TC2_B_BYTES = (TC2_BN / 2) * TC2_BK * 4;  // 16 KB (this CTA's half)
+constexpr int TC2_STAGE = TC2_A_BYTES + TC2_B_BYTES;
+constexpr int TC2_EPI_BYTES = 8 * 32 * 32 * 4;
+constexpr int TC2_SMEM_BYTES = TC2_STAGES * 2 * TC2_STAGE + TC2_EPI_BYTES + 1024 + 256;
+
+#ifdef HNN_TC2_TRACE  // debug build only (tools/tc2_trace.py): per-CTA wait-cycle counters
+__device__ unsigned long long g_tc2_trace[296 * 16];
+#define TC2_T0(v) const long long v = clock64()
+#define TC2_T1(v, slot) tr[slot] += clock64() - (v)
+#else
+#define TC2_T0(v)
+#define TC2_T1(v, slot)
+#endif
+
+template <int OP>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC2_THREADS, 1)
+    gemm_tc2_kernel(const hnn_gemm_problem* __restrict__ probs, int nprob, int total_tiles,
+                    const hnn_step_row* __restrict__ cur, const hnn_model_status* __restrict__ status) {
+  constexpr int A_MN = (OP == HNN_WGRAD) ? 1 : 0;
+  constexpr int B_MN = (OP == HNN_FWD) ? 0 : 1;
+  constexpr int SR = TC2_STAGES;
+  extern __shared__ uint8_t smem_raw[];
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const uint32_t rank = cluster_rank();
+  const bool leader = rank == 0;
+#ifdef HNN_TC2_TRACE
+  const long long t_start = clock64();
+  long long tr[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
+#endif
+
+  uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  const uint32_t raw_base = smem_u32(base);
+  constexpr int SSTRIDE = 2 * TC2_STAGE;  // stage s: raw at s * SSTRIDE, lo right after it
+  const uint32_t epi_base = raw_base + SR * SSTRIDE;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(base + SR * SSTRIDE + TC2_EPI_BYTES);
+  constexpr int RAW_FULL = 0, RAW_EMPTY = SR, LO_FULL = 2 * SR;
+  constexpr int ACC_FULL = 3 * SR, ACC_EMPTY = ACC_FULL + 2, NBARS = ACC_EMPTY + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + NBARS);
+  auto bar = [&](int i) { return smem_u32(bars + i); };
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < SR; ++s) {
+      mbar_init(bar(RAW_FULL + s), 1);                  // local TMA expect_tx arrival + bytes
+      mbar_init(bar(RAW_EMPTY + s), 1);                 // leader MMA commit (multicast): stage free
+      mbar_init(bar(LO_FULL + s), 2 * TC2_CONV_WARPS);  // converter warps of both CTAs (leader's copy)
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(bar(ACC_FULL + b), 1);    // leader MMA commit (multicast)
+      mbar_init(bar(ACC_EMPTY + b), 16);  // 8 accumulator warps x 2 CTAs (leader's copy)
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                 "r"(512));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+  }
+  tc_fence_before();
+  __syncthreads();
+  cluster_sync_all();  // peer barriers initialised before any remote arrive / multicast commit
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  auto tile_info = [&](int tile, const hnn_gemm_problem*& p, int& m0, int& n0, int& nkb, int& rows) -> bool {
+    p = &probs[find_problem(probs, nprob, tile, [](const hnn_gemm_problem& q) { return q.tile_base; })];
+    if (!live(cur, status, p->model)) return false;
+    rows = cur[p->model].rows;
+    const int t = tile - p->tile_base;
+    m0 = (t / p->tiles_n) * (2 * TC2_BM);
+    n0 = (t % p->tiles_n) * TC2_BN;
+    const int ktot = (OP == HNN_WGRAD) ? rows : p->k;
+    nkb = (ktot + TC2_BK - 1) / TC2_BK;
+    return nkb > 0;
+  };
+  const int pair = blockIdx.x / 2, npairs = gridDim.x / 2;
+  // tile schedule (host LPT, trailing the problem table): this pair's tiles are
+  // sched_ids[sched_off[pair] .. sched_off[pair + 1]); round-robin if absent / mismatched
+  const int* sched = reinterpret_cast<const int*>(probs + nprob);
+  const bool use_sched = sched[0] == npairs;
+  const int t_begin = use_sched ? sched[1 + pair] : pair;
+  const int t_end = use_sched ? sched[2 + pair] : total_tiles;
+  const int t_step = use_sched ? 1 : npairs;
+  const int* sched_ids = sched + 2 + npairs;
+  auto tile_id = [&](int i) { return use_sched ? __ldg(sched_ids + i) : i; };
+
+  if (warp == 0) {
+    // ---------------- TMA producer (both CTAs): rows m0 + rank*128.., columns n0 + rank*128..
+    if (lane == 0) {
+      uint32_t kg = 0;
+      for (int ti = t_begin; ti < t_end; ti += t_step) {
+        const int tile = tile_id(ti);
+        const hnn_gemm_problem* p;
+        int m0, n0, nkb, rows;
+        if (!tile_info(tile, p, m0, n0, nkb, rows)) continue;
+        const int am = m0 + int(rank) * TC2_BM, bn = n0 + int(rank) * (TC2_BN / 2);
+        for (int kb = 0; kb < nkb; ++kb, ++kg) {
+          const int s = kg % SR;
+          TC2_T0(t3);
+          if (kg >= SR) mbar_wait(bar(RAW_EMPTY + s), ((kg / SR) - 1) & 1);
+          TC2_T1(t3, 3);
+          const uint32_t st = raw_base + s * SSTRIDE;
+          mbar_expect_tx(bar(RAW_FULL + s), TC2_STAGE);
+          const int k0 = kb * TC2_BK;
+          if (A_MN) {
+#pragma unroll
+            for (int b = 0; b < TC2_BM / 32; ++b) tma_load_2d(st + b * 4096, p->tmap_a, bar(RAW_FULL + s), am + 32 * b, k0);
+          } else {
+            tma_load_2d(st, p->tmap_a, bar(RAW_FULL + s), k0, am);
+          }
+          if (B_MN) {
+#pragma unroll
+            for (int b = 0; b < TC2_BN / 64; ++b)
+              tma_load_2d(st + TC2_A_BYTES + b * 4096, p->tmap_b, bar(RAW_FULL + s), bn + 32 * b, k0);
+          } else {
+            tma_load_2d(st + TC2_A_BYTES, p->tmap_b, bar(RAW_FULL + s), k0, bn);
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ---------------- MMA issuer: leader CTA, one thread
+    if (leader && lane == 0) {
+      constexpr uint32_t idesc = tf32_idesc(2 * TC2_BM, TC2_BN, A_MN, B_MN);
+      constexpr uint32_t alb = A_MN ? 4096 : 16, asb = A_MN ? 512 : 1024, alt = A_MN ? 1 : 2;
+      constexpr uint32_t blb = B_MN ? 4096 : 16, bsb = B_MN ? 512 : 1024, blt = B_MN ? 1 : 2;
+      uint32_t kg = 0, cg = 0;
+      for (int ti = t_begin; ti < t_end; ti += t_step) {
+        const int tile = tile_id(ti);
+        const hnn_gemm_problem* p;
+        int m0, n0, nkb, rows;
+        if (!tile_info(tile, p, m0, n0, nkb, rows)) continue;
+        for (int kb = 0; kb < nkb; ++kb, ++kg) {
+          const int in_chunk = kb % TC2_CHUNK_KB;
+          const uint32_t buf = cg & 1;
+          TC2_T0(t1);
+          if (in_chunk == 0 && cg >= 2) mbar_wait(bar(ACC_EMPTY + buf), ((cg >> 1) - 1) & 1);  // promoted
+          TC2_T1(t1, 1);
+          const int s = kg % SR;
+          const uint32_t a_hi = raw_base + s * SSTRIDE, b_hi = a_hi + TC2_A_BYTES;
+          const uint32_t a_lo = a_hi + TC2_STAGE, b_lo = a_lo + TC2_A_BYTES;
+          const uint32_t acc = tmem + buf * TC2_BN;
+          TC2_T0(t0);
+          mbar_wait(bar(LO_FULL + s), (kg / SR) & 1);  // both CTAs: raw landed, lo written
+          TC2_T1(t0, 0);
+          tc_fence_after();
+#pragma unroll
+          for (int j = 0; j < TC2_BK / 8; ++j) {
+            const uint32_t ao = A_MN ? j * 1024 : j * 32, bo = B_MN ? j * 1024 : j * 32;
+            const uint64_t dah = smem_desc(a_hi + ao, alb, asb, alt), dal = smem_desc(a_lo + ao, alb, asb, alt);
+            const uint64_t dbh = smem_desc(b_hi + bo, blb, bsb, blt), dbl = smem_desc(b_lo + bo, blb, bsb, blt);
+            mma_tf32_pair(acc, dah, dbh, idesc, (in_chunk | j) != 0);
+            mma_tf32_pair(acc, dal, dbh, idesc, 1u);
+            mma_tf32_pair(acc, dah, dbl, idesc, 1u);
+          }
+          mma_commit_pair(bar(RAW_EMPTY + s));  // raw and lo of stage s consumed
+          TC2_T1(t0, 5);
+          if (in_chunk == TC2_CHUNK_KB - 1 || kb == nkb - 1) {
+            mma_commit_pair(bar(ACC_FULL + buf));
+            ++cg;
+          }
+        }
+      }
+    }
+  } else if (warp < 2 + TC2_CONV_WARPS) {
+    // ---------------- converters (both CTAs): lo = rna_tf32(x - trunc_tf32(x)); raw stays as hi
+    const int ct = threadIdx.x - 64;
+    constexpr int CT = 32 * TC2_CONV_WARPS, PER = TC2_STAGE / 16 / CT, NPART = 4, PART = PER / NPART;
+    const uint32_t lo_full_leader = map_cluster(bar(LO_FULL), 0);
+    uint32_t kg = 0;
+    for (int ti = t_begin; ti < t_end; ti += t_step) {
+        const int tile = tile_id(ti);
+      const hnn_gemm_problem* p;
+      int m0, n0, nkb, rows;
+      if (!tile_info(tile, p, m0, n0, nkb, rows)) continue;
+      for (int kb = 0; kb < nkb; ++kb, ++kg) {
+        const int s = kg % SR;
+        TC2_T0(t2);
+        mbar_wait(bar(RAW_FULL + s), (kg / SR) & 1);  // (the stage's lo is free: TMA reused it)
+        TC2_T1(t2, 2);
+        const uint32_t hi = raw_base + s * SSTRIDE, lo = hi + TC2_STAGE;
+#pragma unroll
+        for (int h = 0; h < NPART; ++h) {
+          uint4 v[PART];
+#pragma unroll
+          for (int u = 0; u < PART; ++u) v[u] = lds128(hi + 16 * (ct + (h * PART + u) * CT));
+#pragma unroll
+          for (int u = 0; u < PART; ++u) {
+            // lo = rna_tf32(x - trunc_tf32(x)) (truncating lo instead moved Adam's first-step
+            // weights by 3.3e-4 relative against the oracle: above the per-step tolerance)
+            uint4 o;
+            o.x = tf32_bits(__float_as_uint(__uint_as_float(v[u].x) - __uint_as_float(v[u].x & 0xFFFFE000u)));
+            o.y = tf32_bits(__float_as_uint(__uint_as_float(v[u].y) - __uint_as_float(v[u].y & 0xFFFFE000u)));
+            o.z = tf32_bits(__float_as_uint(__uint_as_float(v[u].z) - __uint_as_float(v[u].z & 0xFFFFE000u)));
+            o.w = tf32_bits(__float_as_uint(__uint_as_float(v[u].w) - __uint_as_float(v[u].w & 0xFFFFE000u)));
+            sts128(lo + 16 * (ct + (h * PART + u) * CT), o);
+          }
+        }
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        __syncwarp();
+        if (lane == 0) mbar_arrive_cluster(lo_full_leader + 8 * s);
+      }
+    }
+  } else {
+    // ---------------- accumulators + epilogue (warps 4..11): lane quarter warp % 4, column half
+    constexpr int HALF = TC2_BN / 2;  // 128 columns per warp
+    const int aw = warp - 2 - TC2_CONV_WARPS, q = warp & 3, half = aw >> 2;
+    const uint32_t lane_base = tmem + (uint32_t(q * 32) << 16) + half * HALF;
+    const uint32_t stg = epi_base + aw * 4096;
+    const uint32_t acc_empty_leader = map_cluster(bar(ACC_EMPTY), 0);
+    uint32_t cg = 0, nstore = 0;
+    for (int ti = t_begin; ti < t_end; ti += t_step) {
+        const int tile = tile_id(ti);
+      const hnn_gemm_problem* p;
+      int m0, n0, nkb, rows;
+      if (!tile_info(tile, p, m0, n0, nkb, rows)) continue;
+      const int nchunks = (nkb + TC2_CHUNK_KB - 1) / TC2_CHUNK_KB;
+      float sum[HALF];
+      for (int c = 0; c < nchunks; ++c, ++cg) {
+        const uint32_t buf = cg & 1;
+        TC2_T0(t4);
+        mbar_wait(bar(ACC_FULL + buf), (cg >> 1) & 1);
+        TC2_T1(t4, 4);
+        tc_fence_after();
+#pragma unroll
+        for (int cb = 0; cb < HALF; cb += 16) {
+          uint32_t r0[16];
+          tmem_ld16(lane_base + buf * TC2_BN + cb, r0);
+#pragma unroll
+          for (int j = 0; j < 16; ++j)
+            sum[cb + j] = (c == 0) ? __uint_as_float(r0[j]) : __fadd_rn(sum[cb + j], __uint_as_float(r0[j]));
+        }
+        TC2_T1(t4, 6);
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive_cluster(acc_empty_leader + 8 * buf);
+      }
+      TC2_T0(t5);
+      // epilogue: this CTA's rows m0 + rank*128 + q*32 + lane, columns n0 + half*128 + cb + j.
+      // Problem fields are copied to registers first: the smem stores below carry a "memory"
+      // clobber, which would otherwise reload them from global memory per element.
+      const int pm = p->m, pn = p->n, ldc = p->ldc;
+      const float* bias = p->bias;
+      const bool relu = (p->relu & 1) != 0;
+      float* const cptr = p->c;
+      const void* tmap_c = p->tmap_c;
+      float* const ow = p->opt_w;
+      float* const owm = p->opt_wm;
+      float* const owv = p->opt_wv;
+      const bool fuse = OP == HNN_WGRAD && ow != nullptr;
+      const Update u = fuse ? make_update(cur[p->model], p->opt_kind, p->opt_momentum) : Update{};
+      const int row0 = m0 + int(rank) * TC2_BM + q * 32, row = row0 + lane;
+      const int nh = n0 + half * HALF;
+      const bool zero_row = (OP != HNN_WGRAD) && row >= rows;
+      const float* mrow = (OP == HNN_DGRAD && p->mask && row < pm) ? p->mask + size_t(row) * ldc : nullptr;
+#pragma unroll
+      for (int cb = 0; cb < HALF; cb += 32) {
+        if (nh + cb >= pn || row0 >= pm) continue;  // 32 x 32 block outside the problem
+        if (lane == 0 && nstore > 0) tma_store_wait_read();  // previous store done reading staging
+        __syncwarp();
+        // registers (lane = row) -> 128B-swizzled staging (16-byte chunk j of row r at chunk
+        // j ^ (r & 7): conflict-free STS.128) -> one TMA store per 32 x 32 block
+        float bv = 0.0f;
+        if (OP == HNN_FWD && nh + cb + lane < pn) bv = __ldg(bias + nh + cb + lane);  // lane j: column j
+#pragma unroll
+        for (int j4 = 0; j4 < 8; ++j4) {
+          float v[4], mv[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+          if (OP == HNN_DGRAD && mrow) {  // this row's relu mask, 4 columns
+            const int n = nh + cb + j4 * 4;
+            if (n + 3 < pn && (ldc & 3) == 0) {
+              const float4 m4 = __ldg(reinterpret_cast<const float4*>(mrow + n));
+              mv[0] = m4.x; mv[1] = m4.y; mv[2] = m4.z; mv[3] = m4.w;
+            } else {
+#pragma unroll
+              for (int e = 0; e < 4; ++e) mv[e] = n + e < pn ? __ldg(mrow + n + e) : 0.0f;
+            }
+          }
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            const int jj = j4 * 4 + e;
+            float x = sum[cb + jj];
+            if (OP == HNN_FWD) {
+              const float b = __shfl_sync(0xffffffffu, bv, jj);  // column jj's bias
+              if (zero_row) x = 0.0f;
+              else {
+                x = __fadd_rn(x, b);  // columns >= n are clipped by the TMA store
+                if (relu) x = np_relu(x);
+              }
+            } else if (OP == HNN_DGRAD) {
+              if (zero_row) x = 0.0f;
+              else if (mrow) x = np_mask(x, mv[e]);
+            }
+            v[e] = x;
+          }
+          sts128(stg + lane * 128 + ((j4 ^ (lane & 7)) << 4),
+                 make_uint4(__float_as_uint(v[0]), __float_as_uint(v[1]), __float_as_uint(v[2]), __float_as_uint(v[3])));
+        }
+        __syncwarp();
+        if (fuse) {
+          // fused optimizer: lane = column, so W / moment accesses of a row are one coalesced
+          // 128-byte transaction; the gradient comes back out of the swizzled staging block
+          const int n = nh + cb + lane;
+          if (n < pn) {
+            const int rmax = min(32, pm - row0);
+            for (int rr = 0; rr < rmax; ++rr) {
+              const float g = lds32(stg + rr * 128 + ((((lane >> 2) ^ (rr & 7))) << 4) + ((lane & 3) << 2));
+              const size_t off = size_t(row0 + rr) * ldc + n;
+              float w = ow[off], mm = owm ? owm[off] : 0.0f, vv = owv ? owv[off] : 0.0f;
+              update_one(u, w, g, mm, vv);
+              ow[off] = w;
+              if (owm) owm[off] = mm;
+              if (owv) owv[off] = vv;
+            }
+          }
+          __syncwarp();
+        }
+        if (cptr != nullptr) {
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+          __syncwarp();
+          if (lane == 0) tma_store_2d(tmap_c, stg, nh + cb, row0);
+          ++nstore;
+        }
+      }
+      TC2_T1(t5, 7);
+    }
+    if (lane == 0) tma_store_wait_all();
+  }
+  TC2_T0(t6);
+  tc_fence_before();
+  __syncthreads();
+  TC2_T1(t6, 8);
+#ifdef HNN_TC2_TRACE
+  if (threadIdx.x == 0) g_tc2_trace[blockIdx.x * 16 + 15] += clock64() - t_start;
+  if ((threadIdx.x & 31) == 0)
+    for (int i = 0; i < 9; ++i)
+      if (tr[i]) atomicAdd(&g_tc2_trace[blockIdx.x * 16 + i], (unsigned long long)tr[i]);
+#endif
+  cluster_sync_all();  // the leader's MMAs into the peer's TMEM are complete
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512));
+  }
+}
+
+int gemm_tc2_tile_shape(int op, int32_t* tm, int32_t* tn) {
+  *tm = 2 * TC2_BM;
+  *tn = TC2_BN;
+  return HNN_OK;
+}
+
+int launch_colsum(const hnn_gemm_problem* probs, int nprob, const hnn_step_row* cur, const hnn_model_status* status,
+                  cudaStream_t s);
+
+int grouped_gemm_tc2(int op, const hnn_gemm_problem* probs, int nprob, int total_tiles, const hnn_step_row* cur,
+                     const hnn_model_status* status, cudaStream_t s) {
+  static bool configured[3] = {false, false, false};
+  if (!configured[op]) {
+    cudaError_t e;
+    if (op == HNN_FWD) e = cudaFuncSetAttribute(gemm_tc2_kernel<HNN_FWD>, cudaFuncAttributeMaxDynamicSharedMemorySize, TC2_SMEM_BYTES);
+    else if (op == HNN_DGRAD) e = cudaFuncSetAttribute(gemm_tc2_kernel<HNN_DGRAD>, cudaFuncAttributeMaxDynamicSharedMemorySize, TC2_SMEM_BYTES);
+    else e = cudaFuncSetAttribute(gemm_tc2_kernel<HNN_WGRAD>, cudaFuncAttributeMaxDynamicSharedMemorySize, TC2_SMEM_BYTES);
+    if (e != cudaSuccess) {
+      set_error("hnn_grouped_gemm(tc2)", cudaGetErrorString(e));
+      return HNN_ERR_CUDA;
+    }
+    configured[op] = true;
+  }
+  static int sms = 0;
+  if (!sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  }
+  const int pairs = total_tiles < sms / 2 ? total_tiles : sms / 2;
+  const int grid = 2 * pairs;
+  if (op == HNN_FWD)
+    gemm_tc2_kernel<HNN_FWD><<<grid, TC2_THREADS, TC2_SMEM_BYTES, s>>>(probs, nprob, total_tiles, cur, status);
+  else if (op == HNN_DGRAD)
+    gemm_tc2_kernel<HNN_DGRAD><<<grid, TC2_THREADS, TC2_SMEM_BYTES, s>>>(probs, nprob, total_tiles, cur, status);
+  else {
+    gemm_tc2_kernel<HNN_WGRAD><<<grid, TC2_THREADS, TC2_SMEM_BYTES, s>>>(probs, nprob, total_tiles, cur, status);
+    int rc = check_launch("hnn_grouped_gemm(tc2)");
+    if (rc) return rc;
+    return launch_colsum(probs, nprob, cur, status, s);
+  }
+  return check_launch("hnn_grouped_gemm(tc2)");
+}
+
+}  // namespace hnn
+
+#ifdef HNN_TC2_TRACE
+extern "C" int hnn_debug_tc2_trace(void* host_out, int reset) {
+  cudaMemcpyFromSymbol(host_out, hnn::g_tc2_trace, sizeof(hnn::g_tc2_trace));
+  if (reset) {
+    static unsigned long long zeros[296 * 16] = {};
+    cudaMemcpyToSymbol(hnn::g_tc2_trace, zeros, sizeof(zeros));
+  }
+  return 0;
+}
+#endif

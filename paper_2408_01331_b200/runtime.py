@@ -20,6 +20,8 @@ Everything here calls the C-ABI (``_native``); nothing computes on the CPU.
 """
 from __future__ import annotations
 
+import os
+
 import math
 from dataclasses import dataclass, field
 
@@ -221,9 +223,9 @@ class Launch:
         N.call(self.entry, *self.args, stream)
 
 
-def _dev_table(cls, rows, device):
+def _dev_table(cls, rows, device, extra: bytes = b""):
     torch = _torch()
-    raw = N.table_bytes(cls, rows)
+    raw = N.table_bytes(cls, rows) + extra
     t = torch.frombuffer(bytearray(raw), dtype=torch.uint8).to(device)
     return t
 
@@ -260,6 +262,8 @@ class DeviceHybrid:
         self.slots = slots
         self.n = len(slots)
         self.use_tc = use_tensor_cores
+        # CTA-pair tcgen05 GEMM (HNN_TC_PAIR=0: single-CTA kernel)
+        self.use_pairs = os.environ.get("HNN_TC_PAIR", "1") != "0"
         off = 0
         for s in slots:
             s.stages, s.classes, _ = lower_graph(s.graph)
@@ -480,9 +484,36 @@ class DeviceHybrid:
         ptrs = ("b", "c", "mask") if op == N.HNN_DGRAD else ("b", "c", "opt_w", "opt_wm", "opt_wv")
         return all(d.get(k, 0) % 16 == 0 for k in ptrs)
 
+    def _pair_schedule(self, probs, rows, total_tiles, tm, tn) -> bytes:
+        """Longest-processing-time assignment of a CTA-pair launch's tiles to its pairs (the
+        table trailer read by gemm_tc2.cu): int32 npairs, offsets[npairs + 1], tile ids.
+        Cost of a tile = its 32-wide K blocks + a fixed epilogue share.  Which pair computes a
+        tile never changes the tile's arithmetic (bit-exact isolation)."""
+        torch = _torch()
+        sms = torch.cuda.get_device_properties(self.device).multi_processor_count
+        npairs = max(1, min(total_tiles, sms // 2))
+        costs = []
+        for pr, (s, d) in zip(probs, rows):
+            kb = -(-d["k"] // 32)
+            tiles = pr.tiles_n * -(-d["m"] // tm)
+            costs += [(kb + 3, pr.tile_base + i) for i in range(tiles)]
+        costs.sort(key=lambda c: (-c[0], c[1]))
+        import heapq
+
+        heap = [(0, p) for p in range(npairs)]
+        lists = [[] for _ in range(npairs)]
+        for cost, tile in costs:
+            load, p = heapq.heappop(heap)
+            lists[p].append(tile)
+            heapq.heappush(heap, (load + cost, p))
+        offs = np.zeros(npairs + 1, dtype=np.int32)
+        offs[1:] = np.cumsum([len(l) for l in lists])
+        ids = np.array([t for l in lists for t in l], dtype=np.int32)
+        return np.concatenate([np.array([npairs], np.int32), offs, ids]).tobytes()
+
     def _gemm_launch(self, op, items, label):
         """items: list of (slot, stage).  Splits into SIMT / 3xTF32 launches."""
-        groups = {N.PREC_SIMT: [], N.PREC_SIMT_SKINNY: [], N.PREC_3XTF32: []}
+        groups = {N.PREC_SIMT: [], N.PREC_SIMT_SKINNY: [], N.PREC_3XTF32: [], N.PREC_3XTF32_PAIR: []}
         for s, st in items:
             cap = s.batch_size
             K, U = int(np.prod(st.in_shape)), st.out_shape[0]
@@ -511,7 +542,9 @@ class DeviceHybrid:
                              opt_bv=arena(self.m2, st.params[1]) if kind == N.OPT_ADAM else 0,
                              opt_kind=kind, opt_momentum=float(np.float32(s.momentum)))
             if self.use_tc and self._route_tc(op, d):
-                prec = N.PREC_3XTF32
+                # CTA-pair 256x256 tiles (one launch per wave, LPT-scheduled); HNN_TC_PAIR=0
+                # selects the single-CTA 128x128 kernel
+                prec = N.PREC_3XTF32_PAIR if self.use_pairs else N.PREC_3XTF32
             elif self._route_skinny(op, d):
                 prec = N.PREC_SIMT_SKINNY
             else:
@@ -530,7 +563,7 @@ class DeviceHybrid:
                 probs.append(N.GemmProblem(tile_base=base, tiles_n=tiles_n, model=s.index, **d))
                 base += tiles_m * tiles_n
             keep = None
-            if prec == N.PREC_3XTF32:
+            if prec in (N.PREC_3XTF32, N.PREC_3XTF32_PAIR):
                 torch = _torch()
                 maps = bytearray(128 * 3 * len(probs))
                 host = (N.GemmProblem * len(probs))(*probs)
@@ -540,7 +573,10 @@ class DeviceHybrid:
                     pr.tmap_a = _ptr(keep) + 384 * i
                     pr.tmap_b = _ptr(keep) + 384 * i + 128
                     pr.tmap_c = _ptr(keep) + 384 * i + 256
-            t = _dev_table(N.GemmProblem, probs, self.device)
+            extra = b""
+            if prec == N.PREC_3XTF32_PAIR:
+                extra = self._pair_schedule(probs, rows, base, tm, tn)
+            t = _dev_table(N.GemmProblem, probs, self.device, extra)
             flops = sum(2 * d["m"] * d["n"] * d["k"] for _, d in rows)
             # bytes: A + B read once, C written once (fp32); a fused optimizer adds its p/m/v traffic
             nbytes = sum(4 * (d["m"] * d["k"] + d["k"] * d["n"] + (d["m"] * d["n"] if d.get("c") else 0))
@@ -549,7 +585,7 @@ class DeviceHybrid:
             nbytes += sum(per_param[d["opt_kind"]] * d["m"] * (d["n"] + 1) for _, d in rows if d.get("opt_w"))
             launch = Launch("hnn_grouped_gemm", (op, prec, _ptr(t), len(probs), base, _ptr(self.cur),
                                                  _ptr(self.status)), t,
-                            f"{label}/{ {N.PREC_SIMT: 'simt', N.PREC_SIMT_SKINNY: 'simt16', N.PREC_3XTF32: 'tc'}[prec] }",
+                            f"{label}/{ {N.PREC_SIMT: 'simt', N.PREC_SIMT_SKINNY: 'simt16', N.PREC_3XTF32: 'tc', N.PREC_3XTF32_PAIR: 'tc2'}[prec] }",
                             flops=flops, nbytes=nbytes)
             launch.maps = keep
             out.append(launch)

@@ -347,7 +347,7 @@ def test_step_gradients_match_oracle(pkg, name):
     for pid, g in ref.items():
         assert rel(got["grads"][pid], g) <= 1e-5, (name, pid, rel(got["grads"][pid], g))
     if name == "c3_mlp":
-        assert any(l.endswith("/tc") for l in labels)
+        assert any(l.endswith(("/tc", "/tc2")) for l in labels)
 
 
 @pytest.mark.parametrize("fuse", [True, False])
@@ -368,8 +368,8 @@ def test_tensor_core_path_matches_cuda_core_path(pkg, name):
     """3xTF32 tcgen05 GEMMs vs the fp32 FFMA kernels: first-step gradients agree to fp32 noise."""
     tc, tc_labels, _ = _first_step_grads(pkg, name, True)
     simt, simt_labels, _ = _first_step_grads(pkg, name, False)
-    assert any(l.endswith("/tc") for l in tc_labels)
-    assert not any(l.endswith("/tc") for l in simt_labels)
+    assert any(l.endswith(("/tc", "/tc2")) for l in tc_labels)
+    assert not any(l.endswith(("/tc", "/tc2")) for l in simt_labels)
     for pid in tc["grads"]:
         assert rel(tc["grads"][pid], simt["grads"][pid]) <= 5e-6, pid
 
@@ -540,3 +540,37 @@ def test_exact_div_sqrt_match_numpy(pkg):
     bad_q, bad_r = ~same(gq, rq), ~same(gr, rr)
     assert not bad_q.any(), (A[bad_q][:5], B[bad_q][:5], gq[bad_q][:5], rq[bad_q][:5], int(bad_q.sum()))
     assert not bad_r.any(), (A[bad_r][:5], gr[bad_r][:5], rr[bad_r][:5], int(bad_r.sum()))
+
+
+@pytest.mark.parametrize("hidden,batch", [((384, 320), 200), ((640, 136), 256)])
+def test_pair_tensor_core_gemms_match_oracle(pkg, hidden, batch):
+    """CTA-pair (cta_group::2, 256x256 tiles) 3xTF32 GEMMs on every op: first-step gradients vs the
+    numpy oracle (rel <= 1e-5) and vs the FFMA path, incl. a ragged 200-row batch (tile rows beyond
+    the batch) and widths that are not multiples of the 256-column tile."""
+    from paper_2408_01331_b200 import store, zoo
+
+    splits = oracle.blob_splits("pair", "mini", 10, 784, 600, 64)
+    ds = store.from_splits(splits)
+    graph = zoo.mlp(784, hidden, 10)
+
+    def grads(tc):
+        job = pkg.TrainingJob("p", graph, ds.content_hash, pkg.HyperParams(1, batch, 0.01, "sgd", (), 5), 0, 0)
+        h = pkg.merge([job])
+        grabbed = {}
+        tr = pkg.Trainer(h, pkg.make_plan("fcfs", [job]), [job], {"p": ds}, use_tensor_cores=tc, keep_grads=True,
+                         fuse_optimizer=False)
+        tr.step_observer = lambda j, p: grabbed or grabbed.update(grads=tr.device.download_grads(0))
+        tr.run()
+        return grabbed["grads"], [l.label for l in tr.device.train_plan]
+
+    got, labels = grads(True)
+    assert sum(l.endswith("/tc2") for l in labels) >= 3, labels  # FWD, DGRAD and WGRAD on pairs
+    ref_simt, _ = grads(False)
+    params = oracle.init_model(graph, 5)
+    bx, by, _ = oracle.epoch_batches(splits["train_x"], splits["train_y"], ds.content_hash, batch, 5, 0)[0]
+    logits, tape = oracle.model_forward(graph, params, bx)
+    _, dl = oracle.sce_loss_and_grad(logits, by)
+    ref = oracle.model_backward(tape, dl)
+    for pid, g in ref.items():
+        assert rel(got[pid], g) <= 1e-5, (pid, rel(got[pid], g))
+        assert rel(got[pid], ref_simt[pid]) <= 1e-5, (pid, rel(got[pid], ref_simt[pid]))
