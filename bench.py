@@ -40,8 +40,10 @@ WORKLOADS = {
     "c2": "C2: 8 LeNet-5 per GPU, SGD lr 0.01, batch 128, synthetic CIFAR-shaped 50000x3x32x32",
     "c5": "C5: 32 MLP 784-256-10 per GPU (256 over 8), SGD lr 10^(-3+2i/255), batch 64, MNIST-shaped blob",
     "c1": "C1: 2 MLP 784-256-10, SGD lr 0.01/0.05, batch 64, MNIST-shaped blob",
+    "c4": "C4: 4 CNNs per GPU (32 over 8): ResNet-18-plain, VGG-11-noBN, 2 LeNet-5; SGD lr 1e-3, batch 128, "
+          "synthetic CIFAR-shaped 50000x3x32x32",
 }
-MODELS_PER_GPU = {"c3": 32, "c2": 8, "c5": 32, "c1": 2}
+MODELS_PER_GPU = {"c3": 32, "c2": 8, "c5": 32, "c1": 2, "c4": 4}
 
 
 def peaks():
@@ -62,7 +64,7 @@ def dist_env():
 def make_dataset(workload):
     from paper_2408_01331_b200 import zoo
 
-    if workload == "c2":
+    if workload in ("c2", "c4"):
         return zoo.image_dataset()
     return zoo.blob_dataset()
 

@@ -110,7 +110,7 @@ def c3_width(i: int) -> int:
 
 
 def config_jobs(config: str, dataset, first_model=0, count=None, epochs=1):
-    """Jobs of a BASELINE config ("c1", "c2", "c3", "c5") with global model ids."""
+    """Jobs of a BASELINE config ("c1" .. "c5") with global model ids."""
     if config == "c1":
         ids, make = range(2), lambda i: job(f"m{i:03d}", mlp(), dataset, i, epochs, 64, (0.01, 0.05)[i], "sgd", i)
     elif config == "c2":
@@ -121,6 +121,13 @@ def config_jobs(config: str, dataset, first_model=0, count=None, epochs=1):
         def make(i):
             h = c3_width(i)
             return job(f"m{i:03d}", mlp(784, (h, h), 10), dataset, i, epochs, 256, 1e-3, "adam", i)
+    elif config == "c4":
+        # 32 mixed CNNs, 4 per GPU: {ResNet-18-plain, VGG-11-noBN, 2 x LeNet-5}
+        ids = range(32)
+
+        def make(i):
+            graph = (resnet18_plain, vgg11_nobn, lenet5, lenet5)[i % 4]()
+            return job(f"m{i:03d}", graph, dataset, i, epochs, 128, 1e-3, "sgd", i)
     elif config == "c5":
         ids = range(256)
 
