@@ -150,6 +150,24 @@ typedef struct hnn_gemm_problem {
   float* opt_bv;
   int32_t opt_kind; /* HNN_OPT_* */
   float opt_momentum;
+  /* Convolution lowering (HNN_PREC_F32_3XTF32_PAIR; 1 / 0 for dense layers):
+   *   row_mult    GEMM rows (FWD/DGRAD M, WGRAD K) per batch sample (OH*OW for a conv): this
+   *               step's valid rows are cur.rows * row_mult;
+   *   c_mode      FWD output layout: 0 row-major [m, ldc]; 1 NCHW, element (m, n) at
+   *               c[((m / row_mult) * n_total + n) * row_mult + m % row_mult], n_total = n; with
+   *               c_mode 1 a non-NULL mask (same NCHW layout) multiplies by (mask > 0) and a NULL
+   *               bias adds nothing (a conv input gradient computed as a forward conv of dy);
+   *   ksplit      WGRAD fixed K split count (>= 1): split s covers K rows [s*ksplit_len,
+   *               (s+1)*ksplit_len) and writes rows [s*m, (s+1)*m) of c (the TMA map covers
+   *               ksplit*m rows); the splits are summed in order by hnn_gemm_ksplit_reduce. */
+  int32_t row_mult;
+  int32_t c_mode;
+  int32_t ksplit;
+  int32_t ksplit_len;
+  /* HNN_PREC_F32_3XTF32_PAIR: tile columns 64, 128 or 256 (0 = 256); the K-major B TMA box is
+   * tile_n / 2 rows (each CTA of the pair stages half of the tile's B columns). */
+  int32_t tile_n;
+  int32_t reserved;
 } hnn_gemm_problem;
 
 /* Tile edge (m, n) used by (op, prec); lets the host lay out tile_base / tiles_n. */
@@ -283,6 +301,50 @@ int hnn_multi_tensor_sgd(const hnn_opt_segment* segs, int nseg, int total_chunks
                          const hnn_model_status* status, void* stream);
 int hnn_multi_tensor_adam(const hnn_opt_segment* segs, int nseg, int total_chunks, const hnn_step_row* cur,
                           const hnn_model_status* status, void* stream);
+
+/*
+ * Tensor-core convolution path (conv_tc.cu): a conv2d layer lowered onto the CTA-pair GEMM
+ * (HNN_PREC_F32_3XTF32_PAIR) with explicit im2col buffers; NCHW activations.  Replaces the same
+ * reference functions as hnn_grouped_conv (ops.py:91-130) for layers with C*k*k, F >= 64.
+ *   HNN_CONVTC_IM2COL        cols[m, kk] = x[b, c, oh*s-p+r, ow*s-p+s'], m = (b, oh, ow), kk = (c, r, s');
+ *                            rows are kkp wide (pad columns zero)
+ *   HNN_CONVTC_TRANSPOSE_DY  dyt[m, f] = dy[b, f, oh, ow]; bpart[b, f] = sum_hw dy[b, f, hw]
+ *   HNN_CONVTC_COL2IM        dx[b, c, h, w] = (mask > 0) * sum_(r, s') dcols[m, kk] (gather, tap order)
+ *   HNN_CONVTC_WGRAD_REDUCE  dw[f, kk] = sum_s partial[s][f][kk] (splits in order); db[f] = sum_b bpart[b, f]
+ * Each problem covers `blocks` CTAs starting at block_base: im2col one per (32 output pixels, 32
+ * channels), transpose one per (sample, 32 pixels, 32 filters), col2im one per (sample, input row,
+ * 32 columns, 16 channels), reduce any count (grid-stride).  max_k = largest kernel size (<= 3).
+ */
+#define HNN_CONVTC_IM2COL 0
+#define HNN_CONVTC_TRANSPOSE_DY 1
+#define HNN_CONVTC_COL2IM 2
+#define HNN_CONVTC_WGRAD_REDUCE 3
+#define HNN_CONVTC_PAD_WEIGHTS 4  /* wpad[f, kk'] = w[f, kk] (kk' < kkp, zero pad): when C*k*k % 4 != 0 */
+#define HNN_CONVTC_FLIP_WEIGHTS 5 /* wpad[c, (f, r, s)] = w[f, c, k-1-r, k-1-s]: stride-1 input gradient as a
+                                     forward conv of dy (im2col of dy with pad k-1-pad, then a GEMM) */
+
+typedef struct hnn_convtc_problem {
+  const float* x;    /* [cap, c, h, w] */
+  float* cols;       /* [cap*oh*ow, kk] */
+  const float* dy;   /* [cap, f, oh, ow] */
+  float* dyt;        /* [cap*oh*ow, f] */
+  const float* dcols;/* [cap*oh*ow, kk] */
+  float* dx;         /* [cap, c, h, w] */
+  const float* mask; /* [cap, c, h, w] or NULL */
+  const float* partial; /* [ksplit, f, kk] */
+  float* dw;         /* [f, kk] */
+  float* db;         /* [f] */
+  float* bpart;      /* [cap, f] */
+  const float* weight; /* [f, kk] (HNN_CONVTC_PAD_WEIGHTS) */
+  float* wpad;       /* [f, kkp] */
+  int32_t cap, c, h, w, f, k, stride, pad, oh, ow, kk;
+  int32_t kkp;       /* cols / partial / wpad row length: kk rounded up to a multiple of 4 */
+  int32_t ksplit, ksplit_len;
+  int32_t model, block_base, blocks;
+} hnn_convtc_problem;
+
+int hnn_conv_tc_aux(int op, const hnn_convtc_problem* probs, int nprob, int total_blocks, int max_k,
+                    const hnn_step_row* cur, const hnn_model_status* status, void* stream);
 
 /* Self-test of the optimizer's exact float32 arithmetic (no reference counterpart): for i < n,
  * q[i] = a[i] / b[i] and r[i] = sqrt(a[i]) with the same round-to-nearest-even routines the

@@ -15,6 +15,8 @@ LIB_PATH = Path(__file__).resolve().parent / "_lib" / "libhnn_b200.so"
 
 HNN_FWD, HNN_DGRAD, HNN_WGRAD = 0, 1, 2
 PREC_SIMT, PREC_3XTF32, PREC_SIMT_SKINNY, PREC_3XTF32_PAIR = 0, 1, 2, 3
+CONVTC_IM2COL, CONVTC_TRANSPOSE_DY, CONVTC_COL2IM, CONVTC_WGRAD_REDUCE, CONVTC_PAD_WEIGHTS = 0, 1, 2, 3, 4
+CONVTC_FLIP_WEIGHTS = 5
 OPT_SGD, OPT_SGD_MOMENTUM, OPT_ADAM = 0, 1, 2
 CONV_DIRECT_BCHUNK = 4
 
@@ -43,7 +45,13 @@ class GemmProblem(C.Structure):
                 ("m", I), ("n", I), ("k", I), ("lda", I), ("ldb", I), ("ldc", I),
                 ("model", I), ("relu", I), ("tile_base", I), ("tiles_n", I), ("tmap_a", P), ("tmap_b", P),
                 ("tmap_c", P), ("opt_w", P), ("opt_wm", P), ("opt_wv", P), ("opt_b", P), ("opt_bm", P),
-                ("opt_bv", P), ("opt_kind", I), ("opt_momentum", C.c_float)]
+                ("opt_bv", P), ("opt_kind", I), ("opt_momentum", C.c_float),
+                ("row_mult", I), ("c_mode", I), ("ksplit", I), ("ksplit_len", I), ("tile_n", I), ("reserved", I)]
+
+    def __init__(self, **kw):
+        kw.setdefault("row_mult", 1)
+        kw.setdefault("ksplit", 1)
+        super().__init__(**kw)
 
 
 class ConvProblem(C.Structure):
@@ -52,6 +60,14 @@ class ConvProblem(C.Structure):
                 ("cap", I), ("c", I), ("h", I), ("w", I), ("f", I), ("k", I), ("stride", I), ("pad", I),
                 ("oh", I), ("ow", I), ("model", I), ("relu", I), ("tile_base", I), ("tiles_n", I),
                 ("splits", I), ("split_len", I)]
+
+
+class ConvTcProblem(C.Structure):
+    _fields_ = [("x", P), ("cols", P), ("dy", P), ("dyt", P), ("dcols", P), ("dx", P), ("mask", P),
+                ("partial", P), ("dw", P), ("db", P), ("bpart", P), ("weight", P), ("wpad", P),
+                ("cap", I), ("c", I), ("h", I), ("w", I), ("f", I), ("k", I), ("stride", I), ("pad", I),
+                ("oh", I), ("ow", I), ("kk", I), ("kkp", I), ("ksplit", I), ("ksplit_len", I),
+                ("model", I), ("block_base", I), ("blocks", I)]
 
 
 class PoolProblem(C.Structure):
@@ -77,7 +93,7 @@ class OptSegment(C.Structure):
 STRUCTS = {
     "hnn_step_row": StepRow, "hnn_model_status": ModelStatus, "hnn_gather_problem": GatherProblem,
     "hnn_gemm_problem": GemmProblem, "hnn_conv_problem": ConvProblem, "hnn_pool_problem": PoolProblem,
-    "hnn_relu_problem": ReluProblem, "hnn_sce_problem": SceProblem, "hnn_opt_segment": OptSegment,
+    "hnn_relu_problem": ReluProblem, "hnn_convtc_problem": ConvTcProblem, "hnn_sce_problem": SceProblem, "hnn_opt_segment": OptSegment,
 }
 
 # every symbol include/hnn_b200.h declares, with its ctypes signature
@@ -99,6 +115,7 @@ SIGNATURES = {
     "hnn_multi_tensor_sgd": [P, C.c_int, C.c_int, P, P, VP],
     "hnn_multi_tensor_adam": [P, C.c_int, C.c_int, P, P, VP],
     "hnn_selftest_div_sqrt": [VP, VP, VP, VP, C.c_int64, VP],
+    "hnn_conv_tc_aux": [C.c_int, P, C.c_int, C.c_int, C.c_int, P, P, VP],
     "hnn_struct_size": [C.c_char_p],
     "hnn_last_error": [],
     "hnn_version": [],

@@ -78,6 +78,7 @@ int hnn_struct_size(const char* name) {
   if (!strcmp(name, "hnn_relu_problem")) return sizeof(hnn_relu_problem);
   if (!strcmp(name, "hnn_sce_problem")) return sizeof(hnn_sce_problem);
   if (!strcmp(name, "hnn_opt_segment")) return sizeof(hnn_opt_segment);
+  if (!strcmp(name, "hnn_convtc_problem")) return sizeof(hnn_convtc_problem);
   return -1;
 }
 

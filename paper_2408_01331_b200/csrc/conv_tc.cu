@@ -1,0 +1,328 @@
+// Data-movement kernels around the tensor-core convolution path (pkg/src/hybridnn/ops.py:91-130).
+//
+// A conv2d layer big enough for the tensor cores (C*k*k and F >= 64) is lowered onto the CTA-pair
+// 3xTF32 GEMM (gemm_tc2.cu) with NCHW activations kept in the reference layout:
+//   FWD    cols[m, kk] = im2col(x)  (m = (b, oh, ow), kk = (c, r, s): the reference's K order)
+//          y = cols x W^T + bias (+relu)      GEMM epilogue stores NCHW directly (c_mode 1)
+//   DGRAD  dyT[m, f] = dy (NCHW -> rows)      transpose
+//          dcols = dyT x W                    GEMM (row-major [m, kk])
+//          dx = col2im(dcols) * (x > 0)       gather form, taps in (r, s) order, no atomics
+//   WGRAD  partial[s] = dyT^T x cols          GEMM, fixed K splits over output pixels
+//          dW = sum_s partial[s] (in order); db = sum_b sum_hw dy (in order)
+// Every kernel is a fixed function of the problem's shape (bit-exact isolation, no atomics).
+#include "common.cuh"
+
+namespace hnn {
+
+constexpr int CT_THREADS = 256;
+
+__device__ __forceinline__ const hnn_convtc_problem& ct_problem(const hnn_convtc_problem* probs, int nprob,
+                                                                int block) {
+  return probs[find_problem(probs, nprob, block, [](const hnn_convtc_problem& q) { return q.block_base; })];
+}
+
+// cols[m, kk] for m < cap*OH*OW, kk < K (row stride kkp): zeros outside the image (padding) and for
+// samples beyond this step's batch rows.  One CTA = 32 consecutive output pixels x 32 channels:
+// the x reads (lane = pixel) and the cols writes (a pixel's 32*k*k contiguous floats, lane-strided)
+// are both coalesced, through a shared-memory tile of 32 x (32*k*k) floats.
+constexpr int IC_PIX = 32, IC_CH = 32;
+
+__global__ void __launch_bounds__(CT_THREADS) im2col_kernel(const hnn_convtc_problem* __restrict__ probs, int nprob,
+                                                           const hnn_step_row* __restrict__ cur,
+                                                           const hnn_model_status* __restrict__ status) {
+  extern __shared__ float ic_tile[];  // [IC_PIX][IC_CH * k * k + 1]
+  const hnn_convtc_problem& p = ct_problem(probs, nprob, blockIdx.x);
+  if (!live(cur, status, p.model)) return;
+  const int rows = cur[p.model].rows;
+  const int kk2 = p.k * p.k, seg = IC_CH * kk2, ld = seg + 1;
+  const int ohw = p.oh * p.ow;
+  const int cblocks = (p.c + IC_CH - 1) / IC_CH;
+  const int t = blockIdx.x - p.block_base;
+  const int pb = t / cblocks, cb = t - pb * cblocks;
+  const int m0 = pb * IC_PIX, c0 = cb * IC_CH;
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const int m = m0 + lane;
+  const int b = m / ohw, o = m - b * ohw, oh = o / p.ow, ow = o - oh * p.ow;
+  const bool valid = m < p.cap * ohw && b < rows;
+  for (int ci = warp; ci < IC_CH; ci += CT_THREADS / 32) {
+    const int c = c0 + ci;
+    const float* xc = p.x + (size_t(b) * p.c + c) * p.h * p.w;
+    for (int r = 0; r < p.k; ++r) {
+      const int h = oh * p.stride - p.pad + r;
+      for (int s = 0; s < p.k; ++s) {
+        const int w = ow * p.stride - p.pad + s;
+        float v = 0.0f;
+        if (valid && c < p.c && h >= 0 && h < p.h && w >= 0 && w < p.w) v = __ldg(xc + h * p.w + w);
+        ic_tile[lane * ld + ci * kk2 + r * p.k + s] = v;
+      }
+    }
+  }
+  __syncthreads();
+  const int width = min(seg, (p.c - c0) * kk2);
+  for (int pi = warp; pi < IC_PIX; pi += CT_THREADS / 32) {
+    const int mm = m0 + pi;
+    if (mm >= p.cap * ohw) break;
+    float* dst = p.cols + size_t(mm) * p.kkp + c0 * kk2;
+    for (int j = lane; j < width; j += 32) dst[j] = ic_tile[pi * ld + j];
+    if (cb == 0)  // zero pad columns kk..kkp-1 (TMA needs 16-byte rows)
+      for (int j = p.kk + lane; j < p.kkp; j += 32) p.cols[size_t(mm) * p.kkp + j] = 0.0f;
+  }
+}
+
+int im2col_smem_bytes(int k) { return IC_PIX * (IC_CH * k * k + 1) * 4; }
+
+// dyT[m, f] = dy[b, f, hw] (m = b*HW + hw) through a 32 x 32 shared-memory tile per (b, hw, f)
+// block; bpart[b, f] = sum over hw of dy[b, f, hw] (sequential, for the bias gradient).
+__global__ void __launch_bounds__(CT_THREADS) transpose_dy_kernel(const hnn_convtc_problem* __restrict__ probs,
+                                                                 int nprob, const hnn_step_row* __restrict__ cur,
+                                                                 const hnn_model_status* __restrict__ status) {
+  __shared__ float tile[32][33];
+  const hnn_convtc_problem& p = ct_problem(probs, nprob, blockIdx.x);
+  if (!live(cur, status, p.model)) return;
+  const int rows = cur[p.model].rows;
+  const int hw_n = p.oh * p.ow;
+  const int tiles_hw = (hw_n + 31) / 32, tiles_f = (p.f + 31) / 32;
+  const int t = blockIdx.x - p.block_base;
+  const int b = t / (tiles_hw * tiles_f), r = t - b * tiles_hw * tiles_f;
+  const int th = r / tiles_f, tf = r - th * tiles_f;
+  if (b >= rows) return;  // rows beyond the batch are never read by the GEMMs
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // 32 x 8
+  for (int j = ty; j < 32; j += 8) {
+    const int f = tf * 32 + j, hw = th * 32 + tx;
+    tile[j][tx] = (f < p.f && hw < hw_n) ? __ldg(p.dy + (size_t(b) * p.f + f) * hw_n + hw) : 0.0f;
+  }
+  __syncthreads();
+  for (int j = ty; j < 32; j += 8) {
+    const int hw = th * 32 + j, f = tf * 32 + tx;
+    if (hw < hw_n && f < p.f) p.dyt[(size_t(b) * hw_n + hw) * p.f + f] = tile[tx][j];
+  }
+  if (th == 0 && ty == 0) {  // one warp per (b, 32 filters): sequential sum over hw
+    const int f = tf * 32 + tx;
+    if (f < p.f) {
+      const float* src = p.dy + (size_t(b) * p.f + f) * hw_n;
+      float acc = -0.0f;
+      for (int hw = 0; hw < hw_n; ++hw) acc = __fadd_rn(acc, __ldg(src + hw));
+      p.bpart[size_t(b) * p.f + f] = acc;
+    }
+  }
+}
+
+// dx[b, c, h, w] = (x > 0 if masked) * sum over taps (r, s) in order of dcols[m(oh, ow), (c, r, s)]
+// with h = oh*stride - pad + r, w = ow*stride - pad + s; zeros for samples beyond the batch.
+// One CTA = one input row segment (b, h, 32 columns) x 16 channels: the dcols rows it needs
+// (valid oh, an ow window) are staged in shared memory with coalesced row reads, then each thread
+// (column, channel) gathers its taps from the tile.
+constexpr int CI_W = 32, CI_CH = 16, CI_OWMAX = 40;
+
+// STRIDE / K as template parameters: the tap arithmetic is shifts and compares (runtime integer
+// divisions made this kernel issue-bound: ~900 instructions per output element, ncu IPC 2.5).
+template <int STRIDE, int K>
+__device__ __forceinline__ void col2im_tile(const hnn_convtc_problem& p, int rows, float* ci_tile) {
+  constexpr int KK2 = K * K, SEG = CI_CH * KK2, SLD = SEG + 1;
+  const int wblocks = (p.w + CI_W - 1) / CI_W, cblocks = (p.c + CI_CH - 1) / CI_CH;
+  int t = blockIdx.x - p.block_base;
+  const int cb = t % cblocks;
+  t /= cblocks;
+  const int wb = t % wblocks;
+  t /= wblocks;
+  const int h = t % p.h, b = t / p.h;
+  const int c0 = cb * CI_CH, w0 = wb * CI_W;
+  const int w1 = min(p.w, w0 + CI_W) - 1;
+  // output-column window touched by input columns w0..w1 (any tap): ow in [ow_lo, ow_hi]
+  const int ow_lo = max(0, (w0 + p.pad - (K - 1) + STRIDE - 1) / STRIDE);
+  const int ow_hi = min(p.ow - 1, (w1 + p.pad) / STRIDE);
+  const int nw = ow_hi - ow_lo + 1;
+  const bool live_rows = b < rows;
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  // staged rows: (valid tap row r, output column ow_lo + i); their source / destination offsets
+  // go to a small table so that every thread then issues all its 16-byte loads back to back
+  // (a row-at-a-time copy loop serialised ~13 L2 round trips per warp)
+  __shared__ int row_src[K * CI_OWMAX], row_dst[K * CI_OWMAX];
+  __shared__ int nrows_s;
+  if (threadIdx.x == 0) {
+    int n = 0;
+    if (live_rows && nw > 0) {
+      for (int r = 0; r < K; ++r) {
+        const int hh = h + p.pad - r;
+        if (hh < 0 || (STRIDE > 1 && hh % STRIDE) || hh / STRIDE >= p.oh) continue;
+        for (int i = 0; i < nw; ++i, ++n) {
+          row_src[n] = int(((size_t(b) * p.oh + hh / STRIDE) * p.ow + ow_lo + i) * p.kkp / 4);
+          row_dst[n] = (r * CI_OWMAX + i) * SLD;
+        }
+      }
+    }
+    nrows_s = n;
+  }
+  __syncthreads();
+  {
+    const int width = min(SEG, (p.c - c0) * KK2);
+    const bool vec = (width & 3) == 0 && (p.kkp & 3) == 0 && ((c0 * KK2) & 3) == 0;
+    const int w4 = vec ? width / 4 : 0;
+    const int total = nrows_s * w4;
+    const float4* base4 = reinterpret_cast<const float4*>(p.dcols) + (c0 * KK2) / 4;
+    constexpr int PER = (3 * CI_OWMAX * SEG / 4 + CT_THREADS - 1) / CT_THREADS;  // max loads per thread
+    float4 v[PER];
+#pragma unroll
+    for (int u = 0; u < PER; ++u) {
+      const int e = threadIdx.x + u * CT_THREADS;
+      if (e < total) {
+        const int q = e / (SEG / 4), j = e - q * (SEG / 4);  // constant divisor
+        v[u] = j < w4 ? __ldg(base4 + row_src[q] + j) : make_float4(0.0f, 0.0f, 0.0f, 0.0f);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < PER; ++u) {
+      const int e = threadIdx.x + u * CT_THREADS;
+      if (e < total) {
+        const int q = e / (SEG / 4), j = e - q * (SEG / 4);
+        float* dst = ci_tile + row_dst[q] + 4 * j;
+        dst[0] = v[u].x;
+        dst[1] = v[u].y;
+        dst[2] = v[u].z;
+        dst[3] = v[u].w;
+      }
+    }
+    if (!vec && live_rows) {  // unaligned channel segments (not produced by the planner)
+      for (int e = threadIdx.x; e < nrows_s * width; e += CT_THREADS) {
+        const int q = e / width, j = e - q * width;
+        ci_tile[row_dst[q] + j] = __ldg(p.dcols + size_t(row_src[q]) * 4 + c0 * KK2 + j);
+      }
+    }
+  }
+  __syncthreads();
+  for (int e = threadIdx.x; e < CI_W * CI_CH; e += CT_THREADS) {
+    const int ci = e / CI_W, w = w0 + e % CI_W, c = c0 + ci;
+    if (w >= p.w || c >= p.c) continue;
+    float acc = 0.0f;
+    if (live_rows) {
+#pragma unroll
+      for (int r = 0; r < K; ++r) {
+        const int hh = h + p.pad - r;
+        if (hh < 0 || (STRIDE > 1 && hh % STRIDE) || hh / STRIDE >= p.oh) continue;
+#pragma unroll
+        for (int s = 0; s < K; ++s) {
+          const int ww = w + p.pad - s;
+          if (ww < 0 || (STRIDE > 1 && ww % STRIDE)) continue;
+          const int ow = ww / STRIDE;
+          if (ow >= p.ow) continue;
+          acc = __fadd_rn(acc, ci_tile[(r * CI_OWMAX + ow - ow_lo) * SLD + ci * KK2 + r * K + s]);
+        }
+      }
+    }
+    const size_t off = ((size_t(b) * p.c + c) * p.h + h) * p.w + w;
+    if (live_rows && p.mask) acc = np_mask(acc, __ldg(p.mask + off));
+    p.dx[off] = acc;
+  }
+}
+
+__global__ void __launch_bounds__(CT_THREADS) col2im_kernel(const hnn_convtc_problem* __restrict__ probs, int nprob,
+                                                           const hnn_step_row* __restrict__ cur,
+                                                           const hnn_model_status* __restrict__ status) {
+  extern __shared__ float ci_tile[];  // [k][CI_OWMAX][CI_CH * k * k + 1]
+  const hnn_convtc_problem& p = ct_problem(probs, nprob, blockIdx.x);
+  if (!live(cur, status, p.model)) return;
+  const int rows = cur[p.model].rows;
+  if (p.k == 3 && p.stride == 1) col2im_tile<1, 3>(p, rows, ci_tile);
+  else if (p.k == 3 && p.stride == 2) col2im_tile<2, 3>(p, rows, ci_tile);
+  else if (p.k == 2 && p.stride == 1) col2im_tile<1, 2>(p, rows, ci_tile);
+  else if (p.k == 2 && p.stride == 2) col2im_tile<2, 2>(p, rows, ci_tile);
+  else if (p.k == 1 && p.stride == 1) col2im_tile<1, 1>(p, rows, ci_tile);
+  else if (p.k == 1 && p.stride == 2) col2im_tile<2, 1>(p, rows, ci_tile);
+  // other (kernel, stride) pairs are not routed to this path (runtime.py)
+}
+
+int col2im_smem_bytes(int k) { return k * CI_OWMAX * (CI_CH * k * k + 1) * 4; }
+
+// dW[f, kk] = sum over the valid splits (in order) of partial[s*F + f, kk];
+// db[f] = sum over batch rows (in order) of bpart[b, f].
+__global__ void __launch_bounds__(CT_THREADS) wgrad_reduce_kernel(const hnn_convtc_problem* __restrict__ probs,
+                                                                 int nprob, const hnn_step_row* __restrict__ cur,
+                                                                 const hnn_model_status* __restrict__ status) {
+  const hnn_convtc_problem& p = ct_problem(probs, nprob, blockIdx.x);
+  if (!live(cur, status, p.model)) return;
+  const int rows = cur[p.model].rows;
+  const long long kmax = (long long)rows * p.oh * p.ow;
+  const int splits = int(min((long long)p.ksplit, (kmax + p.ksplit_len - 1) / p.ksplit_len));
+  const long long total = (long long)p.f * p.kk, ptotal = (long long)p.f * p.kkp;
+  for (long long e = (long long)(blockIdx.x - p.block_base) * CT_THREADS + threadIdx.x; e < total + p.f;
+       e += (long long)p.blocks * CT_THREADS) {
+    if (e < total) {
+      const long long f = e / p.kk, pe = f * p.kkp + (e - f * p.kk);  // partial rows are kkp wide
+      float acc = 0.0f;
+      for (int s = 0; s < splits; ++s) acc = __fadd_rn(acc, __ldg(p.partial + size_t(s) * ptotal + pe));
+      p.dw[e] = acc;
+    } else {
+      const int f = int(e - total);
+      float acc = 0.0f;
+      for (int b = 0; b < rows; ++b) acc = __fadd_rn(acc, __ldg(p.bpart + size_t(b) * p.f + f));
+      p.db[f] = acc;
+    }
+  }
+}
+
+// wpad[f, kk'] = w[f, kk] for kk < K, 0 for the pad columns (GEMM B operand with 16-byte rows).
+__global__ void __launch_bounds__(CT_THREADS) pad_weights_kernel(const hnn_convtc_problem* __restrict__ probs, int nprob,
+                                                                const hnn_step_row* __restrict__ cur,
+                                                                const hnn_model_status* __restrict__ status) {
+  const hnn_convtc_problem& p = ct_problem(probs, nprob, blockIdx.x);
+  if (!live(cur, status, p.model)) return;
+  const long long total = (long long)p.f * p.kkp;
+  for (long long e = (long long)(blockIdx.x - p.block_base) * CT_THREADS + threadIdx.x; e < total;
+       e += (long long)p.blocks * CT_THREADS) {
+    const long long f = e / p.kkp, j = e - f * p.kkp;
+    p.wpad[e] = j < p.kk ? __ldg(p.weight + f * p.kk + j) : 0.0f;
+  }
+}
+
+// Flipped, transposed weights for the stride-1 input gradient computed as a forward conv of dy:
+// wflip[c, (f, r', s')] = w[f, c, k-1-r', k-1-s'] (row length f*k*k; written to p.wpad).
+__global__ void __launch_bounds__(CT_THREADS) flip_weights_kernel(const hnn_convtc_problem* __restrict__ probs,
+                                                                 int nprob, const hnn_step_row* __restrict__ cur,
+                                                                 const hnn_model_status* __restrict__ status) {
+  const hnn_convtc_problem& p = ct_problem(probs, nprob, blockIdx.x);
+  if (!live(cur, status, p.model)) return;
+  const int kk2 = p.k * p.k, row = p.f * kk2;
+  const long long total = (long long)p.c * row;
+  for (long long e = (long long)(blockIdx.x - p.block_base) * CT_THREADS + threadIdx.x; e < total;
+       e += (long long)p.blocks * CT_THREADS) {
+    const int c = int(e / row), j = int(e - (long long)c * row);
+    const int f = j / kk2, rs = j - f * kk2, r = rs / p.k, s = rs - r * p.k;
+    p.wpad[e] = __ldg(p.weight + ((size_t(f) * p.c + c) * p.k + (p.k - 1 - r)) * p.k + (p.k - 1 - s));
+  }
+}
+
+}  // namespace hnn
+
+extern "C" int hnn_conv_tc_aux(int op, const hnn_convtc_problem* probs, int nprob, int total_blocks, int max_k,
+                               const hnn_step_row* cur, const hnn_model_status* status, void* stream) {
+  HNN_REQUIRE(probs && cur && nprob > 0 && total_blocks > 0, "hnn_conv_tc_aux", "bad arguments");
+  cudaStream_t s = hnn::as_stream(stream);
+  switch (op) {
+    case HNN_CONVTC_IM2COL:
+      HNN_REQUIRE(max_k > 0 && max_k <= 3, "hnn_conv_tc_aux", "kernel size above 3");
+      cudaFuncSetAttribute(hnn::im2col_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, hnn::im2col_smem_bytes(3));
+      hnn::im2col_kernel<<<total_blocks, hnn::CT_THREADS, hnn::im2col_smem_bytes(max_k), s>>>(probs, nprob, cur, status);
+      break;
+    case HNN_CONVTC_TRANSPOSE_DY:
+      hnn::transpose_dy_kernel<<<total_blocks, hnn::CT_THREADS, 0, s>>>(probs, nprob, cur, status);
+      break;
+    case HNN_CONVTC_COL2IM:
+      HNN_REQUIRE(max_k > 0 && max_k <= 3, "hnn_conv_tc_aux", "kernel size above 3");
+      cudaFuncSetAttribute(hnn::col2im_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, hnn::col2im_smem_bytes(3));
+      hnn::col2im_kernel<<<total_blocks, hnn::CT_THREADS, hnn::col2im_smem_bytes(max_k), s>>>(probs, nprob, cur, status);
+      break;
+    case HNN_CONVTC_PAD_WEIGHTS:
+      hnn::pad_weights_kernel<<<total_blocks, hnn::CT_THREADS, 0, s>>>(probs, nprob, cur, status);
+      break;
+    case HNN_CONVTC_FLIP_WEIGHTS:
+      hnn::flip_weights_kernel<<<total_blocks, hnn::CT_THREADS, 0, s>>>(probs, nprob, cur, status);
+      break;
+    case HNN_CONVTC_WGRAD_REDUCE:
+      hnn::wgrad_reduce_kernel<<<total_blocks, hnn::CT_THREADS, 0, s>>>(probs, nprob, cur, status);
+      break;
+    default:
+      hnn::set_error("hnn_conv_tc_aux", "unknown op");
+      return HNN_ERR_INVALID;
+  }
+  return hnn::check_launch("hnn_conv_tc_aux");
+}

@@ -332,7 +332,7 @@ __global__ void colsum_kernel(const hnn_gemm_problem* __restrict__ probs, int np
   if ((!p.dbias && !p.opt_b) || !live(cur, status, p.model)) return;
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= p.m) return;
-  const int R = cur[p.model].rows;
+  const int R = cur[p.model].rows * p.row_mult;
   // loads of 16 rows issue before their (sequential, order-preserving) adds: the loop is
   // latency-bound otherwise (58 us per C3 launch at one load in flight per thread)
   float acc = -0.0f;
@@ -453,8 +453,9 @@ extern "C" int hnn_gemm_tc_encode(int op, const hnn_gemm_problem* host_probs, in
     const hnn_gemm_problem& p = host_probs[i];
     int rc;
     if (op == HNN_FWD) {          // A = X[cap, K] (K-major), B = W[N, K] (K-major)
+      const uint32_t brows = p.tile_n > 0 ? uint32_t(p.tile_n / 2) : uint32_t(hnn::TC_BN);
       rc = hnn::encode_2d(&maps[3 * i], p.a, p.k, p.m, p.lda, hnn::TC_BM, false);
-      if (!rc) rc = hnn::encode_2d(&maps[3 * i + 1], p.b, p.k, p.n, p.ldb, hnn::TC_BN, false);
+      if (!rc) rc = hnn::encode_2d(&maps[3 * i + 1], p.b, p.k, p.n, p.ldb, brows, false);
     } else if (op == HNN_DGRAD) { // A = dY[cap, U] (K-major), B = W[U, N] (N-major)
       rc = hnn::encode_2d(&maps[3 * i], p.a, p.k, p.m, p.lda, hnn::TC_BM, false);
       if (!rc) rc = hnn::encode_2d(&maps[3 * i + 1], p.b, p.n, p.k, p.ldb, 32, true);
@@ -463,7 +464,9 @@ extern "C" int hnn_gemm_tc_encode(int op, const hnn_gemm_problem* host_probs, in
       if (!rc) rc = hnn::encode_2d(&maps[3 * i + 1], p.b, p.n, p.k, p.ldb, 32, true);
     }
     // C (all ops): row-major [m, n] with row stride ldc; 32x32 boxes, 128-byte swizzle
-    if (!rc && p.c) rc = hnn::encode_2d(&maps[3 * i + 2], p.c, p.n, p.m, p.ldc, 32, false);
+    // (a K-split WGRAD writes ksplit stacked [m, n] partials)
+    const uint64_t crows = uint64_t(p.m) * uint64_t(op == HNN_WGRAD && p.ksplit > 1 ? p.ksplit : 1);
+    if (!rc && p.c) rc = hnn::encode_2d(&maps[3 * i + 2], p.c, p.n, crows, p.ldc, 32, false);
     if (rc) {
       hnn::set_error("hnn_gemm_tc_encode", "cuTensorMapEncodeTiled failed (alignment / stride / driver)");
       return rc;

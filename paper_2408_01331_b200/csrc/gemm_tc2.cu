@@ -103,15 +103,32 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC2_THREADS, 1)
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
 
-  auto tile_info = [&](int tile, const hnn_gemm_problem*& p, int& m0, int& n0, int& nkb, int& rows) -> bool {
+  // tile -> (problem, m0, n0, K blocks, valid rows, K offset, split); rows = this step's valid
+  // GEMM rows (batch rows x row_mult: output pixels of a conv).  WGRAD tiles are split along K
+  // into ksplit fixed ranges (t = (mt * tiles_n + nt) * ksplit + split).
+  auto tile_info = [&](int tile, const hnn_gemm_problem*& p, int& m0, int& n0, int& nkb, int& rows, int& kofs,
+                       int& sp, int& tn) -> bool {
     p = &probs[find_problem(probs, nprob, tile, [](const hnn_gemm_problem& q) { return q.tile_base; })];
     if (!live(cur, status, p->model)) return false;
-    rows = cur[p->model].rows;
-    const int t = tile - p->tile_base;
+    rows = cur[p->model].rows * p->row_mult;
+    int t = tile - p->tile_base;
+    sp = 0;
+    kofs = 0;
+    int ktot = p->k;
+    if (OP == HNN_WGRAD) {
+      ktot = rows;
+      const int S = p->ksplit;
+      if (S > 1) {
+        sp = t % S;
+        t /= S;
+        kofs = sp * p->ksplit_len;
+        ktot = min(rows, kofs + p->ksplit_len) - kofs;
+      }
+    }
+    tn = p->tile_n > 0 ? p->tile_n : TC2_BN;  // pair tile columns: 64, 128 or 256
     m0 = (t / p->tiles_n) * (2 * TC2_BM);
-    n0 = (t % p->tiles_n) * TC2_BN;
-    const int ktot = (OP == HNN_WGRAD) ? rows : p->k;
-    nkb = (ktot + TC2_BK - 1) / TC2_BK;
+    n0 = (t % p->tiles_n) * tn;
+    nkb = ktot > 0 ? (ktot + TC2_BK - 1) / TC2_BK : 0;
     return nkb > 0;
   };
   const int pair = blockIdx.x / 2, npairs = gridDim.x / 2;
@@ -132,17 +149,18 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC2_THREADS, 1)
       for (int ti = t_begin; ti < t_end; ti += t_step) {
         const int tile = tile_id(ti);
         const hnn_gemm_problem* p;
-        int m0, n0, nkb, rows;
-        if (!tile_info(tile, p, m0, n0, nkb, rows)) continue;
-        const int am = m0 + int(rank) * TC2_BM, bn = n0 + int(rank) * (TC2_BN / 2);
+        int m0, n0, nkb, rows, kofs, sp, tn;
+        if (!tile_info(tile, p, m0, n0, nkb, rows, kofs, sp, tn)) continue;
+        const int am = m0 + int(rank) * TC2_BM, bn = n0 + int(rank) * (tn / 2);
+        const uint32_t stage_bytes = TC2_A_BYTES + (tn / 2) * TC2_BK * 4;
         for (int kb = 0; kb < nkb; ++kb, ++kg) {
           const int s = kg % SR;
           TC2_T0(t3);
           if (kg >= SR) mbar_wait(bar(RAW_EMPTY + s), ((kg / SR) - 1) & 1);
           TC2_T1(t3, 3);
           const uint32_t st = raw_base + s * SSTRIDE;
-          mbar_expect_tx(bar(RAW_FULL + s), TC2_STAGE);
-          const int k0 = kb * TC2_BK;
+          mbar_expect_tx(bar(RAW_FULL + s), stage_bytes);
+          const int k0 = kofs + kb * TC2_BK;
           if (A_MN) {
 #pragma unroll
             for (int b = 0; b < TC2_BM / 32; ++b) tma_load_2d(st + b * 4096, p->tmap_a, bar(RAW_FULL + s), am + 32 * b, k0);
@@ -150,8 +168,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC2_THREADS, 1)
             tma_load_2d(st, p->tmap_a, bar(RAW_FULL + s), k0, am);
           }
           if (B_MN) {
-#pragma unroll
-            for (int b = 0; b < TC2_BN / 64; ++b)
+            for (int b = 0; b < tn / 64; ++b)
               tma_load_2d(st + TC2_A_BYTES + b * 4096, p->tmap_b, bar(RAW_FULL + s), bn + 32 * b, k0);
           } else {
             tma_load_2d(st + TC2_A_BYTES, p->tmap_b, bar(RAW_FULL + s), k0, bn);
@@ -162,15 +179,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC2_THREADS, 1)
   } else if (warp == 1) {
     // ---------------- MMA issuer: leader CTA, one thread
     if (leader && lane == 0) {
-      constexpr uint32_t idesc = tf32_idesc(2 * TC2_BM, TC2_BN, A_MN, B_MN);
       constexpr uint32_t alb = A_MN ? 4096 : 16, asb = A_MN ? 512 : 1024, alt = A_MN ? 1 : 2;
       constexpr uint32_t blb = B_MN ? 4096 : 16, bsb = B_MN ? 512 : 1024, blt = B_MN ? 1 : 2;
       uint32_t kg = 0, cg = 0;
       for (int ti = t_begin; ti < t_end; ti += t_step) {
         const int tile = tile_id(ti);
         const hnn_gemm_problem* p;
-        int m0, n0, nkb, rows;
-        if (!tile_info(tile, p, m0, n0, nkb, rows)) continue;
+        int m0, n0, nkb, rows, kofs, sp, tn;
+        if (!tile_info(tile, p, m0, n0, nkb, rows, kofs, sp, tn)) continue;
+        const uint32_t idesc = tf32_idesc(2 * TC2_BM, tn, A_MN, B_MN);
         for (int kb = 0; kb < nkb; ++kb, ++kg) {
           const int in_chunk = kb % TC2_CHUNK_KB;
           const uint32_t buf = cg & 1;
@@ -212,16 +229,18 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC2_THREADS, 1)
     for (int ti = t_begin; ti < t_end; ti += t_step) {
         const int tile = tile_id(ti);
       const hnn_gemm_problem* p;
-      int m0, n0, nkb, rows;
-      if (!tile_info(tile, p, m0, n0, nkb, rows)) continue;
+      int m0, n0, nkb, rows, kofs, sp, tn;
+      if (!tile_info(tile, p, m0, n0, nkb, rows, kofs, sp, tn)) continue;
       for (int kb = 0; kb < nkb; ++kb, ++kg) {
         const int s = kg % SR;
         TC2_T0(t2);
         mbar_wait(bar(RAW_FULL + s), (kg / SR) & 1);  // (the stage's lo is free: TMA reused it)
         TC2_T1(t2, 2);
         const uint32_t hi = raw_base + s * SSTRIDE, lo = hi + TC2_STAGE;
+        const int n16 = (TC2_A_BYTES + (tn / 2) * TC2_BK * 4) / 16;  // this tile's A + B-half 16-byte chunks
 #pragma unroll
         for (int h = 0; h < NPART; ++h) {
+          if ((h * PART) * CT >= n16) break;
           uint4 v[PART];
 #pragma unroll
           for (int u = 0; u < PART; ++u) v[u] = lds128(hi + 16 * (ct + (h * PART + u) * CT));
@@ -244,18 +263,20 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC2_THREADS, 1)
     }
   } else {
     // ---------------- accumulators + epilogue (warps 4..11): lane quarter warp % 4, column half
-    constexpr int HALF = TC2_BN / 2;  // 128 columns per warp
+    constexpr int HALF = TC2_BN / 2;  // up to 128 columns per warp (tile_n / 2)
     const int aw = warp - 2 - TC2_CONV_WARPS, q = warp & 3, half = aw >> 2;
-    const uint32_t lane_base = tmem + (uint32_t(q * 32) << 16) + half * HALF;
+    const uint32_t lane_quarter = tmem + (uint32_t(q * 32) << 16);
     const uint32_t stg = epi_base + aw * 4096;
     const uint32_t acc_empty_leader = map_cluster(bar(ACC_EMPTY), 0);
     uint32_t cg = 0, nstore = 0;
     for (int ti = t_begin; ti < t_end; ti += t_step) {
         const int tile = tile_id(ti);
       const hnn_gemm_problem* p;
-      int m0, n0, nkb, rows;
-      if (!tile_info(tile, p, m0, n0, nkb, rows)) continue;
+      int m0, n0, nkb, rows, kofs, sp, tn;
+      if (!tile_info(tile, p, m0, n0, nkb, rows, kofs, sp, tn)) continue;
       const int nchunks = (nkb + TC2_CHUNK_KB - 1) / TC2_CHUNK_KB;
+      const int hn = tn / 2;  // this warp's columns: [half * hn, half * hn + hn)
+      const uint32_t lane_base = lane_quarter + half * hn;
       float sum[HALF];
       for (int c = 0; c < nchunks; ++c, ++cg) {
         const uint32_t buf = cg & 1;
@@ -265,6 +286,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC2_THREADS, 1)
         tc_fence_after();
 #pragma unroll
         for (int cb = 0; cb < HALF; cb += 16) {
+          if (cb >= hn) break;
           uint32_t r0[16];
           tmem_ld16(lane_base + buf * TC2_BN + cb, r0);
 #pragma unroll
@@ -289,20 +311,24 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC2_THREADS, 1)
       float* const owm = p->opt_wm;
       float* const owv = p->opt_wv;
       const bool fuse = OP == HNN_WGRAD && ow != nullptr;
+      const bool nchw = OP == HNN_FWD && p->c_mode == 1;  // conv output straight to NCHW
+      const float* nmask = nchw ? p->mask : nullptr;
+      const int hw_n = p->row_mult;
       const Update u = fuse ? make_update(cur[p->model], p->opt_kind, p->opt_momentum) : Update{};
       const int row0 = m0 + int(rank) * TC2_BM + q * 32, row = row0 + lane;
-      const int nh = n0 + half * HALF;
+      const int nh = n0 + half * hn;
       const bool zero_row = (OP != HNN_WGRAD) && row >= rows;
       const float* mrow = (OP == HNN_DGRAD && p->mask && row < pm) ? p->mask + size_t(row) * ldc : nullptr;
 #pragma unroll
       for (int cb = 0; cb < HALF; cb += 32) {
+        if (cb >= hn) break;
         if (nh + cb >= pn || row0 >= pm) continue;  // 32 x 32 block outside the problem
         if (lane == 0 && nstore > 0) tma_store_wait_read();  // previous store done reading staging
         __syncwarp();
         // registers (lane = row) -> 128B-swizzled staging (16-byte chunk j of row r at chunk
         // j ^ (r & 7): conflict-free STS.128) -> one TMA store per 32 x 32 block
         float bv = 0.0f;
-        if (OP == HNN_FWD && nh + cb + lane < pn) bv = __ldg(bias + nh + cb + lane);  // lane j: column j
+        if (OP == HNN_FWD && bias && nh + cb + lane < pn) bv = __ldg(bias + nh + cb + lane);  // lane j: column j
 #pragma unroll
         for (int j4 = 0; j4 < 8; ++j4) {
           float v[4], mv[4] = {0.0f, 0.0f, 0.0f, 0.0f};
@@ -333,9 +359,27 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC2_THREADS, 1)
             }
             v[e] = x;
           }
+          if (nchw) {
+            // element (pixel row, filter n) -> y[b][n][hw]: for a fixed n the 32 lanes (rows =
+            // consecutive pixels) write consecutive addresses
+            if (row < pm) {
+              const int b = row / hw_n, hw = row - b * hw_n;
+#pragma unroll
+              for (int e = 0; e < 4; ++e) {
+                const int n = nh + cb + j4 * 4 + e;
+                if (n < pn) {
+                  const size_t off = (size_t(b) * pn + n) * hw_n + hw;
+                  // (a conv input gradient computed as a forward conv of dy: relu mask of the input)
+                  cptr[off] = nmask ? (zero_row ? 0.0f : np_mask(v[e], __ldg(nmask + off))) : v[e];
+                }
+              }
+            }
+            continue;
+          }
           sts128(stg + lane * 128 + ((j4 ^ (lane & 7)) << 4),
                  make_uint4(__float_as_uint(v[0]), __float_as_uint(v[1]), __float_as_uint(v[2]), __float_as_uint(v[3])));
         }
+        if (nchw) continue;
         __syncwarp();
         if (fuse) {
           // fused optimizer: lane = column, so W / moment accesses of a row are one coalesced
@@ -358,7 +402,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC2_THREADS, 1)
         if (cptr != nullptr) {
           asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
           __syncwarp();
-          if (lane == 0) tma_store_2d(tmap_c, stg, nh + cb, row0);
+          if (lane == 0) tma_store_2d(tmap_c, stg, nh + cb, row0 + sp * pm);  // split sp: rows sp*m..
           ++nstore;
         }
       }

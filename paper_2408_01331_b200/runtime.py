@@ -82,6 +82,17 @@ class Stage:
     idx = None
     partial = None
     splits: int = 0
+    # tensor-core conv lowering (im2col + CTA-pair GEMM)
+    tc: bool = False
+    ksplit: int = 1
+    ksplit_len: int = 0
+    cols = None
+    dyt = None
+    bpart = None
+    kkp: int = 0
+    wpad = None
+    dg_fwd: bool = False
+    wflip = None
 
 
 def lower_graph(graph) -> tuple:
@@ -320,6 +331,7 @@ class DeviceHybrid:
             s.batch_y = self.label_arena[b:b + cap]
             prev_out, prev_ld = s.batch_x, ld0
             widest = ld0
+            dcols_need = 0
             for st in s.stages:
                 st.x, st.ld_in = prev_out, prev_ld
                 feats = int(np.prod(st.out_shape))
@@ -336,14 +348,44 @@ class DeviceHybrid:
                     c, h, w = st.in_shape
                     f, oh, ow = self._conv_out(st)
                     k = st.attrs["kernel"]
-                    # small layers (LeNet-class) use the direct shared-memory kernels
+                    # small layers (LeNet-class) use the direct shared-memory kernels; layers with
+                    # C*k*k and F >= 64 go to the tensor cores (im2col + CTA-pair 3xTF32 GEMM)
                     st.direct = N.conv_direct_ok(c, h, w, f, k, oh, ow)
-                    st.splits = (-(-cap // N.CONV_DIRECT_BCHUNK) if st.direct
-                                 else -(-cap * oh * ow // CONV_SPLIT_LEN))
-                    st.partial = torch.zeros(st.splits * f * (c * k * k + 1), dtype=torch.float32, device=dev)
+                    kk = c * k * k
+                    st.tc = (not st.direct and self.use_tc and self.use_pairs and kk >= 16
+                             and f >= 64 and f % 4 == 0 and k <= 3 and st.attrs.get("stride", 1) <= 2)
+                    if st.tc:
+                        pix = cap * oh * ow
+                        st.kkp = _align4(kk)  # cols / weight rows padded to 16 bytes for TMA
+                        st.wpad = (torch.zeros(f * st.kkp, dtype=torch.float32, device=dev)
+                                   if st.kkp != kk else None)
+                        kk = st.kkp
+                        tiles_mn = -(-f // 256) * -(-kk // 256)
+                        split = max(1, min(-(-148 // tiles_mn), -(-pix // 1024)))
+                        st.ksplit_len = -(-(-(-pix // split)) // 32) * 32
+                        st.ksplit = -(-pix // st.ksplit_len)
+                        st.cols = torch.zeros(pix * kk, dtype=torch.float32, device=dev)
+                        st.dyt = torch.zeros(pix * f, dtype=torch.float32, device=dev)
+                        st.bpart = torch.zeros(cap * f, dtype=torch.float32, device=dev)
+                        st.partial = torch.zeros(st.ksplit * f * kk, dtype=torch.float32, device=dev)
+                        # input gradient: stride 1 -> a forward conv of dy (im2col of dy, flipped
+                        # weights; scratch [cap*H*W, F*k*k]); stride 2 -> dcols GEMM + col2im
+                        st.dg_fwd = st.attrs.get("stride", 1) == 1 and (f * k * k) % 4 == 0
+                        if st.needs_dx and st.dg_fwd:
+                            st.wflip = torch.zeros(c * f * k * k, dtype=torch.float32, device=dev)
+                            dcols_need = max(dcols_need, cap * h * w * f * k * k)
+                        elif st.needs_dx:
+                            dcols_need = max(dcols_need, pix * kk)
+                    else:
+                        st.splits = (-(-cap // N.CONV_DIRECT_BCHUNK) if st.direct
+                                     else -(-cap * oh * ow // CONV_SPLIT_LEN))
+                        st.partial = torch.zeros(st.splits * f * (c * k * k + 1), dtype=torch.float32, device=dev)
                 widest = max(widest, st.ld_out, st.ld_in)
                 prev_out, prev_ld = st.y, st.ld_out
             s.grads_buf = [torch.zeros(cap * widest, dtype=torch.float32, device=dev) for _ in range(2)]
+            # one DGRAD column scratch per model: a tensor-core conv's dcols lives only between its
+            # DGRAD GEMM and col2im, inside one backward wave
+            s.dcols = torch.zeros(max(dcols_need, 4), dtype=torch.float32, device=dev) if dcols_need else None
             for k, st in enumerate(s.stages):
                 st.dy = s.grads_buf[k % 2][: cap * st.ld_out].view(cap, st.ld_out)
                 st.dx = s.grads_buf[(k + 1) % 2][: cap * st.ld_in].view(cap, st.ld_in)
@@ -484,7 +526,7 @@ class DeviceHybrid:
         ptrs = ("b", "c", "mask") if op == N.HNN_DGRAD else ("b", "c", "opt_w", "opt_wm", "opt_wv")
         return all(d.get(k, 0) % 16 == 0 for k in ptrs)
 
-    def _pair_schedule(self, probs, rows, total_tiles, tm, tn) -> bytes:
+    def _pair_schedule(self, probs, rows, total_tiles, tm) -> bytes:
         """Longest-processing-time assignment of a CTA-pair launch's tiles to its pairs (the
         table trailer read by gemm_tc2.cu): int32 npairs, offsets[npairs + 1], tile ids.
         Cost of a tile = its 32-wide K blocks + a fixed epilogue share.  Which pair computes a
@@ -494,9 +536,11 @@ class DeviceHybrid:
         npairs = max(1, min(total_tiles, sms // 2))
         costs = []
         for pr, (s, d) in zip(probs, rows):
-            kb = -(-d["k"] // 32)
-            tiles = pr.tiles_n * -(-d["m"] // tm)
-            costs += [(kb + 3, pr.tile_base + i) for i in range(tiles)]
+            split = d.get("ksplit", 1) if d.get("ksplit_len") else 1
+            kb = -(-(d["ksplit_len"] if split > 1 else d["k"]) // 32)
+            tiles = pr.tiles_n * -(-d["m"] // tm) * split
+            width = pr.tile_n / 256  # MMA and operand time scale with the tile's columns
+            costs += [(kb * (0.5 + 0.5 * width) + 3, pr.tile_base + i) for i in range(tiles)]
         costs.sort(key=lambda c: (-c[0], c[1]))
         import heapq
 
@@ -552,16 +596,26 @@ class DeviceHybrid:
             groups[prec].append((s, d))
         out = []
         for prec, rows in groups.items():
-            if not rows:
-                continue
+            if rows:
+                out += self._emit_gemm(op, prec, rows, label)
+        return out
+
+    def _emit_gemm(self, op, prec, rows, label):
+        """One grouped-GEMM launch over rows = [(slot, problem dict)] (dense layers or lowered convs)."""
+        out = []
+        if True:
             tm, tn = N.tile_shape(op, prec)
             # heaviest problems first: their tiles start in the first wave (LPT over SMs)
             rows = sorted(rows, key=lambda r: -(r[1]["m"] * r[1]["n"] * r[1]["k"]))
             probs, base = [], 0
             for s, d in rows:
-                tiles_m, tiles_n = -(-d["m"] // tm), -(-d["n"] // tn)
+                tn_p = tn
+                if prec == N.PREC_3XTF32_PAIR:  # narrowest pair tile that covers n (64 / 128 / 256)
+                    tn_p = 64 if d["n"] <= 64 else (128 if d["n"] <= 128 else 256)
+                    d = dict(d, tile_n=tn_p)
+                tiles_m, tiles_n = -(-d["m"] // tm), -(-d["n"] // tn_p)
                 probs.append(N.GemmProblem(tile_base=base, tiles_n=tiles_n, model=s.index, **d))
-                base += tiles_m * tiles_n
+                base += tiles_m * tiles_n * (d.get("ksplit", 1) if op == N.HNN_WGRAD else 1)
             keep = None
             if prec in (N.PREC_3XTF32, N.PREC_3XTF32_PAIR):
                 torch = _torch()
@@ -575,7 +629,7 @@ class DeviceHybrid:
                     pr.tmap_c = _ptr(keep) + 384 * i + 256
             extra = b""
             if prec == N.PREC_3XTF32_PAIR:
-                extra = self._pair_schedule(probs, rows, base, tm, tn)
+                extra = self._pair_schedule(probs, rows, base, tm)
             t = _dev_table(N.GemmProblem, probs, self.device, extra)
             flops = sum(2 * d["m"] * d["n"] * d["k"] for _, d in rows)
             # bytes: A + B read once, C written once (fp32); a fused optimizer adds its p/m/v traffic
@@ -593,10 +647,151 @@ class DeviceHybrid:
 
     def _conv_launch(self, op, items, label):
         out = []
+        tc = [(s, st) for s, st in items if getattr(st, "tc", False)]
+        if tc:
+            out += self._conv_tc_launches(op, tc, label)
         for direct in (False, True):
-            group = [(s, st) for s, st in items if getattr(st, "direct", False) == direct]
+            group = [(s, st) for s, st in items if getattr(st, "direct", False) == direct
+                     and not getattr(st, "tc", False)]
             if group:
                 out += self._conv_group(op, group, label + ("/direct" if direct else ""), direct)
+        return out
+
+    def _convtc_aux(self, aux, items, label, blocks_of, nbytes=0):
+        probs, base = [], 0
+        for s, st in items:
+            c, h, w = st.in_shape
+            f, oh, ow = self._conv_out(st)
+            k = st.attrs["kernel"]
+            W = self.pview(self.grads, s.index, st.params[0])
+            B = self.pview(self.grads, s.index, st.params[1])
+            nb = blocks_of(s, st)
+            probs.append(N.ConvTcProblem(
+                x=_ptr(st.x), cols=_ptr(st.cols), dy=_ptr(st.dy), dyt=_ptr(st.dyt),
+                dcols=_ptr(s.dcols) if s.dcols is not None else 0, dx=_ptr(st.dx),
+                mask=_ptr(st.x) if st.mask_input else 0, partial=_ptr(st.partial), dw=_ptr(W), db=_ptr(B),
+                bpart=_ptr(st.bpart), weight=_ptr(self.pview(self.params, s.index, st.params[0])),
+                wpad=_ptr(st.wpad), cap=s.batch_size, c=c, h=h, w=w, f=f, k=k,
+                stride=st.attrs.get("stride", 1), pad=st.attrs.get("padding", 0), oh=oh, ow=ow, kk=c * k * k,
+                kkp=st.kkp,
+                ksplit=st.ksplit, ksplit_len=st.ksplit_len, model=s.index, block_base=base, blocks=nb))
+            base += nb
+        t = _dev_table(N.ConvTcProblem, probs, self.device)
+        max_k = max(st.attrs["kernel"] for _, st in items)
+        return Launch("hnn_conv_tc_aux", (aux, _ptr(t), len(probs), base, max_k, _ptr(self.cur), _ptr(self.status)),
+                      t, label, nbytes=nbytes)
+
+    def _conv_dgrad_as_fwd(self, items, label, grid):
+        """Stride-1 conv input gradient = conv(dy, flipped weights, pad k-1-p): flip the weights,
+        im2col dy into the model's scratch, one forward-type CTA-pair GEMM writing NCHW dx with the
+        relu mask of x (no dcols round trip through col2im)."""
+        out, flips, cols = [], [], []
+        for s, st in items:
+            c, h, w = st.in_shape
+            f, oh, ow = self._conv_out(st)
+            k = st.attrs["kernel"]
+            p = st.attrs.get("padding", 0)
+            W = self.pview(self.params, s.index, st.params[0])
+            kf = f * k * k
+            flips.append((s, N.ConvTcProblem(weight=_ptr(W), wpad=_ptr(st.wflip), c=c, f=f, k=k,
+                                             model=s.index)))
+            # im2col over dy: channels F, spatial OH x OW -> H x W, padding k-1-p
+            cols.append((s, N.ConvTcProblem(x=_ptr(st.dy), cols=_ptr(s.dcols), cap=s.batch_size, c=f, h=oh, w=ow,
+                                            f=c, k=k, stride=1, pad=k - 1 - p, oh=h, ow=w, kk=kf, kkp=kf,
+                                            model=s.index)))
+        out.append(self._aux_table(N.CONVTC_FLIP_WEIGHTS, flips, f"{label}/tc/flipw",
+                                   lambda pr: grid(pr.c * pr.f * pr.k * pr.k), 3))
+        out.append(self._aux_table(N.CONVTC_IM2COL, cols, f"{label}/tc/im2col_dy",
+                                   lambda pr: -(-(pr.cap * pr.oh * pr.ow) // 32) * -(-pr.c // 32), 3))
+        rows = []
+        for s, st in items:
+            c, h, w = st.in_shape
+            f, oh, ow = self._conv_out(st)
+            kf = f * st.attrs["kernel"] ** 2
+            rows.append((s, dict(a=_ptr(s.dcols), b=_ptr(st.wflip), c=_ptr(st.dx), bias=0,
+                                 mask=_ptr(st.x) if st.mask_input else 0, dbias=0, m=s.batch_size * h * w, n=c,
+                                 k=kf, lda=kf, ldb=kf, ldc=c, relu=0, row_mult=h * w, c_mode=1)))
+        out += self._emit_gemm(N.HNN_FWD, N.PREC_3XTF32_PAIR, rows, f"{label}/tc/dgfwd")
+        return out
+
+    def _aux_table(self, aux, probs_by_slot, label, blocks_of, max_k):
+        probs, base = [], 0
+        for s, pr in probs_by_slot:
+            nb = blocks_of(pr)
+            pr.block_base, pr.blocks = base, nb
+            probs.append(pr)
+            base += nb
+        t = _dev_table(N.ConvTcProblem, probs, self.device)
+        return Launch("hnn_conv_tc_aux", (aux, _ptr(t), len(probs), base, max_k, _ptr(self.cur), _ptr(self.status)),
+                      t, label)
+
+    def _conv_tc_launches(self, op, items, label):
+        """Tensor-core conv layers of one wave: im2col / transpose / col2im / split reduce around
+        CTA-pair 3xTF32 GEMMs (csrc/conv_tc.cu, csrc/gemm_tc2.cu)."""
+        def geo(st):  # GEMM K = C*k*k padded to kkp
+            c, h, w = st.in_shape
+            f, oh, ow = self._conv_out(st)
+            return c, h, w, f, oh, ow, st.kkp
+
+        def weight(s, st):  # GEMM B operand rows [f, kkp]: the weights, or their padded copy
+            return _ptr(st.wpad) if st.wpad is not None else _ptr(self.pview(self.params, s.index, st.params[0]))
+
+        def grid(total):
+            return max(1, min(-(-total // 256), 4 * 148))
+
+        out = []
+        if op == N.HNN_FWD:
+            padded = [(s, st) for s, st in items if st.wpad is not None]
+            if padded:
+                out.append(self._convtc_aux(N.CONVTC_PAD_WEIGHTS, padded, f"{label}/tc/padw",
+                                            lambda s, st: grid(geo(st)[3] * geo(st)[6])))
+            out.append(self._convtc_aux(
+                N.CONVTC_IM2COL, items, f"{label}/tc/im2col",
+                lambda s, st: -(-(s.batch_size * geo(st)[4] * geo(st)[5]) // 32) * -(-geo(st)[0] // 32),
+                nbytes=sum(8 * s.batch_size * geo(st)[4] * geo(st)[5] * geo(st)[6] for s, st in items)))
+            rows = []
+            for s, st in items:
+                c, h, w, f, oh, ow, kk = geo(st)
+                B = self.pview(self.params, s.index, st.params[1])
+                rows.append((s, dict(a=_ptr(st.cols), b=weight(s, st), c=_ptr(st.y), bias=_ptr(B), mask=0, dbias=0,
+                                     m=s.batch_size * oh * ow, n=f, k=kk, lda=kk, ldb=kk, ldc=f, relu=int(st.relu),
+                                     row_mult=oh * ow, c_mode=1)))
+            out += self._emit_gemm(N.HNN_FWD, N.PREC_3XTF32_PAIR, rows, f"{label}/tc")
+            return out
+        tiles_t = lambda s, st: (s.batch_size * -(-(geo(st)[4] * geo(st)[5]) // 32) * -(-geo(st)[3] // 32))
+        if op == N.HNN_DGRAD:
+            # (only stages whose input gradient is needed reach here)
+            fw = [(s, st) for s, st in items if st.dg_fwd]
+            if fw:
+                out += self._conv_dgrad_as_fwd(fw, label, grid)
+            items = [(s, st) for s, st in items if not st.dg_fwd]
+            if not items:
+                return out
+            out.append(self._convtc_aux(N.CONVTC_TRANSPOSE_DY, items, f"{label}/tc/transpose", tiles_t))
+            rows = []
+            for s, st in items:
+                c, h, w, f, oh, ow, kk = geo(st)
+                rows.append((s, dict(a=_ptr(st.dyt), b=weight(s, st), c=_ptr(s.dcols), bias=0, mask=0, dbias=0,
+                                     m=s.batch_size * oh * ow, n=kk, k=f, lda=f, ldb=kk, ldc=kk, relu=0,
+                                     row_mult=oh * ow)))
+            out += self._emit_gemm(N.HNN_DGRAD, N.PREC_3XTF32_PAIR, rows, f"{label}/tc")
+            out.append(self._convtc_aux(N.CONVTC_COL2IM, items, f"{label}/tc/col2im",
+                                        lambda s, st: (s.batch_size * geo(st)[1] * -(-geo(st)[2] // 32)
+                                                       * -(-geo(st)[0] // 16))))
+            return out
+        # WGRAD (the transpose already ran in this wave's DGRAD phase when the stage needs dx)
+        fresh = [(s, st) for s, st in items if not (st.needs_dx and not st.dg_fwd)]
+        if fresh:
+            out.append(self._convtc_aux(N.CONVTC_TRANSPOSE_DY, fresh, f"{label}/tc/transpose", tiles_t))
+        rows = []
+        for s, st in items:
+            c, h, w, f, oh, ow, kk = geo(st)
+            rows.append((s, dict(a=_ptr(st.dyt), b=_ptr(st.cols), c=_ptr(st.partial), bias=0, mask=0, dbias=0,
+                                 m=f, n=kk, k=s.batch_size * oh * ow, lda=f, ldb=kk, ldc=kk, relu=0,
+                                 row_mult=oh * ow, ksplit=st.ksplit, ksplit_len=st.ksplit_len)))
+        out += self._emit_gemm(N.HNN_WGRAD, N.PREC_3XTF32_PAIR, rows, f"{label}/tc")
+        out.append(self._convtc_aux(N.CONVTC_WGRAD_REDUCE, items, f"{label}/tc/reduce",
+                                    lambda s, st: grid(geo(st)[3] * geo(st)[6] + geo(st)[3])))
         return out
 
     def _conv_group(self, op, items, label, direct):

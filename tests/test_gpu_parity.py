@@ -542,7 +542,7 @@ def test_exact_div_sqrt_match_numpy(pkg):
     assert not bad_r.any(), (A[bad_r][:5], gr[bad_r][:5], rr[bad_r][:5], int(bad_r.sum()))
 
 
-@pytest.mark.parametrize("hidden,batch", [((384, 320), 200), ((640, 136), 256)])
+@pytest.mark.parametrize("hidden,batch", [((384, 320), 200), ((640, 136), 256), ((64, 100), 256)])
 def test_pair_tensor_core_gemms_match_oracle(pkg, hidden, batch):
     """CTA-pair (cta_group::2, 256x256 tiles) 3xTF32 GEMMs on every op: first-step gradients vs the
     numpy oracle (rel <= 1e-5) and vs the FFMA path, incl. a ragged 200-row batch (tile rows beyond
@@ -574,3 +574,39 @@ def test_pair_tensor_core_gemms_match_oracle(pkg, hidden, batch):
     for pid, g in ref.items():
         assert rel(got[pid], g) <= 1e-5, (pid, rel(got[pid], g))
         assert rel(got[pid], ref_simt[pid]) <= 1e-5, (pid, rel(got[pid], ref_simt[pid]))
+
+
+@pytest.mark.parametrize("batch", [24, 32])
+def test_tensor_core_conv_layers_match_oracle(pkg, batch):
+    """Conv layers with C*k*k, F >= 64 run as im2col + CTA-pair 3xTF32 GEMMs (NCHW epilogue, K-split
+    weight gradient, col2im input gradient), incl. a stride-2 layer, a ragged batch (24 of a 32-row
+    capacity in the second step) and a relu-masked input gradient: first-step gradients vs the numpy
+    oracle (rel <= 1e-5)."""
+    from paper_2408_01331_b200 import store, zoo
+
+    spec = [("conv0", "conv2d", {"filters": 64, "kernel": 3, "padding": 1}), ("act0", "relu", {}),
+            ("conv1", "conv2d", {"filters": 64, "kernel": 3, "padding": 1}), ("act1", "relu", {}),
+            ("pool1", "maxpool2d", {"kernel": 2}),
+            ("conv2", "conv2d", {"filters": 128, "kernel": 3, "padding": 1, "stride": 2}), ("act2", "relu", {}),
+            ("pool2", "maxpool2d", {"kernel": 4}),
+            ("flat", "flatten", {}), ("fc", "dense", {"units": 10})]
+    graph = zoo._seq("tc-conv", (3, 16, 16), spec)
+    splits = oracle.image_splits("tcconv", "mini", 10, (3, 16, 16), 56, 8)
+    ds = store.from_splits(splits)
+    job = pkg.TrainingJob("v", graph, ds.content_hash, pkg.HyperParams(1, batch, 0.01, "sgd", (), 4), 0, 0)
+    h = pkg.merge([job])
+    grabbed = []
+    tr = pkg.Trainer(h, pkg.make_plan("fcfs", [job]), [job], {"v": ds}, keep_grads=True, fuse_optimizer=False)
+    tr.step_observer = lambda j, p: grabbed.append(tr.device.download_grads(0))
+    tr.run()
+    labels = [l.label for l in tr.device.train_plan]
+    assert sum("/conv/tc" in l for l in labels) >= 6, labels
+    params = oracle.init_model(graph, 4)
+    batches = oracle.epoch_batches(splits["train_x"], splits["train_y"], ds.content_hash, batch, 4, 0)
+    bx, by, _ = batches[0]
+    logits, tape = oracle.model_forward(graph, params, bx)
+    _, dl = oracle.sce_loss_and_grad(logits, by)
+    ref = oracle.model_backward(tape, dl)
+    for pid, g in ref.items():
+        assert rel(grabbed[0][pid], g) <= 1e-5, (pid, rel(grabbed[0][pid], g))
+    assert len(grabbed) == len(batches)
