@@ -186,7 +186,8 @@ def build_rank(workload, rank, world, device):
     per = MODELS_PER_GPU[workload]
     jobs = zoo.config_jobs(workload, meta, first_model=per * rank, count=per)
     hy = merge(jobs)
-    dev = hy.materialize(device)
+    # C4 is specified on bf16 tensor cores (BASELINE.json configs[3]); the other configs are fp32
+    dev = hy.materialize(device, conv_precision="bf16" if workload == "c4" else "f32")
     dev.bind_datasets([ddev] * dev.n, ddev.n_train)
     dev.build_plans()
     return jobs, hy, dev, ddev, meta, ds, comm
@@ -333,7 +334,9 @@ def gpu_arm(args):
     line = {
         "metric": METRIC, "value": round(value, 1), "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": round(ms / args.steps, 4), "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic (keyed-Philox blob/image "
+        "scaling": "weak", "vs_baseline": None,
+        "dtype": "bf16 conv operands, f32 accumulate / dense / optimizer" if args.workload == "c4" else "f32",
+        "data": "synthetic (keyed-Philox blob/image "
         "generators of the reference), random-init weights from the reference's keyed init",
         "config": {"workload": WORKLOADS[args.workload], "models_per_gpu": n_models,
                    "global_batch": int(samples_per_step * world), "parallelism": f"model-identity sharding x{world}",

@@ -63,6 +63,9 @@ extern "C" {
                                       followed by a tile schedule: int32 npairs, offsets[npairs + 1], tile
                                       ids[total_tiles]; when npairs != min(total_tiles, SMs/2) (or npairs is
                                       0) the pairs take tiles round-robin instead */
+#define HNN_PREC_BF16_PAIR 4 /* CTA-pair tcgen05 kind::f16: a / b point to bf16 data, BOTH K-major for every op
+                                (A [m, k], B [n, k], lda / ldb in elements; maps from hnn_gemm_bf16_encode),
+                                fp32 accumulation, promotion and outputs as HNN_PREC_F32_3XTF32_PAIR */
 #define HNN_PREC_F32_SIMT_SKINNY 2 /* fp32 FFMA streaming kernels for one dimension <= 16 (logits layers):
                                       FWD n <= 16, DGRAD k <= 16, WGRAD m <= 16; rows/columns multiple of 4 */
 
@@ -183,6 +186,7 @@ int hnn_grouped_gemm(int op, int prec, const hnn_gemm_problem* probs, int nprob,
  * Tiles are 128 x 128 (hnn_gemm_tile_shape); WGRAD problems need m <= 4096.
  */
 int hnn_gemm_tc_encode(int op, const hnn_gemm_problem* host_probs, int nprob, void* host_maps);
+int hnn_gemm_bf16_encode(int op, const hnn_gemm_problem* host_probs, int nprob, void* host_maps);
 
 /*
  * Implicit-GEMM convolution on NCHW, zero padding `pad`, square kernel k.
@@ -320,6 +324,7 @@ int hnn_multi_tensor_adam(const hnn_opt_segment* segs, int nseg, int total_chunk
 #define HNN_CONVTC_COL2IM 2
 #define HNN_CONVTC_WGRAD_REDUCE 3
 #define HNN_CONVTC_PAD_WEIGHTS 4  /* wpad[f, kk'] = w[f, kk] (kk' < kkp, zero pad): when C*k*k % 4 != 0 */
+#define HNN_CONVTC_WT_WEIGHTS 6   /* bf16 wpad[kk, f] = w[f, kk] */
 #define HNN_CONVTC_FLIP_WEIGHTS 5 /* wpad[c, (f, r, s)] = w[f, c, k-1-r, k-1-s]: stride-1 input gradient as a
                                      forward conv of dy (im2col of dy with pad k-1-pad, then a GEMM) */
 
@@ -341,6 +346,13 @@ typedef struct hnn_convtc_problem {
   int32_t kkp;       /* cols / partial / wpad row length: kk rounded up to a multiple of 4 */
   int32_t ksplit, ksplit_len;
   int32_t model, block_base, blocks;
+  /* bf16 mode (HNN_PREC_BF16_PAIR GEMMs): cols, dyt, wpad hold bf16; im2col also writes colst
+   * [kkp, pix_ld] and the transpose dyk [f, pix_ld] (pixel-contiguous K-major weight-gradient
+   * operands); HNN_CONVTC_WT_WEIGHTS writes wpad = w^T [kkp, f] (stride-2 dcols GEMM operand). */
+  void* colst;
+  void* dyk;
+  int32_t bf16;
+  int32_t pix_ld;
 } hnn_convtc_problem;
 
 int hnn_conv_tc_aux(int op, const hnn_convtc_problem* probs, int nprob, int total_blocks, int max_k,

@@ -14,9 +14,9 @@ from .errors import DeviceError
 LIB_PATH = Path(__file__).resolve().parent / "_lib" / "libhnn_b200.so"
 
 HNN_FWD, HNN_DGRAD, HNN_WGRAD = 0, 1, 2
-PREC_SIMT, PREC_3XTF32, PREC_SIMT_SKINNY, PREC_3XTF32_PAIR = 0, 1, 2, 3
+PREC_SIMT, PREC_3XTF32, PREC_SIMT_SKINNY, PREC_3XTF32_PAIR, PREC_BF16_PAIR = 0, 1, 2, 3, 4
 CONVTC_IM2COL, CONVTC_TRANSPOSE_DY, CONVTC_COL2IM, CONVTC_WGRAD_REDUCE, CONVTC_PAD_WEIGHTS = 0, 1, 2, 3, 4
-CONVTC_FLIP_WEIGHTS = 5
+CONVTC_FLIP_WEIGHTS, CONVTC_WT_WEIGHTS = 5, 6
 OPT_SGD, OPT_SGD_MOMENTUM, OPT_ADAM = 0, 1, 2
 CONV_DIRECT_BCHUNK = 4
 
@@ -67,7 +67,8 @@ class ConvTcProblem(C.Structure):
                 ("partial", P), ("dw", P), ("db", P), ("bpart", P), ("weight", P), ("wpad", P),
                 ("cap", I), ("c", I), ("h", I), ("w", I), ("f", I), ("k", I), ("stride", I), ("pad", I),
                 ("oh", I), ("ow", I), ("kk", I), ("kkp", I), ("ksplit", I), ("ksplit_len", I),
-                ("model", I), ("block_base", I), ("blocks", I)]
+                ("model", I), ("block_base", I), ("blocks", I), ("colst", P), ("dyk", P), ("bf16", I),
+                ("pix_ld", I)]
 
 
 class PoolProblem(C.Structure):
@@ -104,6 +105,7 @@ SIGNATURES = {
     "hnn_gemm_tile_shape": [C.c_int, C.c_int, C.POINTER(I), C.POINTER(I)],
     "hnn_grouped_gemm": [C.c_int, C.c_int, P, C.c_int, C.c_int, P, P, VP],
     "hnn_gemm_tc_encode": [C.c_int, C.c_void_p, C.c_int, C.c_void_p],
+    "hnn_gemm_bf16_encode": [C.c_int, C.c_void_p, C.c_int, C.c_void_p],
     "hnn_conv_tile_shape": [C.c_int, C.POINTER(I), C.POINTER(I)],
     "hnn_grouped_conv": [C.c_int, P, C.c_int, C.c_int, P, P, VP],
     "hnn_conv_wgrad_reduce": [P, C.c_int, C.c_int, P, P, VP],

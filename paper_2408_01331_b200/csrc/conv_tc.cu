@@ -10,6 +10,8 @@
 //   WGRAD  partial[s] = dyT^T x cols          GEMM, fixed K splits over output pixels
 //          dW = sum_s partial[s] (in order); db = sum_b sum_hw dy (in order)
 // Every kernel is a fixed function of the problem's shape (bit-exact isolation, no atomics).
+#include <cuda_bf16.h>
+
 #include "common.cuh"
 
 namespace hnn {
@@ -59,6 +61,25 @@ __global__ void __launch_bounds__(CT_THREADS) im2col_kernel(const hnn_convtc_pro
   }
   __syncthreads();
   const int width = min(seg, (p.c - c0) * kk2);
+  if (p.bf16) {
+    __nv_bfloat16* cb16 = reinterpret_cast<__nv_bfloat16*>(p.cols);
+    for (int pi = warp; pi < IC_PIX; pi += CT_THREADS / 32) {
+      const int mm = m0 + pi;
+      if (mm >= p.cap * ohw) break;
+      __nv_bfloat16* dst = cb16 + size_t(mm) * p.kkp + c0 * kk2;
+      for (int j = lane; j < width; j += 32) dst[j] = __float2bfloat16_rn(ic_tile[pi * ld + j]);
+      if (cb == 0)
+        for (int j = p.kk + lane; j < p.kkp; j += 32) cb16[size_t(mm) * p.kkp + j] = __float2bfloat16_rn(0.0f);
+    }
+    if (p.colst) {  // pixel-contiguous copy [kkp, pix_ld] for the weight-gradient GEMM
+      __nv_bfloat16* ct = reinterpret_cast<__nv_bfloat16*>(p.colst);
+      const int mm = m0 + lane;
+      if (mm < p.cap * ohw)
+        for (int j = warp; j < width; j += CT_THREADS / 32)
+          ct[size_t(c0 * kk2 + j) * p.pix_ld + mm] = __float2bfloat16_rn(ic_tile[lane * ld + j]);
+    }
+    return;
+  }
   for (int pi = warp; pi < IC_PIX; pi += CT_THREADS / 32) {
     const int mm = m0 + pi;
     if (mm >= p.cap * ohw) break;
@@ -90,12 +111,20 @@ __global__ void __launch_bounds__(CT_THREADS) transpose_dy_kernel(const hnn_conv
   for (int j = ty; j < 32; j += 8) {
     const int f = tf * 32 + j, hw = th * 32 + tx;
     tile[j][tx] = (f < p.f && hw < hw_n) ? __ldg(p.dy + (size_t(b) * p.f + f) * hw_n + hw) : 0.0f;
+    if (p.bf16 && p.dyk && f < p.f && hw < hw_n)  // dyk[f, b*HW + hw]: filter-major, pixel-contiguous
+      reinterpret_cast<__nv_bfloat16*>(p.dyk)[size_t(f) * p.pix_ld + size_t(b) * hw_n + hw] =
+          __float2bfloat16_rn(tile[j][tx]);
   }
   __syncthreads();
-  for (int j = ty; j < 32; j += 8) {
-    const int hw = th * 32 + j, f = tf * 32 + tx;
-    if (hw < hw_n && f < p.f) p.dyt[(size_t(b) * hw_n + hw) * p.f + f] = tile[tx][j];
-  }
+  if (p.dyt)
+    for (int j = ty; j < 32; j += 8) {
+      const int hw = th * 32 + j, f = tf * 32 + tx;
+      if (hw < hw_n && f < p.f) {
+        const size_t o = (size_t(b) * hw_n + hw) * p.f + f;
+        if (p.bf16) reinterpret_cast<__nv_bfloat16*>(p.dyt)[o] = __float2bfloat16_rn(tile[tx][j]);
+        else p.dyt[o] = tile[tx][j];
+      }
+    }
   if (th == 0 && ty == 0) {  // one warp per (b, 32 filters): sequential sum over hw
     const int f = tf * 32 + tx;
     if (f < p.f) {
@@ -270,7 +299,9 @@ __global__ void __launch_bounds__(CT_THREADS) pad_weights_kernel(const hnn_convt
   for (long long e = (long long)(blockIdx.x - p.block_base) * CT_THREADS + threadIdx.x; e < total;
        e += (long long)p.blocks * CT_THREADS) {
     const long long f = e / p.kkp, j = e - f * p.kkp;
-    p.wpad[e] = j < p.kk ? __ldg(p.weight + f * p.kk + j) : 0.0f;
+    const float v = j < p.kk ? __ldg(p.weight + f * p.kk + j) : 0.0f;
+    if (p.bf16) reinterpret_cast<__nv_bfloat16*>(p.wpad)[e] = __float2bfloat16_rn(v);
+    else p.wpad[e] = v;
   }
 }
 
@@ -287,7 +318,24 @@ __global__ void __launch_bounds__(CT_THREADS) flip_weights_kernel(const hnn_conv
        e += (long long)p.blocks * CT_THREADS) {
     const int c = int(e / row), j = int(e - (long long)c * row);
     const int f = j / kk2, rs = j - f * kk2, r = rs / p.k, s = rs - r * p.k;
-    p.wpad[e] = __ldg(p.weight + ((size_t(f) * p.c + c) * p.k + (p.k - 1 - r)) * p.k + (p.k - 1 - s));
+    const float v = __ldg(p.weight + ((size_t(f) * p.c + c) * p.k + (p.k - 1 - r)) * p.k + (p.k - 1 - s));
+    if (p.bf16) reinterpret_cast<__nv_bfloat16*>(p.wpad)[e] = __float2bfloat16_rn(v);
+    else p.wpad[e] = v;
+  }
+}
+
+// bf16 wpad[kk, f] = w[f, kk] (kk < kkp; pad rows zero): the stride-2 dcols GEMM's K-major B.
+__global__ void __launch_bounds__(CT_THREADS) wt_weights_kernel(const hnn_convtc_problem* __restrict__ probs, int nprob,
+                                                               const hnn_step_row* __restrict__ cur,
+                                                               const hnn_model_status* __restrict__ status) {
+  const hnn_convtc_problem& p = ct_problem(probs, nprob, blockIdx.x);
+  if (!live(cur, status, p.model)) return;
+  const long long total = (long long)p.kkp * p.f;
+  for (long long e = (long long)(blockIdx.x - p.block_base) * CT_THREADS + threadIdx.x; e < total;
+       e += (long long)p.blocks * CT_THREADS) {
+    const long long j = e / p.f, f = e - j * p.f;
+    const float v = j < p.kk ? __ldg(p.weight + f * p.kk + j) : 0.0f;
+    reinterpret_cast<__nv_bfloat16*>(p.wpad)[e] = __float2bfloat16_rn(v);
   }
 }
 
@@ -316,6 +364,9 @@ extern "C" int hnn_conv_tc_aux(int op, const hnn_convtc_problem* probs, int npro
       break;
     case HNN_CONVTC_FLIP_WEIGHTS:
       hnn::flip_weights_kernel<<<total_blocks, hnn::CT_THREADS, 0, s>>>(probs, nprob, cur, status);
+      break;
+    case HNN_CONVTC_WT_WEIGHTS:
+      hnn::wt_weights_kernel<<<total_blocks, hnn::CT_THREADS, 0, s>>>(probs, nprob, cur, status);
       break;
     case HNN_CONVTC_WGRAD_REDUCE:
       hnn::wgrad_reduce_kernel<<<total_blocks, hnn::CT_THREADS, 0, s>>>(probs, nprob, cur, status);

@@ -230,6 +230,8 @@ int gemm_tc_tile_shape(int op, int32_t* tm, int32_t* tn);
 int grouped_gemm_tc2(int op, const hnn_gemm_problem* probs, int nprob, int total_tiles, const hnn_step_row* cur,
                      const hnn_model_status* status, cudaStream_t s);
 int gemm_tc2_tile_shape(int op, int32_t* tm, int32_t* tn);
+int grouped_gemm_bf16(int op, const hnn_gemm_problem* probs, int nprob, int total_tiles, const hnn_step_row* cur,
+                      const hnn_model_status* status, cudaStream_t s);
 
 }  // namespace hnn
 
@@ -242,7 +244,7 @@ extern "C" int hnn_gemm_tile_shape(int op, int prec, int32_t* tile_m, int32_t* t
   }
   if (prec == HNN_PREC_F32_SIMT_SKINNY) return hnn::skinny_tile_shape(op, tile_m, tile_n);
   if (prec == HNN_PREC_F32_3XTF32) return hnn::gemm_tc_tile_shape(op, tile_m, tile_n);
-  if (prec == HNN_PREC_F32_3XTF32_PAIR) return hnn::gemm_tc2_tile_shape(op, tile_m, tile_n);
+  if (prec == HNN_PREC_F32_3XTF32_PAIR || prec == HNN_PREC_BF16_PAIR) return hnn::gemm_tc2_tile_shape(op, tile_m, tile_n);
   hnn::set_error("hnn_gemm_tile_shape", "unknown precision");
   return HNN_ERR_INVALID;
 }
@@ -256,6 +258,7 @@ extern "C" int hnn_grouped_gemm(int op, int prec, const hnn_gemm_problem* probs,
     return hnn::grouped_gemm_simt(op, prec == HNN_PREC_F32_SIMT_SKINNY, probs, nprob, total_tiles, cur, status, s);
   if (prec == HNN_PREC_F32_3XTF32) return hnn::grouped_gemm_tc(op, probs, nprob, total_tiles, cur, status, s);
   if (prec == HNN_PREC_F32_3XTF32_PAIR) return hnn::grouped_gemm_tc2(op, probs, nprob, total_tiles, cur, status, s);
+  if (prec == HNN_PREC_BF16_PAIR) return hnn::grouped_gemm_bf16(op, probs, nprob, total_tiles, cur, status, s);
   hnn::set_error("hnn_grouped_gemm", "unknown precision");
   return HNN_ERR_INVALID;
 }

@@ -392,6 +392,22 @@ int encode_2d(CUtensorMap* map, const float* ptr, uint64_t inner, uint64_t outer
   return r == CUDA_SUCCESS ? HNN_OK : HNN_ERR_CUDA;
 }
 
+// 2D bf16 map, K-major operand: inner extent `inner` (contiguous K), `outer` rows, box {64, box_outer}
+// (64 bf16 = one 128-byte swizzled row).
+int encode_2d_bf16(CUtensorMap* map, const void* ptr, uint64_t inner, uint64_t outer, uint64_t stride_elems,
+                   uint32_t box_outer) {
+  EncodeTiled enc = encoder();
+  if (!enc) return HNN_ERR_CUDA;
+  cuuint64_t dims[2] = {inner, outer};
+  cuuint64_t strides[1] = {stride_elems * 2};
+  cuuint32_t box[2] = {64, box_outer};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(ptr), dims, strides, box, estr,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS ? HNN_OK : HNN_ERR_CUDA;
+}
+
 int gemm_tc_tile_shape(int op, int32_t* tm, int32_t* tn) {
   *tm = TC_BM;
   *tn = TC_BN;
@@ -469,6 +485,25 @@ extern "C" int hnn_gemm_tc_encode(int op, const hnn_gemm_problem* host_probs, in
     if (!rc && p.c) rc = hnn::encode_2d(&maps[3 * i + 2], p.c, p.n, crows, p.ldc, 32, false);
     if (rc) {
       hnn::set_error("hnn_gemm_tc_encode", "cuTensorMapEncodeTiled failed (alignment / stride / driver)");
+      return rc;
+    }
+  }
+  return HNN_OK;
+}
+
+// HNN_PREC_BF16_PAIR: A [m, k] and B [n, k] are K-major bf16 (lda / ldb in elements); C fp32 as above.
+extern "C" int hnn_gemm_bf16_encode(int op, const hnn_gemm_problem* host_probs, int nprob, void* host_maps) {
+  HNN_REQUIRE(host_probs && host_maps && nprob > 0, "hnn_gemm_bf16_encode", "bad arguments");
+  CUtensorMap* maps = reinterpret_cast<CUtensorMap*>(host_maps);
+  for (int i = 0; i < nprob; ++i) {
+    const hnn_gemm_problem& p = host_probs[i];
+    const uint32_t brows = p.tile_n > 0 ? uint32_t(p.tile_n / 2) : 128u;
+    int rc = hnn::encode_2d_bf16(&maps[3 * i], p.a, p.k, p.m, p.lda, hnn::TC_BM);
+    if (!rc) rc = hnn::encode_2d_bf16(&maps[3 * i + 1], p.b, p.k, p.n, p.ldb, brows);
+    const uint64_t crows = uint64_t(p.m) * uint64_t(op == HNN_WGRAD && p.ksplit > 1 ? p.ksplit : 1);
+    if (!rc && p.c) rc = hnn::encode_2d(&maps[3 * i + 2], p.c, p.n, crows, p.ldc, 32, false);
+    if (rc) {
+      hnn::set_error("hnn_gemm_bf16_encode", "cuTensorMapEncodeTiled failed (alignment / stride / driver)");
       return rc;
     }
   }

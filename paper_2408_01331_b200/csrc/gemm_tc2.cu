@@ -54,12 +54,17 @@ __device__ unsigned long long g_tc2_trace[296 * 16];
 #define TC2_T1(v, slot)
 #endif
 
-template <int OP>
+// KIND: 0 = fp32 operands, 3xTF32 (kind::tf32, converters write lo); 1 = bf16 operands, one
+// kind::f16 MMA per K step (HNN_PREC_BF16_PAIR: every operand K-major, 64-element K blocks; the
+// converter warps only relay "stage landed" to the leader).
+template <int OP, int KIND = 0>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC2_THREADS, 1)
     gemm_tc2_kernel(const hnn_gemm_problem* __restrict__ probs, int nprob, int total_tiles,
                     const hnn_step_row* __restrict__ cur, const hnn_model_status* __restrict__ status) {
-  constexpr int A_MN = (OP == HNN_WGRAD) ? 1 : 0;
-  constexpr int B_MN = (OP == HNN_FWD) ? 0 : 1;
+  constexpr bool BF16 = KIND == 1;
+  constexpr int A_MN = (!BF16 && OP == HNN_WGRAD) ? 1 : 0;
+  constexpr int B_MN = (!BF16 && OP != HNN_FWD) ? 1 : 0;
+  constexpr int KBE = BF16 ? 64 : TC2_BK;  // K elements per 128-byte stage row
   constexpr int SR = TC2_STAGES;
   extern __shared__ uint8_t smem_raw[];
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
@@ -128,7 +133,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC2_THREADS, 1)
     tn = p->tile_n > 0 ? p->tile_n : TC2_BN;  // pair tile columns: 64, 128 or 256
     m0 = (t / p->tiles_n) * (2 * TC2_BM);
     n0 = (t % p->tiles_n) * tn;
-    nkb = ktot > 0 ? (ktot + TC2_BK - 1) / TC2_BK : 0;
+    nkb = ktot > 0 ? (ktot + KBE - 1) / KBE : 0;
     return nkb > 0;
   };
   const int pair = blockIdx.x / 2, npairs = gridDim.x / 2;
@@ -160,7 +165,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC2_THREADS, 1)
           TC2_T1(t3, 3);
           const uint32_t st = raw_base + s * SSTRIDE;
           mbar_expect_tx(bar(RAW_FULL + s), stage_bytes);
-          const int k0 = kofs + kb * TC2_BK;
+          const int k0 = kofs + kb * KBE;
           if (A_MN) {
 #pragma unroll
             for (int b = 0; b < TC2_BM / 32; ++b) tma_load_2d(st + b * 4096, p->tmap_a, bar(RAW_FULL + s), am + 32 * b, k0);
@@ -187,7 +192,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC2_THREADS, 1)
         const hnn_gemm_problem* p;
         int m0, n0, nkb, rows, kofs, sp, tn;
         if (!tile_info(tile, p, m0, n0, nkb, rows, kofs, sp, tn)) continue;
-        const uint32_t idesc = tf32_idesc(2 * TC2_BM, tn, A_MN, B_MN);
+        const uint32_t idesc = BF16 ? bf16_idesc(2 * TC2_BM, tn) : tf32_idesc(2 * TC2_BM, tn, A_MN, B_MN);
         for (int kb = 0; kb < nkb; ++kb, ++kg) {
           const int in_chunk = kb % TC2_CHUNK_KB;
           const uint32_t buf = cg & 1;
@@ -202,14 +207,21 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC2_THREADS, 1)
           mbar_wait(bar(LO_FULL + s), (kg / SR) & 1);  // both CTAs: raw landed, lo written
           TC2_T1(t0, 0);
           tc_fence_after();
+          if (BF16) {
 #pragma unroll
-          for (int j = 0; j < TC2_BK / 8; ++j) {
-            const uint32_t ao = A_MN ? j * 1024 : j * 32, bo = B_MN ? j * 1024 : j * 32;
-            const uint64_t dah = smem_desc(a_hi + ao, alb, asb, alt), dal = smem_desc(a_lo + ao, alb, asb, alt);
-            const uint64_t dbh = smem_desc(b_hi + bo, blb, bsb, blt), dbl = smem_desc(b_lo + bo, blb, bsb, blt);
-            mma_tf32_pair(acc, dah, dbh, idesc, (in_chunk | j) != 0);
-            mma_tf32_pair(acc, dal, dbh, idesc, 1u);
-            mma_tf32_pair(acc, dah, dbl, idesc, 1u);
+            for (int j = 0; j < 4; ++j)  // K step 16 bf16 = +32 B inside the K-major rows
+              mma_f16_pair(acc, smem_desc(a_hi + j * 32, 16, 1024, 2), smem_desc(b_hi + j * 32, 16, 1024, 2), idesc,
+                           (in_chunk | j) != 0);
+          } else {
+#pragma unroll
+            for (int j = 0; j < TC2_BK / 8; ++j) {
+              const uint32_t ao = A_MN ? j * 1024 : j * 32, bo = B_MN ? j * 1024 : j * 32;
+              const uint64_t dah = smem_desc(a_hi + ao, alb, asb, alt), dal = smem_desc(a_lo + ao, alb, asb, alt);
+              const uint64_t dbh = smem_desc(b_hi + bo, blb, bsb, blt), dbl = smem_desc(b_lo + bo, blb, bsb, blt);
+              mma_tf32_pair(acc, dah, dbh, idesc, (in_chunk | j) != 0);
+              mma_tf32_pair(acc, dal, dbh, idesc, 1u);
+              mma_tf32_pair(acc, dah, dbl, idesc, 1u);
+            }
           }
           mma_commit_pair(bar(RAW_EMPTY + s));  // raw and lo of stage s consumed
           TC2_T1(t0, 5);
@@ -237,7 +249,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC2_THREADS, 1)
         mbar_wait(bar(RAW_FULL + s), (kg / SR) & 1);  // (the stage's lo is free: TMA reused it)
         TC2_T1(t2, 2);
         const uint32_t hi = raw_base + s * SSTRIDE, lo = hi + TC2_STAGE;
-        const int n16 = (TC2_A_BYTES + (tn / 2) * TC2_BK * 4) / 16;  // this tile's A + B-half 16-byte chunks
+        const int n16 = BF16 ? 0 : (TC2_A_BYTES + (tn / 2) * TC2_BK * 4) / 16;  // A + B-half 16-byte chunks
 #pragma unroll
         for (int h = 0; h < NPART; ++h) {
           if ((h * PART) * CT >= n16) break;
@@ -436,14 +448,15 @@ int gemm_tc2_tile_shape(int op, int32_t* tm, int32_t* tn) {
 int launch_colsum(const hnn_gemm_problem* probs, int nprob, const hnn_step_row* cur, const hnn_model_status* status,
                   cudaStream_t s);
 
-int grouped_gemm_tc2(int op, const hnn_gemm_problem* probs, int nprob, int total_tiles, const hnn_step_row* cur,
-                     const hnn_model_status* status, cudaStream_t s) {
+template <int KIND>
+int launch_tc2(int op, const hnn_gemm_problem* probs, int nprob, int total_tiles, const hnn_step_row* cur,
+               const hnn_model_status* status, cudaStream_t s) {
   static bool configured[3] = {false, false, false};
   if (!configured[op]) {
     cudaError_t e;
-    if (op == HNN_FWD) e = cudaFuncSetAttribute(gemm_tc2_kernel<HNN_FWD>, cudaFuncAttributeMaxDynamicSharedMemorySize, TC2_SMEM_BYTES);
-    else if (op == HNN_DGRAD) e = cudaFuncSetAttribute(gemm_tc2_kernel<HNN_DGRAD>, cudaFuncAttributeMaxDynamicSharedMemorySize, TC2_SMEM_BYTES);
-    else e = cudaFuncSetAttribute(gemm_tc2_kernel<HNN_WGRAD>, cudaFuncAttributeMaxDynamicSharedMemorySize, TC2_SMEM_BYTES);
+    if (op == HNN_FWD) e = cudaFuncSetAttribute(gemm_tc2_kernel<HNN_FWD, KIND>, cudaFuncAttributeMaxDynamicSharedMemorySize, TC2_SMEM_BYTES);
+    else if (op == HNN_DGRAD) e = cudaFuncSetAttribute(gemm_tc2_kernel<HNN_DGRAD, KIND>, cudaFuncAttributeMaxDynamicSharedMemorySize, TC2_SMEM_BYTES);
+    else e = cudaFuncSetAttribute(gemm_tc2_kernel<HNN_WGRAD, KIND>, cudaFuncAttributeMaxDynamicSharedMemorySize, TC2_SMEM_BYTES);
     if (e != cudaSuccess) {
       set_error("hnn_grouped_gemm(tc2)", cudaGetErrorString(e));
       return HNN_ERR_CUDA;
@@ -459,16 +472,26 @@ int grouped_gemm_tc2(int op, const hnn_gemm_problem* probs, int nprob, int total
   const int pairs = total_tiles < sms / 2 ? total_tiles : sms / 2;
   const int grid = 2 * pairs;
   if (op == HNN_FWD)
-    gemm_tc2_kernel<HNN_FWD><<<grid, TC2_THREADS, TC2_SMEM_BYTES, s>>>(probs, nprob, total_tiles, cur, status);
+    gemm_tc2_kernel<HNN_FWD, KIND><<<grid, TC2_THREADS, TC2_SMEM_BYTES, s>>>(probs, nprob, total_tiles, cur, status);
   else if (op == HNN_DGRAD)
-    gemm_tc2_kernel<HNN_DGRAD><<<grid, TC2_THREADS, TC2_SMEM_BYTES, s>>>(probs, nprob, total_tiles, cur, status);
+    gemm_tc2_kernel<HNN_DGRAD, KIND><<<grid, TC2_THREADS, TC2_SMEM_BYTES, s>>>(probs, nprob, total_tiles, cur, status);
   else {
-    gemm_tc2_kernel<HNN_WGRAD><<<grid, TC2_THREADS, TC2_SMEM_BYTES, s>>>(probs, nprob, total_tiles, cur, status);
+    gemm_tc2_kernel<HNN_WGRAD, KIND><<<grid, TC2_THREADS, TC2_SMEM_BYTES, s>>>(probs, nprob, total_tiles, cur, status);
     int rc = check_launch("hnn_grouped_gemm(tc2)");
     if (rc) return rc;
     return launch_colsum(probs, nprob, cur, status, s);
   }
   return check_launch("hnn_grouped_gemm(tc2)");
+}
+
+int grouped_gemm_tc2(int op, const hnn_gemm_problem* probs, int nprob, int total_tiles, const hnn_step_row* cur,
+                     const hnn_model_status* status, cudaStream_t s) {
+  return launch_tc2<0>(op, probs, nprob, total_tiles, cur, status, s);
+}
+
+int grouped_gemm_bf16(int op, const hnn_gemm_problem* probs, int nprob, int total_tiles, const hnn_step_row* cur,
+                      const hnn_model_status* status, cudaStream_t s) {
+  return launch_tc2<1>(op, probs, nprob, total_tiles, cur, status, s);
 }
 
 }  // namespace hnn

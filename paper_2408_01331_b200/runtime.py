@@ -93,6 +93,11 @@ class Stage:
     wpad = None
     dg_fwd: bool = False
     wflip = None
+    bf16: bool = False
+    pix_ld: int = 0
+    colst = None
+    dyk = None
+    wt = None
 
 
 def lower_graph(graph) -> tuple:
@@ -261,7 +266,7 @@ class DeviceHybrid:
     """Packed device state + launch plans for the models of one rank."""
 
     def __init__(self, slots: list, device=None, use_tensor_cores: bool = True, fuse_optimizer: bool = True,
-                 keep_grads: bool = False):
+                 keep_grads: bool = False, conv_precision: str = "f32"):
         torch = _torch()
         # fuse_optimizer: dense layers apply SGD/Adam in their weight-gradient epilogue (the
         # gradient never round-trips HBM); keep_grads: still store dW/db (tests, diagnostics)
@@ -273,6 +278,11 @@ class DeviceHybrid:
         self.slots = slots
         self.n = len(slots)
         self.use_tc = use_tensor_cores
+        if conv_precision not in ("f32", "bf16"):
+            raise ValueError(f"conv_precision must be 'f32' or 'bf16', not {conv_precision!r}")
+        # tensor-core convolutions: "f32" = 3xTF32 (fp32 parity), "bf16" = kind::f16 with bf16
+        # operands, fp32 accumulation and fp32 master weights (BASELINE C4)
+        self.conv_bf16 = conv_precision == "bf16"
         # CTA-pair tcgen05 GEMM (HNN_TC_PAIR=0: single-CTA kernel)
         self.use_pairs = os.environ.get("HNN_TC_PAIR", "1") != "0"
         off = 0
@@ -331,7 +341,7 @@ class DeviceHybrid:
             s.batch_y = self.label_arena[b:b + cap]
             prev_out, prev_ld = s.batch_x, ld0
             widest = ld0
-            dcols_need = 0
+            dcols_need = dgb_need = 0
             for st in s.stages:
                 st.x, st.ld_in = prev_out, prev_ld
                 feats = int(np.prod(st.out_shape))
@@ -356,26 +366,40 @@ class DeviceHybrid:
                              and f >= 64 and f % 4 == 0 and k <= 3 and st.attrs.get("stride", 1) <= 2)
                     if st.tc:
                         pix = cap * oh * ow
-                        st.kkp = _align4(kk)  # cols / weight rows padded to 16 bytes for TMA
-                        st.wpad = (torch.zeros(f * st.kkp, dtype=torch.float32, device=dev)
-                                   if st.kkp != kk else None)
+                        st.bf16 = self.conv_bf16
+                        # cols / weight rows padded to 16 bytes for TMA (8 bf16 / 4 fp32 elements)
+                        st.kkp = -(-kk // 8) * 8 if st.bf16 else _align4(kk)
+                        wdt = torch.bfloat16 if st.bf16 else torch.float32
+                        st.wpad = (torch.zeros(f * st.kkp, dtype=wdt, device=dev)
+                                   if (st.kkp != kk or st.bf16) else None)
                         kk = st.kkp
+                        kq = 64 if st.bf16 else 32  # K block of the GEMM
                         tiles_mn = -(-f // 256) * -(-kk // 256)
                         split = max(1, min(-(-148 // tiles_mn), -(-pix // 1024)))
-                        st.ksplit_len = -(-(-(-pix // split)) // 32) * 32
+                        st.ksplit_len = -(-(-(-pix // split)) // kq) * kq
                         st.ksplit = -(-pix // st.ksplit_len)
-                        st.cols = torch.zeros(pix * kk, dtype=torch.float32, device=dev)
-                        st.dyt = torch.zeros(pix * f, dtype=torch.float32, device=dev)
+                        st.pix_ld = -(-pix // 8) * 8
+                        st.cols = torch.zeros(pix * kk, dtype=wdt, device=dev)
                         st.bpart = torch.zeros(cap * f, dtype=torch.float32, device=dev)
                         st.partial = torch.zeros(st.ksplit * f * kk, dtype=torch.float32, device=dev)
+                        if st.bf16:  # pixel-contiguous (K-major) weight-gradient operands
+                            st.colst = torch.zeros(kk * st.pix_ld, dtype=wdt, device=dev)
+                            st.dyk = torch.zeros(f * st.pix_ld, dtype=wdt, device=dev)
                         # input gradient: stride 1 -> a forward conv of dy (im2col of dy, flipped
                         # weights; scratch [cap*H*W, F*k*k]); stride 2 -> dcols GEMM + col2im
-                        st.dg_fwd = st.attrs.get("stride", 1) == 1 and (f * k * k) % 4 == 0
+                        st.dg_fwd = st.attrs.get("stride", 1) == 1 and (f * k * k) % 8 == 0
+                        if not st.bf16 or (st.needs_dx and not st.dg_fwd):
+                            st.dyt = torch.zeros(pix * f, dtype=wdt, device=dev)
                         if st.needs_dx and st.dg_fwd:
-                            st.wflip = torch.zeros(c * f * k * k, dtype=torch.float32, device=dev)
-                            dcols_need = max(dcols_need, cap * h * w * f * k * k)
+                            st.wflip = torch.zeros(c * f * k * k, dtype=wdt, device=dev)
+                            if st.bf16:
+                                dgb_need = max(dgb_need, cap * h * w * f * k * k)
+                            else:
+                                dcols_need = max(dcols_need, cap * h * w * f * k * k)
                         elif st.needs_dx:
                             dcols_need = max(dcols_need, pix * kk)
+                            if st.bf16:
+                                st.wt = torch.zeros(kk * f, dtype=wdt, device=dev)
                     else:
                         st.splits = (-(-cap // N.CONV_DIRECT_BCHUNK) if st.direct
                                      else -(-cap * oh * ow // CONV_SPLIT_LEN))
@@ -386,6 +410,7 @@ class DeviceHybrid:
             # one DGRAD column scratch per model: a tensor-core conv's dcols lives only between its
             # DGRAD GEMM and col2im, inside one backward wave
             s.dcols = torch.zeros(max(dcols_need, 4), dtype=torch.float32, device=dev) if dcols_need else None
+            s.dgcols = torch.zeros(dgb_need, dtype=torch.bfloat16, device=dev) if dgb_need else None
             for k, st in enumerate(s.stages):
                 st.dy = s.grads_buf[k % 2][: cap * st.ld_out].view(cap, st.ld_out)
                 st.dx = s.grads_buf[(k + 1) % 2][: cap * st.ld_in].view(cap, st.ld_in)
@@ -610,25 +635,26 @@ class DeviceHybrid:
             probs, base = [], 0
             for s, d in rows:
                 tn_p = tn
-                if prec == N.PREC_3XTF32_PAIR:  # narrowest pair tile that covers n (64 / 128 / 256)
+                if prec in (N.PREC_3XTF32_PAIR, N.PREC_BF16_PAIR):  # narrowest pair tile covering n
                     tn_p = 64 if d["n"] <= 64 else (128 if d["n"] <= 128 else 256)
                     d = dict(d, tile_n=tn_p)
                 tiles_m, tiles_n = -(-d["m"] // tm), -(-d["n"] // tn_p)
                 probs.append(N.GemmProblem(tile_base=base, tiles_n=tiles_n, model=s.index, **d))
                 base += tiles_m * tiles_n * (d.get("ksplit", 1) if op == N.HNN_WGRAD else 1)
             keep = None
-            if prec in (N.PREC_3XTF32, N.PREC_3XTF32_PAIR):
+            if prec in (N.PREC_3XTF32, N.PREC_3XTF32_PAIR, N.PREC_BF16_PAIR):
                 torch = _torch()
                 maps = bytearray(128 * 3 * len(probs))
                 host = (N.GemmProblem * len(probs))(*probs)
-                N.call("hnn_gemm_tc_encode", op, C_addr(host), len(probs), C_addr_bytes(maps))
+                enc = "hnn_gemm_bf16_encode" if prec == N.PREC_BF16_PAIR else "hnn_gemm_tc_encode"
+                N.call(enc, op, C_addr(host), len(probs), C_addr_bytes(maps))
                 keep = torch.frombuffer(maps, dtype=torch.uint8).to(self.device)
                 for i, pr in enumerate(probs):
                     pr.tmap_a = _ptr(keep) + 384 * i
                     pr.tmap_b = _ptr(keep) + 384 * i + 128
                     pr.tmap_c = _ptr(keep) + 384 * i + 256
             extra = b""
-            if prec == N.PREC_3XTF32_PAIR:
+            if prec in (N.PREC_3XTF32_PAIR, N.PREC_BF16_PAIR):
                 extra = self._pair_schedule(probs, rows, base, tm)
             t = _dev_table(N.GemmProblem, probs, self.device, extra)
             flops = sum(2 * d["m"] * d["n"] * d["k"] for _, d in rows)
@@ -639,7 +665,7 @@ class DeviceHybrid:
             nbytes += sum(per_param[d["opt_kind"]] * d["m"] * (d["n"] + 1) for _, d in rows if d.get("opt_w"))
             launch = Launch("hnn_grouped_gemm", (op, prec, _ptr(t), len(probs), base, _ptr(self.cur),
                                                  _ptr(self.status)), t,
-                            f"{label}/{ {N.PREC_SIMT: 'simt', N.PREC_SIMT_SKINNY: 'simt16', N.PREC_3XTF32: 'tc', N.PREC_3XTF32_PAIR: 'tc2'}[prec] }",
+                            f"{label}/{ {N.PREC_SIMT: 'simt', N.PREC_SIMT_SKINNY: 'simt16', N.PREC_3XTF32: 'tc', N.PREC_3XTF32_PAIR: 'tc2', N.PREC_BF16_PAIR: 'bf16'}[prec] }",
                             flops=flops, nbytes=nbytes)
             launch.maps = keep
             out.append(launch)
@@ -671,7 +697,8 @@ class DeviceHybrid:
                 dcols=_ptr(s.dcols) if s.dcols is not None else 0, dx=_ptr(st.dx),
                 mask=_ptr(st.x) if st.mask_input else 0, partial=_ptr(st.partial), dw=_ptr(W), db=_ptr(B),
                 bpart=_ptr(st.bpart), weight=_ptr(self.pview(self.params, s.index, st.params[0])),
-                wpad=_ptr(st.wpad), cap=s.batch_size, c=c, h=h, w=w, f=f, k=k,
+                wpad=_ptr(st.wt if aux == N.CONVTC_WT_WEIGHTS else st.wpad), colst=_ptr(st.colst),
+                dyk=_ptr(st.dyk), bf16=int(st.bf16), pix_ld=st.pix_ld, cap=s.batch_size, c=c, h=h, w=w, f=f, k=k,
                 stride=st.attrs.get("stride", 1), pad=st.attrs.get("padding", 0), oh=oh, ow=ow, kk=c * k * k,
                 kkp=st.kkp,
                 ksplit=st.ksplit, ksplit_len=st.ksplit_len, model=s.index, block_base=base, blocks=nb))
@@ -694,24 +721,28 @@ class DeviceHybrid:
             W = self.pview(self.params, s.index, st.params[0])
             kf = f * k * k
             flips.append((s, N.ConvTcProblem(weight=_ptr(W), wpad=_ptr(st.wflip), c=c, f=f, k=k,
-                                             model=s.index)))
+                                             model=s.index, bf16=int(st.bf16))))
             # im2col over dy: channels F, spatial OH x OW -> H x W, padding k-1-p
-            cols.append((s, N.ConvTcProblem(x=_ptr(st.dy), cols=_ptr(s.dcols), cap=s.batch_size, c=f, h=oh, w=ow,
+            dst = s.dgcols if st.bf16 else s.dcols
+            cols.append((s, N.ConvTcProblem(x=_ptr(st.dy), cols=_ptr(dst), cap=s.batch_size, c=f, h=oh, w=ow,
                                             f=c, k=k, stride=1, pad=k - 1 - p, oh=h, ow=w, kk=kf, kkp=kf,
-                                            model=s.index)))
+                                            model=s.index, bf16=int(st.bf16))))
         out.append(self._aux_table(N.CONVTC_FLIP_WEIGHTS, flips, f"{label}/tc/flipw",
                                    lambda pr: grid(pr.c * pr.f * pr.k * pr.k), 3))
         out.append(self._aux_table(N.CONVTC_IM2COL, cols, f"{label}/tc/im2col_dy",
                                    lambda pr: -(-(pr.cap * pr.oh * pr.ow) // 32) * -(-pr.c // 32), 3))
-        rows = []
+        by_prec = {}
         for s, st in items:
             c, h, w = st.in_shape
             f, oh, ow = self._conv_out(st)
             kf = f * st.attrs["kernel"] ** 2
-            rows.append((s, dict(a=_ptr(s.dcols), b=_ptr(st.wflip), c=_ptr(st.dx), bias=0,
-                                 mask=_ptr(st.x) if st.mask_input else 0, dbias=0, m=s.batch_size * h * w, n=c,
-                                 k=kf, lda=kf, ldb=kf, ldc=c, relu=0, row_mult=h * w, c_mode=1)))
-        out += self._emit_gemm(N.HNN_FWD, N.PREC_3XTF32_PAIR, rows, f"{label}/tc/dgfwd")
+            src = s.dgcols if st.bf16 else s.dcols
+            by_prec.setdefault(N.PREC_BF16_PAIR if st.bf16 else N.PREC_3XTF32_PAIR, []).append(
+                (s, dict(a=_ptr(src), b=_ptr(st.wflip), c=_ptr(st.dx), bias=0,
+                         mask=_ptr(st.x) if st.mask_input else 0, dbias=0, m=s.batch_size * h * w, n=c,
+                         k=kf, lda=kf, ldb=kf, ldc=c, relu=0, row_mult=h * w, c_mode=1)))
+        for prec, rows in by_prec.items():
+            out += self._emit_gemm(N.HNN_FWD, prec, rows, f"{label}/tc/dgfwd")
         return out
 
     def _aux_table(self, aux, probs_by_slot, label, blocks_of, max_k):
@@ -727,17 +758,27 @@ class DeviceHybrid:
 
     def _conv_tc_launches(self, op, items, label):
         """Tensor-core conv layers of one wave: im2col / transpose / col2im / split reduce around
-        CTA-pair 3xTF32 GEMMs (csrc/conv_tc.cu, csrc/gemm_tc2.cu)."""
+        CTA-pair GEMMs (csrc/conv_tc.cu, csrc/gemm_tc2.cu): 3xTF32 on fp32 operands, or kind::f16 on
+        bf16 operand copies (every operand K-major: pixel-contiguous copies for the weight gradient)."""
         def geo(st):  # GEMM K = C*k*k padded to kkp
             c, h, w = st.in_shape
             f, oh, ow = self._conv_out(st)
             return c, h, w, f, oh, ow, st.kkp
 
-        def weight(s, st):  # GEMM B operand rows [f, kkp]: the weights, or their padded copy
+        def weight(s, st):  # GEMM B operand rows [f, kkp]: the weights, or their padded / bf16 copy
             return _ptr(st.wpad) if st.wpad is not None else _ptr(self.pview(self.params, s.index, st.params[0]))
 
         def grid(total):
             return max(1, min(-(-total // 256), 4 * 148))
+
+        def prec(st):
+            return N.PREC_BF16_PAIR if st.bf16 else N.PREC_3XTF32_PAIR
+
+        def gemms(op_, rows_by_prec, lab):
+            res = []
+            for pr, rows in rows_by_prec.items():
+                res += self._emit_gemm(op_, pr, rows, lab)
+            return res
 
         out = []
         if op == N.HNN_FWD:
@@ -749,15 +790,15 @@ class DeviceHybrid:
                 N.CONVTC_IM2COL, items, f"{label}/tc/im2col",
                 lambda s, st: -(-(s.batch_size * geo(st)[4] * geo(st)[5]) // 32) * -(-geo(st)[0] // 32),
                 nbytes=sum(8 * s.batch_size * geo(st)[4] * geo(st)[5] * geo(st)[6] for s, st in items)))
-            rows = []
+            rows = {}
             for s, st in items:
                 c, h, w, f, oh, ow, kk = geo(st)
                 B = self.pview(self.params, s.index, st.params[1])
-                rows.append((s, dict(a=_ptr(st.cols), b=weight(s, st), c=_ptr(st.y), bias=_ptr(B), mask=0, dbias=0,
-                                     m=s.batch_size * oh * ow, n=f, k=kk, lda=kk, ldb=kk, ldc=f, relu=int(st.relu),
-                                     row_mult=oh * ow, c_mode=1)))
-            out += self._emit_gemm(N.HNN_FWD, N.PREC_3XTF32_PAIR, rows, f"{label}/tc")
-            return out
+                rows.setdefault(prec(st), []).append(
+                    (s, dict(a=_ptr(st.cols), b=weight(s, st), c=_ptr(st.y), bias=_ptr(B), mask=0, dbias=0,
+                             m=s.batch_size * oh * ow, n=f, k=kk, lda=kk, ldb=kk, ldc=f, relu=int(st.relu),
+                             row_mult=oh * ow, c_mode=1)))
+            return out + gemms(N.HNN_FWD, rows, f"{label}/tc")
         tiles_t = lambda s, st: (s.batch_size * -(-(geo(st)[4] * geo(st)[5]) // 32) * -(-geo(st)[3] // 32))
         if op == N.HNN_DGRAD:
             # (only stages whose input gradient is needed reach here)
@@ -767,14 +808,22 @@ class DeviceHybrid:
             items = [(s, st) for s, st in items if not st.dg_fwd]
             if not items:
                 return out
+            wt = [(s, st) for s, st in items if st.bf16]
+            if wt:
+                out.append(self._convtc_aux(N.CONVTC_WT_WEIGHTS, wt, f"{label}/tc/wt",
+                                            lambda s, st: grid(geo(st)[3] * geo(st)[6])))
             out.append(self._convtc_aux(N.CONVTC_TRANSPOSE_DY, items, f"{label}/tc/transpose", tiles_t))
-            rows = []
+            rows = {}
             for s, st in items:
                 c, h, w, f, oh, ow, kk = geo(st)
-                rows.append((s, dict(a=_ptr(st.dyt), b=weight(s, st), c=_ptr(s.dcols), bias=0, mask=0, dbias=0,
-                                     m=s.batch_size * oh * ow, n=kk, k=f, lda=f, ldb=kk, ldc=kk, relu=0,
-                                     row_mult=oh * ow)))
-            out += self._emit_gemm(N.HNN_DGRAD, N.PREC_3XTF32_PAIR, rows, f"{label}/tc")
+                if st.bf16:  # B = w^T [kkp, f] (K-major)
+                    d = dict(a=_ptr(st.dyt), b=_ptr(st.wt), ldb=f)
+                else:
+                    d = dict(a=_ptr(st.dyt), b=weight(s, st), ldb=kk)
+                rows.setdefault(prec(st), []).append(
+                    (s, dict(d, c=_ptr(s.dcols), bias=0, mask=0, dbias=0, m=s.batch_size * oh * ow, n=kk, k=f,
+                             lda=f, ldc=kk, relu=0, row_mult=oh * ow)))
+            out += gemms(N.HNN_DGRAD, rows, f"{label}/tc")
             out.append(self._convtc_aux(N.CONVTC_COL2IM, items, f"{label}/tc/col2im",
                                         lambda s, st: (s.batch_size * geo(st)[1] * -(-geo(st)[2] // 32)
                                                        * -(-geo(st)[0] // 16))))
@@ -783,13 +832,17 @@ class DeviceHybrid:
         fresh = [(s, st) for s, st in items if not (st.needs_dx and not st.dg_fwd)]
         if fresh:
             out.append(self._convtc_aux(N.CONVTC_TRANSPOSE_DY, fresh, f"{label}/tc/transpose", tiles_t))
-        rows = []
+        rows = {}
         for s, st in items:
             c, h, w, f, oh, ow, kk = geo(st)
-            rows.append((s, dict(a=_ptr(st.dyt), b=_ptr(st.cols), c=_ptr(st.partial), bias=0, mask=0, dbias=0,
-                                 m=f, n=kk, k=s.batch_size * oh * ow, lda=f, ldb=kk, ldc=kk, relu=0,
-                                 row_mult=oh * ow, ksplit=st.ksplit, ksplit_len=st.ksplit_len)))
-        out += self._emit_gemm(N.HNN_WGRAD, N.PREC_3XTF32_PAIR, rows, f"{label}/tc")
+            if st.bf16:  # A = dy [f, pixels], B = cols^T [kkp, pixels]: both pixel-contiguous
+                d = dict(a=_ptr(st.dyk), b=_ptr(st.colst), lda=st.pix_ld, ldb=st.pix_ld)
+            else:
+                d = dict(a=_ptr(st.dyt), b=_ptr(st.cols), lda=f, ldb=kk)
+            rows.setdefault(prec(st), []).append(
+                (s, dict(d, c=_ptr(st.partial), bias=0, mask=0, dbias=0, m=f, n=kk, k=s.batch_size * oh * ow,
+                         ldc=kk, relu=0, row_mult=oh * ow, ksplit=st.ksplit, ksplit_len=st.ksplit_len)))
+        out += gemms(N.HNN_WGRAD, rows, f"{label}/tc")
         out.append(self._convtc_aux(N.CONVTC_WGRAD_REDUCE, items, f"{label}/tc/reduce",
                                     lambda s, st: grid(geo(st)[3] * geo(st)[6] + geo(st)[3])))
         return out

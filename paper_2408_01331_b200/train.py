@@ -176,14 +176,18 @@ class Trainer:
     Hooks are the reference's (src/train.py:294-325).  Extra keyword options:
     ``use_graph`` (replay each step as a CUDA graph), ``use_tensor_cores``,
     ``device``, ``comm`` (a :class:`paper_2408_01331_b200.parallel.RankGroup`
-    for multi-GPU dataset broadcast / metric gather).
+    for multi-GPU dataset broadcast / metric gather), ``conv_precision``
+    ("f32": 3xTF32 tensor-core convolutions, fp32 parity; "bf16": bf16 operands with fp32
+    accumulation and fp32 master weights, the BASELINE C4 setting).
     """
 
     def __init__(self, hybrid: HybridModel, plan, jobs: list, datasets: dict, completion_sink=None,
                  pause_sink=None, pause_poll=None, step_observer=None, slice_observer=None, *,
                  use_graph: bool = True, use_tensor_cores: bool = True, device=None, comm=None,
-                 loss_observer=None, fuse_optimizer: bool = True, keep_grads: bool = False):
+                 loss_observer=None, fuse_optimizer: bool = True, keep_grads: bool = False,
+                 conv_precision: str = "f32"):
         self.hybrid = hybrid
+        self.conv_precision = conv_precision
         self.plan = plan
         jobs = [TrainingJob.coerce(j) for j in jobs]
         self.jobs = {j.job_id: j for j in jobs}
@@ -223,7 +227,8 @@ class Trainer:
 
     def _device(self):
         dev = self.hybrid.materialize(self.device_name, use_tensor_cores=self.use_tc,
-                                      fuse_optimizer=self.fuse_optimizer, keep_grads=self.keep_grads)
+                                      fuse_optimizer=self.fuse_optimizer, keep_grads=self.keep_grads,
+                                      conv_precision=self.conv_precision)
         for jid, sub in self.hybrid.sub_models.items():
             opt = sub.optimizer
             if opt.m1 or opt.m2 or opt.velocity:

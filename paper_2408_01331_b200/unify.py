@@ -146,7 +146,7 @@ class HybridModel:
             self.device.upload_params(sub.slot, bare)
 
     def materialize(self, device=None, use_tensor_cores: bool = True, fuse_optimizer: bool = True,
-                    keep_grads: bool = False):
+                    keep_grads: bool = False, conv_precision: str = "f32"):
         """Pack every sub-model into device arenas (idempotent)."""
         if self.device is not None:
             return self.device
@@ -159,7 +159,7 @@ class HybridModel:
             slots.append(ModelSlot(i, jid, sub.original, hp.batch_size if hp else 1, sub.optimizer.kind,
                                    sub.optimizer.momentum, engine.param_specs(sub.original)))
         dev = DeviceHybrid(slots, device=device, use_tensor_cores=use_tensor_cores, fuse_optimizer=fuse_optimizer,
-                           keep_grads=keep_grads)
+                           keep_grads=keep_grads, conv_precision=conv_precision)
         for jid, sub in self.sub_models.items():
             dev.upload_params(sub.slot, {unqualify(jid, pid): self._host_params[pid] for pid in sub.param_ids()})
         self.device = dev

@@ -610,3 +610,42 @@ def test_tensor_core_conv_layers_match_oracle(pkg, batch):
     for pid, g in ref.items():
         assert rel(grabbed[0][pid], g) <= 1e-5, (pid, rel(grabbed[0][pid], g))
     assert len(grabbed) == len(batches)
+
+
+def test_bf16_tensor_core_convs_track_oracle(pkg):
+    """conv_precision="bf16" (BASELINE C4): conv GEMMs on kind::f16 with bf16 operand copies, fp32
+    accumulation, fp32 master weights.  Parity is accuracy-class, not fp32: first-step gradients within
+    1e-1 (max-abs relative; bf16 activations flip a few relu masks) of the fp32 oracle, and the
+    per-step losses of a short run within 2e-2."""
+    from paper_2408_01331_b200 import store, zoo
+
+    spec = [("conv0", "conv2d", {"filters": 64, "kernel": 3, "padding": 1}), ("act0", "relu", {}),
+            ("conv1", "conv2d", {"filters": 64, "kernel": 3, "padding": 1}), ("act1", "relu", {}),
+            ("pool1", "maxpool2d", {"kernel": 2}),
+            ("conv2", "conv2d", {"filters": 128, "kernel": 3, "padding": 1, "stride": 2}), ("act2", "relu", {}),
+            ("pool2", "maxpool2d", {"kernel": 4}),
+            ("flat", "flatten", {}), ("fc", "dense", {"units": 10})]
+    graph = zoo._seq("tc-conv", (3, 16, 16), spec)
+    splits = oracle.image_splits("tcconv", "mini", 10, (3, 16, 16), 96, 8)
+    ds = store.from_splits(splits)
+    job = pkg.TrainingJob("v", graph, ds.content_hash, pkg.HyperParams(1, 24, 0.01, "sgd", (), 4), 0, 0)
+    h = pkg.merge([job])
+    grabbed, losses = [], []
+    tr = pkg.Trainer(h, pkg.make_plan("fcfs", [job]), [job], {"v": ds}, keep_grads=True, fuse_optimizer=False,
+                     conv_precision="bf16", loss_observer=lambda j, step, loss, hits: losses.append(loss))
+    tr.step_observer = lambda j, p: grabbed.append(tr.device.download_grads(0))
+    tr.run()
+    labels = [l.label for l in tr.device.train_plan]
+    assert sum(l.endswith("/bf16") for l in labels) >= 5, labels
+    params = oracle.init_model(graph, 4)
+    bx, by, _ = oracle.epoch_batches(splits["train_x"], splits["train_y"], ds.content_hash, 24, 4, 0)[0]
+    logits, tape = oracle.model_forward(graph, params, bx)
+    _, dl = oracle.sce_loss_and_grad(logits, by)
+    ref = oracle.model_backward(tape, dl)
+    errs = {pid: rel(grabbed[0][pid], g) for pid, g in ref.items()}
+    assert max(errs.values()) <= 1e-1, errs
+    ref_losses = []
+    oracle.standalone_training(graph, splits, ds.content_hash, 1, 24, 0.01, "sgd", 4,
+                               observer=lambda s, p, l: ref_losses.append(l))
+    assert len(losses) == len(ref_losses)
+    assert max(abs(a - b) / abs(b) for a, b in zip(losses, ref_losses)) <= 2e-2, (losses, ref_losses)
