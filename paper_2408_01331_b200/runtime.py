@@ -528,8 +528,10 @@ class DeviceHybrid:
         return [[(s, s.stages[w]) for s in self.slots if w < len(s.stages)] for w in range(depth)]
 
     def _route_tc(self, op, d) -> bool:
-        """Dense problems big and aligned enough for a 128x128 tcgen05 tile go to the 3xTF32 kernel."""
-        if d["m"] < 128 or d["n"] < 64 or d["k"] < 64:
+        """Dense problems big and aligned enough for the tcgen05 tiles go to the 3xTF32 kernels.
+        The CTA-pair kernel takes short batches too (64 rows: a quarter of its 256-row tile still
+        beats the FFMA path 3x on C5's first layer); the single-CTA kernel needs 128 rows."""
+        if d["m"] < (32 if self.use_pairs else 128) or d["n"] < 64 or d["k"] < 64:
             return False
         if op == N.HNN_WGRAD and d["m"] > 4096:
             return False
@@ -683,7 +685,7 @@ class DeviceHybrid:
                 out += self._conv_group(op, group, label + ("/direct" if direct else ""), direct)
         return out
 
-    def _convtc_aux(self, aux, items, label, blocks_of, nbytes=0):
+    def _convtc_aux(self, aux, items, label, blocks_of, nbytes=None):
         probs, base = [], 0
         for s, st in items:
             c, h, w = st.in_shape
@@ -703,6 +705,21 @@ class DeviceHybrid:
                 kkp=st.kkp,
                 ksplit=st.ksplit, ksplit_len=st.ksplit_len, model=s.index, block_base=base, blocks=nb))
             base += nb
+        if nbytes is None:  # algorithmic bytes (read + write) for the roofline
+            nbytes = 0
+            for pr in probs:
+                esz = 2 if pr.bf16 else 4
+                pix_out, pix_in = pr.cap * pr.oh * pr.ow, pr.cap * pr.h * pr.w
+                if aux == N.CONVTC_IM2COL:
+                    nbytes += 4 * pr.c * pix_in + esz * pix_out * pr.kkp * (2 if pr.colst else 1)
+                elif aux == N.CONVTC_TRANSPOSE_DY:
+                    nbytes += 4 * pr.f * pix_out + esz * pr.f * pix_out * ((1 if pr.dyt else 0) + (1 if pr.dyk else 0))
+                elif aux == N.CONVTC_COL2IM:
+                    nbytes += 4 * pix_out * pr.kkp + 4 * pr.c * pix_in * (3 if pr.mask else 2)
+                elif aux == N.CONVTC_WGRAD_REDUCE:
+                    nbytes += 4 * pr.f * pr.kkp * (pr.ksplit + 1) + 4 * pr.f * (pr.cap + 1)
+                else:
+                    nbytes += (4 + esz) * pr.f * pr.kkp
         t = _dev_table(N.ConvTcProblem, probs, self.device)
         max_k = max(st.attrs["kernel"] for _, st in items)
         return Launch("hnn_conv_tc_aux", (aux, _ptr(t), len(probs), base, max_k, _ptr(self.cur), _ptr(self.status)),
@@ -788,8 +805,7 @@ class DeviceHybrid:
                                             lambda s, st: grid(geo(st)[3] * geo(st)[6])))
             out.append(self._convtc_aux(
                 N.CONVTC_IM2COL, items, f"{label}/tc/im2col",
-                lambda s, st: -(-(s.batch_size * geo(st)[4] * geo(st)[5]) // 32) * -(-geo(st)[0] // 32),
-                nbytes=sum(8 * s.batch_size * geo(st)[4] * geo(st)[5] * geo(st)[6] for s, st in items)))
+                lambda s, st: -(-(s.batch_size * geo(st)[4] * geo(st)[5]) // 32) * -(-geo(st)[0] // 32)))
             rows = {}
             for s, st in items:
                 c, h, w, f, oh, ow, kk = geo(st)
