@@ -15,7 +15,7 @@
 namespace hnn {
 
 constexpr int KTHREADS = 256;
-constexpr int FWD_ROWS = 4;  // rows per warp; tile = 8 warps x 4 rows = 32 rows
+constexpr int FWD_ROWS = 2;  // rows per warp; tile = 8 warps x 2 rows = 16 rows (2 waves of CTAs on C3)
 constexpr int DG_ROWS = 4;   // DGRAD rows per thread; tile = 8 row groups x 4 rows x 128 columns
 constexpr int WG_QUADS = 64; // WGRAD column quads per CTA; tile = 256 columns, 4 row quarters
 
@@ -114,31 +114,37 @@ __global__ void __launch_bounds__(KTHREADS) skinny_fwd_kernel(const hnn_gemm_pro
 
 // ---------------------------------------------------------------------------------------- DGRAD
 template <int KJ>
-__device__ __forceinline__ void outer_rows(const hnn_gemm_problem& p, int r0, int col, int rows) {
+__device__ __forceinline__ void outer_rows(const hnn_gemm_problem& p, int r0, int col, int rows, const float* dys) {
   float4 w[KJ];
 #pragma unroll
   for (int j = 0; j < KJ; ++j) w[j] = j < p.k ? ldg4(p.b + size_t(j) * p.ldb + col) : make_float4(0, 0, 0, 0);
+  // the relu-mask quads of all DG_ROWS rows are requested together (one round trip, not four)
+  float4 mk[DG_ROWS];
+#pragma unroll
+  for (int i = 0; i < DG_ROWS; ++i) {
+    const int r = r0 + i;
+    mk[i] = (p.mask && r < rows && r < p.m) ? ldg4(p.mask + size_t(r) * p.ldc + col) : make_float4(1, 1, 1, 1);
+  }
 #pragma unroll
   for (int i = 0; i < DG_ROWS; ++i) {
     const int r = r0 + i;
     if (r >= p.m) break;
     float4 o = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
     if (r < rows) {
-      const float* dy = p.a + size_t(r) * p.lda;
+      const float* dy = dys + (threadIdx.x >> 5) * DG_ROWS * 16 + i * 16;  // staged dy row (shared)
 #pragma unroll
       for (int j = 0; j < KJ; ++j) {
-        const float d = j < p.k ? __ldg(dy + j) : 0.0f;
+        const float d = dy[j];
         o.x = fmaf(d, w[j].x, o.x);
         o.y = fmaf(d, w[j].y, o.y);
         o.z = fmaf(d, w[j].z, o.z);
         o.w = fmaf(d, w[j].w, o.w);
       }
       if (p.mask) {
-        const float4 m = ldg4(p.mask + size_t(r) * p.ldc + col);
-        o.x = np_mask(o.x, m.x);
-        o.y = np_mask(o.y, m.y);
-        o.z = np_mask(o.z, m.z);
-        o.w = np_mask(o.w, m.w);
+        o.x = np_mask(o.x, mk[i].x);
+        o.y = np_mask(o.y, mk[i].y);
+        o.z = np_mask(o.z, mk[i].z);
+        o.w = np_mask(o.w, mk[i].w);
       }
     }
     *reinterpret_cast<float4*>(p.c + size_t(r) * p.ldc + col) = o;
@@ -148,18 +154,24 @@ __device__ __forceinline__ void outer_rows(const hnn_gemm_problem& p, int r0, in
 __global__ void __launch_bounds__(KTHREADS) skinny_dgrad_kernel(const hnn_gemm_problem* __restrict__ probs, int nprob,
                                                                 const hnn_step_row* __restrict__ cur,
                                                                 const hnn_model_status* __restrict__ status) {
+  __shared__ float dys[8 * DG_ROWS * 16];  // the CTA's 32 dy rows, 16 columns (zero padded)
   const int pi = find_problem(probs, nprob, blockIdx.x, [](const hnn_gemm_problem& q) { return q.tile_base; });
   const hnn_gemm_problem& p = probs[pi];
   if (!live(cur, status, p.model)) return;
   const int rows = cur[p.model].rows;
   const int t = blockIdx.x - p.tile_base;
   const int m0 = (t / p.tiles_n) * (8 * DG_ROWS), n0 = (t % p.tiles_n) * 128;
+  for (int e = threadIdx.x; e < 8 * DG_ROWS * 16; e += KTHREADS) {
+    const int r = m0 + e / 16, j = e % 16;
+    dys[e] = (j < p.k && r < rows && r < p.m) ? __ldg(p.a + size_t(r) * p.lda + j) : 0.0f;
+  }
+  __syncthreads();
   const int col = n0 + (threadIdx.x & 31) * 4, r0 = m0 + (threadIdx.x >> 5) * DG_ROWS;
   if (col >= p.n || r0 >= p.m) return;  // n is a multiple of 4 (host routing)
-  if (p.k <= 4) outer_rows<4>(p, r0, col, rows);
-  else if (p.k <= 8) outer_rows<8>(p, r0, col, rows);
-  else if (p.k <= 12) outer_rows<12>(p, r0, col, rows);
-  else outer_rows<16>(p, r0, col, rows);
+  if (p.k <= 4) outer_rows<4>(p, r0, col, rows, dys);
+  else if (p.k <= 8) outer_rows<8>(p, r0, col, rows, dys);
+  else if (p.k <= 12) outer_rows<12>(p, r0, col, rows, dys);
+  else outer_rows<16>(p, r0, col, rows, dys);
 }
 
 // ---------------------------------------------------------------------------------------- WGRAD

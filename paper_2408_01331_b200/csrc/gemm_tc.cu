@@ -333,17 +333,17 @@ __global__ void colsum_kernel(const hnn_gemm_problem* __restrict__ probs, int np
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= p.m) return;
   const int R = cur[p.model].rows * p.row_mult;
-  // loads of 16 rows issue before their (sequential, order-preserving) adds: the loop is
+  // loads of 32 rows issue before their (sequential, order-preserving) adds: the loop is
   // latency-bound otherwise (58 us per C3 launch at one load in flight per thread)
   float acc = -0.0f;
   const float* col = p.a + i;
   int r = 0;
-  for (; r + 16 <= R; r += 16) {
-    float v[16];
+  for (; r + 32 <= R; r += 32) {
+    float v[32];
 #pragma unroll
-    for (int j = 0; j < 16; ++j) v[j] = __ldg(col + size_t(r + j) * p.lda);
+    for (int j = 0; j < 32; ++j) v[j] = __ldg(col + size_t(r + j) * p.lda);
 #pragma unroll
-    for (int j = 0; j < 16; ++j) acc = __fadd_rn(acc, v[j]);
+    for (int j = 0; j < 32; ++j) acc = __fadd_rn(acc, v[j]);
   }
   for (; r < R; ++r) acc = __fadd_rn(acc, __ldg(col + size_t(r) * p.lda));
   if (p.dbias) p.dbias[i] = acc;

@@ -401,6 +401,23 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC2_THREADS, 1)
           const int n = nh + cb + lane;
           if (n < pn) {
             const int rmax = min(32, pm - row0);
+            if (!owm && !owv) {  // plain SGD: 16 rows' weights in flight at once
+              for (int r16 = 0; r16 < rmax; r16 += 16) {
+                float w[16];
+#pragma unroll
+                for (int i = 0; i < 16; ++i)
+                  w[i] = r16 + i < rmax ? ow[size_t(row0 + r16 + i) * ldc + n] : 0.0f;
+#pragma unroll
+                for (int i = 0; i < 16; ++i) {
+                  const int rr = r16 + i;
+                  if (rr >= rmax) break;
+                  const float g = lds32(stg + rr * 128 + ((((lane >> 2) ^ (rr & 7))) << 4) + ((lane & 3) << 2));
+                  float m0v = 0.0f, v0v = 0.0f;
+                  update_one(u, w[i], g, m0v, v0v);
+                  ow[size_t(row0 + rr) * ldc + n] = w[i];
+                }
+              }
+            } else
             for (int r8 = 0; r8 < rmax; r8 += 8) {
               float w[8], mm[8], vv[8];
 #pragma unroll

@@ -37,6 +37,74 @@ __device__ float np_pairwise_sum(const float* a, int n) {
   return __fadd_rn(np_pairwise_sum(a, n2), np_pairwise_sum(a + n2, n - n2));
 }
 
+// One row per thread for C <= 16 classes (every config: 10): the warp-per-row path below spends
+// its time in lane-0 serial sections (34 us for C3's 32 x 256 rows).  Same arithmetic, in
+// registers: numpy max / argmax NaN rules, expf of shifted logits, numpy's pairwise float32 sum.
+template <int CM>
+__device__ __forceinline__ void sce_row_thread(const float* lrow, float* drow, int C, int t, float inv_n,
+                                               float& logp, int& hit) {
+  float v[CM], e[CM];
+#pragma unroll
+  for (int j = 0; j < CM; ++j) v[j] = j < C ? lrow[j] : 0.0f;
+  float mx = v[0], best = v[0];
+  int arg = 0;
+  bool nan_seen = (best != best);
+#pragma unroll
+  for (int j = 1; j < CM; ++j) {
+    if (j >= C) break;
+    const float x = v[j];
+    if (!nan_seen && !(x <= best)) {
+      best = x;
+      arg = j;
+      if (x != x) nan_seen = true;
+    }
+    mx = (mx >= x || mx != mx) ? mx : x;
+  }
+  if (nan_seen) mx = __int_as_float(0x7fc00000);
+  float sh_t = 0.0f;
+#pragma unroll
+  for (int j = 0; j < CM; ++j) {
+    if (j >= C) break;
+    const float sh = __fsub_rn(v[j], mx);
+    if (j == t) sh_t = sh;
+    e[j] = expf(sh);
+  }
+  float sum;
+  if (C < 8) {
+    sum = 0.0f;
+#pragma unroll
+    for (int j = 0; j < 8; ++j)
+      if (j < C) sum = __fadd_rn(sum, e[j]);
+  } else {
+    float r[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) r[j] = e[j];
+    const int full = C - (C % 8);
+#pragma unroll
+    for (int i = 8; i < CM; i += 8)
+      if (i < full)
+#pragma unroll
+        for (int j = 0; j < 8; ++j) r[j] = __fadd_rn(r[j], e[i + j]);
+    sum = __fadd_rn(__fadd_rn(__fadd_rn(r[0], r[1]), __fadd_rn(r[2], r[3])),
+                    __fadd_rn(__fadd_rn(r[4], r[5]), __fadd_rn(r[6], r[7])));
+#pragma unroll
+    for (int j = 8; j < CM; ++j)
+      if (j >= full && j < C) sum = __fadd_rn(sum, e[j]);
+  }
+  const float lse = logf(sum);
+  logp = __fsub_rn(sh_t, lse);
+  hit = (arg == t);
+  if (drow) {
+#pragma unroll
+    for (int j = 0; j < CM; ++j) {
+      if (j >= C) break;
+      float pr = expf(__fsub_rn(__fsub_rn(v[j], mx), lse));
+      if (j == t) pr = __fsub_rn(pr, 1.0f);
+      drow[j] = __fmul_rn(pr, inv_n);
+    }
+  }
+}
+
 __global__ void __launch_bounds__(SCE_THREADS) sce_kernel(const hnn_sce_problem* __restrict__ probs,
                                                           const hnn_step_row* __restrict__ cur,
                                                           hnn_model_status* __restrict__ status, int train,
@@ -54,6 +122,22 @@ __global__ void __launch_bounds__(SCE_THREADS) sce_kernel(const hnn_sce_problem*
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   int hits = 0;
   const float inv_n = __fdiv_rn(1.0f, (float)R);
+  if (C <= 16) {
+    for (int r = threadIdx.x; r < p.cap; r += SCE_THREADS) {
+      float* drow = p.dlogits ? p.dlogits + size_t(r) * p.ld : nullptr;
+      if (r >= R) {
+        if (drow)
+          for (int j = 0; j < C; ++j) drow[j] = 0.0f;
+        continue;
+      }
+      float lp;
+      int hit;
+      sce_row_thread<16>(p.logits + size_t(r) * p.ld, drow, C, p.labels[r], inv_n, lp, hit);
+      logp[r] = lp;
+      hits += hit;
+    }
+    hits = __reduce_add_sync(0xffffffffu, hits);
+  } else
   for (int r = warp; r < p.cap; r += SCE_WARPS) {
     float* drow = p.dlogits ? p.dlogits + size_t(r) * p.ld : nullptr;
     if (r >= R) {
