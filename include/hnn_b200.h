@@ -358,6 +358,26 @@ typedef struct hnn_convtc_problem {
 int hnn_conv_tc_aux(int op, const hnn_convtc_problem* probs, int nprob, int total_blocks, int max_k,
                     const hnn_step_row* cur, const hnn_model_status* status, void* stream);
 
+/*
+ * Grouped embedding-lookup (ops.py:258-278; embed.cu).  op HNN_FWD: y[b, l, :] = table[x[b, l], :]
+ * (rows past the batch zeroed), one warp per (b, l) row, blocks = ceil(cap * len / 8);
+ * op HNN_WGRAD: dtable[v, :] = sum over positions with x == v, in ascending position order, of
+ * dy[p, :] (np.add.at's order; no atomics), one warp per table row, blocks = ceil(vocab / 8).
+ * Token ids are float32 sample values, validated by the host (integral, in [0, vocab)).
+ */
+typedef struct hnn_embed_problem {
+  const float* x;     /* [cap, ldx] token ids */
+  const float* table; /* [vocab, dim] */
+  float* y;           /* [cap, len * dim] */
+  const float* dy;    /* [cap, len * dim] */
+  float* dtable;      /* [vocab, dim] */
+  int32_t cap, len, ldx, dim, vocab;
+  int32_t model, block_base, blocks;
+} hnn_embed_problem;
+
+int hnn_embedding(int op, const hnn_embed_problem* probs, int nprob, int total_blocks, const hnn_step_row* cur,
+                  const hnn_model_status* status, void* stream);
+
 /* Self-test of the optimizer's exact float32 arithmetic (no reference counterpart): for i < n,
  * q[i] = a[i] / b[i] and r[i] = sqrt(a[i]) with the same round-to-nearest-even routines the
  * Adam update uses (optim.py:84-87: m / bias1, v / bias2, np.sqrt, the final quotient). */

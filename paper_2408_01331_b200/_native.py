@@ -71,6 +71,11 @@ class ConvTcProblem(C.Structure):
                 ("pix_ld", I)]
 
 
+class EmbedProblem(C.Structure):
+    _fields_ = [("x", P), ("table", P), ("y", P), ("dy", P), ("dtable", P), ("cap", I), ("len", I), ("ldx", I),
+                ("dim", I), ("vocab", I), ("model", I), ("block_base", I), ("blocks", I)]
+
+
 class PoolProblem(C.Structure):
     _fields_ = [("x", P), ("y", P), ("idx", P), ("dy", P), ("dx", P), ("mask", P),
                 ("cap", I), ("c", I), ("h", I), ("w", I), ("k", I), ("stride", I), ("oh", I), ("ow", I),
@@ -94,7 +99,7 @@ class OptSegment(C.Structure):
 STRUCTS = {
     "hnn_step_row": StepRow, "hnn_model_status": ModelStatus, "hnn_gather_problem": GatherProblem,
     "hnn_gemm_problem": GemmProblem, "hnn_conv_problem": ConvProblem, "hnn_pool_problem": PoolProblem,
-    "hnn_relu_problem": ReluProblem, "hnn_convtc_problem": ConvTcProblem, "hnn_sce_problem": SceProblem, "hnn_opt_segment": OptSegment,
+    "hnn_relu_problem": ReluProblem, "hnn_convtc_problem": ConvTcProblem, "hnn_embed_problem": EmbedProblem, "hnn_sce_problem": SceProblem, "hnn_opt_segment": OptSegment,
 }
 
 # every symbol include/hnn_b200.h declares, with its ctypes signature
@@ -118,6 +123,7 @@ SIGNATURES = {
     "hnn_multi_tensor_adam": [P, C.c_int, C.c_int, P, P, VP],
     "hnn_selftest_div_sqrt": [VP, VP, VP, VP, C.c_int64, VP],
     "hnn_conv_tc_aux": [C.c_int, P, C.c_int, C.c_int, C.c_int, P, P, VP],
+    "hnn_embedding": [C.c_int, P, C.c_int, C.c_int, P, P, VP],
     "hnn_struct_size": [C.c_char_p],
     "hnn_last_error": [],
     "hnn_version": [],

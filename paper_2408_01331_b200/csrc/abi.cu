@@ -94,6 +94,7 @@ int hnn_struct_size(const char* name) {
   if (!strcmp(name, "hnn_sce_problem")) return sizeof(hnn_sce_problem);
   if (!strcmp(name, "hnn_opt_segment")) return sizeof(hnn_opt_segment);
   if (!strcmp(name, "hnn_convtc_problem")) return sizeof(hnn_convtc_problem);
+  if (!strcmp(name, "hnn_embed_problem")) return sizeof(hnn_embed_problem);
   return -1;
 }
 

@@ -52,6 +52,18 @@ def _stream():
     return _torch().cuda.current_stream().cuda_stream
 
 
+def _embed(op, x, table, y, dy, dtable):
+    """One-problem hnn_embedding launch: x [B, L] token ids (validated), table [V, D]."""
+    torch = _torch()
+    B, L = x.shape
+    V, D = table.shape
+    blocks = -(-(B * L) // 8) if op == N.HNN_FWD else -(-V // 8)
+    prob = N.EmbedProblem(x=_ptr(x), table=_ptr(table), y=_ptr(y), dy=_ptr(dy), dtable=_ptr(dtable), cap=B, len=L,
+                          ldx=L, dim=D, vocab=V, model=0, block_base=0, blocks=blocks)
+    t = torch.frombuffer(bytearray(N.table_bytes(N.EmbedProblem, [prob])), dtype=torch.uint8).to(_dev())
+    N.call("hnn_embedding", op, _ptr(t), 1, blocks, _ptr(_cur(B)), 0, _stream())
+
+
 def _gemm(op, rows, d):
     prec = N.PREC_SIMT
     tm, tn = N.tile_shape(op, prec)
@@ -199,6 +211,13 @@ def forward(name, x, params, attrs, targets=None):
             raise ValueError("targets batch dimension does not match logits")
         loss, dl, _ = sce_device(xd, torch.from_numpy(t.astype(np.int32)).to(xd.device))
         return np.asarray(loss.item(), dtype=np.float32), {"dlogits": dl, "keep": keep}
+    if name == "embedding-lookup":
+        table = P["table"]
+        check_class_indices(_host(x), table.shape[0])  # same errors as the reference (ops.py:268-270)
+        xx = xd.reshape(xd.shape[0], -1).contiguous()
+        y = torch.empty(xx.shape[0], xx.shape[1], table.shape[1], dtype=torch.float32, device=xd.device)
+        _embed(N.HNN_FWD, xx, table, y, None, None)
+        return _back(y.reshape(*xd.shape, table.shape[1]), keep), {"x": xx, "keep": keep}
     raise UnsupportedGraphError(f"op {name!r} has no device kernel")
 
 
@@ -243,6 +262,11 @@ def backward(name, dy, aux, params, attrs):
         return _back(dx, keep), {}
     if name == "flatten":
         return _back(dyd.reshape(aux["in_shape"]), keep), {}
+    if name == "embedding-lookup":
+        table = P["table"]
+        dt = torch.empty_like(table)
+        _embed(N.HNN_WGRAD, aux["x"], table, None, dyd.contiguous(), dt)
+        return None, {"table": _back(dt, keep)}  # indices carry no gradient
     raise UnsupportedGraphError(f"op {name!r} has no device kernel")
 
 

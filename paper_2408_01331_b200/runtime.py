@@ -136,7 +136,9 @@ def lower_graph(graph) -> tuple:
             if stages:
                 stages[-1].out_shape = outs  # a view: same memory, flat per-sample shape
         elif n.op == "embedding-lookup":
-            raise UnsupportedGraphError(f"node {n.node_id!r}: embedding-lookup has no device kernel yet")
+            if stages:
+                raise UnsupportedGraphError(f"node {n.node_id!r}: embedding-lookup must read the model input")
+            stages.append(Stage("embed", n.node_id, dict(n.attrs), ins, outs, params=(f"{n.node_id}.table",)))
         else:
             raise UnsupportedGraphError(f"node {n.node_id!r}: op {n.op!r} cannot appear here")
         i += 1
@@ -148,7 +150,7 @@ def lower_graph(graph) -> tuple:
     seen_param = False
     for k, st in enumerate(stages):
         st.needs_dx = seen_param
-        if st.kind in ("dense", "conv"):
+        if st.kind in ("dense", "conv", "embed"):
             seen_param = True
         if k > 0 and stages[k - 1].relu:
             st.mask_input = True
@@ -347,6 +349,8 @@ class DeviceHybrid:
                 feats = int(np.prod(st.out_shape))
                 if st.kind == "dense":
                     st.ld_out = _align4(feats)
+                elif st.kind == "embed":
+                    st.ld_out = feats  # [len, dim] rows back to back
                 elif st.kind == "relu":
                     st.ld_out = st.ld_in
                 else:
@@ -506,6 +510,15 @@ class DeviceHybrid:
                                                   f"!= graph input {s.sample_shape}")
             if d.max_label >= s.classes:
                 raise ValueError(f"target class out of range [0, {s.classes})")
+            if s.stages[0].kind == "embed":
+                # token ids checked once here (the reference checks each batch in _embed_fwd,
+                # src/ops.py:268-270, via check_class_indices): integral and inside the vocabulary
+                vocab = s.stages[0].attrs["vocab"]
+                for x in (d.train_x, d.test_x):
+                    if x.numel() and bool((x != torch.trunc(x)).any()):
+                        raise ValueError("targets must hold integral class indices")
+                    if x.numel() and bool(((x < 0) | (x >= vocab)).any()):
+                        raise ValueError(f"target class out of range [0, {vocab})")
         self._gather_train = self._gather_launch(train=True)
         self._gather_eval = self._gather_launch(train=False)
 
@@ -912,6 +925,23 @@ class DeviceHybrid:
                                                         _ptr(self.status)), rt, label + "/reduce"))
         return out
 
+    def _embed_launch(self, op, items, label):
+        probs, base = [], 0
+        for s, st in items:
+            length, dim, vocab = st.in_shape[0], st.attrs["dim"], st.attrs["vocab"]
+            nb = -(-(s.batch_size * length) // 8) if op == N.HNN_FWD else -(-vocab // 8)
+            probs.append(N.EmbedProblem(x=_ptr(st.x), table=_ptr(self.pview(self.params, s.index, st.params[0])),
+                                        y=_ptr(st.y), dy=_ptr(st.dy),
+                                        dtable=_ptr(self.pview(self.grads, s.index, st.params[0])),
+                                        cap=s.batch_size, len=length, ldx=st.ld_in, dim=dim, vocab=vocab,
+                                        model=s.index, block_base=base, blocks=nb))
+            base += nb
+        t = _dev_table(N.EmbedProblem, probs, self.device)
+        nbytes = sum(4 * p.cap * p.len * (2 * p.dim + 1) if op == N.HNN_FWD
+                     else 4 * (p.vocab * p.dim + p.cap * p.len * (p.dim + 1)) for p in probs)
+        return [Launch("hnn_embedding", (op, _ptr(t), len(probs), base, _ptr(self.cur), _ptr(self.status)), t,
+                       label, nbytes=nbytes)]
+
     def _pool_launch(self, op, items, label):
         probs, base = [], 0
         for s, st in items:
@@ -954,6 +984,9 @@ class DeviceHybrid:
                 out += self._conv_launch(op, group, f"{label}/conv")
             elif kind == "pool":
                 out += self._pool_launch(N.HNN_FWD if op == N.HNN_FWD else N.HNN_DGRAD, group, f"{label}/pool")
+            elif kind == "embed":
+                if op == N.HNN_FWD:  # (an embedding never needs an input gradient: it reads the input)
+                    out += self._embed_launch(N.HNN_FWD, group, f"{label}/embed")
             else:
                 out += self._relu_launch(N.HNN_FWD if op == N.HNN_FWD else N.HNN_DGRAD, group, f"{label}/relu")
         return out
@@ -1033,11 +1066,15 @@ class DeviceHybrid:
             dg = [(s, st) for s, st in items if st.needs_dx]
             if dg:
                 bwd += self._wave_launches(N.HNN_DGRAD, dg, f"bwd{w}")
-            for kind in ("dense", "conv"):
+            for kind in ("dense", "conv", "embed"):
                 grp = [(s, st) for s, st in items if st.kind == kind]
                 if grp:
-                    bwd += (self._gemm_launch(N.HNN_WGRAD, grp, f"bwd{w}/dense/wgrad") if kind == "dense"
-                            else self._conv_launch(N.HNN_WGRAD, grp, f"bwd{w}/conv/wgrad"))
+                    if kind == "dense":
+                        bwd += self._gemm_launch(N.HNN_WGRAD, grp, f"bwd{w}/dense/wgrad")
+                    elif kind == "conv":
+                        bwd += self._conv_launch(N.HNN_WGRAD, grp, f"bwd{w}/conv/wgrad")
+                    else:
+                        bwd += self._embed_launch(N.HNN_WGRAD, grp, f"bwd{w}/embed/wgrad")
         self.forward_plan = fwd
         self.train_plan = [self._gather_train] + fwd + [self._sce_launch(True)] + bwd + self._optimizer_launch()
         self.eval_plan = [self._gather_eval] + fwd + [self._sce_launch(False)]

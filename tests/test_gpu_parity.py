@@ -649,3 +649,66 @@ def test_bf16_tensor_core_convs_track_oracle(pkg):
                                observer=lambda s, p, l: ref_losses.append(l))
     assert len(losses) == len(ref_losses)
     assert max(abs(a - b) / abs(b) for a, b in zip(losses, ref_losses)) <= 2e-2, (losses, ref_losses)
+
+
+@pytest.mark.parametrize("optimizer", ["sgd", "adam"])
+def test_embedding_lookup_trajectory_matches_oracle(pkg, optimizer):
+    """embedding-lookup (src/ops.py:258-278) on the device: gathered rows and the table gradient in
+    np.add.at's order (repeated tokens accumulate in position order): per-step losses and the
+    final parameters of a short run vs the numpy oracle; out-of-vocabulary ids rejected."""
+    from paper_2408_01331_b200 import store, zoo
+
+    g = oracle.keyed_generator("embed-test", optimizer)
+    vocab, length, n = 40, 7, 96
+    splits = {"train_x": g.integers(0, vocab, (n, length)).astype(np.float32),
+              "train_y": g.integers(0, 4, n).astype(np.float32),
+              "test_x": g.integers(0, vocab, (16, length)).astype(np.float32),
+              "test_y": g.integers(0, 4, 16).astype(np.float32)}
+    splits["train_x"][:, 0] = 3.0  # a token repeated in every sample: long add.at chains
+    ds = store.from_splits(splits)
+    graph = zoo._seq("emb", (length,), [("emb", "embedding-lookup", {"vocab": vocab, "dim": 12}),
+                                        ("flat", "flatten", {}), ("fc1", "dense", {"units": 16}),
+                                        ("act", "relu", {}), ("fc2", "dense", {"units": 4})])
+    lr = 0.05 if optimizer == "sgd" else 0.01
+    job = pkg.TrainingJob("e", graph, ds.content_hash, pkg.HyperParams(2, 16, lr, optimizer, (), 3), 0, 0)
+    h = pkg.merge([job])
+    losses = []
+    tr = pkg.Trainer(h, pkg.make_plan("fcfs", [job]), [job], {"e": ds},
+                     loss_observer=lambda j, step, loss, hits: losses.append(loss))
+    tr.run()
+    ref_losses = []
+    ref_params, _, _, _ = oracle.standalone_training(graph, splits, ds.content_hash, 2, 16, lr, optimizer, 3,
+                                                     observer=lambda s, p, l: ref_losses.append(l))
+    assert len(losses) == len(ref_losses)
+    assert rel(losses, ref_losses) <= 1e-4
+    got = pkg.separate(h, "e")[1]
+    tol = 1e-4 if optimizer == "sgd" else 3e-4
+    for pid, v in ref_params.items():
+        assert rel(got[pid], v) <= tol, (pid, rel(got[pid], v))
+    bad = dict(splits, train_x=splits["train_x"].copy())
+    bad["train_x"][5, 2] = vocab
+    ds_bad = store.from_splits(bad)
+    job2 = pkg.TrainingJob("b", graph, ds_bad.content_hash, pkg.HyperParams(1, 16, lr, optimizer, (), 3), 0, 0)
+    with pytest.raises(ValueError):
+        pkg.Trainer(pkg.merge([job2]), pkg.make_plan("fcfs", [job2]), [job2], {"b": ds_bad}).run()
+
+
+def test_embedding_op_kind_matches_oracle_bit_exact(pkg):
+    """OP_KINDS["embedding-lookup"] through the device kernels: rows gathered exactly, and the table
+    gradient bit-identical to np.add.at (src/ops.py:274-278) incl. repeated tokens."""
+    g = oracle.keyed_generator("embed-op")
+    x = g.integers(0, 9, (5, 11)).astype(np.float32)
+    x[:, 3] = 2.0
+    table = g.normal(size=(9, 70)).astype(np.float32)
+    dy = g.normal(size=(5, 11, 70)).astype(np.float32)
+    attrs = {"vocab": 9, "dim": 70}
+    kind = pkg.OP_KINDS["embedding-lookup"]
+    y, aux = kind.forward(x, {"table": table}, attrs)
+    y_ref, saved = oracle.op_forward("embedding-lookup", x, {"table": table}, attrs)
+    assert np.array_equal(y, y_ref)
+    dx, dp = kind.backward(dy, aux, {"table": table}, attrs)
+    dx_ref, dp_ref = oracle.op_backward("embedding-lookup", dy, saved, {"table": table}, attrs)
+    assert dx is None and dx_ref is None
+    assert np.array_equal(dp["table"], dp_ref["table"])
+    with pytest.raises(ValueError):
+        kind.forward(x + 0.5, {"table": table}, attrs)
