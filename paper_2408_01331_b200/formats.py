@@ -1,8 +1,11 @@
-"""UNND v1 dataset container (src/formats.py:27-120).
+"""UNND containers (src/formats.py): v1 datasets and v2 packaged models.
 
-Only the dataset flavour is needed on the hot path: its sha256 is the
-content hash that keys every epoch's shuffle (src/store.py:74-76), so the
-encoding must be byte-identical to the reference's.
+The dataset flavour is on the hot path: its sha256 is the content hash that
+keys every epoch's shuffle (src/store.py:74-76).  The model flavour is what
+``package`` writes from separated parameters (src/separate.py:39-72,
+src/formats.py:157-181).  Both must be byte-identical to the reference's:
+little-endian, a canonical JSON header (sorted keys, no whitespace) for
+models, then float32 sections ``name(u8 len) rank(u8) dims(u32...) data``.
 """
 from __future__ import annotations
 
@@ -12,8 +15,11 @@ import numpy as np
 
 from .errors import FormatError
 
+import json
+
 MAGIC = b"UNND"
 VERSION_DATASET = 1
+VERSION_MODEL = 2
 DATASET_SECTIONS = ("train_x", "train_y", "test_x", "test_y")
 
 
@@ -82,3 +88,62 @@ def decode_dataset(blob: bytes) -> dict:
         if not xs or not ys or xs[0] != ys[0]:
             raise FormatError(f"{split} split rows disagree: x {xs}, y {ys}")
     return out
+
+
+# --------------------------------------------------------------------------- models (v2)
+
+
+def canonical_json(obj) -> bytes:
+    """Sorted keys, no whitespace: identical content, identical bytes (src/formats.py:36-37)."""
+    return json.dumps(obj, sort_keys=True, separators=(",", ":")).encode("utf-8")
+
+
+def encode_model(header: dict, params: dict, order: list) -> bytes:
+    """magic, u16 version 2, u32 header length, canonical JSON header, u16 section count, the
+    parameter sections in ``order`` (src/formats.py:157-170)."""
+    if sorted(order) != sorted(params):
+        raise FormatError("parameter order does not cover the parameter set")
+    head = canonical_json(header)
+    parts = [MAGIC, struct.pack("<H", VERSION_MODEL), struct.pack("<I", len(head)), head,
+             struct.pack("<H", len(order))]
+    parts += [_section(pid, params[pid]) for pid in order]
+    return b"".join(parts)
+
+
+def _reader(blob: bytes, version: int):
+    view = memoryview(blob)
+    pos = [0]
+
+    def take(n):
+        if pos[0] + n > len(view):
+            raise FormatError("truncated container")
+        chunk = bytes(view[pos[0]:pos[0] + n])
+        pos[0] += n
+        return chunk
+
+    if take(4) != MAGIC:
+        raise FormatError("bad magic: not a container file")
+    (got,) = struct.unpack("<H", take(2))
+    if got != version:
+        raise FormatError(f"expected format version {version}, got {got}")
+    return take
+
+
+def decode_model(blob: bytes) -> tuple:
+    """Inverse of encode_model; checks the header's declared parameter count (src/formats.py:173-181)."""
+    take = _reader(blob, VERSION_MODEL)
+    (hlen,) = struct.unpack("<I", take(4))
+    header = json.loads(take(hlen).decode("utf-8"))
+    (count,) = struct.unpack("<H", take(2))
+    sections = {}
+    for _ in range(count):
+        name = take(take(1)[0]).decode("utf-8")
+        rank = take(1)[0]
+        shape = tuple(struct.unpack("<I", take(4))[0] for _ in range(rank))
+        n = int(np.prod(shape)) if shape else 1
+        sections[name] = np.frombuffer(take(4 * n), dtype="<f4").reshape(shape).astype(np.float32)
+    declared = header.get("param_count")
+    actual = sum(int(a.size) for a in sections.values())
+    if declared is not None and declared != actual:
+        raise FormatError(f"header says {declared} parameters, file holds {actual}")
+    return header, sections

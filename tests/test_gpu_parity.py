@@ -313,6 +313,9 @@ def test_separation_layout_and_roundtrip(pkg):
             assert params[pid].shape == shape and params[pid].dtype == np.float32
             assert params[pid].flags["C_CONTIGUOUS"]
             assert np.array_equal(params[pid], init[pid])
+        blob = pkg.package(graph, params)  # UNND v2 file of the device-resident model
+        g2, p2 = pkg.load_package(blob)
+        assert g2.to_dict() == job.graph.to_dict() and all(np.array_equal(p2[k], params[k]) for k in params)
         params[next(iter(params))][...] = 7.0
         assert not np.array_equal(pkg.separate(h, job.job_id)[1][next(iter(params))], params[next(iter(params))])
     with pytest.raises(pkg.UnknownJobError):

@@ -6,7 +6,7 @@ import numpy as np
 import pytest
 
 import oracle
-from conftest import REPO, load_case
+from conftest import GOLDEN, REPO, load_case
 
 import paper_2408_01331_b200 as h
 from paper_2408_01331_b200 import _native, store, zoo
@@ -137,3 +137,27 @@ def test_schedule_rows_follow_reference_batches_and_adam_steps():
     # milestone 2 (one-based) decays from zero-based epoch 1 on (src/optim.py:22-30)
     assert np.all(rows["lr"][:3, 0] == np.float32(0.1)) and np.all(rows["lr"][3:, 0] == np.float32(0.1 * 0.1))
     assert rows["bias1"][0, 0] == np.float32(1.0 - 0.9) and rows["bias2"][4, 0] == np.float32(1.0 - 0.999 ** 5)
+
+
+@pytest.mark.parametrize("tag", ["mlp", "conv"])
+def test_package_is_byte_identical_to_reference(tag):
+    """package() writes the reference's UNND v2 bytes (src/separate.py:39-59) for the same graph and
+    keyed init; load_package() round-trips them (fixtures: tests/golden/make_package_golden.py)."""
+    from paper_2408_01331_b200 import init_params, load_package, package, zoo
+
+    spec = {"mlp": ("pkg-mlp", (12,), [("fc1", "dense", {"units": 6}), ("act", "relu", {}),
+                                       ("fc2", "dense", {"units": 3})]),
+            "conv": ("pkg-conv", (2, 6, 6), [("conv", "conv2d", {"filters": 3, "kernel": 3, "padding": 1}),
+                                             ("act", "relu", {}), ("pool", "maxpool2d", {"kernel": 2}),
+                                             ("flat", "flatten", {}), ("fc", "dense", {"units": 4})])}[tag]
+    graph = zoo._seq(*spec)
+    golden = (GOLDEN / f"package_{tag}.bin").read_bytes()
+    assert package(graph, init_params(graph, 7)) == golden
+    g2, params = load_package(golden)
+    assert g2.to_dict() == graph.to_dict()
+    for pid, v in init_params(graph, 7).items():
+        assert np.array_equal(params[pid], v)
+    bad = dict(init_params(graph, 7))
+    bad.pop(next(iter(bad)))
+    with pytest.raises(Exception):
+        package(graph, bad)
