@@ -161,8 +161,9 @@ typedef struct hnn_gemm_problem {
    *               c_mode 1 a non-NULL mask (same NCHW layout) multiplies by (mask > 0) and a NULL
    *               bias adds nothing (a conv input gradient computed as a forward conv of dy);
    *   ksplit      WGRAD fixed K split count (>= 1): split s covers K rows [s*ksplit_len,
-   *               (s+1)*ksplit_len) and writes rows [s*m, (s+1)*m) of c (the TMA map covers
-   *               ksplit*m rows); the splits are summed in order by hnn_gemm_ksplit_reduce. */
+   *               (s+1)*ksplit_len) and writes rows [s*mp, s*mp + m) of c, mp = m rounded up
+   *               to 32 (the TMA map covers ksplit*mp rows); the splits are summed in order by
+   *               hnn_conv_tc_aux(HNN_CONVTC_WGRAD_REDUCE). */
   int32_t row_mult;
   int32_t c_mode;
   int32_t ksplit;
@@ -312,12 +313,13 @@ int hnn_multi_tensor_adam(const hnn_opt_segment* segs, int nseg, int total_chunk
  * reference functions as hnn_grouped_conv (ops.py:91-130) for layers with C*k*k, F >= 64.
  *   HNN_CONVTC_IM2COL        cols[m, kk] = x[b, c, oh*s-p+r, ow*s-p+s'], m = (b, oh, ow), kk = (c, r, s');
  *                            rows are kkp wide (pad columns zero)
- *   HNN_CONVTC_TRANSPOSE_DY  dyt[m, f] = dy[b, f, oh, ow]; bpart[b, f] = sum_hw dy[b, f, hw]
+ *   HNN_CONVTC_TRANSPOSE_DY  dyt[m, f] = dy[b, f, oh, ow] (rows padded to 16 bytes); bpart[b, f] = sum_hw dy[b, f, hw]
  *   HNN_CONVTC_COL2IM        dx[b, c, h, w] = (mask > 0) * sum_(r, s') dcols[m, kk] (gather, tap order)
  *   HNN_CONVTC_WGRAD_REDUCE  dw[f, kk] = sum_s partial[s][f][kk] (splits in order); db[f] = sum_b bpart[b, f]
  * Each problem covers `blocks` CTAs starting at block_base: im2col one per (32 output pixels, 32
  * channels), transpose one per (sample, 32 pixels, 32 filters), col2im one per (sample, input row,
- * 32 columns, 16 channels), reduce any count (grid-stride).  max_k = largest kernel size (<= 3).
+ * 32 columns, 16 channels), reduce any count (grid-stride).  max_k = largest kernel size (<= 5;
+ * col2im <= 3).
  */
 #define HNN_CONVTC_IM2COL 0
 #define HNN_CONVTC_TRANSPOSE_DY 1
@@ -336,7 +338,7 @@ typedef struct hnn_convtc_problem {
   const float* dcols;/* [cap*oh*ow, kk] */
   float* dx;         /* [cap, c, h, w] */
   const float* mask; /* [cap, c, h, w] or NULL */
-  const float* partial; /* [ksplit, f, kk] */
+  const float* partial; /* [ksplit, round_up(f, 32), kkp] */
   float* dw;         /* [f, kk] */
   float* db;         /* [f] */
   float* bpart;      /* [cap, f] */

@@ -116,11 +116,12 @@ __global__ void __launch_bounds__(CT_THREADS) transpose_dy_kernel(const hnn_conv
           __float2bfloat16_rn(tile[j][tx]);
   }
   __syncthreads();
+  const int fld = p.bf16 ? (p.f + 7) & ~7 : (p.f + 3) & ~3;  // dyt rows padded to 16 bytes (TMA)
   if (p.dyt)
     for (int j = ty; j < 32; j += 8) {
       const int hw = th * 32 + j, f = tf * 32 + tx;
       if (hw < hw_n && f < p.f) {
-        const size_t o = (size_t(b) * hw_n + hw) * p.f + f;
+        const size_t o = (size_t(b) * hw_n + hw) * fld + f;
         if (p.bf16) reinterpret_cast<__nv_bfloat16*>(p.dyt)[o] = __float2bfloat16_rn(tile[tx][j]);
         else p.dyt[o] = tile[tx][j];
       }
@@ -272,7 +273,8 @@ __global__ void __launch_bounds__(CT_THREADS) wgrad_reduce_kernel(const hnn_conv
   const int rows = cur[p.model].rows;
   const long long kmax = (long long)rows * p.oh * p.ow;
   const int splits = int(min((long long)p.ksplit, (kmax + p.ksplit_len - 1) / p.ksplit_len));
-  const long long total = (long long)p.f * p.kk, ptotal = (long long)p.f * p.kkp;
+  // split s occupies rows [s * fp, s * fp + f) of the partial buffer, fp = f rounded up to 32
+  const long long total = (long long)p.f * p.kk, ptotal = (long long)((p.f + 31) & ~31) * p.kkp;
   for (long long e = (long long)(blockIdx.x - p.block_base) * CT_THREADS + threadIdx.x; e < total + p.f;
        e += (long long)p.blocks * CT_THREADS) {
     if (e < total) {
@@ -347,8 +349,8 @@ extern "C" int hnn_conv_tc_aux(int op, const hnn_convtc_problem* probs, int npro
   cudaStream_t s = hnn::as_stream(stream);
   switch (op) {
     case HNN_CONVTC_IM2COL:
-      HNN_REQUIRE(max_k > 0 && max_k <= 3, "hnn_conv_tc_aux", "kernel size above 3");
-      cudaFuncSetAttribute(hnn::im2col_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, hnn::im2col_smem_bytes(3));
+      HNN_REQUIRE(max_k > 0 && max_k <= 5, "hnn_conv_tc_aux", "kernel size above 5");
+      cudaFuncSetAttribute(hnn::im2col_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, hnn::im2col_smem_bytes(5));
       hnn::im2col_kernel<<<total_blocks, hnn::CT_THREADS, hnn::im2col_smem_bytes(max_k), s>>>(probs, nprob, cur, status);
       break;
     case HNN_CONVTC_TRANSPOSE_DY:

@@ -481,8 +481,10 @@ extern "C" int hnn_gemm_tc_encode(int op, const hnn_gemm_problem* host_probs, in
     }
     // C (all ops): row-major [m, n] with row stride ldc; 32x32 boxes, 128-byte swizzle
     // (a K-split WGRAD writes ksplit stacked [m, n] partials)
-    const uint64_t crows = uint64_t(p.m) * uint64_t(op == HNN_WGRAD && p.ksplit > 1 ? p.ksplit : 1);
-    if (!rc && p.c) rc = hnn::encode_2d(&maps[3 * i + 2], p.c, p.n, crows, p.ldc, 32, false);
+    const uint64_t crows = (op == HNN_WGRAD && p.ksplit > 1) ? uint64_t((p.m + 31) & ~31) * uint64_t(p.ksplit)
+                                                             : uint64_t(p.m);
+    if (!rc && p.c && p.c_mode == 0)  // (c_mode 1 stores NCHW directly, no map)
+      rc = hnn::encode_2d(&maps[3 * i + 2], p.c, p.n, crows, p.ldc, 32, false);
     if (rc) {
       hnn::set_error("hnn_gemm_tc_encode", "cuTensorMapEncodeTiled failed (alignment / stride / driver)");
       return rc;
@@ -500,8 +502,10 @@ extern "C" int hnn_gemm_bf16_encode(int op, const hnn_gemm_problem* host_probs, 
     const uint32_t brows = p.tile_n > 0 ? uint32_t(p.tile_n / 2) : 128u;
     int rc = hnn::encode_2d_bf16(&maps[3 * i], p.a, p.k, p.m, p.lda, hnn::TC_BM);
     if (!rc) rc = hnn::encode_2d_bf16(&maps[3 * i + 1], p.b, p.k, p.n, p.ldb, brows);
-    const uint64_t crows = uint64_t(p.m) * uint64_t(op == HNN_WGRAD && p.ksplit > 1 ? p.ksplit : 1);
-    if (!rc && p.c) rc = hnn::encode_2d(&maps[3 * i + 2], p.c, p.n, crows, p.ldc, 32, false);
+    const uint64_t crows = (op == HNN_WGRAD && p.ksplit > 1) ? uint64_t((p.m + 31) & ~31) * uint64_t(p.ksplit)
+                                                             : uint64_t(p.m);
+    if (!rc && p.c && p.c_mode == 0)  // (c_mode 1 stores NCHW directly, no map)
+      rc = hnn::encode_2d(&maps[3 * i + 2], p.c, p.n, crows, p.ldc, 32, false);
     if (rc) {
       hnn::set_error("hnn_gemm_bf16_encode", "cuTensorMapEncodeTiled failed (alignment / stride / driver)");
       return rc;

@@ -446,7 +446,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC2_THREADS, 1)
         if (cptr != nullptr) {
           asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
           __syncwarp();
-          if (lane == 0) tma_store_2d(tmap_c, stg, nh + cb, row0 + sp * pm);  // split sp: rows sp*m..
+          if (lane == 0) tma_store_2d(tmap_c, stg, nh + cb, row0 + sp * ((pm + 31) & ~31));  // split sp's rows
           ++nstore;
         }
       }

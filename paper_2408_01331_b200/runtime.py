@@ -98,6 +98,7 @@ class Stage:
     colst = None
     dyk = None
     wt = None
+    fld: int = 0
 
 
 def lower_graph(graph) -> tuple:
@@ -286,6 +287,8 @@ class DeviceHybrid:
         # operands, fp32 accumulation and fp32 master weights (BASELINE C4)
         self.conv_bf16 = conv_precision == "bf16"
         # CTA-pair tcgen05 GEMM (HNN_TC_PAIR=0: single-CTA kernel)
+        # conv layers with at least this many filters use the tensor-core conv path
+        self.tc_conv_min_f = int(os.environ.get("HNN_TC_CONV_MIN_F", "64"))
         self.use_pairs = os.environ.get("HNN_TC_PAIR", "1") != "0"
         off = 0
         for s in slots:
@@ -366,8 +369,10 @@ class DeviceHybrid:
                     # C*k*k and F >= 64 go to the tensor cores (im2col + CTA-pair 3xTF32 GEMM)
                     st.direct = N.conv_direct_ok(c, h, w, f, k, oh, ow)
                     kk = c * k * k
-                    st.tc = (not st.direct and self.use_tc and self.use_pairs and kk >= 16
-                             and f >= 64 and f % 4 == 0 and k <= 3 and st.attrs.get("stride", 1) <= 2)
+                    stride = st.attrs.get("stride", 1)
+                    st.tc = (self.use_tc and self.use_pairs and kk >= 16 and f >= self.tc_conv_min_f
+                             and (k <= 3 or (k <= 5 and stride == 1)) and stride <= 2
+                             and (not st.direct or self.tc_conv_min_f < 64))
                     if st.tc:
                         pix = cap * oh * ow
                         st.bf16 = self.conv_bf16
@@ -385,15 +390,17 @@ class DeviceHybrid:
                         st.pix_ld = -(-pix // 8) * 8
                         st.cols = torch.zeros(pix * kk, dtype=wdt, device=dev)
                         st.bpart = torch.zeros(cap * f, dtype=torch.float32, device=dev)
-                        st.partial = torch.zeros(st.ksplit * f * kk, dtype=torch.float32, device=dev)
+                        st.partial = torch.zeros(st.ksplit * (-(-f // 32) * 32) * kk, dtype=torch.float32,
+                                                 device=dev)
                         if st.bf16:  # pixel-contiguous (K-major) weight-gradient operands
                             st.colst = torch.zeros(kk * st.pix_ld, dtype=wdt, device=dev)
                             st.dyk = torch.zeros(f * st.pix_ld, dtype=wdt, device=dev)
                         # input gradient: stride 1 -> a forward conv of dy (im2col of dy, flipped
                         # weights; scratch [cap*H*W, F*k*k]); stride 2 -> dcols GEMM + col2im
                         st.dg_fwd = st.attrs.get("stride", 1) == 1 and (f * k * k) % 8 == 0
+                        st.fld = -(-f // 8) * 8 if st.bf16 else _align4(f)  # dyt rows: 16 bytes
                         if not st.bf16 or (st.needs_dx and not st.dg_fwd):
-                            st.dyt = torch.zeros(pix * f, dtype=wdt, device=dev)
+                            st.dyt = torch.zeros(pix * st.fld, dtype=wdt, device=dev)
                         if st.needs_dx and st.dg_fwd:
                             st.wflip = torch.zeros(c * f * k * k, dtype=wdt, device=dev)
                             if st.bf16:
@@ -757,10 +764,11 @@ class DeviceHybrid:
             cols.append((s, N.ConvTcProblem(x=_ptr(st.dy), cols=_ptr(dst), cap=s.batch_size, c=f, h=oh, w=ow,
                                             f=c, k=k, stride=1, pad=k - 1 - p, oh=h, ow=w, kk=kf, kkp=kf,
                                             model=s.index, bf16=int(st.bf16))))
+        max_k = max(st.attrs["kernel"] for _, st in items)
         out.append(self._aux_table(N.CONVTC_FLIP_WEIGHTS, flips, f"{label}/tc/flipw",
-                                   lambda pr: grid(pr.c * pr.f * pr.k * pr.k), 3))
+                                   lambda pr: grid(pr.c * pr.f * pr.k * pr.k), max_k))
         out.append(self._aux_table(N.CONVTC_IM2COL, cols, f"{label}/tc/im2col_dy",
-                                   lambda pr: -(-(pr.cap * pr.oh * pr.ow) // 32) * -(-pr.c // 32), 3))
+                                   lambda pr: -(-(pr.cap * pr.oh * pr.ow) // 32) * -(-pr.c // 32), max_k))
         by_prec = {}
         for s, st in items:
             c, h, w = st.in_shape
@@ -851,7 +859,7 @@ class DeviceHybrid:
                     d = dict(a=_ptr(st.dyt), b=weight(s, st), ldb=kk)
                 rows.setdefault(prec(st), []).append(
                     (s, dict(d, c=_ptr(s.dcols), bias=0, mask=0, dbias=0, m=s.batch_size * oh * ow, n=kk, k=f,
-                             lda=f, ldc=kk, relu=0, row_mult=oh * ow)))
+                             lda=st.fld, ldc=kk, relu=0, row_mult=oh * ow)))
             out += gemms(N.HNN_DGRAD, rows, f"{label}/tc")
             out.append(self._convtc_aux(N.CONVTC_COL2IM, items, f"{label}/tc/col2im",
                                         lambda s, st: (s.batch_size * geo(st)[1] * -(-geo(st)[2] // 32)
@@ -867,7 +875,7 @@ class DeviceHybrid:
             if st.bf16:  # A = dy [f, pixels], B = cols^T [kkp, pixels]: both pixel-contiguous
                 d = dict(a=_ptr(st.dyk), b=_ptr(st.colst), lda=st.pix_ld, ldb=st.pix_ld)
             else:
-                d = dict(a=_ptr(st.dyt), b=_ptr(st.cols), lda=f, ldb=kk)
+                d = dict(a=_ptr(st.dyt), b=_ptr(st.cols), lda=st.fld, ldb=kk)
             rows.setdefault(prec(st), []).append(
                 (s, dict(d, c=_ptr(st.partial), bias=0, mask=0, dbias=0, m=f, n=kk, k=s.batch_size * oh * ow,
                          ldc=kk, relu=0, row_mult=oh * ow, ksplit=st.ksplit, ksplit_len=st.ksplit_len)))
