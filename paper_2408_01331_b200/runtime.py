@@ -1039,11 +1039,35 @@ class DeviceHybrid:
                 out.append((off, cnt))
         return out
 
+    def _optimizer_order(self):
+        """(slot, offset, count) ranges in the order the multi-tensor kernel walks them: grouped by
+        stage, first stage first.  Backward runs the stages in reverse, so the first stage's
+        gradients were written last and are still in L2 when the optimizer starts."""
+        items = []
+        for s in self.slots:
+            ranges = self._unfused_ranges(s)
+            if len(ranges) == 1 and ranges[0] == (s.seg_off, s.seg_len):  # split by stage
+                ranges = []
+                for st in s.stages:
+                    if not st.params:
+                        continue
+                    offs = [s.offsets[pid] for pid in st.params]
+                    end = max(s.offsets[pid] + _align4(int(np.prod(s.specs[pid]))) for pid in st.params)
+                    ranges.append((min(offs), end - min(offs)))
+            for r in ranges:
+                stage = next((k for k, st in enumerate(s.stages) for pid in st.params
+                              if s.offsets[pid] <= r[0] < s.offsets[pid] + _align4(int(np.prod(s.specs[pid])))), 0)
+                items.append((stage, s.index, s, r[0], r[1]))
+        items.sort(key=lambda t: (t[0], t[1]))
+        covered = sum(t[4] for t in items)
+        assert covered == sum(c for s in self.slots for _, c in self._unfused_ranges(s)), "optimizer ranges"
+        return [(t[2], t[3], t[4]) for t in items]
+
     def _optimizer_launch(self):
         segs, base = [], 0
-        for s in self.slots:
+        for s, off, cnt in self._optimizer_order():
             kind = s.opt_kind
-            for off, cnt in self._unfused_ranges(s):
+            if True:
                 chunks = -(-cnt // OPT_CHUNK)
                 segs.append(N.OptSegment(
                     _ptr(self.params) + 4 * off, _ptr(self.grads) + 4 * off,
