@@ -313,9 +313,10 @@ int hnn_multi_tensor_adam(const hnn_opt_segment* segs, int nseg, int total_chunk
  * reference functions as hnn_grouped_conv (ops.py:91-130) for layers with C*k*k, F >= 64.
  *   HNN_CONVTC_IM2COL        cols[m, kk] = x[b, c, oh*s-p+r, ow*s-p+s'], m = (b, oh, ow), kk = (c, r, s');
  *                            rows are kkp wide (pad columns zero)
- *   HNN_CONVTC_TRANSPOSE_DY  dyt[m, f] = dy[b, f, oh, ow] (rows padded to 16 bytes); bpart[b, f] = sum_hw dy[b, f, hw]
+ *   HNN_CONVTC_TRANSPOSE_DY  dyt[m, f] = dy[b, f, oh, ow] (rows padded to 16 bytes); bpart[b, t, f] = sum of dy[b, f, hw]
+ *                            over pixel tile t (32 pixels)
  *   HNN_CONVTC_COL2IM        dx[b, c, h, w] = (mask > 0) * sum_(r, s') dcols[m, kk] (gather, tap order)
- *   HNN_CONVTC_WGRAD_REDUCE  dw[f, kk] = sum_s partial[s][f][kk] (splits in order); db[f] = sum_b bpart[b, f]
+ *   HNN_CONVTC_WGRAD_REDUCE  dw[f, kk] = sum_s partial[s][f][kk] (splits in order); db[f] = sum over (b, t) of bpart[b, t, f]
  * Each problem covers `blocks` CTAs starting at block_base: im2col one per (32 output pixels, 32
  * channels), transpose one per (sample, 32 pixels, 32 filters), col2im one per (sample, input row,
  * 32 columns, 16 channels), reduce any count (grid-stride).  max_k = largest kernel size (<= 5;
@@ -341,7 +342,7 @@ typedef struct hnn_convtc_problem {
   const float* partial; /* [ksplit, round_up(f, 32), kkp] */
   float* dw;         /* [f, kk] */
   float* db;         /* [f] */
-  float* bpart;      /* [cap, f] */
+  float* bpart;      /* [cap, ceil(oh*ow/32), f] */
   const float* weight; /* [f, kk] (HNN_CONVTC_PAD_WEIGHTS) */
   float* wpad;       /* [f, kkp] */
   int32_t cap, c, h, w, f, k, stride, pad, oh, ow, kk;

@@ -93,7 +93,7 @@ __global__ void __launch_bounds__(CT_THREADS) im2col_kernel(const hnn_convtc_pro
 int im2col_smem_bytes(int k) { return IC_PIX * (IC_CH * k * k + 1) * 4; }
 
 // dyT[m, f] = dy[b, f, hw] (m = b*HW + hw) through a 32 x 32 shared-memory tile per (b, hw, f)
-// block; bpart[b, f] = sum over hw of dy[b, f, hw] (sequential, for the bias gradient).
+// block; bpart[b, th, f] = sum over the tile's 32 pixels of dy[b, f, hw] (bias gradient partials).
 __global__ void __launch_bounds__(CT_THREADS) transpose_dy_kernel(const hnn_convtc_problem* __restrict__ probs,
                                                                  int nprob, const hnn_step_row* __restrict__ cur,
                                                                  const hnn_model_status* __restrict__ status) {
@@ -126,13 +126,16 @@ __global__ void __launch_bounds__(CT_THREADS) transpose_dy_kernel(const hnn_conv
         else p.dyt[o] = tile[tx][j];
       }
     }
-  if (th == 0 && ty == 0) {  // one warp per (b, 32 filters): sequential sum over hw
+  // bias partial of this tile: bpart[b, th, f] = sum over the tile's 32 pixels of dy[b, f, hw]
+  // (fixed order; the reduce adds the tiles in (b, th) order).  A per-(b, f) sequential sum over all
+  // HW pixels was a 1024-long dependent chain per thread (0.1-0.16 ms per C4 layer).
+  if (ty == 0) {
     const int f = tf * 32 + tx;
     if (f < p.f) {
-      const float* src = p.dy + (size_t(b) * p.f + f) * hw_n;
-      float acc = -0.0f;
-      for (int hw = 0; hw < hw_n; ++hw) acc = __fadd_rn(acc, __ldg(src + hw));
-      p.bpart[size_t(b) * p.f + f] = acc;
+      float acc = 0.0f;
+#pragma unroll 8
+      for (int j = 0; j < 32; ++j) acc = __fadd_rn(acc, tile[tx][j]);  // pixels th*32 + j (0 past HW)
+      p.bpart[(size_t(b) * tiles_hw + th) * p.f + f] = acc;
     }
   }
 }
@@ -264,7 +267,7 @@ __global__ void __launch_bounds__(CT_THREADS) col2im_kernel(const hnn_convtc_pro
 int col2im_smem_bytes(int k) { return k * CI_OWMAX * (CI_CH * k * k + 1) * 4; }
 
 // dW[f, kk] = sum over the valid splits (in order) of partial[s*F + f, kk];
-// db[f] = sum over batch rows (in order) of bpart[b, f].
+// db[f] = sum over (batch row, pixel tile) in order of bpart[b, tile, f].
 __global__ void __launch_bounds__(CT_THREADS) wgrad_reduce_kernel(const hnn_convtc_problem* __restrict__ probs,
                                                                  int nprob, const hnn_step_row* __restrict__ cur,
                                                                  const hnn_model_status* __restrict__ status) {
@@ -275,21 +278,27 @@ __global__ void __launch_bounds__(CT_THREADS) wgrad_reduce_kernel(const hnn_conv
   const int splits = int(min((long long)p.ksplit, (kmax + p.ksplit_len - 1) / p.ksplit_len));
   // split s occupies rows [s * fp, s * fp + f) of the partial buffer, fp = f rounded up to 32
   const long long total = (long long)p.f * p.kk, ptotal = (long long)((p.f + 31) & ~31) * p.kkp;
-  for (long long e = (long long)(blockIdx.x - p.block_base) * CT_THREADS + threadIdx.x; e < total + p.f;
-       e += (long long)p.blocks * CT_THREADS) {
-    if (e < total) {
-      const long long f = e / p.kk, pe = f * p.kkp + (e - f * p.kk);  // partial rows are kkp wide
-      float acc = 0.0f;
-      for (int s = 0; s < splits; ++s) acc = __fadd_rn(acc, __ldg(p.partial + size_t(s) * ptotal + pe));
-      p.dw[e] = acc;
-    } else {
-      const int f = int(e - total);
-      float acc = 0.0f;
-      for (int b = 0; b < rows; ++b) acc = __fadd_rn(acc, __ldg(p.bpart + size_t(b) * p.f + f));
-      p.db[f] = acc;
-    }
+  const long long tid = (long long)(blockIdx.x - p.block_base) * CT_THREADS + threadIdx.x;
+  for (long long e = tid; e < total; e += (long long)p.blocks * CT_THREADS) {
+    const long long f = e / p.kk, pe = f * p.kkp + (e - f * p.kk);  // partial rows are kkp wide
+    float acc = 0.0f;
+    for (int s = 0; s < splits; ++s) acc = __fadd_rn(acc, __ldg(p.partial + size_t(s) * ptotal + pe));
+    p.dw[e] = acc;
+  }
+  // bias: one warp per filter; lane l sums the (batch row, pixel tile) partials l, l+32, ... in
+  // order, then a fixed xor tree combines the lanes
+  const int lane = threadIdx.x % 32;
+  const long long warp = tid / 32, nwarps = (long long)p.blocks * CT_THREADS / 32;
+  const int nq = rows * ((p.oh * p.ow + 31) / 32);
+  for (long long f = warp; f < p.f; f += nwarps) {
+    float acc = 0.0f;
+    for (int q = lane; q < nq; q += 32) acc = __fadd_rn(acc, __ldg(p.bpart + size_t(q) * p.f + f));
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) acc = __fadd_rn(acc, __shfl_xor_sync(0xffffffffu, acc, o));
+    if (lane == 0) p.db[f] = acc;
   }
 }
+
 
 // wpad[f, kk'] = w[f, kk] for kk < K, 0 for the pad columns (GEMM B operand with 16-byte rows).
 __global__ void __launch_bounds__(CT_THREADS) pad_weights_kernel(const hnn_convtc_problem* __restrict__ probs, int nprob,

@@ -389,7 +389,7 @@ class DeviceHybrid:
                         st.ksplit = -(-pix // st.ksplit_len)
                         st.pix_ld = -(-pix // 8) * 8
                         st.cols = torch.zeros(pix * kk, dtype=wdt, device=dev)
-                        st.bpart = torch.zeros(cap * f, dtype=torch.float32, device=dev)
+                        st.bpart = torch.zeros(cap * -(-(oh * ow) // 32) * f, dtype=torch.float32, device=dev)
                         st.partial = torch.zeros(st.ksplit * (-(-f // 32) * 32) * kk, dtype=torch.float32,
                                                  device=dev)
                         if st.bf16:  # pixel-contiguous (K-major) weight-gradient operands
