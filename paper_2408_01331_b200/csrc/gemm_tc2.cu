@@ -36,8 +36,11 @@ constexpr int TC2_BM = 128;                // rows per CTA (pair tile: 256)
 constexpr int TC2_BN = 256;                // pair tile columns (each CTA stages 128 of B)
 constexpr int TC2_BK = 32;
 constexpr int TC2_STAGES = 3;  // each stage: raw A | raw B | lo A | lo B (64 KB)
-constexpr int TC2_THREADS = 384;
-constexpr int TC2_CONV_WARPS = 2;
+#ifndef HNN_TC2_CONV_WARPS
+#define HNN_TC2_CONV_WARPS 2
+#endif
+constexpr int TC2_CONV_WARPS = HNN_TC2_CONV_WARPS;
+constexpr int TC2_THREADS = 64 + 32 * TC2_CONV_WARPS + 256;
 constexpr int TC2_CHUNK_KB = 4;
 constexpr int TC2_A_BYTES = TC2_BM * TC2_BK * 4;        // 16 KB
 constexpr int TC2_B_BYTES = (TC2_BN / 2) * TC2_BK * 4;  // 16 KB (this CTA's half)

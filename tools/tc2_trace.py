@@ -15,7 +15,8 @@ import torch
 import bench
 
 torch.cuda.set_device(0)
-jobs, hy, dev, ddev, meta, ds, comm = bench.build_rank("c3", 0, 1, torch.device("cuda", 0))
+wl = sys.argv[2] if len(sys.argv) > 2 else "c3"
+jobs, hy, dev, ddev, meta, ds, comm = bench.build_rank(wl, 0, 1, torch.device("cuda", 0))
 rows = bench.schedule(jobs, meta, 200)
 bench.upload_perms(dev, jobs, meta)
 dev.load_schedule(rows)
@@ -26,7 +27,7 @@ fn = lib.hnn_debug_tc2_trace
 fn.argtypes = [C.c_void_p, C.c_int]
 st = torch.cuda.current_stream().cuda_stream
 for launch in dev.train_plan:
-    if not launch.label.endswith("/tc2"):
+    if not launch.label.endswith(("/tc2", "/bf16")):
         continue
     fn(buf.ctypes.data, 1)
     reps = 5
