@@ -228,7 +228,7 @@ int hnn_grouped_conv(int op, const hnn_conv_problem* probs, int nprob, int total
  * hnn_conv_wgrad_reduce).  tile_base counts CTAs; `smem` = max over the launch's problems of
  * hnn_conv_direct_smem(op, ...).
  */
-#define HNN_CONV_DIRECT_BCHUNK 4
+#define HNN_CONV_DIRECT_BCHUNK 1
 int hnn_conv_direct_smem(int op, int c, int h, int w, int f, int k, int oh, int ow);
 int hnn_grouped_conv_direct(int op, const hnn_conv_problem* probs, int nprob, int total_blocks, int smem,
                             const hnn_step_row* cur, const hnn_model_status* status, void* stream);

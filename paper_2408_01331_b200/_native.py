@@ -18,7 +18,7 @@ PREC_SIMT, PREC_3XTF32, PREC_SIMT_SKINNY, PREC_3XTF32_PAIR, PREC_BF16_PAIR = 0, 
 CONVTC_IM2COL, CONVTC_TRANSPOSE_DY, CONVTC_COL2IM, CONVTC_WGRAD_REDUCE, CONVTC_PAD_WEIGHTS = 0, 1, 2, 3, 4
 CONVTC_FLIP_WEIGHTS, CONVTC_WT_WEIGHTS = 5, 6
 OPT_SGD, OPT_SGD_MOMENTUM, OPT_ADAM = 0, 1, 2
-CONV_DIRECT_BCHUNK = 4
+CONV_DIRECT_BCHUNK = 1
 
 P = C.c_uint64  # device pointers travel as integers
 I = C.c_int32

@@ -230,6 +230,160 @@ __device__ __forceinline__ void stage(float* dst, const float* __restrict__ src,
   for (int i = threadIdx.x; i < n; i += blockDim.x) dst[i] = __ldg(src + i);
 }
 
+// Register-blocked stride-1 paths (LeNet-class layers): a thread computes 4 consecutive outputs of
+// one row, so each staged input row segment (4 + K - 1 values) and each weight are loaded from
+// shared memory once for 4 * K FMAs (the one-output-per-thread loop issued 2 shared loads per
+// FMA and was bound by the 1-wavefront/clock shared-memory pipe).
+constexpr int RB = 4;
+
+template <int K>
+__device__ __forceinline__ void direct_fwd_blocked(const hnn_conv_problem& p, const ConvGeom& g, const float* xs,
+                                                   const float* ws, float* yb) {
+  const int qblocks = (g.ow + RB - 1) / RB;
+  for (int e = threadIdx.x; e < g.f * g.oh * qblocks; e += blockDim.x) {
+    const int f = e / (g.oh * qblocks), rq = e - f * g.oh * qblocks, oy = rq / qblocks, ox0 = (rq - oy * qblocks) * RB;
+    float acc[RB] = {0.0f, 0.0f, 0.0f, 0.0f};
+    const float* wf = ws + f * g.ckk;
+    for (int c = 0; c < g.c; ++c) {
+#pragma unroll
+      for (int i = 0; i < K; ++i) {
+        const int y = oy - g.pad + i;
+        if (y < 0 || y >= g.h) continue;
+        const float* xr = xs + (c * g.h + y) * g.w;
+        float seg[RB + K - 1];
+#pragma unroll
+        for (int t = 0; t < RB + K - 1; ++t) {
+          const int x = ox0 - g.pad + t;
+          seg[t] = (x >= 0 && x < g.w) ? xr[x] : 0.0f;
+        }
+        const float* wr = wf + (c * K + i) * K;
+#pragma unroll
+        for (int j = 0; j < K; ++j) {
+          const float w = wr[j];
+#pragma unroll
+          for (int q = 0; q < RB; ++q) acc[q] = fmaf(seg[q + j], w, acc[q]);
+        }
+      }
+    }
+    const float bias = __ldg(p.bias + f);
+#pragma unroll
+    for (int q = 0; q < RB; ++q) {
+      const int ox = ox0 + q;
+      if (ox >= g.ow) break;
+      float v = __fadd_rn(acc[q], bias);
+      if (p.relu) v = np_relu(v);
+      yb[(f * g.oh + oy) * g.ow + ox] = v;
+    }
+  }
+}
+
+template <int K>
+__device__ __forceinline__ void direct_dgrad_blocked(const hnn_conv_problem& p, const ConvGeom& g, const float* ds,
+                                                     const float* ws, float* dxb, const float* mb) {
+  const int qblocks = (g.w + RB - 1) / RB;
+  for (int e = threadIdx.x; e < g.c * g.h * qblocks; e += blockDim.x) {
+    const int c = e / (g.h * qblocks), rq = e - c * g.h * qblocks, y = rq / qblocks, x0 = (rq - y * qblocks) * RB;
+    float acc[RB] = {0.0f, 0.0f, 0.0f, 0.0f};
+    for (int f = 0; f < g.f; ++f) {
+#pragma unroll
+      for (int i = 0; i < K; ++i) {
+        const int oy = y + g.pad - i;
+        if (oy < 0 || oy >= g.oh) continue;
+        const float* dr = ds + (f * g.oh + oy) * g.ow;
+        // dx[x] gets dy[x + pad - j] * w[j]; seg[t] = dy[x0 + pad - (K - 1) + t]
+        float seg[RB + K - 1];
+#pragma unroll
+        for (int t = 0; t < RB + K - 1; ++t) {
+          const int ox = x0 + g.pad - (K - 1) + t;
+          seg[t] = (ox >= 0 && ox < g.ow) ? dr[ox] : 0.0f;
+        }
+        const float* wr = ws + ((f * g.c + c) * K + i) * K;
+#pragma unroll
+        for (int j = 0; j < K; ++j) {
+          const float w = wr[j];
+#pragma unroll
+          for (int q = 0; q < RB; ++q) acc[q] = fmaf(seg[q + K - 1 - j], w, acc[q]);
+        }
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < RB; ++q) {
+      const int x = x0 + q;
+      if (x >= g.w) break;
+      const int o = (c * g.h + y) * g.w + x;
+      dxb[o] = mb ? np_mask(acc[q], mb[o]) : acc[q];
+    }
+  }
+}
+
+// Weight gradient of one staged sample, stride 1: a thread owns (f, c, i) and the K taps j of that
+// filter row, sweeping the output rows of its row group; per 4 outputs it loads 4 dy values and
+// one 4 + K - 1 input segment for 4 * K FMAs.  G row groups (fixed) are combined in order.
+template <int K>
+__device__ __forceinline__ void direct_wgrad_blocked(const hnn_conv_problem& p, const ConvGeom& g, const float* xs,
+                                                     int cs, int rs, const float* ds, int nb, float* red,
+                                                     float* out) {
+  const int nrow = g.f * g.c * K;  // (f, c, i) filter rows
+  const int G = max(1, min(8, int(blockDim.x) / nrow));
+  const int cols = g.ckk + 1;
+  const int qblocks = (g.ow + RB - 1) / RB;
+  for (int t = threadIdx.x; t < nrow * G; t += blockDim.x) {
+    const int grp = t / nrow, rrow = t - grp * nrow;
+    const int f = rrow / (g.c * K), ci = rrow - f * g.c * K, c = ci / K, i = ci - c * K;
+    float acc[K];
+#pragma unroll
+    for (int j = 0; j < K; ++j) acc[j] = 0.0f;
+    for (int sb = 0; sb < nb; ++sb) {
+      const float* df = ds + (sb * g.f + f) * g.ohw;
+      const float* xc = xs + (sb * g.c + c) * cs;
+      for (int oy = grp; oy < g.oh; oy += G) {
+        const int y = oy - g.pad + i;
+        if (y < 0 || y >= g.h) continue;
+        const float* xr = xc + y * rs;
+        const float* dr = df + oy * g.ow;
+        for (int qb = 0; qb < qblocks; ++qb) {
+          const int ox0 = qb * RB;
+          float d[RB], seg[RB + K - 1];
+#pragma unroll
+          for (int q = 0; q < RB; ++q) d[q] = ox0 + q < g.ow ? dr[ox0 + q] : 0.0f;
+#pragma unroll
+          for (int u = 0; u < RB + K - 1; ++u) {
+            const int x = ox0 - g.pad + u;
+            seg[u] = (x >= 0 && x < g.w) ? xr[x] : 0.0f;
+          }
+#pragma unroll
+          for (int j = 0; j < K; ++j)
+#pragma unroll
+            for (int q = 0; q < RB; ++q) acc[j] = fmaf(d[q], seg[q + j], acc[j]);
+        }
+      }
+    }
+    // group 0 -> slot G-1, group g > 0 -> slot g-1 (combined in group order after the barrier)
+    const int slot = grp > 0 ? grp - 1 : G - 1;
+#pragma unroll
+    for (int j = 0; j < K; ++j) red[(slot * nrow + rrow) * K + j] = acc[j];
+  }
+  __syncthreads();
+  for (int rrow = threadIdx.x; rrow < nrow; rrow += blockDim.x) {
+    const int f = rrow / (g.c * K), ci = rrow - f * g.c * K, c = ci / K, i = ci - c * K;
+#pragma unroll
+    for (int j = 0; j < K; ++j) {
+      float a = red[((G - 1) * nrow + rrow) * K + j];  // group 0
+      for (int grp = 1; grp < G; ++grp) a = __fadd_rn(a, red[((grp - 1) * nrow + rrow) * K + j]);
+      out[f * cols + c * K * K + i * K + j] = a;
+    }
+  }
+  // bias gradient: sequential sum of the staged samples' dy per filter
+  for (int f = threadIdx.x; f < g.f; f += blockDim.x) {
+    float a = 0.0f;
+    for (int sb = 0; sb < nb; ++sb) {
+      const float* df = ds + (sb * g.f + f) * g.ohw;
+      for (int u = 0; u < g.ohw; ++u) a = __fadd_rn(a, df[u]);
+    }
+    out[f * cols + g.ckk] = a;
+  }
+}
+
 template <int OP>
 __global__ void __launch_bounds__(DTHREADS) conv_direct_kernel(const hnn_conv_problem* __restrict__ probs, int nprob,
                                                                const hnn_step_row* __restrict__ cur,
@@ -253,6 +407,8 @@ __global__ void __launch_bounds__(DTHREADS) conv_direct_kernel(const hnn_conv_pr
     stage(xs, p.x + size_t(b) * g.c * g.hw, g.c * g.hw);
     stage(ws, p.weight, g.f * g.ckk);
     __syncthreads();
+    if (g.s == 1 && g.k == 5) return direct_fwd_blocked<5>(p, g, xs, ws, yb);
+    if (g.s == 1 && g.k == 3) return direct_fwd_blocked<3>(p, g, xs, ws, yb);
     for (int e = threadIdx.x; e < g.f * g.ohw; e += blockDim.x) {
       const int f = e / g.ohw, opix = e - f * g.ohw;
       const int oy = opix / g.ow, ox = opix - oy * g.ow;
@@ -283,6 +439,8 @@ __global__ void __launch_bounds__(DTHREADS) conv_direct_kernel(const hnn_conv_pr
     stage(ws, p.weight, g.f * g.ckk);
     __syncthreads();
     const float* mb = p.mask ? p.mask + size_t(b) * g.c * g.hw : nullptr;
+    if (g.s == 1 && g.k == 5) return direct_dgrad_blocked<5>(p, g, ds, ws, dxb, mb);
+    if (g.s == 1 && g.k == 3) return direct_dgrad_blocked<3>(p, g, ds, ws, dxb, mb);
     for (int e = threadIdx.x; e < g.c * g.hw; e += blockDim.x) {
       const int c = e / g.hw, pix = e - c * g.hw;
       const int y = pix / g.w, x = pix - y * g.w;
@@ -322,6 +480,13 @@ __global__ void __launch_bounds__(DTHREADS) conv_direct_kernel(const hnn_conv_pr
     }
     stage(ds, p.dy + size_t(b0) * g.f * g.ohw, nb * g.f * g.ohw);
     __syncthreads();
+    if (g.s == 1 && (g.k == 5 || g.k == 3)) {
+      float* red = ds + HNN_CONV_DIRECT_BCHUNK * g.f * g.ohw;  // [G][f*c*k][k] group partials
+      float* out = p.partial + size_t(unit) * nw;
+      if (g.k == 5) direct_wgrad_blocked<5>(p, g, xs, cs, rs, ds, nb, red, out);
+      else direct_wgrad_blocked<3>(p, g, xs, cs, rs, ds, nb, red, out);
+      return;
+    }
     float acc[MAXW];
 #pragma unroll
     for (int q = 0; q < MAXW; ++q) acc[q] = 0.0f;
@@ -378,7 +543,8 @@ __host__ __device__ inline int conv_direct_smem(int op, int c, int h, int w, int
   const int ckk = c * k * k;
   if (op == HNN_FWD) return 4 * (c * h * w + f * ckk);
   if (op == HNN_DGRAD) return 4 * (f * oh * ow + f * ckk);
-  return 4 * HNN_CONV_DIRECT_BCHUNK * (c * (h * (w + 1) + 1) + f * oh * ow);
+  // staged samples + the blocked stride-1 path's row-group partials (G <= 8 groups of f*c*k*k)
+  return 4 * HNN_CONV_DIRECT_BCHUNK * (c * (h * (w + 1) + 1) + f * oh * ow) + 4 * 8 * f * c * k * k;
 }
 
 }  // namespace hnn
