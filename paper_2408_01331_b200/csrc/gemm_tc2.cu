@@ -68,7 +68,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC2_THREADS, 1)
   constexpr int A_MN = (!BF16 && OP == HNN_WGRAD) ? 1 : 0;
   constexpr int B_MN = (!BF16 && OP != HNN_FWD) ? 1 : 0;
   constexpr int KBE = BF16 ? 64 : TC2_BK;  // K elements per 128-byte stage row
-  constexpr int SR = TC2_STAGES;
+  // bf16 stages carry no lo half: twice as many of them in the same shared memory, i.e. twice the
+  // bytes in flight for the HBM-streaming conv GEMMs (a 64-filter layer's MMA needs 20 KB per
+  // 128 clocks per CTA, so these launches are bound by the TMA pipeline depth)
+  constexpr int SR = BF16 ? 2 * TC2_STAGES : TC2_STAGES;
   extern __shared__ uint8_t smem_raw[];
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const uint32_t rank = cluster_rank();
@@ -80,7 +83,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC2_THREADS, 1)
 
   uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const uint32_t raw_base = smem_u32(base);
-  constexpr int SSTRIDE = 2 * TC2_STAGE;  // stage s: raw at s * SSTRIDE, lo right after it
+  constexpr int SSTRIDE = BF16 ? TC2_STAGE : 2 * TC2_STAGE;  // stage s: raw at s * SSTRIDE (fp32: lo after it)
   const uint32_t epi_base = raw_base + SR * SSTRIDE;
   uint64_t* bars = reinterpret_cast<uint64_t*>(base + SR * SSTRIDE + TC2_EPI_BYTES);
   constexpr int RAW_FULL = 0, RAW_EMPTY = SR, LO_FULL = 2 * SR;
@@ -328,6 +331,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC2_THREADS, 1)
       const bool fuse = OP == HNN_WGRAD && ow != nullptr;
       const bool nchw = OP == HNN_FWD && p->c_mode == 1;  // conv output straight to NCHW
       const float* nmask = nchw ? p->mask : nullptr;
+      const int nchw_b = nchw ? (m0 + int(rank) * TC2_BM + q * 32 + lane) / p->row_mult : 0;  // row's sample
+      const int nchw_hw = nchw ? (m0 + int(rank) * TC2_BM + q * 32 + lane) - nchw_b * p->row_mult : 0;
       const int hw_n = p->row_mult;
       const Update u = fuse ? make_update(cur[p->model], p->opt_kind, p->opt_momentum) : Update{};
       const int row0 = m0 + int(rank) * TC2_BM + q * 32, row = row0 + lane;
@@ -378,7 +383,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC2_THREADS, 1)
             // element (pixel row, filter n) -> y[b][n][hw]: for a fixed n the 32 lanes (rows =
             // consecutive pixels) write consecutive addresses
             if (row < pm) {
-              const int b = row / hw_n, hw = row - b * hw_n;
+              const int b = nchw_b, hw = nchw_hw;
 #pragma unroll
               for (int e = 0; e < 4; ++e) {
                 const int n = nh + cb + j4 * 4 + e;
