@@ -142,9 +142,10 @@ typedef struct hnn_gemm_problem {
   const void* tmap_a; /* HNN_PREC_F32_3XTF32: device copies of the problem's TMA maps (hnn_gemm_tc_encode) */
   const void* tmap_b;
   const void* tmap_c;
-  /* WGRAD optimizer fusion: when opt_w != NULL the epilogue applies the model's SGD / momentum /
-   * Adam update (arithmetic of hnn_multi_tensor_*) to the weight with the tile's finished
-   * gradient, and to the bias with dbias; c / dbias may then be NULL (gradient not stored). */
+  /* WGRAD optimizer fusion: when opt_w != NULL the epilogue applies the model's SGD / momentum
+   * update (arithmetic of hnn_multi_tensor_*) to the weight with the tile's finished gradient,
+   * and to the bias with dbias; c / dbias may then be NULL (gradient not stored).  The pair
+   * kernels (HNN_PREC_*_PAIR) trap on a fused Adam problem: Adam runs in hnn_multi_tensor_adam. */
   float* opt_w;
   float* opt_wm;
   float* opt_wv;

@@ -57,6 +57,98 @@ __device__ unsigned long long g_tc2_trace[296 * 16];
 #define TC2_T1(v, slot)
 #endif
 
+// Fused plain SGD over a single-chunk weight-gradient tile (K <= 128: the C1 / C2 / C5 dense
+// layers): nothing to promote, so the accumulators are read from TMEM block by block and the
+// registers a running sum would hold carry the weights instead, loaded ahead (block 0's before
+// the MMAs finish).  Returns the updated TMA-store count.  (Every register array here and in the
+// promoting epilogue is defined on all paths: a conditionally-written array is live across the
+// tile loop in ptxas's eyes, and that alone spilled 1-2 KB per thread.)
+static __device__ __forceinline__ uint32_t tc2_sgd_direct(uint32_t lane_base, uint32_t buf, uint32_t acc_full, uint32_t parity,
+                                                       uint32_t acc_empty, uint32_t stg, int row0, int nh, int hn,
+                                                       int pm, int pn, int ldc, float* ow, float* cptr,
+                                                       const void* tmap_c, float lr, int sp, uint32_t nstore) {
+  const int lane = threadIdx.x % 32;
+  const int rmax = min(32, pm - row0);
+  const int nblk = rmax > 0 ? (min(hn, pn - nh) + 31) / 32 : 0;  // live 32 x 32 blocks
+  // lane = row here (the TMEM layout): each lane streams its own row's 32 weights of a block
+  // as 8 float4 (the sibling float4 fills the other half of each 32-byte sector) and updates
+  // them straight from the accumulator registers; block cb + 1's weights load during block cb
+  const bool row_ok = lane < rmax;
+  float* const wrow = ow + size_t(row0 + (row_ok ? lane : 0)) * ldc + nh;
+  const bool vec = (ldc & 3) == 0 && (reinterpret_cast<uintptr_t>(ow) & 15) == 0;
+  float4 wA[8], wB[8];
+#pragma unroll
+  for (int j = 0; j < 8; ++j) wA[j] = wB[j] = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
+#define TC2_LOADW(WV, cb)                                                                          \
+  if (row_ok) {                                                                                   \
+    if (vec && nh + (cb) + 32 <= pn) {                                                            \
+      _Pragma("unroll") for (int j = 0; j < 8; ++j) WV[j] = *reinterpret_cast<const float4*>(wrow + (cb) + 4 * j); \
+    } else {                                                                                      \
+      _Pragma("unroll") for (int j = 0; j < 8; ++j) {                                             \
+  const int c = nh + (cb) + 4 * j;                                                          \
+  WV[j].x = c < pn ? wrow[(cb) + 4 * j] : 0.0f;                                              \
+  WV[j].y = c + 1 < pn ? wrow[(cb) + 4 * j + 1] : 0.0f;                                      \
+  WV[j].z = c + 2 < pn ? wrow[(cb) + 4 * j + 2] : 0.0f;                                      \
+  WV[j].w = c + 3 < pn ? wrow[(cb) + 4 * j + 3] : 0.0f;                                      \
+      }                                                                                           \
+    }                                                                                             \
+  }
+// one 32 x 32 block: accumulators out of TMEM, the next block's weights into `wn`, optional
+// gradient store, SGD on `w` (optim.py: p - lr * g)
+#define G32(k) ((k) < 16 ? g0[(k) & 15] : g1[(k) & 15])
+#define TC2_SGD_BLOCK(WV, WN, cb)                                                                  \
+  if ((cb) < 32 * nblk) {                                                                         \
+    uint32_t g0[16], g1[16];                                                                      \
+    tmem_ld16(lane_base + buf * TC2_BN + (cb), g0);                                               \
+    tmem_ld16(lane_base + buf * TC2_BN + (cb) + 16, g1);                                          \
+    if ((cb) + 32 < 32 * nblk) { TC2_LOADW(WN, (cb) + 32) }                                       \
+    if (cptr != nullptr) {                                                                        \
+      if (lane == 0 && nstore > 0) tma_store_wait_read();                                         \
+      __syncwarp();                                                                               \
+      _Pragma("unroll") for (int j4 = 0; j4 < 8; ++j4)                                            \
+  sts128(stg + lane * 128 + ((j4 ^ (lane & 7)) << 4), make_uint4(G32(4 * j4), G32(4 * j4 + 1), G32(4 * j4 + 2), G32(4 * j4 + 3))); \
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");                                \
+      __syncwarp();                                                                               \
+      if (lane == 0) tma_store_2d(tmap_c, stg, nh + (cb), row0 + sp * ((pm + 31) & ~31));         \
+      ++nstore;                                                                                   \
+    }                                                                                             \
+    if (row_ok) {                                                                                 \
+      _Pragma("unroll") for (int j = 0; j < 8; ++j) {                                             \
+  WV[j].x = __fsub_rn(WV[j].x, __fmul_rn(lr, __uint_as_float(G32(4 * j))));                    \
+  WV[j].y = __fsub_rn(WV[j].y, __fmul_rn(lr, __uint_as_float(G32(4 * j + 1))));                \
+  WV[j].z = __fsub_rn(WV[j].z, __fmul_rn(lr, __uint_as_float(G32(4 * j + 2))));                \
+  WV[j].w = __fsub_rn(WV[j].w, __fmul_rn(lr, __uint_as_float(G32(4 * j + 3))));                \
+      }                                                                                           \
+      if (vec && nh + (cb) + 32 <= pn) {                                                          \
+  _Pragma("unroll") for (int j = 0; j < 8; ++j) *reinterpret_cast<float4*>(wrow + (cb) + 4 * j) = WV[j]; \
+      } else {                                                                                    \
+  _Pragma("unroll") for (int j = 0; j < 8; ++j) {                                           \
+    const int c = nh + (cb) + 4 * j;                                                        \
+    if (c < pn) wrow[(cb) + 4 * j] = WV[j].x;                                                \
+    if (c + 1 < pn) wrow[(cb) + 4 * j + 1] = WV[j].y;                                        \
+    if (c + 2 < pn) wrow[(cb) + 4 * j + 2] = WV[j].z;                                        \
+    if (c + 3 < pn) wrow[(cb) + 4 * j + 3] = WV[j].w;                                        \
+  }                                                                                         \
+      }                                                                                           \
+    }                                                                                             \
+  }
+  if (nblk > 0) { TC2_LOADW(wA, 0) }
+  mbar_wait(acc_full, parity);
+  tc_fence_after();
+  static_assert(TC2_BN / 2 == 128, "four 32-column blocks per warp");
+  TC2_SGD_BLOCK(wA, wB, 0)
+  TC2_SGD_BLOCK(wB, wA, 32)
+  TC2_SGD_BLOCK(wA, wB, 64)
+  TC2_SGD_BLOCK(wB, wA, 96)
+#undef TC2_SGD_BLOCK
+#undef G32
+#undef TC2_LOADW
+  tc_fence_before();
+  __syncwarp();
+  if (lane == 0) mbar_arrive_cluster(acc_empty + 8 * buf);
+  return nstore;
+}
+
 // KIND: 0 = fp32 operands, 3xTF32 (kind::tf32, converters write lo); 1 = bf16 operands, one
 // kind::f16 MMA per K step (HNN_PREC_BF16_PAIR: every operand K-major, 64-element K blocks; the
 // converter warps only relay "stage landed" to the leader).
@@ -295,7 +387,23 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC2_THREADS, 1)
       const int nchunks = (nkb + TC2_CHUNK_KB - 1) / TC2_CHUNK_KB;
       const int hn = tn / 2;  // this warp's columns: [half * hn, half * hn + hn)
       const uint32_t lane_base = lane_quarter + half * hn;
+      // Fused plain SGD over a single chunk (K <= 128: C1 / C2 / C5 weight gradients): nothing to
+      // promote, so the epilogue reads TMEM block by block and the registers the running sum
+      // would hold carry the weights instead, loaded ahead (block 0's before the MMAs finish).
+      const bool direct = OP == HNN_WGRAD && nchunks == 1 && p->opt_w != nullptr && p->opt_wm == nullptr;
+      if (direct) {
+        TC2_T0(t5);
+        const uint32_t buf = cg & 1;
+        nstore = tc2_sgd_direct(lane_base, buf, bar(ACC_FULL + buf), (cg >> 1) & 1, acc_empty_leader, stg,
+                                m0 + int(rank) * TC2_BM + q * 32, n0 + half * hn, hn, p->m, p->n, p->ldc, p->opt_w,
+                                p->c, p->tmap_c, cur[p->model].lr, sp, nstore);
+        ++cg;
+        TC2_T1(t5, 7);
+        continue;
+      }
       float sum[HALF];
+#pragma unroll
+      for (int j = 0; j < HALF; ++j) sum[j] = 0.0f;  // defined on every path: not live across tiles
       for (int c = 0; c < nchunks; ++c, ++cg) {
         const uint32_t buf = cg & 1;
         TC2_T0(t4);
@@ -327,7 +435,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC2_THREADS, 1)
       const void* tmap_c = p->tmap_c;
       float* const ow = p->opt_w;
       float* const owm = p->opt_wm;
-      float* const owv = p->opt_wv;
       const bool fuse = OP == HNN_WGRAD && ow != nullptr;
       const bool nchw = OP == HNN_FWD && p->c_mode == 1;  // conv output straight to NCHW
       const float* nmask = nchw ? p->mask : nullptr;
@@ -335,6 +442,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC2_THREADS, 1)
       const int nchw_hw = nchw ? (m0 + int(rank) * TC2_BM + q * 32 + lane) - nchw_b * p->row_mult : 0;
       const int hw_n = p->row_mult;
       const Update u = fuse ? make_update(cur[p->model], p->opt_kind, p->opt_momentum) : Update{};
+      if (fuse && u.kind == HNN_OPT_ADAM) __trap();  // fused epilogues take SGD / momentum (hnn_b200.h)
       const int row0 = m0 + int(rank) * TC2_BM + q * 32, row = row0 + lane;
       const int nh = n0 + half * hn;
       const bool zero_row = (OP != HNN_WGRAD) && row >= rows;
@@ -409,7 +517,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC2_THREADS, 1)
           const int n = nh + cb + lane;
           if (n < pn) {
             const int rmax = min(32, pm - row0);
-            if (!owm && !owv) {  // plain SGD: 16 rows' weights in flight at once
+            if (!owm) {  // plain SGD: 16 rows' weights in flight at once
               for (int r16 = 0; r16 < rmax; r16 += 16) {
                 float w[16];
 #pragma unroll
@@ -420,32 +528,29 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC2_THREADS, 1)
                   const int rr = r16 + i;
                   if (rr >= rmax) break;
                   const float g = lds32(stg + rr * 128 + ((((lane >> 2) ^ (rr & 7))) << 4) + ((lane & 3) << 2));
-                  float m0v = 0.0f, v0v = 0.0f;
-                  update_one(u, w[i], g, m0v, v0v);
-                  ow[size_t(row0 + rr) * ldc + n] = w[i];
+                  ow[size_t(row0 + rr) * ldc + n] = __fsub_rn(w[i], __fmul_rn(u.lr, g));
                 }
               }
-            } else
-            for (int r8 = 0; r8 < rmax; r8 += 8) {
-              float w[8], mm[8], vv[8];
+            } else {  // momentum: 8 rows' weights + velocities in flight
+              for (int r8 = 0; r8 < rmax; r8 += 8) {
+                float w[8], mm[8];
 #pragma unroll
-              for (int i = 0; i < 8; ++i) {
-                const size_t off = size_t(row0 + r8 + i) * ldc + n;
-                const bool in = r8 + i < rmax;
-                w[i] = in ? ow[off] : 0.0f;
-                mm[i] = (in && owm) ? owm[off] : 0.0f;
-                vv[i] = (in && owv) ? owv[off] : 0.0f;
-              }
+                for (int i = 0; i < 8; ++i) {
+                  const size_t off = size_t(row0 + r8 + i) * ldc + n;
+                  const bool in = r8 + i < rmax;
+                  w[i] = in ? ow[off] : 0.0f;
+                  mm[i] = in ? owm[off] : 0.0f;
+                }
 #pragma unroll
-              for (int i = 0; i < 8; ++i) {
-                const int rr = r8 + i;
-                if (rr >= rmax) break;
-                const float g = lds32(stg + rr * 128 + ((((lane >> 2) ^ (rr & 7))) << 4) + ((lane & 3) << 2));
-                const size_t off = size_t(row0 + rr) * ldc + n;
-                update_one(u, w[i], g, mm[i], vv[i]);
-                ow[off] = w[i];
-                if (owm) owm[off] = mm[i];
-                if (owv) owv[off] = vv[i];
+                for (int i = 0; i < 8; ++i) {
+                  const int rr = r8 + i;
+                  if (rr >= rmax) break;
+                  const float g = lds32(stg + rr * 128 + ((((lane >> 2) ^ (rr & 7))) << 4) + ((lane & 3) << 2));
+                  const size_t off = size_t(row0 + rr) * ldc + n;
+                  update_sgd(u, w[i], g, mm[i]);
+                  ow[off] = w[i];
+                  owm[off] = mm[i];
+                }
               }
             }
           }

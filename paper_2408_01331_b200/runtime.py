@@ -290,6 +290,8 @@ class DeviceHybrid:
         # conv layers with at least this many filters use the tensor-core conv path
         self.tc_conv_min_f = int(os.environ.get("HNN_TC_CONV_MIN_F", "64"))
         self.use_pairs = os.environ.get("HNN_TC_PAIR", "1") != "0"
+        if os.environ.get("HNN_FUSE_OPT", "1") == "0":  # SGD / momentum in the multi-tensor pass
+            self.fuse_optimizer = False
         off = 0
         for s in slots:
             s.stages, s.classes, _ = lower_graph(s.graph)
@@ -647,6 +649,34 @@ class DeviceHybrid:
                 out += self._emit_gemm(op, prec, rows, label)
         return out
 
+    def _pair_tile_cap(self, op, rows, tm) -> int:
+        """Widest pair-tile width (256 / 128 / 64) for one launch: narrower tiles put more CTA pairs
+        to work when a launch has fewer tiles than pairs (C5's 32 batch-64 forward GEMMs: 32
+        tiles at 256 columns, 64 at 128).  Cost model per tile: 0.5 + 0.5 * width / 256 (the A
+        operand streams whatever the width); makespan = max(total / pairs, largest tile)."""
+        pairs = self._sm_count() // 2
+        best, best_cost = 256, None
+        for cap in (256, 128, 64):
+            total, largest = 0.0, 0.0
+            for _, d in rows:
+                w = min(cap, 64 if d["n"] <= 64 else (128 if d["n"] <= 128 else 256))
+                cost = 0.5 + 0.5 * w / 256
+                n_tiles = -(-d["m"] // tm) * -(-d["n"] // w) * (d.get("ksplit", 1) if op == N.HNN_WGRAD else 1)
+                total += n_tiles * cost
+                largest = max(largest, cost)
+            c = max(total / pairs, largest)
+            if best_cost is None or c < best_cost * 0.95:
+                best, best_cost = cap, c
+        return best
+
+    def _sm_count(self) -> int:
+        torch = _torch()
+        if getattr(self, "_sms", None) is None:
+            dev = torch.device(self.device) if self.device is not None else None
+            self._sms = (torch.cuda.get_device_properties(dev).multi_processor_count
+                         if dev is not None and dev.type == "cuda" else 148)
+        return self._sms
+
     def _emit_gemm(self, op, prec, rows, label):
         """One grouped-GEMM launch over rows = [(slot, problem dict)] (dense layers or lowered convs)."""
         out = []
@@ -655,10 +685,11 @@ class DeviceHybrid:
             # heaviest problems first: their tiles start in the first wave (LPT over SMs)
             rows = sorted(rows, key=lambda r: -(r[1]["m"] * r[1]["n"] * r[1]["k"]))
             probs, base = [], 0
+            cap = self._pair_tile_cap(op, rows, tm) if prec in (N.PREC_3XTF32_PAIR, N.PREC_BF16_PAIR) else tn
             for s, d in rows:
                 tn_p = tn
                 if prec in (N.PREC_3XTF32_PAIR, N.PREC_BF16_PAIR):  # narrowest pair tile covering n
-                    tn_p = 64 if d["n"] <= 64 else (128 if d["n"] <= 128 else 256)
+                    tn_p = min(cap, 64 if d["n"] <= 64 else (128 if d["n"] <= 128 else 256))
                     d = dict(d, tile_n=tn_p)
                 tiles_m, tiles_n = -(-d["m"] // tm), -(-d["n"] // tn_p)
                 probs.append(N.GemmProblem(tile_base=base, tiles_n=tiles_n, model=s.index, **d))
