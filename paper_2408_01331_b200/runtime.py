@@ -780,24 +780,20 @@ class DeviceHybrid:
         """Stride-1 conv input gradient = conv(dy, flipped weights, pad k-1-p): flip the weights,
         im2col dy into the model's scratch, one forward-type CTA-pair GEMM writing NCHW dx with the
         relu mask of x (no dcols round trip through col2im)."""
-        out, flips, cols = [], [], []
+        out, cols = [], []
         for s, st in items:
             c, h, w = st.in_shape
             f, oh, ow = self._conv_out(st)
             k = st.attrs["kernel"]
             p = st.attrs.get("padding", 0)
-            W = self.pview(self.params, s.index, st.params[0])
             kf = f * k * k
-            flips.append((s, N.ConvTcProblem(weight=_ptr(W), wpad=_ptr(st.wflip), c=c, f=f, k=k,
-                                             model=s.index, bf16=int(st.bf16))))
             # im2col over dy: channels F, spatial OH x OW -> H x W, padding k-1-p
             dst = s.dgcols if st.bf16 else s.dcols
             cols.append((s, N.ConvTcProblem(x=_ptr(st.dy), cols=_ptr(dst), cap=s.batch_size, c=f, h=oh, w=ow,
                                             f=c, k=k, stride=1, pad=k - 1 - p, oh=h, ow=w, kk=kf, kkp=kf,
                                             model=s.index, bf16=int(st.bf16))))
         max_k = max(st.attrs["kernel"] for _, st in items)
-        out.append(self._aux_table(N.CONVTC_FLIP_WEIGHTS, flips, f"{label}/tc/flipw",
-                                   lambda pr: grid(pr.c * pr.f * pr.k * pr.k), max_k))
+        # (the flipped weights come from the step's prep launch: conv_weight_prep)
         out.append(self._aux_table(N.CONVTC_IM2COL, cols, f"{label}/tc/im2col_dy",
                                    lambda pr: -(-(pr.cap * pr.oh * pr.ow) // 32) * -(-pr.c // 32), max_k))
         by_prec = {}
@@ -851,10 +847,7 @@ class DeviceHybrid:
 
         out = []
         if op == N.HNN_FWD:
-            padded = [(s, st) for s, st in items if st.wpad is not None]
-            if padded:
-                out.append(self._convtc_aux(N.CONVTC_PAD_WEIGHTS, padded, f"{label}/tc/padw",
-                                            lambda s, st: grid(geo(st)[3] * geo(st)[6])))
+            # (the padded weight copies come from the step's prep launch: conv_weight_prep)
             out.append(self._convtc_aux(
                 N.CONVTC_IM2COL, items, f"{label}/tc/im2col",
                 lambda s, st: -(-(s.batch_size * geo(st)[4] * geo(st)[5]) // 32) * -(-geo(st)[0] // 32)))
@@ -876,10 +869,6 @@ class DeviceHybrid:
             items = [(s, st) for s, st in items if not st.dg_fwd]
             if not items:
                 return out
-            wt = [(s, st) for s, st in items if st.bf16]
-            if wt:
-                out.append(self._convtc_aux(N.CONVTC_WT_WEIGHTS, wt, f"{label}/tc/wt",
-                                            lambda s, st: grid(geo(st)[3] * geo(st)[6])))
             out.append(self._convtc_aux(N.CONVTC_TRANSPOSE_DY, items, f"{label}/tc/transpose", tiles_t))
             rows = {}
             for s, st in items:
@@ -911,8 +900,66 @@ class DeviceHybrid:
                 (s, dict(d, c=_ptr(st.partial), bias=0, mask=0, dbias=0, m=f, n=kk, k=s.batch_size * oh * ow,
                          ldc=kk, relu=0, row_mult=oh * ow, ksplit=st.ksplit, ksplit_len=st.ksplit_len)))
         out += gemms(N.HNN_WGRAD, rows, f"{label}/tc")
-        out.append(self._convtc_aux(N.CONVTC_WGRAD_REDUCE, items, f"{label}/tc/reduce",
-                                    lambda s, st: grid(geo(st)[3] * geo(st)[6] + geo(st)[3])))
+        # (the split partials are summed for every layer at once before the optimizer: conv_reduce_all)
+        return out
+
+    @staticmethod
+    def _aux_grid(total):
+        return max(1, min(-(-total // 256), 4 * 148))
+
+    def _tc_conv_stages(self):
+        return [(s, st) for w in self._stage_waves() for s, st in w if st.kind == "conv" and getattr(st, "tc", False)]
+
+    def conv_weight_prep(self, train: bool) -> list:
+        """One launch per weight transform for every tensor-core conv layer of the step (the
+        weights only change in the optimizer, after the backward): the padded GEMM copies for
+        the forward, and for training the flipped (stride-1 input gradient as a forward conv) and
+        transposed (stride-2 dcols GEMM) copies.  Per-layer launches of these cost ~13 us each."""
+        stages = self._tc_conv_stages()
+        out = []
+        blocks = lambda s, st: self._aux_grid(self._conv_out(st)[0] * st.kkp)
+        padded = [(s, st) for s, st in stages if st.wpad is not None]
+        if padded:
+            out.append(self._convtc_aux(N.CONVTC_PAD_WEIGHTS, padded, "prep/conv/tc/padw", blocks))
+        if not train:
+            return out
+        flips = []
+        for s, st in stages:
+            if st.needs_dx and st.dg_fwd:
+                c = st.in_shape[0]
+                f = self._conv_out(st)[0]
+                k = st.attrs["kernel"]
+                W = self.pview(self.params, s.index, st.params[0])
+                flips.append((s, N.ConvTcProblem(weight=_ptr(W), wpad=_ptr(st.wflip), c=c, f=f, k=k,
+                                                 model=s.index, bf16=int(st.bf16))))
+        if flips:
+            max_k = max(pr.k for _, pr in flips)
+            out.append(self._aux_table(N.CONVTC_FLIP_WEIGHTS, flips, "prep/conv/tc/flipw",
+                                       lambda pr: self._aux_grid(pr.c * pr.f * pr.k * pr.k), max_k))
+        wt = [(s, st) for s, st in stages if st.needs_dx and not st.dg_fwd and st.bf16]
+        if wt:
+            out.append(self._convtc_aux(N.CONVTC_WT_WEIGHTS, wt, "prep/conv/tc/wt", blocks))
+        return out
+
+    def conv_reduce_all(self) -> list:
+        """The weight / bias gradients of every tensor-core conv layer from their split partials,
+        one launch after the last weight-gradient GEMM (each layer has its own partial buffers)."""
+        out = []
+        if self._pending_reduce:  # SIMT / direct conv layers: hnn_conv_wgrad_reduce
+            red, base = [], 0
+            for pr in self._pending_reduce:
+                n = -(-(pr.f * (pr.c * pr.k * pr.k + 1)) // 256)
+                pr.tile_base = base
+                red.append(pr)
+                base += n
+            rt = _dev_table(N.ConvProblem, red, self.device)
+            out.append(Launch("hnn_conv_wgrad_reduce", (_ptr(rt), len(red), base, _ptr(self.cur), _ptr(self.status)),
+                              rt, "bwd/conv/reduce"))
+        stages = self._tc_conv_stages()
+        if stages:
+            out.append(self._convtc_aux(N.CONVTC_WGRAD_REDUCE, stages, "bwd/conv/tc/reduce",
+                                        lambda s, st: self._aux_grid(self._conv_out(st)[0] * st.kkp
+                                                                     + self._conv_out(st)[0])))
         return out
 
     def _conv_group(self, op, items, label, direct):
@@ -958,10 +1005,8 @@ class DeviceHybrid:
         else:
             out = [Launch("hnn_grouped_conv", (op, _ptr(t), len(probs), base, _ptr(self.cur), _ptr(self.status)), t,
                           label, flops=flops)]
-        if op == N.HNN_WGRAD:
-            rt = _dev_table(N.ConvProblem, red, self.device)
-            out.append(Launch("hnn_conv_wgrad_reduce", (_ptr(rt), len(red), rbase, _ptr(self.cur),
-                                                        _ptr(self.status)), rt, label + "/reduce"))
+        if op == N.HNN_WGRAD:  # split partials summed with every other layer's (conv_reduce_all)
+            self._pending_reduce += red
         return out
 
     def _embed_launch(self, op, items, label):
@@ -1117,6 +1162,7 @@ class DeviceHybrid:
 
     def build_plans(self):
         waves = self._stage_waves()
+        self._pending_reduce = []
         fwd = []
         for w, items in enumerate(waves):
             fwd += self._wave_launches(N.HNN_FWD, items, f"fwd{w}")
@@ -1138,9 +1184,10 @@ class DeviceHybrid:
                         bwd += self._conv_launch(N.HNN_WGRAD, grp, f"bwd{w}/conv/wgrad")
                     else:
                         bwd += self._embed_launch(N.HNN_WGRAD, grp, f"bwd{w}/embed/wgrad")
-        self.forward_plan = fwd
-        self.train_plan = [self._gather_train] + fwd + [self._sce_launch(True)] + bwd + self._optimizer_launch()
-        self.eval_plan = [self._gather_eval] + fwd + [self._sce_launch(False)]
+        self.forward_plan = self.conv_weight_prep(False) + fwd
+        self.train_plan = ([self._gather_train] + self.conv_weight_prep(True) + fwd + [self._sce_launch(True)] + bwd
+                           + self.conv_reduce_all() + self._optimizer_launch())
+        self.eval_plan = [self._gather_eval] + self.conv_weight_prep(False) + fwd + [self._sce_launch(False)]
         self.graph = None
 
     # ------------------------------------------------------------------ running
