@@ -173,6 +173,14 @@ typedef struct hnn_gemm_problem {
    * tile_n / 2 rows (each CTA of the pair stages half of the tile's B columns). */
   int32_t tile_n;
   int32_t reserved;
+  /* HNN_PREC_BF16_PAIR FWD, implicit convolution (im_c > 0): A is not a [m, k] matrix but NHWC
+   * bf16 activations a[n][h][w][c] (im_n x im_h x im_w x im_c, c contiguous, im_c % 64 == 0); GEMM
+   * row m = (b, oh, ow) of a stride-1 conv's im_oh x im_ow output (row_mult = im_oh * im_ow) and
+   * K = (r, s, c) over the im_k x im_k taps with padding im_pad (taps outside the image read as
+   * zeros, by the TMA), so the B rows are in (r, s, c) order (HNN_CONVTC_PAD_WEIGHTS_RSC /
+   * FLIP_WEIGHTS_RSC).  Each 128-row CTA tile must be whole output rows of whole or one image:
+   * 128 % im_ow == 0 and (im_oh * im_ow) % 128 == 0 or 128 % (im_oh * im_ow) == 0. */
+  int32_t im_c, im_k, im_pad, im_h, im_w, im_oh, im_ow, im_n;
 } hnn_gemm_problem;
 
 /* Tile edge (m, n) used by (op, prec); lets the host lay out tile_base / tiles_n. */
@@ -315,7 +323,9 @@ int hnn_multi_tensor_adam(const hnn_opt_segment* segs, int nseg, int total_chunk
  *   HNN_CONVTC_IM2COL        cols[m, kk] = x[b, c, oh*s-p+r, ow*s-p+s'], m = (b, oh, ow), kk = (c, r, s');
  *                            rows are kkp wide (pad columns zero)
  *   HNN_CONVTC_TRANSPOSE_DY  dyt[m, f] = dy[b, f, oh, ow] (rows padded to 16 bytes); bpart[b, t, f] = sum of dy[b, f, hw]
- *                            over pixel tile t (32 pixels)
+ *                            over pixel tile t (32 pixels) when bpart != NULL.  Also the NCHW -> NHWC bf16
+ *                            copy of a conv input for the implicit GEMM (dy = x, f = c, oh/ow = h/w).
+ *   im2col in bf16 mode skips cols when cols == NULL (only colst, the weight-gradient operand).
  *   HNN_CONVTC_COL2IM        dx[b, c, h, w] = (mask > 0) * sum_(r, s') dcols[m, kk] (gather, tap order)
  *   HNN_CONVTC_WGRAD_REDUCE  dw[f, kk] = sum_s partial[s][f][kk] (splits in order); db[f] = sum over (b, t) of bpart[b, t, f]
  * Each problem covers `blocks` CTAs starting at block_base: im2col one per (32 output pixels, 32
@@ -331,6 +341,9 @@ int hnn_multi_tensor_adam(const hnn_opt_segment* segs, int nseg, int total_chunk
 #define HNN_CONVTC_WT_WEIGHTS 6   /* bf16 wpad[kk, f] = w[f, kk] */
 #define HNN_CONVTC_FLIP_WEIGHTS 5 /* wpad[c, (f, r, s)] = w[f, c, k-1-r, k-1-s]: stride-1 input gradient as a
                                      forward conv of dy (im2col of dy with pad k-1-pad, then a GEMM) */
+#define HNN_CONVTC_PAD_WEIGHTS_RSC 7  /* bf16 wpad[f, (r, s, c)] = w[f, c, r, s]: implicit-GEMM forward B */
+#define HNN_CONVTC_FLIP_WEIGHTS_RSC 8 /* bf16 wpad[c, (r, s, f)] = w[f, c, k-1-r, k-1-s]: implicit-GEMM input
+                                         gradient (forward conv of NHWC dy) B */
 
 typedef struct hnn_convtc_problem {
   const float* x;    /* [cap, c, h, w] */

@@ -46,16 +46,35 @@ __global__ void __launch_bounds__(CT_THREADS) im2col_kernel(const hnn_convtc_pro
   const int m = m0 + lane;
   const int b = m / ohw, o = m - b * ohw, oh = o / p.ow, ow = o - oh * p.ow;
   const bool valid = m < p.cap * ohw && b < rows;
-  for (int ci = warp; ci < IC_CH; ci += CT_THREADS / 32) {
-    const int c = c0 + ci;
-    const float* xc = p.x + (size_t(b) * p.c + c) * p.h * p.w;
-    for (int r = 0; r < p.k; ++r) {
-      const int h = oh * p.stride - p.pad + r;
-      for (int s = 0; s < p.k; ++s) {
-        const int w = ow * p.stride - p.pad + s;
-        float v = 0.0f;
-        if (valid && c < p.c && h >= 0 && h < p.h && w >= 0 && w < p.w) v = __ldg(xc + h * p.w + w);
-        ic_tile[lane * ld + ci * kk2 + r * p.k + s] = v;
+  if (p.k == 3) {  // the common 3 x 3 case: a channel's 9 taps load together (independent requests)
+    for (int ci = warp; ci < IC_CH; ci += CT_THREADS / 32) {
+      const int c = c0 + ci;
+      const float* xc = p.x + (size_t(b) * p.c + c) * p.h * p.w;
+      float v[9];
+#pragma unroll
+      for (int r = 0; r < 3; ++r) {
+        const int h = oh * p.stride - p.pad + r;
+#pragma unroll
+        for (int s = 0; s < 3; ++s) {
+          const int w = ow * p.stride - p.pad + s;
+          v[r * 3 + s] = (valid && c < p.c && h >= 0 && h < p.h && w >= 0 && w < p.w) ? __ldg(xc + h * p.w + w) : 0.0f;
+        }
+      }
+#pragma unroll
+      for (int j = 0; j < 9; ++j) ic_tile[lane * ld + ci * 9 + j] = v[j];
+    }
+  } else {
+    for (int ci = warp; ci < IC_CH; ci += CT_THREADS / 32) {
+      const int c = c0 + ci;
+      const float* xc = p.x + (size_t(b) * p.c + c) * p.h * p.w;
+      for (int r = 0; r < p.k; ++r) {
+        const int h = oh * p.stride - p.pad + r;
+        for (int s = 0; s < p.k; ++s) {
+          const int w = ow * p.stride - p.pad + s;
+          float v = 0.0f;
+          if (valid && c < p.c && h >= 0 && h < p.h && w >= 0 && w < p.w) v = __ldg(xc + h * p.w + w);
+          ic_tile[lane * ld + ci * kk2 + r * p.k + s] = v;
+        }
       }
     }
   }
@@ -63,7 +82,7 @@ __global__ void __launch_bounds__(CT_THREADS) im2col_kernel(const hnn_convtc_pro
   const int width = min(seg, (p.c - c0) * kk2);
   if (p.bf16) {
     __nv_bfloat16* cb16 = reinterpret_cast<__nv_bfloat16*>(p.cols);
-    for (int pi = warp; pi < IC_PIX; pi += CT_THREADS / 32) {
+    for (int pi = warp; pi < IC_PIX && cb16; pi += CT_THREADS / 32) {  // (no cols: implicit-GEMM forward)
       const int mm = m0 + pi;
       if (mm >= p.cap * ohw) break;
       __nv_bfloat16* dst = cb16 + size_t(mm) * p.kkp + c0 * kk2;
@@ -129,7 +148,7 @@ __global__ void __launch_bounds__(CT_THREADS) transpose_dy_kernel(const hnn_conv
   // bias partial of this tile: bpart[b, th, f] = sum over the tile's 32 pixels of dy[b, f, hw]
   // (fixed order; the reduce adds the tiles in (b, th) order).  A per-(b, f) sequential sum over all
   // HW pixels was a 1024-long dependent chain per thread (0.1-0.16 ms per C4 layer).
-  if (ty == 0) {
+  if (ty == 0 && p.bpart) {
     const int f = tf * 32 + tx;
     if (f < p.f) {
       float acc = 0.0f;
@@ -335,6 +354,29 @@ __global__ void __launch_bounds__(CT_THREADS) flip_weights_kernel(const hnn_conv
   }
 }
 
+// Implicit-GEMM B operands, K in (r, s, channel) order (the NHWC A tile of a K block is one tap's
+// 64 channels):  RSC   wpad[f, (r, s, c)] = w[f, c, r, s]
+//                FLIP  wpad[c, (r, s, f)] = w[f, c, k-1-r, k-1-s]   (input gradient as a forward conv)
+template <bool FLIP>
+__global__ void __launch_bounds__(CT_THREADS) rsc_weights_kernel(const hnn_convtc_problem* __restrict__ probs, int nprob,
+                                                                const hnn_step_row* __restrict__ cur,
+                                                                const hnn_model_status* __restrict__ status) {
+  const hnn_convtc_problem& p = ct_problem(probs, nprob, blockIdx.x);
+  if (!live(cur, status, p.model)) return;
+  const int kk2 = p.k * p.k;
+  const int inner = FLIP ? p.f : p.c;           // contiguous channel of the K index
+  const long long row = (long long)kk2 * inner;  // K
+  const long long total = (long long)(FLIP ? p.c : p.f) * row;
+  for (long long e = (long long)(blockIdx.x - p.block_base) * CT_THREADS + threadIdx.x; e < total;
+       e += (long long)p.blocks * CT_THREADS) {
+    const int o = int(e / row), j = int(e - (long long)o * row);
+    const int rs = j / inner, ch = j - rs * inner, r = rs / p.k, sx = rs - r * p.k;
+    const float v = FLIP ? __ldg(p.weight + ((size_t(ch) * p.c + o) * p.k + (p.k - 1 - r)) * p.k + (p.k - 1 - sx))
+                         : __ldg(p.weight + ((size_t(o) * p.c + ch) * p.k + r) * p.k + sx);
+    reinterpret_cast<__nv_bfloat16*>(p.wpad)[e] = __float2bfloat16_rn(v);
+  }
+}
+
 // bf16 wpad[kk, f] = w[f, kk] (kk < kkp; pad rows zero): the stride-2 dcols GEMM's K-major B.
 __global__ void __launch_bounds__(CT_THREADS) wt_weights_kernel(const hnn_convtc_problem* __restrict__ probs, int nprob,
                                                                const hnn_step_row* __restrict__ cur,
@@ -375,6 +417,12 @@ extern "C" int hnn_conv_tc_aux(int op, const hnn_convtc_problem* probs, int npro
       break;
     case HNN_CONVTC_FLIP_WEIGHTS:
       hnn::flip_weights_kernel<<<total_blocks, hnn::CT_THREADS, 0, s>>>(probs, nprob, cur, status);
+      break;
+    case HNN_CONVTC_PAD_WEIGHTS_RSC:
+      hnn::rsc_weights_kernel<false><<<total_blocks, hnn::CT_THREADS, 0, s>>>(probs, nprob, cur, status);
+      break;
+    case HNN_CONVTC_FLIP_WEIGHTS_RSC:
+      hnn::rsc_weights_kernel<true><<<total_blocks, hnn::CT_THREADS, 0, s>>>(probs, nprob, cur, status);
       break;
     case HNN_CONVTC_WT_WEIGHTS:
       hnn::wt_weights_kernel<<<total_blocks, hnn::CT_THREADS, 0, s>>>(probs, nprob, cur, status);

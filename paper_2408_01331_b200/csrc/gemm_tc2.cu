@@ -267,6 +267,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC2_THREADS, 1)
           if (A_MN) {
 #pragma unroll
             for (int b = 0; b < TC2_BM / 32; ++b) tma_load_2d(st + b * 4096, p->tmap_a, bar(RAW_FULL + s), am + 32 * b, k0);
+          } else if (BF16 && OP == HNN_FWD && p->im_c > 0) {
+            // implicit-GEMM convolution: K block kb = tap (r, s) x 64 channels of the NHWC input,
+            // this CTA's 128 output pixels = whole output rows (or images) starting at (b0, oh0)
+            const int cbk = p->im_c / 64, tap = kb / cbk, r = tap / p->im_k, sx = tap - r * p->im_k;
+            const int hw = p->im_oh * p->im_ow, b0 = am / hw, oh0 = (am - b0 * hw) / p->im_ow;
+            tma_load_4d(st, p->tmap_a, bar(RAW_FULL + s), (kb - tap * cbk) * 64, sx - p->im_pad, oh0 + r - p->im_pad, b0);
           } else {
             tma_load_2d(st, p->tmap_a, bar(RAW_FULL + s), k0, am);
           }

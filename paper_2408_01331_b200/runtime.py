@@ -54,6 +54,11 @@ def _torch():
     return torch
 
 
+def _implicit_tiles(oh: int, ow: int) -> bool:
+    """A 128-row GEMM tile is whole output rows of one image, or whole images (the 4D TMA box)."""
+    return ow <= 128 and 128 % ow == 0 and ((oh * ow) % 128 == 0 or 128 % (oh * ow) == 0)
+
+
 def _align4(n: int) -> int:
     return (n + 3) // 4 * 4
 
@@ -99,6 +104,9 @@ class Stage:
     dyk = None
     wt = None
     fld: int = 0
+    im_fwd: bool = False       # implicit-GEMM forward over xh (NHWC bf16 copy of x)
+    im_dg: bool = False        # implicit-GEMM input gradient over dyt (NHWC dy)
+    xh = None
 
 
 def lower_graph(graph) -> tuple:
@@ -290,6 +298,8 @@ class DeviceHybrid:
         # conv layers with at least this many filters use the tensor-core conv path
         self.tc_conv_min_f = int(os.environ.get("HNN_TC_CONV_MIN_F", "64"))
         self.use_pairs = os.environ.get("HNN_TC_PAIR", "1") != "0"
+        # bf16 tensor-core convs read NHWC activations through 4D TMA maps where the shape allows
+        self.implicit_conv = os.environ.get("HNN_IMPLICIT_CONV", "1") != "0"
         if os.environ.get("HNN_FUSE_OPT", "1") == "0":  # SGD / momentum in the multi-tensor pass
             self.fuse_optimizer = False
         off = 0
@@ -390,7 +400,13 @@ class DeviceHybrid:
                         st.ksplit_len = -(-(-(-pix // split)) // kq) * kq
                         st.ksplit = -(-pix // st.ksplit_len)
                         st.pix_ld = -(-pix // 8) * 8
-                        st.cols = torch.zeros(pix * kk, dtype=wdt, device=dev)
+                        # implicit-GEMM forward (bf16, stride 1, 64-channel K blocks, output tiles of
+                        # whole rows / images): the GEMM reads an NHWC copy of x through a 4D TMA map,
+                        # no cols matrix (im2col still writes the weight-gradient copy colst)
+                        st.im_fwd = (self.implicit_conv and st.bf16 and stride == 1 and c % 64 == 0
+                                     and _implicit_tiles(oh, ow))
+                        st.xh = torch.zeros(cap * h * w * c, dtype=wdt, device=dev) if st.im_fwd else None
+                        st.cols = None if st.im_fwd else torch.zeros(pix * kk, dtype=wdt, device=dev)
                         st.bpart = torch.zeros(cap * -(-(oh * ow) // 32) * f, dtype=torch.float32, device=dev)
                         st.partial = torch.zeros(st.ksplit * (-(-f // 32) * 32) * kk, dtype=torch.float32,
                                                  device=dev)
@@ -401,11 +417,15 @@ class DeviceHybrid:
                         # weights; scratch [cap*H*W, F*k*k]); stride 2 -> dcols GEMM + col2im
                         st.dg_fwd = st.attrs.get("stride", 1) == 1 and (f * k * k) % 8 == 0
                         st.fld = -(-f // 8) * 8 if st.bf16 else _align4(f)  # dyt rows: 16 bytes
-                        if not st.bf16 or (st.needs_dx and not st.dg_fwd):
+                        # implicit-GEMM input gradient: a forward conv of the NHWC dy (dyt) with the
+                        # flipped weights, no im2col of dy
+                        st.im_dg = (self.implicit_conv and st.bf16 and st.needs_dx and st.dg_fwd and f % 64 == 0
+                                    and _implicit_tiles(h, w))
+                        if not st.bf16 or (st.needs_dx and not st.dg_fwd) or st.im_dg:
                             st.dyt = torch.zeros(pix * st.fld, dtype=wdt, device=dev)
                         if st.needs_dx and st.dg_fwd:
                             st.wflip = torch.zeros(c * f * k * k, dtype=wdt, device=dev)
-                            if st.bf16:
+                            if st.bf16 and not st.im_dg:
                                 dgb_need = max(dgb_need, cap * h * w * f * k * k)
                             else:
                                 dcols_need = max(dcols_need, cap * h * w * f * k * k)
@@ -781,7 +801,14 @@ class DeviceHybrid:
         im2col dy into the model's scratch, one forward-type CTA-pair GEMM writing NCHW dx with the
         relu mask of x (no dcols round trip through col2im)."""
         out, cols = [], []
+        imp = [(s, st) for s, st in items if st.im_dg]
+        if imp:  # NHWC dy (+ the weight-gradient copies and bias partials of the same transpose)
+            out.append(self._convtc_aux(N.CONVTC_TRANSPOSE_DY, imp, f"{label}/tc/transpose",
+                                        lambda s, st: (s.batch_size * -(-(self._conv_out(st)[1] * self._conv_out(st)[2]) // 32)
+                                                       * -(-self._conv_out(st)[0] // 32))))
         for s, st in items:
+            if st.im_dg:
+                continue
             c, h, w = st.in_shape
             f, oh, ow = self._conv_out(st)
             k = st.attrs["kernel"]
@@ -794,18 +821,23 @@ class DeviceHybrid:
                                             model=s.index, bf16=int(st.bf16))))
         max_k = max(st.attrs["kernel"] for _, st in items)
         # (the flipped weights come from the step's prep launch: conv_weight_prep)
-        out.append(self._aux_table(N.CONVTC_IM2COL, cols, f"{label}/tc/im2col_dy",
-                                   lambda pr: -(-(pr.cap * pr.oh * pr.ow) // 32) * -(-pr.c // 32), max_k))
+        if cols:
+            out.append(self._aux_table(N.CONVTC_IM2COL, cols, f"{label}/tc/im2col_dy",
+                                       lambda pr: -(-(pr.cap * pr.oh * pr.ow) // 32) * -(-pr.c // 32), max_k))
         by_prec = {}
         for s, st in items:
             c, h, w = st.in_shape
             f, oh, ow = self._conv_out(st)
-            kf = f * st.attrs["kernel"] ** 2
+            k = st.attrs["kernel"]
+            kf = f * k * k
             src = s.dgcols if st.bf16 else s.dcols
-            by_prec.setdefault(N.PREC_BF16_PAIR if st.bf16 else N.PREC_3XTF32_PAIR, []).append(
-                (s, dict(a=_ptr(src), b=_ptr(st.wflip), c=_ptr(st.dx), bias=0,
-                         mask=_ptr(st.x) if st.mask_input else 0, dbias=0, m=s.batch_size * h * w, n=c,
-                         k=kf, lda=kf, ldb=kf, ldc=c, relu=0, row_mult=h * w, c_mode=1)))
+            d = dict(a=_ptr(src), b=_ptr(st.wflip), c=_ptr(st.dx), bias=0,
+                     mask=_ptr(st.x) if st.mask_input else 0, dbias=0, m=s.batch_size * h * w, n=c,
+                     k=kf, lda=kf, ldb=kf, ldc=c, relu=0, row_mult=h * w, c_mode=1)
+            if st.im_dg:  # conv of the NHWC dy, pad k-1-p, onto the h x w input grid
+                d.update(a=_ptr(st.dyt), lda=st.fld, im_c=f, im_k=k, im_pad=k - 1 - st.attrs.get("padding", 0),
+                         im_h=oh, im_w=ow, im_oh=h, im_ow=w, im_n=s.batch_size)
+            by_prec.setdefault(N.PREC_BF16_PAIR if st.bf16 else N.PREC_3XTF32_PAIR, []).append((s, d))
         for prec, rows in by_prec.items():
             out += self._emit_gemm(N.HNN_FWD, prec, rows, f"{label}/tc/dgfwd")
         return out
@@ -848,6 +880,15 @@ class DeviceHybrid:
         out = []
         if op == N.HNN_FWD:
             # (the padded weight copies come from the step's prep launch: conv_weight_prep)
+            imp = [(s, st) for s, st in items if st.im_fwd]
+            if imp:  # NHWC bf16 copies of the inputs for the implicit-GEMM layers
+                probs = []
+                for s, st in imp:
+                    c, h, w = st.in_shape
+                    probs.append((s, N.ConvTcProblem(dy=_ptr(st.x), dyt=_ptr(st.xh), cap=s.batch_size, f=c, oh=h,
+                                                     ow=w, model=s.index, bf16=1)))
+                out.append(self._aux_table(N.CONVTC_TRANSPOSE_DY, probs, f"{label}/tc/nhwc",
+                                           lambda pr: pr.cap * -(-(pr.oh * pr.ow) // 32) * -(-pr.f // 32), 3))
             out.append(self._convtc_aux(
                 N.CONVTC_IM2COL, items, f"{label}/tc/im2col",
                 lambda s, st: -(-(s.batch_size * geo(st)[4] * geo(st)[5]) // 32) * -(-geo(st)[0] // 32)))
@@ -855,10 +896,13 @@ class DeviceHybrid:
             for s, st in items:
                 c, h, w, f, oh, ow, kk = geo(st)
                 B = self.pview(self.params, s.index, st.params[1])
-                rows.setdefault(prec(st), []).append(
-                    (s, dict(a=_ptr(st.cols), b=weight(s, st), c=_ptr(st.y), bias=_ptr(B), mask=0, dbias=0,
-                             m=s.batch_size * oh * ow, n=f, k=kk, lda=kk, ldb=kk, ldc=f, relu=int(st.relu),
-                             row_mult=oh * ow, c_mode=1)))
+                d = dict(a=_ptr(st.cols), b=weight(s, st), c=_ptr(st.y), bias=_ptr(B), mask=0, dbias=0,
+                         m=s.batch_size * oh * ow, n=f, k=kk, lda=kk, ldb=kk, ldc=f, relu=int(st.relu),
+                         row_mult=oh * ow, c_mode=1)
+                if st.im_fwd:
+                    d.update(a=_ptr(st.xh), lda=c, im_c=c, im_k=st.attrs["kernel"], im_pad=st.attrs.get("padding", 0),
+                             im_h=h, im_w=w, im_oh=oh, im_ow=ow, im_n=s.batch_size)
+                rows.setdefault(prec(st), []).append((s, d))
             return out + gemms(N.HNN_FWD, rows, f"{label}/tc")
         tiles_t = lambda s, st: (s.batch_size * -(-(geo(st)[4] * geo(st)[5]) // 32) * -(-geo(st)[3] // 32))
         if op == N.HNN_DGRAD:
@@ -886,7 +930,7 @@ class DeviceHybrid:
                                                        * -(-geo(st)[0] // 16))))
             return out
         # WGRAD (the transpose already ran in this wave's DGRAD phase when the stage needs dx)
-        fresh = [(s, st) for s, st in items if not (st.needs_dx and not st.dg_fwd)]
+        fresh = [(s, st) for s, st in items if not (st.needs_dx and not st.dg_fwd) and not st.im_dg]
         if fresh:
             out.append(self._convtc_aux(N.CONVTC_TRANSPOSE_DY, fresh, f"{label}/tc/transpose", tiles_t))
         rows = {}
@@ -918,20 +962,28 @@ class DeviceHybrid:
         stages = self._tc_conv_stages()
         out = []
         blocks = lambda s, st: self._aux_grid(self._conv_out(st)[0] * st.kkp)
-        padded = [(s, st) for s, st in stages if st.wpad is not None]
+        padded = [(s, st) for s, st in stages if st.wpad is not None and not st.im_fwd]
         if padded:
             out.append(self._convtc_aux(N.CONVTC_PAD_WEIGHTS, padded, "prep/conv/tc/padw", blocks))
+        rsc = [(s, st) for s, st in stages if st.im_fwd]
+        if rsc:  # (r, s, c)-ordered K for the implicit-GEMM forward
+            out.append(self._convtc_aux(N.CONVTC_PAD_WEIGHTS_RSC, rsc, "prep/conv/tc/padw_rsc", blocks))
         if not train:
             return out
-        flips = []
+        flips, flips_rsc = [], []
         for s, st in stages:
             if st.needs_dx and st.dg_fwd:
                 c = st.in_shape[0]
                 f = self._conv_out(st)[0]
                 k = st.attrs["kernel"]
                 W = self.pview(self.params, s.index, st.params[0])
-                flips.append((s, N.ConvTcProblem(weight=_ptr(W), wpad=_ptr(st.wflip), c=c, f=f, k=k,
-                                                 model=s.index, bf16=int(st.bf16))))
+                (flips_rsc if st.im_dg else flips).append(
+                    (s, N.ConvTcProblem(weight=_ptr(W), wpad=_ptr(st.wflip), c=c, f=f, k=k, model=s.index,
+                                        bf16=int(st.bf16))))
+        if flips_rsc:
+            out.append(self._aux_table(N.CONVTC_FLIP_WEIGHTS_RSC, flips_rsc, "prep/conv/tc/flipw_rsc",
+                                       lambda pr: self._aux_grid(pr.c * pr.f * pr.k * pr.k),
+                                       max(pr.k for _, pr in flips_rsc)))
         if flips:
             max_k = max(pr.k for _, pr in flips)
             out.append(self._aux_table(N.CONVTC_FLIP_WEIGHTS, flips, "prep/conv/tc/flipw",

@@ -654,6 +654,52 @@ def test_bf16_tensor_core_convs_track_oracle(pkg):
     assert max(abs(a - b) / abs(b) for a, b in zip(losses, ref_losses)) <= 2e-2, (losses, ref_losses)
 
 
+def test_implicit_gemm_convs_match_explicit(pkg, monkeypatch):
+    """bf16 implicit-GEMM convolutions (NHWC activations through 4D TMA boxes, K in (r, s, c) order,
+    taps outside the image zero-filled by the TMA) against the explicit im2col path: whole-row
+    tiles (16 x 16), two images per tile (8 x 8), and a padding-0 layer whose input gradient is an
+    implicit conv with padding 2.  Same bf16 operands, different fp32 summation order: first-step
+    gradients agree to 1e-2 (relative, max-abs) and both track the fp32 oracle to 1e-1."""
+    from paper_2408_01331_b200 import store, zoo
+
+    spec = [("conv0", "conv2d", {"filters": 64, "kernel": 3, "padding": 1}), ("act0", "relu", {}),
+            ("conv1", "conv2d", {"filters": 64, "kernel": 3, "padding": 1}), ("act1", "relu", {}),
+            ("pool1", "maxpool2d", {"kernel": 2}),
+            ("conv2", "conv2d", {"filters": 128, "kernel": 3, "padding": 1}), ("act2", "relu", {}),
+            ("conv3", "conv2d", {"filters": 64, "kernel": 3, "padding": 0}), ("act3", "relu", {}),
+            ("pool3", "maxpool2d", {"kernel": 2}),
+            ("flat", "flatten", {}), ("fc", "dense", {"units": 10})]
+    graph = zoo._seq("implicit-conv", (3, 16, 16), spec)
+    splits = oracle.image_splits("imconv", "mini", 10, (3, 16, 16), 64, 8)
+    ds = store.from_splits(splits)
+
+    def run(implicit):
+        monkeypatch.setenv("HNN_IMPLICIT_CONV", "1" if implicit else "0")
+        job = pkg.TrainingJob("v", graph, ds.content_hash, pkg.HyperParams(1, 32, 0.01, "sgd", (), 4), 0, 0)
+        h = pkg.merge([job])
+        grabbed = []
+        tr = pkg.Trainer(h, pkg.make_plan("fcfs", [job]), [job], {"v": ds}, keep_grads=True, fuse_optimizer=False,
+                         conv_precision="bf16")
+        tr.step_observer = lambda j, p: grabbed.append(tr.device.download_grads(0))
+        tr.run()
+        st = {s.node_id: s for s in tr.device.slots[0].stages}
+        return grabbed[0], st
+
+    imp, st = run(True)
+    assert st["conv1"].im_fwd and st["conv1"].im_dg and st["conv2"].im_fwd and st["conv3"].im_dg
+    assert not st["conv0"].im_fwd and not st["conv3"].im_fwd
+    exp, st0 = run(False)
+    assert not any(s.im_fwd or s.im_dg for s in st0.values() if s.kind == "conv")
+    params = oracle.init_model(graph, 4)
+    bx, by, _ = oracle.epoch_batches(splits["train_x"], splits["train_y"], ds.content_hash, 32, 4, 0)[0]
+    logits, tape = oracle.model_forward(graph, params, bx)
+    _, dl = oracle.sce_loss_and_grad(logits, by)
+    ref = oracle.model_backward(tape, dl)
+    for pid, g in ref.items():
+        assert rel(imp[pid], exp[pid]) <= 1e-2, (pid, rel(imp[pid], exp[pid]))
+        assert rel(imp[pid], g) <= 1e-1, (pid, rel(imp[pid], g))
+
+
 @pytest.mark.parametrize("optimizer", ["sgd", "adam"])
 def test_embedding_lookup_trajectory_matches_oracle(pkg, optimizer):
     """embedding-lookup (src/ops.py:258-278) on the device: gathered rows and the table gradient in
