@@ -298,7 +298,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC2_THREADS, 1)
         if (!tile_info(tile, p, m0, n0, nkb, rows, kofs, sp, tn)) continue;
         const uint32_t idesc = BF16 ? bf16_idesc(2 * TC2_BM, tn) : tf32_idesc(2 * TC2_BM, tn, A_MN, B_MN);
         for (int kb = 0; kb < nkb; ++kb, ++kg) {
-          const int in_chunk = kb % TC2_CHUNK_KB;
+          const int in_chunk = BF16 ? kb : kb % TC2_CHUNK_KB;  // bf16: one chunk per tile (no promotion)
           const uint32_t buf = cg & 1;
           TC2_T0(t1);
           if (in_chunk == 0 && cg >= 2) mbar_wait(bar(ACC_EMPTY + buf), ((cg >> 1) - 1) & 1);  // promoted
@@ -329,7 +329,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC2_THREADS, 1)
           }
           mma_commit_pair(bar(RAW_EMPTY + s));  // raw and lo of stage s consumed
           TC2_T1(t0, 5);
-          if (in_chunk == TC2_CHUNK_KB - 1 || kb == nkb - 1) {
+          if ((!BF16 && in_chunk == TC2_CHUNK_KB - 1) || kb == nkb - 1) {
             mma_commit_pair(bar(ACC_FULL + buf));
             ++cg;
           }
@@ -390,7 +390,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC2_THREADS, 1)
       const hnn_gemm_problem* p;
       int m0, n0, nkb, rows, kofs, sp, tn;
       if (!tile_info(tile, p, m0, n0, nkb, rows, kofs, sp, tn)) continue;
-      const int nchunks = (nkb + TC2_CHUNK_KB - 1) / TC2_CHUNK_KB;
+      const int nchunks = BF16 ? 1 : (nkb + TC2_CHUNK_KB - 1) / TC2_CHUNK_KB;
       const int hn = tn / 2;  // this warp's columns: [half * hn, half * hn + hn)
       const uint32_t lane_base = lane_quarter + half * hn;
       // Fused plain SGD over a single chunk (K <= 128: C1 / C2 / C5 weight gradients): nothing to
@@ -407,15 +407,20 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC2_THREADS, 1)
         TC2_T1(t5, 7);
         continue;
       }
-      float sum[HALF];
+      // bf16 (kind::f16, exact products, fp32 accumulation in the tensor core): the whole K is one
+      // chunk and the epilogue reads the accumulators straight from TMEM, block by block, releasing
+      // the buffer after the last block; fp32 (3xTF32): running sum in registers, promoted per chunk
+      float sum[BF16 ? 1 : HALF];
 #pragma unroll
-      for (int j = 0; j < HALF; ++j) sum[j] = 0.0f;  // defined on every path: not live across tiles
+      for (int j = 0; j < (BF16 ? 1 : HALF); ++j) sum[j] = 0.0f;  // defined on every path: not live across tiles
+      const uint32_t dbuf = cg & 1;  // (bf16) the tile's accumulator buffer
       for (int c = 0; c < nchunks; ++c, ++cg) {
         const uint32_t buf = cg & 1;
         TC2_T0(t4);
         mbar_wait(bar(ACC_FULL + buf), (cg >> 1) & 1);
         TC2_T1(t4, 4);
         tc_fence_after();
+        if (BF16) continue;
 #pragma unroll
         for (int cb = 0; cb < HALF; cb += 16) {
           if (cb >= hn) break;
@@ -463,6 +468,50 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC2_THREADS, 1)
         // j ^ (r & 7): conflict-free STS.128) -> one TMA store per 32 x 32 block
         float bv = 0.0f;
         if (OP == HNN_FWD && bias && nh + cb + lane < pn) bv = __ldg(bias + nh + cb + lane);  // lane j: column j
+        float tv[32];
+        if (BF16) {
+          uint32_t r0[16], r1[16];
+          tmem_ld16(lane_base + dbuf * TC2_BN + cb, r0);
+          tmem_ld16(lane_base + dbuf * TC2_BN + cb + 16, r1);
+#pragma unroll
+          for (int j = 0; j < 16; ++j) {
+            tv[j] = __uint_as_float(r0[j]);
+            tv[16 + j] = __uint_as_float(r1[j]);
+          }
+        }
+#define TC2_ACC(j) (BF16 ? tv[(j)] : sum[(cb + (j)) % (BF16 ? 1 : HALF)])
+        if (nchw) {
+          // element (pixel row, filter n) -> y[b][n][hw]: for a fixed n the 32 lanes (rows =
+          // consecutive pixels) write consecutive addresses.  NG columns at a time: their relu-mask
+          // loads (a conv input gradient as a forward conv of dy) are all issued before any store
+          // (interleaved, each load waited behind the previous store: the epilogue was 75% of the
+          // dgrad launches' time)
+          constexpr int NG = BF16 ? 8 : 2;  // (fp32: the running sum holds 128 registers)
+          const bool rok = row < pm;
+          const size_t ybase = rok ? size_t(nchw_b) * pn * hw_n + nchw_hw : 0;
+#pragma unroll
+          for (int g = 0; g < 32 / NG; ++g) {
+            float mk[NG];
+#pragma unroll
+            for (int jj = 0; jj < NG; ++jj) {
+              const int n = nh + cb + g * NG + jj;
+              mk[jj] = (nmask && rok && n < pn) ? __ldg(nmask + ybase + size_t(n) * hw_n) : 1.0f;
+            }
+#pragma unroll
+            for (int jj = 0; jj < NG; ++jj) {
+              const int n = nh + cb + g * NG + jj;
+              float x = TC2_ACC(g * NG + jj);
+              const float b = __shfl_sync(0xffffffffu, bv, g * NG + jj);  // column's bias
+              if (zero_row) x = 0.0f;
+              else {
+                x = __fadd_rn(x, b);
+                if (relu) x = np_relu(x);
+              }
+              if (rok && n < pn) cptr[ybase + size_t(n) * hw_n] = nmask ? (zero_row ? 0.0f : np_mask(x, mk[jj])) : x;
+            }
+          }
+          continue;
+        }
 #pragma unroll
         for (int j4 = 0; j4 < 8; ++j4) {
           float v[4], mv[4] = {0.0f, 0.0f, 0.0f, 0.0f};
@@ -479,7 +528,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC2_THREADS, 1)
 #pragma unroll
           for (int e = 0; e < 4; ++e) {
             const int jj = j4 * 4 + e;
-            float x = sum[cb + jj];
+            float x = TC2_ACC(jj);
             if (OP == HNN_FWD) {
               const float b = __shfl_sync(0xffffffffu, bv, jj);  // column jj's bias
               if (zero_row) x = 0.0f;
@@ -493,27 +542,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC2_THREADS, 1)
             }
             v[e] = x;
           }
-          if (nchw) {
-            // element (pixel row, filter n) -> y[b][n][hw]: for a fixed n the 32 lanes (rows =
-            // consecutive pixels) write consecutive addresses
-            if (row < pm) {
-              const int b = nchw_b, hw = nchw_hw;
-#pragma unroll
-              for (int e = 0; e < 4; ++e) {
-                const int n = nh + cb + j4 * 4 + e;
-                if (n < pn) {
-                  const size_t off = (size_t(b) * pn + n) * hw_n + hw;
-                  // (a conv input gradient computed as a forward conv of dy: relu mask of the input)
-                  cptr[off] = nmask ? (zero_row ? 0.0f : np_mask(v[e], __ldg(nmask + off))) : v[e];
-                }
-              }
-            }
-            continue;
-          }
           sts128(stg + lane * 128 + ((j4 ^ (lane & 7)) << 4),
                  make_uint4(__float_as_uint(v[0]), __float_as_uint(v[1]), __float_as_uint(v[2]), __float_as_uint(v[3])));
         }
-        if (nchw) continue;
         __syncwarp();
         if (fuse) {
           // fused optimizer: lane = column, so W / moment accesses of a row are one coalesced
@@ -568,6 +599,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC2_THREADS, 1)
           if (lane == 0) tma_store_2d(tmap_c, stg, nh + cb, row0 + sp * ((pm + 31) & ~31));  // split sp's rows
           ++nstore;
         }
+      }
+#undef TC2_ACC
+      if (BF16) {  // accumulators read: the buffer goes back to the MMA issuer
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive_cluster(acc_empty_leader + 8 * dbuf);
       }
       TC2_T1(t5, 7);
     }
