@@ -325,7 +325,8 @@ int hnn_multi_tensor_adam(const hnn_opt_segment* segs, int nseg, int total_chunk
  *   HNN_CONVTC_TRANSPOSE_DY  dyt[m, f] = dy[b, f, oh, ow] (rows padded to 16 bytes); bpart[b, t, f] = sum of dy[b, f, hw]
  *                            over pixel tile t (32 pixels) when bpart != NULL.  Also the NCHW -> NHWC bf16
  *                            copy of a conv input for the implicit GEMM (dy = x, f = c, oh/ow = h/w).
- *   im2col in bf16 mode skips cols when cols == NULL (only colst, the weight-gradient operand).
+ *   im2col in bf16 mode skips cols when cols == NULL (only colst, the weight-gradient operand), and
+ *   for a "same" stride-1 layer with dyt != NULL also writes the NHWC bf16 copy of x to dyt.
  *   HNN_CONVTC_COL2IM        dx[b, c, h, w] = (mask > 0) * sum_(r, s') dcols[m, kk] (gather, tap order)
  *   HNN_CONVTC_WGRAD_REDUCE  dw[f, kk] = sum_s partial[s][f][kk] (splits in order); db[f] = sum over (b, t) of bpart[b, t, f]
  * Each problem covers `blocks` CTAs starting at block_base: im2col one per (32 output pixels, 32

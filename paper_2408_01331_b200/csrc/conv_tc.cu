@@ -80,6 +80,17 @@ __global__ void __launch_bounds__(CT_THREADS) im2col_kernel(const hnn_convtc_pro
   }
   __syncthreads();
   const int width = min(seg, (p.c - c0) * kk2);
+  if (p.bf16 && p.dyt) {
+    // the implicit-GEMM forward's NHWC bf16 copy of x, from the centre taps of this tile ("same"
+    // stride-1 layers only: output pixel = input pixel): 32 channels of a pixel per warp store
+    const int centre = p.pad * p.k + p.pad;
+    __nv_bfloat16* xh = reinterpret_cast<__nv_bfloat16*>(p.dyt);
+    for (int pi = warp; pi < IC_PIX; pi += CT_THREADS / 32) {
+      const int mm = m0 + pi;
+      if (mm < p.cap * ohw && c0 + lane < p.c)
+        xh[size_t(mm) * p.c + c0 + lane] = __float2bfloat16_rn(ic_tile[pi * ld + lane * kk2 + centre]);
+    }
+  }
   if (p.bf16) {
     __nv_bfloat16* cb16 = reinterpret_cast<__nv_bfloat16*>(p.cols);
     for (int pi = warp; pi < IC_PIX && cb16; pi += CT_THREADS / 32) {  // (no cols: implicit-GEMM forward)
@@ -191,20 +202,26 @@ __device__ __forceinline__ void col2im_tile(const hnn_convtc_problem& p, int row
   // (a row-at-a-time copy loop serialised ~13 L2 round trips per warp)
   __shared__ int row_src[K * CI_OWMAX], row_dst[K * CI_OWMAX];
   __shared__ int nrows_s;
-  if (threadIdx.x == 0) {
-    int n = 0;
-    if (live_rows && nw > 0) {
-      for (int r = 0; r < K; ++r) {
-        const int hh = h + p.pad - r;
-        if (hh < 0 || (STRIDE > 1 && hh % STRIDE) || hh / STRIDE >= p.oh) continue;
-        for (int i = 0; i < nw; ++i, ++n) {
-          row_src[n] = int(((size_t(b) * p.oh + hh / STRIDE) * p.ow + ow_lo + i) * p.kkp / 4);
-          row_dst[n] = (r * CI_OWMAX + i) * SLD;
-        }
-      }
-    }
-    nrows_s = n;
+  // valid tap rows r (compile-time K: a handful of compares), then one table entry per thread
+  // (a single thread filling the table serially was most of this kernel's time)
+  int vr[K], nvr = 0;
+#pragma unroll
+  for (int r = 0; r < K; ++r) {
+    const int hh = h + p.pad - r;
+    vr[r] = 0;
+    if (live_rows && nw > 0 && hh >= 0 && !(STRIDE > 1 && hh % STRIDE) && hh / STRIDE < p.oh) vr[nvr++] = r;
   }
+  for (int e = threadIdx.x; e < nvr * nw; e += CT_THREADS) {
+    const int k = e / nw, i = e - k * nw;
+    int r = 0;
+#pragma unroll
+    for (int j = 0; j < K; ++j)
+      if (j == k) r = vr[j];
+    const int hh = h + p.pad - r;
+    row_src[e] = int(((size_t(b) * p.oh + hh / STRIDE) * p.ow + ow_lo + i) * p.kkp / 4);
+    row_dst[e] = (r * CI_OWMAX + i) * SLD;
+  }
+  if (threadIdx.x == 0) nrows_s = nvr * nw;
   __syncthreads();
   {
     const int width = min(SEG, (p.c - c0) * KK2);

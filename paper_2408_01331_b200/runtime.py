@@ -756,6 +756,11 @@ class DeviceHybrid:
                 out += self._conv_group(op, group, label + ("/direct" if direct else ""), direct)
         return out
 
+    def _same_conv(self, st) -> bool:
+        c, h, w = st.in_shape
+        _, oh, ow = self._conv_out(st)
+        return st.attrs.get("stride", 1) == 1 and (oh, ow) == (h, w)
+
     def _convtc_aux(self, aux, items, label, blocks_of, nbytes=None):
         probs, base = [], 0
         for s, st in items:
@@ -765,8 +770,11 @@ class DeviceHybrid:
             W = self.pview(self.grads, s.index, st.params[0])
             B = self.pview(self.grads, s.index, st.params[1])
             nb = blocks_of(s, st)
+            dyt = st.dyt
+            if aux == N.CONVTC_IM2COL:  # (im2col's dyt = the NHWC copy of x, "same" implicit layers)
+                dyt = st.xh if (st.im_fwd and self._same_conv(st)) else None
             probs.append(N.ConvTcProblem(
-                x=_ptr(st.x), cols=_ptr(st.cols), dy=_ptr(st.dy), dyt=_ptr(st.dyt),
+                x=_ptr(st.x), cols=_ptr(st.cols), dy=_ptr(st.dy), dyt=_ptr(dyt),
                 dcols=_ptr(s.dcols) if s.dcols is not None else 0, dx=_ptr(st.dx),
                 mask=_ptr(st.x) if st.mask_input else 0, partial=_ptr(st.partial), dw=_ptr(W), db=_ptr(B),
                 bpart=_ptr(st.bpart), weight=_ptr(self.pview(self.params, s.index, st.params[0])),
@@ -880,8 +888,10 @@ class DeviceHybrid:
         out = []
         if op == N.HNN_FWD:
             # (the padded weight copies come from the step's prep launch: conv_weight_prep)
-            imp = [(s, st) for s, st in items if st.im_fwd]
-            if imp:  # NHWC bf16 copies of the inputs for the implicit-GEMM layers
+            # NHWC bf16 copies of the inputs for the implicit-GEMM layers: written by the im2col
+            # launch for "same" layers (output pixel = input pixel), a transpose otherwise
+            imp = [(s, st) for s, st in items if st.im_fwd and not self._same_conv(st)]
+            if imp:
                 probs = []
                 for s, st in imp:
                     c, h, w = st.in_shape
