@@ -161,6 +161,10 @@ typedef struct hnn_gemm_problem {
    *               c[((m / row_mult) * n_total + n) * row_mult + m % row_mult], n_total = n; with
    *               c_mode 1 a non-NULL mask (same NCHW layout) multiplies by (mask > 0) and a NULL
    *               bias adds nothing (a conv input gradient computed as a forward conv of dy);
+   *               2 + (ph * 2 + pw): NCHW into one parity class of a grid twice as large in each
+   *               direction, element (m, n) with hw = m % row_mult = i * im_ow + j at
+   *               c[((m / row_mult) * n_total + n) * 4 * row_mult + (2i + ph) * 2 * im_ow + 2j + pw]
+   *               (a stride-2 conv's input gradient as four stride-1 convs of dy);
    *   ksplit      WGRAD fixed K split count (>= 1): split s covers K rows [s*ksplit_len,
    *               (s+1)*ksplit_len) and writes rows [s*mp, s*mp + m) of c, mp = m rounded up
    *               to 32 (the TMA map covers ksplit*mp rows); the splits are summed in order by
@@ -172,11 +176,11 @@ typedef struct hnn_gemm_problem {
   /* HNN_PREC_F32_3XTF32_PAIR: tile columns 64, 128 or 256 (0 = 256); the K-major B TMA box is
    * tile_n / 2 rows (each CTA of the pair stages half of the tile's B columns). */
   int32_t tile_n;
-  int32_t reserved;
+  int32_t im_kw;  /* implicit convolution: taps per row (0 = im_k, i.e. square) */
   /* HNN_PREC_BF16_PAIR FWD, implicit convolution (im_c > 0): A is not a [m, k] matrix but NHWC
    * bf16 activations a[n][h][w][c] (im_n x im_h x im_w x im_c, c contiguous, im_c % 64 == 0); GEMM
    * row m = (b, oh, ow) of a stride-1 conv's im_oh x im_ow output (row_mult = im_oh * im_ow) and
-   * K = (r, s, c) over the im_k x im_k taps with padding im_pad (taps outside the image read as
+   * K = (r, s, c) over the im_k x im_kw taps with padding im_pad (taps outside the image read as
    * zeros, by the TMA), so the B rows are in (r, s, c) order (HNN_CONVTC_PAD_WEIGHTS_RSC /
    * FLIP_WEIGHTS_RSC).  Each 128-row CTA tile must be whole output rows of whole or one image:
    * 128 % im_ow == 0 and (im_oh * im_ow) % 128 == 0 or 128 % (im_oh * im_ow) == 0. */
@@ -345,6 +349,9 @@ int hnn_multi_tensor_adam(const hnn_opt_segment* segs, int nseg, int total_chunk
 #define HNN_CONVTC_PAD_WEIGHTS_RSC 7  /* bf16 wpad[f, (r, s, c)] = w[f, c, r, s]: implicit-GEMM forward B */
 #define HNN_CONVTC_FLIP_WEIGHTS_RSC 8 /* bf16 wpad[c, (r, s, f)] = w[f, c, k-1-r, k-1-s]: implicit-GEMM input
                                          gradient (forward conv of NHWC dy) B */
+#define HNN_CONVTC_PARITY_WEIGHTS 9   /* 3x3 / stride 2 / pad 1 input gradient as four stride-1 convs of dy:
+                                         class q = ksplit (ph = q >> 1, pw = q & 1), taps rr < 1 + ph,
+                                         ss < 1 + pw: bf16 wpad[c, (rr, ss, f)] = w[f, c, ph+1-2rr, pw+1-2ss] */
 
 typedef struct hnn_convtc_problem {
   const float* x;    /* [cap, c, h, w] */

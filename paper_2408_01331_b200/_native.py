@@ -17,6 +17,7 @@ HNN_FWD, HNN_DGRAD, HNN_WGRAD = 0, 1, 2
 PREC_SIMT, PREC_3XTF32, PREC_SIMT_SKINNY, PREC_3XTF32_PAIR, PREC_BF16_PAIR = 0, 1, 2, 3, 4
 CONVTC_IM2COL, CONVTC_TRANSPOSE_DY, CONVTC_COL2IM, CONVTC_WGRAD_REDUCE, CONVTC_PAD_WEIGHTS = 0, 1, 2, 3, 4
 CONVTC_FLIP_WEIGHTS, CONVTC_WT_WEIGHTS, CONVTC_PAD_WEIGHTS_RSC, CONVTC_FLIP_WEIGHTS_RSC = 5, 6, 7, 8
+CONVTC_PARITY_WEIGHTS = 9
 OPT_SGD, OPT_SGD_MOMENTUM, OPT_ADAM = 0, 1, 2
 CONV_DIRECT_BCHUNK = 1
 
@@ -46,7 +47,7 @@ class GemmProblem(C.Structure):
                 ("model", I), ("relu", I), ("tile_base", I), ("tiles_n", I), ("tmap_a", P), ("tmap_b", P),
                 ("tmap_c", P), ("opt_w", P), ("opt_wm", P), ("opt_wv", P), ("opt_b", P), ("opt_bm", P),
                 ("opt_bv", P), ("opt_kind", I), ("opt_momentum", C.c_float),
-                ("row_mult", I), ("c_mode", I), ("ksplit", I), ("ksplit_len", I), ("tile_n", I), ("reserved", I),
+                ("row_mult", I), ("c_mode", I), ("ksplit", I), ("ksplit_len", I), ("tile_n", I), ("im_kw", I),
                 ("im_c", I), ("im_k", I), ("im_pad", I), ("im_h", I), ("im_w", I), ("im_oh", I), ("im_ow", I),
                 ("im_n", I)]
 

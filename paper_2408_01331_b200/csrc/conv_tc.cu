@@ -394,6 +394,25 @@ __global__ void __launch_bounds__(CT_THREADS) rsc_weights_kernel(const hnn_convt
   }
 }
 
+// Parity-class weights of a 3x3 / stride-2 / pad-1 input gradient (HNN_CONVTC_PARITY_WEIGHTS): dx at
+// (2i + ph, 2j + pw) = sum over rr < 1 + ph, ss < 1 + pw of dy[i + rr][j + ss] . w[., ., ph+1-2rr, pw+1-2ss]
+__global__ void __launch_bounds__(CT_THREADS) parity_weights_kernel(const hnn_convtc_problem* __restrict__ probs,
+                                                                   int nprob, const hnn_step_row* __restrict__ cur,
+                                                                   const hnn_model_status* __restrict__ status) {
+  const hnn_convtc_problem& p = ct_problem(probs, nprob, blockIdx.x);
+  if (!live(cur, status, p.model)) return;
+  const int ph = p.ksplit >> 1, pw = p.ksplit & 1, kh = 1 + ph, kw = 1 + pw;
+  const long long row = (long long)kh * kw * p.f, total = (long long)p.c * row;
+  for (long long e = (long long)(blockIdx.x - p.block_base) * CT_THREADS + threadIdx.x; e < total;
+       e += (long long)p.blocks * CT_THREADS) {
+    const int c = int(e / row), j = int(e - (long long)c * row);
+    const int rs = j / p.f, f = j - rs * p.f, rr = rs / kw, ss = rs - rr * kw;
+    const int r = ph + 1 - 2 * rr, sx = pw + 1 - 2 * ss;
+    reinterpret_cast<__nv_bfloat16*>(p.wpad)[e] =
+        __float2bfloat16_rn(__ldg(p.weight + ((size_t(f) * p.c + c) * 3 + r) * 3 + sx));
+  }
+}
+
 // bf16 wpad[kk, f] = w[f, kk] (kk < kkp; pad rows zero): the stride-2 dcols GEMM's K-major B.
 __global__ void __launch_bounds__(CT_THREADS) wt_weights_kernel(const hnn_convtc_problem* __restrict__ probs, int nprob,
                                                                const hnn_step_row* __restrict__ cur,
@@ -440,6 +459,9 @@ extern "C" int hnn_conv_tc_aux(int op, const hnn_convtc_problem* probs, int npro
       break;
     case HNN_CONVTC_FLIP_WEIGHTS_RSC:
       hnn::rsc_weights_kernel<true><<<total_blocks, hnn::CT_THREADS, 0, s>>>(probs, nprob, cur, status);
+      break;
+    case HNN_CONVTC_PARITY_WEIGHTS:
+      hnn::parity_weights_kernel<<<total_blocks, hnn::CT_THREADS, 0, s>>>(probs, nprob, cur, status);
       break;
     case HNN_CONVTC_WT_WEIGHTS:
       hnn::wt_weights_kernel<<<total_blocks, hnn::CT_THREADS, 0, s>>>(probs, nprob, cur, status);

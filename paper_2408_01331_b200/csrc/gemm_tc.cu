@@ -500,7 +500,7 @@ extern "C" int hnn_gemm_tc_encode(int op, const hnn_gemm_problem* host_probs, in
     // (a K-split WGRAD writes ksplit stacked [m, n] partials)
     const uint64_t crows = (op == HNN_WGRAD && p.ksplit > 1) ? uint64_t((p.m + 31) & ~31) * uint64_t(p.ksplit)
                                                              : uint64_t(p.m);
-    if (!rc && p.c && p.c_mode == 0)  // (c_mode 1 stores NCHW directly, no map)
+    if (!rc && p.c && p.c_mode == 0)  // (c_mode >= 1 stores NCHW directly, no map)
       rc = hnn::encode_2d(&maps[3 * i + 2], p.c, p.n, crows, p.ldc, 32, false);
     if (rc) {
       hnn::set_error("hnn_gemm_tc_encode", "cuTensorMapEncodeTiled failed (alignment / stride / driver)");
@@ -521,7 +521,8 @@ extern "C" int hnn_gemm_bf16_encode(int op, const hnn_gemm_problem* host_probs, 
     if (p.im_c > 0) {  // implicit-GEMM convolution: A = NHWC activations
       const int hw = p.im_oh * p.im_ow;
       HNN_REQUIRE(op == HNN_FWD && p.im_c % 64 == 0 && p.im_ow > 0 && 128 % p.im_ow == 0 &&
-                      (hw % 128 == 0 || 128 % hw == 0) && p.k == p.im_k * p.im_k * p.im_c,
+                      (hw % 128 == 0 || 128 % hw == 0) &&
+                      p.k == p.im_k * (p.im_kw > 0 ? p.im_kw : p.im_k) * p.im_c,
                   "hnn_gemm_bf16_encode", "implicit convolution geometry not supported");
       rc = hnn::encode_nhwc_bf16(&maps[3 * i], p.a, p);
     } else {
@@ -530,7 +531,7 @@ extern "C" int hnn_gemm_bf16_encode(int op, const hnn_gemm_problem* host_probs, 
     if (!rc) rc = hnn::encode_2d_bf16(&maps[3 * i + 1], p.b, p.k, p.n, p.ldb, brows);
     const uint64_t crows = (op == HNN_WGRAD && p.ksplit > 1) ? uint64_t((p.m + 31) & ~31) * uint64_t(p.ksplit)
                                                              : uint64_t(p.m);
-    if (!rc && p.c && p.c_mode == 0)  // (c_mode 1 stores NCHW directly, no map)
+    if (!rc && p.c && p.c_mode == 0)  // (c_mode >= 1 stores NCHW directly, no map)
       rc = hnn::encode_2d(&maps[3 * i + 2], p.c, p.n, crows, p.ldc, 32, false);
     if (rc) {
       hnn::set_error("hnn_gemm_bf16_encode", "cuTensorMapEncodeTiled failed (alignment / stride / driver)");

@@ -270,7 +270,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC2_THREADS, 1)
           } else if (BF16 && OP == HNN_FWD && p->im_c > 0) {
             // implicit-GEMM convolution: K block kb = tap (r, s) x 64 channels of the NHWC input,
             // this CTA's 128 output pixels = whole output rows (or images) starting at (b0, oh0)
-            const int cbk = p->im_c / 64, tap = kb / cbk, r = tap / p->im_k, sx = tap - r * p->im_k;
+            const int kw = p->im_kw > 0 ? p->im_kw : p->im_k;
+            const int cbk = p->im_c / 64, tap = kb / cbk, r = tap / kw, sx = tap - r * kw;
             const int hw = p->im_oh * p->im_ow, b0 = am / hw, oh0 = (am - b0 * hw) / p->im_ow;
             tma_load_4d(st, p->tmap_a, bar(RAW_FULL + s), (kb - tap * cbk) * 64, sx - p->im_pad, oh0 + r - p->im_pad, b0);
           } else {
@@ -447,7 +448,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC2_THREADS, 1)
       float* const ow = p->opt_w;
       float* const owm = p->opt_wm;
       const bool fuse = OP == HNN_WGRAD && ow != nullptr;
-      const bool nchw = OP == HNN_FWD && p->c_mode == 1;  // conv output straight to NCHW
+      const bool nchw = OP == HNN_FWD && p->c_mode >= 1;  // conv output straight to NCHW (c_mode >= 2: a parity class)
       const float* nmask = nchw ? p->mask : nullptr;
       const int nchw_b = nchw ? (m0 + int(rank) * TC2_BM + q * 32 + lane) / p->row_mult : 0;  // row's sample
       const int nchw_hw = nchw ? (m0 + int(rank) * TC2_BM + q * 32 + lane) - nchw_b * p->row_mult : 0;
@@ -488,14 +489,21 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC2_THREADS, 1)
           // dgrad launches' time)
           constexpr int NG = BF16 ? 8 : 2;  // (fp32: the running sum holds 128 registers)
           const bool rok = row < pm;
-          const size_t ybase = rok ? size_t(nchw_b) * pn * hw_n + nchw_hw : 0;
+          // c_mode >= 2: pixel (i, j) of parity class (ph, pw) lands at (2i + ph, 2j + pw) of a
+          // 4x larger plane
+          const int cm = p->c_mode, par = cm >= 2;
+          const int plane = par ? 4 * hw_n : hw_n;
+          const int pix = par ? (2 * (nchw_hw / p->im_ow) + ((cm - 2) >> 1)) * 2 * p->im_ow + 2 * (nchw_hw % p->im_ow) +
+                                    ((cm - 2) & 1)
+                              : nchw_hw;
+          const size_t ybase = rok ? size_t(nchw_b) * pn * plane + pix : 0;
 #pragma unroll
           for (int g = 0; g < 32 / NG; ++g) {
             float mk[NG];
 #pragma unroll
             for (int jj = 0; jj < NG; ++jj) {
               const int n = nh + cb + g * NG + jj;
-              mk[jj] = (nmask && rok && n < pn) ? __ldg(nmask + ybase + size_t(n) * hw_n) : 1.0f;
+              mk[jj] = (nmask && rok && n < pn) ? __ldg(nmask + ybase + size_t(n) * plane) : 1.0f;
             }
 #pragma unroll
             for (int jj = 0; jj < NG; ++jj) {
@@ -507,7 +515,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC2_THREADS, 1)
                 x = __fadd_rn(x, b);
                 if (relu) x = np_relu(x);
               }
-              if (rok && n < pn) cptr[ybase + size_t(n) * hw_n] = nmask ? (zero_row ? 0.0f : np_mask(x, mk[jj])) : x;
+              if (rok && n < pn) cptr[ybase + size_t(n) * plane] = nmask ? (zero_row ? 0.0f : np_mask(x, mk[jj])) : x;
             }
           }
           continue;

@@ -59,6 +59,15 @@ def _implicit_tiles(oh: int, ow: int) -> bool:
     return ow <= 128 and 128 % ow == 0 and ((oh * ow) % 128 == 0 or 128 % (oh * ow) == 0)
 
 
+def _parity_offsets(c: int, f: int) -> list:
+    """Element offsets of the four parity-class weight blocks [c, kh*kw*f] inside wpar (9*c*f)."""
+    offs, o = [], 0
+    for q in range(4):
+        offs.append(o)
+        o += c * f * (1 + (q >> 1)) * (1 + (q & 1))
+    return offs
+
+
 def _align4(n: int) -> int:
     return (n + 3) // 4 * 4
 
@@ -107,6 +116,8 @@ class Stage:
     im_fwd: bool = False       # implicit-GEMM forward over xh (NHWC bf16 copy of x)
     im_dg: bool = False        # implicit-GEMM input gradient over dyt (NHWC dy)
     xh = None
+    par_dg: bool = False       # stride-2 input gradient as four parity-class implicit convs
+    wpar = None
 
 
 def lower_graph(graph) -> tuple:
@@ -421,6 +432,12 @@ class DeviceHybrid:
                         # flipped weights, no im2col of dy
                         st.im_dg = (self.implicit_conv and st.bf16 and st.needs_dx and st.dg_fwd and f % 64 == 0
                                     and _implicit_tiles(h, w))
+                        # stride-2 3x3 input gradient as four stride-1 implicit convs of the NHWC dy
+                        # (one per output parity class), no dcols / col2im
+                        st.par_dg = (self.implicit_conv and st.bf16 and st.needs_dx and not st.dg_fwd and k == 3
+                                     and stride == 2 and st.attrs.get("padding", 0) == 1 and (h, w) == (2 * oh, 2 * ow)
+                                     and f % 64 == 0 and _implicit_tiles(oh, ow))
+                        st.wpar = torch.zeros(9 * c * f, dtype=wdt, device=dev) if st.par_dg else None
                         if not st.bf16 or (st.needs_dx and not st.dg_fwd) or st.im_dg:
                             st.dyt = torch.zeros(pix * st.fld, dtype=wdt, device=dev)
                         if st.needs_dx and st.dg_fwd:
@@ -429,7 +446,7 @@ class DeviceHybrid:
                                 dgb_need = max(dgb_need, cap * h * w * f * k * k)
                             else:
                                 dcols_need = max(dcols_need, cap * h * w * f * k * k)
-                        elif st.needs_dx:
+                        elif st.needs_dx and not st.par_dg:
                             dcols_need = max(dcols_need, pix * kk)
                             if st.bf16:
                                 st.wt = torch.zeros(kk * f, dtype=wdt, device=dev)
@@ -924,6 +941,23 @@ class DeviceHybrid:
             if not items:
                 return out
             out.append(self._convtc_aux(N.CONVTC_TRANSPOSE_DY, items, f"{label}/tc/transpose", tiles_t))
+            par = [(s, st) for s, st in items if st.par_dg]
+            if par:
+                prow = []
+                for s, st in par:
+                    c, h, w, f, oh, ow, kk = geo(st)
+                    for q, off in enumerate(_parity_offsets(c, f)):
+                        kh, kw = 1 + (q >> 1), 1 + (q & 1)
+                        prow.append((s, dict(a=_ptr(st.dyt), b=_ptr(st.wpar) + 2 * off, c=_ptr(st.dx), bias=0,
+                                             mask=_ptr(st.x) if st.mask_input else 0, dbias=0,
+                                             m=s.batch_size * oh * ow, n=c, k=kh * kw * f, lda=st.fld,
+                                             ldb=kh * kw * f, ldc=c, relu=0, row_mult=oh * ow, c_mode=2 + q,
+                                             im_c=f, im_k=kh, im_kw=kw, im_pad=0, im_h=oh, im_w=ow, im_oh=oh,
+                                             im_ow=ow, im_n=s.batch_size)))
+                out += self._emit_gemm(N.HNN_FWD, N.PREC_BF16_PAIR, prow, f"{label}/tc/dgpar")
+            items = [(s, st) for s, st in items if not st.par_dg]
+            if not items:
+                return out
             rows = {}
             for s, st in items:
                 c, h, w, f, oh, ow, kk = geo(st)
@@ -998,7 +1032,19 @@ class DeviceHybrid:
             max_k = max(pr.k for _, pr in flips)
             out.append(self._aux_table(N.CONVTC_FLIP_WEIGHTS, flips, "prep/conv/tc/flipw",
                                        lambda pr: self._aux_grid(pr.c * pr.f * pr.k * pr.k), max_k))
-        wt = [(s, st) for s, st in stages if st.needs_dx and not st.dg_fwd and st.bf16]
+        par = []
+        for s, st in stages:
+            if st.par_dg:
+                c, f = st.in_shape[0], self._conv_out(st)[0]
+                W = self.pview(self.params, s.index, st.params[0])
+                for q, off in enumerate(_parity_offsets(c, f)):
+                    par.append((s, N.ConvTcProblem(weight=_ptr(W), wpad=_ptr(st.wpar) + 2 * off, c=c, f=f, k=3,
+                                                   ksplit=q, model=s.index, bf16=1)))
+        if par:
+            out.append(self._aux_table(N.CONVTC_PARITY_WEIGHTS, par, "prep/conv/tc/parity_w",
+                                       lambda pr: self._aux_grid(pr.c * pr.f * (1 + (pr.ksplit >> 1)) * (1 + (pr.ksplit & 1))),
+                                       3))
+        wt = [(s, st) for s, st in stages if st.needs_dx and not st.dg_fwd and st.bf16 and not st.par_dg]
         if wt:
             out.append(self._convtc_aux(N.CONVTC_WT_WEIGHTS, wt, "prep/conv/tc/wt", blocks))
         return out

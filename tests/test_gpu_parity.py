@@ -657,15 +657,18 @@ def test_bf16_tensor_core_convs_track_oracle(pkg):
 def test_implicit_gemm_convs_match_explicit(pkg, monkeypatch):
     """bf16 implicit-GEMM convolutions (NHWC activations through 4D TMA boxes, K in (r, s, c) order,
     taps outside the image zero-filled by the TMA) against the explicit im2col path: whole-row
-    tiles (16 x 16), two images per tile (8 x 8), and a padding-0 layer whose input gradient is an
-    implicit conv with padding 2.  Same bf16 operands, different fp32 summation order: first-step
-    gradients agree to 1e-2 (relative, max-abs) and both track the fp32 oracle to 1e-1."""
+    tiles (16 x 16), two images per tile (8 x 8), 32 images per tile (2 x 2), a stride-2 layer
+    whose input gradient runs as four parity-class convs of dy, and a padding-0 layer whose input
+    gradient is an implicit conv with padding 2.  Same bf16 operands, different fp32 summation
+    order: first-step gradients agree to 1e-2 (relative, max-abs) and both track the fp32 oracle
+    to 1e-1."""
     from paper_2408_01331_b200 import store, zoo
 
     spec = [("conv0", "conv2d", {"filters": 64, "kernel": 3, "padding": 1}), ("act0", "relu", {}),
             ("conv1", "conv2d", {"filters": 64, "kernel": 3, "padding": 1}), ("act1", "relu", {}),
             ("pool1", "maxpool2d", {"kernel": 2}),
             ("conv2", "conv2d", {"filters": 128, "kernel": 3, "padding": 1}), ("act2", "relu", {}),
+            ("conv2s", "conv2d", {"filters": 128, "kernel": 3, "padding": 1, "stride": 2}), ("act2s", "relu", {}),
             ("conv3", "conv2d", {"filters": 64, "kernel": 3, "padding": 0}), ("act3", "relu", {}),
             ("pool3", "maxpool2d", {"kernel": 2}),
             ("flat", "flatten", {}), ("fc", "dense", {"units": 10})]
@@ -687,9 +690,11 @@ def test_implicit_gemm_convs_match_explicit(pkg, monkeypatch):
 
     imp, st = run(True)
     assert st["conv1"].im_fwd and st["conv1"].im_dg and st["conv2"].im_fwd and st["conv3"].im_dg
-    assert not st["conv0"].im_fwd and not st["conv3"].im_fwd
+    assert st["conv2s"].par_dg and not st["conv2s"].im_fwd
+    assert st["conv3"].im_fwd  # 2 x 2 output: 32 images per tile
+    assert not st["conv0"].im_fwd
     exp, st0 = run(False)
-    assert not any(s.im_fwd or s.im_dg for s in st0.values() if s.kind == "conv")
+    assert not any(s.im_fwd or s.im_dg or s.par_dg for s in st0.values() if s.kind == "conv")
     params = oracle.init_model(graph, 4)
     bx, by, _ = oracle.epoch_batches(splits["train_x"], splits["train_y"], ds.content_hash, 32, 4, 0)[0]
     logits, tape = oracle.model_forward(graph, params, bx)
