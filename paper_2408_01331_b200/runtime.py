@@ -54,6 +54,9 @@ def _torch():
     return torch
 
 
+RSC_STAGE_MAX = 512 * 9  # k*k*channels one (r, s, c) weight-permute CTA stages (csrc/conv_tc.cu RSC_MAX)
+
+
 def _implicit_tiles(oh: int, ow: int) -> bool:
     """A 128-row GEMM tile is whole output rows of one image, or whole images (the 4D TMA box)."""
     return ow <= 128 and 128 % ow == 0 and ((oh * ow) % 128 == 0 or 128 % (oh * ow) == 0)
@@ -415,7 +418,7 @@ class DeviceHybrid:
                         # whole rows / images): the GEMM reads an NHWC copy of x through a 4D TMA map,
                         # no cols matrix (im2col still writes the weight-gradient copy colst)
                         st.im_fwd = (self.implicit_conv and st.bf16 and stride == 1 and c % 64 == 0
-                                     and _implicit_tiles(oh, ow))
+                                     and k * k * c <= RSC_STAGE_MAX and _implicit_tiles(oh, ow))
                         st.xh = torch.zeros(cap * h * w * c, dtype=wdt, device=dev) if st.im_fwd else None
                         st.cols = None if st.im_fwd else torch.zeros(pix * kk, dtype=wdt, device=dev)
                         st.bpart = torch.zeros(cap * -(-(oh * ow) // 32) * f, dtype=torch.float32, device=dev)
@@ -431,7 +434,7 @@ class DeviceHybrid:
                         # implicit-GEMM input gradient: a forward conv of the NHWC dy (dyt) with the
                         # flipped weights, no im2col of dy
                         st.im_dg = (self.implicit_conv and st.bf16 and st.needs_dx and st.dg_fwd and f % 64 == 0
-                                    and _implicit_tiles(h, w))
+                                    and k * k * f <= RSC_STAGE_MAX and _implicit_tiles(h, w))
                         # stride-2 3x3 input gradient as four stride-1 implicit convs of the NHWC dy
                         # (one per output parity class), no dcols / col2im
                         st.par_dg = (self.implicit_conv and st.bf16 and st.needs_dx and not st.dg_fwd and k == 3
@@ -1010,8 +1013,9 @@ class DeviceHybrid:
         if padded:
             out.append(self._convtc_aux(N.CONVTC_PAD_WEIGHTS, padded, "prep/conv/tc/padw", blocks))
         rsc = [(s, st) for s, st in stages if st.im_fwd]
-        if rsc:  # (r, s, c)-ordered K for the implicit-GEMM forward
-            out.append(self._convtc_aux(N.CONVTC_PAD_WEIGHTS_RSC, rsc, "prep/conv/tc/padw_rsc", blocks))
+        if rsc:  # (r, s, c)-ordered K for the implicit-GEMM forward: one CTA per filter (grid-stride)
+            out.append(self._convtc_aux(N.CONVTC_PAD_WEIGHTS_RSC, rsc, "prep/conv/tc/padw_rsc",
+                                        lambda s, st: min(self._conv_out(st)[0], 148)))
         if not train:
             return out
         flips, flips_rsc = [], []
@@ -1024,9 +1028,9 @@ class DeviceHybrid:
                 (flips_rsc if st.im_dg else flips).append(
                     (s, N.ConvTcProblem(weight=_ptr(W), wpad=_ptr(st.wflip), c=c, f=f, k=k, model=s.index,
                                         bf16=int(st.bf16))))
-        if flips_rsc:
+        if flips_rsc:  # one CTA per input channel (grid-stride)
             out.append(self._aux_table(N.CONVTC_FLIP_WEIGHTS_RSC, flips_rsc, "prep/conv/tc/flipw_rsc",
-                                       lambda pr: self._aux_grid(pr.c * pr.f * pr.k * pr.k),
+                                       lambda pr: min(pr.c, 148),
                                        max(pr.k for _, pr in flips_rsc)))
         if flips:
             max_k = max(pr.k for _, pr in flips)
