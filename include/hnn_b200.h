@@ -183,7 +183,11 @@ typedef struct hnn_gemm_problem {
    * K = (r, s, c) over the im_k x im_kw taps with padding im_pad (taps outside the image read as
    * zeros, by the TMA), so the B rows are in (r, s, c) order (HNN_CONVTC_PAD_WEIGHTS_RSC /
    * FLIP_WEIGHTS_RSC).  Each 128-row CTA tile must be whole output rows of whole or one image:
-   * 128 % im_ow == 0 and (im_oh * im_ow) % 128 == 0 or 128 % (im_oh * im_ow) == 0. */
+   * 128 % im_ow == 0 and (im_oh * im_ow) % 128 == 0 or 128 % (im_oh * im_ow) == 0.
+   * WGRAD with im_c > 0: B (the weight-gradient GEMM's N = (r, s, c) x K = output pixels operand)
+   * is read implicitly from the same NHWC activations as an MN-major operand, 64 pixels x 64
+   * channels of one tap per CTA (tile_n must be 128; 64-pixel K blocks of whole rows / images);
+   * A (dy, [f, pixels]) stays an ordinary K-major matrix. */
   int32_t im_c, im_k, im_pad, im_h, im_w, im_oh, im_ow, im_n;
 } hnn_gemm_problem;
 
@@ -378,6 +382,10 @@ typedef struct hnn_convtc_problem {
   void* dyk;
   int32_t bf16;
   int32_t pix_ld;
+  /* HNN_CONVTC_WGRAD_REDUCE: the partial columns are in (r, s, c) order (implicit-GEMM weight
+   * gradient); dw is still written in the reference [f, c, r, s] layout */
+  int32_t rsc;
+  int32_t reserved;
 } hnn_convtc_problem;
 
 int hnn_conv_tc_aux(int op, const hnn_convtc_problem* probs, int nprob, int total_blocks, int max_k,

@@ -71,7 +71,7 @@ class ConvTcProblem(C.Structure):
                 ("cap", I), ("c", I), ("h", I), ("w", I), ("f", I), ("k", I), ("stride", I), ("pad", I),
                 ("oh", I), ("ow", I), ("kk", I), ("kkp", I), ("ksplit", I), ("ksplit_len", I),
                 ("model", I), ("block_base", I), ("blocks", I), ("colst", P), ("dyk", P), ("bf16", I),
-                ("pix_ld", I)]
+                ("pix_ld", I), ("rsc", I), ("reserved", I)]
 
 
 class EmbedProblem(C.Structure):

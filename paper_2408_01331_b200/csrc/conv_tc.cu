@@ -46,6 +46,22 @@ __global__ void __launch_bounds__(CT_THREADS) im2col_kernel(const hnn_convtc_pro
   const int m = m0 + lane;
   const int b = m / ohw, o = m - b * ohw, oh = o / p.ow, ow = o - oh * p.ow;
   const bool valid = m < p.cap * ohw && b < rows;
+  if (p.bf16 && !p.cols && !p.colst) {
+    // only the NHWC copy (implicit-GEMM forward and weight gradient of a "same" layer): one tap,
+    // through a 32 x 33 transpose tile; zeros past the batch
+    float* t = ic_tile;
+    for (int ci = warp; ci < IC_CH; ci += CT_THREADS / 32) {
+      const int c = c0 + ci;
+      t[lane * 33 + ci] = (valid && c < p.c) ? __ldg(p.x + (size_t(b) * p.c + c) * ohw + o) : 0.0f;
+    }
+    __syncthreads();
+    __nv_bfloat16* xh = reinterpret_cast<__nv_bfloat16*>(p.dyt);
+    for (int pi = warp; pi < IC_PIX; pi += CT_THREADS / 32) {
+      const int mm = m0 + pi;
+      if (mm < p.cap * ohw && c0 + lane < p.c) xh[size_t(mm) * p.c + c0 + lane] = __float2bfloat16_rn(t[pi * 33 + lane]);
+    }
+    return;
+  }
   if (p.k == 3) {  // the common 3 x 3 case: a channel's 9 taps load together (independent requests)
     for (int ci = warp; ci < IC_CH; ci += CT_THREADS / 32) {
       const int c = c0 + ci;
@@ -316,7 +332,14 @@ __global__ void __launch_bounds__(CT_THREADS) wgrad_reduce_kernel(const hnn_conv
   const long long total = (long long)p.f * p.kk, ptotal = (long long)((p.f + 31) & ~31) * p.kkp;
   const long long tid = (long long)(blockIdx.x - p.block_base) * CT_THREADS + threadIdx.x;
   for (long long e = tid; e < total; e += (long long)p.blocks * CT_THREADS) {
-    const long long f = e / p.kk, pe = f * p.kkp + (e - f * p.kk);  // partial rows are kkp wide
+    const long long f = e / p.kk, kr = e - f * p.kk;  // reference column (c, r, s)
+    long long col = kr;
+    if (p.rsc) {  // partial columns in (r, s, c) order
+      const int kk2 = p.k * p.k;
+      const long long c = kr / kk2;
+      col = (kr - c * kk2) * p.c + c;
+    }
+    const long long pe = f * p.kkp + col;  // partial rows are kkp wide
     float acc = 0.0f;
     for (int s = 0; s < splits; ++s) acc = __fadd_rn(acc, __ldg(p.partial + size_t(s) * ptotal + pe));
     p.dw[e] = acc;

@@ -410,16 +410,17 @@ int encode_2d_bf16(CUtensorMap* map, const void* ptr, uint64_t inner, uint64_t o
 
 // 4D bf16 map over NHWC activations for the implicit-GEMM convolution: dims {c, w, h, n}, box
 // {64, ow, box_h, box_n} = one 128-row K-major tile (rows (n, h, w), 128-byte swizzled rows).
-int encode_nhwc_bf16(CUtensorMap* map, const void* ptr, const hnn_gemm_problem& p) {
+int encode_nhwc_bf16(CUtensorMap* map, const void* ptr, const hnn_gemm_problem& p, int pixels) {
   EncodeTiled enc = encoder();
   if (!enc) return HNN_ERR_CUDA;
   const int hw = p.im_oh * p.im_ow;
-  const uint32_t box_h = uint32_t(hw >= 128 ? 128 / p.im_ow : p.im_oh), box_n = uint32_t(hw >= 128 ? 1 : 128 / hw);
+  const uint32_t box_h = uint32_t(hw >= pixels ? pixels / p.im_ow : p.im_oh),
+                 box_n = uint32_t(hw >= pixels ? 1 : pixels / hw);
   cuuint64_t dims[4] = {uint64_t(p.im_c), uint64_t(p.im_w), uint64_t(p.im_h), uint64_t(p.im_n)};
   cuuint64_t strides[3] = {uint64_t(p.im_c) * 2, uint64_t(p.im_w) * p.im_c * 2, uint64_t(p.im_h) * p.im_w * p.im_c * 2};
   cuuint32_t box[4] = {64, uint32_t(p.im_ow), box_h, box_n};
   cuuint32_t estr[4] = {1, 1, 1, 1};
-  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<float*>(p.a), dims, strides, box, estr,
+  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(ptr), dims, strides, box, estr,
                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS ? HNN_OK : HNN_ERR_CUDA;
@@ -518,17 +519,25 @@ extern "C" int hnn_gemm_bf16_encode(int op, const hnn_gemm_problem* host_probs, 
     const hnn_gemm_problem& p = host_probs[i];
     const uint32_t brows = p.tile_n > 0 ? uint32_t(p.tile_n / 2) : 128u;
     int rc;
-    if (p.im_c > 0) {  // implicit-GEMM convolution: A = NHWC activations
-      const int hw = p.im_oh * p.im_ow;
-      HNN_REQUIRE(op == HNN_FWD && p.im_c % 64 == 0 && p.im_ow > 0 && 128 % p.im_ow == 0 &&
-                      (hw % 128 == 0 || 128 % hw == 0) &&
-                      p.k == p.im_k * (p.im_kw > 0 ? p.im_kw : p.im_k) * p.im_c,
+    const int hw = p.im_oh * p.im_ow;
+    const int taps = p.im_k * (p.im_kw > 0 ? p.im_kw : p.im_k);
+    if (p.im_c > 0 && op == HNN_FWD) {  // implicit-GEMM convolution: A = NHWC activations
+      HNN_REQUIRE(p.im_c % 64 == 0 && p.im_ow > 0 && 128 % p.im_ow == 0 && (hw % 128 == 0 || 128 % hw == 0) &&
+                      p.k == taps * p.im_c,
                   "hnn_gemm_bf16_encode", "implicit convolution geometry not supported");
-      rc = hnn::encode_nhwc_bf16(&maps[3 * i], p.a, p);
+      rc = hnn::encode_nhwc_bf16(&maps[3 * i], p.a, p, 128);
     } else {
       rc = hnn::encode_2d_bf16(&maps[3 * i], p.a, p.k, p.m, p.lda, hnn::TC_BM);
     }
-    if (!rc) rc = hnn::encode_2d_bf16(&maps[3 * i + 1], p.b, p.k, p.n, p.ldb, brows);
+    if (rc) {
+    } else if (p.im_c > 0 && op == HNN_WGRAD) {  // implicit weight gradient: B = NHWC activations, MN-major
+      HNN_REQUIRE(p.im_c % 64 == 0 && p.tile_n == 128 && p.im_ow > 0 && 64 % p.im_ow == 0 &&
+                      (hw % 64 == 0 || 64 % hw == 0) && p.n == taps * p.im_c,
+                  "hnn_gemm_bf16_encode", "implicit weight-gradient geometry not supported");
+      rc = hnn::encode_nhwc_bf16(&maps[3 * i + 1], p.b, p, 64);
+    } else {
+      rc = hnn::encode_2d_bf16(&maps[3 * i + 1], p.b, p.k, p.n, p.ldb, brows);
+    }
     const uint64_t crows = (op == HNN_WGRAD && p.ksplit > 1) ? uint64_t((p.m + 31) & ~31) * uint64_t(p.ksplit)
                                                              : uint64_t(p.m);
     if (!rc && p.c && p.c_mode == 0)  // (c_mode >= 1 stores NCHW directly, no map)

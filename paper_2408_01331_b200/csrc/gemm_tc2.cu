@@ -280,6 +280,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC2_THREADS, 1)
           if (B_MN) {
             for (int b = 0; b < tn / 64; ++b)
               tma_load_2d(st + TC2_A_BYTES + b * 4096, p->tmap_b, bar(RAW_FULL + s), bn + 32 * b, k0);
+          } else if (BF16 && OP == HNN_WGRAD && p->im_c > 0) {
+            // implicit weight gradient: this CTA's 64 columns = 64 channels of one tap (r, s) of
+            // the NHWC input; the K block = 64 output pixels (whole rows / images) -> MN-major tile
+            const int kw = p->im_kw > 0 ? p->im_kw : p->im_k;
+            const int tap = bn / p->im_c, c0 = bn - tap * p->im_c, r = tap / kw, sx = tap - r * kw;
+            const int hw = p->im_oh * p->im_ow, b0 = k0 / hw, oh0 = (k0 - b0 * hw) / p->im_ow;
+            // columns past the last tap (n not a multiple of 128) read an image past the end: zeros
+            tma_load_4d(st + TC2_A_BYTES, p->tmap_b, bar(RAW_FULL + s), c0, sx - p->im_pad, oh0 + r - p->im_pad,
+                        tap < p->im_k * kw ? b0 : p->im_n);
           } else {
             tma_load_2d(st + TC2_A_BYTES, p->tmap_b, bar(RAW_FULL + s), k0, bn);
           }
@@ -297,7 +306,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC2_THREADS, 1)
         const hnn_gemm_problem* p;
         int m0, n0, nkb, rows, kofs, sp, tn;
         if (!tile_info(tile, p, m0, n0, nkb, rows, kofs, sp, tn)) continue;
-        const uint32_t idesc = BF16 ? bf16_idesc(2 * TC2_BM, tn) : tf32_idesc(2 * TC2_BM, tn, A_MN, B_MN);
+        // (bf16 implicit weight gradient: B is MN-major, bit 16)
+        const bool b_imp = BF16 && OP == HNN_WGRAD && p->im_c > 0;
+        const uint32_t idesc =
+            BF16 ? (bf16_idesc(2 * TC2_BM, tn) | (b_imp ? (1u << 16) : 0u)) : tf32_idesc(2 * TC2_BM, tn, A_MN, B_MN);
         for (int kb = 0; kb < nkb; ++kb, ++kg) {
           const int in_chunk = BF16 ? kb : kb % TC2_CHUNK_KB;  // bf16: one chunk per tile (no promotion)
           const uint32_t buf = cg & 1;
@@ -315,8 +327,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC2_THREADS, 1)
           if (BF16) {
 #pragma unroll
             for (int j = 0; j < 4; ++j)  // K step 16 bf16 = +32 B inside the K-major rows
-              mma_f16_pair(acc, smem_desc(a_hi + j * 32, 16, 1024, 2), smem_desc(b_hi + j * 32, 16, 1024, 2), idesc,
-                           (in_chunk | j) != 0);
+              mma_f16_pair(acc, smem_desc(a_hi + j * 32, 16, 1024, 2),
+                           b_imp ? smem_desc(b_hi + j * 2048, 8192, 1024, 2)  // MN-major: 16 K rows = 2 KB
+                                 : smem_desc(b_hi + j * 32, 16, 1024, 2),
+                           idesc, (in_chunk | j) != 0);
           } else {
 #pragma unroll
             for (int j = 0; j < TC2_BK / 8; ++j) {

@@ -57,9 +57,9 @@ def _torch():
 RSC_STAGE_MAX = 512 * 9  # k*k*channels one (r, s, c) weight-permute CTA stages (csrc/conv_tc.cu RSC_MAX)
 
 
-def _implicit_tiles(oh: int, ow: int) -> bool:
-    """A 128-row GEMM tile is whole output rows of one image, or whole images (the 4D TMA box)."""
-    return ow <= 128 and 128 % ow == 0 and ((oh * ow) % 128 == 0 or 128 % (oh * ow) == 0)
+def _implicit_tiles(oh: int, ow: int, rows: int = 128) -> bool:
+    """A GEMM tile of `rows` output pixels is whole rows of one image, or whole images (4D TMA box)."""
+    return ow <= rows and rows % ow == 0 and ((oh * ow) % rows == 0 or rows % (oh * ow) == 0)
 
 
 def _parity_offsets(c: int, f: int) -> list:
@@ -119,6 +119,7 @@ class Stage:
     im_fwd: bool = False       # implicit-GEMM forward over xh (NHWC bf16 copy of x)
     im_dg: bool = False        # implicit-GEMM input gradient over dyt (NHWC dy)
     xh = None
+    im_wg: bool = False        # implicit-GEMM weight gradient (B = xh, MN-major)
     par_dg: bool = False       # stride-2 input gradient as four parity-class implicit convs
     wpar = None
 
@@ -420,12 +421,16 @@ class DeviceHybrid:
                         st.im_fwd = (self.implicit_conv and st.bf16 and stride == 1 and c % 64 == 0
                                      and k * k * c <= RSC_STAGE_MAX and _implicit_tiles(oh, ow))
                         st.xh = torch.zeros(cap * h * w * c, dtype=wdt, device=dev) if st.im_fwd else None
+                        # implicit weight gradient too (B = the same NHWC copy, MN-major, 64-pixel K
+                        # blocks): needs the zero-filled copy im2col writes for "same" layers
+                        st.im_wg = (st.im_fwd and stride == 1 and (oh, ow) == (h, w) and _implicit_tiles(oh, ow, 64)
+                                    and st.ksplit_len % 64 == 0)
                         st.cols = None if st.im_fwd else torch.zeros(pix * kk, dtype=wdt, device=dev)
                         st.bpart = torch.zeros(cap * -(-(oh * ow) // 32) * f, dtype=torch.float32, device=dev)
                         st.partial = torch.zeros(st.ksplit * (-(-f // 32) * 32) * kk, dtype=torch.float32,
                                                  device=dev)
                         if st.bf16:  # pixel-contiguous (K-major) weight-gradient operands
-                            st.colst = torch.zeros(kk * st.pix_ld, dtype=wdt, device=dev)
+                            st.colst = None if st.im_wg else torch.zeros(kk * st.pix_ld, dtype=wdt, device=dev)
                             st.dyk = torch.zeros(f * st.pix_ld, dtype=wdt, device=dev)
                         # input gradient: stride 1 -> a forward conv of dy (im2col of dy, flipped
                         # weights; scratch [cap*H*W, F*k*k]); stride 2 -> dcols GEMM + col2im
@@ -730,6 +735,8 @@ class DeviceHybrid:
                 tn_p = tn
                 if prec in (N.PREC_3XTF32_PAIR, N.PREC_BF16_PAIR):  # narrowest pair tile covering n
                     tn_p = min(cap, 64 if d["n"] <= 64 else (128 if d["n"] <= 128 else 256))
+                    if d.get("im_c") and op == N.HNN_WGRAD:
+                        tn_p = 128  # implicit weight gradient: one tap's 64 channels per CTA
                     d = dict(d, tile_n=tn_p)
                 tiles_m, tiles_n = -(-d["m"] // tm), -(-d["n"] // tn_p)
                 probs.append(N.GemmProblem(tile_base=base, tiles_n=tiles_n, model=s.index, **d))
@@ -798,7 +805,7 @@ class DeviceHybrid:
                 dcols=_ptr(s.dcols) if s.dcols is not None else 0, dx=_ptr(st.dx),
                 mask=_ptr(st.x) if st.mask_input else 0, partial=_ptr(st.partial), dw=_ptr(W), db=_ptr(B),
                 bpart=_ptr(st.bpart), weight=_ptr(self.pview(self.params, s.index, st.params[0])),
-                wpad=_ptr(st.wt if aux == N.CONVTC_WT_WEIGHTS else st.wpad), colst=_ptr(st.colst),
+                wpad=_ptr(st.wt if aux == N.CONVTC_WT_WEIGHTS else st.wpad), colst=_ptr(st.colst), rsc=int(st.im_wg),
                 dyk=_ptr(st.dyk), bf16=int(st.bf16), pix_ld=st.pix_ld, cap=s.batch_size, c=c, h=h, w=w, f=f, k=k,
                 stride=st.attrs.get("stride", 1), pad=st.attrs.get("padding", 0), oh=oh, ow=ow, kk=c * k * k,
                 kkp=st.kkp,
@@ -983,7 +990,11 @@ class DeviceHybrid:
         rows = {}
         for s, st in items:
             c, h, w, f, oh, ow, kk = geo(st)
-            if st.bf16:  # A = dy [f, pixels], B = cols^T [kkp, pixels]: both pixel-contiguous
+            if st.im_wg:  # A = dy [f, pixels]; B read from the NHWC x, columns (r, s, c)
+                d = dict(a=_ptr(st.dyk), b=_ptr(st.xh), lda=st.pix_ld, ldb=c, tile_n=128, im_c=c,
+                         im_k=st.attrs["kernel"], im_pad=st.attrs.get("padding", 0), im_h=h, im_w=w, im_oh=oh,
+                         im_ow=ow, im_n=s.batch_size)
+            elif st.bf16:  # A = dy [f, pixels], B = cols^T [kkp, pixels]: both pixel-contiguous
                 d = dict(a=_ptr(st.dyk), b=_ptr(st.colst), lda=st.pix_ld, ldb=st.pix_ld)
             else:
                 d = dict(a=_ptr(st.dyt), b=_ptr(st.cols), lda=st.fld, ldb=kk)

@@ -656,7 +656,8 @@ def test_bf16_tensor_core_convs_track_oracle(pkg):
 
 def test_implicit_gemm_convs_match_explicit(pkg, monkeypatch):
     """bf16 implicit-GEMM convolutions (NHWC activations through 4D TMA boxes, K in (r, s, c) order,
-    taps outside the image zero-filled by the TMA) against the explicit im2col path: whole-row
+    taps outside the image zero-filled by the TMA; the weight gradient reads the same NHWC copy as an
+    MN-major operand) against the explicit im2col path: whole-row
     tiles (16 x 16), two images per tile (8 x 8), 32 images per tile (2 x 2), a stride-2 layer
     whose input gradient runs as four parity-class convs of dy, and a padding-0 layer whose input
     gradient is an implicit conv with padding 2.  Same bf16 operands, different fp32 summation
@@ -690,11 +691,12 @@ def test_implicit_gemm_convs_match_explicit(pkg, monkeypatch):
 
     imp, st = run(True)
     assert st["conv1"].im_fwd and st["conv1"].im_dg and st["conv2"].im_fwd and st["conv3"].im_dg
+    assert st["conv1"].im_wg and st["conv2"].im_wg and not st["conv3"].im_wg  # (conv3: padding 0)
     assert st["conv2s"].par_dg and not st["conv2s"].im_fwd
     assert st["conv3"].im_fwd  # 2 x 2 output: 32 images per tile
     assert not st["conv0"].im_fwd
     exp, st0 = run(False)
-    assert not any(s.im_fwd or s.im_dg or s.par_dg for s in st0.values() if s.kind == "conv")
+    assert not any(s.im_fwd or s.im_dg or s.par_dg or s.im_wg for s in st0.values() if s.kind == "conv")
     params = oracle.init_model(graph, 4)
     bx, by, _ = oracle.epoch_batches(splits["train_x"], splits["train_y"], ds.content_hash, 32, 4, 0)[0]
     logits, tape = oracle.model_forward(graph, params, bx)
