@@ -329,20 +329,32 @@ __global__ void __launch_bounds__(CT_THREADS) wgrad_reduce_kernel(const hnn_conv
   const long long kmax = (long long)rows * p.oh * p.ow;
   const int splits = int(min((long long)p.ksplit, (kmax + p.ksplit_len - 1) / p.ksplit_len));
   // split s occupies rows [s * fp, s * fp + f) of the partial buffer, fp = f rounded up to 32
-  const long long total = (long long)p.f * p.kk, ptotal = (long long)((p.f + 31) & ~31) * p.kkp;
+  // (32-bit element indices: a weight tensor is far below 2^31 elements; 64-bit divisions per
+  // element made this launch issue-bound)
+  const int total = p.f * p.kk;
+  const size_t ptotal = size_t((p.f + 31) & ~31) * p.kkp;
   const long long tid = (long long)(blockIdx.x - p.block_base) * CT_THREADS + threadIdx.x;
-  for (long long e = tid; e < total; e += (long long)p.blocks * CT_THREADS) {
-    const long long f = e / p.kk, kr = e - f * p.kk;  // reference column (c, r, s)
-    long long col = kr;
-    if (p.rsc) {  // partial columns in (r, s, c) order
-      const int kk2 = p.k * p.k;
-      const long long c = kr / kk2;
-      col = (kr - c * kk2) * p.c + c;
+  const int kk2 = p.k * p.k;
+  for (int e = int(tid); e < total; e += p.blocks * CT_THREADS) {
+    // e walks the partial columns (coalesced reads of every split); rsc: partial column (r, s, c)
+    // goes to reference column (c, r, s)
+    const int f = e / p.kk, col = e - f * p.kk;
+    int kr = col;
+    if (p.rsc) {
+      const int rs = col / p.c;
+      kr = (col - rs * p.c) * kk2 + rs;
     }
-    const long long pe = f * p.kkp + col;  // partial rows are kkp wide
+    const size_t pe = size_t(f) * p.kkp + col;  // partial rows are kkp wide
+    float v[8];
+    const int s8 = min(splits, 8);
+#pragma unroll
+    for (int s = 0; s < 8; ++s) v[s] = s < s8 ? __ldg(p.partial + s * ptotal + pe) : 0.0f;  // loads together
     float acc = 0.0f;
-    for (int s = 0; s < splits; ++s) acc = __fadd_rn(acc, __ldg(p.partial + size_t(s) * ptotal + pe));
-    p.dw[e] = acc;
+#pragma unroll
+    for (int s = 0; s < 8; ++s)
+      if (s < s8) acc = __fadd_rn(acc, v[s]);
+    for (int s = 8; s < splits; ++s) acc = __fadd_rn(acc, __ldg(p.partial + s * ptotal + pe));
+    p.dw[size_t(f) * p.kk + kr] = acc;
   }
   // bias: one warp per filter; lane l sums the (batch row, pixel tile) partials l, l+32, ... in
   // order, then a fixed xor tree combines the lanes

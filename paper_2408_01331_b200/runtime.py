@@ -817,7 +817,11 @@ class DeviceHybrid:
                 esz = 2 if pr.bf16 else 4
                 pix_out, pix_in = pr.cap * pr.oh * pr.ow, pr.cap * pr.h * pr.w
                 if aux == N.CONVTC_IM2COL:
-                    nbytes += 4 * pr.c * pix_in + esz * pix_out * pr.kkp * (2 if pr.colst else 1)
+                    if pr.bf16 and not pr.cols and not pr.colst:  # only the NHWC copy
+                        nbytes += (4 + 2) * pr.c * pix_in
+                    else:
+                        nbytes += (4 * pr.c * pix_in + esz * pix_out * pr.kkp * ((1 if pr.cols else 0) + (1 if pr.colst else 0))
+                                   + (2 * pr.c * pix_in if pr.dyt else 0))
                 elif aux == N.CONVTC_TRANSPOSE_DY:
                     nbytes += 4 * pr.f * pix_out + esz * pr.f * pix_out * ((1 if pr.dyt else 0) + (1 if pr.dyk else 0))
                 elif aux == N.CONVTC_COL2IM:
@@ -1157,6 +1161,8 @@ class DeviceHybrid:
             stride = st.attrs.get("stride", k)
             oh, ow = conv_extent(h, k, stride, 0), conv_extent(w, k, stride, 0)
             total = s.batch_size * c * (oh * ow if op == N.HNN_FWD else h * w)
+            if s.batch_size * c * h * w >= 2 ** 31:  # (the pool kernels index in 32 bits)
+                raise UnsupportedGraphError(f"{st.node_id}: pooled tensor above 2^31 elements")
             blocks = -(-total // 256)
             probs.append(N.PoolProblem(_ptr(st.x), _ptr(st.y), _ptr(st.idx), _ptr(st.dy), _ptr(st.dx),
                                        _ptr(st.x) if st.mask_input else 0, s.batch_size, c, h, w, k, stride, oh,
@@ -1170,6 +1176,8 @@ class DeviceHybrid:
     def _relu_launch(self, op, items, label):
         probs, base = [], 0
         for s, st in items:
+            if s.batch_size * st.ld_in >= 2 ** 31:  # (the relu kernel indexes in 32 bits)
+                raise UnsupportedGraphError(f"{st.node_id}: relu tensor above 2^31 elements")
             blocks = -(-(s.batch_size * st.ld_in) // 256)
             probs.append(N.ReluProblem(_ptr(st.x), _ptr(st.y), _ptr(st.dy), _ptr(st.dx), s.batch_size, st.ld_in,
                                        s.index, base, blocks, 0))
