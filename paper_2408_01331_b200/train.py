@@ -438,6 +438,11 @@ class HostFedStepper:
     one H2D copy per arena, runs the step's kernels (no device gather), and copies the
     per-job loss and correct count back to pinned host memory.  The schedule rows
     (rows / lr / optimizer step) come from :meth:`DeviceHybrid.load_schedule` as usual.
+
+    The H2D copies run on their own stream into one of two HBM staging buffers, so step t's
+    upload overlaps step t-1's kernels (the way a data loader prefetches); the step itself
+    waits for its upload, moves the staged batch into the arena with one device copy, and
+    frees the staging buffer for step t+2.
     """
 
     def __init__(self, hybrid: HybridModel, datasets: dict, use_graph: bool = True):
@@ -451,6 +456,11 @@ class HostFedStepper:
         self.hits_host = torch.zeros(self.dev.n, dtype=torch.int32).pin_memory()
         self.h2d_bytes_per_step = int(self.dev.batch_arena.numel() * 4 + self.dev.label_arena.numel() * 4)
         self.d2h_bytes_per_step = int(self.dev.n * 8)
+        self.copy_stream = torch.cuda.Stream(device=self.dev.device)
+        self.staging = [(torch.empty_like(self.dev.batch_arena), torch.empty_like(self.dev.label_arena))
+                        for _ in range(2)]
+        self.staging_free = [None, None]
+        self.steps_issued = 0
 
     def stage_epoch_batches(self, ds, rows, count: int = 2, comm=None) -> list:
         """Pinned host copies of the first `count` steps' batches (store.batches order, src/store.py:68-81)."""
@@ -480,9 +490,26 @@ class HostFedStepper:
         return staged
 
     def step(self, host_batch) -> None:
+        import torch
+
         x, y = host_batch
-        self.dev.batch_arena.copy_(x, non_blocking=True)
-        self.dev.label_arena.copy_(y, non_blocking=True)
+        k = self.steps_issued % 2
+        sx, sy = self.staging[k]
+        compute = torch.cuda.current_stream(self.dev.device)
+        with torch.cuda.stream(self.copy_stream):
+            if self.staging_free[k] is not None:  # step t-2 has moved its batch out
+                self.copy_stream.wait_event(self.staging_free[k])
+            sx.copy_(x, non_blocking=True)
+            sy.copy_(y, non_blocking=True)
+            ready = torch.cuda.Event()
+            ready.record(self.copy_stream)
+        compute.wait_event(ready)
+        self.dev.batch_arena.copy_(sx, non_blocking=True)
+        self.dev.label_arena.copy_(sy, non_blocking=True)
+        free = torch.cuda.Event()
+        free.record(compute)
+        self.staging_free[k] = free
+        self.steps_issued += 1
         self.dev.train_steps(1, use_graph=self.use_graph, host_fed=True)
         self.loss_host.copy_(self.dev.loss_out, non_blocking=True)
         self.hits_host.copy_(self.dev.correct_out, non_blocking=True)

@@ -768,3 +768,36 @@ def test_embedding_op_kind_matches_oracle_bit_exact(pkg):
     assert np.array_equal(dp["table"], dp_ref["table"])
     with pytest.raises(ValueError):
         kind.forward(x + 0.5, {"table": table}, attrs)
+
+
+@pytest.mark.gpu
+def test_host_fed_stepper_matches_device_gather(pkg):
+    """The public host-fed API (HostFedStepper: pinned host batches uploaded on a copy stream into
+    double-buffered staging, overlapping the previous step) trains bit-identically to the
+    device-gather path on the same schedule (C1, 4 steps)."""
+    import torch
+
+    import bench  # (repo root on sys.path: tests/conftest.py)
+    from paper_2408_01331_b200.train import HostFedStepper
+
+    device = torch.device("cuda", 0)
+    outs = []
+    for host in (False, True):
+        jobs, hy, dev, ddev, meta, ds, comm = bench.build_rank("c1", 0, 1, device)
+        rows = bench.schedule(jobs, meta, 4)
+        bench.upload_perms(dev, jobs, meta)
+        dev.load_schedule(rows)
+        if host:
+            st = HostFedStepper(hy, {j.job_id: meta for j in jobs})
+            staged = st.stage_epoch_batches(ds, rows, count=4)
+            for b in staged:
+                st.step(b)
+            losses = st.finish()
+            assert all(np.isfinite(l) for l, _ in losses.values())
+        else:
+            dev.train_steps(4, use_graph=True)
+        torch.cuda.synchronize()
+        outs.append([dev.download_params(m) for m in range(len(jobs))])
+    for a, b in zip(*outs):
+        for k in a:
+            assert np.array_equal(a[k], b[k]), k
