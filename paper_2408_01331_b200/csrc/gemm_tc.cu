@@ -426,6 +426,21 @@ int encode_nhwc_bf16(CUtensorMap* map, const void* ptr, const hnn_gemm_problem& 
   return r == CUDA_SUCCESS ? HNN_OK : HNN_ERR_CUDA;
 }
 
+// 3D fp32 map over an NCHW conv output [cap][c][hw] (c_mode 1 with hw % 32 == 0): box {32 pixels,
+// 32 channels, 1 image}, unswizzled (the epilogue stages [channel][pixel] blocks)
+int encode_nchw_f32(CUtensorMap* map, const float* ptr, uint64_t hw, uint64_t c, uint64_t cap) {
+  EncodeTiled enc = encoder();
+  if (!enc) return HNN_ERR_CUDA;
+  cuuint64_t dims[3] = {hw, c, cap};
+  cuuint64_t strides[2] = {hw * 4, c * hw * 4};
+  cuuint32_t box[3] = {32, 32, 1};
+  cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float*>(ptr), dims, strides, box, estr,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS ? HNN_OK : HNN_ERR_CUDA;
+}
+
 int gemm_tc_tile_shape(int op, int32_t* tm, int32_t* tn) {
   *tm = TC_BM;
   *tn = TC_BN;
@@ -501,7 +516,10 @@ extern "C" int hnn_gemm_tc_encode(int op, const hnn_gemm_problem* host_probs, in
     // (a K-split WGRAD writes ksplit stacked [m, n] partials)
     const uint64_t crows = (op == HNN_WGRAD && p.ksplit > 1) ? uint64_t((p.m + 31) & ~31) * uint64_t(p.ksplit)
                                                              : uint64_t(p.m);
-    if (!rc && p.c && p.c_mode == 0)  // (c_mode >= 1 stores NCHW directly, no map)
+    if (!rc && p.c && p.c_mode == 1 && p.row_mult % 32 == 0)  // NCHW via 3D TMA stores
+      rc = hnn::encode_nchw_f32(&maps[3 * i + 2], p.c, uint64_t(p.row_mult), uint64_t(p.n),
+                                uint64_t(p.m / p.row_mult));
+    else if (!rc && p.c && p.c_mode == 0)  // (other c_modes store NCHW directly, no map)
       rc = hnn::encode_2d(&maps[3 * i + 2], p.c, p.n, crows, p.ldc, 32, false);
     if (rc) {
       hnn::set_error("hnn_gemm_tc_encode", "cuTensorMapEncodeTiled failed (alignment / stride / driver)");
@@ -540,7 +558,10 @@ extern "C" int hnn_gemm_bf16_encode(int op, const hnn_gemm_problem* host_probs, 
     }
     const uint64_t crows = (op == HNN_WGRAD && p.ksplit > 1) ? uint64_t((p.m + 31) & ~31) * uint64_t(p.ksplit)
                                                              : uint64_t(p.m);
-    if (!rc && p.c && p.c_mode == 0)  // (c_mode >= 1 stores NCHW directly, no map)
+    if (!rc && p.c && p.c_mode == 1 && p.row_mult % 32 == 0)  // NCHW via 3D TMA stores
+      rc = hnn::encode_nchw_f32(&maps[3 * i + 2], p.c, uint64_t(p.row_mult), uint64_t(p.n),
+                                uint64_t(p.m / p.row_mult));
+    else if (!rc && p.c && p.c_mode == 0)  // (other c_modes store NCHW directly, no map)
       rc = hnn::encode_2d(&maps[3 * i + 2], p.c, p.n, crows, p.ldc, 32, false);
     if (rc) {
       hnn::set_error("hnn_gemm_bf16_encode", "cuTensorMapEncodeTiled failed (alignment / stride / driver)");

@@ -170,7 +170,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC2_THREADS, 1)
   const bool leader = rank == 0;
 #ifdef HNN_TC2_TRACE
   const long long t_start = clock64();
-  long long tr[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
+  long long tr[11] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
 #endif
 
   uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -404,7 +404,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC2_THREADS, 1)
         const int tile = tile_id(ti);
       const hnn_gemm_problem* p;
       int m0, n0, nkb, rows, kofs, sp, tn;
+      TC2_T0(t9);
       if (!tile_info(tile, p, m0, n0, nkb, rows, kofs, sp, tn)) continue;
+      TC2_T1(t9, 9);
       const int nchunks = BF16 ? 1 : (nkb + TC2_CHUNK_KB - 1) / TC2_CHUNK_KB;
       const int hn = tn / 2;  // this warp's columns: [half * hn, half * hn + hn)
       const uint32_t lane_base = lane_quarter + half * hn;
@@ -484,6 +486,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC2_THREADS, 1)
         float bv = 0.0f;
         if (OP == HNN_FWD && bias && nh + cb + lane < pn) bv = __ldg(bias + nh + cb + lane);  // lane j: column j
         float tv[32];
+        TC2_T0(t10);
         if (BF16) {
           uint32_t r0[16], r1[16];
           tmem_ld16(lane_base + dbuf * TC2_BN + cb, r0);
@@ -494,6 +497,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC2_THREADS, 1)
             tv[16 + j] = __uint_as_float(r1[j]);
           }
         }
+        TC2_T1(t10, 10);
 #define TC2_ACC(j) (BF16 ? tv[(j)] : sum[(cb + (j)) % (BF16 ? 1 : HALF)])
         if (nchw) {
           // element (pixel row, filter n) -> y[b][n][hw]: for a fixed n the 32 lanes (rows =
@@ -511,6 +515,36 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC2_THREADS, 1)
                                     ((cm - 2) & 1)
                               : nchw_hw;
           const size_t ybase = rok ? size_t(nchw_b) * pn * plane + pix : 0;
+          if (BF16 && cm == 1 && (hw_n & 31) == 0) {  // (bf16 convs; fp32 keeps the direct stores)
+            // whole 32-pixel runs of one image: stage the block as [channel][pixel] (for a fixed
+            // channel the lanes write consecutive words) and store it with one 3D TMA box
+            // {32 pixels, 32 channels, 1 image}; rows / channels past the tensor are clipped
+#pragma unroll
+            for (int g = 0; g < 32 / NG; ++g) {
+              float mk[NG];
+#pragma unroll
+              for (int jj = 0; jj < NG; ++jj) {
+                const int n = nh + cb + g * NG + jj;
+                mk[jj] = (nmask && rok && n < pn) ? __ldg(nmask + ybase + size_t(n) * plane) : 1.0f;
+              }
+#pragma unroll
+              for (int jj = 0; jj < NG; ++jj) {
+                float x = TC2_ACC(g * NG + jj);
+                const float b = __shfl_sync(0xffffffffu, bv, g * NG + jj);  // column's bias
+                if (zero_row) x = 0.0f;
+                else {
+                  x = __fadd_rn(x, b);
+                  if (relu) x = np_relu(x);
+                }
+                sts32(stg + (g * NG + jj) * 128 + lane * 4, nmask ? (zero_row ? 0.0f : np_mask(x, mk[jj])) : x);
+              }
+            }
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            __syncwarp();
+            if (lane == 0) tma_store_3d(tmap_c, stg, row0 % hw_n, nh + cb, row0 / hw_n);
+            ++nstore;
+            continue;
+          }
 #pragma unroll
           for (int g = 0; g < 32 / NG; ++g) {
             float mk[NG];
@@ -639,7 +673,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC2_THREADS, 1)
 #ifdef HNN_TC2_TRACE
   if (threadIdx.x == 0) g_tc2_trace[blockIdx.x * 16 + 15] += clock64() - t_start;
   if ((threadIdx.x & 31) == 0)
-    for (int i = 0; i < 9; ++i)
+    for (int i = 0; i < 11; ++i)
       if (tr[i]) atomicAdd(&g_tc2_trace[blockIdx.x * 16 + i], (unsigned long long)tr[i]);
 #endif
   cluster_sync_all();  // the leader's MMAs into the peer's TMEM are complete

@@ -43,3 +43,4 @@ for launch in dev.train_plan:
           f" | acc warps wait full {t[:, 4].mean() / 8:8.0f}")
     print(f"{'':26s} MMA issue {lead[:, 5].mean():8.0f} | acc promote {t[:, 6].mean() / 8:8.0f} epilogue {t[:, 7].mean() / 8:8.0f}"
           f" | end barrier (per warp) {t[:, 8].mean() / 12:8.0f} | life min/max {t[:, 15].min():.0f}/{t[:, 15].max():.0f}")
+    print(f"{'':26s} acc tile_info {t[:, 9].mean() / 8:8.0f} | bias+tmem ld (bf16) {t[:, 10].mean() / 8:8.0f}")
