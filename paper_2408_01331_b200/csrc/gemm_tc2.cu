@@ -430,14 +430,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC2_THREADS, 1)
       float sum[BF16 ? 1 : HALF];
 #pragma unroll
       for (int j = 0; j < (BF16 ? 1 : HALF); ++j) sum[j] = 0.0f;  // defined on every path: not live across tiles
-      const uint32_t dbuf = cg & 1;  // (bf16) the tile's accumulator buffer
-      for (int c = 0; c < nchunks; ++c, ++cg) {
+      const uint32_t dbuf = cg & 1, dpar = (cg >> 1) & 1;  // (bf16) the tile's accumulator buffer
+      // bf16: the wait for the accumulators comes after the problem fields and biases are loaded
+      // (their global-memory latency then overlaps the MMAs instead of following them)
+      if (BF16) ++cg;
+      for (int c = 0; c < (BF16 ? 0 : nchunks); ++c, ++cg) {
         const uint32_t buf = cg & 1;
         TC2_T0(t4);
         mbar_wait(bar(ACC_FULL + buf), (cg >> 1) & 1);
         TC2_T1(t4, 4);
         tc_fence_after();
-        if (BF16) continue;
 #pragma unroll
         for (int cb = 0; cb < HALF; cb += 16) {
           if (cb >= hn) break;
@@ -474,6 +476,18 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC2_THREADS, 1)
       const int row0 = m0 + int(rank) * TC2_BM + q * 32, row = row0 + lane;
       const int nh = n0 + half * hn;
       const bool zero_row = (OP != HNN_WGRAD) && row >= rows;
+      float bvp[BF16 ? HALF / 32 : 1];  // (bf16) each 32-column block's bias, lane j = column j
+#pragma unroll
+      for (int blk = 0; blk < (BF16 ? HALF / 32 : 1); ++blk)
+        bvp[blk] = (BF16 && OP == HNN_FWD && bias && blk * 32 < hn && nh + blk * 32 + lane < pn)
+                       ? __ldg(bias + nh + blk * 32 + lane)
+                       : 0.0f;
+      if (BF16) {
+        TC2_T0(t4b);
+        mbar_wait(bar(ACC_FULL + dbuf), dpar);
+        TC2_T1(t4b, 4);
+        tc_fence_after();
+      }
       const float* mrow = (OP == HNN_DGRAD && p->mask && row < pm) ? p->mask + size_t(row) * ldc : nullptr;
 #pragma unroll
       for (int cb = 0; cb < HALF; cb += 32) {
@@ -483,8 +497,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC2_THREADS, 1)
         __syncwarp();
         // registers (lane = row) -> 128B-swizzled staging (16-byte chunk j of row r at chunk
         // j ^ (r & 7): conflict-free STS.128) -> one TMA store per 32 x 32 block
-        float bv = 0.0f;
-        if (OP == HNN_FWD && bias && nh + cb + lane < pn) bv = __ldg(bias + nh + cb + lane);  // lane j: column j
+        const float bv = BF16 ? bvp[(cb / 32) % (BF16 ? HALF / 32 : 1)]  // lane j: column j
+                              : ((OP == HNN_FWD && bias && nh + cb + lane < pn) ? __ldg(bias + nh + cb + lane) : 0.0f);
         float tv[32];
         TC2_T0(t10);
         if (BF16) {
