@@ -18,4 +18,8 @@ timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --lo
   python bench.py --workload c3 --steps 2 --warmup 1 --no-cpu > gpurun_out/ncu_launch_c3.log 2>&1
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:'multi_tensor|gemm_tc2' -s 12 -c 6 \
   -o gpurun_out/prof_c3 python bench.py --workload c3 --steps 2 --warmup 1 --no-cpu > gpurun_out/ncu_full_c3.log 2>&1
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:'gemm_tc2|transpose_dy|im2col|wgrad_reduce' -s 20 -c 8 \
+  -o gpurun_out/prof_c4 python bench.py --workload c4 --steps 1 --warmup 3 --no-cpu > gpurun_out/ncu_full_c4.log 2>&1
+timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_c4.csv \
+  python bench.py --workload c4 --steps 2 --warmup 1 --no-cpu > gpurun_out/ncu_launch_c4.log 2>&1
 echo done
