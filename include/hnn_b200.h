@@ -189,6 +189,12 @@ typedef struct hnn_gemm_problem {
    * channels of one tap per CTA (tile_n must be 128; 64-pixel K blocks of whole rows / images);
    * A (dy, [f, pixels]) stays an ordinary K-major matrix. */
   int32_t im_c, im_k, im_pad, im_h, im_w, im_oh, im_ow, im_n;
+  /* HNN_PREC_BF16_PAIR FWD with c_mode 1 (row_mult % 32 == 0): when xh_out != NULL the epilogue
+   * also writes the output as NHWC bf16 rows [m, n] (after bias / relu; zero rows past the batch):
+   * the next layer's implicit-GEMM input, so that layer needs no separate NHWC copy.  tmap_xh: its
+   * TMA map (hnn_gemm_bf16_encode, the problem's fourth map). */
+  void* xh_out;
+  const void* tmap_xh;
 } hnn_gemm_problem;
 
 /* Tile edge (m, n) used by (op, prec); lets the host lay out tile_base / tiles_n. */
@@ -198,9 +204,10 @@ int hnn_grouped_gemm(int op, int prec, const hnn_gemm_problem* probs, int nprob,
                      const hnn_step_row* cur, const hnn_model_status* status, void* stream);
 
 /*
- * Host-side: encode the three TMA tensor maps (A, B, C; 128 bytes each) of every problem for the
- * tcgen05 path into host_maps[3*nprob]; the caller copies them to device memory and stores their
- * device addresses in tmap_a / tmap_b / tmap_c.  Requirements: 16-byte aligned bases and row strides.
+ * Host-side: encode the TMA tensor maps (A, B, C, and the bf16 path's NHWC copy X2; 128 bytes each)
+ * of every problem for the tcgen05 path into host_maps[4*nprob]; the caller copies them to device
+ * memory and stores their device addresses in tmap_a / tmap_b / tmap_c / tmap_xh.  Requirements:
+ * 16-byte aligned bases and row strides.
  * Tiles are 128 x 128 (hnn_gemm_tile_shape); WGRAD problems need m <= 4096.
  */
 int hnn_gemm_tc_encode(int op, const hnn_gemm_problem* host_probs, int nprob, void* host_maps);

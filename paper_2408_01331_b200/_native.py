@@ -49,7 +49,7 @@ class GemmProblem(C.Structure):
                 ("opt_bv", P), ("opt_kind", I), ("opt_momentum", C.c_float),
                 ("row_mult", I), ("c_mode", I), ("ksplit", I), ("ksplit_len", I), ("tile_n", I), ("im_kw", I),
                 ("im_c", I), ("im_k", I), ("im_pad", I), ("im_h", I), ("im_w", I), ("im_oh", I), ("im_ow", I),
-                ("im_n", I)]
+                ("im_n", I), ("xh_out", P), ("tmap_xh", P)]
 
     def __init__(self, **kw):
         kw.setdefault("row_mult", 1)

@@ -441,6 +441,21 @@ int encode_nchw_f32(CUtensorMap* map, const float* ptr, uint64_t hw, uint64_t c,
   return r == CUDA_SUCCESS ? HNN_OK : HNN_ERR_CUDA;
 }
 
+// 2D bf16 map over NHWC rows [m, n] (the epilogue's second output), box {32 channels, 32 pixels},
+// unswizzled (staged as [pixel][channel])
+int encode_rows_bf16(CUtensorMap* map, const void* ptr, uint64_t n, uint64_t m) {
+  EncodeTiled enc = encoder();
+  if (!enc) return HNN_ERR_CUDA;
+  cuuint64_t dims[2] = {n, m};
+  cuuint64_t strides[1] = {n * 2};
+  cuuint32_t box[2] = {32, 32};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(ptr), dims, strides, box, estr,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS ? HNN_OK : HNN_ERR_CUDA;
+}
+
 int gemm_tc_tile_shape(int op, int32_t* tm, int32_t* tn) {
   *tm = TC_BM;
   *tn = TC_BN;
@@ -503,24 +518,24 @@ extern "C" int hnn_gemm_tc_encode(int op, const hnn_gemm_problem* host_probs, in
     int rc;
     if (op == HNN_FWD) {          // A = X[cap, K] (K-major), B = W[N, K] (K-major)
       const uint32_t brows = p.tile_n > 0 ? uint32_t(p.tile_n / 2) : uint32_t(hnn::TC_BN);
-      rc = hnn::encode_2d(&maps[3 * i], p.a, p.k, p.m, p.lda, hnn::TC_BM, false);
-      if (!rc) rc = hnn::encode_2d(&maps[3 * i + 1], p.b, p.k, p.n, p.ldb, brows, false);
+      rc = hnn::encode_2d(&maps[4 * i], p.a, p.k, p.m, p.lda, hnn::TC_BM, false);
+      if (!rc) rc = hnn::encode_2d(&maps[4 * i + 1], p.b, p.k, p.n, p.ldb, brows, false);
     } else if (op == HNN_DGRAD) { // A = dY[cap, U] (K-major), B = W[U, N] (N-major)
-      rc = hnn::encode_2d(&maps[3 * i], p.a, p.k, p.m, p.lda, hnn::TC_BM, false);
-      if (!rc) rc = hnn::encode_2d(&maps[3 * i + 1], p.b, p.n, p.k, p.ldb, 32, true);
+      rc = hnn::encode_2d(&maps[4 * i], p.a, p.k, p.m, p.lda, hnn::TC_BM, false);
+      if (!rc) rc = hnn::encode_2d(&maps[4 * i + 1], p.b, p.n, p.k, p.ldb, 32, true);
     } else {                      // A = dY[cap, M] (M-major), B = X[cap, N] (N-major)
-      rc = hnn::encode_2d(&maps[3 * i], p.a, p.m, p.k, p.lda, 32, true);
-      if (!rc) rc = hnn::encode_2d(&maps[3 * i + 1], p.b, p.n, p.k, p.ldb, 32, true);
+      rc = hnn::encode_2d(&maps[4 * i], p.a, p.m, p.k, p.lda, 32, true);
+      if (!rc) rc = hnn::encode_2d(&maps[4 * i + 1], p.b, p.n, p.k, p.ldb, 32, true);
     }
     // C (all ops): row-major [m, n] with row stride ldc; 32x32 boxes, 128-byte swizzle
     // (a K-split WGRAD writes ksplit stacked [m, n] partials)
     const uint64_t crows = (op == HNN_WGRAD && p.ksplit > 1) ? uint64_t((p.m + 31) & ~31) * uint64_t(p.ksplit)
                                                              : uint64_t(p.m);
     if (!rc && p.c && p.c_mode == 1 && p.row_mult % 32 == 0)  // NCHW via 3D TMA stores
-      rc = hnn::encode_nchw_f32(&maps[3 * i + 2], p.c, uint64_t(p.row_mult), uint64_t(p.n),
+      rc = hnn::encode_nchw_f32(&maps[4 * i + 2], p.c, uint64_t(p.row_mult), uint64_t(p.n),
                                 uint64_t(p.m / p.row_mult));
     else if (!rc && p.c && p.c_mode == 0)  // (other c_modes store NCHW directly, no map)
-      rc = hnn::encode_2d(&maps[3 * i + 2], p.c, p.n, crows, p.ldc, 32, false);
+      rc = hnn::encode_2d(&maps[4 * i + 2], p.c, p.n, crows, p.ldc, 32, false);
     if (rc) {
       hnn::set_error("hnn_gemm_tc_encode", "cuTensorMapEncodeTiled failed (alignment / stride / driver)");
       return rc;
@@ -543,26 +558,31 @@ extern "C" int hnn_gemm_bf16_encode(int op, const hnn_gemm_problem* host_probs, 
       HNN_REQUIRE(p.im_c % 64 == 0 && p.im_ow > 0 && 128 % p.im_ow == 0 && (hw % 128 == 0 || 128 % hw == 0) &&
                       p.k == taps * p.im_c,
                   "hnn_gemm_bf16_encode", "implicit convolution geometry not supported");
-      rc = hnn::encode_nhwc_bf16(&maps[3 * i], p.a, p, 128);
+      rc = hnn::encode_nhwc_bf16(&maps[4 * i], p.a, p, 128);
     } else {
-      rc = hnn::encode_2d_bf16(&maps[3 * i], p.a, p.k, p.m, p.lda, hnn::TC_BM);
+      rc = hnn::encode_2d_bf16(&maps[4 * i], p.a, p.k, p.m, p.lda, hnn::TC_BM);
     }
     if (rc) {
     } else if (p.im_c > 0 && op == HNN_WGRAD) {  // implicit weight gradient: B = NHWC activations, MN-major
       HNN_REQUIRE(p.im_c % 64 == 0 && p.tile_n == 128 && p.im_ow > 0 && 64 % p.im_ow == 0 &&
                       (hw % 64 == 0 || 64 % hw == 0) && p.n == taps * p.im_c,
                   "hnn_gemm_bf16_encode", "implicit weight-gradient geometry not supported");
-      rc = hnn::encode_nhwc_bf16(&maps[3 * i + 1], p.b, p, 64);
+      rc = hnn::encode_nhwc_bf16(&maps[4 * i + 1], p.b, p, 64);
     } else {
-      rc = hnn::encode_2d_bf16(&maps[3 * i + 1], p.b, p.k, p.n, p.ldb, brows);
+      rc = hnn::encode_2d_bf16(&maps[4 * i + 1], p.b, p.k, p.n, p.ldb, brows);
     }
     const uint64_t crows = (op == HNN_WGRAD && p.ksplit > 1) ? uint64_t((p.m + 31) & ~31) * uint64_t(p.ksplit)
                                                              : uint64_t(p.m);
     if (!rc && p.c && p.c_mode == 1 && p.row_mult % 32 == 0)  // NCHW via 3D TMA stores
-      rc = hnn::encode_nchw_f32(&maps[3 * i + 2], p.c, uint64_t(p.row_mult), uint64_t(p.n),
+      rc = hnn::encode_nchw_f32(&maps[4 * i + 2], p.c, uint64_t(p.row_mult), uint64_t(p.n),
                                 uint64_t(p.m / p.row_mult));
     else if (!rc && p.c && p.c_mode == 0)  // (other c_modes store NCHW directly, no map)
-      rc = hnn::encode_2d(&maps[3 * i + 2], p.c, p.n, crows, p.ldc, 32, false);
+      rc = hnn::encode_2d(&maps[4 * i + 2], p.c, p.n, crows, p.ldc, 32, false);
+    if (!rc && p.xh_out) {
+      HNN_REQUIRE(op == HNN_FWD && p.c_mode == 1 && p.row_mult % 32 == 0 && p.n % 8 == 0, "hnn_gemm_bf16_encode",
+                  "xh_out needs a bf16 NCHW forward with 32-pixel runs and 16-byte rows");
+      rc = hnn::encode_rows_bf16(&maps[4 * i + 3], p.xh_out, uint64_t(p.n), uint64_t(p.m));
+    }
     if (rc) {
       hnn::set_error("hnn_gemm_bf16_encode", "cuTensorMapEncodeTiled failed (alignment / stride / driver)");
       return rc;

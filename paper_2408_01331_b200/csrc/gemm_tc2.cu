@@ -28,6 +28,8 @@
 // soon as its raw tiles land (up to two K blocks ahead of the MMAs).
 // Barriers: raw full/empty, acc full: per CTA (the leader's commits multicast to both);
 // lo full and acc empty: in the leader, arrived on by both CTAs.
+#include <cuda_bf16.h>
+
 #include "tc_common.cuh"
 
 namespace hnn {
@@ -463,6 +465,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC2_THREADS, 1)
       const bool relu = (p->relu & 1) != 0;
       float* const cptr = p->c;
       const void* tmap_c = p->tmap_c;
+      const void* xh_out = BF16 ? p->xh_out : nullptr;  // (bf16 NCHW forward: NHWC copy for the next layer)
+      const void* tmap_xh = p->tmap_xh;
       float* const ow = p->opt_w;
       float* const owm = p->opt_wm;
       const bool fuse = OP == HNN_WGRAD && ow != nullptr;
@@ -557,6 +561,39 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC2_THREADS, 1)
             __syncwarp();
             if (lane == 0) tma_store_3d(tmap_c, stg, row0 % hw_n, nh + cb, row0 / hw_n);
             ++nstore;
+            if (xh_out) {
+              // the next layer's NHWC bf16 input: the same 32 x 32 block as [pixel][channel] rows
+              // (64 bytes per pixel) once the NCHW store has read the staging block
+              if (lane == 0) tma_store_wait_read();
+              __syncwarp();
+#pragma unroll
+              for (int j8 = 0; j8 < 4; ++j8) {
+                uint32_t w[4];
+#pragma unroll
+                for (int h2 = 0; h2 < 4; ++h2) {
+                  float y2[2];
+#pragma unroll
+                  for (int e = 0; e < 2; ++e) {
+                    const int jj = j8 * 8 + h2 * 2 + e;
+                    float x = TC2_ACC(jj);
+                    const float b = __shfl_sync(0xffffffffu, bv, jj);
+                    if (zero_row) x = 0.0f;
+                    else {
+                      x = __fadd_rn(x, b);
+                      if (relu) x = np_relu(x);
+                    }
+                    y2[e] = x;
+                  }
+                  const __nv_bfloat162 pr = __floats2bfloat162_rn(y2[0], y2[1]);
+                  w[h2] = *reinterpret_cast<const uint32_t*>(&pr);
+                }
+                sts128(stg + lane * 64 + j8 * 16, make_uint4(w[0], w[1], w[2], w[3]));
+              }
+              asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+              __syncwarp();
+              if (lane == 0) tma_store_2d(tmap_xh, stg, nh + cb, row0);
+              ++nstore;
+            }
             continue;
           }
 #pragma unroll

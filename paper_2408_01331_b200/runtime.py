@@ -122,6 +122,8 @@ class Stage:
     im_wg: bool = False        # implicit-GEMM weight gradient (B = xh, MN-major)
     par_dg: bool = False       # stride-2 input gradient as four parity-class implicit convs
     wpar = None
+    xh_next = None             # the next conv's xh, written by this conv's forward epilogue
+    xh_from_prev: bool = False # xh is written by the previous conv's forward epilogue
 
 
 def lower_graph(graph) -> tuple:
@@ -744,15 +746,16 @@ class DeviceHybrid:
             keep = None
             if prec in (N.PREC_3XTF32, N.PREC_3XTF32_PAIR, N.PREC_BF16_PAIR):
                 torch = _torch()
-                maps = bytearray(128 * 3 * len(probs))
+                maps = bytearray(128 * 4 * len(probs))
                 host = (N.GemmProblem * len(probs))(*probs)
                 enc = "hnn_gemm_bf16_encode" if prec == N.PREC_BF16_PAIR else "hnn_gemm_tc_encode"
                 N.call(enc, op, C_addr(host), len(probs), C_addr_bytes(maps))
                 keep = torch.frombuffer(maps, dtype=torch.uint8).to(self.device)
                 for i, pr in enumerate(probs):
-                    pr.tmap_a = _ptr(keep) + 384 * i
-                    pr.tmap_b = _ptr(keep) + 384 * i + 128
-                    pr.tmap_c = _ptr(keep) + 384 * i + 256
+                    pr.tmap_a = _ptr(keep) + 512 * i
+                    pr.tmap_b = _ptr(keep) + 512 * i + 128
+                    pr.tmap_c = _ptr(keep) + 512 * i + 256
+                    pr.tmap_xh = _ptr(keep) + 512 * i + 384
             extra = b""
             if prec in (N.PREC_3XTF32_PAIR, N.PREC_BF16_PAIR):
                 extra = self._pair_schedule(probs, rows, base, tm)
@@ -799,7 +802,7 @@ class DeviceHybrid:
             nb = blocks_of(s, st)
             dyt = st.dyt
             if aux == N.CONVTC_IM2COL:  # (im2col's dyt = the NHWC copy of x, "same" implicit layers)
-                dyt = st.xh if (st.im_fwd and self._same_conv(st)) else None
+                dyt = st.xh if (st.im_fwd and self._same_conv(st) and not st.xh_from_prev) else None
             probs.append(N.ConvTcProblem(
                 x=_ptr(st.x), cols=_ptr(st.cols), dy=_ptr(st.dy), dyt=_ptr(dyt),
                 dcols=_ptr(s.dcols) if s.dcols is not None else 0, dx=_ptr(st.dx),
@@ -921,7 +924,7 @@ class DeviceHybrid:
             # (the padded weight copies come from the step's prep launch: conv_weight_prep)
             # NHWC bf16 copies of the inputs for the implicit-GEMM layers: written by the im2col
             # launch for "same" layers (output pixel = input pixel), a transpose otherwise
-            imp = [(s, st) for s, st in items if st.im_fwd and not self._same_conv(st)]
+            imp = [(s, st) for s, st in items if st.im_fwd and not self._same_conv(st) and not st.xh_from_prev]
             if imp:
                 probs = []
                 for s, st in imp:
@@ -930,9 +933,13 @@ class DeviceHybrid:
                                                      ow=w, model=s.index, bf16=1)))
                 out.append(self._aux_table(N.CONVTC_TRANSPOSE_DY, probs, f"{label}/tc/nhwc",
                                            lambda pr: pr.cap * -(-(pr.oh * pr.ow) // 32) * -(-pr.f // 32), 3))
-            out.append(self._convtc_aux(
-                N.CONVTC_IM2COL, items, f"{label}/tc/im2col",
-                lambda s, st: -(-(s.batch_size * geo(st)[4] * geo(st)[5]) // 32) * -(-geo(st)[0] // 32)))
+            # (no im2col at all for a layer whose NHWC input came from the previous epilogue and
+            # whose weight gradient is implicit too)
+            cols_items = [(s, st) for s, st in items if not (st.xh_from_prev and st.im_wg)]
+            if cols_items:
+                out.append(self._convtc_aux(
+                    N.CONVTC_IM2COL, cols_items, f"{label}/tc/im2col",
+                    lambda s, st: -(-(s.batch_size * geo(st)[4] * geo(st)[5]) // 32) * -(-geo(st)[0] // 32)))
             rows = {}
             for s, st in items:
                 c, h, w, f, oh, ow, kk = geo(st)
@@ -943,6 +950,8 @@ class DeviceHybrid:
                 if st.im_fwd:
                     d.update(a=_ptr(st.xh), lda=c, im_c=c, im_k=st.attrs["kernel"], im_pad=st.attrs.get("padding", 0),
                              im_h=h, im_w=w, im_oh=oh, im_ow=ow, im_n=s.batch_size)
+                if st.xh_next is not None:
+                    d.update(xh_out=_ptr(st.xh_next))
                 rows.setdefault(prec(st), []).append((s, d))
             return out + gemms(N.HNN_FWD, rows, f"{label}/tc")
         tiles_t = lambda s, st: (s.batch_size * -(-(geo(st)[4] * geo(st)[5]) // 32) * -(-geo(st)[3] // 32))
@@ -1291,9 +1300,25 @@ class DeviceHybrid:
         return [Launch(entry, (_ptr(t), len(segs), base, _ptr(self.cur), _ptr(self.status)), t, "optimizer",
                        nbytes=nbytes)]
 
+    def _link_nhwc_producers(self):
+        """A bf16 conv whose output feeds an implicit-GEMM "same" conv directly writes that conv's
+        NHWC input from its forward epilogue (second TMA store per block), so the consumer needs
+        no NHWC copy launch."""
+        for s in self.slots:
+            for a, b in zip(s.stages, s.stages[1:]):
+                a.xh_next, b.xh_from_prev = None, False
+            for a, b in zip(s.stages, s.stages[1:]):
+                if not (a.kind == b.kind == "conv" and getattr(a, "tc", False) and getattr(b, "tc", False)):
+                    continue
+                f, oh, ow = self._conv_out(a)
+                if (a.bf16 and b.im_fwd and self._same_conv(b) and b.x is a.y and (oh * ow) % 32 == 0
+                        and f % 8 == 0):
+                    a.xh_next, b.xh_from_prev = b.xh, True
+
     def build_plans(self):
         waves = self._stage_waves()
         self._pending_reduce = []
+        self._link_nhwc_producers()
         fwd = []
         for w, items in enumerate(waves):
             fwd += self._wave_launches(N.HNN_FWD, items, f"fwd{w}")

@@ -47,10 +47,10 @@ def run(op, prec, M, Nn, K, rows=None, seed=0, dbg=0):
                          dbias=_ptr(db) if op == 2 else 0, model=0, relu=dbg << 8, tile_base=0, tiles_n=tiles_n, **d)
     keep = None
     if prec == N.PREC_3XTF32:
-        maps = bytearray(384)
+        maps = bytearray(512)
         host = (N.GemmProblem * 1)(prob)
         N.call("hnn_gemm_tc_encode", op, ctypes.addressof(host), 1,
-               ctypes.addressof((ctypes.c_char * 384).from_buffer(maps)))
+               ctypes.addressof((ctypes.c_char * 512).from_buffer(maps)))
         keep = torch.frombuffer(maps, dtype=torch.uint8).to(dev)
         prob.tmap_a, prob.tmap_b, prob.tmap_c = _ptr(keep), _ptr(keep) + 128, _ptr(keep) + 256
     t = _dev_table(N.GemmProblem, [prob], dev)
