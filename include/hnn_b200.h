@@ -273,6 +273,9 @@ typedef struct hnn_pool_problem {
   int32_t block_base;
   int32_t blocks;
   int32_t reserved;
+  /* FWD: when non-NULL, the output is also written as NHWC bf16 rows [cap * oh * ow, c] (zeros
+   * past the batch): the next layer's implicit-GEMM input */
+  void* xh;
 } hnn_pool_problem;
 
 int hnn_grouped_maxpool(int op, const hnn_pool_problem* probs, int nprob, int total_blocks,

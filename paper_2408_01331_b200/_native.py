@@ -82,7 +82,7 @@ class EmbedProblem(C.Structure):
 class PoolProblem(C.Structure):
     _fields_ = [("x", P), ("y", P), ("idx", P), ("dy", P), ("dx", P), ("mask", P),
                 ("cap", I), ("c", I), ("h", I), ("w", I), ("k", I), ("stride", I), ("oh", I), ("ow", I),
-                ("model", I), ("block_base", I), ("blocks", I), ("reserved", I)]
+                ("model", I), ("block_base", I), ("blocks", I), ("reserved", I), ("xh", P)]
 
 
 class ReluProblem(C.Structure):

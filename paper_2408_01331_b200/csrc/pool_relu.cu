@@ -2,6 +2,8 @@
 // (pkg/src/hybridnn/ops.py:62-67, 149-174).  HBM-bound elementwise kernels:
 // one thread per output (fwd) or per input element (bwd, gather form, so the
 // reference's np.add.at scatter becomes a fixed-order sum with no atomics).
+#include <cuda_bf16.h>
+
 #include "common.cuh"
 
 namespace hnn {
@@ -23,9 +25,12 @@ __global__ void __launch_bounds__(PTHREADS) maxpool_fwd_kernel(const hnn_pool_pr
   const int plane = e / ohw;  // b*C + c
   const int o = e - plane * ohw, oy = o / p.ow, ox = o - oy * p.ow;
   const int b = plane / p.c;
+  __nv_bfloat16* xh = reinterpret_cast<__nv_bfloat16*>(p.xh);  // NHWC bf16 copy: [(b, o), c]
+  const size_t xo = (size_t(b) * ohw + o) * p.c + (plane - b * p.c);
   if (b >= cur[p.model].rows) {
     p.y[e] = 0.0f;
     p.idx[e] = 0;
+    if (xh) xh[xo] = __float2bfloat16_rn(0.0f);
     return;
   }
   const float* src = p.x + size_t(plane) * p.h * p.w;
@@ -45,6 +50,7 @@ __global__ void __launch_bounds__(PTHREADS) maxpool_fwd_kernel(const hnn_pool_pr
   }
   p.y[e] = best;
   p.idx[e] = (uint8_t)best_i;
+  if (xh) xh[xo] = __float2bfloat16_rn(best);
 }
 
 __global__ void __launch_bounds__(PTHREADS) maxpool_bwd_kernel(const hnn_pool_problem* __restrict__ probs, int nprob,

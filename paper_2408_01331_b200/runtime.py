@@ -1175,7 +1175,8 @@ class DeviceHybrid:
             blocks = -(-total // 256)
             probs.append(N.PoolProblem(_ptr(st.x), _ptr(st.y), _ptr(st.idx), _ptr(st.dy), _ptr(st.dx),
                                        _ptr(st.x) if st.mask_input else 0, s.batch_size, c, h, w, k, stride, oh,
-                                       ow, s.index, base, blocks, 0))
+                                       ow, s.index, base, blocks, 0,
+                                       _ptr(st.xh_next) if op == N.HNN_FWD else 0))
             base += blocks
         nbytes = sum(4 * p.cap * p.c * (p.h * p.w + p.oh * p.ow) + p.cap * p.c * p.oh * p.ow for p in probs)
         t = _dev_table(N.PoolProblem, probs, self.device)
@@ -1308,6 +1309,10 @@ class DeviceHybrid:
             for a, b in zip(s.stages, s.stages[1:]):
                 a.xh_next, b.xh_from_prev = None, False
             for a, b in zip(s.stages, s.stages[1:]):
+                if (a.kind == "pool" and b.kind == "conv" and getattr(b, "tc", False) and b.im_fwd
+                        and self._same_conv(b) and b.x is a.y):  # the pool writes the NHWC copy
+                    a.xh_next, b.xh_from_prev = b.xh, True
+                    continue
                 if not (a.kind == b.kind == "conv" and getattr(a, "tc", False) and getattr(b, "tc", False)):
                     continue
                 f, oh, ow = self._conv_out(a)
