@@ -37,6 +37,62 @@ __global__ void __launch_bounds__(CT_THREADS) im2col_kernel(const hnn_convtc_pro
   if (!live(cur, status, p.model)) return;
   const int rows = cur[p.model].rows;
   const int kk2 = p.k * p.k, seg = IC_CH * kk2, ld = seg + 1;
+  if (p.bf16 && p.c * kk2 <= 32) {
+    // a network's first layer (C = 3): one thread per output pixel, its C*k*k taps straight from x
+    // (consecutive threads = consecutive pixels: coalesced reads and colst writes), the cols row
+    // (<= 32 bf16 = 64 bytes incl. zero padding) as four 16-byte stores.  256 pixels per CTA.
+    const int m = (blockIdx.x - p.block_base) * CT_THREADS + threadIdx.x;
+    const int ohw = p.oh * p.ow;
+    if (m >= p.cap * ohw) return;
+    const int b = m / ohw, o = m - b * ohw, oy = o / p.ow, ox = o - oy * p.ow;
+    const bool valid = b < cur[p.model].rows;
+    __nv_bfloat16 v[32];
+#pragma unroll
+    for (int j = 0; j < 32; ++j) v[j] = __float2bfloat16_rn(0.0f);
+    if (p.k == 3) {  // (C <= 3): every tap index is a compile-time register slot
+#pragma unroll
+      for (int c = 0; c < 3; ++c)
+#pragma unroll
+        for (int r = 0; r < 3; ++r) {
+          const int h = oy * p.stride - p.pad + r;
+#pragma unroll
+          for (int sx = 0; sx < 3; ++sx) {
+            const int w = ox * p.stride - p.pad + sx;
+            float x = 0.0f;
+            if (c < p.c && valid && h >= 0 && h < p.h && w >= 0 && w < p.w)
+              x = __ldg(p.x + ((size_t(b) * p.c + c) * p.h + h) * p.w + w);
+            v[c * 9 + r * 3 + sx] = __float2bfloat16_rn(x);
+          }
+        }
+    } else {
+      for (int c = 0; c < p.c; ++c)
+        for (int r = 0; r < p.k; ++r) {
+          const int h = oy * p.stride - p.pad + r;
+          for (int sx = 0; sx < p.k; ++sx) {
+            const int w = ox * p.stride - p.pad + sx, j = (c * p.k + r) * p.k + sx;
+            float x = 0.0f;
+            if (valid && h >= 0 && h < p.h && w >= 0 && w < p.w)
+              x = __ldg(p.x + ((size_t(b) * p.c + c) * p.h + h) * p.w + w);
+#pragma unroll
+            for (int q = 0; q < 32; ++q)
+              if (q == j) v[q] = __float2bfloat16_rn(x);
+          }
+        }
+    }
+    if (p.cols) {
+      uint4* dst = reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(p.cols) + size_t(m) * p.kkp);
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+        if (q * 8 < p.kkp) dst[q] = *reinterpret_cast<const uint4*>(&v[q * 8]);
+    }
+    if (p.colst) {
+      __nv_bfloat16* ct = reinterpret_cast<__nv_bfloat16*>(p.colst);
+#pragma unroll
+      for (int j = 0; j < 32; ++j)
+        if (j < p.kk) ct[size_t(j) * p.pix_ld + m] = v[j];
+    }
+    return;
+  }
   const int ohw = p.oh * p.ow;
   const int cblocks = (p.c + IC_CH - 1) / IC_CH;
   const int t = blockIdx.x - p.block_base;

@@ -939,7 +939,9 @@ class DeviceHybrid:
             if cols_items:
                 out.append(self._convtc_aux(
                     N.CONVTC_IM2COL, cols_items, f"{label}/tc/im2col",
-                    lambda s, st: -(-(s.batch_size * geo(st)[4] * geo(st)[5]) // 32) * -(-geo(st)[0] // 32)))
+                    lambda s, st: (-(-(s.batch_size * geo(st)[4] * geo(st)[5]) // 256)
+                                   if st.bf16 and geo(st)[0] * st.attrs["kernel"] ** 2 <= 32  # (first layers)
+                                   else -(-(s.batch_size * geo(st)[4] * geo(st)[5]) // 32) * -(-geo(st)[0] // 32))))
             rows = {}
             for s, st in items:
                 c, h, w, f, oh, ow, kk = geo(st)
