@@ -210,12 +210,20 @@ __global__ void __launch_bounds__(CT_THREADS) transpose_dy_kernel(const hnn_conv
   const int th = r / tiles_f, tf = r - th * tiles_f;
   if (b >= rows) return;  // rows beyond the batch are never read by the GEMMs
   const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // 32 x 8
-  for (int j = ty; j < 32; j += 8) {
-    const int f = tf * 32 + j, hw = th * 32 + tx;
-    tile[j][tx] = (f < p.f && hw < hw_n) ? __ldg(p.dy + (size_t(b) * p.f + f) * hw_n + hw) : 0.0f;
+  // all four loads first (a store consuming each loaded value right away serialised the loads:
+  // the compiler cannot move a load of dy above a store to dyk)
+  float v[4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int f = tf * 32 + ty + 8 * i, hw = th * 32 + tx;
+    v[i] = (f < p.f && hw < hw_n) ? __ldg(p.dy + (size_t(b) * p.f + f) * hw_n + hw) : 0.0f;
+  }
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int j = ty + 8 * i, f = tf * 32 + j, hw = th * 32 + tx;
+    tile[j][tx] = v[i];
     if (p.bf16 && p.dyk && f < p.f && hw < hw_n)  // dyk[f, b*HW + hw]: filter-major, pixel-contiguous
-      reinterpret_cast<__nv_bfloat16*>(p.dyk)[size_t(f) * p.pix_ld + size_t(b) * hw_n + hw] =
-          __float2bfloat16_rn(tile[j][tx]);
+      reinterpret_cast<__nv_bfloat16*>(p.dyk)[size_t(f) * p.pix_ld + size_t(b) * hw_n + hw] = __float2bfloat16_rn(v[i]);
   }
   __syncthreads();
   const int fld = p.bf16 ? (p.f + 7) & ~7 : (p.f + 3) & ~3;  // dyt rows padded to 16 bytes (TMA)
