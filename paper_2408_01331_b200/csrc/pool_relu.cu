@@ -69,12 +69,17 @@ __global__ void __launch_bounds__(PTHREADS) maxpool_bwd_kernel(const hnn_pool_pr
   if (b < cur[p.model].rows && p.k == 2 && p.stride == 2) {
     // the common non-overlapping 2 x 2 window: exactly one window covers (y, x)
     const int oy = y >> 1, ox = x >> 1;
+    // the window's argmax, its gradient and the relu mask are requested together (a gradient
+    // load issued only after the argmax compare cost a second round trip)
+    const float mk = p.mask ? p.mask[e] : 1.0f;
     if (oy < p.oh && ox < p.ow) {
       const size_t o = size_t(plane) * p.oh * p.ow + size_t(oy) * p.ow + ox;
-      if (p.idx[o] == ((y & 1) << 1 | (x & 1))) acc = p.dy[o];
+      const float d = p.dy[o];
+      const int ix = p.idx[o];
+      if (ix == ((y & 1) << 1 | (x & 1))) acc = d;
       acc = __fadd_rn(0.0f, acc);  // (the general path's 0 + dy: -0 -> +0)
     }
-    if (p.mask) acc = np_mask(acc, p.mask[e]);
+    if (p.mask) acc = np_mask(acc, mk);
   } else if (b < cur[p.model].rows) {
     // windows (oy, ox) covering (y, x), visited in ascending (oy, ox) like np.add.at's index order
     const int oy_lo = max(0, (y - p.k + p.stride) / p.stride), oy_hi = min(p.oh - 1, y / p.stride);
