@@ -227,7 +227,17 @@ namespace hnn {
 constexpr int DTHREADS = 256;
 
 __device__ __forceinline__ void stage(float* dst, const float* __restrict__ src, int n) {
-  for (int i = threadIdx.x; i < n; i += blockDim.x) dst[i] = __ldg(src + i);
+  // eight loads in flight per thread before their shared-memory stores
+  const int step = blockDim.x;
+  int i = threadIdx.x;
+  for (; i + 7 * step < n; i += 8 * step) {
+    float v[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) v[u] = __ldg(src + i + u * step);
+#pragma unroll
+    for (int u = 0; u < 8; ++u) dst[i + u * step] = v[u];
+  }
+  for (; i < n; i += step) dst[i] = __ldg(src + i);
 }
 
 // Register-blocked stride-1 paths (LeNet-class layers): a thread computes 4 consecutive outputs of
