@@ -35,9 +35,26 @@ __global__ void __launch_bounds__(PTHREADS) maxpool_fwd_kernel(const hnn_pool_pr
   }
   const float* src = p.x + size_t(plane) * p.h * p.w;
   // numpy argmax over the window flattened (i, j): first max wins, first NaN wins outright
-  float best = src[(oy * p.stride) * p.w + ox * p.stride];
+  float best;
   int best_i = 0;
-  if (best == best) {
+  if (p.k == 2 && p.stride == 2 && 2 * oy + 1 < p.h && 2 * ox + 1 < p.w) {
+    // the common 2 x 2 window: its four values requested together, then the same scan
+    const float* s0 = src + (2 * oy) * p.w + 2 * ox;
+    const float v0 = s0[0], v1 = s0[1], v2 = s0[p.w], v3 = s0[p.w + 1];
+    best = v0;
+    if (best == best) {
+      const float vs[3] = {v1, v2, v3};
+#pragma unroll
+      for (int q = 1; q < 4; ++q) {
+        const float v = vs[q - 1];
+        if (!(v <= best)) {
+          best = v;
+          best_i = q;
+          if (v != v) break;
+        }
+      }
+    }
+  } else if ((best = src[(oy * p.stride) * p.w + ox * p.stride]) == best) {
     for (int q = 1; q < p.k * p.k; ++q) {
       const int i = q / p.k, j = q - i * p.k;
       const float v = src[(oy * p.stride + i) * p.w + ox * p.stride + j];
