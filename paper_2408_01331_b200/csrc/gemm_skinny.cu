@@ -16,7 +16,7 @@ namespace hnn {
 
 constexpr int KTHREADS = 256;
 constexpr int FWD_ROWS = 2;  // rows per warp; tile = 8 warps x 2 rows = 16 rows (2 waves of CTAs on C3)
-constexpr int DG_ROWS = 4;   // DGRAD rows per thread; tile = 8 row groups x 4 rows x 128 columns
+constexpr int DG_ROWS = 8;   // DGRAD rows per thread; tile = 8 row groups x 8 rows x 128 columns
 constexpr int WG_QUADS = 64; // WGRAD column quads per CTA; tile = 256 columns, 4 row quarters
 
 __device__ __forceinline__ float4 ldg4(const float* p) { return __ldg(reinterpret_cast<const float4*>(p)); }
@@ -154,16 +154,23 @@ __device__ __forceinline__ void outer_rows(const hnn_gemm_problem& p, int r0, in
 __global__ void __launch_bounds__(KTHREADS) skinny_dgrad_kernel(const hnn_gemm_problem* __restrict__ probs, int nprob,
                                                                 const hnn_step_row* __restrict__ cur,
                                                                 const hnn_model_status* __restrict__ status) {
-  __shared__ float dys[8 * DG_ROWS * 16];  // the CTA's 32 dy rows, 16 columns (zero padded)
+  __shared__ float dys[8 * DG_ROWS * 16];  // the CTA's 64 dy rows, 16 columns (zero padded)
   const int pi = find_problem(probs, nprob, blockIdx.x, [](const hnn_gemm_problem& q) { return q.tile_base; });
   const hnn_gemm_problem& p = probs[pi];
   if (!live(cur, status, p.model)) return;
   const int rows = cur[p.model].rows;
   const int t = blockIdx.x - p.tile_base;
   const int m0 = (t / p.tiles_n) * (8 * DG_ROWS), n0 = (t % p.tiles_n) * 128;
-  for (int e = threadIdx.x; e < 8 * DG_ROWS * 16; e += KTHREADS) {
-    const int r = m0 + e / 16, j = e % 16;
-    dys[e] = (j < p.k && r < rows && r < p.m) ? __ldg(p.a + size_t(r) * p.lda + j) : 0.0f;
+  {  // the CTA's dy rows: every thread's loads issued before its shared-memory stores
+    constexpr int PER = 8 * DG_ROWS * 16 / KTHREADS;
+    float v[PER];
+#pragma unroll
+    for (int u = 0; u < PER; ++u) {
+      const int e = threadIdx.x + u * KTHREADS, r = m0 + e / 16, j = e % 16;
+      v[u] = (j < p.k && r < rows && r < p.m) ? __ldg(p.a + size_t(r) * p.lda + j) : 0.0f;
+    }
+#pragma unroll
+    for (int u = 0; u < PER; ++u) dys[threadIdx.x + u * KTHREADS] = v[u];
   }
   __syncthreads();
   const int col = n0 + (threadIdx.x & 31) * 4, r0 = m0 + (threadIdx.x >> 5) * DG_ROWS;
