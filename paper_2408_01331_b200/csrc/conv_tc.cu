@@ -399,6 +399,44 @@ __global__ void __launch_bounds__(CT_THREADS) wgrad_reduce_kernel(const hnn_conv
   const size_t ptotal = size_t((p.f + 31) & ~31) * p.kkp;
   const long long tid = (long long)(blockIdx.x - p.block_base) * CT_THREADS + threadIdx.x;
   const int kk2 = p.k * p.k;
+  if ((p.kk & 3) == 0 && (p.kkp & 3) == 0) {
+    // four consecutive partial columns per thread: 16-byte loads, 8 splits x 16 bytes in flight
+    for (int e4 = int(tid); e4 < total / 4; e4 += p.blocks * CT_THREADS) {
+      const int e = 4 * e4, f = e / p.kk, col = e - f * p.kk;
+      const size_t pe = size_t(f) * p.kkp + col;
+      float4 v[8];
+      const int s8 = min(splits, 8);
+#pragma unroll
+      for (int s = 0; s < 8; ++s)
+        v[s] = s < s8 ? __ldg(reinterpret_cast<const float4*>(p.partial + s * ptotal + pe)) : make_float4(0, 0, 0, 0);
+      float4 acc = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
+#pragma unroll
+      for (int s = 0; s < 8; ++s)
+        if (s < s8) {
+          acc.x = __fadd_rn(acc.x, v[s].x);
+          acc.y = __fadd_rn(acc.y, v[s].y);
+          acc.z = __fadd_rn(acc.z, v[s].z);
+          acc.w = __fadd_rn(acc.w, v[s].w);
+        }
+      for (int s = 8; s < splits; ++s) {
+        const float4 t = __ldg(reinterpret_cast<const float4*>(p.partial + s * ptotal + pe));
+        acc.x = __fadd_rn(acc.x, t.x);
+        acc.y = __fadd_rn(acc.y, t.y);
+        acc.z = __fadd_rn(acc.z, t.z);
+        acc.w = __fadd_rn(acc.w, t.w);
+      }
+      const float a4[4] = {acc.x, acc.y, acc.z, acc.w};
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        int kr = col + q;
+        if (p.rsc) {
+          const int rs = (col + q) / p.c;
+          kr = (col + q - rs * p.c) * kk2 + rs;
+        }
+        p.dw[size_t(f) * p.kk + kr] = a4[q];
+      }
+    }
+  } else
   for (int e = int(tid); e < total; e += p.blocks * CT_THREADS) {
     // e walks the partial columns (coalesced reads of every split); rsc: partial column (r, s, c)
     // goes to reference column (c, r, s)
@@ -427,7 +465,15 @@ __global__ void __launch_bounds__(CT_THREADS) wgrad_reduce_kernel(const hnn_conv
   const int nq = rows * ((p.oh * p.ow + 31) / 32);
   for (long long f = warp; f < p.f; f += nwarps) {
     float acc = 0.0f;
-    for (int q = lane; q < nq; q += 32) acc = __fadd_rn(acc, __ldg(p.bpart + size_t(q) * p.f + f));
+    int q = lane;
+    for (; q + 7 * 32 < nq; q += 8 * 32) {  // eight partials in flight, added in the same order
+      float v[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) v[u] = __ldg(p.bpart + size_t(q + u * 32) * p.f + f);
+#pragma unroll
+      for (int u = 0; u < 8; ++u) acc = __fadd_rn(acc, v[u]);
+    }
+    for (; q < nq; q += 32) acc = __fadd_rn(acc, __ldg(p.bpart + size_t(q) * p.f + f));
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) acc = __fadd_rn(acc, __shfl_xor_sync(0xffffffffu, acc, o));
     if (lane == 0) p.db[f] = acc;
