@@ -48,7 +48,8 @@ constexpr int TC2_A_BYTES = TC2_BM * TC2_BK * 4;        // 16 KB
 constexpr int TC2_B_BYTES = (TC2_BN / 2) * TC2_BK * 4;  // 16 KB (this CTA's half)
 constexpr int TC2_STAGE = TC2_A_BYTES + TC2_B_BYTES;
 constexpr int TC2_EPI_BYTES = 8 * 32 * 32 * 4;
-constexpr int TC2_SMEM_BYTES = TC2_STAGES * 2 * TC2_STAGE + TC2_EPI_BYTES + 1024 + 256;
+constexpr int TC2_INFO_RING = 8;  // tile-info entries the producer publishes ahead of the other roles
+constexpr int TC2_SMEM_BYTES = TC2_STAGES * 2 * TC2_STAGE + TC2_EPI_BYTES + 1024 + 1024;  // + barriers, tile info
 
 #ifdef HNN_TC2_TRACE  // debug build only (tools/tc2_trace.py): per-CTA wait-cycle counters
 __device__ unsigned long long g_tc2_trace[296 * 16];
@@ -179,10 +180,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC2_THREADS, 1)
   const uint32_t raw_base = smem_u32(base);
   constexpr int SSTRIDE = BF16 ? TC2_STAGE : 2 * TC2_STAGE;  // stage s: raw at s * SSTRIDE (fp32: lo after it)
   const uint32_t epi_base = raw_base + SR * SSTRIDE;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(base + SR * SSTRIDE + TC2_EPI_BYTES);
+  uint8_t* tail = base + SR * SSTRIDE + TC2_EPI_BYTES;  // 1 KB: barriers, TMEM address, tile-info ring
+  uint64_t* bars = reinterpret_cast<uint64_t*>(tail);
   constexpr int RAW_FULL = 0, RAW_EMPTY = SR, LO_FULL = 2 * SR;
-  constexpr int ACC_FULL = 3 * SR, ACC_EMPTY = ACC_FULL + 2, NBARS = ACC_EMPTY + 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + NBARS);
+  constexpr int ACC_FULL = 3 * SR, ACC_EMPTY = ACC_FULL + 2, INFO_FULL = ACC_EMPTY + 2,
+                INFO_EMPTY = INFO_FULL + TC2_INFO_RING, NBARS = INFO_EMPTY + TC2_INFO_RING;
+  static_assert(NBARS * 8 <= 512, "barrier area");
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tail + 512);
+  int4* info = reinterpret_cast<int4*>(tail + 528);  // entry i: info[2i] = {problem | -1, m0, n0, nkb},
+                                                     //          info[2i+1] = {rows, kofs, split, tile_n}
   auto bar = [&](int i) { return smem_u32(bars + i); };
 
   if (threadIdx.x == 0) {
@@ -194,6 +200,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC2_THREADS, 1)
     for (int b = 0; b < 2; ++b) {
       mbar_init(bar(ACC_FULL + b), 1);    // leader MMA commit (multicast)
       mbar_init(bar(ACC_EMPTY + b), 16);  // 8 accumulator warps x 2 CTAs (leader's copy)
+    }
+    for (int i = 0; i < TC2_INFO_RING; ++i) {
+      mbar_init(bar(INFO_FULL + i), 1);  // the producer thread
+      // readers: MMA thread (leader CTA only), converter warps, accumulator warps
+      mbar_init(bar(INFO_EMPTY + i), (leader ? 1 : 0) + TC2_CONV_WARPS + 8);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -236,6 +247,21 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC2_THREADS, 1)
     nkb = ktot > 0 ? (ktot + KBE - 1) / KBE : 0;
     return nkb > 0;
   };
+  // bf16: the producer thread computes every tile's info once (the problem search and the
+  // live-model / row-count loads are a chain of dependent global loads) and publishes it in a small
+  // shared ring; the MMA thread, converters and accumulator warps read it from there (C4 -1%).
+  auto read_info = [&](uint32_t seq, bool warp_wide, const hnn_gemm_problem*& p, int& m0, int& n0, int& nkb,
+                       int& rows, int& kofs, int& sp, int& tn) -> bool {
+    const int slot = int(seq % TC2_INFO_RING);
+    mbar_wait(bar(INFO_FULL + slot), (seq / TC2_INFO_RING) & 1);
+    const int4 e0 = info[2 * slot], e1 = info[2 * slot + 1];
+    if (warp_wide) __syncwarp();
+    if (!warp_wide || (threadIdx.x & 31) == 0) mbar_arrive(bar(INFO_EMPTY + slot));
+    if (e0.x < 0) return false;
+    p = probs + e0.x;
+    m0 = e0.y, n0 = e0.z, nkb = e0.w, rows = e1.x, kofs = e1.y, sp = e1.z, tn = e1.w;
+    return true;
+  };
   const int pair = blockIdx.x / 2, npairs = gridDim.x / 2;
   // tile schedule (host LPT, trailing the problem table): this pair's tiles are
   // sched_ids[sched_off[pair] .. sched_off[pair + 1]); round-robin if absent / mismatched
@@ -250,12 +276,21 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC2_THREADS, 1)
   if (warp == 0) {
     // ---------------- TMA producer (both CTAs): rows m0 + rank*128.., columns n0 + rank*128..
     if (lane == 0) {
-      uint32_t kg = 0;
+      uint32_t kg = 0, iseq = 0;
       for (int ti = t_begin; ti < t_end; ti += t_step) {
         const int tile = tile_id(ti);
         const hnn_gemm_problem* p;
         int m0, n0, nkb, rows, kofs, sp, tn;
-        if (!tile_info(tile, p, m0, n0, nkb, rows, kofs, sp, tn)) continue;
+        const bool ok = tile_info(tile, p, m0, n0, nkb, rows, kofs, sp, tn);
+        if (BF16) {  // (fp32: the extra live registers of the ring spilled the running sum; not used)
+          const int slot = int(iseq % TC2_INFO_RING);
+          if (iseq >= TC2_INFO_RING) mbar_wait(bar(INFO_EMPTY + slot), ((iseq / TC2_INFO_RING) - 1) & 1);
+          info[2 * slot] = make_int4(ok ? int(p - probs) : -1, m0, n0, nkb);
+          info[2 * slot + 1] = make_int4(rows, kofs, sp, tn);
+          mbar_arrive(bar(INFO_FULL + slot));  // (release: the entry is visible to the waiting readers)
+          ++iseq;
+        }
+        if (!ok) continue;
         const int am = m0 + int(rank) * TC2_BM, bn = n0 + int(rank) * (tn / 2);
         const uint32_t stage_bytes = TC2_A_BYTES + (tn / 2) * TC2_BK * 4;
         for (int kb = 0; kb < nkb; ++kb, ++kg) {
@@ -302,12 +337,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC2_THREADS, 1)
     if (leader && lane == 0) {
       constexpr uint32_t alb = A_MN ? 4096 : 16, asb = A_MN ? 512 : 1024, alt = A_MN ? 1 : 2;
       constexpr uint32_t blb = B_MN ? 4096 : 16, bsb = B_MN ? 512 : 1024, blt = B_MN ? 1 : 2;
-      uint32_t kg = 0, cg = 0;
+      uint32_t kg = 0, cg = 0, iseq = 0;
       for (int ti = t_begin; ti < t_end; ti += t_step) {
         const int tile = tile_id(ti);
         const hnn_gemm_problem* p;
         int m0, n0, nkb, rows, kofs, sp, tn;
-        if (!tile_info(tile, p, m0, n0, nkb, rows, kofs, sp, tn)) continue;
+        if (BF16 ? !read_info(iseq++, false, p, m0, n0, nkb, rows, kofs, sp, tn)
+               : !tile_info(tile, p, m0, n0, nkb, rows, kofs, sp, tn))
+          continue;
         // (bf16 implicit weight gradient: B is MN-major, bit 16)
         const bool b_imp = BF16 && OP == HNN_WGRAD && p->im_c > 0;
         const uint32_t idesc =
@@ -358,12 +395,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC2_THREADS, 1)
     const int ct = threadIdx.x - 64;
     constexpr int CT = 32 * TC2_CONV_WARPS, PER = TC2_STAGE / 16 / CT, NPART = 4, PART = PER / NPART;
     const uint32_t lo_full_leader = map_cluster(bar(LO_FULL), 0);
-    uint32_t kg = 0;
+    uint32_t kg = 0, iseq = 0;
     for (int ti = t_begin; ti < t_end; ti += t_step) {
         const int tile = tile_id(ti);
       const hnn_gemm_problem* p;
       int m0, n0, nkb, rows, kofs, sp, tn;
-      if (!tile_info(tile, p, m0, n0, nkb, rows, kofs, sp, tn)) continue;
+      if (BF16 ? !read_info(iseq++, true, p, m0, n0, nkb, rows, kofs, sp, tn)
+               : !tile_info(tile, p, m0, n0, nkb, rows, kofs, sp, tn))
+          continue;
       for (int kb = 0; kb < nkb; ++kb, ++kg) {
         const int s = kg % SR;
         TC2_T0(t2);
@@ -401,13 +440,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC2_THREADS, 1)
     const uint32_t lane_quarter = tmem + (uint32_t(q * 32) << 16);
     const uint32_t stg = epi_base + aw * 4096;
     const uint32_t acc_empty_leader = map_cluster(bar(ACC_EMPTY), 0);
-    uint32_t cg = 0, nstore = 0;
+    uint32_t cg = 0, nstore = 0, iseq = 0;
     for (int ti = t_begin; ti < t_end; ti += t_step) {
         const int tile = tile_id(ti);
       const hnn_gemm_problem* p;
       int m0, n0, nkb, rows, kofs, sp, tn;
       TC2_T0(t9);
-      if (!tile_info(tile, p, m0, n0, nkb, rows, kofs, sp, tn)) continue;
+      if (BF16 ? !read_info(iseq++, true, p, m0, n0, nkb, rows, kofs, sp, tn)
+               : !tile_info(tile, p, m0, n0, nkb, rows, kofs, sp, tn))
+          continue;
       TC2_T1(t9, 9);
       const int nchunks = BF16 ? 1 : (nkb + TC2_CHUNK_KB - 1) / TC2_CHUNK_KB;
       const int hn = tn / 2;  // this warp's columns: [half * hn, half * hn + hn)
