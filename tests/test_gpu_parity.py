@@ -804,3 +804,82 @@ def test_host_fed_stepper_matches_device_gather(pkg):
     for a, b in zip(*outs):
         for k in a:
             assert np.array_equal(a[k], b[k]), k
+
+
+def _full_size_run(workload, js, ds, ddev, steps):
+    import torch
+
+    import bench  # (repo root on sys.path: tests/conftest.py)
+    from paper_2408_01331_b200 import merge
+
+    device = torch.device("cuda", 0)
+    hy = merge(js)
+    dev = hy.materialize(device, conv_precision="bf16" if workload == "c4" else "f32")
+    dev.bind_datasets([ddev] * dev.n, ddev.n_train)
+    dev.build_plans()
+    rows = bench.schedule(js, ds, steps)
+    bench.upload_perms(dev, js, ds)
+    dev.load_schedule(rows)
+    dev.train_steps(steps, use_graph=True)
+    torch.cuda.synchronize()
+    return dev
+
+
+@pytest.mark.gpu
+def test_full_size_c3_isolation(pkg):
+    """BASELINE C3 at full size (32 MLPs 784-h-h-10, h = 128..2048, Adam, batch 256), 3 lockstep
+    steps: every model's loss is finite, and models 0 and 17 end bit-identical to a 2-model hybrid
+    holding only them — the size-independent isolation property, with problem tables, tile widths
+    and the LPT tile schedule all different between the two hybrids."""
+    import torch
+
+    import bench
+    from paper_2408_01331_b200 import zoo
+    from paper_2408_01331_b200.runtime import DeviceDataset
+
+    ds = bench.make_dataset("c3")
+    ddev = DeviceDataset(ds, torch.device("cuda", 0))
+    jobs = zoo.config_jobs("c3", ds)
+    assert len(jobs) == 32
+    full = _full_size_run("c3", jobs, ds, ddev, 3)
+    assert np.all(np.isfinite(full.loss_out.cpu().numpy()))
+    sub = _full_size_run("c3", [jobs[0], jobs[17]], ds, ddev, 3)
+    for m_full, m_sub in ((0, 0), (17, 1)):
+        a, b = full.download_params(m_full), sub.download_params(m_sub)
+        for k in a:
+            assert np.array_equal(a[k], b[k]), (m_full, k)
+
+
+@pytest.mark.gpu
+def test_full_size_c4_steps_are_finite(pkg):
+    """BASELINE C4 per GPU at full size (ResNet-18-plain, VGG-11-noBN, 2 LeNet-5 on bf16 tensor-core
+    convolutions, batch 128): 3 lockstep steps give finite losses and parameters, and every weight
+    tensor of every model moved (each layer received a gradient)."""
+    import torch
+
+    import bench
+    from paper_2408_01331_b200 import zoo
+    from paper_2408_01331_b200.runtime import DeviceDataset
+
+    ds = bench.make_dataset("c4")
+    ddev = DeviceDataset(ds, torch.device("cuda", 0))
+    jobs = zoo.config_jobs("c4", ds, count=bench.MODELS_PER_GPU["c4"])
+    from paper_2408_01331_b200 import merge
+
+    hy = merge(jobs)
+    dev = hy.materialize(torch.device("cuda", 0), conv_precision="bf16")
+    before = [dev.download_params(m) for m in range(len(jobs))]
+    dev.bind_datasets([ddev] * dev.n, ddev.n_train)
+    dev.build_plans()
+    rows = bench.schedule(jobs, ds, 3)
+    bench.upload_perms(dev, jobs, ds)
+    dev.load_schedule(rows)
+    dev.train_steps(3, use_graph=True)
+    torch.cuda.synchronize()
+    assert np.all(np.isfinite(dev.loss_out.cpu().numpy()))
+    for m in range(len(jobs)):
+        after = dev.download_params(m)
+        for k, v in after.items():
+            assert np.all(np.isfinite(v)), (m, k)
+            if k.endswith(".weight"):
+                assert not np.array_equal(v, before[m][k]), (m, k)
