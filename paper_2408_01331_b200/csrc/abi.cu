@@ -59,14 +59,21 @@ __global__ void __launch_bounds__(32 * GATHER_ROWS) gather_rows_kernel(const hnn
     float4* d4 = reinterpret_cast<float4*>(dst);
     const int n4 = p.sample / 4;
     int i = lane;
-    for (; i + 96 < n4; i += 128) {  // 4 independent 16-byte loads per lane per round
-      const float4 a = __ldg(s4 + i), b = __ldg(s4 + i + 32), c = __ldg(s4 + i + 64), d = __ldg(s4 + i + 96);
-      d4[i] = a;
-      d4[i + 32] = b;
-      d4[i + 64] = c;
-      d4[i + 96] = d;
+    for (; i + 224 < n4; i += 256) {  // 8 independent 16-byte loads per lane per round
+      float4 v[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) v[u] = __ldg(s4 + i + 32 * u);
+#pragma unroll
+      for (int u = 0; u < 8; ++u) d4[i + 32 * u] = v[u];
     }
-    for (; i < n4; i += 32) d4[i] = __ldg(s4 + i);
+    {  // the rest (an MNIST row: 196 float4 = 6.1 per lane) in one round as well
+      float4 v[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) v[u] = i + 32 * u < n4 ? __ldg(s4 + i + 32 * u) : make_float4(0, 0, 0, 0);
+#pragma unroll
+      for (int u = 0; u < 8; ++u)
+        if (i + 32 * u < n4) d4[i + 32 * u] = v[u];
+    }
   } else {
     for (int i = lane; i < p.sample; i += 32) dst[i] = __ldg(src + i);
   }
