@@ -188,7 +188,7 @@ template <int MJ>
 __device__ __forceinline__ void colacc(const hnn_gemm_problem& p, int col, int r_lo, int r_hi, int base,
                                        float (&part)[16][4], const float* dys) {
   const float* x = p.b + col;
-#pragma unroll 4
+#pragma unroll 8  // (eight rows of x in flight per thread: one CTA per SM on C3)
   for (int r = r_lo; r < r_hi; ++r) {
     const float4 xv = ldg4(x + size_t(r) * p.ldb);
     const float* d = dys + (r - base) * 16;
