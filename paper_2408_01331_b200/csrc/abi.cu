@@ -23,6 +23,7 @@ int check_launch(const char* where) {
 // sched row block `*counter` -> cur, then advance.  One block; n_models*12 words.
 __global__ void step_begin_kernel(const hnn_step_row* __restrict__ sched, int32_t* counter,
                                   hnn_step_row* __restrict__ cur, int n_models) {
+  hnn::pdl_wait();
   const int step = *counter;
   const int words = n_models * int(sizeof(hnn_step_row) / 4);
   const int32_t* src = reinterpret_cast<const int32_t*>(sched + size_t(step) * n_models);
@@ -39,6 +40,7 @@ constexpr int GATHER_ROWS = 8;
 
 __global__ void __launch_bounds__(32 * GATHER_ROWS) gather_rows_kernel(const hnn_gather_problem* __restrict__ probs,
                                                                        const hnn_step_row* __restrict__ cur) {
+  hnn::pdl_wait();
   const hnn_gather_problem& p = probs[blockIdx.y];
   const int lane = threadIdx.x % 32;
   const int r = blockIdx.x * GATHER_ROWS + threadIdx.x / 32;
@@ -107,7 +109,7 @@ int hnn_struct_size(const char* name) {
 
 int hnn_step_begin(const hnn_step_row* sched, int32_t* counter, hnn_step_row* cur, int n_models, void* stream) {
   HNN_REQUIRE(sched && counter && cur && n_models > 0, "hnn_step_begin", "null pointer or empty model set");
-  hnn::step_begin_kernel<<<1, 256, 0, hnn::as_stream(stream)>>>(sched, counter, cur, n_models);
+  hnn::launch_pdl(hnn::step_begin_kernel, dim3(1), dim3(256), 0, hnn::as_stream(stream), sched, counter, cur, n_models);
   return hnn::check_launch("hnn_step_begin");
 }
 
@@ -116,7 +118,7 @@ int hnn_gather_rows(const hnn_gather_problem* probs, int nprob, int max_cap, con
   HNN_REQUIRE(probs && cur && nprob > 0 && max_cap > 0, "hnn_gather_rows", "bad arguments");
   HNN_REQUIRE(nprob <= 65535, "hnn_gather_rows", "too many problems");
   dim3 grid((max_cap + hnn::GATHER_ROWS - 1) / hnn::GATHER_ROWS, nprob);
-  hnn::gather_rows_kernel<<<grid, 32 * hnn::GATHER_ROWS, 0, hnn::as_stream(stream)>>>(probs, cur);
+  hnn::launch_pdl(hnn::gather_rows_kernel, dim3(grid), dim3(32 * hnn::GATHER_ROWS), 0, hnn::as_stream(stream), probs, cur);
   return hnn::check_launch("hnn_gather_rows");
 }
 

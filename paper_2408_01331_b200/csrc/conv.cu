@@ -38,6 +38,7 @@ template <int OP>
 __global__ void __launch_bounds__(CTHREADS) conv_kernel(const hnn_conv_problem* __restrict__ probs, int nprob,
                                                         const hnn_step_row* __restrict__ cur,
                                                         const hnn_model_status* __restrict__ status) {
+  hnn::pdl_wait();
   __shared__ float As[CBK][CBM + 4];
   __shared__ float Bs[CBK][CBN + 4];
   const int pi = find_problem(probs, nprob, blockIdx.x, [](const hnn_conv_problem& q) { return q.tile_base; });
@@ -170,6 +171,7 @@ __global__ void __launch_bounds__(CTHREADS) conv_kernel(const hnn_conv_problem* 
 __global__ void conv_wgrad_reduce_kernel(const hnn_conv_problem* __restrict__ probs, int nprob,
                                          const hnn_step_row* __restrict__ cur,
                                          const hnn_model_status* __restrict__ status) {
+  hnn::pdl_wait();
   const int pi = find_problem(probs, nprob, blockIdx.x, [](const hnn_conv_problem& q) { return q.tile_base; });
   const hnn_conv_problem p = probs[pi];
   if (!live(cur, status, p.model)) return;
@@ -196,9 +198,9 @@ extern "C" int hnn_grouped_conv(int op, const hnn_conv_problem* probs, int nprob
                                 const hnn_step_row* cur, const hnn_model_status* status, void* stream) {
   HNN_REQUIRE(probs && cur && nprob > 0 && total_tiles > 0, "hnn_grouped_conv", "bad arguments");
   cudaStream_t s = hnn::as_stream(stream);
-  if (op == HNN_FWD) hnn::conv_kernel<HNN_FWD><<<total_tiles, hnn::CTHREADS, 0, s>>>(probs, nprob, cur, status);
-  else if (op == HNN_DGRAD) hnn::conv_kernel<HNN_DGRAD><<<total_tiles, hnn::CTHREADS, 0, s>>>(probs, nprob, cur, status);
-  else if (op == HNN_WGRAD) hnn::conv_kernel<HNN_WGRAD><<<total_tiles, hnn::CTHREADS, 0, s>>>(probs, nprob, cur, status);
+  if (op == HNN_FWD) hnn::launch_pdl(hnn::conv_kernel<HNN_FWD>, dim3(total_tiles), dim3(hnn::CTHREADS), 0, s, probs, nprob, cur, status);
+  else if (op == HNN_DGRAD) hnn::launch_pdl(hnn::conv_kernel<HNN_DGRAD>, dim3(total_tiles), dim3(hnn::CTHREADS), 0, s, probs, nprob, cur, status);
+  else if (op == HNN_WGRAD) hnn::launch_pdl(hnn::conv_kernel<HNN_WGRAD>, dim3(total_tiles), dim3(hnn::CTHREADS), 0, s, probs, nprob, cur, status);
   else {
     hnn::set_error("hnn_grouped_conv", "unknown op");
     return HNN_ERR_INVALID;
@@ -210,7 +212,7 @@ extern "C" int hnn_grouped_conv(int op, const hnn_conv_problem* probs, int nprob
 extern "C" int hnn_conv_wgrad_reduce(const hnn_conv_problem* probs, int nprob, int total_blocks,
                                      const hnn_step_row* cur, const hnn_model_status* status, void* stream) {
   HNN_REQUIRE(probs && cur && nprob > 0 && total_blocks > 0, "hnn_conv_wgrad_reduce", "bad arguments");
-  hnn::conv_wgrad_reduce_kernel<<<total_blocks, 256, 0, hnn::as_stream(stream)>>>(probs, nprob, cur, status);
+  hnn::launch_pdl(hnn::conv_wgrad_reduce_kernel, dim3(total_blocks), dim3(256), 0, hnn::as_stream(stream), probs, nprob, cur, status);
   return hnn::check_launch("hnn_conv_wgrad_reduce");
 }
 
@@ -398,6 +400,7 @@ template <int OP>
 __global__ void __launch_bounds__(DTHREADS) conv_direct_kernel(const hnn_conv_problem* __restrict__ probs, int nprob,
                                                                const hnn_step_row* __restrict__ cur,
                                                                const hnn_model_status* __restrict__ status) {
+  hnn::pdl_wait();
   extern __shared__ float sm[];
   const int pi = find_problem(probs, nprob, blockIdx.x, [](const hnn_conv_problem& q) { return q.tile_base; });
   const hnn_conv_problem& p = probs[pi];
@@ -574,19 +577,19 @@ extern "C" int hnn_grouped_conv_direct(int op, const hnn_conv_problem* probs, in
       cudaFuncSetAttribute(hnn::conv_direct_kernel<HNN_FWD>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
       configured[0] = 200 * 1024;
     }
-    hnn::conv_direct_kernel<HNN_FWD><<<total_blocks, hnn::DTHREADS, smem, s>>>(probs, nprob, cur, status);
+    hnn::launch_pdl(hnn::conv_direct_kernel<HNN_FWD>, dim3(total_blocks), dim3(hnn::DTHREADS), smem, s, probs, nprob, cur, status);
   } else if (op == HNN_DGRAD) {
     if (smem > configured[1]) {
       cudaFuncSetAttribute(hnn::conv_direct_kernel<HNN_DGRAD>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
       configured[1] = 200 * 1024;
     }
-    hnn::conv_direct_kernel<HNN_DGRAD><<<total_blocks, hnn::DTHREADS, smem, s>>>(probs, nprob, cur, status);
+    hnn::launch_pdl(hnn::conv_direct_kernel<HNN_DGRAD>, dim3(total_blocks), dim3(hnn::DTHREADS), smem, s, probs, nprob, cur, status);
   } else if (op == HNN_WGRAD) {
     if (smem > configured[2]) {
       cudaFuncSetAttribute(hnn::conv_direct_kernel<HNN_WGRAD>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
       configured[2] = 200 * 1024;
     }
-    hnn::conv_direct_kernel<HNN_WGRAD><<<total_blocks, hnn::DTHREADS, smem, s>>>(probs, nprob, cur, status);
+    hnn::launch_pdl(hnn::conv_direct_kernel<HNN_WGRAD>, dim3(total_blocks), dim3(hnn::DTHREADS), smem, s, probs, nprob, cur, status);
   } else {
     hnn::set_error("hnn_grouped_conv_direct", "unknown op");
     return HNN_ERR_INVALID;

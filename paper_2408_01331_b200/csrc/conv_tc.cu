@@ -32,6 +32,7 @@ constexpr int IC_PIX = 32, IC_CH = 32;
 __global__ void __launch_bounds__(CT_THREADS) im2col_kernel(const hnn_convtc_problem* __restrict__ probs, int nprob,
                                                            const hnn_step_row* __restrict__ cur,
                                                            const hnn_model_status* __restrict__ status) {
+  hnn::pdl_wait();
   extern __shared__ float ic_tile[];  // [IC_PIX][IC_CH * k * k + 1]
   const hnn_convtc_problem& p = ct_problem(probs, nprob, blockIdx.x);
   if (!live(cur, status, p.model)) return;
@@ -199,6 +200,7 @@ int im2col_smem_bytes(int k) { return IC_PIX * (IC_CH * k * k + 1) * 4; }
 __global__ void __launch_bounds__(CT_THREADS) transpose_dy_kernel(const hnn_convtc_problem* __restrict__ probs,
                                                                  int nprob, const hnn_step_row* __restrict__ cur,
                                                                  const hnn_model_status* __restrict__ status) {
+  hnn::pdl_wait();
   __shared__ float tile[32][33];
   const hnn_convtc_problem& p = ct_problem(probs, nprob, blockIdx.x);
   if (!live(cur, status, p.model)) return;
@@ -367,6 +369,7 @@ __device__ __forceinline__ void col2im_tile(const hnn_convtc_problem& p, int row
 __global__ void __launch_bounds__(CT_THREADS) col2im_kernel(const hnn_convtc_problem* __restrict__ probs, int nprob,
                                                            const hnn_step_row* __restrict__ cur,
                                                            const hnn_model_status* __restrict__ status) {
+  hnn::pdl_wait();
   extern __shared__ float ci_tile[];  // [k][CI_OWMAX][CI_CH * k * k + 1]
   const hnn_convtc_problem& p = ct_problem(probs, nprob, blockIdx.x);
   if (!live(cur, status, p.model)) return;
@@ -387,6 +390,7 @@ int col2im_smem_bytes(int k) { return k * CI_OWMAX * (CI_CH * k * k + 1) * 4; }
 __global__ void __launch_bounds__(CT_THREADS) wgrad_reduce_kernel(const hnn_convtc_problem* __restrict__ probs,
                                                                  int nprob, const hnn_step_row* __restrict__ cur,
                                                                  const hnn_model_status* __restrict__ status) {
+  hnn::pdl_wait();
   const hnn_convtc_problem& p = ct_problem(probs, nprob, blockIdx.x);
   if (!live(cur, status, p.model)) return;
   const int rows = cur[p.model].rows;
@@ -485,6 +489,7 @@ __global__ void __launch_bounds__(CT_THREADS) wgrad_reduce_kernel(const hnn_conv
 __global__ void __launch_bounds__(CT_THREADS) pad_weights_kernel(const hnn_convtc_problem* __restrict__ probs, int nprob,
                                                                 const hnn_step_row* __restrict__ cur,
                                                                 const hnn_model_status* __restrict__ status) {
+  hnn::pdl_wait();
   const hnn_convtc_problem& p = ct_problem(probs, nprob, blockIdx.x);
   if (!live(cur, status, p.model)) return;
   const long long total = (long long)p.f * p.kkp;
@@ -502,6 +507,7 @@ __global__ void __launch_bounds__(CT_THREADS) pad_weights_kernel(const hnn_convt
 __global__ void __launch_bounds__(CT_THREADS) flip_weights_kernel(const hnn_convtc_problem* __restrict__ probs,
                                                                  int nprob, const hnn_step_row* __restrict__ cur,
                                                                  const hnn_model_status* __restrict__ status) {
+  hnn::pdl_wait();
   const hnn_convtc_problem& p = ct_problem(probs, nprob, blockIdx.x);
   if (!live(cur, status, p.model)) return;
   const int kk2 = p.k * p.k, row = p.f * kk2;
@@ -528,6 +534,7 @@ template <bool FLIP>
 __global__ void __launch_bounds__(CT_THREADS) rsc_weights_kernel(const hnn_convtc_problem* __restrict__ probs, int nprob,
                                                                 const hnn_step_row* __restrict__ cur,
                                                                 const hnn_model_status* __restrict__ status) {
+  hnn::pdl_wait();
   __shared__ float stage[RSC_MAX];
   const hnn_convtc_problem& p = ct_problem(probs, nprob, blockIdx.x);
   if (!live(cur, status, p.model)) return;
@@ -560,6 +567,7 @@ __global__ void __launch_bounds__(CT_THREADS) rsc_weights_kernel(const hnn_convt
 __global__ void __launch_bounds__(CT_THREADS) parity_weights_kernel(const hnn_convtc_problem* __restrict__ probs,
                                                                    int nprob, const hnn_step_row* __restrict__ cur,
                                                                    const hnn_model_status* __restrict__ status) {
+  hnn::pdl_wait();
   const hnn_convtc_problem& p = ct_problem(probs, nprob, blockIdx.x);
   if (!live(cur, status, p.model)) return;
   const int ph = p.ksplit >> 1, pw = p.ksplit & 1, kh = 1 + ph, kw = 1 + pw;
@@ -578,6 +586,7 @@ __global__ void __launch_bounds__(CT_THREADS) parity_weights_kernel(const hnn_co
 __global__ void __launch_bounds__(CT_THREADS) wt_weights_kernel(const hnn_convtc_problem* __restrict__ probs, int nprob,
                                                                const hnn_step_row* __restrict__ cur,
                                                                const hnn_model_status* __restrict__ status) {
+  hnn::pdl_wait();
   const hnn_convtc_problem& p = ct_problem(probs, nprob, blockIdx.x);
   if (!live(cur, status, p.model)) return;
   const long long total = (long long)p.kkp * p.f;
@@ -599,36 +608,36 @@ extern "C" int hnn_conv_tc_aux(int op, const hnn_convtc_problem* probs, int npro
     case HNN_CONVTC_IM2COL:
       HNN_REQUIRE(max_k > 0 && max_k <= 5, "hnn_conv_tc_aux", "kernel size above 5");
       cudaFuncSetAttribute(hnn::im2col_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, hnn::im2col_smem_bytes(5));
-      hnn::im2col_kernel<<<total_blocks, hnn::CT_THREADS, hnn::im2col_smem_bytes(max_k), s>>>(probs, nprob, cur, status);
+      hnn::launch_pdl(hnn::im2col_kernel, dim3(total_blocks), dim3(hnn::CT_THREADS), hnn::im2col_smem_bytes(max_k), s, probs, nprob, cur, status);
       break;
     case HNN_CONVTC_TRANSPOSE_DY:
-      hnn::transpose_dy_kernel<<<total_blocks, hnn::CT_THREADS, 0, s>>>(probs, nprob, cur, status);
+      hnn::launch_pdl(hnn::transpose_dy_kernel, dim3(total_blocks), dim3(hnn::CT_THREADS), 0, s, probs, nprob, cur, status);
       break;
     case HNN_CONVTC_COL2IM:
       HNN_REQUIRE(max_k > 0 && max_k <= 3, "hnn_conv_tc_aux", "kernel size above 3");
       cudaFuncSetAttribute(hnn::col2im_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, hnn::col2im_smem_bytes(3));
-      hnn::col2im_kernel<<<total_blocks, hnn::CT_THREADS, hnn::col2im_smem_bytes(max_k), s>>>(probs, nprob, cur, status);
+      hnn::launch_pdl(hnn::col2im_kernel, dim3(total_blocks), dim3(hnn::CT_THREADS), hnn::col2im_smem_bytes(max_k), s, probs, nprob, cur, status);
       break;
     case HNN_CONVTC_PAD_WEIGHTS:
-      hnn::pad_weights_kernel<<<total_blocks, hnn::CT_THREADS, 0, s>>>(probs, nprob, cur, status);
+      hnn::launch_pdl(hnn::pad_weights_kernel, dim3(total_blocks), dim3(hnn::CT_THREADS), 0, s, probs, nprob, cur, status);
       break;
     case HNN_CONVTC_FLIP_WEIGHTS:
-      hnn::flip_weights_kernel<<<total_blocks, hnn::CT_THREADS, 0, s>>>(probs, nprob, cur, status);
+      hnn::launch_pdl(hnn::flip_weights_kernel, dim3(total_blocks), dim3(hnn::CT_THREADS), 0, s, probs, nprob, cur, status);
       break;
     case HNN_CONVTC_PAD_WEIGHTS_RSC:
-      hnn::rsc_weights_kernel<false><<<total_blocks, hnn::CT_THREADS, 0, s>>>(probs, nprob, cur, status);
+      hnn::launch_pdl(hnn::rsc_weights_kernel<false>, dim3(total_blocks), dim3(hnn::CT_THREADS), 0, s, probs, nprob, cur, status);
       break;
     case HNN_CONVTC_FLIP_WEIGHTS_RSC:
-      hnn::rsc_weights_kernel<true><<<total_blocks, hnn::CT_THREADS, 0, s>>>(probs, nprob, cur, status);
+      hnn::launch_pdl(hnn::rsc_weights_kernel<true>, dim3(total_blocks), dim3(hnn::CT_THREADS), 0, s, probs, nprob, cur, status);
       break;
     case HNN_CONVTC_PARITY_WEIGHTS:
-      hnn::parity_weights_kernel<<<total_blocks, hnn::CT_THREADS, 0, s>>>(probs, nprob, cur, status);
+      hnn::launch_pdl(hnn::parity_weights_kernel, dim3(total_blocks), dim3(hnn::CT_THREADS), 0, s, probs, nprob, cur, status);
       break;
     case HNN_CONVTC_WT_WEIGHTS:
-      hnn::wt_weights_kernel<<<total_blocks, hnn::CT_THREADS, 0, s>>>(probs, nprob, cur, status);
+      hnn::launch_pdl(hnn::wt_weights_kernel, dim3(total_blocks), dim3(hnn::CT_THREADS), 0, s, probs, nprob, cur, status);
       break;
     case HNN_CONVTC_WGRAD_REDUCE:
-      hnn::wgrad_reduce_kernel<<<total_blocks, hnn::CT_THREADS, 0, s>>>(probs, nprob, cur, status);
+      hnn::launch_pdl(hnn::wgrad_reduce_kernel, dim3(total_blocks), dim3(hnn::CT_THREADS), 0, s, probs, nprob, cur, status);
       break;
     default:
       hnn::set_error("hnn_conv_tc_aux", "unknown op");

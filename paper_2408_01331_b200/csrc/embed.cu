@@ -19,6 +19,7 @@ __device__ __forceinline__ const hnn_embed_problem& em_problem(const hnn_embed_p
 __global__ void __launch_bounds__(32 * EM_WARPS) embed_fwd_kernel(const hnn_embed_problem* __restrict__ probs, int nprob,
                                                                  const hnn_step_row* __restrict__ cur,
                                                                  const hnn_model_status* __restrict__ status) {
+  hnn::pdl_wait();
   const hnn_embed_problem& p = em_problem(probs, nprob, blockIdx.x);
   if (!live(cur, status, p.model)) return;
   const int rows = cur[p.model].rows;
@@ -39,6 +40,7 @@ __global__ void __launch_bounds__(32 * EM_WARPS) embed_fwd_kernel(const hnn_embe
 __global__ void __launch_bounds__(32 * EM_WARPS) embed_bwd_kernel(const hnn_embed_problem* __restrict__ probs, int nprob,
                                                                  const hnn_step_row* __restrict__ cur,
                                                                  const hnn_model_status* __restrict__ status) {
+  hnn::pdl_wait();
   const hnn_embed_problem& p = em_problem(probs, nprob, blockIdx.x);
   if (!live(cur, status, p.model)) return;
   const int rows = cur[p.model].rows;
@@ -86,8 +88,8 @@ extern "C" int hnn_embedding(int op, const hnn_embed_problem* probs, int nprob, 
   HNN_REQUIRE(op == HNN_FWD || op == HNN_WGRAD, "hnn_embedding", "op must be HNN_FWD or HNN_WGRAD");
   cudaStream_t s = hnn::as_stream(stream);
   if (op == HNN_FWD)
-    hnn::embed_fwd_kernel<<<total_blocks, 32 * hnn::EM_WARPS, 0, s>>>(probs, nprob, cur, status);
+    hnn::launch_pdl(hnn::embed_fwd_kernel, dim3(total_blocks), dim3(32 * hnn::EM_WARPS), 0, s, probs, nprob, cur, status);
   else
-    hnn::embed_bwd_kernel<<<total_blocks, 32 * hnn::EM_WARPS, 0, s>>>(probs, nprob, cur, status);
+    hnn::launch_pdl(hnn::embed_bwd_kernel, dim3(total_blocks), dim3(32 * hnn::EM_WARPS), 0, s, probs, nprob, cur, status);
   return hnn::check_launch("hnn_embedding");
 }

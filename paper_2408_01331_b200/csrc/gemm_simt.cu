@@ -26,6 +26,7 @@ template <int OP, int BM, int BN>
 __global__ void __launch_bounds__(STHREADS) gemm_simt_kernel(const hnn_gemm_problem* __restrict__ probs, int nprob,
                                                              const hnn_step_row* __restrict__ cur,
                                                              const hnn_model_status* __restrict__ status) {
+  hnn::pdl_wait();
   using T = SimtTile<BM, BN>;
   constexpr int BK = T::BK, TM = T::TM, TN = T::TN;
   __shared__ __align__(16) float As[BK][BM + 4];
@@ -216,9 +217,9 @@ int skinny_tile_shape(int op, int32_t* tm, int32_t* tn);
 int grouped_gemm_simt(int op, int skinny, const hnn_gemm_problem* probs, int nprob, int total_tiles,
                       const hnn_step_row* cur, const hnn_model_status* status, cudaStream_t s) {
   if (skinny) return grouped_gemm_skinny(op, probs, nprob, total_tiles, cur, status, s);
-  if (op == HNN_FWD) gemm_simt_kernel<HNN_FWD, 64, 64><<<total_tiles, STHREADS, 0, s>>>(probs, nprob, cur, status);
-  else if (op == HNN_DGRAD) gemm_simt_kernel<HNN_DGRAD, 64, 64><<<total_tiles, STHREADS, 0, s>>>(probs, nprob, cur, status);
-  else gemm_simt_kernel<HNN_WGRAD, 64, 64><<<total_tiles, STHREADS, 0, s>>>(probs, nprob, cur, status);
+  if (op == HNN_FWD) hnn::launch_pdl(gemm_simt_kernel<HNN_FWD, 64, 64>, dim3(total_tiles), dim3(STHREADS), 0, s, probs, nprob, cur, status);
+  else if (op == HNN_DGRAD) hnn::launch_pdl(gemm_simt_kernel<HNN_DGRAD, 64, 64>, dim3(total_tiles), dim3(STHREADS), 0, s, probs, nprob, cur, status);
+  else hnn::launch_pdl(gemm_simt_kernel<HNN_WGRAD, 64, 64>, dim3(total_tiles), dim3(STHREADS), 0, s, probs, nprob, cur, status);
   return check_launch("hnn_grouped_gemm(simt)");
 }
 

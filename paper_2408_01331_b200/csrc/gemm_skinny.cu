@@ -98,6 +98,7 @@ __device__ __forceinline__ void rowdot_rows(const hnn_gemm_problem& p, int r0, i
 __global__ void __launch_bounds__(KTHREADS) skinny_fwd_kernel(const hnn_gemm_problem* __restrict__ probs, int nprob,
                                                               const hnn_step_row* __restrict__ cur,
                                                               const hnn_model_status* __restrict__ status) {
+  hnn::pdl_wait();
   const int pi = find_problem(probs, nprob, blockIdx.x, [](const hnn_gemm_problem& q) { return q.tile_base; });
   const hnn_gemm_problem& p = probs[pi];
   if (!live(cur, status, p.model)) return;
@@ -154,6 +155,7 @@ __device__ __forceinline__ void outer_rows(const hnn_gemm_problem& p, int r0, in
 __global__ void __launch_bounds__(KTHREADS) skinny_dgrad_kernel(const hnn_gemm_problem* __restrict__ probs, int nprob,
                                                                 const hnn_step_row* __restrict__ cur,
                                                                 const hnn_model_status* __restrict__ status) {
+  hnn::pdl_wait();
   __shared__ float dys[8 * DG_ROWS * 16];  // the CTA's 64 dy rows, 16 columns (zero padded)
   const int pi = find_problem(probs, nprob, blockIdx.x, [](const hnn_gemm_problem& q) { return q.tile_base; });
   const hnn_gemm_problem& p = probs[pi];
@@ -205,6 +207,7 @@ __device__ __forceinline__ void colacc(const hnn_gemm_problem& p, int col, int r
 __global__ void __launch_bounds__(KTHREADS) skinny_wgrad_kernel(const hnn_gemm_problem* __restrict__ probs, int nprob,
                                                                 const hnn_step_row* __restrict__ cur,
                                                                 const hnn_model_status* __restrict__ status) {
+  hnn::pdl_wait();
   extern __shared__ __align__(16) float wg_smem[];
   float* dys = wg_smem;                   // [WG_CHUNK][16] staged dy rows (zero padded)
   float* red = wg_smem + WG_CHUNK * 16;   // [3][WG_QUADS][16][4] partials of row quarters 1..3
@@ -304,9 +307,9 @@ int skinny_tile_shape(int op, int32_t* tm, int32_t* tn) {
 int grouped_gemm_skinny(int op, const hnn_gemm_problem* probs, int nprob, int total_tiles, const hnn_step_row* cur,
                         const hnn_model_status* status, cudaStream_t s) {
   if (op == HNN_FWD) {
-    skinny_fwd_kernel<<<total_tiles, KTHREADS, 0, s>>>(probs, nprob, cur, status);
+    hnn::launch_pdl(skinny_fwd_kernel, dim3(total_tiles), dim3(KTHREADS), 0, s, probs, nprob, cur, status);
   } else if (op == HNN_DGRAD) {
-    skinny_dgrad_kernel<<<total_tiles, KTHREADS, 0, s>>>(probs, nprob, cur, status);
+    hnn::launch_pdl(skinny_dgrad_kernel, dim3(total_tiles), dim3(KTHREADS), 0, s, probs, nprob, cur, status);
   } else {
     constexpr int smem = (WG_CHUNK * 16 + 3 * WG_QUADS * 64) * 4;  // 64 KB
     static bool configured = false;
@@ -314,7 +317,7 @@ int grouped_gemm_skinny(int op, const hnn_gemm_problem* probs, int nprob, int to
       cudaFuncSetAttribute(skinny_wgrad_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
       configured = true;
     }
-    skinny_wgrad_kernel<<<total_tiles, KTHREADS, smem, s>>>(probs, nprob, cur, status);
+    hnn::launch_pdl(skinny_wgrad_kernel, dim3(total_tiles), dim3(KTHREADS), smem, s, probs, nprob, cur, status);
   }
   return check_launch("hnn_grouped_gemm(skinny)");
 }

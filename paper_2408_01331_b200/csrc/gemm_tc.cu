@@ -56,6 +56,7 @@ template <int OP>
 __global__ void __launch_bounds__(TC_THREADS, 1)
     gemm_tc_kernel(const hnn_gemm_problem* __restrict__ probs, int nprob, int total_tiles,
                    const hnn_step_row* __restrict__ cur, const hnn_model_status* __restrict__ status) {
+  hnn::pdl_wait();
   constexpr int A_MN = (OP == HNN_WGRAD) ? 1 : 0;
   constexpr int B_MN = (OP == HNN_FWD) ? 0 : 1;
   constexpr int SR = TC_RAW_STAGES, SL = TC_LO_STAGES;
@@ -328,6 +329,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
 // column; with optimizer fusion the bias is updated here too.
 __global__ void colsum_kernel(const hnn_gemm_problem* __restrict__ probs, int nprob, const hnn_step_row* __restrict__ cur,
                               const hnn_model_status* __restrict__ status) {
+  hnn::pdl_wait();
   const hnn_gemm_problem& p = probs[blockIdx.y];
   if ((!p.dbias && !p.opt_b) || !live(cur, status, p.model)) return;
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
@@ -487,11 +489,11 @@ int grouped_gemm_tc(int op, const hnn_gemm_problem* probs, int nprob, int total_
   }
   const int grid = total_tiles < sms ? total_tiles : sms;
   if (op == HNN_FWD)
-    gemm_tc_kernel<HNN_FWD><<<grid, TC_THREADS, TC_SMEM_BYTES, s>>>(probs, nprob, total_tiles, cur, status);
+    hnn::launch_pdl(gemm_tc_kernel<HNN_FWD>, dim3(grid), dim3(TC_THREADS), TC_SMEM_BYTES, s, probs, nprob, total_tiles, cur, status);
   else if (op == HNN_DGRAD)
-    gemm_tc_kernel<HNN_DGRAD><<<grid, TC_THREADS, TC_SMEM_BYTES, s>>>(probs, nprob, total_tiles, cur, status);
+    hnn::launch_pdl(gemm_tc_kernel<HNN_DGRAD>, dim3(grid), dim3(TC_THREADS), TC_SMEM_BYTES, s, probs, nprob, total_tiles, cur, status);
   else {
-    gemm_tc_kernel<HNN_WGRAD><<<grid, TC_THREADS, TC_SMEM_BYTES, s>>>(probs, nprob, total_tiles, cur, status);
+    hnn::launch_pdl(gemm_tc_kernel<HNN_WGRAD>, dim3(grid), dim3(TC_THREADS), TC_SMEM_BYTES, s, probs, nprob, total_tiles, cur, status);
     int rc = check_launch("hnn_grouped_gemm(tc)");
     if (rc) return rc;
     return launch_colsum(probs, nprob, cur, status, s);
@@ -503,7 +505,7 @@ int grouped_gemm_tc(int op, const hnn_gemm_problem* probs, int nprob, int total_
 int launch_colsum(const hnn_gemm_problem* probs, int nprob, const hnn_step_row* cur, const hnn_model_status* status,
                   cudaStream_t s) {
   dim3 grid2(16, nprob);  // columns up to 16*256 = 4096 per problem (planner guarantees m <= 4096)
-  colsum_kernel<<<grid2, 256, 0, s>>>(probs, nprob, cur, status);
+  hnn::launch_pdl(colsum_kernel, dim3(grid2), dim3(256), 0, s, probs, nprob, cur, status);
   return check_launch("hnn_grouped_gemm(colsum)");
 }
 

@@ -159,6 +159,7 @@ template <int OP, int KIND = 0>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC2_THREADS, 1)
     gemm_tc2_kernel(const hnn_gemm_problem* __restrict__ probs, int nprob, int total_tiles,
                     const hnn_step_row* __restrict__ cur, const hnn_model_status* __restrict__ status) {
+  hnn::pdl_wait();
   constexpr bool BF16 = KIND == 1;
   constexpr int A_MN = (!BF16 && OP == HNN_WGRAD) ? 1 : 0;
   constexpr int B_MN = (!BF16 && OP != HNN_FWD) ? 1 : 0;
@@ -808,11 +809,11 @@ int launch_tc2(int op, const hnn_gemm_problem* probs, int nprob, int total_tiles
   const int pairs = total_tiles < sms / 2 ? total_tiles : sms / 2;
   const int grid = 2 * pairs;
   if (op == HNN_FWD)
-    gemm_tc2_kernel<HNN_FWD, KIND><<<grid, TC2_THREADS, TC2_SMEM_BYTES, s>>>(probs, nprob, total_tiles, cur, status);
+    hnn::launch_pdl(gemm_tc2_kernel<HNN_FWD, KIND>, dim3(grid), dim3(TC2_THREADS), TC2_SMEM_BYTES, s, probs, nprob, total_tiles, cur, status);
   else if (op == HNN_DGRAD)
-    gemm_tc2_kernel<HNN_DGRAD, KIND><<<grid, TC2_THREADS, TC2_SMEM_BYTES, s>>>(probs, nprob, total_tiles, cur, status);
+    hnn::launch_pdl(gemm_tc2_kernel<HNN_DGRAD, KIND>, dim3(grid), dim3(TC2_THREADS), TC2_SMEM_BYTES, s, probs, nprob, total_tiles, cur, status);
   else {
-    gemm_tc2_kernel<HNN_WGRAD, KIND><<<grid, TC2_THREADS, TC2_SMEM_BYTES, s>>>(probs, nprob, total_tiles, cur, status);
+    hnn::launch_pdl(gemm_tc2_kernel<HNN_WGRAD, KIND>, dim3(grid), dim3(TC2_THREADS), TC2_SMEM_BYTES, s, probs, nprob, total_tiles, cur, status);
     int rc = check_launch("hnn_grouped_gemm(tc2)");
     if (rc) return rc;
     return launch_colsum(probs, nprob, cur, status, s);

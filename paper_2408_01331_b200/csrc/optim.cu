@@ -46,6 +46,7 @@ constexpr int OPT_MIN_CTAS = HNN_OPT_MIN_CTAS, OPT_UNROLL = HNN_OPT_UNROLL;
 __global__ void __launch_bounds__(OPT_THREADS, OPT_MIN_CTAS)
     multi_tensor_kernel(const hnn_opt_segment* __restrict__ segs, int nseg, int total_chunks,
                         const hnn_step_row* __restrict__ cur, const hnn_model_status* __restrict__ status) {
+  hnn::pdl_wait();
   for (int chunk = blockIdx.x; chunk < total_chunks; chunk += gridDim.x) {
     const int si = find_problem(segs, nseg, chunk, [](const hnn_opt_segment& q) { return q.chunk_base; });
     const hnn_opt_segment& sg = segs[si];
@@ -99,7 +100,7 @@ int launch_multi_tensor(const char* who, const hnn_opt_segment* segs, int nseg, 
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   }
   const int grid = total_chunks < OPT_MIN_CTAS * sms ? total_chunks : OPT_MIN_CTAS * sms;  // one wave
-  multi_tensor_kernel<<<grid, OPT_THREADS, 0, as_stream(stream)>>>(segs, nseg, total_chunks, cur, status);
+  hnn::launch_pdl(multi_tensor_kernel, dim3(grid), dim3(OPT_THREADS), 0, as_stream(stream), segs, nseg, total_chunks, cur, status);
   return check_launch(who);
 }
 
@@ -120,6 +121,7 @@ extern "C" int hnn_multi_tensor_adam(const hnn_opt_segment* segs, int nseg, int 
 
 namespace hnn {
 __global__ void selftest_div_sqrt_kernel(const float* a, const float* b, float* q, float* r, int64_t n) {
+  hnn::pdl_wait();
   for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x) {
     q[i] = div_rn_exact(a[i], b[i]);
     r[i] = sqrt_rn_exact(a[i]);
@@ -130,6 +132,6 @@ __global__ void selftest_div_sqrt_kernel(const float* a, const float* b, float* 
 extern "C" int hnn_selftest_div_sqrt(const float* a, const float* b, float* q, float* r, int64_t n, void* stream) {
   HNN_REQUIRE(a && b && q && r && n >= 0, "hnn_selftest_div_sqrt", "bad arguments");
   if (n == 0) return HNN_OK;
-  hnn::selftest_div_sqrt_kernel<<<1184, 256, 0, hnn::as_stream(stream)>>>(a, b, q, r, n);
+  hnn::launch_pdl(hnn::selftest_div_sqrt_kernel, dim3(1184), dim3(256), 0, hnn::as_stream(stream), a, b, q, r, n);
   return hnn::check_launch("hnn_selftest_div_sqrt");
 }

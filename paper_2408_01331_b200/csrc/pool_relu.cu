@@ -13,6 +13,7 @@ constexpr int PTHREADS = 256;
 __global__ void __launch_bounds__(PTHREADS) maxpool_fwd_kernel(const hnn_pool_problem* __restrict__ probs, int nprob,
                                                                const hnn_step_row* __restrict__ cur,
                                                                const hnn_model_status* __restrict__ status) {
+  hnn::pdl_wait();
   const int pi = find_problem(probs, nprob, blockIdx.x, [](const hnn_pool_problem& q) { return q.block_base; });
   const hnn_pool_problem p = probs[pi];
   if (!live(cur, status, p.model)) return;
@@ -73,6 +74,7 @@ __global__ void __launch_bounds__(PTHREADS) maxpool_fwd_kernel(const hnn_pool_pr
 __global__ void __launch_bounds__(PTHREADS) maxpool_bwd_kernel(const hnn_pool_problem* __restrict__ probs, int nprob,
                                                                const hnn_step_row* __restrict__ cur,
                                                                const hnn_model_status* __restrict__ status) {
+  hnn::pdl_wait();
   const int pi = find_problem(probs, nprob, blockIdx.x, [](const hnn_pool_problem& q) { return q.block_base; });
   const hnn_pool_problem p = probs[pi];
   if (!live(cur, status, p.model)) return;
@@ -120,6 +122,7 @@ __global__ void __launch_bounds__(PTHREADS) maxpool_bwd_kernel(const hnn_pool_pr
 __global__ void __launch_bounds__(PTHREADS) relu_kernel(int op, const hnn_relu_problem* __restrict__ probs, int nprob,
                                                         const hnn_step_row* __restrict__ cur,
                                                         const hnn_model_status* __restrict__ status) {
+  hnn::pdl_wait();
   const int pi = find_problem(probs, nprob, blockIdx.x, [](const hnn_relu_problem& q) { return q.block_base; });
   const hnn_relu_problem p = probs[pi];
   if (!live(cur, status, p.model)) return;
@@ -136,8 +139,8 @@ extern "C" int hnn_grouped_maxpool(int op, const hnn_pool_problem* probs, int np
                                    const hnn_step_row* cur, const hnn_model_status* status, void* stream) {
   HNN_REQUIRE(probs && cur && nprob > 0 && total_blocks > 0, "hnn_grouped_maxpool", "bad arguments");
   cudaStream_t s = hnn::as_stream(stream);
-  if (op == HNN_FWD) hnn::maxpool_fwd_kernel<<<total_blocks, hnn::PTHREADS, 0, s>>>(probs, nprob, cur, status);
-  else if (op == HNN_DGRAD) hnn::maxpool_bwd_kernel<<<total_blocks, hnn::PTHREADS, 0, s>>>(probs, nprob, cur, status);
+  if (op == HNN_FWD) hnn::launch_pdl(hnn::maxpool_fwd_kernel, dim3(total_blocks), dim3(hnn::PTHREADS), 0, s, probs, nprob, cur, status);
+  else if (op == HNN_DGRAD) hnn::launch_pdl(hnn::maxpool_bwd_kernel, dim3(total_blocks), dim3(hnn::PTHREADS), 0, s, probs, nprob, cur, status);
   else {
     hnn::set_error("hnn_grouped_maxpool", "op must be HNN_FWD or HNN_DGRAD");
     return HNN_ERR_INVALID;
@@ -149,6 +152,6 @@ extern "C" int hnn_grouped_relu(int op, const hnn_relu_problem* probs, int nprob
                                 const hnn_step_row* cur, const hnn_model_status* status, void* stream) {
   HNN_REQUIRE(probs && cur && nprob > 0 && total_blocks > 0, "hnn_grouped_relu", "bad arguments");
   HNN_REQUIRE(op == HNN_FWD || op == HNN_DGRAD, "hnn_grouped_relu", "op must be HNN_FWD or HNN_DGRAD");
-  hnn::relu_kernel<<<total_blocks, hnn::PTHREADS, 0, hnn::as_stream(stream)>>>(op, probs, nprob, cur, status);
+  hnn::launch_pdl(hnn::relu_kernel, dim3(total_blocks), dim3(hnn::PTHREADS), 0, hnn::as_stream(stream), op, probs, nprob, cur, status);
   return hnn::check_launch("hnn_grouped_relu");
 }

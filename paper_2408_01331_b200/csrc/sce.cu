@@ -110,6 +110,7 @@ __global__ void __launch_bounds__(SCE_THREADS) sce_kernel(const hnn_sce_problem*
                                                           hnn_model_status* __restrict__ status, int train,
                                                           float* __restrict__ loss_out,
                                                           int32_t* __restrict__ correct_out, int max_classes) {
+  hnn::pdl_wait();
   extern __shared__ float smem[];
   const hnn_sce_problem p = probs[blockIdx.x];
   if (!cur[p.model].active) return;
@@ -233,7 +234,7 @@ extern "C" int hnn_sce_fused(const hnn_sce_problem* probs, int nprob, int max_ca
   HNN_REQUIRE(smem <= 200 * 1024, "hnn_sce_fused", "batch capacity / class count too large for one CTA");
   if (smem > 48 * 1024)
     cudaFuncSetAttribute(hnn::sce_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  hnn::sce_kernel<<<nprob, hnn::SCE_THREADS, smem, hnn::as_stream(stream)>>>(probs, cur, status, train, loss_out,
+  hnn::launch_pdl(hnn::sce_kernel, dim3(nprob), dim3(hnn::SCE_THREADS), smem, hnn::as_stream(stream), probs, cur, status, train, loss_out,
                                                                               correct_out, max_classes);
   return hnn::check_launch("hnn_sce_fused");
 }
