@@ -211,6 +211,15 @@ int hnn_grouped_gemm(int op, int prec, const hnn_gemm_problem* probs, int nprob,
  * Tiles are 128 x 128 (hnn_gemm_tile_shape); WGRAD problems need m <= 4096.
  */
 int hnn_gemm_tc_encode(int op, const hnn_gemm_problem* host_probs, int nprob, void* host_maps);
+/*
+ * Split-K forward (HNN_PREC_F32_3XTF32_PAIR FWD problems with ksplit > 1 write raw partial sums
+ * of K range [s*ksplit_len, ...) to rows s*mp + r of c, mp = m rounded up to 32; bias / relu 0):
+ * y[r, j] = relu?(sum_s partial + bias[j]) for r < the step's rows, 0 beyond (_dense_fwd,
+ * ops.py:46-48).  Table fields: a = partials (lda = partial row stride), c = y (ldc), bias, relu,
+ * m, n, ksplit, model; tile_base / tiles_n = the problem's first block and block count.
+ */
+int hnn_splitk_epilogue(const hnn_gemm_problem* probs, int nprob, int total_blocks, const hnn_step_row* cur,
+                        const hnn_model_status* status, void* stream);
 int hnn_gemm_bf16_encode(int op, const hnn_gemm_problem* host_probs, int nprob, void* host_maps);
 
 /*

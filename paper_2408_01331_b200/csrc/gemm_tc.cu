@@ -359,6 +359,42 @@ __global__ void colsum_kernel(const hnn_gemm_problem* __restrict__ probs, int np
   }
 }
 
+// Split-K forward epilogue (HNN_PREC_F32_3XTF32_PAIR problems with ksplit > 1 wrote raw partial
+// sums): y[r, j] = relu?(sum over splits in order of partial[s*mp + r, j] + bias[j]) for r < rows,
+// 0 beyond the batch.  Problem fields: a = partials (row stride lda, split stride mp = m rounded up
+// to 32 rows), c = y (row stride ldc), bias, relu, m, n, ksplit, model; tile_base / tiles_n = this
+// problem's first block and block count.
+__global__ void __launch_bounds__(256) splitk_epilogue_kernel(const hnn_gemm_problem* __restrict__ probs, int nprob,
+                                                             const hnn_step_row* __restrict__ cur,
+                                                             const hnn_model_status* __restrict__ status) {
+  hnn::pdl_wait();
+  const int pi = find_problem(probs, nprob, blockIdx.x, [](const hnn_gemm_problem& q) { return q.tile_base; });
+  const hnn_gemm_problem& p = probs[pi];
+  if (!live(cur, status, p.model)) return;
+  const int rows = cur[p.model].rows;
+  const int S = p.ksplit, total = p.m * p.n;
+  const size_t split_stride = size_t((p.m + 31) & ~31) * p.lda;
+  for (int e = (blockIdx.x - p.tile_base) * 256 + threadIdx.x; e < total; e += p.tiles_n * 256) {
+    const int r = e / p.n, j = e - r * p.n;
+    float v[8];
+#pragma unroll
+    for (int s = 0; s < 8; ++s) v[s] = s < S ? __ldg(p.a + s * split_stride + size_t(r) * p.lda + j) : 0.0f;
+    // in order, the first split taken as is: the unsplit kernel's promotion sequence when every
+    // split is one 128-term chunk (then the result is bit-identical to not splitting)
+    float acc = 0.0f;
+#pragma unroll
+    for (int s = 0; s < 8; ++s)
+      if (s < S) acc = s == 0 ? v[0] : __fadd_rn(acc, v[s]);
+    for (int s = 8; s < S; ++s) acc = __fadd_rn(acc, __ldg(p.a + s * split_stride + size_t(r) * p.lda + j));
+    float y = 0.0f;
+    if (r < rows) {
+      y = __fadd_rn(acc, p.bias ? __ldg(p.bias + j) : 0.0f);
+      if (p.relu & 1) y = np_relu(y);
+    }
+    p.c[size_t(r) * p.ldc + j] = y;
+  }
+}
+
 // ---------------------------------------------------------------- host side
 
 typedef CUresult (*EncodeTiled)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
@@ -531,7 +567,7 @@ extern "C" int hnn_gemm_tc_encode(int op, const hnn_gemm_problem* host_probs, in
     }
     // C (all ops): row-major [m, n] with row stride ldc; 32x32 boxes, 128-byte swizzle
     // (a K-split WGRAD writes ksplit stacked [m, n] partials)
-    const uint64_t crows = (op == HNN_WGRAD && p.ksplit > 1) ? uint64_t((p.m + 31) & ~31) * uint64_t(p.ksplit)
+    const uint64_t crows = ((op == HNN_WGRAD || op == HNN_FWD) && p.ksplit > 1) ? uint64_t((p.m + 31) & ~31) * uint64_t(p.ksplit)
                                                              : uint64_t(p.m);
     if (!rc && p.c && p.c_mode == 1 && p.row_mult % 32 == 0)  // NCHW via 3D TMA stores
       rc = hnn::encode_nchw_f32(&maps[4 * i + 2], p.c, uint64_t(p.row_mult), uint64_t(p.n),
@@ -547,6 +583,14 @@ extern "C" int hnn_gemm_tc_encode(int op, const hnn_gemm_problem* host_probs, in
 }
 
 // HNN_PREC_BF16_PAIR: A [m, k] and B [n, k] are K-major bf16 (lda / ldb in elements); C fp32 as above.
+extern "C" int hnn_splitk_epilogue(const hnn_gemm_problem* probs, int nprob, int total_blocks,
+                                   const hnn_step_row* cur, const hnn_model_status* status, void* stream) {
+  HNN_REQUIRE(probs && cur && nprob > 0 && total_blocks > 0, "hnn_splitk_epilogue", "bad arguments");
+  hnn::launch_pdl(hnn::splitk_epilogue_kernel, dim3(total_blocks), dim3(256), 0, hnn::as_stream(stream), probs, nprob,
+                  cur, status);
+  return hnn::check_launch("hnn_splitk_epilogue");
+}
+
 extern "C" int hnn_gemm_bf16_encode(int op, const hnn_gemm_problem* host_probs, int nprob, void* host_maps) {
   HNN_REQUIRE(host_probs && host_maps && nprob > 0, "hnn_gemm_bf16_encode", "bad arguments");
   CUtensorMap* maps = reinterpret_cast<CUtensorMap*>(host_maps);
@@ -573,7 +617,7 @@ extern "C" int hnn_gemm_bf16_encode(int op, const hnn_gemm_problem* host_probs, 
     } else {
       rc = hnn::encode_2d_bf16(&maps[4 * i + 1], p.b, p.k, p.n, p.ldb, brows);
     }
-    const uint64_t crows = (op == HNN_WGRAD && p.ksplit > 1) ? uint64_t((p.m + 31) & ~31) * uint64_t(p.ksplit)
+    const uint64_t crows = ((op == HNN_WGRAD || op == HNN_FWD) && p.ksplit > 1) ? uint64_t((p.m + 31) & ~31) * uint64_t(p.ksplit)
                                                              : uint64_t(p.m);
     if (!rc && p.c && p.c_mode == 1 && p.row_mult % 32 == 0)  // NCHW via 3D TMA stores
       rc = hnn::encode_nchw_f32(&maps[4 * i + 2], p.c, uint64_t(p.row_mult), uint64_t(p.n),

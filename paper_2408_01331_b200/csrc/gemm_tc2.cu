@@ -241,6 +241,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC2_THREADS, 1)
         kofs = sp * p->ksplit_len;
         ktot = min(rows, kofs + p->ksplit_len) - kofs;
       }
+    } else if (OP == HNN_FWD && p->ksplit > 1) {  // split-K forward: raw partial sums per K range
+      const int S = p->ksplit;
+      sp = t % S;
+      t /= S;
+      kofs = sp * p->ksplit_len;
+      ktot = min(p->k, kofs + p->ksplit_len) - kofs;
     }
     tn = p->tile_n > 0 ? p->tile_n : TC2_BN;  // pair tile columns: 64, 128 or 256
     m0 = (t / p->tiles_n) * (2 * TC2_BM);

@@ -733,6 +733,9 @@ class DeviceHybrid:
             rows = sorted(rows, key=lambda r: -(r[1]["m"] * r[1]["n"] * r[1]["k"]))
             probs, base = [], 0
             cap = self._pair_tile_cap(op, rows, tm) if prec in (N.PREC_3XTF32_PAIR, N.PREC_BF16_PAIR) else tn
+            finals = []
+            if prec == N.PREC_3XTF32_PAIR and op == N.HNN_FWD:
+                rows, finals = self._split_k_forward(rows, tm, cap)
             for s, d in rows:
                 tn_p = tn
                 if prec in (N.PREC_3XTF32_PAIR, N.PREC_BF16_PAIR):  # narrowest pair tile covering n
@@ -742,7 +745,7 @@ class DeviceHybrid:
                     d = dict(d, tile_n=tn_p)
                 tiles_m, tiles_n = -(-d["m"] // tm), -(-d["n"] // tn_p)
                 probs.append(N.GemmProblem(tile_base=base, tiles_n=tiles_n, model=s.index, **d))
-                base += tiles_m * tiles_n * (d.get("ksplit", 1) if op == N.HNN_WGRAD else 1)
+                base += tiles_m * tiles_n * (d.get("ksplit", 1) if op in (N.HNN_WGRAD, N.HNN_FWD) else 1)
             keep = None
             if prec in (N.PREC_3XTF32, N.PREC_3XTF32_PAIR, N.PREC_BF16_PAIR):
                 torch = _torch()
@@ -772,7 +775,52 @@ class DeviceHybrid:
                             flops=flops, nbytes=nbytes)
             launch.maps = keep
             out.append(launch)
+            if finals:  # the split-K forward's partial sums -> bias / relu output
+                eprobs, ebase = [], 0
+                for d in finals:
+                    nb = max(1, min(-(-(d["m"] * d["n"]) // 256), 2 * self._sm_count()))
+                    eprobs.append(N.GemmProblem(a=d["partial"], c=d["c"], bias=d["bias"], relu=d["relu"], m=d["m"],
+                                                n=d["n"], k=d["k"], lda=d["n"], ldc=d["ldc"], ksplit=d["ksplit"],
+                                                model=d["model"], tile_base=ebase, tiles_n=nb))
+                    ebase += nb
+                et = _dev_table(N.GemmProblem, eprobs, self.device)
+                el = Launch("hnn_splitk_epilogue", (_ptr(et), len(eprobs), ebase, _ptr(self.cur), _ptr(self.status)),
+                            et, f"{label}/splitk")
+                el.keep = [d["keep"] for d in finals]
+                out.append(el)
         return out
+
+    def _split_k_forward(self, rows, tm, cap):
+        """A CTA-pair forward launch with fewer tiles than a third of the pairs and long-K dense
+        problems (C1's two 64 x 784 x 256 first layers: 2 tiles for 74 pairs) splits every such
+        problem's K into 128-term ranges — exactly the tensor-core accumulation chunks of the
+        unsplit kernel — whose raw sums a second launch adds in order before the bias / relu
+        (hnn_splitk_epilogue).  That is the unsplit kernel's own promotion order, so the result is
+        bit-identical to not splitting (model isolation does not depend on the launch's
+        composition); the launch just spreads over K/128 times more CTA pairs.
+        Returns the rewritten rows and the epilogue descriptions."""
+        torch = _torch()
+        pairs = self._sm_count() // 2
+        tiles = 0
+        for _, d in rows:
+            w = min(cap, 64 if d["n"] <= 64 else (128 if d["n"] <= 128 else 256))
+            tiles += -(-d["m"] // tm) * -(-d["n"] // w)
+        if os.environ.get("HNN_SPLITK_FWD", "1") == "0" or tiles * 3 > pairs:
+            return rows, []
+        out, finals = [], []
+        for s, d in rows:
+            dense = d.get("c_mode", 0) == 0 and d.get("row_mult", 1) == 1 and not d.get("im_c")
+            if not (dense and d["k"] >= 512):
+                out.append((s, d))
+                continue
+            length = 128  # one promotion chunk (gemm_tc2.cu TC2_CHUNK_KB x 32)
+            split = -(-d["k"] // length)
+            mp = -(-d["m"] // 32) * 32
+            part = torch.empty(split * mp * d["n"], dtype=torch.float32, device=self.device)
+            finals.append(dict(partial=_ptr(part), c=d["c"], bias=d["bias"], relu=d["relu"], m=d["m"], n=d["n"],
+                               k=d["k"], ldc=d["ldc"], ksplit=split, model=s.index, keep=part))
+            out.append((s, dict(d, c=_ptr(part), ldc=d["n"], bias=0, relu=0, ksplit=split, ksplit_len=length)))
+        return out, finals
 
     def _conv_launch(self, op, items, label):
         out = []

@@ -883,3 +883,30 @@ def test_full_size_c4_steps_are_finite(pkg):
             assert np.all(np.isfinite(v)), (m, k)
             if k.endswith(".weight"):
                 assert not np.array_equal(v, before[m][k]), (m, k)
+
+
+@pytest.mark.gpu
+def test_split_k_forward_is_bit_identical(pkg, monkeypatch):
+    """C1's first layers (two 64 x 784 x 256 GEMMs: 2 tiles for 74 CTA pairs) run split-K in
+    128-term ranges — the unsplit kernel's own accumulation chunks, added in the same order by
+    hnn_splitk_epilogue — so 4 training steps end bit-identical to the unsplit launch."""
+    import torch
+
+    import bench
+
+    device = torch.device("cuda", 0)
+    outs = []
+    for split in ("1", "0"):
+        monkeypatch.setenv("HNN_SPLITK_FWD", split)
+        jobs, hy, dev, ddev, meta, ds, comm = bench.build_rank("c1", 0, 1, device)
+        labels = [l.label for l in dev.train_plan]
+        assert any(l.endswith("/splitk") for l in labels) == (split == "1"), labels
+        rows = bench.schedule(jobs, meta, 4)
+        bench.upload_perms(dev, jobs, meta)
+        dev.load_schedule(rows)
+        dev.train_steps(4, use_graph=True)
+        torch.cuda.synchronize()
+        outs.append([dev.download_params(m) for m in range(len(jobs))])
+    for a, b in zip(*outs):
+        for k in a:
+            assert np.array_equal(a[k], b[k]), k
