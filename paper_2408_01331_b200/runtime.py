@@ -810,7 +810,7 @@ class DeviceHybrid:
         out, finals = [], []
         for s, d in rows:
             dense = d.get("c_mode", 0) == 0 and d.get("row_mult", 1) == 1 and not d.get("im_c")
-            if not (dense and d["k"] >= 512):
+            if not (dense and d["k"] >= 256):  # (at least two chunks)
                 out.append((s, d))
                 continue
             length = 128  # one promotion chunk (gemm_tc2.cu TC2_CHUNK_KB x 32)
