@@ -26,12 +26,13 @@ __device__ __forceinline__ void st_cs4(float4* p, float4 v) {
 }
 
 constexpr int OPT_THREADS = 256, OPT_CHUNK = 4096;  // 4 float4 per thread per chunk
-// Measured on C3 (76.7M Adam params, tools/opt_variants.py): 5 CTAs/SM x 1 float4 per arena per
-// thread 0.399 ms (5.39 TB/s, 82% of the copy peak; a pure-traffic kernel with the same access
-// pattern 0.375 ms); 4 CTAs 0.404; 6 / 8 CTAs (register-capped, spilling) 0.44 / 0.51;
-// 2 float4 per thread 0.49; 4 float4 at 2 CTAs 0.61.
+// Measured on C3 (76.7M Adam params, tools/opt_variants.py), launched alone: 5 CTAs/SM x 1 float4
+// per arena per thread 0.399 ms (5.39 TB/s, 82% of the copy peak; a pure-traffic kernel with the
+// same access pattern 0.375 ms); 4 CTAs 0.404; 6 / 8 CTAs (register-capped, spilling) 0.44 /
+// 0.51; 2 float4 per thread 0.49; 4 float4 at 2 CTAs 0.61.  Inside the step (after the weight-
+// gradient GEMMs, profiles/r01) 4 CTAs win: 0.419 ms against 0.443 (5) and 0.461 (3).
 #ifndef HNN_OPT_MIN_CTAS
-#define HNN_OPT_MIN_CTAS 5
+#define HNN_OPT_MIN_CTAS 4
 #endif
 #ifndef HNN_OPT_UNROLL
 #define HNN_OPT_UNROLL 1
