@@ -15,8 +15,14 @@
 namespace hnn {
 
 constexpr int KTHREADS = 256;
-constexpr int FWD_ROWS = 2;  // rows per warp; tile = 8 warps x 2 rows = 16 rows (2 waves of CTAs on C3)
-constexpr int DG_ROWS = 8;   // DGRAD rows per thread; tile = 8 row groups x 8 rows x 128 columns
+#ifndef HNN_SKINNY_FWD_ROWS
+#define HNN_SKINNY_FWD_ROWS 2
+#endif
+constexpr int FWD_ROWS = HNN_SKINNY_FWD_ROWS;  // rows per warp; tile = 8 warps x 2 rows = 16 rows
+#ifndef HNN_SKINNY_DG_ROWS
+#define HNN_SKINNY_DG_ROWS 8
+#endif
+constexpr int DG_ROWS = HNN_SKINNY_DG_ROWS;  // DGRAD rows per thread; tile = 8 row groups x 8 rows x 128 columns
 constexpr int WG_QUADS = 64; // WGRAD column quads per CTA; tile = 256 columns, 4 row quarters
 
 __device__ __forceinline__ float4 ldg4(const float* p) { return __ldg(reinterpret_cast<const float4*>(p)); }
