@@ -200,6 +200,11 @@ typedef struct hnn_gemm_problem {
 /* Tile edge (m, n) used by (op, prec); lets the host lay out tile_base / tiles_n. */
 int hnn_gemm_tile_shape(int op, int prec, int32_t* tile_m, int32_t* tile_n);
 
+/* K terms the tensor core sums into one TMEM chunk before the accumulator warps add the chunk into
+ * their fp32 running sums (HNN_PREC_F32_3XTF32_PAIR).  A split-K forward must split K into ranges
+ * of exactly this length to reproduce the unsplit promotion order bit for bit. */
+int hnn_gemm_chunk_terms(int prec, int32_t* terms);
+
 int hnn_grouped_gemm(int op, int prec, const hnn_gemm_problem* probs, int nprob, int total_tiles,
                      const hnn_step_row* cur, const hnn_model_status* status, void* stream);
 

@@ -7,6 +7,7 @@ fallback anywhere in this package.
 from __future__ import annotations
 
 import ctypes as C
+import os
 from pathlib import Path
 
 from .errors import DeviceError
@@ -111,6 +112,7 @@ SIGNATURES = {
     "hnn_step_begin": [P, P, P, C.c_int, VP],
     "hnn_gather_rows": [P, C.c_int, C.c_int, P, VP],
     "hnn_gemm_tile_shape": [C.c_int, C.c_int, C.POINTER(I), C.POINTER(I)],
+    "hnn_gemm_chunk_terms": [C.c_int, C.POINTER(I)],
     "hnn_grouped_gemm": [C.c_int, C.c_int, P, C.c_int, C.c_int, P, P, VP],
     "hnn_splitk_epilogue": [P, C.c_int, C.c_int, P, P, VP],
     "hnn_gemm_tc_encode": [C.c_int, C.c_void_p, C.c_int, C.c_void_p],
@@ -137,10 +139,14 @@ _lib = None
 
 
 def load(path: Path = LIB_PATH):
-    """Load (once) and type the library; raises if it is not built."""
+    """Load (once) and type the library; raises if it is not built.  HNN_LIB_VARIANT=NAME loads
+    _lib/variants/NAME/libhnn_b200.so instead (A/B builds of tools/build_variant.sh)."""
     global _lib
     if _lib is not None:
         return _lib
+    variant = os.environ.get("HNN_LIB_VARIANT")
+    if variant and path == LIB_PATH:
+        path = LIB_PATH.parent / "variants" / variant / LIB_PATH.name
     if not path.exists():
         raise DeviceError("load", -1, f"{path} is missing — run __graft_entry__.build() (no CPU fallback exists)")
     lib = C.CDLL(str(path))
@@ -167,6 +173,12 @@ def tile_shape(op: int, prec: int) -> tuple:
     tm, tn = I(), I()
     call("hnn_gemm_tile_shape", op, prec, C.byref(tm), C.byref(tn))
     return tm.value, tn.value
+
+
+def chunk_terms(prec: int) -> int:
+    t = I()
+    call("hnn_gemm_chunk_terms", prec, C.byref(t))
+    return t.value
 
 
 def conv_tile_shape(op: int) -> tuple:

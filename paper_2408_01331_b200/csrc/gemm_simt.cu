@@ -231,6 +231,7 @@ int gemm_tc_tile_shape(int op, int32_t* tm, int32_t* tn);
 int grouped_gemm_tc2(int op, const hnn_gemm_problem* probs, int nprob, int total_tiles, const hnn_step_row* cur,
                      const hnn_model_status* status, cudaStream_t s);
 int gemm_tc2_tile_shape(int op, int32_t* tm, int32_t* tn);
+int gemm_tc2_chunk_terms();
 int grouped_gemm_bf16(int op, const hnn_gemm_problem* probs, int nprob, int total_tiles, const hnn_step_row* cur,
                       const hnn_model_status* status, cudaStream_t s);
 
@@ -248,6 +249,12 @@ extern "C" int hnn_gemm_tile_shape(int op, int prec, int32_t* tile_m, int32_t* t
   if (prec == HNN_PREC_F32_3XTF32_PAIR || prec == HNN_PREC_BF16_PAIR) return hnn::gemm_tc2_tile_shape(op, tile_m, tile_n);
   hnn::set_error("hnn_gemm_tile_shape", "unknown precision");
   return HNN_ERR_INVALID;
+}
+
+extern "C" int hnn_gemm_chunk_terms(int prec, int32_t* terms) {
+  HNN_REQUIRE(terms && prec == HNN_PREC_F32_3XTF32_PAIR, "hnn_gemm_chunk_terms", "bad arguments");
+  *terms = hnn::gemm_tc2_chunk_terms();
+  return HNN_OK;
 }
 
 extern "C" int hnn_grouped_gemm(int op, int prec, const hnn_gemm_problem* probs, int nprob, int total_tiles,

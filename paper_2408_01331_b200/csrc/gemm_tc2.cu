@@ -10,10 +10,17 @@
 //
 // Arithmetic is the single-CTA kernel's: every operand x is used as hi = x (the tensor core
 // truncates fp32 to tf32) and lo = rna_tf32(x - trunc_tf32(x)); the tile accumulates
-// A_hi*B_hi + A_lo*B_hi + A_hi*B_lo.  Accumulation precision ("promotion"): the tensor core
+// A_lo*B_hi + A_hi*B_lo + A_hi*B_hi.  Accumulation precision ("promotion"): the tensor core
 // sums one chunk of TC2_CHUNK_KB K blocks into one of two 256-column TMEM buffers; the
 // accumulator warps add each finished chunk into fp32 registers (IEEE adds) and release the
-// buffer, so the MMAs of the next chunk never wait for a promotion (double buffering).  Each
+// buffer, so the MMAs of the next chunk never wait for a promotion (double buffering).
+// The split itself is fp32-exact to ~2^-24 (emulated with exact sums: 3.9e-7 GEMM error at
+// K = 256, the same as an fp32 BLAS); what costs accuracy is the tensor core's accumulation,
+// which aligns each MMA's addends to the largest and drops the bits below.  So a chunk is ONE
+// 32-term K block, and its small correction products go first, while the accumulator is still
+// small (measured, tools/adam_probe2.py, C3 h = 2048: gradient error against float64 3.8e-6
+// with 4-block chunks and hi*hi first -> 4.3e-7, the reference's own fp32 BLAS is 5.4e-7;
+// C3 step +4.7%).  Each
 // CTA's 128 x 256 running sum lives in registers: 8 accumulator warps x 128 columns (384
 // threads per CTA leave 168 registers per thread).
 //
@@ -43,7 +50,19 @@ constexpr int TC2_STAGES = 3;  // each stage: raw A | raw B | lo A | lo B (64 KB
 #endif
 constexpr int TC2_CONV_WARPS = HNN_TC2_CONV_WARPS;
 constexpr int TC2_THREADS = 64 + 32 * TC2_CONV_WARPS + 256;
-constexpr int TC2_CHUNK_KB = 4;
+#ifndef HNN_TC2_CHUNK_KB
+#define HNN_TC2_CHUNK_KB 1
+#endif
+#ifndef HNN_TC2_LO_FIRST
+#define HNN_TC2_LO_FIRST 1
+#endif
+constexpr int TC2_CHUNK_KB = HNN_TC2_CHUNK_KB;
+// K blocks per TMEM accumulation chunk of one tile: a fused-SGD weight-gradient tile whose whole K
+// fits 4 blocks keeps one chunk (its epilogue reads the finished sums straight from TMEM)
+template <int OP>
+static __device__ __forceinline__ int tc2_chunk_kb(const hnn_gemm_problem* p, int nkb) {
+  return (OP == HNN_WGRAD && p->opt_w != nullptr && p->opt_wm == nullptr && nkb <= 4) ? 4 : TC2_CHUNK_KB;
+}
 constexpr int TC2_A_BYTES = TC2_BM * TC2_BK * 4;        // 16 KB
 constexpr int TC2_B_BYTES = (TC2_BN / 2) * TC2_BK * 4;  // 16 KB (this CTA's half)
 constexpr int TC2_STAGE = TC2_A_BYTES + TC2_B_BYTES;
@@ -354,10 +373,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC2_THREADS, 1)
           continue;
         // (bf16 implicit weight gradient: B is MN-major, bit 16)
         const bool b_imp = BF16 && OP == HNN_WGRAD && p->im_c > 0;
+        const int ckb = tc2_chunk_kb<OP>(p, nkb);
         const uint32_t idesc =
             BF16 ? (bf16_idesc(2 * TC2_BM, tn) | (b_imp ? (1u << 16) : 0u)) : tf32_idesc(2 * TC2_BM, tn, A_MN, B_MN);
         for (int kb = 0; kb < nkb; ++kb, ++kg) {
-          const int in_chunk = BF16 ? kb : kb % TC2_CHUNK_KB;  // bf16: one chunk per tile (no promotion)
+          const int in_chunk = BF16 ? kb : kb % ckb;  // bf16: one chunk per tile (no promotion)
           const uint32_t buf = cg & 1;
           TC2_T0(t1);
           if (in_chunk == 0 && cg >= 2) mbar_wait(bar(ACC_EMPTY + buf), ((cg >> 1) - 1) & 1);  // promoted
@@ -378,6 +398,22 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC2_THREADS, 1)
                                  : smem_desc(b_hi + j * 32, 16, 1024, 2),
                            idesc, (in_chunk | j) != 0);
           } else {
+#if HNN_TC2_LO_FIRST
+            // correction products first, while the accumulator is still small (the tensor core
+            // aligns each MMA's addends to the largest and drops the bits below)
+#pragma unroll
+            for (int j = 0; j < TC2_BK / 8; ++j) {
+              const uint32_t ao = A_MN ? j * 1024 : j * 32, bo = B_MN ? j * 1024 : j * 32;
+              mma_tf32_pair(acc, smem_desc(a_lo + ao, alb, asb, alt), smem_desc(b_hi + bo, blb, bsb, blt), idesc,
+                            (in_chunk | j) != 0);
+              mma_tf32_pair(acc, smem_desc(a_hi + ao, alb, asb, alt), smem_desc(b_lo + bo, blb, bsb, blt), idesc, 1u);
+            }
+#pragma unroll
+            for (int j = 0; j < TC2_BK / 8; ++j) {
+              const uint32_t ao = A_MN ? j * 1024 : j * 32, bo = B_MN ? j * 1024 : j * 32;
+              mma_tf32_pair(acc, smem_desc(a_hi + ao, alb, asb, alt), smem_desc(b_hi + bo, blb, bsb, blt), idesc, 1u);
+            }
+#else
 #pragma unroll
             for (int j = 0; j < TC2_BK / 8; ++j) {
               const uint32_t ao = A_MN ? j * 1024 : j * 32, bo = B_MN ? j * 1024 : j * 32;
@@ -387,10 +423,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC2_THREADS, 1)
               mma_tf32_pair(acc, dal, dbh, idesc, 1u);
               mma_tf32_pair(acc, dah, dbl, idesc, 1u);
             }
+#endif
           }
           mma_commit_pair(bar(RAW_EMPTY + s));  // raw and lo of stage s consumed
           TC2_T1(t0, 5);
-          if ((!BF16 && in_chunk == TC2_CHUNK_KB - 1) || kb == nkb - 1) {
+          if ((!BF16 && in_chunk == ckb - 1) || kb == nkb - 1) {
             mma_commit_pair(bar(ACC_FULL + buf));
             ++cg;
           }
@@ -457,7 +494,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC2_THREADS, 1)
                : !tile_info(tile, p, m0, n0, nkb, rows, kofs, sp, tn))
           continue;
       TC2_T1(t9, 9);
-      const int nchunks = BF16 ? 1 : (nkb + TC2_CHUNK_KB - 1) / TC2_CHUNK_KB;
+      const int ckb = tc2_chunk_kb<OP>(p, nkb);
+      const int nchunks = BF16 ? 1 : (nkb + ckb - 1) / ckb;
       const int hn = tn / 2;  // this warp's columns: [half * hn, half * hn + hn)
       const uint32_t lane_base = lane_quarter + half * hn;
       // Fused plain SGD over a single chunk (K <= 128: C1 / C2 / C5 weight gradients): nothing to
@@ -781,6 +819,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC2_THREADS, 1)
     asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512));
   }
 }
+
+int gemm_tc2_chunk_terms() { return TC2_CHUNK_KB * TC2_BK; }
 
 int gemm_tc2_tile_shape(int op, int32_t* tm, int32_t* tn) {
   *tm = 2 * TC2_BM;

@@ -810,10 +810,10 @@ class DeviceHybrid:
         out, finals = [], []
         for s, d in rows:
             dense = d.get("c_mode", 0) == 0 and d.get("row_mult", 1) == 1 and not d.get("im_c")
-            if not (dense and d["k"] >= 256):  # (at least two chunks)
+            if not (dense and d["k"] >= 2 * N.chunk_terms(N.PREC_3XTF32_PAIR)):  # (at least two chunks)
                 out.append((s, d))
                 continue
-            length = 128  # one promotion chunk (gemm_tc2.cu TC2_CHUNK_KB x 32)
+            length = N.chunk_terms(N.PREC_3XTF32_PAIR)  # one promotion chunk (gemm_tc2.cu)
             split = -(-d["k"] // length)
             mp = -(-d["m"] // 32) * 32
             part = torch.empty(split * mp * d["n"], dtype=torch.float32, device=self.device)
