@@ -9,6 +9,7 @@
  *   hnn_step_begin              per-batch schedule: store.batches / lr_at_epoch / opt step
  *                               (store.py:68-81, optim.py:22-30, optim.py:57,73-76)
  *   hnn_gather_rows             Batch(x=train_x[idx], y=train_y[idx])   (store.py:77-80)
+ *   hnn_host_gather_rows        the same gather on the host (data loader of the host-fed step)
  *   hnn_grouped_gemm            dense fwd / bwd  _dense_fwd, _dense_bwd (ops.py:46-55) with
  *                               relu fwd/bwd fused (ops.py:62-67); fp32 SIMT or tcgen05 3xTF32
  *   hnn_gemm_tc_encode          host-side TMA descriptors for the tcgen05 path
@@ -118,6 +119,13 @@ typedef struct hnn_gather_problem {
 
 int hnn_gather_rows(const hnn_gather_problem* probs, int nprob, int max_cap, const hnn_step_row* cur,
                     void* stream);
+
+/* Host-side batch gather for the host-fed step (the same Batch(x=train_x[idx], y=train_y[idx]) as
+ * store.py:77-80, done by the host data loader into pinned memory): for r < n,
+ * dst_x[r*ld_dst .. + cols) = src_x[idx[r]*ld_src .. + cols) and dst_y[r] = (int32) src_y[idx[r]].
+ * Plain host code (no CUDA calls); reentrant, so loader threads run it in parallel. */
+int hnn_host_gather_rows(float* dst_x, int64_t ld_dst, int32_t* dst_y, const float* src_x, int64_t ld_src,
+                         const float* src_y, const int64_t* idx, int64_t n, int64_t cols);
 
 /*
  * Row-major grouped GEMM problem.  Let R = cur[model].rows.

@@ -111,6 +111,7 @@ VP = C.c_void_p
 SIGNATURES = {
     "hnn_step_begin": [P, P, P, C.c_int, VP],
     "hnn_gather_rows": [P, C.c_int, C.c_int, P, VP],
+    "hnn_host_gather_rows": [VP, C.c_int64, VP, VP, C.c_int64, VP, VP, C.c_int64, C.c_int64],
     "hnn_gemm_tile_shape": [C.c_int, C.c_int, C.POINTER(I), C.POINTER(I)],
     "hnn_gemm_chunk_terms": [C.c_int, C.POINTER(I)],
     "hnn_grouped_gemm": [C.c_int, C.c_int, P, C.c_int, C.c_int, P, P, VP],

@@ -122,4 +122,18 @@ int hnn_gather_rows(const hnn_gather_problem* probs, int nprob, int max_cap, con
   return hnn::check_launch("hnn_gather_rows");
 }
 
+int hnn_host_gather_rows(float* dst_x, int64_t ld_dst, int32_t* dst_y, const float* src_x, int64_t ld_src,
+                         const float* src_y, const int64_t* idx, int64_t n, int64_t cols) {
+  HNN_REQUIRE(dst_x && dst_y && src_x && src_y && (idx || n == 0) && n >= 0 && cols >= 0 && ld_dst >= cols &&
+                  ld_src >= cols,
+              "hnn_host_gather_rows", "bad arguments");
+  const size_t bytes = size_t(cols) * sizeof(float);
+  for (int64_t r = 0; r < n; ++r) {
+    const int64_t i = idx[r];
+    std::memcpy(dst_x + r * ld_dst, src_x + i * ld_src, bytes);
+    dst_y[r] = static_cast<int32_t>(src_y[i]);
+  }
+  return HNN_OK;
+}
+
 }  // extern "C"

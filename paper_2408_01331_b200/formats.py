@@ -1,9 +1,11 @@
-"""UNND containers (src/formats.py): v1 datasets and v2 packaged models.
+"""UNND containers (src/formats.py): v1 datasets, v2 packaged models, v3 checkpoints.
 
 The dataset flavour is on the hot path: its sha256 is the content hash that
 keys every epoch's shuffle (src/store.py:74-76).  The model flavour is what
 ``package`` writes from separated parameters (src/separate.py:39-72,
-src/formats.py:157-181).  Both must be byte-identical to the reference's:
+src/formats.py:157-181); the checkpoint flavour is what a paused job's
+``Checkpoint.encode`` writes (src/train.py:57-99, src/formats.py:188-207).
+All must be byte-identical to the reference's:
 little-endian, a canonical JSON header (sorted keys, no whitespace) for
 models, then float32 sections ``name(u8 len) rank(u8) dims(u32...) data``.
 """
@@ -20,6 +22,7 @@ import json
 MAGIC = b"UNND"
 VERSION_DATASET = 1
 VERSION_MODEL = 2
+VERSION_CHECKPOINT = 3
 DATASET_SECTIONS = ("train_x", "train_y", "test_x", "test_y")
 
 
@@ -111,6 +114,7 @@ def encode_model(header: dict, params: dict, order: list) -> bytes:
 
 
 def _reader(blob: bytes, version: int):
+    """(take, done) over a container body after its magic and version."""
     view = memoryview(blob)
     pos = [0]
 
@@ -126,12 +130,13 @@ def _reader(blob: bytes, version: int):
     (got,) = struct.unpack("<H", take(2))
     if got != version:
         raise FormatError(f"expected format version {version}, got {got}")
-    return take
+    return take, lambda: pos[0] == len(view)
 
 
-def decode_model(blob: bytes) -> tuple:
-    """Inverse of encode_model; checks the header's declared parameter count (src/formats.py:173-181)."""
-    take = _reader(blob, VERSION_MODEL)
+def _header_and_sections(blob: bytes, version: int) -> tuple:
+    """u32-prefixed JSON header, u16 section count, the sections; no duplicates, no trailing
+    bytes (src/formats.py:98-107)."""
+    take, done = _reader(blob, version)
     (hlen,) = struct.unpack("<I", take(4))
     header = json.loads(take(hlen).decode("utf-8"))
     (count,) = struct.unpack("<H", take(2))
@@ -141,9 +146,38 @@ def decode_model(blob: bytes) -> tuple:
         rank = take(1)[0]
         shape = tuple(struct.unpack("<I", take(4))[0] for _ in range(rank))
         n = int(np.prod(shape)) if shape else 1
+        if name in sections:
+            raise FormatError(f"duplicate section {name!r}")
         sections[name] = np.frombuffer(take(4 * n), dtype="<f4").reshape(shape).astype(np.float32)
+    if not done():
+        raise FormatError("trailing bytes after final section")
+    return header, sections
+
+
+def decode_model(blob: bytes) -> tuple:
+    """Inverse of encode_model; checks the header's declared parameter count (src/formats.py:173-181)."""
+    header, sections = _header_and_sections(blob, VERSION_MODEL)
     declared = header.get("param_count")
     actual = sum(int(a.size) for a in sections.values())
     if declared is not None and declared != actual:
         raise FormatError(f"header says {declared} parameters, file holds {actual}")
     return header, sections
+
+
+# --------------------------------------------------------------------------- checkpoints (v3)
+
+
+def encode_checkpoint(header: dict, sections: dict, order: list) -> bytes:
+    """The v2 layout under version 3: header, then the named sections in ``order``
+    (src/formats.py:188-201)."""
+    if sorted(order) != sorted(sections):
+        raise FormatError("section order does not cover the section set")
+    head = canonical_json(header)
+    parts = [MAGIC, struct.pack("<H", VERSION_CHECKPOINT), struct.pack("<I", len(head)), head,
+             struct.pack("<H", len(order))]
+    parts += [_section(name, sections[name]) for name in order]
+    return b"".join(parts)
+
+
+def decode_checkpoint(blob: bytes) -> tuple:
+    return _header_and_sections(blob, VERSION_CHECKPOINT)

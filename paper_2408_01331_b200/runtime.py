@@ -255,6 +255,16 @@ class DeviceDataset:
 # --------------------------------------------------------------------------- launches
 
 
+# kernel families for the roofline (bench.py) and the ncu traffic map (tools/ncu_traffic.py)
+GEMM_FAMILY = {N.PREC_SIMT: "gemm/simt", N.PREC_SIMT_SKINNY: "gemm/skinny", N.PREC_3XTF32: "gemm/tc-3xtf32",
+               N.PREC_3XTF32_PAIR: "gemm/tc2-3xtf32", N.PREC_BF16_PAIR: "gemm/tc2-bf16"}
+ENTRY_FAMILY = {"hnn_multi_tensor_adam": "optimizer", "hnn_multi_tensor_sgd": "optimizer", "hnn_sce_fused": "sce",
+                "hnn_gather_rows": "gather", "hnn_splitk_epilogue": "splitk_epilogue",
+                "hnn_grouped_conv": "conv/simt", "hnn_grouped_conv_direct": "conv/direct",
+                "hnn_conv_wgrad_reduce": "conv/wgrad_reduce", "hnn_embedding": "embed",
+                "hnn_grouped_maxpool": "pool", "hnn_grouped_relu": "relu", "hnn_conv_tc_aux": "conv/tc_aux"}
+
+
 class Launch:
     """One C-ABI call with its device-resident problem table."""
 
@@ -262,6 +272,10 @@ class Launch:
         self.entry, self.args, self.table, self.label = entry, args, table, label
         # algorithmic work of one launch (all problems, full batches): the roofline numerators
         self.flops, self.nbytes = flops, nbytes
+        if entry == "hnn_grouped_gemm":
+            self.family = GEMM_FAMILY[args[1]]
+        else:
+            self.family = ENTRY_FAMILY.get(entry, entry)
 
     def run(self, stream) -> None:
         N.call(self.entry, *self.args, stream)
@@ -1443,7 +1457,8 @@ class DeviceHybrid:
             side = torch.cuda.Stream(self.device)
             side.wait_stream(torch.cuda.current_stream(self.device))
             g = torch.cuda.CUDAGraph()
-            with torch.cuda.graph(g, stream=side):
+            # thread-local capture: host loader threads may sync events while a step is captured
+            with torch.cuda.graph(g, stream=side, capture_error_mode="thread_local"):
                 self.run_plan(plan, side.cuda_stream)
             torch.cuda.current_stream(self.device).wait_stream(side)
             graphs[host_fed] = g

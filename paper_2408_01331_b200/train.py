@@ -23,6 +23,7 @@ from functools import lru_cache
 
 import numpy as np
 
+from . import formats
 from .errors import StateError, UnknownJobError
 from .model import TrainingJob
 from .optim import ADAM_BETA1, ADAM_BETA2, OptimizerState, lr_at_epoch
@@ -56,12 +57,38 @@ class Checkpoint:
     slot_v: dict = field(default_factory=dict)
     slot_momentum: dict = field(default_factory=dict)
 
+    _TAGS = (("p", "params"), ("m", "slot_m"), ("v", "slot_v"), ("mom", "slot_momentum"))
+
+    def encode(self) -> bytes:
+        """UNND v3 bytes, identical to the reference's for the same state (src/train.py:57-80):
+        canonical JSON header {job_id, completed_epochs, data_cursor, optimizer{kind, step,
+        momentum}}, then sections "p/", "m/", "v/", "mom/" + param id in sorted name order."""
+        header = {"job_id": self.job_id, "completed_epochs": self.completed_epochs, "data_cursor": self.data_cursor,
+                  "optimizer": {"kind": self.optimizer_kind, "step": self.optimizer_step, "momentum": self.momentum}}
+        sections = {f"{tag}/{pid}": arr for tag, attr in self._TAGS for pid, arr in getattr(self, attr).items()}
+        return formats.encode_checkpoint(header, sections, sorted(sections))
+
+    @classmethod
+    def decode(cls, blob: bytes) -> "Checkpoint":
+        """Inverse of :meth:`encode` (src/train.py:82-99); unknown section tags are a StateError."""
+        header, sections = formats.decode_checkpoint(blob)
+        opt = header["optimizer"]
+        out = cls(header["job_id"], int(header["completed_epochs"]), int(header["data_cursor"]), opt["kind"],
+                  int(opt["step"]), float(opt.get("momentum", 0.0)), {})
+        by_tag = {tag: getattr(out, attr) for tag, attr in cls._TAGS}
+        for name, arr in sections.items():
+            tag, _, pid = name.partition("/")
+            if tag not in by_tag or not pid:
+                raise StateError(f"unrecognized checkpoint section {name!r}")
+            by_tag[tag][pid] = arr
+        return out
+
 
 def make_checkpoint(hybrid: HybridModel, job_id: str) -> Checkpoint:
     sub = hybrid.sub(job_id)
     params = {unqualify(job_id, k): v.copy() for k, v in hybrid.sub_params(job_id).items()}
     m1 = m2 = {}
-    if hybrid.device is not None:
+    if hybrid.on_device(job_id):
         m1, m2 = hybrid.device.download_moments(sub.slot)
     else:
         opt = sub.optimizer
@@ -90,9 +117,12 @@ def restore_checkpoint(hybrid: HybridModel, ckpt: Checkpoint) -> None:
     opt = sub.optimizer
     opt.step, opt.momentum = ckpt.optimizer_step, ckpt.momentum
     q = lambda d: {qualify(ckpt.job_id, k): np.array(v, copy=True) for k, v in d.items()}
-    opt.m1, opt.m2, opt.velocity = q(ckpt.slot_m), q(ckpt.slot_v), q(ckpt.slot_momentum)
-    if hybrid.device is not None:
+    if hybrid.on_device(ckpt.job_id):
+        # the device copy is the truth: no host moments left behind to be re-uploaded later
         hybrid.device.upload_moments(sub.slot, ckpt.slot_m or ckpt.slot_momentum, ckpt.slot_v)
+        opt.m1, opt.m2, opt.velocity = {}, {}, {}
+    else:
+        opt.m1, opt.m2, opt.velocity = q(ckpt.slot_m), q(ckpt.slot_v), q(ckpt.slot_momentum)
     sub.completed_epochs = ckpt.completed_epochs
 
 
@@ -202,7 +232,11 @@ class Trainer:
         self.results = {j.job_id: JobResult(job_id=j.job_id, epochs_completed=j.completed_epochs) for j in jobs}
         self.checkpoints: dict = {}
         self._executed: list = []
+        self._exec_keys: list = []          # (lockstep step, job order) of each executed slice
+        self._completion_keys: dict = {}
+        self._local: set = set(self.jobs)
         self._device_data: dict = {}
+        self.device = None
         for job_id in self.jobs:
             if job_id not in hybrid.sub_models:
                 raise UnknownJobError(job_id)
@@ -225,32 +259,35 @@ class Trainer:
                 out[s.job_id].append(s.epoch)
         return out
 
-    def _device(self):
-        dev = self.hybrid.materialize(self.device_name, use_tensor_cores=self.use_tc,
-                                      fuse_optimizer=self.fuse_optimizer, keep_grads=self.keep_grads,
-                                      conv_precision=self.conv_precision)
-        for jid, sub in self.hybrid.sub_models.items():
-            opt = sub.optimizer
-            if opt.m1 or opt.m2 or opt.velocity:
-                strip = lambda d: {unqualify(jid, k): v for k, v in d.items()}
-                dev.upload_moments(sub.slot, strip(opt.m1 or opt.velocity), strip(opt.m2))
-        return dev
+    def _local_ids(self) -> list:
+        """Jobs this process trains: all of them, or its model-identity shard (parallel.shard_jobs)."""
+        if self.comm is None or self.comm.world == 1:
+            return list(self.jobs)
+        from .parallel import shard_jobs
+
+        return [j.job_id for j in shard_jobs(list(self.jobs.values()), self.comm.world)[self.comm.rank]]
+
+    def _device(self, local):
+        """Materialise with this Trainer's options.  Single-process: every sub-model of the hybrid
+        (jobs of other Trainers ride along untouched); sharded: only this rank's jobs."""
+        return self.hybrid.materialize(self.device_name, use_tensor_cores=self.use_tc,
+                                       fuse_optimizer=self.fuse_optimizer, keep_grads=self.keep_grads,
+                                       conv_precision=self.conv_precision,
+                                       local=None if self.comm is None else local)
 
     def _upload_datasets(self, dev) -> list:
         by_model = [None] * dev.n
         cache = self._device_data
-        for jid, sub in self.hybrid.sub_models.items():
-            if jid not in self.jobs:
-                ds = None
-            else:
-                ds = self.datasets[jid]
-            if ds is None:
-                continue
-            key = ds.content_hash
-            if key not in cache:
-                cache[key] = (self.comm.share_dataset(ds, dev.device)[0] if self.comm is not None
-                              else DeviceDataset(ds, dev.device))
-            by_model[sub.slot] = cache[key]
+        wanted = [self.datasets[s.job_id] for s in dev.slots if s.job_id in self.jobs]
+        if self.comm is not None:
+            missing = [d for d in wanted if d.content_hash not in cache]
+            cache.update(self.comm.share_datasets(missing, dev.device))
+        for ds in wanted:
+            if ds.content_hash not in cache:
+                cache[ds.content_hash] = DeviceDataset(ds, dev.device)
+        for s in dev.slots:
+            if s.job_id in self.jobs:
+                by_model[s.index] = cache[self.datasets[s.job_id].content_hash]
         # models of the hybrid not trained by this Trainer borrow any dataset of the right shape
         for i, d in enumerate(by_model):
             if d is None:
@@ -261,24 +298,34 @@ class Trainer:
                 by_model[i] = match[0]
         return by_model
 
+    def _prepare_device(self, local):
+        dev = self._device(local)
+        by_model = self._upload_datasets(dev)
+        dev.bind_datasets(by_model, max(d.n_train for d in by_model))
+        dev.build_plans()
+        dev.reset_status()
+        self.device = dev
+        return dev
+
     # ------------------------------------------------------------------ run
     def run(self) -> TrainReport:
         started = time.perf_counter()
-        for job in self.jobs.values():
-            if job.completed_epochs >= job.hypers.epochs:
-                self._complete(job.job_id)
-        # pause requests pending before the first slice apply immediately (src/train.py:341-342)
-        self._apply_pauses()
         epochs = self._epochs_from_plan()
-        live = [jid for jid in self.jobs if self.results[jid].status == "training" and epochs[jid]]
+        local = self._local_ids()
+        self._local = set(local)
+        # a resumed job may arrive with nothing left to do (src/train.py:339-341); its test
+        # evaluation runs on the device, so the device is set up first, with this Trainer's options
+        finished = [jid for jid in local if self.jobs[jid].completed_epochs >= self.jobs[jid].hypers.epochs]
+        live = [jid for jid in local if jid not in finished and epochs[jid]]
         steps_run, samples = 0, 0
+        if live or finished:
+            dev = self._prepare_device(local)
+        for jid in finished:
+            self._complete(jid, key=(-1, self._order(jid)))
+        # pause requests pending before the first slice apply immediately (src/train.py:343)
+        self._apply_pauses()
+        live = [jid for jid in live if self.results[jid].status == "training"]
         if live:
-            dev = self._device()
-            by_model = self._upload_datasets(dev)
-            dev.bind_datasets(by_model, max(d.n_train for d in by_model))
-            dev.build_plans()
-            dev.reset_status()
-            self.device = dev
             tracks = {}
             for jid in live:
                 sub = self.hybrid.sub(jid)
@@ -287,9 +334,48 @@ class Trainer:
                 tracks[jid] = tr
             steps_run, samples = self._lockstep(dev, tracks)
         self._apply_pauses(force_all=True)
+        if self.comm is not None and self.comm.world > 1:
+            steps_run, samples = self._gather(local, steps_run, samples)
         report = TrainReport(self.plan.policy, self.results, executed=list(self._executed),
                              wall_time=time.perf_counter() - started, steps=steps_run, samples=samples)
         return report
+
+    def _order(self, jid) -> int:
+        return list(self.jobs).index(jid)
+
+    def _gather(self, local, steps_run, samples) -> tuple:
+        """Sharded run: all-gather every rank's job results, slice log and checkpoints, then
+        broadcast each job's final state from its owner, so every rank returns the report (and
+        holds the parameters) a single-process run over all jobs would have produced."""
+        comm = self.comm
+        mine = {
+            "results": {jid: self.results[jid] for jid in local},
+            "log": [(k, e) for k, e in zip(self._exec_keys, self._executed)],
+            "completions": {jid: self._completion_keys[jid] for jid in local if jid in self._completion_keys},
+            "checkpoints": {jid: c for jid, c in self.checkpoints.items() if jid in self._local},
+            "state": {jid: (self.hybrid.sub(jid).optimizer.step, self.hybrid.sub(jid).completed_epochs)
+                      for jid in local},
+            "steps": steps_run, "samples": samples,
+        }
+        every = comm.all_gather_object(mine)
+        owners, state, log = {}, {}, []
+        for r, part in enumerate(every):
+            for jid, res in part["results"].items():
+                owners[jid] = r
+                if r != comm.rank:
+                    self.results[jid] = res
+            state.update(part["state"])
+            log += part["log"]
+            self.checkpoints.update(part["checkpoints"])
+        log.sort(key=lambda t: t[0])
+        self._exec_keys = [k for k, _ in log]
+        self._executed = [e for _, e in log]
+        # completion_index = slices executed up to and including the job's last slice (lockstep order)
+        for part in every:
+            for jid, key in part["completions"].items():
+                self.results[jid].completion_index = sum(1 for k in self._exec_keys if k <= key)
+        comm.exchange_models(self.hybrid, owners, state)
+        return max(p["steps"] for p in every), sum(p["samples"] for p in every)
 
     def _boundaries(self, tracks) -> list:
         pts = {0}
@@ -300,7 +386,8 @@ class Trainer:
         return sorted(pts)
 
     def _window_rows(self, tracks, t0, t1) -> np.ndarray:
-        rows = np.zeros((t1 - t0, len(self.hybrid.sub_models)), dtype=STEP_DTYPE)
+        width = self.device.n if self.device is not None else len(self.hybrid.sub_models)
+        rows = np.zeros((t1 - t0, width), dtype=STEP_DTYPE)
         for tr in tracks.values():
             if tr.done:
                 continue
@@ -354,6 +441,7 @@ class Trainer:
                         self.step_observer(tr.job.job_id, self.hybrid.sub_params(tr.job.job_id))
             st = dev.read_status()  # synchronises the stream
             elapsed = time.perf_counter() - wall0
+            self._poll_pauses()  # once per window: every hit is kept until its job's boundary
             for tr in tracks.values():
                 if tr.done or t0 >= tr.total:
                     continue
@@ -378,24 +466,29 @@ class Trainer:
                     sub = self.hybrid.sub(tr.job.job_id)
                     sub.completed_epochs = e + 1
                     sub.optimizer.step = tr.opt_base + t1
+                    key = (t1, self._order(tr.job.job_id))
                     self._executed.append((tr.job.job_id, e))
+                    self._exec_keys.append(key)
                     if self.slice_observer is not None:
                         self.slice_observer(tr.job.job_id, e)
                     if e == tr.job.hypers.epochs - 1:
                         tr.done = True
-                        self._complete(tr.job.job_id)
-                    elif self._pause_wanted(tr.job.job_id):
+                        self._complete(tr.job.job_id, key)
+                    elif tr.job.job_id in self._pause_requests:
                         tr.done = True
                         self._pause(tr.job.job_id)
         return steps_run, samples
 
     # ------------------------------------------------------------------ completion / pause
-    def _pause_wanted(self, job_id) -> bool:
-        if job_id in self._pause_requests:
-            return True
-        if self.pause_poll is not None:
-            return job_id in set(self.pause_poll())
-        return False
+    def _poll_pauses(self):
+        """Call pause_poll once and keep every hit for a job of this Trainer that is still training
+        (the reference's poll consumes its markers, src/workspace.py:293-301, so a hit must not be
+        dropped just because its job is mid-epoch right now)."""
+        if self.pause_poll is None:
+            return
+        for jid in self.pause_poll():
+            if jid in self.jobs and self.results[jid].status == "training":
+                self._pause_requests.add(jid)
 
     def _pause(self, job_id):
         self._pause_requests.discard(job_id)
@@ -407,21 +500,20 @@ class Trainer:
 
     def _apply_pauses(self, force_all=False):
         """Checkpoint and stop every job with a pending pause request (reference _apply_pauses)."""
-        wanted = set(self._pause_requests)
-        if self.pause_poll is not None:
-            wanted |= {j for j in self.pause_poll() if j in self.jobs and self.results[j].status == "training"}
-        self._pause_requests.clear()
+        self._poll_pauses()
+        wanted = {j for j in self._pause_requests if j in self._local}
+        self._pause_requests -= wanted
         for jid in sorted(wanted):
             if self.results[jid].status == "training":
                 self._pause(jid)
 
-    def _complete(self, job_id: str) -> None:
+    def _complete(self, job_id: str, key: tuple) -> None:
         result = self.results[job_id]
-        sub = self.hybrid.sub(job_id)
         ds = self.datasets[job_id]
-        loss, acc = evaluate_hybrid(self.hybrid, [job_id], {job_id: ds}, trainer=self)[job_id]
+        loss, acc = evaluate_hybrid(self.hybrid, [job_id], {job_id: ds})[job_id]
         result.status = "complete"
         result.completion_index = len(self._executed)
+        self._completion_keys[job_id] = key
         result.final_test_loss, result.final_test_accuracy = loss, acc
         if self.completion_sink is not None:
             self.completion_sink(job_id, self.hybrid.snapshot(), result)
@@ -461,38 +553,26 @@ class HostFedStepper:
                         for _ in range(2)]
         self.staging_free = [None, None]
         self.steps_issued = 0
+        self.dev.train_steps(0, use_graph=use_graph, host_fed=True)  # capture the step graph up front
 
-    def stage_epoch_batches(self, ds, rows, count: int = 2, comm=None) -> list:
-        """Pinned host copies of the first `count` steps' batches (store.batches order, src/store.py:68-81)."""
-        import torch
-
-        from . import rng
-
-        dev = self.dev
+    def stage_epoch_batches(self, rows, count: int = 2, host_datasets: dict | None = None) -> list:
+        """Pinned host copies of the first `count` steps' batches (store.batches order, src/store.py:68-81),
+        each model from its own dataset and its row's epoch permutation."""
+        fill = _BatchAssembler(self.hybrid, host_datasets or self.datasets)
         staged = []
-        perms = {}
         for t in range(count):
-            x = torch.zeros(dev.batch_arena.numel(), dtype=torch.float32).pin_memory()
-            y = torch.zeros(dev.label_arena.numel(), dtype=torch.int32).pin_memory()
-            xn, yn = x.numpy(), y.numpy()
-            for slot, (xo, yo, ld) in zip(dev.slots, dev.batch_layout):
-                d = self.datasets[slot.job_id]
-                if slot.index not in perms:
-                    perms[slot.index] = rng.permutation(d.sample_count, "shuffle", d.content_hash,
-                                                        self.hybrid.sub(slot.job_id).hypers.seed, 0)
-                r = rows[t, slot.index]
-                idx = perms[slot.index][r["perm_base"]:r["perm_base"] + r["rows"]]
-                sample = int(np.prod(slot.sample_shape))
-                blk = xn[xo:xo + slot.batch_size * ld].reshape(slot.batch_size, ld)
-                blk[: idx.size, :sample] = ds.train_x[idx].reshape(idx.size, sample)
-                yn[yo:yo + idx.size] = ds.train_y[idx].astype(np.int32)
+            x, y = fill.buffers()
+            for slot in self.dev.slots:
+                fill.fill(x, y, rows[t], slot.index)
             staged.append((x, y))
         return staged
 
     def step(self, host_batch) -> None:
+        """Enqueue one step from a host batch: a ``(x, y)`` pair of pinned arena-layout tensors or a
+        :class:`HostBatchLoader` batch (its buffer is handed back once the H2D copy has run)."""
         import torch
 
-        x, y = host_batch
+        x, y = host_batch[0], host_batch[1]
         k = self.steps_issued % 2
         sx, sy = self.staging[k]
         compute = torch.cuda.current_stream(self.dev.device)
@@ -503,6 +583,8 @@ class HostFedStepper:
             sy.copy_(y, non_blocking=True)
             ready = torch.cuda.Event()
             ready.record(self.copy_stream)
+        if isinstance(host_batch, LoadedBatch):
+            host_batch.release(ready)
         compute.wait_event(ready)
         self.dev.batch_arena.copy_(sx, non_blocking=True)
         self.dev.label_arena.copy_(sy, non_blocking=True)
@@ -521,25 +603,206 @@ class HostFedStepper:
         return {s.job_id: (float(self.loss_host[s.index]), int(self.hits_host[s.index])) for s in self.dev.slots}
 
 
+class _BatchAssembler:
+    """Host-side batch gather into the device batch-arena layout (the reference's store.batches:
+    ``train_x[perm[s:s+B]]``, src/store.py:68-81), one model slot at a time."""
+
+    def __init__(self, hybrid: HybridModel, datasets: dict):
+        self.hybrid, self.dev, self.datasets = hybrid, hybrid.device, datasets
+        self._perms: dict = {}
+
+    def buffers(self) -> tuple:
+        import torch
+
+        return (torch.zeros(self.dev.batch_arena.numel(), dtype=torch.float32).pin_memory(),
+                torch.zeros(self.dev.label_arena.numel(), dtype=torch.int32).pin_memory())
+
+    def perm(self, slot, epoch: int) -> np.ndarray:
+        from . import rng
+
+        key = (slot.index, epoch)
+        p = self._perms.get(key)
+        if p is None:
+            d = self.datasets[slot.job_id]
+            p = rng.permutation(d.sample_count, "shuffle", d.content_hash, self.hybrid.sub(slot.job_id).hypers.seed,
+                                epoch)
+            self._perms = {k: v for k, v in self._perms.items() if k[0] != slot.index}  # one epoch per slot
+            self._perms[key] = p
+        return p
+
+    def fill(self, x, y, row, m: int, perm=None) -> None:
+        """Gather model m's rows of step `row` into the pinned arenas x / y (native, GIL released)."""
+        from . import _native as N
+
+        slot = self.dev.slots[m]
+        xo, yo, ld = self.dev.batch_layout[m]
+        r = row[m]
+        if not r["active"]:
+            return
+        d = self.datasets[slot.job_id]
+        perm = self.perm(slot, int(r["epoch"])) if perm is None else perm
+        idx = np.ascontiguousarray(perm[r["perm_base"]:r["perm_base"] + r["rows"]], dtype=np.int64)
+        sample = int(np.prod(slot.sample_shape))
+        src, ys = self._sources(slot.job_id, d, sample)
+        N.call("hnn_host_gather_rows", x.data_ptr() + 4 * xo, ld, y.data_ptr() + 4 * yo, src.ctypes.data, sample,
+               ys.ctypes.data, idx.ctypes.data, idx.size, sample)
+        if idx.size < slot.batch_size:  # a short final batch: zero rows, as the device gather writes
+            x.numpy()[xo + idx.size * ld:xo + slot.batch_size * ld] = 0.0
+            y.numpy()[yo + idx.size:yo + slot.batch_size] = 0
+
+    def _sources(self, job_id, d, sample):
+        cache = self.__dict__.setdefault("_src", {})
+        got = cache.get(job_id)
+        if got is None:
+            got = (np.ascontiguousarray(d.train_x.reshape(d.train_x.shape[0], sample), dtype=np.float32),
+                   np.ascontiguousarray(d.train_y, dtype=np.float32))
+            cache[job_id] = got
+        return got
+
+
+class LoadedBatch(tuple):
+    """One step's pinned (x, y) arena buffers from a :class:`HostBatchLoader`."""
+
+    def release(self, copied_event) -> None:
+        self.loader._recycle(self.slot_index, copied_event)
+
+
+class HostBatchLoader:
+    """Host data loader for :class:`HostFedStepper`: worker threads gather every upcoming step's
+    batches — each model's rows of its epoch permutation from its host dataset, the reference's
+    ``store.batches`` work (src/store.py:68-81) — into a ring of pinned arena-layout buffers,
+    ``depth`` steps ahead of the device.  A buffer is refilled only after the H2D copy that
+    read it has completed (the CUDA event the stepper hands back)."""
+
+    def __init__(self, hybrid: HybridModel, datasets: dict, rows: np.ndarray, threads: int = 8, depth: int = 3):
+        from concurrent.futures import ThreadPoolExecutor
+
+        self.asm = _BatchAssembler(hybrid, datasets)
+        self.rows = rows
+        self.depth = depth
+        self.bufs = [self.asm.buffers() for _ in range(depth)]
+        self.pool = ThreadPoolExecutor(max(1, threads))
+        self.pending: list = [None] * depth
+        self.t_next = 0
+        self.t_issue = 0
+        # permutations are computed on the caller's thread before any worker needs them
+        for t in range(min(depth, rows.shape[0])):
+            self._issue(t % depth, None)
+
+    def _issue(self, k: int, after) -> None:
+        t = self.t_issue
+        self.t_issue += 1
+        if t >= self.rows.shape[0]:
+            self.pending[k] = None
+            return
+        row = self.rows[t]
+        dev = self.asm.dev
+        perms = {m: self.asm.perm(dev.slots[m], int(row[m]["epoch"])) for m in range(dev.n) if row[m]["active"]}
+        x, y = self.bufs[k]
+
+        def job(m):
+            if after is not None:
+                after.synchronize()
+            self.asm.fill(x, y, row, m, perms.get(m))
+
+        self.pending[k] = [self.pool.submit(job, m) for m in range(dev.n)]
+
+    def next(self) -> LoadedBatch:
+        """The next step's batch (blocks until its gather is complete)."""
+        k = self.t_next % self.depth
+        futs = self.pending[k]
+        if futs is None:
+            raise StateError("HostBatchLoader: schedule exhausted")
+        for f in futs:
+            f.result()
+        self.t_next += 1
+        out = LoadedBatch(self.bufs[k])
+        out.loader, out.slot_index = self, k
+        return out
+
+    def _recycle(self, k: int, copied_event) -> None:
+        self._issue(k, copied_event)
+
+    def close(self) -> None:
+        self.pool.shutdown(wait=True)
+
+
+# --------------------------------------------------------------------------- one model, one batch
+
+
+def run_batch(graph, params, order, batch, optimizer, lr, observer=None) -> tuple:
+    """Forward, loss, backward, update for one batch of one model; returns (loss, correct)
+    (src/train.py:223-256) — the reference's step, each stage on the device kernels.
+
+    A non-finite loss returns ``(loss, 0)`` before any gradient or update (the caller's abort
+    signal).  ``correct`` counts argmax hits of the pre-update logits.  The Trainer does not go
+    through here: it runs every model's step as one grouped launch sequence (:mod:`.runtime`)."""
+    from . import devops, engine
+    from .errors import MissingGradientError
+    from .ops import OP_KINDS, check_class_indices
+    from .optim import apply_update
+
+    torch = devops._torch()
+    output_node = graph.node(graph.output)
+    if OP_KINDS[output_node.op].loss_head:
+        loss, tape = engine.forward(graph, params, batch.x, targets=batch.y, order=order)
+        logits = tape.outputs[output_node.inputs[0]]
+        upstream = np.float32(1.0)
+    else:
+        logits, tape = engine.forward(graph, params, batch.x, order=order)
+        logits_dev = devops._to_dev(logits)[0]
+        t = torch.from_numpy(check_class_indices(devops._host(batch.y), logits_dev.shape[1]).astype(np.int32))
+        loss_t, upstream, _ = devops.sce_device(logits_dev, t.to(logits_dev.device))
+        loss = np.float32(loss_t.item())
+        if tape.host:
+            upstream = upstream.cpu().numpy()
+    loss_value = float(loss)
+    if not np.isfinite(loss_value):
+        return loss_value, 0
+    grads = engine.backward(graph, params, tape, upstream)
+    missing = [pid for pid in params if pid not in grads]
+    if missing:
+        raise MissingGradientError(missing[0])
+    extra = [pid for pid in grads if pid not in params]
+    if extra:
+        raise MissingGradientError(extra[0], extra=True)
+    apply_update(optimizer, params, grads, lr)
+    if observer is not None:
+        observer(params)
+    logits_host = devops._host(logits)
+    targets = check_class_indices(devops._host(batch.y), logits_host.shape[1])
+    return loss_value, int((logits_host.argmax(axis=1) == targets).sum())
+
+
 # --------------------------------------------------------------------------- evaluation
 
 
-def evaluate_hybrid(hybrid: HybridModel, job_ids: list, datasets: dict, trainer=None) -> dict:
-    """Test-split loss/accuracy of several sub-models in one lockstep forward pass (src/train.py:259-279)."""
+def evaluate_hybrid(hybrid: HybridModel, job_ids: list, datasets: dict, **options) -> dict:
+    """Test-split loss/accuracy of several sub-models in one lockstep forward pass (src/train.py:259-279).
+
+    Uses the hybrid's device as bound by its Trainer.  A hybrid that was never set up for the
+    device is materialised here (``options``: the Trainer's materialisation options) with each
+    sub-model bound to its own dataset from ``datasets``; sub-models without one borrow a dataset
+    of their input shape, and evaluating a job without a dataset is an error."""
     dev = hybrid.device
     if dev is None or not dev.eval_plan:
-        t = Trainer(hybrid, _NoPlan(), [], {}, use_graph=False)
-        dev = hybrid.materialize()
-        by_model = []
+        dev = hybrid.materialize(**options)
         cache = {}
-        for jid, sub in hybrid.sub_models.items():
-            ds = datasets.get(jid) or next(iter(datasets.values()))
-            if ds.content_hash not in cache:
-                cache[ds.content_hash] = DeviceDataset(ds, dev.device)
-            by_model.append(cache[ds.content_hash])
+        for ds in datasets.values():
+            cache.setdefault(ds.content_hash, ds)
+        by_model = []
+        uploaded = {}
+        for slot in dev.slots:
+            ds = datasets.get(slot.job_id)
+            if ds is None:
+                ds = next((d for d in cache.values() if tuple(d.sample_shape) == tuple(slot.sample_shape)), None)
+            if ds is None:
+                raise StateError(f"job {slot.job_id!r}: dataset not resolved")
+            if ds.content_hash not in uploaded:
+                uploaded[ds.content_hash] = DeviceDataset(ds, dev.device)
+            by_model.append(uploaded[ds.content_hash])
         dev.bind_datasets(by_model, max(d.n_train for d in by_model))
         dev.build_plans()
-        del t
     out = {}
     todo = []
     for jid in job_ids:
@@ -550,6 +813,9 @@ def evaluate_hybrid(hybrid: HybridModel, job_ids: list, datasets: dict, trainer=
             todo.append(jid)
     if not todo:
         return out
+    for jid in todo:
+        if not hybrid.on_device(jid):
+            raise StateError(f"job {jid!r} is held by another rank; evaluate it where it trained")
     slots = {jid: hybrid.sub(jid).slot for jid in todo}
     for jid in todo:
         if dev.model_data[slots[jid]].content_hash != datasets[jid].content_hash:
@@ -573,11 +839,6 @@ def evaluate_hybrid(hybrid: HybridModel, job_ids: list, datasets: dict, trainer=
         total = int(row["seen"])
         out[jid] = (float(row["loss_sum"]) / total, int(row["correct_sum"]) / total)
     return out
-
-
-class _NoPlan:
-    policy = "lockstep"
-    slices = ()
 
 
 def evaluate(graph, params, order, x, y, batch_size: int) -> tuple:

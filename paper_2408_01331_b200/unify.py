@@ -101,6 +101,10 @@ class HybridModel:
     def node_count(self) -> int:
         return sum(len(s.graph.nodes) for s in self.sub_models.values()) + 2
 
+    def on_device(self, job_id: str) -> bool:
+        """True when the job's state lives in this process's HBM arenas (its slot is local)."""
+        return self.device is not None and self.sub(job_id).slot >= 0
+
     @property
     def params(self) -> dict:
         if self.device is None:
@@ -112,8 +116,10 @@ class HybridModel:
 
     def sub_params(self, job_id: str) -> dict:
         sub = self.sub(job_id)
-        if self.device is None:
-            return {pid: self._host_params[pid] for pid in sub.param_ids()}
+        if not self.on_device(job_id):
+            if self.device is None:
+                return {pid: self._host_params[pid] for pid in sub.param_ids()}
+            return {pid: np.array(self._host_params[pid], copy=True) for pid in sub.param_ids()}
         host = self.device.download_params(sub.slot)
         return {qualify(job_id, pid): arr for pid, arr in host.items()}
 
@@ -121,16 +127,17 @@ class HybridModel:
         snap = HybridModel(copy.deepcopy(self.sub_models),
                            {pid: np.array(a, copy=True) for pid, a in self.params.items()},
                            self.global_input, self.global_output)
-        if self.device is not None:
-            for jid, sub in snap.sub_models.items():
-                slot = self.sub_models[jid].slot
-                m1, m2 = self.device.download_moments(slot)
-                kind = sub.optimizer.kind
-                if kind == "adam":
-                    sub.optimizer.m1 = {qualify(jid, k): v for k, v in m1.items()}
-                    sub.optimizer.m2 = {qualify(jid, k): v for k, v in m2.items()}
-                elif m1:
-                    sub.optimizer.velocity = {qualify(jid, k): v for k, v in m1.items()}
+        for jid, sub in snap.sub_models.items():
+            sub.slot = -1
+            if not self.on_device(jid):
+                continue  # host-held state was deep-copied with the sub-model
+            m1, m2 = self.device.download_moments(self.sub_models[jid].slot)
+            kind = sub.optimizer.kind
+            if kind == "adam":
+                sub.optimizer.m1 = {qualify(jid, k): v for k, v in m1.items()}
+                sub.optimizer.m2 = {qualify(jid, k): v for k, v in m2.items()}
+            elif m1:
+                sub.optimizer.velocity = {qualify(jid, k): v for k, v in m1.items()}
         return snap
 
     # ---------------------------------------------------------------- device side
@@ -139,31 +146,86 @@ class HybridModel:
         sub = self.sub(job_id)
         bare = {(unqualify(job_id, k) if k.startswith(job_id + "/") else k): np.asarray(v, dtype=np.float32)
                 for k, v in params.items()}
-        if self.device is None:
+        if not self.on_device(job_id):
             for pid, arr in bare.items():
                 self._host_params[qualify(job_id, pid)][...] = arr
         else:
             self.device.upload_params(sub.slot, bare)
 
     def materialize(self, device=None, use_tensor_cores: bool = True, fuse_optimizer: bool = True,
-                    keep_grads: bool = False, conv_precision: str = "f32"):
-        """Pack every sub-model into device arenas (idempotent)."""
+                    keep_grads: bool = False, conv_precision: str = "f32", local=None):
+        """Pack sub-models into device arenas (idempotent).
+
+        ``local``: the job ids this process holds in HBM (model-identity sharding over ranks,
+        :mod:`.parallel`); the others keep their state on the host.  Default: every job.
+        Host-held optimizer moments (a restored checkpoint, a released device) are uploaded
+        here, once, with the parameters."""
+        want = [jid for jid in self.sub_models if local is None or jid in set(local)]
         if self.device is not None:
-            return self.device
+            if [s.job_id for s in self.device.slots] == want:
+                return self.device
+            self.release_device()
         from .runtime import DeviceHybrid, ModelSlot
 
         slots = []
-        for i, (jid, sub) in enumerate(self.sub_models.items()):
+        for sub in self.sub_models.values():
+            sub.slot = -1
+        for i, jid in enumerate(want):
+            sub = self.sub_models[jid]
             sub.slot = i
             hp = sub.hypers
             slots.append(ModelSlot(i, jid, sub.original, hp.batch_size if hp else 1, sub.optimizer.kind,
                                    sub.optimizer.momentum, engine.param_specs(sub.original)))
         dev = DeviceHybrid(slots, device=device, use_tensor_cores=use_tensor_cores, fuse_optimizer=fuse_optimizer,
                            keep_grads=keep_grads, conv_precision=conv_precision)
-        for jid, sub in self.sub_models.items():
+        for jid in want:
+            sub = self.sub_models[jid]
             dev.upload_params(sub.slot, {unqualify(jid, pid): self._host_params[pid] for pid in sub.param_ids()})
+            opt = sub.optimizer
+            if opt.m1 or opt.m2 or opt.velocity:
+                strip = lambda d: {unqualify(jid, k): v for k, v in d.items()}
+                dev.upload_moments(sub.slot, strip(opt.m1 or opt.velocity), strip(opt.m2))
+                # the device copy is the truth from here on: drop the host moments so a later
+                # run can never re-upload stale ones (they are re-read by snapshot / checkpoints)
+                opt.m1, opt.m2, opt.velocity = {}, {}, {}
         self.device = dev
         return dev
+
+    def release_device(self) -> None:
+        """Copy every device-held sub-model's parameters and moments back to the host and drop
+        the device arenas (before re-packing a different local set)."""
+        dev = self.device
+        if dev is None:
+            return
+        for jid, sub in self.sub_models.items():
+            if sub.slot < 0:
+                continue
+            for pid, arr in dev.download_params(sub.slot).items():
+                self._host_params[qualify(jid, pid)] = arr
+            m1, m2 = dev.download_moments(sub.slot)
+            q = lambda d: {qualify(jid, k): v for k, v in d.items()}
+            if sub.optimizer.kind == "adam":
+                sub.optimizer.m1, sub.optimizer.m2 = q(m1), q(m2)
+            elif m1:
+                sub.optimizer.velocity = q(m1)
+            sub.slot = -1
+        self.device = None
+
+    def store_remote(self, job_id: str, params: dict, m1: dict, m2: dict, step: int, completed_epochs: int) -> None:
+        """Host state of a sub-model trained on another rank (bare ids), after a gather."""
+        sub = self.sub(job_id)
+        if self.on_device(job_id):
+            raise StateError(f"job {job_id!r} is held on this rank's device")
+        for pid, arr in params.items():
+            self._host_params[qualify(job_id, pid)] = np.array(arr, dtype=np.float32, copy=True)
+        q = lambda d: {qualify(job_id, k): np.array(v, dtype=np.float32, copy=True) for k, v in d.items()}
+        opt = sub.optimizer
+        if opt.kind == "adam":
+            opt.m1, opt.m2 = q(m1), q(m2)
+        elif m1:
+            opt.velocity = q(m1)
+        opt.step = step
+        sub.completed_epochs = completed_epochs
 
 
 def merge(jobs: list) -> HybridModel:

@@ -445,8 +445,8 @@ def test_pause_before_run_checkpoints_immediately(pkg):
 
 
 def test_pause_and_resume_is_bit_identical_to_a_straight_run(pkg):
-    """Checkpoint at an epoch boundary, restore into a fresh hybrid, finish: same bits as no pause
-    (mirrors pkg/tests/test_trainer.py:288-372 on the device path)."""
+    """Checkpoint at an epoch boundary, encode / decode it (UNND v3), restore into a fresh hybrid,
+    finish: same bits as no pause (mirrors pkg/tests/test_trainer.py:288-372 on the device path)."""
     from paper_2408_01331_b200 import store, zoo
 
     splits = oracle.blob_splits("golden", "four", 4, 12, 96, 32)
@@ -465,7 +465,8 @@ def test_pause_and_resume_is_bit_identical_to_a_straight_run(pkg):
     t1.slice_observer = lambda j, e: t1.request_pause("a") if (j, e) == ("a", 0) else None
     r1 = t1.run()
     assert r1.jobs["a"].status == "paused" and r1.jobs["b"].status == "complete"
-    ckpt = t1.checkpoints["a"]
+    # through the UNND v3 bytes a Workspace would write to disk (src/train.py:57-99)
+    ckpt = pkg.Checkpoint.decode(t1.checkpoints["a"].encode())
     assert ckpt.completed_epochs == 1 and ckpt.optimizer_step == 6 and ckpt.slot_m and ckpt.slot_v
 
     resumed = mk()[0]
@@ -477,6 +478,54 @@ def test_pause_and_resume_is_bit_identical_to_a_straight_run(pkg):
     got = pkg.separate(h2, "a")[1]
     for pid, v in straight["a"].items():
         assert np.array_equal(got[pid], v), pid
+
+
+@pytest.mark.parametrize("kind", ["adam", "sgd"])
+def test_resume_from_reference_checkpoint_bytes(pkg, kind):
+    """A checkpoint the unmodified reference wrote when its Trainer paused a job after epoch 1
+    (tests/golden/make_checkpoint_golden.py) decodes, restores into our hybrid and finishes the
+    remaining two epochs on the device (the lr milestone falls after the resume) at the
+    reference's own final weights: rel 1e-3 after 12 steps (the trajectory drift bound)."""
+    from paper_2408_01331_b200 import store, zoo
+
+    arr = np.load(GOLDEN / "checkpoint_resumed.npz")
+    ds = store.from_splits({k: arr[f"data/{k}"] for k in ("train_x", "train_y", "test_x", "test_y")})
+    ckpt = pkg.Checkpoint.decode((GOLDEN / f"checkpoint_paused_{kind}.bin").read_bytes())
+    job = zoo.job(ckpt.job_id, zoo.mlp(12, (16,), 4, name="ckpt-mlp"), ds, 0, epochs=3, batch_size=16,
+                  lr=0.01 if kind == "adam" else 0.1, optimizer=kind, seed=3, milestones=(2,))
+    job.completed_epochs = ckpt.completed_epochs
+    h = pkg.merge([job])
+    pkg.restore_checkpoint(h, ckpt)
+    r = pkg.Trainer(h, pkg.make_plan("fcfs", [job]), [job], {job.job_id: ds}).run()
+    assert r.jobs[job.job_id].status == "complete" and r.jobs[job.job_id].epochs_completed == 3
+    got = pkg.separate(h, job.job_id)[1]
+    for pid, v in got.items():
+        ref = arr[f"{kind}/{job.job_id}/{pid}"]
+        assert rel(v, ref) <= 1e-3, (pid, rel(v, ref))
+    assert pkg.make_checkpoint(h, job.job_id).optimizer_step == ckpt.optimizer_step + 12
+
+
+def test_pause_poll_hits_are_kept_until_the_jobs_boundary(pkg):
+    """the reference's poll consumes its markers (src/workspace.py:293-301).  A hit
+    for job b that arrives while only job a is at a boundary must still pause b at b's own
+    boundary, and the poll is called once per window, not once per job."""
+    from paper_2408_01331_b200 import store, zoo
+
+    ds = store.from_splits(oracle.blob_splits("golden", "poll", 2, 8, 64, 32))
+    # a: 2 steps per epoch, b: 4 -> the window ending at step 2 is a's boundary only
+    jobs = [zoo.job("a", zoo.mlp(8, (16,), 2), ds, 0, epochs=3, batch_size=32, lr=0.05, seed=1),
+            zoo.job("b", zoo.mlp(8, (16,), 2), ds, 1, epochs=3, batch_size=16, lr=0.05, seed=2)]
+    h = pkg.merge(jobs)
+    calls = []
+
+    def poll():  # call 1: before the first slice; call 2: after the window ending at step 2
+        calls.append(1)
+        return ["b"] if len(calls) == 2 else []
+
+    t = pkg.Trainer(h, pkg.make_plan("rr", jobs), jobs, {"a": ds, "b": ds}, pause_poll=poll)
+    r = t.run()
+    assert r.jobs["b"].status == "paused" and r.jobs["a"].status == "complete"
+    assert t.checkpoints["b"].completed_epochs == 1  # paused at b's own first boundary (step 4)
 
 
 @pytest.mark.parametrize("opt_step", [1, 7])
@@ -817,13 +866,14 @@ def test_host_fed_stepper_matches_device_gather(pkg):
     device = torch.device("cuda", 0)
     outs = []
     for host in (False, True):
-        jobs, hy, dev, ddev, meta, ds, comm = bench.build_rank("c1", 0, 1, device)
+        _, jobs, hy, dev, ddev, ds, comm = bench.build_rank("c1", 0, 1, device)
+        meta = ds
         rows = bench.schedule(jobs, meta, 4)
         bench.upload_perms(dev, jobs, meta)
         dev.load_schedule(rows)
         if host:
             st = HostFedStepper(hy, {j.job_id: meta for j in jobs})
-            staged = st.stage_epoch_batches(ds, rows, count=4)
+            staged = st.stage_epoch_batches(rows, count=4, host_datasets={j.job_id: ds for j in jobs})
             for b in staged:
                 st.step(b)
             losses = st.finish()
@@ -929,7 +979,8 @@ def test_split_k_forward_is_bit_identical(pkg, monkeypatch):
     outs = []
     for split in ("1", "0"):
         monkeypatch.setenv("HNN_SPLITK_FWD", split)
-        jobs, hy, dev, ddev, meta, ds, comm = bench.build_rank("c1", 0, 1, device)
+        _, jobs, hy, dev, ddev, ds, comm = bench.build_rank("c1", 0, 1, device)
+        meta = ds
         labels = [l.label for l in dev.train_plan]
         assert any(l.endswith("/splitk") for l in labels) == (split == "1"), labels
         rows = bench.schedule(jobs, meta, 4)

@@ -161,3 +161,75 @@ def test_package_is_byte_identical_to_reference(tag):
     bad.pop(next(iter(bad)))
     with pytest.raises(Exception):
         package(graph, bad)
+
+
+@pytest.mark.parametrize("kind", ["adam", "momentum"])
+def test_checkpoint_encode_is_byte_identical_to_reference(kind):
+    """Checkpoint.encode writes the reference's UNND v3 bytes (src/train.py:57-80,
+    src/formats.py:188-201) for the same state; decode inverts it (fixtures:
+    tests/golden/make_checkpoint_golden.py, written by the unmodified reference)."""
+    from paper_2408_01331_b200 import Checkpoint, init_params, zoo
+
+    graph = zoo.mlp(12, (16,), 4, name="ckpt-mlp")
+    params = init_params(graph, 5)
+    m = {k: np.arange(v.size, dtype=np.float32).reshape(v.shape) * np.float32(0.001) for k, v in params.items()}
+    if kind == "adam":
+        ours = Checkpoint("job-a", 2, 2, "adam", 17, 0.0, params, slot_m=m, slot_v={k: a * a for k, a in m.items()})
+    else:
+        ours = Checkpoint("job-m", 1, 1, "sgd", 9, 0.9, params, slot_momentum=m)
+    golden = (GOLDEN / f"checkpoint_synthetic_{kind}.bin").read_bytes()
+    assert ours.encode() == golden
+    back = Checkpoint.decode(golden)
+    assert (back.job_id, back.completed_epochs, back.data_cursor, back.optimizer_kind, back.optimizer_step,
+            back.momentum) == (ours.job_id, ours.completed_epochs, ours.data_cursor, ours.optimizer_kind,
+                               ours.optimizer_step, ours.momentum)
+    for attr in ("params", "slot_m", "slot_v", "slot_momentum"):
+        a, b = getattr(back, attr), getattr(ours, attr)
+        assert sorted(a) == sorted(b) and all(np.array_equal(a[k], b[k]) for k in a), attr
+
+
+@pytest.mark.parametrize("kind", ["adam", "sgd"])
+def test_checkpoint_decode_reencodes_reference_bytes(kind):
+    from paper_2408_01331_b200 import Checkpoint
+
+    golden = (GOLDEN / f"checkpoint_paused_{kind}.bin").read_bytes()
+    ck = Checkpoint.decode(golden)
+    assert ck.completed_epochs == 1 and ck.data_cursor == 1 and ck.optimizer_kind == kind
+    assert ck.encode() == golden
+
+
+def test_checkpoint_decode_errors_match_reference():
+    from paper_2408_01331_b200 import Checkpoint, FormatError, StateError
+    from paper_2408_01331_b200 import formats
+
+    golden = (GOLDEN / "checkpoint_paused_sgd.bin").read_bytes()
+    with pytest.raises(FormatError, match="truncated container"):
+        Checkpoint.decode(golden[:-3])
+    with pytest.raises(FormatError, match="trailing bytes"):
+        Checkpoint.decode(golden + b"\x00")
+    with pytest.raises(FormatError, match="expected format version 3, got 2"):
+        Checkpoint.decode(golden[:4] + b"\x02\x00" + golden[6:])
+    bad = formats.encode_checkpoint({"job_id": "j", "completed_epochs": 0, "data_cursor": 0,
+                                     "optimizer": {"kind": "sgd", "step": 0, "momentum": 0.0}},
+                                    {"q/x": np.zeros(2, np.float32)}, ["q/x"])
+    with pytest.raises(StateError, match="unrecognized checkpoint section"):
+        Checkpoint.decode(bad)
+
+
+def test_host_gather_rows_matches_store_batches():
+    """hnn_host_gather_rows (the host-fed step's data loader) writes Batch(x=train_x[idx],
+    y=train_y[idx]) (src/store.py:77-80) into a strided arena, labels as int32; host code only."""
+    g = np.random.default_rng(3)
+    src = g.normal(size=(50, 7)).astype(np.float32)
+    ys = g.integers(0, 9, size=50).astype(np.float32)
+    idx = g.permutation(50)[:13].astype(np.int64)
+    ld = 8
+    dst = np.full((16, ld), -1.0, dtype=np.float32)
+    dy = np.full(16, -1, dtype=np.int32)
+    _native.call("hnn_host_gather_rows", dst.ctypes.data, ld, dy.ctypes.data, src.ctypes.data, 7, ys.ctypes.data,
+                 idx.ctypes.data, idx.size, 7)
+    assert np.array_equal(dst[:13, :7], src[idx]) and np.all(dst[:13, 7] == -1) and np.all(dst[13:] == -1)
+    assert np.array_equal(dy[:13], ys[idx].astype(np.int32)) and np.all(dy[13:] == -1)
+    with pytest.raises(h.DeviceError):
+        _native.call("hnn_host_gather_rows", dst.ctypes.data, 4, dy.ctypes.data, src.ctypes.data, 7, ys.ctypes.data,
+                     idx.ctypes.data, idx.size, 7)

@@ -69,3 +69,47 @@ def test_dataset_broadcast_and_metric_gather_with_gloo():
         assert np.array_equal(x, ref.train_x)
         assert np.array_equal(y, ref.train_y.astype(np.int32))
         assert gathered == {"m0": [1.5, 0.0, 64.0, 1.0], "m1": [2.5, 10.0, 64.0, 1.0]}
+
+
+def _datasets_worker(rank, world, port, blobs, out):
+    """Ranks ask for different dataset sets, in different orders; rank 1 holds one only as metadata."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2408_01331_b200.parallel import DatasetMeta
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    comm = RankGroup(rank, world, torch.device("cpu"))
+    a, b, c = (store.from_splits(s) for s in blobs)
+    if rank == 0:
+        mine = [b, a]
+    else:
+        mine = [c, DatasetMeta(a.content_hash, a.sample_count, a.test_x.shape[0], a.sample_shape)]
+    got = comm.share_datasets(mine, torch.device("cpu"))
+    out[rank] = {h: (d.train_x.numpy().copy(), d.train_y.numpy().copy(), d.test_x.numpy().copy()) for h, d in got.items()}
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_share_datasets_agrees_on_the_set_before_broadcasting():
+    """each rank must receive exactly the datasets it asked for, under their own hash,
+    whatever order the ranks list them in (src/store.py:55-56 content hashes)."""
+    import torch.multiprocessing as mp
+
+    blobs = [oracle.blob_splits("t", f"set{i}", 3, 5 + i, 12 + i, 4) for i in range(3)]
+    ref = [store.from_splits(s) for s in blobs]
+    with mp.Manager() as mgr:
+        out = mgr.dict()
+        mp.spawn(_datasets_worker, args=(2, _free_port(), blobs, out), nprocs=2, join=True)
+        res = dict(out)
+    a, b, c = ref
+    assert sorted(res[0]) == sorted([a.content_hash, b.content_hash])
+    assert sorted(res[1]) == sorted([a.content_hash, c.content_hash])
+    for rank, got in res.items():
+        for d in ref:
+            if d.content_hash in got:
+                x, y, tx = got[d.content_hash]
+                assert np.array_equal(x, d.train_x) and np.array_equal(tx, d.test_x)
+                assert np.array_equal(y, d.train_y.astype(np.int32))
+

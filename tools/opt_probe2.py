@@ -10,7 +10,8 @@ import bench
 from paper_2408_01331_b200 import _native as N
 
 torch.cuda.set_device(0)
-jobs, hy, dev, ddev, meta, ds, comm = bench.build_rank("c3", 0, 1, torch.device("cuda", 0))
+_, jobs, hy, dev, ddev, ds, comm = bench.build_rank("c3", 0, 1, torch.device("cuda", 0))
+meta = ds
 rows = bench.schedule(jobs, meta, 400)
 bench.upload_perms(dev, jobs, meta)
 dev.load_schedule(rows)

@@ -9,7 +9,8 @@ import torch
 import bench
 
 torch.cuda.set_device(0)
-jobs, hy, dev, ddev, meta, ds, comm = bench.build_rank("c2", 0, 1, torch.device("cuda", 0))
+_, jobs, hy, dev, ddev, ds, comm = bench.build_rank("c2", 0, 1, torch.device("cuda", 0))
+meta = ds
 rows = bench.schedule(jobs, meta, 20)
 bench.upload_perms(dev, jobs, meta)
 dev.load_schedule(rows)

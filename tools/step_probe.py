@@ -13,7 +13,8 @@ from paper_2408_01331_b200 import _native as N
 torch.cuda.set_device(0)
 dev_t = torch.device("cuda", 0)
 workload = sys.argv[1] if len(sys.argv) > 1 else "c3"
-jobs, hy, dev, ddev, meta, ds, comm = bench.build_rank(workload, 0, 1, dev_t)
+_, jobs, hy, dev, ddev, ds, comm = bench.build_rank(workload, 0, 1, dev_t)
+meta = ds
 rows = bench.schedule(jobs, meta, 200)
 bench.upload_perms(dev, jobs, meta)
 dev.load_schedule(rows)

@@ -16,7 +16,8 @@ import bench
 
 torch.cuda.set_device(0)
 wl = sys.argv[2] if len(sys.argv) > 2 else "c3"
-jobs, hy, dev, ddev, meta, ds, comm = bench.build_rank(wl, 0, 1, torch.device("cuda", 0))
+_, jobs, hy, dev, ddev, ds, comm = bench.build_rank(wl, 0, 1, torch.device("cuda", 0))
+meta = ds
 rows = bench.schedule(jobs, meta, 200)
 bench.upload_perms(dev, jobs, meta)
 dev.load_schedule(rows)
