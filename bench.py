@@ -221,7 +221,7 @@ class ClockSampler:
 # ----------------------------------------------------------------------------- GPU arm
 
 
-def build_rank(workload, rank, world, device):
+def build_rank(workload, rank, world, device, shard_of=None):
     """This rank's jobs (model-identity shard of the workload), hybrid, device dataset, plans."""
     from paper_2408_01331_b200 import merge
     from paper_2408_01331_b200.parallel import RankGroup, shard_jobs
@@ -235,8 +235,8 @@ def build_rank(workload, rank, world, device):
         from paper_2408_01331_b200.runtime import DeviceDataset
 
         ddev = DeviceDataset(ds, device)
-    all_jobs = workload_jobs(workload, ds, world)
-    jobs = shard_jobs(all_jobs, world)[rank]
+    all_jobs = workload_jobs(workload, ds, world if shard_of is None else shard_of[1])
+    jobs = shard_jobs(all_jobs, world)[rank] if shard_of is None else shard_jobs(all_jobs, shard_of[1])[shard_of[0]]
     hy = merge(jobs)
     # C4 is specified on bf16 tensor cores (BASELINE.json configs[3]); the other configs are fp32
     dev = hy.materialize(device, conv_precision="bf16" if workload == "c4" else "f32")
@@ -389,7 +389,8 @@ def gpu_arm(args):
             dist.init_process_group("gloo")
         else:
             dist.init_process_group("nccl", device_id=device)
-    all_jobs, jobs, hy, dev, ddev, ds, comm = build_rank(args.workload, rank, world, device)
+    shard_of = tuple(int(v) for v in args.shard.split("/")) if args.shard else None
+    all_jobs, jobs, hy, dev, ddev, ds, comm = build_rank(args.workload, rank, world, device, shard_of)
     meta = ds
     upload_perms(dev, jobs, meta)
     sync = lambda: (torch.cuda.synchronize(), dist.barrier() if world > 1 else None)
@@ -471,6 +472,7 @@ def gpu_arm(args):
                 "reference's keyed init",
         "config": bench_config(args.workload, all_jobs, world),
         "repeats": repeats, "timed_s": round(sum(times) / 1e3, 3),
+        **({"diagnostic_shard": args.shard, "shard_models": len(jobs)} if args.shard else {}),
         "repeat_ms": [round(t, 3) for t in times],
         "hbm_bytes_per_model": int((peak_alloc - ddev.nbytes) / n_models + ddev.nbytes / n_models),
         "reference_modeled_bytes_per_model": memory.reference_model_bytes(jobs),
@@ -532,6 +534,8 @@ def main():
     ap.add_argument("--min-seconds", type=float, default=1.0)
     ap.add_argument("--loader-threads", type=int, default=8)
     ap.add_argument("--no-cpu", action="store_true")
+    # diagnostic: time only shard R of an N-GPU run on this one GPU (per-GPU work at N GPUs)
+    ap.add_argument("--shard", default=None, metavar="R/N")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

@@ -388,6 +388,12 @@ int hnn_multi_tensor_adam(const hnn_opt_segment* segs, int nseg, int total_chunk
 #define HNN_CONVTC_PARITY_WEIGHTS 9   /* 3x3 / stride 2 / pad 1 input gradient as four stride-1 convs of dy:
                                          class q = ksplit (ph = q >> 1, pw = q & 1), taps rr < 1 + ph,
                                          ss < 1 + pw: bf16 wpad[c, (rr, ss, f)] = w[f, c, ph+1-2rr, pw+1-2ss] */
+#define HNN_CONVTC_SPLITK_FWD 10      /* finish a K-split forward-type conv GEMM (bf16 layers whose output tiles
+                                         fill few CTA pairs): for m = (b, hw) < cap*oh*ow, n < f:
+                                         v = sum_s partial[s*pix_ld + m][n] (splits in order) + db[n],
+                                         relu if rsc; dx[b, n, hw] = v, times (mask[b, n, hw] > 0) if mask;
+                                         rows past the step's batch are 0; dyt (bf16 [m, f]) = v if dyt.
+                                         One CTA per 32 pixels x 32 columns. */
 
 typedef struct hnn_convtc_problem {
   const float* x;    /* [cap, c, h, w] */

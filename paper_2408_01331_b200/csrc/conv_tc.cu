@@ -598,6 +598,60 @@ __global__ void __launch_bounds__(CT_THREADS) wt_weights_kernel(const hnn_convtc
   }
 }
 
+// K-split forward-type conv GEMM finish (HNN_CONVTC_SPLITK_FWD): the splits' raw sums, in order,
+// + bias, relu; written NCHW (and the NHWC bf16 copy for an implicit next layer) exactly like the
+// unsplit GEMM epilogue (gemm_tc2.cu, c_mode 1).  Phase 1 reads the partials along n (coalesced),
+// phase 2 writes NCHW along the pixels through a padded shared tile.
+constexpr int SK_BATCH = 4;  // partial loads in flight per element
+
+__global__ void __launch_bounds__(CT_THREADS) splitk_fwd_kernel(const hnn_convtc_problem* __restrict__ probs,
+                                                                int nprob, const hnn_step_row* __restrict__ cur,
+                                                                const hnn_model_status* __restrict__ status) {
+  hnn::pdl_wait();
+  const hnn_convtc_problem& p = ct_problem(probs, nprob, blockIdx.x);
+  if (!live(cur, status, p.model)) return;
+  __shared__ float tile[32][33];
+  const int t = blockIdx.x - p.block_base, nblk = (p.f + 31) / 32;
+  const int m0 = (t / nblk) * 32, n0 = (t % nblk) * 32;
+  const int hw = p.oh * p.ow, M = p.cap * hw, R = cur[p.model].rows * hw;
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+  const int n = n0 + tx;
+  const float bias = (p.db && n < p.f) ? __ldg(p.db + n) : 0.0f;
+  const size_t split = size_t(p.pix_ld) * p.f;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int r = ty + 8 * i, m = m0 + r;
+    float v = 0.0f;
+    if (m < R && n < p.f) {
+      const float* src = p.partial + size_t(m) * p.f + n;
+      v = __ldg(src);
+      for (int s0 = 1; s0 < p.ksplit; s0 += SK_BATCH) {
+        float q[SK_BATCH];
+#pragma unroll
+        for (int j = 0; j < SK_BATCH; ++j) q[j] = s0 + j < p.ksplit ? __ldg(src + (s0 + j) * split) : 0.0f;
+#pragma unroll
+        for (int j = 0; j < SK_BATCH; ++j)
+          if (s0 + j < p.ksplit) v = __fadd_rn(v, q[j]);
+      }
+      v = __fadd_rn(v, bias);
+      if (p.rsc) v = np_relu(v);
+    }
+    tile[r][tx] = v;
+    if (p.dyt && m < M && n < p.f) reinterpret_cast<__nv_bfloat16*>(p.dyt)[size_t(m) * p.f + n] = __float2bfloat16_rn(v);
+  }
+  __syncthreads();
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int c = ty + 8 * i, no = n0 + c, m = m0 + tx;
+    if (m >= M || no >= p.f) continue;
+    const int b = m / hw, pix = m - b * hw;
+    const size_t o = (size_t(b) * p.f + no) * hw + pix;
+    float v = tile[tx][c];
+    if (p.mask) v = m < R ? np_mask(v, __ldg(p.mask + o)) : 0.0f;
+    p.dx[o] = v;
+  }
+}
+
 }  // namespace hnn
 
 extern "C" int hnn_conv_tc_aux(int op, const hnn_convtc_problem* probs, int nprob, int total_blocks, int max_k,
@@ -635,6 +689,9 @@ extern "C" int hnn_conv_tc_aux(int op, const hnn_convtc_problem* probs, int npro
       break;
     case HNN_CONVTC_WT_WEIGHTS:
       hnn::launch_pdl(hnn::wt_weights_kernel, dim3(total_blocks), dim3(hnn::CT_THREADS), 0, s, probs, nprob, cur, status);
+      break;
+    case HNN_CONVTC_SPLITK_FWD:
+      hnn::launch_pdl(hnn::splitk_fwd_kernel, dim3(total_blocks), dim3(hnn::CT_THREADS), 0, s, probs, nprob, cur, status);
       break;
     case HNN_CONVTC_WGRAD_REDUCE:
       hnn::launch_pdl(hnn::wgrad_reduce_kernel, dim3(total_blocks), dim3(hnn::CT_THREADS), 0, s, probs, nprob, cur, status);

@@ -23,7 +23,7 @@ constexpr int FWD_ROWS = HNN_SKINNY_FWD_ROWS;  // rows per warp; tile = 8 warps 
 #define HNN_SKINNY_DG_ROWS 8
 #endif
 constexpr int DG_ROWS = HNN_SKINNY_DG_ROWS;  // DGRAD rows per thread; tile = 8 row groups x 8 rows x 128 columns
-constexpr int WG_QUADS = 64; // WGRAD column quads per CTA; tile = 256 columns, 4 row quarters
+constexpr int WG_QUADS = 32; // WGRAD column quads per CTA; tile = 128 columns, 8 row groups
 
 __device__ __forceinline__ float4 ldg4(const float* p) { return __ldg(reinterpret_cast<const float4*>(p)); }
 
@@ -115,6 +115,7 @@ __global__ void __launch_bounds__(KTHREADS) skinny_fwd_kernel(const hnn_gemm_pro
   // CTA-uniform dispatch on the column count: loads and FMAs carry no per-column branches
   if (p.n <= 4) rowdot_rows<4>(p, r0, rows, lane);
   else if (p.n <= 8) rowdot_rows<8>(p, r0, rows, lane);
+  else if (p.n <= 10) rowdot_rows<10>(p, r0, rows, lane);
   else if (p.n <= 12) rowdot_rows<12>(p, r0, rows, lane);
   else rowdot_rows<16>(p, r0, rows, lane);
 }
@@ -125,36 +126,41 @@ __device__ __forceinline__ void outer_rows(const hnn_gemm_problem& p, int r0, in
   float4 w[KJ];
 #pragma unroll
   for (int j = 0; j < KJ; ++j) w[j] = j < p.k ? ldg4(p.b + size_t(j) * p.ldb + col) : make_float4(0, 0, 0, 0);
-  // the relu-mask quads of all DG_ROWS rows are requested together (one round trip, not four)
-  float4 mk[DG_ROWS];
+  // the relu-mask quads of MK rows are requested together (one round trip per MK rows); four for
+  // the 16-row W, whose quads already hold 64 registers
+  constexpr int MK = KJ > 12 ? 4 : DG_ROWS;
 #pragma unroll
-  for (int i = 0; i < DG_ROWS; ++i) {
-    const int r = r0 + i;
-    mk[i] = (p.mask && r < rows && r < p.m) ? ldg4(p.mask + size_t(r) * p.ldc + col) : make_float4(1, 1, 1, 1);
-  }
+  for (int h = 0; h < DG_ROWS; h += MK) {
+    float4 mk[MK];
 #pragma unroll
-  for (int i = 0; i < DG_ROWS; ++i) {
-    const int r = r0 + i;
-    if (r >= p.m) break;
-    float4 o = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
-    if (r < rows) {
-      const float* dy = dys + (threadIdx.x >> 5) * DG_ROWS * 16 + i * 16;  // staged dy row (shared)
-#pragma unroll
-      for (int j = 0; j < KJ; ++j) {
-        const float d = dy[j];
-        o.x = fmaf(d, w[j].x, o.x);
-        o.y = fmaf(d, w[j].y, o.y);
-        o.z = fmaf(d, w[j].z, o.z);
-        o.w = fmaf(d, w[j].w, o.w);
-      }
-      if (p.mask) {
-        o.x = np_mask(o.x, mk[i].x);
-        o.y = np_mask(o.y, mk[i].y);
-        o.z = np_mask(o.z, mk[i].z);
-        o.w = np_mask(o.w, mk[i].w);
-      }
+    for (int i = 0; i < MK; ++i) {
+      const int r = r0 + h + i;
+      mk[i] = (p.mask && r < rows && r < p.m) ? ldg4(p.mask + size_t(r) * p.ldc + col) : make_float4(1, 1, 1, 1);
     }
-    *reinterpret_cast<float4*>(p.c + size_t(r) * p.ldc + col) = o;
+#pragma unroll
+    for (int i = 0; i < MK; ++i) {
+      const int r = r0 + h + i;
+      if (r >= p.m) break;
+      float4 o = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
+      if (r < rows) {
+        const float* dy = dys + (threadIdx.x >> 5) * DG_ROWS * 16 + (h + i) * 16;  // staged dy row (shared)
+#pragma unroll
+        for (int j = 0; j < KJ; ++j) {
+          const float d = dy[j];
+          o.x = fmaf(d, w[j].x, o.x);
+          o.y = fmaf(d, w[j].y, o.y);
+          o.z = fmaf(d, w[j].z, o.z);
+          o.w = fmaf(d, w[j].w, o.w);
+        }
+        if (p.mask) {
+          o.x = np_mask(o.x, mk[i].x);
+          o.y = np_mask(o.y, mk[i].y);
+          o.z = np_mask(o.z, mk[i].z);
+          o.w = np_mask(o.w, mk[i].w);
+        }
+      }
+      *reinterpret_cast<float4*>(p.c + size_t(r) * p.ldc + col) = o;
+    }
   }
 }
 
@@ -185,18 +191,24 @@ __global__ void __launch_bounds__(KTHREADS) skinny_dgrad_kernel(const hnn_gemm_p
   if (col >= p.n || r0 >= p.m) return;  // n is a multiple of 4 (host routing)
   if (p.k <= 4) outer_rows<4>(p, r0, col, rows, dys);
   else if (p.k <= 8) outer_rows<8>(p, r0, col, rows, dys);
+  else if (p.k <= 10) outer_rows<10>(p, r0, col, rows, dys);
   else if (p.k <= 12) outer_rows<12>(p, r0, col, rows, dys);
   else outer_rows<16>(p, r0, col, rows, dys);
 }
 
 // ---------------------------------------------------------------------------------------- WGRAD
+// CTA = WG_QUADS column quads x WG_GROUPS row groups (256 threads); each thread accumulates its
+// quad over its group's rows (8 x rows in flight), the groups are summed in fixed order through
+// shared memory.  128-column tiles and 8 groups (272 CTAs on C3, 3 per SM) instead of 256 columns
+// x 4 groups (144 CTAs at one per SM: ncu 10% occupancy, L1TEX-latency bound).
 constexpr int WG_CHUNK = 256;  // dy rows staged in shared memory per pass ([256][16] floats)
+constexpr int WG_GROUPS = KTHREADS / WG_QUADS;
 
 template <int MJ>
 __device__ __forceinline__ void colacc(const hnn_gemm_problem& p, int col, int r_lo, int r_hi, int base,
-                                       float (&part)[16][4], const float* dys) {
+                                       float (&part)[MJ][4], const float* dys) {
   const float* x = p.b + col;
-#pragma unroll 8  // (eight rows of x in flight per thread: one CTA per SM on C3)
+#pragma unroll 8  // (eight rows of x in flight per thread)
   for (int r = r_lo; r < r_hi; ++r) {
     const float4 xv = ldg4(x + size_t(r) * p.ldb);
     const float* d = dys + (r - base) * 16;
@@ -210,27 +222,15 @@ __device__ __forceinline__ void colacc(const hnn_gemm_problem& p, int col, int r
   }
 }
 
-__global__ void __launch_bounds__(KTHREADS) skinny_wgrad_kernel(const hnn_gemm_problem* __restrict__ probs, int nprob,
-                                                                const hnn_step_row* __restrict__ cur,
-                                                                const hnn_model_status* __restrict__ status) {
-  hnn::pdl_wait();
-  extern __shared__ __align__(16) float wg_smem[];
-  float* dys = wg_smem;                   // [WG_CHUNK][16] staged dy rows (zero padded)
-  float* red = wg_smem + WG_CHUNK * 16;   // [3][WG_QUADS][16][4] partials of row quarters 1..3
-  const int pi = find_problem(probs, nprob, blockIdx.x, [](const hnn_gemm_problem& q) { return q.tile_base; });
-  const hnn_gemm_problem& p = probs[pi];
-  if (!live(cur, status, p.model)) return;
-  const int rows = cur[p.model].rows;
-  const int n0 = (blockIdx.x - p.tile_base) * (4 * WG_QUADS);
-  const int qd = threadIdx.x % WG_QUADS, q = threadIdx.x / WG_QUADS;
-  const int col = n0 + qd * 4;
-  const bool active = col < p.n;  // n is a multiple of 4 (host routing)
-  const bool bias_thread = n0 == 0 && threadIdx.x < p.m && (p.dbias || p.opt_b);
-  float part[16][4];
+template <int MJ>
+__device__ __forceinline__ void wgrad_tile(const hnn_gemm_problem& p, const hnn_step_row& row, int col, bool active,
+                                           int q, int qd, float* dys, float* red, bool bias_thread) {
+  const int rows = row.rows;
+  float part[MJ][4];
 #pragma unroll
-  for (int j = 0; j < 16; ++j) part[j][0] = part[j][1] = part[j][2] = part[j][3] = 0.0f;
+  for (int j = 0; j < MJ; ++j) part[j][0] = part[j][1] = part[j][2] = part[j][3] = 0.0f;
   float bsum = -0.0f;
-  // fixed decomposition: 256-row chunks in order; inside a chunk, row quarter q of each thread
+  // fixed decomposition: 256-row chunks in order; inside a chunk, row group q of each thread
   for (int base = 0; base < rows; base += WG_CHUNK) {
     const int n = min(WG_CHUNK, rows - base);
     __syncthreads();
@@ -241,18 +241,12 @@ __global__ void __launch_bounds__(KTHREADS) skinny_wgrad_kernel(const hnn_gemm_p
     __syncthreads();
     if (bias_thread)  // numpy's axis-0 sum: sequential row order per column
       for (int r = 0; r < n; ++r) bsum = __fadd_rn(bsum, dys[r * 16 + threadIdx.x]);
-    if (active) {
-      const int lo = base + (n * q) / 4, hi = base + (n * (q + 1)) / 4;
-      if (p.m <= 4) colacc<4>(p, col, lo, hi, base, part, dys);
-      else if (p.m <= 8) colacc<8>(p, col, lo, hi, base, part, dys);
-      else if (p.m <= 12) colacc<12>(p, col, lo, hi, base, part, dys);
-      else colacc<16>(p, col, lo, hi, base, part, dys);
-    }
+    if (active) colacc<MJ>(p, col, base + (n * q) / WG_GROUPS, base + (n * (q + 1)) / WG_GROUPS, base, part, dys);
   }
   if (bias_thread) {
     if (p.dbias) p.dbias[threadIdx.x] = bsum;
     if (p.opt_b) {
-      const Update u = make_update(cur[p.model], p.opt_kind, p.opt_momentum);
+      const Update u = make_update(row, p.opt_kind, p.opt_momentum);
       const int i = threadIdx.x;
       float w = p.opt_b[i], m = p.opt_bm ? p.opt_bm[i] : 0.0f, v = p.opt_bv ? p.opt_bv[i] : 0.0f;
       update_one(u, w, bsum, m, v);
@@ -264,17 +258,16 @@ __global__ void __launch_bounds__(KTHREADS) skinny_wgrad_kernel(const hnn_gemm_p
   if (q > 0) {
     float* dst = red + (size_t(q - 1) * WG_QUADS + qd) * 64;
 #pragma unroll
-    for (int j = 0; j < 16; ++j)
+    for (int j = 0; j < MJ; ++j)
       *reinterpret_cast<float4*>(dst + j * 4) = make_float4(part[j][0], part[j][1], part[j][2], part[j][3]);
   }
   __syncthreads();
   if (q != 0 || !active) return;
-  // quarters summed in fixed order 0 + 1 + 2 + 3
+  // row groups summed in fixed order 0 + 1 + ... + WG_GROUPS-1
+  for (int g = 0; g < WG_GROUPS - 1; ++g) {
+    const float* src = red + (size_t(g) * WG_QUADS + qd) * 64;
 #pragma unroll
-  for (int s = 0; s < 3; ++s) {
-    const float* src = red + (size_t(s) * WG_QUADS + qd) * 64;
-#pragma unroll
-    for (int j = 0; j < 16; ++j) {
+    for (int j = 0; j < MJ; ++j) {
       const float4 v = *reinterpret_cast<const float4*>(src + j * 4);
       part[j][0] += v.x;
       part[j][1] += v.y;
@@ -282,9 +275,9 @@ __global__ void __launch_bounds__(KTHREADS) skinny_wgrad_kernel(const hnn_gemm_p
       part[j][3] += v.w;
     }
   }
-  const Update u = make_update(cur[p.model], p.opt_kind, p.opt_momentum);
+  const Update u = make_update(row, p.opt_kind, p.opt_momentum);
 #pragma unroll
-  for (int j = 0; j < 16; ++j) {
+  for (int j = 0; j < MJ; ++j) {
     if (j >= p.m) break;
     const size_t off = size_t(j) * p.ldc + col;
     if (p.c) *reinterpret_cast<float4*>(p.c + off) = make_float4(part[j][0], part[j][1], part[j][2], part[j][3]);
@@ -303,6 +296,28 @@ __global__ void __launch_bounds__(KTHREADS) skinny_wgrad_kernel(const hnn_gemm_p
   }
 }
 
+__global__ void __launch_bounds__(KTHREADS) skinny_wgrad_kernel(const hnn_gemm_problem* __restrict__ probs, int nprob,
+                                                                const hnn_step_row* __restrict__ cur,
+                                                                const hnn_model_status* __restrict__ status) {
+  hnn::pdl_wait();
+  extern __shared__ __align__(16) float wg_smem[];
+  float* dys = wg_smem;                   // [WG_CHUNK][16] staged dy rows (zero padded)
+  float* red = wg_smem + WG_CHUNK * 16;   // [WG_GROUPS - 1][WG_QUADS][16][4] partials of groups 1..
+  const int pi = find_problem(probs, nprob, blockIdx.x, [](const hnn_gemm_problem& q) { return q.tile_base; });
+  const hnn_gemm_problem& p = probs[pi];
+  if (!live(cur, status, p.model)) return;
+  const int n0 = (blockIdx.x - p.tile_base) * (4 * WG_QUADS);
+  const int qd = threadIdx.x % WG_QUADS, q = threadIdx.x / WG_QUADS;
+  const int col = n0 + qd * 4;
+  const bool active = col < p.n;  // n is a multiple of 4 (host routing)
+  const bool bias_thread = n0 == 0 && threadIdx.x < p.m && (p.dbias || p.opt_b);
+  if (p.m <= 4) wgrad_tile<4>(p, cur[p.model], col, active, q, qd, dys, red, bias_thread);
+  else if (p.m <= 8) wgrad_tile<8>(p, cur[p.model], col, active, q, qd, dys, red, bias_thread);
+  else if (p.m <= 10) wgrad_tile<10>(p, cur[p.model], col, active, q, qd, dys, red, bias_thread);
+  else if (p.m <= 12) wgrad_tile<12>(p, cur[p.model], col, active, q, qd, dys, red, bias_thread);
+  else wgrad_tile<16>(p, cur[p.model], col, active, q, qd, dys, red, bias_thread);
+}
+
 int skinny_tile_shape(int op, int32_t* tm, int32_t* tn) {
   if (op == HNN_FWD) { *tm = 8 * FWD_ROWS; *tn = 16; }
   else if (op == HNN_DGRAD) { *tm = 8 * DG_ROWS; *tn = 128; }
@@ -317,7 +332,7 @@ int grouped_gemm_skinny(int op, const hnn_gemm_problem* probs, int nprob, int to
   } else if (op == HNN_DGRAD) {
     hnn::launch_pdl(skinny_dgrad_kernel, dim3(total_tiles), dim3(KTHREADS), 0, s, probs, nprob, cur, status);
   } else {
-    constexpr int smem = (WG_CHUNK * 16 + 3 * WG_QUADS * 64) * 4;  // 64 KB
+    constexpr int smem = (WG_CHUNK * 16 + (WG_GROUPS - 1) * WG_QUADS * 64) * 4;  // 72 KB
     static bool configured = false;
     if (!configured) {
       cudaFuncSetAttribute(skinny_wgrad_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);

@@ -327,6 +327,10 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
 
 // dbias[i] = sum_{r<R} A[r*lda + i], sequential row order (numpy's axis-0 sum), one thread per
 // column; with optimizer fusion the bias is updated here too.
+#ifndef HNN_COLSUM_ROWS
+#define HNN_COLSUM_ROWS 128
+#endif
+constexpr int COLSUM_ROWS = HNN_COLSUM_ROWS;
 __global__ void colsum_kernel(const hnn_gemm_problem* __restrict__ probs, int nprob, const hnn_step_row* __restrict__ cur,
                               const hnn_model_status* __restrict__ status) {
   hnn::pdl_wait();
@@ -335,11 +339,20 @@ __global__ void colsum_kernel(const hnn_gemm_problem* __restrict__ probs, int np
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= p.m) return;
   const int R = cur[p.model].rows * p.row_mult;
-  // loads of 32 rows issue before their (sequential, order-preserving) adds: the loop is
-  // latency-bound otherwise (58 us per C3 launch at one load in flight per thread)
+  // loads of COLSUM_ROWS rows issue before their (sequential, order-preserving) adds: the loop is
+  // latency-bound otherwise (58 us per C3 launch at one load in flight per thread, 21.7 us at 32
+  // rows: one thread per column leaves ~7 warps per SM, so each thread must keep many loads in
+  // flight)
   float acc = -0.0f;
   const float* col = p.a + i;
   int r = 0;
+  for (; r + COLSUM_ROWS <= R; r += COLSUM_ROWS) {
+    float v[COLSUM_ROWS];
+#pragma unroll
+    for (int j = 0; j < COLSUM_ROWS; ++j) v[j] = __ldg(col + size_t(r + j) * p.lda);
+#pragma unroll
+    for (int j = 0; j < COLSUM_ROWS; ++j) acc = __fadd_rn(acc, v[j]);
+  }
   for (; r + 32 <= R; r += 32) {
     float v[32];
 #pragma unroll

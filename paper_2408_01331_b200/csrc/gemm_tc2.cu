@@ -31,8 +31,9 @@
 //   warps 2,3    converters: lo ring from the raw ring, then arrive on the leader
 //   warps 4..11  accumulators: promotion + epilogue (bias / relu / relu-mask / zero rows) of
 //                this CTA's 128 rows, TMA stores; WGRAD optimizer fusion as in gemm_tc.cu
-// Each ring stage holds a K block's raw tiles and their lo tiles, so a converter can work as
-// soon as its raw tiles land (up to two K blocks ahead of the MMAs).
+// The raw ring (TC2_RAW K blocks) and the lo ring (TC2_LO) are separate: TMA refills a raw slot
+// when the MMAs reading it complete; a converter writes a lo slot once its raw tiles have landed
+// and the lo slot's previous MMAs are done (up to TC2_LO - 1 K blocks ahead of the MMAs).
 // Barriers: raw full/empty, acc full: per CTA (the leader's commits multicast to both);
 // lo full and acc empty: in the leader, arrived on by both CTAs.
 #include <cuda_bf16.h>
@@ -44,7 +45,15 @@ namespace hnn {
 constexpr int TC2_BM = 128;                // rows per CTA (pair tile: 256)
 constexpr int TC2_BN = 256;                // pair tile columns (each CTA stages 128 of B)
 constexpr int TC2_BK = 32;
-constexpr int TC2_STAGES = 3;  // each stage: raw A | raw B | lo A | lo B (64 KB)
+constexpr int TC2_STAGES = 3;  // ring bytes = 2 * TC2_STAGES * 32 KB (raw A | raw B and lo A | lo B halves)
+// fp32: the raw tiles (TMA) and their lo tiles (converters) live in separate rings, deeper for raw:
+// a raw slot is refilled as soon as the MMAs that read it complete, so TMA runs TC2_RAW K blocks
+// ahead of the tensor core instead of the two a shared raw+lo stage allowed
+#ifndef HNN_TC2_RAW_STAGES
+#define HNN_TC2_RAW_STAGES 4
+#endif
+constexpr int TC2_RAW = HNN_TC2_RAW_STAGES, TC2_LO = 2 * TC2_STAGES - TC2_RAW;
+static_assert(TC2_RAW >= 2 && TC2_LO >= 2, "raw / lo ring depths");
 #ifndef HNN_TC2_CONV_WARPS
 #define HNN_TC2_CONV_WARPS 2
 #endif
@@ -186,7 +195,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC2_THREADS, 1)
   // bf16 stages carry no lo half: twice as many of them in the same shared memory, i.e. twice the
   // bytes in flight for the HBM-streaming conv GEMMs (a 64-filter layer's MMA needs 20 KB per
   // 128 clocks per CTA, so these launches are bound by the TMA pipeline depth)
-  constexpr int SR = BF16 ? 2 * TC2_STAGES : TC2_STAGES;
+  constexpr int SR = BF16 ? 2 * TC2_STAGES : TC2_RAW;  // raw ring depth
+  constexpr int SL = BF16 ? SR : TC2_LO;               // lo ring (bf16: the converters' per-stage relay)
   extern __shared__ uint8_t smem_raw[];
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const uint32_t rank = cluster_rank();
@@ -198,12 +208,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC2_THREADS, 1)
 
   uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const uint32_t raw_base = smem_u32(base);
-  constexpr int SSTRIDE = BF16 ? TC2_STAGE : 2 * TC2_STAGE;  // stage s: raw at s * SSTRIDE (fp32: lo after it)
-  const uint32_t epi_base = raw_base + SR * SSTRIDE;
-  uint8_t* tail = base + SR * SSTRIDE + TC2_EPI_BYTES;  // 1 KB: barriers, TMEM address, tile-info ring
+  // raw slot s at raw_base + s * TC2_STAGE; (fp32) lo slot l at raw_base + (SR + l) * TC2_STAGE
+  const uint32_t epi_base = raw_base + 2 * TC2_STAGES * TC2_STAGE;
+  uint8_t* tail = base + 2 * TC2_STAGES * TC2_STAGE + TC2_EPI_BYTES;  // 1 KB: barriers, TMEM address, tile-info ring
   uint64_t* bars = reinterpret_cast<uint64_t*>(tail);
-  constexpr int RAW_FULL = 0, RAW_EMPTY = SR, LO_FULL = 2 * SR;
-  constexpr int ACC_FULL = 3 * SR, ACC_EMPTY = ACC_FULL + 2, INFO_FULL = ACC_EMPTY + 2,
+  constexpr int RAW_FULL = 0, RAW_EMPTY = SR, LO_FULL = 2 * SR, LO_EMPTY = 2 * SR + SL;
+  constexpr int ACC_FULL = 2 * SR + 2 * SL, ACC_EMPTY = ACC_FULL + 2, INFO_FULL = ACC_EMPTY + 2,
                 INFO_EMPTY = INFO_FULL + TC2_INFO_RING, NBARS = INFO_EMPTY + TC2_INFO_RING;
   static_assert(NBARS * 8 <= 512, "barrier area");
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tail + 512);
@@ -214,8 +224,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC2_THREADS, 1)
   if (threadIdx.x == 0) {
     for (int s = 0; s < SR; ++s) {
       mbar_init(bar(RAW_FULL + s), 1);                  // local TMA expect_tx arrival + bytes
-      mbar_init(bar(RAW_EMPTY + s), 1);                 // leader MMA commit (multicast): stage free
-      mbar_init(bar(LO_FULL + s), 2 * TC2_CONV_WARPS);  // converter warps of both CTAs (leader's copy)
+      mbar_init(bar(RAW_EMPTY + s), 1);                 // leader MMA commit (multicast): raw slot free
+    }
+    for (int l = 0; l < SL; ++l) {
+      mbar_init(bar(LO_FULL + l), 2 * TC2_CONV_WARPS);  // converter warps of both CTAs (leader's copy)
+      mbar_init(bar(LO_EMPTY + l), 1);                  // (fp32) leader MMA commit (multicast): lo slot free
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(bar(ACC_FULL + b), 1);    // leader MMA commit (multicast)
@@ -324,7 +337,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC2_THREADS, 1)
           TC2_T0(t3);
           if (kg >= SR) mbar_wait(bar(RAW_EMPTY + s), ((kg / SR) - 1) & 1);
           TC2_T1(t3, 3);
-          const uint32_t st = raw_base + s * SSTRIDE;
+          const uint32_t st = raw_base + s * TC2_STAGE;
           mbar_expect_tx(bar(RAW_FULL + s), stage_bytes);
           const int k0 = kofs + kb * KBE;
           if (A_MN) {
@@ -333,10 +346,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC2_THREADS, 1)
           } else if (BF16 && OP == HNN_FWD && p->im_c > 0) {
             // implicit-GEMM convolution: K block kb = tap (r, s) x 64 channels of the NHWC input,
             // this CTA's 128 output pixels = whole output rows (or images) starting at (b0, oh0)
+            // (a split-K tile starts at K block kofs / 64 of the whole problem)
             const int kw = p->im_kw > 0 ? p->im_kw : p->im_k;
-            const int cbk = p->im_c / 64, tap = kb / cbk, r = tap / kw, sx = tap - r * kw;
+            const int kbg = kb + kofs / 64, cbk = p->im_c / 64, tap = kbg / cbk, r = tap / kw, sx = tap - r * kw;
             const int hw = p->im_oh * p->im_ow, b0 = am / hw, oh0 = (am - b0 * hw) / p->im_ow;
-            tma_load_4d(st, p->tmap_a, bar(RAW_FULL + s), (kb - tap * cbk) * 64, sx - p->im_pad, oh0 + r - p->im_pad, b0);
+            tma_load_4d(st, p->tmap_a, bar(RAW_FULL + s), (kbg - tap * cbk) * 64, sx - p->im_pad, oh0 + r - p->im_pad, b0);
           } else {
             tma_load_2d(st, p->tmap_a, bar(RAW_FULL + s), k0, am);
           }
@@ -382,12 +396,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC2_THREADS, 1)
           TC2_T0(t1);
           if (in_chunk == 0 && cg >= 2) mbar_wait(bar(ACC_EMPTY + buf), ((cg >> 1) - 1) & 1);  // promoted
           TC2_T1(t1, 1);
-          const int s = kg % SR;
-          const uint32_t a_hi = raw_base + s * SSTRIDE, b_hi = a_hi + TC2_A_BYTES;
-          const uint32_t a_lo = a_hi + TC2_STAGE, b_lo = a_lo + TC2_A_BYTES;
+          const int s = kg % SR, l = kg % SL;
+          const uint32_t a_hi = raw_base + s * TC2_STAGE, b_hi = a_hi + TC2_A_BYTES;
+          const uint32_t a_lo = raw_base + (SR + l) * TC2_STAGE, b_lo = a_lo + TC2_A_BYTES;
           const uint32_t acc = tmem + buf * TC2_BN;
           TC2_T0(t0);
-          mbar_wait(bar(LO_FULL + s), (kg / SR) & 1);  // both CTAs: raw landed, lo written
+          mbar_wait(bar(LO_FULL + l), (kg / SL) & 1);  // both CTAs: raw landed, lo written
           TC2_T1(t0, 0);
           tc_fence_after();
           if (BF16) {
@@ -425,7 +439,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC2_THREADS, 1)
             }
 #endif
           }
-          mma_commit_pair(bar(RAW_EMPTY + s));  // raw and lo of stage s consumed
+          mma_commit_pair(bar(RAW_EMPTY + s));  // raw slot s consumed
+          if (!BF16) mma_commit_pair(bar(LO_EMPTY + l));  // lo slot l consumed
           TC2_T1(t0, 5);
           if ((!BF16 && in_chunk == ckb - 1) || kb == nkb - 1) {
             mma_commit_pair(bar(ACC_FULL + buf));
@@ -448,11 +463,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC2_THREADS, 1)
                : !tile_info(tile, p, m0, n0, nkb, rows, kofs, sp, tn))
           continue;
       for (int kb = 0; kb < nkb; ++kb, ++kg) {
-        const int s = kg % SR;
+        const int s = kg % SR, l = kg % SL;
         TC2_T0(t2);
-        mbar_wait(bar(RAW_FULL + s), (kg / SR) & 1);  // (the stage's lo is free: TMA reused it)
+        mbar_wait(bar(RAW_FULL + s), (kg / SR) & 1);
+        if (!BF16 && kg >= SL) mbar_wait(bar(LO_EMPTY + l), ((kg / SL) - 1) & 1);  // lo slot's MMAs done
         TC2_T1(t2, 2);
-        const uint32_t hi = raw_base + s * SSTRIDE, lo = hi + TC2_STAGE;
+        const uint32_t hi = raw_base + s * TC2_STAGE, lo = raw_base + (SR + l) * TC2_STAGE;
         const int n16 = BF16 ? 0 : (TC2_A_BYTES + (tn / 2) * TC2_BK * 4) / 16;  // A + B-half 16-byte chunks
 #pragma unroll
         for (int h = 0; h < NPART; ++h) {
@@ -474,7 +490,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC2_THREADS, 1)
         }
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         __syncwarp();
-        if (lane == 0) mbar_arrive_cluster(lo_full_leader + 8 * s);
+        if (lane == 0) mbar_arrive_cluster(lo_full_leader + 8 * l);
       }
     }
   } else {

@@ -304,6 +304,56 @@ def C_addr_bytes(buf: bytearray) -> int:
     return ctypes.addressof((ctypes.c_char * len(buf)).from_buffer(buf))
 
 
+_TF32_CHECKED: set = set()
+
+
+def tf32_truncation_selftest(device) -> float:
+    """Assert the hardware fact the 3xTF32 GEMMs rely on (gemm_tc2.cu:11-13): a kind::tf32 MMA fed
+    raw fp32 operands uses their TRUNCATED tf32 value, so hi = x (no conversion) and the converters'
+    lo = x - trunc_tf32(x) add back to x exactly.  One 64 x 64 x 64 pair-GEMM forward on operands
+    x = 1 + 2^-11 + 2^-12 (truncation gives hi = 1, round-to-nearest would give 1 + 2^-10): the
+    3xTF32 result is 64 x^2 to 5.4e-7 (the dropped lo*lo term) when the hardware truncates and off by
+    2^-9 when it rounds.  Runs once per device and process (DeviceHybrid construction); raises
+    DeviceError if the assumption fails.  Returns the measured relative error."""
+    torch = _torch()
+    key = str(device)
+    if key in _TF32_CHECKED:
+        return 0.0
+    _TF32_CHECKED.add(key)  # (the probe hybrid below must not recurse into the check)
+    from . import zoo
+    from .unify import merge
+
+    x = 1.0 + 2.0 ** -11 + 2.0 ** -12
+    job = zoo.TrainingJob("tf32-selftest", zoo.mlp(64, (64,), 16), "-", zoo.HyperParams(1, 64, 1.0), 0, 0)
+    dev = merge([job]).materialize(device)
+    s = dev.slots[0]
+    st = s.stages[0]
+    dev.upload_params(0, {pid: np.full(shp, x if pid.endswith("weight") else 0.0, np.float32)
+                          for pid, shp in s.specs.items()})
+    fake = DeviceDataset.from_tensors("-", torch.zeros(64, 64, device=dev.device), torch.zeros(64, dtype=torch.int32,
+                                      device=dev.device), torch.zeros(1, 64, device=dev.device),
+                                      torch.zeros(1, dtype=torch.int32, device=dev.device), 0, dev.device)
+    dev.bind_datasets([fake], 64)
+    dev.build_plans()
+    probe = [l for l in dev.forward_plan if l.label.startswith("fwd0/dense/")]  # (+ a split-K epilogue)
+    if not any(l.label == "fwd0/dense/tc2" for l in probe):  # tensor cores routed off: nothing to check
+        return 0.0
+    rows = np.zeros((1, 1), dtype=STEP_DTYPE)
+    rows["active"], rows["rows"] = 1, 64
+    dev.load_schedule(rows)
+    s.batch_x.fill_(x)
+    dev.run_plan(probe)
+    got = st.y[:, :64].double().cpu().numpy()
+    err = float(np.max(np.abs(got - 64.0 * x * x)) / (64.0 * x * x))
+    if not np.isfinite(err) or err > 1e-5:
+        from .errors import DeviceError
+
+        raise DeviceError("tf32_truncation_selftest", -1,
+                          f"3xTF32 GEMM error {err:.2e} on operands with sub-tf32 bits: the tensor core does not "
+                          "truncate raw fp32 operands to tf32 as gemm_tc2.cu assumes (expected <= 1e-5)")
+    return err
+
+
 class DeviceHybrid:
     """Packed device state + launch plans for the models of one rank."""
 
@@ -364,6 +414,8 @@ class DeviceHybrid:
         self.forward_plan: list = []
         self.graph = None
         self.datasets = {}
+        if self.use_tc and self.use_pairs:
+            tf32_truncation_selftest(self.device)
 
     # ------------------------------------------------------------------ buffers
     def _bind_buffers(self):
@@ -928,7 +980,7 @@ class DeviceHybrid:
         if cols:
             out.append(self._aux_table(N.CONVTC_IM2COL, cols, f"{label}/tc/im2col_dy",
                                        lambda pr: -(-(pr.cap * pr.oh * pr.ow) // 32) * -(-pr.c // 32), max_k))
-        by_prec = {}
+        by_prec, fins = {}, []
         for s, st in items:
             c, h, w = st.in_shape
             f, oh, ow = self._conv_out(st)
@@ -941,9 +993,14 @@ class DeviceHybrid:
             if st.im_dg:  # conv of the NHWC dy, pad k-1-p, onto the h x w input grid
                 d.update(a=_ptr(st.dyt), lda=st.fld, im_c=f, im_k=k, im_pad=k - 1 - st.attrs.get("padding", 0),
                          im_h=oh, im_w=ow, im_oh=h, im_ow=w, im_n=s.batch_size)
+            d, fin = self._fwd_split(s, st, d)
+            if fin is not None:
+                fins.append(fin)
             by_prec.setdefault(N.PREC_BF16_PAIR if st.bf16 else N.PREC_3XTF32_PAIR, []).append((s, d))
         for prec, rows in by_prec.items():
             out += self._emit_gemm(N.HNN_FWD, prec, rows, f"{label}/tc/dgfwd")
+        if fins:
+            out.append(self._splitk_finish(fins, f"{label}/tc/dgfwd/splitk"))
         return out
 
     def _aux_table(self, aux, probs_by_slot, label, blocks_of, max_k):
@@ -956,6 +1013,53 @@ class DeviceHybrid:
         t = _dev_table(N.ConvTcProblem, probs, self.device)
         return Launch("hnn_conv_tc_aux", (aux, _ptr(t), len(probs), base, max_k, _ptr(self.cur), _ptr(self.status)),
                       t, label)
+
+    def _fwd_split(self, s, st, d):
+        """K split of a bf16 forward-type conv GEMM whose output tiles fill few CTA pairs (ResNet /
+        VGG layers at 8x8 and below: 4-32 tiles of 256 x n for 74 pairs, K up to 4608).  A fixed
+        function of the problem's own shape and the device's SM count (never of the launch's other
+        problems), so model isolation stays bit-exact: S = min(pairs // tiles, K blocks // 8) ranges
+        of whole 64-element K blocks, raw partial sums stacked [S, m rounded to 32, n] and finished
+        in order by HNN_CONVTC_SPLITK_FWD (+ bias, relu, NCHW, NHWC copy, relu mask).  Returns
+        (problem dict, finish description or None)."""
+        if not st.bf16 or os.environ.get("HNN_CONV_SPLITK", "1") == "0":
+            return d, None
+        M, F, K = d["m"], d["n"], d["k"]
+        tn = 64 if F <= 64 else (128 if F <= 128 else 256)
+        tiles = -(-M // 256) * -(-F // tn)
+        nkb = -(-K // 64)
+        S = min(self._sm_count() // 2 // tiles, nkb // 8)
+        if S < 2:
+            return d, None
+        L = -(-nkb // S) * 64
+        S = -(-K // L)
+        mp = -(-M // 32) * 32
+        part = _torch().empty(S * mp * F, dtype=_torch().float32, device=self.device)
+        fin = dict(partial=part, ksplit=S, pix_ld=mp, f=F, cap=s.batch_size, hw=d["row_mult"], dx=d["c"],
+                   mask=d.get("mask", 0), db=d.get("bias", 0), relu=d.get("relu", 0), dyt=d.get("xh_out", 0),
+                   model=s.index)
+        d2 = dict(d, c=_ptr(part), ldc=F, c_mode=0, bias=0, relu=0, mask=0, xh_out=0, ksplit=S, ksplit_len=L)
+        return d2, fin
+
+    def _splitk_finish(self, fins, label):
+        """One HNN_CONVTC_SPLITK_FWD launch for the split problems of a forward-type GEMM launch."""
+        probs, base = [], 0
+        for f in fins:
+            M = f["cap"] * f["hw"]
+            nb = -(-M // 32) * -(-f["f"] // 32)
+            # (the finish kernel only needs the plane size: oh = hw, ow = 1)
+            probs.append(N.ConvTcProblem(partial=_ptr(f["partial"]), dx=f["dx"], mask=f["mask"], db=f["db"],
+                                         dyt=f["dyt"], cap=f["cap"], f=f["f"], oh=f["hw"], ow=1, ksplit=f["ksplit"],
+                                         pix_ld=f["pix_ld"], rsc=int(f["relu"]), bf16=1, model=f["model"],
+                                         block_base=base, blocks=nb))
+            base += nb
+        t = _dev_table(N.ConvTcProblem, probs, self.device)
+        nbytes = sum(4 * f["cap"] * f["hw"] * f["f"] * (f["ksplit"] + 1 + (1 if f["mask"] else 0))
+                     + (2 * f["cap"] * f["hw"] * f["f"] if f["dyt"] else 0) for f in fins)
+        launch = Launch("hnn_conv_tc_aux", (N.CONVTC_SPLITK_FWD, _ptr(t), len(probs), base, 3, _ptr(self.cur),
+                                            _ptr(self.status)), t, label, nbytes=nbytes)
+        launch.keep = [f["partial"] for f in fins]
+        return launch
 
     def _conv_tc_launches(self, op, items, label):
         """Tensor-core conv layers of one wave: im2col / transpose / col2im / split reduce around
@@ -1004,7 +1108,7 @@ class DeviceHybrid:
                     lambda s, st: (-(-(s.batch_size * geo(st)[4] * geo(st)[5]) // 256)
                                    if st.bf16 and geo(st)[0] * st.attrs["kernel"] ** 2 <= 32  # (first layers)
                                    else -(-(s.batch_size * geo(st)[4] * geo(st)[5]) // 32) * -(-geo(st)[0] // 32))))
-            rows = {}
+            rows, fins = {}, []
             for s, st in items:
                 c, h, w, f, oh, ow, kk = geo(st)
                 B = self.pview(self.params, s.index, st.params[1])
@@ -1016,8 +1120,14 @@ class DeviceHybrid:
                              im_h=h, im_w=w, im_oh=oh, im_ow=ow, im_n=s.batch_size)
                 if st.xh_next is not None:
                     d.update(xh_out=_ptr(st.xh_next))
+                d, fin = self._fwd_split(s, st, d)
+                if fin is not None:
+                    fins.append(fin)
                 rows.setdefault(prec(st), []).append((s, d))
-            return out + gemms(N.HNN_FWD, rows, f"{label}/tc")
+            out += gemms(N.HNN_FWD, rows, f"{label}/tc")
+            if fins:
+                out.append(self._splitk_finish(fins, f"{label}/tc/splitk"))
+            return out
         tiles_t = lambda s, st: (s.batch_size * -(-(geo(st)[4] * geo(st)[5]) // 32) * -(-geo(st)[3] // 32))
         if op == N.HNN_DGRAD:
             # (only stages whose input gradient is needed reach here)

@@ -406,10 +406,23 @@ class Trainer:
         return rows
 
     def _lockstep(self, dev, tracks) -> tuple:
+        from concurrent.futures import ThreadPoolExecutor
+
         from . import rng
 
         bounds = self._boundaries(tracks)
         horizon = max(tr.total for tr in tracks.values())
+        # epoch permutations (src/store.py:74-76) are computed by host threads one epoch ahead,
+        # while the device trains the current one; a boundary only uploads the ready result
+        pool = ThreadPoolExecutor(max_workers=4)
+        perm_of = lambda tr, e: rng.permutation(tr.n, "shuffle", tr.dataset.content_hash, tr.job.hypers.seed, e)
+        ahead = {(tr.slot, tr.epochs[0]): pool.submit(perm_of, tr, tr.epochs[0]) for tr in tracks.values()}
+        try:
+            return self._lockstep_windows(dev, tracks, bounds, horizon, pool, perm_of, ahead)
+        finally:
+            pool.shutdown(wait=False, cancel_futures=True)
+
+    def _lockstep_windows(self, dev, tracks, bounds, horizon, pool, perm_of, ahead) -> tuple:
         steps_run, samples = 0, 0
         for t0, t1 in zip(bounds[:-1], bounds[1:]):
             if t0 >= horizon or all(tr.done for tr in tracks.values()):
@@ -417,10 +430,15 @@ class Trainer:
             starting = []
             for tr in tracks.values():
                 if not tr.done and t0 < tr.total and t0 % tr.spe == 0:
-                    e = tr.epochs[t0 // tr.spe]
-                    perm = rng.permutation(tr.n, "shuffle", tr.dataset.content_hash, tr.job.hypers.seed, e)
+                    i = t0 // tr.spe
+                    e = tr.epochs[i]
+                    fut = ahead.pop((tr.slot, e), None)
+                    perm = fut.result() if fut is not None else perm_of(tr, e)
                     dev.perm_upload(tr.slot, perm)
                     starting.append(tr.slot)
+                    if i + 1 < len(tr.epochs):
+                        nxt = tr.epochs[i + 1]
+                        ahead[(tr.slot, nxt)] = pool.submit(perm_of, tr, nxt)
             dev.reset_accumulators(starting)
             rows = self._window_rows(tracks, t0, t1)
             samples += int(rows["rows"][rows["active"] == 1].sum())

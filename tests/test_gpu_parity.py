@@ -992,3 +992,59 @@ def test_split_k_forward_is_bit_identical(pkg, monkeypatch):
     for a, b in zip(*outs):
         for k in a:
             assert np.array_equal(a[k], b[k]), k
+
+
+def test_tf32_truncation_selftest(pkg):
+    """The load-time check behind the 3xTF32 split (gemm_tc2.cu:11-13): raw fp32 operands are
+    truncated to tf32 by the tensor core, so hi + lo reproduce x; the probe GEMM then misses only
+    the lo*lo term (5.4e-7), where rounding hardware would be off by 2^-9."""
+    import torch
+
+    from paper_2408_01331_b200 import runtime
+
+    runtime._TF32_CHECKED.discard(str(torch.device("cuda", 0)))
+    err = runtime.tf32_truncation_selftest(torch.device("cuda", 0))
+    assert 1e-7 < err <= 1e-6, err
+
+
+@pytest.mark.gpu
+def test_c5_crosses_an_epoch_boundary(pkg):
+    """BASELINE C5 per GPU at full size (32 MLP 784-256-10, batch 64, 60,000 samples: 938 steps per
+    epoch), two epochs: the epoch-1 permutations come from the host prefetch threads (computed while
+    epoch 0 trains).  Every job completes with a two-row curve and improves; models 0 and 31 end
+    bit-identical to a hybrid holding only them; and model 7's losses around the boundary (steps
+    936..940) follow the reference algorithm (the oracle's store.batches order, rel 1e-3 after ~940
+    SGD steps, the trajectory drift bound)."""
+    import bench
+    from paper_2408_01331_b200 import zoo
+
+    ds = bench.make_dataset("c5")
+    jobs = zoo.config_jobs("c5", ds, count=32, epochs=2)
+    h = pkg.merge(jobs)
+    r = pkg.Trainer(h, pkg.make_plan("rr", jobs), jobs, {j.job_id: ds for j in jobs}).run()
+    for j in jobs:
+        res = r.jobs[j.job_id]
+        assert res.status == "complete" and [e for e, _, _ in res.curve] == [0, 1], j.job_id
+    assert sum(r.jobs[j.job_id].curve[1][1] < r.jobs[j.job_id].curve[0][1] for j in jobs) >= 30
+    pair = [jobs[0], jobs[31]]
+    h2 = pkg.merge(pair)
+    pkg.Trainer(h2, pkg.make_plan("rr", pair), pair, {j.job_id: ds for j in pair}).run()
+    for j in pair:
+        a, b = pkg.separate(h, j.job_id)[1], pkg.separate(h2, j.job_id)[1]
+        for k in a:
+            assert np.array_equal(a[k], b[k]), (j.job_id, k)
+
+    one = [zoo.config_jobs("c5", ds, first_model=7, count=1, epochs=2)[0]]
+    got = {}
+    h3 = pkg.merge(one)
+    pkg.Trainer(h3, pkg.make_plan("fcfs", one), one, {one[0].job_id: ds},
+                loss_observer=lambda jid, s, l, k: got.__setitem__(s, l) if 936 <= s <= 940 else None).run()
+    hp = one[0].hypers
+    ref = {}
+    splits = {"train_x": ds.train_x, "train_y": ds.train_y}
+    oracle.standalone_training(one[0].graph, splits, ds.content_hash, 2, hp.batch_size, hp.learning_rate, "sgd",
+                               hp.seed, observer=lambda s, p, l: ref.__setitem__(s, l) if 936 <= s <= 940 else None,
+                               max_steps=941)
+    assert sorted(got) == sorted(ref) == list(range(936, 941))
+    for s in ref:
+        assert abs(got[s] - ref[s]) <= 1e-3 * abs(ref[s]), (s, got[s], ref[s])

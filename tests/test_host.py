@@ -233,3 +233,32 @@ def test_host_gather_rows_matches_store_batches():
     with pytest.raises(h.DeviceError):
         _native.call("hnn_host_gather_rows", dst.ctypes.data, 4, dy.ctypes.data, src.ctypes.data, 7, ys.ctypes.data,
                      idx.ctypes.data, idx.size, 7)
+
+
+def test_backend_switch_rebinds_the_reference_workspace():
+    """backend.install routes hybridnn.workspace's training names to this package and uninstall
+    restores them (needs the reference installed in baseline/_ref; no GPU work)."""
+    import sys
+
+    ref = REPO / "baseline" / "_ref"
+    if not (ref / "hybridnn").exists():
+        pytest.skip("reference not installed in baseline/_ref")
+    sys.path.insert(0, str(ref))
+    try:
+        import hybridnn
+    finally:
+        sys.path.remove(str(ref))
+    from paper_2408_01331_b200 import backend
+    from paper_2408_01331_b200.separate import package, separate
+
+    ws = hybridnn.workspace
+    before = {n: getattr(ws, n) for n in backend.ROUTED}
+    backend.install(hybridnn)
+    backend.install(hybridnn)  # idempotent: the saved bindings stay the reference's
+    try:
+        assert ws.Trainer is h.Trainer and ws.separate is separate and ws.package is package
+        assert ws.Checkpoint is h.Checkpoint and ws.restore_checkpoint is h.restore_checkpoint
+        assert ws.unify_jobs is backend.unify_jobs and backend.installed(hybridnn)
+    finally:
+        backend.uninstall(hybridnn)
+    assert {n: getattr(ws, n) for n in backend.ROUTED} == before and not backend.installed(hybridnn)
