@@ -10,6 +10,7 @@
  *                               (store.py:68-81, optim.py:22-30, optim.py:57,73-76)
  *   hnn_gather_rows             Batch(x=train_x[idx], y=train_y[idx])   (store.py:77-80)
  *   hnn_host_gather_rows        the same gather on the host (data loader of the host-fed step)
+ *   hnn_host_gather_batch       one step's host gather for all models, split over host threads
  *   hnn_grouped_gemm            dense fwd / bwd  _dense_fwd, _dense_bwd (ops.py:46-55) with
  *                               relu fwd/bwd fused (ops.py:62-67); fp32 SIMT or tcgen05 3xTF32
  *   hnn_gemm_tc_encode          host-side TMA descriptors for the tcgen05 path
@@ -126,6 +127,21 @@ int hnn_gather_rows(const hnn_gather_problem* probs, int nprob, int max_cap, con
  * Plain host code (no CUDA calls); reentrant, so loader threads run it in parallel. */
 int hnn_host_gather_rows(float* dst_x, int64_t ld_dst, int32_t* dst_y, const float* src_x, int64_t ld_src,
                          const float* src_y, const int64_t* idx, int64_t n, int64_t cols);
+
+/* One step's host gather for every model at once (the loader's per-step call): item i gathers
+ * rows idx[0..n) exactly as hnn_host_gather_rows and zeroes rows [n, cap) of its destination (a
+ * short final batch, as the device gather writes).  The rows of all items are split evenly over
+ * `threads` host threads (<= 64); the result does not depend on the thread count. */
+typedef struct hnn_host_gather_item {
+  float* dst_x;
+  int32_t* dst_y;
+  const float* src_x;
+  const float* src_y;
+  const int64_t* idx;
+  int64_t ld_dst, ld_src, cols, n, cap;
+} hnn_host_gather_item;
+
+int hnn_host_gather_batch(const hnn_host_gather_item* items, int n_items, int threads);
 
 /*
  * Row-major grouped GEMM problem.  Let R = cur[model].rows.

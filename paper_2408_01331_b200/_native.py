@@ -95,6 +95,11 @@ class SceProblem(C.Structure):
     _fields_ = [("logits", P), ("labels", P), ("dlogits", P), ("ld", I), ("classes", I), ("cap", I), ("model", I)]
 
 
+class HostGatherItem(C.Structure):
+    _fields_ = [("dst_x", P), ("dst_y", P), ("src_x", P), ("src_y", P), ("idx", P), ("ld_dst", C.c_int64),
+                ("ld_src", C.c_int64), ("cols", C.c_int64), ("n", C.c_int64), ("cap", C.c_int64)]
+
+
 class OptSegment(C.Structure):
     _fields_ = [("param", P), ("grad", P), ("m", P), ("v", P), ("count", C.c_int64), ("model", I), ("kind", I),
                 ("momentum", C.c_float), ("chunk_base", I), ("chunks", I), ("reserved", I)]
@@ -104,6 +109,7 @@ STRUCTS = {
     "hnn_step_row": StepRow, "hnn_model_status": ModelStatus, "hnn_gather_problem": GatherProblem,
     "hnn_gemm_problem": GemmProblem, "hnn_conv_problem": ConvProblem, "hnn_pool_problem": PoolProblem,
     "hnn_relu_problem": ReluProblem, "hnn_convtc_problem": ConvTcProblem, "hnn_embed_problem": EmbedProblem, "hnn_sce_problem": SceProblem, "hnn_opt_segment": OptSegment,
+    "hnn_host_gather_item": HostGatherItem,
 }
 
 # every symbol include/hnn_b200.h declares, with its ctypes signature
@@ -112,6 +118,7 @@ SIGNATURES = {
     "hnn_step_begin": [P, P, P, C.c_int, VP],
     "hnn_gather_rows": [P, C.c_int, C.c_int, P, VP],
     "hnn_host_gather_rows": [VP, C.c_int64, VP, VP, C.c_int64, VP, VP, C.c_int64, C.c_int64],
+    "hnn_host_gather_batch": [VP, C.c_int, C.c_int],
     "hnn_gemm_tile_shape": [C.c_int, C.c_int, C.POINTER(I), C.POINTER(I)],
     "hnn_gemm_chunk_terms": [C.c_int, C.POINTER(I)],
     "hnn_grouped_gemm": [C.c_int, C.c_int, P, C.c_int, C.c_int, P, P, VP],

@@ -1,5 +1,8 @@
 // C-ABI plumbing: error state, the per-step schedule prologue and the batch gather.
 #include <cstring>
+#include <algorithm>
+#include <thread>
+#include <vector>
 
 #include "common.cuh"
 
@@ -102,6 +105,7 @@ int hnn_struct_size(const char* name) {
   if (!strcmp(name, "hnn_relu_problem")) return sizeof(hnn_relu_problem);
   if (!strcmp(name, "hnn_sce_problem")) return sizeof(hnn_sce_problem);
   if (!strcmp(name, "hnn_opt_segment")) return sizeof(hnn_opt_segment);
+  if (!strcmp(name, "hnn_host_gather_item")) return sizeof(hnn_host_gather_item);
   if (!strcmp(name, "hnn_convtc_problem")) return sizeof(hnn_convtc_problem);
   if (!strcmp(name, "hnn_embed_problem")) return sizeof(hnn_embed_problem);
   return -1;
@@ -133,6 +137,50 @@ int hnn_host_gather_rows(float* dst_x, int64_t ld_dst, int32_t* dst_y, const flo
     std::memcpy(dst_x + r * ld_dst, src_x + i * ld_src, bytes);
     dst_y[r] = static_cast<int32_t>(src_y[i]);
   }
+  return HNN_OK;
+}
+
+int hnn_host_gather_batch(const hnn_host_gather_item* items, int n_items, int threads) {
+  HNN_REQUIRE(items && n_items >= 0 && threads >= 1 && threads <= 64, "hnn_host_gather_batch", "bad arguments");
+  std::vector<int64_t> start(size_t(n_items) + 1, 0);  // prefix sums of the rows each item writes
+  for (int i = 0; i < n_items; ++i) {
+    const hnn_host_gather_item& it = items[i];
+    HNN_REQUIRE(it.dst_x && it.dst_y && it.src_x && it.src_y && (it.idx || it.n == 0) && it.n >= 0 &&
+                    it.cap >= it.n && it.cols >= 0 && it.ld_dst >= it.cols && it.ld_src >= it.cols,
+                "hnn_host_gather_batch", "bad item");
+    start[i + 1] = start[i] + it.cap;
+  }
+  const int64_t total = start[n_items];
+  auto work = [&](int64_t r0, int64_t r1) {
+    int i = int(std::upper_bound(start.begin(), start.end(), r0) - start.begin()) - 1;
+    for (int64_t g = r0; g < r1;) {
+      while (g >= start[i + 1]) ++i;
+      const hnn_host_gather_item& it = items[i];
+      const int64_t end = std::min(r1, start[i + 1]);
+      for (; g < end; ++g) {
+        const int64_t r = g - start[i];
+        float* dst = it.dst_x + r * it.ld_dst;
+        if (r < it.n) {
+          const int64_t j = it.idx[r];
+          std::memcpy(dst, it.src_x + j * it.ld_src, size_t(it.cols) * sizeof(float));
+          it.dst_y[r] = static_cast<int32_t>(it.src_y[j]);
+        } else {
+          std::memset(dst, 0, size_t(it.cols) * sizeof(float));
+          it.dst_y[r] = 0;
+        }
+      }
+    }
+  };
+  const int nt = int(std::min<int64_t>(threads, std::max<int64_t>(1, total / 64)));
+  if (nt <= 1) {
+    work(0, total);
+    return HNN_OK;
+  }
+  std::vector<std::thread> pool;
+  pool.reserve(nt - 1);
+  for (int t = 1; t < nt; ++t) pool.emplace_back(work, total * t / nt, total * (t + 1) / nt);
+  work(0, total / nt);
+  for (auto& th : pool) th.join();
   return HNN_OK;
 }
 

@@ -327,40 +327,62 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
 
 // dbias[i] = sum_{r<R} A[r*lda + i], sequential row order (numpy's axis-0 sum), one thread per
 // column; with optimizer fusion the bias is updated here too.
-#ifndef HNN_COLSUM_ROWS
-#define HNN_COLSUM_ROWS 128
-#endif
-constexpr int COLSUM_ROWS = HNN_COLSUM_ROWS;
-__global__ void colsum_kernel(const hnn_gemm_problem* __restrict__ probs, int nprob, const hnn_step_row* __restrict__ cur,
-                              const hnn_model_status* __restrict__ status) {
+// WGRAD bias gradient: db[i] = sum over rows r < R of dY[r, i] in numpy's axis-0 order (sequential
+// from -0.0, row by row), + the fused bias update.  One CTA per 32 columns of a problem: the four
+// warps stage COLSUM_CHUNK rows x 32 columns of dY in shared memory with all their float4 loads in
+// flight (8 per thread), then warp 0 (lane = column) adds the rows in order.  One thread per
+// column streaming its own column (the previous form) kept too few bytes in flight per SM: 22 us
+// per C3 launch at 1.6 TB/s (profiles/r02/ncu_step_c3_v2.txt).
+constexpr int COLSUM_CHUNK = 128, COLSUM_THREADS = 128;
+
+__global__ void __launch_bounds__(COLSUM_THREADS) colsum_kernel(const hnn_gemm_problem* __restrict__ probs, int nprob,
+                                                               const hnn_step_row* __restrict__ cur,
+                                                               const hnn_model_status* __restrict__ status) {
   hnn::pdl_wait();
+  __shared__ __align__(16) float tile[COLSUM_CHUNK][32];
   const hnn_gemm_problem& p = probs[blockIdx.y];
   if ((!p.dbias && !p.opt_b) || !live(cur, status, p.model)) return;
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= p.m) return;
+  const int c0 = blockIdx.x * 32;
+  if (c0 >= p.m) return;
   const int R = cur[p.model].rows * p.row_mult;
-  // loads of COLSUM_ROWS rows issue before their (sequential, order-preserving) adds: the loop is
-  // latency-bound otherwise (58 us per C3 launch at one load in flight per thread, 21.7 us at 32
-  // rows: one thread per column leaves ~7 warps per SM, so each thread must keep many loads in
-  // flight)
+  const int t = threadIdx.x, lane = t & 31;
+  const bool vec = (p.lda & 3) == 0 && (reinterpret_cast<uintptr_t>(p.a) & 15) == 0 && c0 + 32 <= p.m;
+  const int q = t & 7, r_in = t >> 3;  // float4 column quad, row within a 16-row slab
   float acc = -0.0f;
-  const float* col = p.a + i;
-  int r = 0;
-  for (; r + COLSUM_ROWS <= R; r += COLSUM_ROWS) {
-    float v[COLSUM_ROWS];
+  for (int base = 0; base < R; base += COLSUM_CHUNK) {
+    const int n = min(COLSUM_CHUNK, R - base);
+    if (vec) {
+      float4 v[COLSUM_CHUNK / 16];
 #pragma unroll
-    for (int j = 0; j < COLSUM_ROWS; ++j) v[j] = __ldg(col + size_t(r + j) * p.lda);
+      for (int j = 0; j < COLSUM_CHUNK / 16; ++j) {
+        const int r = r_in + 16 * j;
+        v[j] = r < n ? __ldg(reinterpret_cast<const float4*>(p.a + size_t(base + r) * p.lda + c0) + q)
+                     : make_float4(0.f, 0.f, 0.f, 0.f);
+      }
 #pragma unroll
-    for (int j = 0; j < COLSUM_ROWS; ++j) acc = __fadd_rn(acc, v[j]);
+      for (int j = 0; j < COLSUM_CHUNK / 16; ++j) *reinterpret_cast<float4*>(&tile[r_in + 16 * j][4 * q]) = v[j];
+    } else {
+      for (int e = t; e < n * 32; e += COLSUM_THREADS) {
+        const int r = e >> 5, c = e & 31;
+        tile[r][c] = c0 + c < p.m ? __ldg(p.a + size_t(base + r) * p.lda + c0 + c) : 0.0f;
+      }
+    }
+    __syncthreads();
+    if (t < 32) {
+      int r = 0;
+      for (; r + 8 <= n; r += 8) {
+        float v[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) v[j] = tile[r + j][lane];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) acc = __fadd_rn(acc, v[j]);
+      }
+      for (; r < n; ++r) acc = __fadd_rn(acc, tile[r][lane]);
+    }
+    __syncthreads();
   }
-  for (; r + 32 <= R; r += 32) {
-    float v[32];
-#pragma unroll
-    for (int j = 0; j < 32; ++j) v[j] = __ldg(col + size_t(r + j) * p.lda);
-#pragma unroll
-    for (int j = 0; j < 32; ++j) acc = __fadd_rn(acc, v[j]);
-  }
-  for (; r < R; ++r) acc = __fadd_rn(acc, __ldg(col + size_t(r) * p.lda));
+  const int i = c0 + lane;
+  if (t >= 32 || i >= p.m) return;
   if (p.dbias) p.dbias[i] = acc;
   if (p.opt_b) {
     const Update u = make_update(cur[p.model], p.opt_kind, p.opt_momentum);
@@ -553,8 +575,8 @@ int grouped_gemm_tc(int op, const hnn_gemm_problem* probs, int nprob, int total_
 // WGRAD bias gradient (+ fused bias update) for every problem of a tensor-core launch.
 int launch_colsum(const hnn_gemm_problem* probs, int nprob, const hnn_step_row* cur, const hnn_model_status* status,
                   cudaStream_t s) {
-  dim3 grid2(16, nprob);  // columns up to 16*256 = 4096 per problem (planner guarantees m <= 4096)
-  hnn::launch_pdl(colsum_kernel, dim3(grid2), dim3(256), 0, s, probs, nprob, cur, status);
+  dim3 grid2(128, nprob);  // columns up to 128*32 = 4096 per problem (planner guarantees m <= 4096)
+  hnn::launch_pdl(colsum_kernel, dim3(grid2), dim3(COLSUM_THREADS), 0, s, probs, nprob, cur, status);
   return check_launch("hnn_grouped_gemm(colsum)");
 }
 

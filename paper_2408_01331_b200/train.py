@@ -621,13 +621,44 @@ class HostFedStepper:
         return {s.job_id: (float(self.loss_host[s.index]), int(self.hits_host[s.index])) for s in self.dev.slots}
 
 
+def C_sizeof(cls) -> int:
+    import ctypes
+
+    return ctypes.sizeof(cls)
+
+
 class _BatchAssembler:
     """Host-side batch gather into the device batch-arena layout (the reference's store.batches:
-    ``train_x[perm[s:s+B]]``, src/store.py:68-81), one model slot at a time."""
+    ``train_x[perm[s:s+B]]``, src/store.py:68-81).  One step of every model is ONE native call
+    (``hnn_host_gather_batch``: the rows of all models split over host threads, GIL released);
+    the per-step Python work is a vectorised update of the item table."""
 
     def __init__(self, hybrid: HybridModel, datasets: dict):
+        from . import _native as N
+
         self.hybrid, self.dev, self.datasets = hybrid, hybrid.device, datasets
         self._perms: dict = {}
+        self._src: dict = {}
+        n = self.dev.n
+        dt = np.dtype([(name, np.uint64 if ctype is N.P else np.int64) for name, ctype in N.HostGatherItem._fields_])
+        assert dt.itemsize == C_sizeof(N.HostGatherItem)
+        self.item_dtype = dt
+        self.static = np.zeros(n, dtype=dt)  # destination offsets (filled per buffer), sources, widths
+        self.caps = np.zeros(n, dtype=np.int64)
+        for slot in self.dev.slots:
+            m = slot.index
+            xo, yo, ld = self.dev.batch_layout[m]
+            d = self.datasets[slot.job_id]
+            sample = int(np.prod(slot.sample_shape))
+            src, ys = self._sources(slot.job_id, d, sample)
+            self.static[m]["dst_x"] = 4 * xo
+            self.static[m]["dst_y"] = 4 * yo
+            self.static[m]["src_x"] = src.ctypes.data
+            self.static[m]["src_y"] = ys.ctypes.data
+            self.static[m]["ld_dst"] = ld
+            self.static[m]["ld_src"] = sample
+            self.static[m]["cols"] = sample
+            self.caps[m] = slot.batch_size
 
     def buffers(self) -> tuple:
         import torch
@@ -642,39 +673,45 @@ class _BatchAssembler:
         p = self._perms.get(key)
         if p is None:
             d = self.datasets[slot.job_id]
-            p = rng.permutation(d.sample_count, "shuffle", d.content_hash, self.hybrid.sub(slot.job_id).hypers.seed,
-                                epoch)
+            p = np.ascontiguousarray(rng.permutation(d.sample_count, "shuffle", d.content_hash,
+                                                     self.hybrid.sub(slot.job_id).hypers.seed, epoch), dtype=np.int64)
             self._perms = {k: v for k, v in self._perms.items() if k[0] != slot.index}  # one epoch per slot
             self._perms[key] = p
         return p
 
-    def fill(self, x, y, row, m: int, perm=None) -> None:
-        """Gather model m's rows of step `row` into the pinned arenas x / y (native, GIL released)."""
+    def items(self, x, y, row, perms: dict) -> np.ndarray:
+        """The step's item table for buffers (x, y): model m gathers its `rows` indices of `perms[m]`
+        from perm_base on (inactive models: no item rows)."""
+        it = self.static.copy()
+        it["dst_x"] += np.uint64(x.data_ptr())
+        it["dst_y"] += np.uint64(y.data_ptr())
+        active = row["active"].astype(bool)
+        it["n"] = np.where(active, row["rows"], 0)
+        it["cap"] = np.where(active, self.caps, 0)
+        for m, p in perms.items():
+            it[m]["idx"] = p.ctypes.data + 8 * int(row[m]["perm_base"])
+        return it
+
+    def gather(self, items: np.ndarray, threads: int) -> None:
         from . import _native as N
 
+        N.call("hnn_host_gather_batch", items.ctypes.data, len(items), int(threads))
+
+    def fill(self, x, y, row, m: int, perm=None) -> None:
+        """Gather model m's rows of step `row` into the pinned arenas x / y."""
         slot = self.dev.slots[m]
-        xo, yo, ld = self.dev.batch_layout[m]
-        r = row[m]
-        if not r["active"]:
+        if not row[m]["active"]:
             return
-        d = self.datasets[slot.job_id]
-        perm = self.perm(slot, int(r["epoch"])) if perm is None else perm
-        idx = np.ascontiguousarray(perm[r["perm_base"]:r["perm_base"] + r["rows"]], dtype=np.int64)
-        sample = int(np.prod(slot.sample_shape))
-        src, ys = self._sources(slot.job_id, d, sample)
-        N.call("hnn_host_gather_rows", x.data_ptr() + 4 * xo, ld, y.data_ptr() + 4 * yo, src.ctypes.data, sample,
-               ys.ctypes.data, idx.ctypes.data, idx.size, sample)
-        if idx.size < slot.batch_size:  # a short final batch: zero rows, as the device gather writes
-            x.numpy()[xo + idx.size * ld:xo + slot.batch_size * ld] = 0.0
-            y.numpy()[yo + idx.size:yo + slot.batch_size] = 0
+        perm = self.perm(slot, int(row[m]["epoch"])) if perm is None else perm
+        it = self.items(x, y, row, {m: perm})[m:m + 1]
+        self.gather(it, 1)
 
     def _sources(self, job_id, d, sample):
-        cache = self.__dict__.setdefault("_src", {})
-        got = cache.get(job_id)
+        got = self._src.get(job_id)
         if got is None:
             got = (np.ascontiguousarray(d.train_x.reshape(d.train_x.shape[0], sample), dtype=np.float32),
                    np.ascontiguousarray(d.train_y, dtype=np.float32))
-            cache[job_id] = got
+            self._src[job_id] = got
         return got
 
 
@@ -698,8 +735,10 @@ class HostBatchLoader:
         self.asm = _BatchAssembler(hybrid, datasets)
         self.rows = rows
         self.depth = depth
+        self.threads = max(1, min(64, int(threads)))
         self.bufs = [self.asm.buffers() for _ in range(depth)]
-        self.pool = ThreadPoolExecutor(max(1, threads))
+        # one worker: each step is one native call that fans out over `threads` host threads
+        self.pool = ThreadPoolExecutor(1)
         self.pending: list = [None] * depth
         self.t_next = 0
         self.t_issue = 0
@@ -717,13 +756,14 @@ class HostBatchLoader:
         dev = self.asm.dev
         perms = {m: self.asm.perm(dev.slots[m], int(row[m]["epoch"])) for m in range(dev.n) if row[m]["active"]}
         x, y = self.bufs[k]
+        items = self.asm.items(x, y, row, perms)
 
-        def job(m):
+        def job():
             if after is not None:
                 after.synchronize()
-            self.asm.fill(x, y, row, m, perms.get(m))
+            self.asm.gather(items, self.threads)
 
-        self.pending[k] = [self.pool.submit(job, m) for m in range(dev.n)]
+        self.pending[k] = [self.pool.submit(job)]
 
     def next(self) -> LoadedBatch:
         """The next step's batch (blocks until its gather is complete)."""

@@ -528,11 +528,15 @@ def test_pause_poll_hits_are_kept_until_the_jobs_boundary(pkg):
     assert t.checkpoints["b"].completed_epochs == 1  # paused at b's own first boundary (step 4)
 
 
-@pytest.mark.parametrize("opt_step", [1, 7])
-def test_adam_is_bit_exact_on_subnormal_and_zero_state(pkg, opt_step):
+@pytest.mark.parametrize("opt_step,mode", [(1, "classes"), (7, "classes"), (1, "binades"), (3, "binades"),
+                                           (40, "binades")])
+def test_adam_is_bit_exact_on_subnormal_and_zero_state(pkg, opt_step, mode):
     """Converged models carry zero and subnormal gradients / moments (C3 after 60 steps: 12% of the
     second moments are subnormal).  The multi-tensor Adam must still equal apply_update bit for bit
-    there (src/optim.py:73-87): m/bias1, v/bias2, sqrt and the final quotient all subnormal-exact."""
+    there (src/optim.py:73-87): m/bias1, v/bias2, sqrt and the final quotient all subnormal-exact.
+    "binades": magnitudes log-uniform over every float32 exponent (2^-149 .. 2^40) for g, m and v,
+    so every boundary of the kernel's fast path (tiny moments scaled by 2^64, the hard cases that
+    fall back to the exact routine) is crossed."""
     import torch
 
     from paper_2408_01331_b200 import store, zoo
@@ -559,10 +563,19 @@ def test_adam_is_bit_exact_on_subnormal_and_zero_state(pkg, opt_step):
                        np.where(cls == 2, g.uniform(1, 1e3, n) * tiny, g.uniform(0, 1, n) * scale)))
         return (mag * np.where(g.integers(0, 2, n) == 1, -1.0, 1.0)).astype(np.float32)
 
+    def binades(lo, hi):
+        e = g.uniform(lo, hi, n)
+        mag = np.exp2(e) * np.where(g.integers(0, 16, n) == 0, 0.0, 1.0)
+        return (mag * np.where(g.integers(0, 2, n) == 1, -1.0, 1.0)).astype(np.float32)
+
     P = g.normal(0, 0.1, n).astype(np.float32)
-    G = crafted(1e-6)
-    M = crafted(1e-7)
-    V = np.abs(crafted(1e-12))
+    if mode == "classes":
+        G = crafted(1e-6)
+        M = crafted(1e-7)
+        V = np.abs(crafted(1e-12))
+    else:
+        G, M, V = binades(-149, 30), binades(-149, 70), np.abs(binades(-149, 60))
+        P = np.where(g.integers(0, 2, n) == 1, P, binades(-149, 0))  # tiny parameters too
     for arena, host in ((dev.params, P), (dev.grads, G), (dev.m1, M), (dev.m2, V)):
         arena.copy_(torch.from_numpy(host))
     b1, b2 = _bias(opt_step)

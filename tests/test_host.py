@@ -1,4 +1,5 @@
 """Host-side logic and the C-ABI library surface (no GPU needed)."""
+import ctypes as C
 import re
 from pathlib import Path
 
@@ -233,6 +234,37 @@ def test_host_gather_rows_matches_store_batches():
     with pytest.raises(h.DeviceError):
         _native.call("hnn_host_gather_rows", dst.ctypes.data, 4, dy.ctypes.data, src.ctypes.data, 7, ys.ctypes.data,
                      idx.ctypes.data, idx.size, 7)
+
+
+@pytest.mark.parametrize("threads", [1, 3, 16])
+def test_host_gather_batch_matches_per_model_gather(threads):
+    """hnn_host_gather_batch (one native call per step for every model, rows split over host
+    threads) writes each model's Batch(x=train_x[idx], y=train_y[idx]) (src/store.py:77-80) and
+    zeroes the rows of a short final batch, independent of the thread count."""
+    g = np.random.default_rng(5)
+    items, dsts, expect = [], [], []
+    for m, (rows, cap, cols, ld) in enumerate([(13, 16, 7, 8), (0, 4, 5, 5), (64, 64, 33, 36), (30, 32, 1, 4)]):
+        src = g.normal(size=(90, cols)).astype(np.float32)
+        ys = g.integers(0, 9, size=90).astype(np.float32)
+        idx = g.permutation(90)[:rows].astype(np.int64)
+        dst = np.full((cap, ld), -1.0, dtype=np.float32)
+        dy = np.full(cap, -1, dtype=np.int32)
+        keep = (src, ys, idx)
+        items.append(_native.HostGatherItem(dst.ctypes.data, dy.ctypes.data, src.ctypes.data, ys.ctypes.data,
+                                            idx.ctypes.data if rows else 0, ld, cols, cols, rows, cap))
+        dsts.append((dst, dy, keep))
+        ex = np.full((cap, ld), -1.0, dtype=np.float32)
+        ex[:, :cols] = 0.0
+        ex[:rows, :cols] = src[idx]
+        ey = np.zeros(cap, dtype=np.int32)
+        ey[:rows] = ys[idx].astype(np.int32)
+        expect.append((ex, ey))
+    arr = (_native.HostGatherItem * len(items))(*items)
+    _native.call("hnn_host_gather_batch", C.addressof(arr), len(items), threads)
+    for (dst, dy, _), (ex, ey) in zip(dsts, expect):
+        assert np.array_equal(dst, ex) and np.array_equal(dy, ey)
+    with pytest.raises(h.DeviceError):
+        _native.call("hnn_host_gather_batch", C.addressof(arr), len(items), 0)
 
 
 def test_backend_switch_rebinds_the_reference_workspace():
