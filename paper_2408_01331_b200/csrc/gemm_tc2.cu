@@ -16,11 +16,15 @@
 // buffer, so the MMAs of the next chunk never wait for a promotion (double buffering).
 // The split itself is fp32-exact to ~2^-24 (emulated with exact sums: 3.9e-7 GEMM error at
 // K = 256, the same as an fp32 BLAS); what costs accuracy is the tensor core's accumulation,
-// which aligns each MMA's addends to the largest and drops the bits below.  So a chunk is ONE
-// 32-term K block, and its small correction products go first, while the accumulator is still
-// small (measured, tools/adam_probe2.py, C3 h = 2048: gradient error against float64 3.8e-6
-// with 4-block chunks and hi*hi first -> 4.3e-7, the reference's own fp32 BLAS is 5.4e-7;
-// C3 step +4.7%).  Each
+// which aligns each MMA's addends to the largest and drops the bits below.  So a chunk is TWO
+// 32-term K blocks, and the small correction products of both go first, while the accumulator is
+// still small (measured, tools/adam_probe2.py, C3 h = 2048: gradient error against float64 3.8e-6
+// with 4-block chunks and hi*hi first; 4.0-5.6e-7 with one-block chunks, lo first; 5.1-7.0e-7 with
+// two-block chunks, both blocks' corrections first; the reference's own fp32 BLAS 3.0-5.4e-7,
+// profiles/r02/chunk_accuracy_v4.txt).  One-block chunks promote once per K block, and every
+// promotion reads the tile's whole 128 x 256 fp32 accumulator out of TMEM (128 KB per CTA at
+// ~64-128 B/clk): the MMA thread waited for promoted buffers 20-43% of its time; two-block chunks
+// cut the C3 GEMMs 0.652 -> 0.622 ms.  Each
 // CTA's 128 x 256 running sum lives in registers: 8 accumulator warps x 128 columns (384
 // threads per CTA leave 168 registers per thread).
 //
@@ -60,12 +64,22 @@ static_assert(TC2_RAW >= 2 && TC2_LO >= 2, "raw / lo ring depths");
 constexpr int TC2_CONV_WARPS = HNN_TC2_CONV_WARPS;
 constexpr int TC2_THREADS = 64 + 32 * TC2_CONV_WARPS + 256;
 #ifndef HNN_TC2_CHUNK_KB
-#define HNN_TC2_CHUNK_KB 1
+#define HNN_TC2_CHUNK_KB 2
 #endif
 #ifndef HNN_TC2_LO_FIRST
 #define HNN_TC2_LO_FIRST 1
 #endif
 constexpr int TC2_CHUNK_KB = HNN_TC2_CHUNK_KB;
+#ifndef HNN_TC2_PROMO_COLS
+#define HNN_TC2_PROMO_COLS 16
+#endif
+constexpr int TC2_PROMO_COLS = HNN_TC2_PROMO_COLS;
+#ifndef HNN_TC2_REGS_ACC
+#define HNN_TC2_REGS_ACC 216  // 0: no setmaxnreg split
+#endif
+#ifndef HNN_TC2_REGS_LO
+#define HNN_TC2_REGS_LO 72
+#endif  // accumulator columns per TMEM load in the promotion
 // K blocks per TMEM accumulation chunk of one tile: a fused-SGD weight-gradient tile whose whole K
 // fits 4 blocks keeps one chunk (its epilogue reads the finished sums straight from TMEM)
 template <int OP>
@@ -312,6 +326,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC2_THREADS, 1)
   const int* sched_ids = sched + 2 + npairs;
   auto tile_id = [&](int i) { return use_sched ? __ldg(sched_ids + i) : i; };
 
+#if HNN_TC2_REGS_ACC
+  // register split: the TMA / MMA / converter warpgroup needs few registers, the accumulator warps
+  // hold a 128-column running sum plus a TMEM load in flight (384 x 168 = 128 x LO + 256 x HI)
+  static_assert(TC2_CONV_WARPS == 2 && 128 * HNN_TC2_REGS_LO + 256 * HNN_TC2_REGS_ACC <= 384 * 168, "register split");
+#endif
+  if (warp < 4) {
+#if HNN_TC2_REGS_ACC
+  asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(HNN_TC2_REGS_LO));
+#endif
   if (warp == 0) {
     // ---------------- TMA producer (both CTAs): rows m0 + rank*128.., columns n0 + rank*128..
     if (lane == 0) {
@@ -390,6 +413,53 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC2_THREADS, 1)
         const int ckb = tc2_chunk_kb<OP>(p, nkb);
         const uint32_t idesc =
             BF16 ? (bf16_idesc(2 * TC2_BM, tn) | (b_imp ? (1u << 16) : 0u)) : tf32_idesc(2 * TC2_BM, tn, A_MN, B_MN);
+        if (!BF16 && HNN_TC2_LO_FIRST && ckb == 2) {
+          // two-block chunks, correction products of BOTH blocks first (the accumulator is still
+          // small while they add), then both hi x hi blocks: half the promotions of one-block
+          // chunks — each promotion reads the whole 128 x 256 fp32 accumulator out of TMEM, and at
+          // one per K block those reads paced the MMAs (tools/tc2_trace.py: MMA thread waiting
+          // for a promoted buffer 20-43% of its time, profiles/r02)
+          for (int kb = 0; kb < nkb; kb += 2) {
+            const int cn = min(2, nkb - kb);
+            const uint32_t buf = cg & 1;
+            TC2_T0(t1);
+            if (cg >= 2) mbar_wait(bar(ACC_EMPTY + buf), ((cg >> 1) - 1) & 1);  // promoted
+            TC2_T1(t1, 1);
+            const uint32_t acc = tmem + buf * TC2_BN;
+            for (int i = 0; i < cn; ++i) {
+              const uint32_t kgi = kg + i;
+              const int s = kgi % SR, l = kgi % SL;
+              const uint32_t a_hi = raw_base + s * TC2_STAGE, b_hi = a_hi + TC2_A_BYTES;
+              const uint32_t a_lo = raw_base + (SR + l) * TC2_STAGE, b_lo = a_lo + TC2_A_BYTES;
+              TC2_T0(t0);
+              mbar_wait(bar(LO_FULL + l), (kgi / SL) & 1);  // both CTAs: raw landed, lo written
+              TC2_T1(t0, 0);
+              tc_fence_after();
+#pragma unroll
+              for (int j = 0; j < TC2_BK / 8; ++j) {
+                const uint32_t ao = A_MN ? j * 1024 : j * 32, bo = B_MN ? j * 1024 : j * 32;
+                mma_tf32_pair(acc, smem_desc(a_lo + ao, alb, asb, alt), smem_desc(b_hi + bo, blb, bsb, blt), idesc,
+                              (i | j) != 0);
+                mma_tf32_pair(acc, smem_desc(a_hi + ao, alb, asb, alt), smem_desc(b_lo + bo, blb, bsb, blt), idesc, 1u);
+              }
+              mma_commit_pair(bar(LO_EMPTY + l));  // lo slot l consumed
+            }
+            for (int i = 0; i < cn; ++i) {
+              const int s = (kg + i) % SR;
+              const uint32_t a_hi = raw_base + s * TC2_STAGE, b_hi = a_hi + TC2_A_BYTES;
+#pragma unroll
+              for (int j = 0; j < TC2_BK / 8; ++j) {
+                const uint32_t ao = A_MN ? j * 1024 : j * 32, bo = B_MN ? j * 1024 : j * 32;
+                mma_tf32_pair(acc, smem_desc(a_hi + ao, alb, asb, alt), smem_desc(b_hi + bo, blb, bsb, blt), idesc, 1u);
+              }
+              mma_commit_pair(bar(RAW_EMPTY + s));  // raw slot s consumed
+            }
+            mma_commit_pair(bar(ACC_FULL + buf));
+            ++cg;
+            kg += cn;
+          }
+          continue;
+        }
         for (int kb = 0; kb < nkb; ++kb, ++kg) {
           const int in_chunk = BF16 ? kb : kb % ckb;  // bf16: one chunk per tile (no promotion)
           const uint32_t buf = cg & 1;
@@ -449,7 +519,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC2_THREADS, 1)
         }
       }
     }
-  } else if (warp < 2 + TC2_CONV_WARPS) {
+  } else {
     // ---------------- converters (both CTAs): lo = rna_tf32(x - trunc_tf32(x)); raw stays as hi
     const int ct = threadIdx.x - 64;
     constexpr int CT = 32 * TC2_CONV_WARPS, PER = TC2_STAGE / 16 / CT, NPART = 4, PART = PER / NPART;
@@ -493,7 +563,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC2_THREADS, 1)
         if (lane == 0) mbar_arrive_cluster(lo_full_leader + 8 * l);
       }
     }
+  }
   } else {
+#if HNN_TC2_REGS_ACC
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(HNN_TC2_REGS_ACC));
+#endif
     // ---------------- accumulators + epilogue (warps 4..11): lane quarter warp % 4, column half
     constexpr int HALF = TC2_BN / 2;  // up to 128 columns per warp (tile_n / 2)
     const int aw = warp - 2 - TC2_CONV_WARPS, q = warp & 3, half = aw >> 2;
@@ -545,12 +619,20 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC2_THREADS, 1)
         TC2_T1(t4, 4);
         tc_fence_after();
 #pragma unroll
-        for (int cb = 0; cb < HALF; cb += 16) {
+        for (int cb = 0; cb < HALF; cb += TC2_PROMO_COLS) {
           if (cb >= hn) break;
-          uint32_t r0[16];
-          tmem_ld16(lane_base + buf * TC2_BN + cb, r0);
+          // TC2_PROMO_COLS columns per TMEM round trip (one tcgen05.wait::ld each)
+          uint32_t r0[TC2_PROMO_COLS];
+          if (TC2_PROMO_COLS >= 32) {
 #pragma unroll
-          for (int j = 0; j < 16; ++j)
+            for (int h = 0; h < TC2_PROMO_COLS / 32; ++h)
+              tmem_ld32_nowait(lane_base + buf * TC2_BN + cb + 32 * h, *reinterpret_cast<uint32_t(*)[32]>(r0 + 32 * h));
+            tmem_wait_ld();
+          } else {
+            tmem_ld16(lane_base + buf * TC2_BN + cb, *reinterpret_cast<uint32_t(*)[16]>(r0));
+          }
+#pragma unroll
+          for (int j = 0; j < TC2_PROMO_COLS; ++j)
             sum[cb + j] = (c == 0) ? __uint_as_float(r0[j]) : __fadd_rn(sum[cb + j], __uint_as_float(r0[j]));
         }
         TC2_T1(t4, 6);

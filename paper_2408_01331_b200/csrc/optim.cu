@@ -111,20 +111,37 @@ __global__ void __launch_bounds__(OPT_THREADS, OPT_MIN_CTAS)
   }
 }
 
-// ------------------------------------------------------------------ bulk-copy (TMA) variant
+// ------------------------------------------------------------------ bulk-copy (TMA) kernel (default)
 // The same update with the memory side moved to the bulk-copy engine: one CTA per SM, a producer
-// thread streams half-chunks (2048 floats of p / g / m / v = 32 KB) into a ring of shared-memory
-// stages with cp.async.bulk (up to 192 KB of loads in flight per SM, no per-thread load
-// registers), 16 update warps read the stage from shared memory, write p / m / v back in place,
-// and one of them issues the bulk stores.  The per-thread kernel's seven LDG/STG streams reach
-// 88% of the copy peak even without arithmetic (0.375 ms on C3); the bulk engine issues whole
-// 8 KB rows.
-constexpr int OPTB_E = 2048;                                  // floats per array per stage
-constexpr int OPTB_STAGES = 6;                                // 6 x 32 KB ring
-constexpr int OPTB_WARPS = 16;                                // update warps (+1 producer warp)
+// thread streams whole 4096-float chunks of p / g / m / v (64 KB) into a 3-stage shared-memory ring
+// with cp.async.bulk (up to 192 KB of loads in flight per SM, no load registers), 16 update warps
+// read the stage from shared memory (two float4 per thread and array), write p / m / v back in
+// place, and one of them issues the bulk stores.  Measured on C3's 76.7M Adam parameters launched
+// alone (tools/opt_variants.py, profiles/r02/opt_ab_v3.txt): 0.342-0.348 ms = 6.2 TB/s, 95% of the
+// copy peak, against 0.373-0.376 ms for the per-thread kernel above (whose seven LDG / STG streams
+// alone take 0.375 ms).  2048-float stages x 6: 0.367 ms; two CTAs per SM of 2048 x 3: 0.352-0.357;
+// 8 warps x 1024 floats x 6 stages, two CTAs: 0.353-0.366.  (Before Adam's fast path the update
+// warps were issue-bound: 0.438 ms.)
+#ifndef HNN_OPTB_E
+#define HNN_OPTB_E 4096
+#endif
+#ifndef HNN_OPTB_STAGES
+#define HNN_OPTB_STAGES 3
+#endif
+#ifndef HNN_OPTB_WARPS
+#define HNN_OPTB_WARPS 16
+#endif
+#ifndef HNN_OPTB_CTAS
+#define HNN_OPTB_CTAS 1
+#endif
+constexpr int OPTB_E = HNN_OPTB_E;                            // floats per array per stage
+constexpr int OPTB_STAGES = HNN_OPTB_STAGES;                  // ring of 4 * OPTB_E floats per stage
+constexpr int OPTB_WARPS = HNN_OPTB_WARPS;                    // update warps (+1 producer warp)
+constexpr int OPTB_CTAS = HNN_OPTB_CTAS;                      // CTAs per SM
 constexpr int OPTB_THREADS = 32 * (OPTB_WARPS + 1);
 constexpr int OPTB_SMEM = OPTB_STAGES * 4 * OPTB_E * 4 + 1024;  // ring + barriers / stage info
-static_assert(OPTB_E / 4 == 32 * OPTB_WARPS, "one float4 per update thread per array and stage");
+static_assert(OPT_CHUNK % OPTB_E == 0 && OPTB_E % (128 * OPTB_WARPS) == 0, "whole float4 per update thread per array and stage");
+static_assert(OPTB_CTAS * OPTB_SMEM <= 228 * 1024, "shared memory per SM");
 
 __device__ __forceinline__ void bulk_load(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar) {
   asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
@@ -144,7 +161,7 @@ __device__ __forceinline__ void sts4f(uint32_t a, float4 v) {
   asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(a), "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w) : "memory");
 }
 
-__global__ void __launch_bounds__(OPTB_THREADS, 1)
+__global__ void __launch_bounds__(OPTB_THREADS, OPTB_CTAS)
     multi_tensor_bulk_kernel(const hnn_opt_segment* __restrict__ segs, int nseg, int total_units,
                              const hnn_step_row* __restrict__ cur, const hnn_model_status* __restrict__ status) {
   hnn::pdl_wait();
@@ -179,10 +196,11 @@ __global__ void __launch_bounds__(OPTB_THREADS, 1)
       for (int u = blockIdx.x; u < total_units; u += gridDim.x, ++it) {
         const int s = int(it % OPTB_STAGES);
         if (it >= OPTB_STAGES) wait(bar(EMPTY + s), ((it / OPTB_STAGES) - 1) & 1);
-        const int chunk = u >> 1;
+        constexpr int UPC = OPT_CHUNK / OPTB_E;  // units per 4096-float chunk
+        const int chunk = u / UPC;
         const int si = find_problem(segs, nseg, chunk, [](const hnn_opt_segment& q) { return q.chunk_base; });
         const hnn_opt_segment& sg = segs[si];
-        const long long off = (long long)(chunk - sg.chunk_base) * OPT_CHUNK + (u & 1) * OPTB_E;
+        const long long off = (long long)(chunk - sg.chunk_base) * OPT_CHUNK + (u % UPC) * OPTB_E;
         const int n = int(max(0LL, min((long long)OPTB_E, sg.count - off)));
         const bool ok = n > 0 && live(cur, status, sg.model);
         info[s] = make_int4(si, int(off), n, ok ? 1 : 0);
@@ -215,13 +233,17 @@ __global__ void __launch_bounds__(OPTB_THREADS, 1)
       const hnn_opt_segment& sg = segs[inf.x];
       const hnn_step_row& row = cur[sg.model];
       const Update up{sg.kind, row.lr, sg.momentum, row.bias1, row.bias2, row.opt_step == 1};
-      if (4 * t < inf.z) {
-        const uint32_t a = st + 16 * t;
+      const float r1 = recip_refined(up.bias1), r2 = recip_refined(up.bias2);
+#pragma unroll
+      for (int j = 0; j < OPTB_E / (128 * OPTB_WARPS); ++j) {
+        const int i = t + j * 32 * OPTB_WARPS;
+        if (4 * i >= inf.z) break;
+        const uint32_t a = st + 16 * i;
         float4 P = lds4f(a), G = lds4f(a + OPTB_E * 4);
         float4 M = make_float4(0.f, 0.f, 0.f, 0.f), V = M;
         if (up.kind != HNN_OPT_SGD) M = lds4f(a + 2 * OPTB_E * 4);
         if (up.kind == HNN_OPT_ADAM) V = lds4f(a + 3 * OPTB_E * 4);
-        update4(up, recip_refined(up.bias1), recip_refined(up.bias2), P, G, M, V);
+        update4(up, r1, r2, P, G, M, V);
         sts4f(a, P);
         if (up.kind != HNN_OPT_SGD) sts4f(a + 2 * OPTB_E * 4, M);
         if (up.kind == HNN_OPT_ADAM) sts4f(a + 3 * OPTB_E * 4, V);
@@ -256,7 +278,7 @@ int launch_multi_tensor(const char* who, const hnn_opt_segment* segs, int nseg, 
   }
   if (bulk < 0) {
     const char* e = getenv("HNN_OPT_BULK");
-    bulk = e ? atoi(e) : 0;  // measured slower (16 update warps per SM issue-bound on Adam); A/B only
+    bulk = e ? atoi(e) : 1;  // HNN_OPT_BULK=0: the per-thread kernel (A/B)
     if (bulk) {
       cudaError_t err = cudaFuncSetAttribute(multi_tensor_bulk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, OPTB_SMEM);
       if (err != cudaSuccess) {
@@ -267,8 +289,8 @@ int launch_multi_tensor(const char* who, const hnn_opt_segment* segs, int nseg, 
     }
   }
   if (bulk) {
-    const int units = 2 * total_chunks;
-    const int grid = units < sms ? units : sms;
+    const int units = total_chunks * (OPT_CHUNK / OPTB_E);
+    const int grid = units < OPTB_CTAS * sms ? units : OPTB_CTAS * sms;
     hnn::launch_pdl(multi_tensor_bulk_kernel, dim3(grid), dim3(OPTB_THREADS), OPTB_SMEM, as_stream(stream), segs, nseg,
                     units, cur, status);
     return check_launch(who);
