@@ -228,6 +228,24 @@ namespace hnn {
 
 constexpr int DTHREADS = 256;
 
+// Shared-memory layouts of the direct kernels, chosen so that the addresses one warp instruction
+// touches fall into distinct banks (ncu, profiles/r02/ncu_direct_c2_v4.txt: 70% of the LeNet conv1
+// forward's shared wavefronts and 61% of its weight gradient's were bank conflicts):
+//  * x rows at a stride of 1 mod 32 words: the forward's lanes (output row, 4-column block) then
+//    read banks oy + 4 * block (at most 2-way for 28-wide rows);
+//  * x channels at a stride of K mod 32: the weight gradient's lanes, which own filter rows
+//    (f, c, i), read input row (c, i) at bank c * K + i (+ f-independent), distinct for C * K <= 32;
+//  * dy planes at a stride of 1 mod 32: lanes of different filters f read distinct banks.
+__host__ __device__ inline int up_to_residue(int x, int r) { return x + ((r - x) % 32 + 32) % 32; }
+struct DirectLayout {
+  int rs, cs, ps;  // x row stride, x channel stride, dy plane stride (floats)
+  __host__ __device__ DirectLayout(int c, int h, int w, int k, int oh, int ow) {
+    rs = up_to_residue(w, 1);
+    cs = up_to_residue(h * rs, k % 32);
+    ps = up_to_residue(oh * ow, 1);
+  }
+};
+
 __device__ __forceinline__ void stage(float* dst, const float* __restrict__ src, int n) {
   // eight loads in flight per thread before their shared-memory stores
   const int step = blockDim.x;
@@ -242,51 +260,102 @@ __device__ __forceinline__ void stage(float* dst, const float* __restrict__ src,
   for (; i < n; i += step) dst[i] = __ldg(src + i);
 }
 
+// rows of `w` floats (n rows, planes of `h` rows) into a padded layout: row stride rs, plane stride cs
+__device__ __forceinline__ void stage_rows(float* dst, const float* __restrict__ src, int n, int w, int h, int rs,
+                                           int cs) {
+  const int total = n * w;
+  for (int e0 = threadIdx.x; e0 < total; e0 += 8 * blockDim.x) {
+    float v[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int e = e0 + u * blockDim.x;
+      v[u] = e < total ? __ldg(src + e) : 0.0f;
+    }
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int e = e0 + u * blockDim.x;
+      if (e >= total) break;
+      const int r = e / w, x = e - r * w, pl = r / h;
+      dst[pl * cs + (r - pl * h) * rs + x] = v[u];
+    }
+  }
+}
+
 // Register-blocked stride-1 paths (LeNet-class layers): a thread computes 4 consecutive outputs of
 // one row, so each staged input row segment (4 + K - 1 values) and each weight are loaded from
 // shared memory once for 4 * K FMAs (the one-output-per-thread loop issued 2 shared loads per
 // FMA and was bound by the 1-wavefront/clock shared-memory pipe).
 constexpr int RB = 4;
 
-template <int K>
+// Forward, stride 1: a thread computes FG filters x RB consecutive outputs of one row, so per
+// (channel, filter row) it loads one RB + K - 1 input segment and, per tap, the FG filters'
+// weights as float4 (weights staged tap-major, filters innermost: wt[(c*K + i)*K + j][f], FP = F
+// rounded up to 4) for FG * RB FMAs; a thread-per-filter form loaded a weight per RB FMAs and
+// was bound by the shared-memory pipe (ncu: issue 73%, FMA pipe 36% on LeNet conv1).
+template <int K, int FG, bool PAD0>
 __device__ __forceinline__ void direct_fwd_blocked(const hnn_conv_problem& p, const ConvGeom& g, const float* xs,
-                                                   const float* ws, float* yb) {
+                                                   int rs, int cs, const float* wt, int fp, float* yb) {
   const int qblocks = (g.ow + RB - 1) / RB;
-  for (int e = threadIdx.x; e < g.f * g.oh * qblocks; e += blockDim.x) {
-    const int f = e / (g.oh * qblocks), rq = e - f * g.oh * qblocks, oy = rq / qblocks, ox0 = (rq - oy * qblocks) * RB;
-    float acc[RB] = {0.0f, 0.0f, 0.0f, 0.0f};
-    const float* wf = ws + f * g.ckk;
+  const int groups = (g.f + FG - 1) / FG;
+  for (int e = threadIdx.x; e < groups * g.oh * qblocks; e += blockDim.x) {
+    const int fg = e / (g.oh * qblocks), rq = e - fg * g.oh * qblocks, oy = rq / qblocks, ox0 = (rq - oy * qblocks) * RB;
+    const int f0 = fg * FG;
+    float acc[FG][RB];
+#pragma unroll
+    for (int ff = 0; ff < FG; ++ff)
+#pragma unroll
+      for (int q = 0; q < RB; ++q) acc[ff][q] = 0.0f;
     for (int c = 0; c < g.c; ++c) {
 #pragma unroll
       for (int i = 0; i < K; ++i) {
         const int y = oy - g.pad + i;
-        if (y < 0 || y >= g.h) continue;
-        const float* xr = xs + (c * g.h + y) * g.w;
+        if (!PAD0 && (y < 0 || y >= g.h)) continue;
+        const float* xr = xs + c * cs + y * rs;
         float seg[RB + K - 1];
 #pragma unroll
         for (int t = 0; t < RB + K - 1; ++t) {
+          // (no padding: columns past w are the padded row's tail, used only by outputs >= ow)
           const int x = ox0 - g.pad + t;
-          seg[t] = (x >= 0 && x < g.w) ? xr[x] : 0.0f;
+          seg[t] = (PAD0 || (x >= 0 && x < g.w)) ? xr[x] : 0.0f;
         }
-        const float* wr = wf + (c * K + i) * K;
+        const float* wr = wt + size_t((c * K + i) * K) * fp + f0;
 #pragma unroll
         for (int j = 0; j < K; ++j) {
-          const float w = wr[j];
 #pragma unroll
-          for (int q = 0; q < RB; ++q) acc[q] = fmaf(seg[q + j], w, acc[q]);
+          for (int f4 = 0; f4 < FG / 4; ++f4) {
+            const float4 w = *reinterpret_cast<const float4*>(wr + j * fp + 4 * f4);
+#pragma unroll
+            for (int q = 0; q < RB; ++q) {
+              acc[4 * f4 + 0][q] = fmaf(seg[q + j], w.x, acc[4 * f4 + 0][q]);
+              acc[4 * f4 + 1][q] = fmaf(seg[q + j], w.y, acc[4 * f4 + 1][q]);
+              acc[4 * f4 + 2][q] = fmaf(seg[q + j], w.z, acc[4 * f4 + 2][q]);
+              acc[4 * f4 + 3][q] = fmaf(seg[q + j], w.w, acc[4 * f4 + 3][q]);
+            }
+          }
         }
       }
     }
-    const float bias = __ldg(p.bias + f);
 #pragma unroll
-    for (int q = 0; q < RB; ++q) {
-      const int ox = ox0 + q;
-      if (ox >= g.ow) break;
-      float v = __fadd_rn(acc[q], bias);
-      if (p.relu) v = np_relu(v);
-      yb[(f * g.oh + oy) * g.ow + ox] = v;
+    for (int ff = 0; ff < FG; ++ff) {
+      const int f = f0 + ff;
+      if (f >= g.f) break;
+      const float bias = __ldg(p.bias + f);
+#pragma unroll
+      for (int q = 0; q < RB; ++q) {
+        const int ox = ox0 + q;
+        if (ox >= g.ow) break;
+        float v = __fadd_rn(acc[ff][q], bias);
+        if (p.relu) v = np_relu(v);
+        yb[(f * g.oh + oy) * g.ow + ox] = v;
+      }
     }
   }
+}
+
+// FG for the blocked forward: 8 filters per thread when that still gives the CTA >= 128 work items
+__device__ __forceinline__ int fwd_fg(const ConvGeom& g) {
+  const int q = (g.ow + RB - 1) / RB;
+  return ((g.f + 7) / 8) * g.oh * q >= 128 ? 8 : 4;
 }
 
 template <int K>
@@ -333,7 +402,7 @@ __device__ __forceinline__ void direct_dgrad_blocked(const hnn_conv_problem& p, 
 // one 4 + K - 1 input segment for 4 * K FMAs.  G row groups (fixed) are combined in order.
 template <int K>
 __device__ __forceinline__ void direct_wgrad_blocked(const hnn_conv_problem& p, const ConvGeom& g, const float* xs,
-                                                     int cs, int rs, const float* ds, int nb, float* red,
+                                                     int cs, int rs, const float* ds, int ps, int nb, float* red,
                                                      float* out) {
   const int nrow = g.f * g.c * K;  // (f, c, i) filter rows
   const int G = max(1, min(8, int(blockDim.x) / nrow));
@@ -346,7 +415,7 @@ __device__ __forceinline__ void direct_wgrad_blocked(const hnn_conv_problem& p, 
 #pragma unroll
     for (int j = 0; j < K; ++j) acc[j] = 0.0f;
     for (int sb = 0; sb < nb; ++sb) {
-      const float* df = ds + (sb * g.f + f) * g.ohw;
+      const float* df = ds + (sb * g.f + f) * ps;
       const float* xc = xs + (sb * g.c + c) * cs;
       for (int oy = grp; oy < g.oh; oy += G) {
         const int y = oy - g.pad + i;
@@ -389,7 +458,7 @@ __device__ __forceinline__ void direct_wgrad_blocked(const hnn_conv_problem& p, 
   for (int f = threadIdx.x; f < g.f; f += blockDim.x) {
     float a = 0.0f;
     for (int sb = 0; sb < nb; ++sb) {
-      const float* df = ds + (sb * g.f + f) * g.ohw;
+      const float* df = ds + (sb * g.f + f) * ps;
       for (int u = 0; u < g.ohw; ++u) a = __fadd_rn(a, df[u]);
     }
     out[f * cols + g.ckk] = a;
@@ -397,7 +466,7 @@ __device__ __forceinline__ void direct_wgrad_blocked(const hnn_conv_problem& p, 
 }
 
 template <int OP>
-__global__ void __launch_bounds__(DTHREADS) conv_direct_kernel(const hnn_conv_problem* __restrict__ probs, int nprob,
+__global__ void __launch_bounds__(DTHREADS, 3) conv_direct_kernel(const hnn_conv_problem* __restrict__ probs, int nprob,
                                                                const hnn_step_row* __restrict__ cur,
                                                                const hnn_model_status* __restrict__ status) {
   hnn::pdl_wait();
@@ -415,13 +484,32 @@ __global__ void __launch_bounds__(DTHREADS) conv_direct_kernel(const hnn_conv_pr
       for (int e = threadIdx.x; e < g.f * g.ohw; e += blockDim.x) yb[e] = 0.0f;
       return;
     }
-    float* xs = sm;                 // [C][H][W]
-    float* ws = sm + g.c * g.hw;    // [F][C*k*k]
-    stage(xs, p.x + size_t(b) * g.c * g.hw, g.c * g.hw);
+    const DirectLayout lay(g.c, g.h, g.w, g.k, g.oh, g.ow);
+    float* xs = sm;                 // [C][H][rs], channel stride cs
+    float* ws = sm + ((g.c * lay.cs + 3) & ~3);  // [F][C*k*k] (generic) / [C*k*k][fp] (blocked; float4 rows)
+    stage_rows(xs, p.x + size_t(b) * g.c * g.hw, g.c * g.h, g.w, g.h, lay.rs, lay.cs);
+    if (g.s == 1 && (g.k == 5 || g.k == 3)) {
+      const int fp = (g.f + 3) & ~3;
+      for (int e = threadIdx.x; e < g.ckk * fp; e += blockDim.x) {  // tap-major, filters innermost
+        const int t = e / fp, f = e - t * fp;
+        ws[e] = f < g.f ? __ldg(p.weight + size_t(f) * g.ckk + t) : 0.0f;
+      }
+      __syncthreads();
+      const bool fg8 = fwd_fg(g) == 8;
+      // padding 0: every tap is in the image (the row tail past w feeds only outputs >= ow, which
+      // the row stride rs >= ow + K - 1 + (RB - 1) keeps inside the staged row)
+      const bool pad0 = g.pad == 0 && lay.rs >= ((g.ow + RB - 1) / RB) * RB + g.k - 1;
+      if (g.k == 5) {
+        if (pad0) return fg8 ? direct_fwd_blocked<5, 8, true>(p, g, xs, lay.rs, lay.cs, ws, fp, yb)
+                             : direct_fwd_blocked<5, 4, true>(p, g, xs, lay.rs, lay.cs, ws, fp, yb);
+        return fg8 ? direct_fwd_blocked<5, 8, false>(p, g, xs, lay.rs, lay.cs, ws, fp, yb)
+                   : direct_fwd_blocked<5, 4, false>(p, g, xs, lay.rs, lay.cs, ws, fp, yb);
+      }
+      return fg8 ? direct_fwd_blocked<3, 8, false>(p, g, xs, lay.rs, lay.cs, ws, fp, yb)
+                 : direct_fwd_blocked<3, 4, false>(p, g, xs, lay.rs, lay.cs, ws, fp, yb);
+    }
     stage(ws, p.weight, g.f * g.ckk);
     __syncthreads();
-    if (g.s == 1 && g.k == 5) return direct_fwd_blocked<5>(p, g, xs, ws, yb);
-    if (g.s == 1 && g.k == 3) return direct_fwd_blocked<3>(p, g, xs, ws, yb);
     for (int e = threadIdx.x; e < g.f * g.ohw; e += blockDim.x) {
       const int f = e / g.ohw, opix = e - f * g.ohw;
       const int oy = opix / g.ow, ox = opix - oy * g.ow;
@@ -430,10 +518,10 @@ __global__ void __launch_bounds__(DTHREADS) conv_direct_kernel(const hnn_conv_pr
       const float* wf = ws + f * g.ckk;
       float acc = 0.0f;
       for (int c = 0; c < g.c; ++c) {
-        const float* xc = xs + c * g.hw + y0 * g.w + x0;
+        const float* xc = xs + c * lay.cs + y0 * lay.rs + x0;
         const float* wc = wf + c * g.kk2;
         for (int i = i0; i < i1; ++i)
-          for (int j = j0; j < j1; ++j) acc = fmaf(xc[i * g.w + j], wc[i * g.k + j], acc);
+          for (int j = j0; j < j1; ++j) acc = fmaf(xc[i * lay.rs + j], wc[i * g.k + j], acc);
       }
       float v = __fadd_rn(acc, __ldg(p.bias + f));
       if (p.relu) v = np_relu(v);
@@ -483,21 +571,19 @@ __global__ void __launch_bounds__(DTHREADS) conv_direct_kernel(const hnn_conv_pr
     // and sweeps the valid output window of each staged sample in order.
     constexpr int MAXW = 16;
     const int cols = g.ckk + 1, nw = g.f * cols;
-    const int rs = g.w + 1, cs = g.h * rs + 1;
+    const DirectLayout lay(g.c, g.h, g.w, g.k, g.oh, g.ow);
+    const int rs = lay.rs, cs = lay.cs, ps = lay.ps;
     const int b0 = unit * HNN_CONV_DIRECT_BCHUNK, nb = max(0, min(HNN_CONV_DIRECT_BCHUNK, rows - b0));
     float* xs = sm;                                            // [nb][C] x (H x rs), channel stride cs
-    float* ds = sm + HNN_CONV_DIRECT_BCHUNK * g.c * cs;        // [nb][F][OH][OW]
-    for (int e = threadIdx.x; e < nb * g.c * g.hw; e += blockDim.x) {
-      const int pc = e / g.hw, pix = e - pc * g.hw, y = pix / g.w, x = pix - y * g.w;
-      xs[pc * cs + y * rs + x] = __ldg(p.x + size_t(b0) * g.c * g.hw + e);
-    }
-    stage(ds, p.dy + size_t(b0) * g.f * g.ohw, nb * g.f * g.ohw);
+    float* ds = sm + HNN_CONV_DIRECT_BCHUNK * g.c * cs;        // [nb][F] dy planes (OH x OW), stride ps
+    stage_rows(xs, p.x + size_t(b0) * g.c * g.hw, nb * g.c * g.h, g.w, g.h, rs, cs);
+    stage_rows(ds, p.dy + size_t(b0) * g.f * g.ohw, nb * g.f, g.ohw, 1, g.ohw, ps);
     __syncthreads();
     if (g.s == 1 && (g.k == 5 || g.k == 3)) {
-      float* red = ds + HNN_CONV_DIRECT_BCHUNK * g.f * g.ohw;  // [G][f*c*k][k] group partials
+      float* red = ds + HNN_CONV_DIRECT_BCHUNK * g.f * ps;  // [G][f*c*k][k] group partials
       float* out = p.partial + size_t(unit) * nw;
-      if (g.k == 5) direct_wgrad_blocked<5>(p, g, xs, cs, rs, ds, nb, red, out);
-      else direct_wgrad_blocked<3>(p, g, xs, cs, rs, ds, nb, red, out);
+      if (g.k == 5) direct_wgrad_blocked<5>(p, g, xs, cs, rs, ds, ps, nb, red, out);
+      else direct_wgrad_blocked<3>(p, g, xs, cs, rs, ds, ps, nb, red, out);
       return;
     }
     float acc[MAXW];
@@ -511,7 +597,7 @@ __global__ void __launch_bounds__(DTHREADS) conv_direct_kernel(const hnn_conv_pr
       float a = 0.0f;
       if (col == g.ckk) {
         for (int sb = 0; sb < nb; ++sb) {
-          const float* df = ds + (sb * g.f + f) * g.ohw;
+          const float* df = ds + (sb * g.f + f) * ps;
           for (int t = 0; t < g.ohw; ++t) a = __fadd_rn(a, df[t]);
         }
       } else {
@@ -523,7 +609,7 @@ __global__ void __launch_bounds__(DTHREADS) conv_direct_kernel(const hnn_conv_pr
         // the dependent FMA chain; they are combined in a fixed order, so results stay deterministic
         float a4[4] = {0.0f, 0.0f, 0.0f, 0.0f};
         for (int sb = 0; sb < nb; ++sb) {
-          const float* df = ds + (sb * g.f + f) * g.ohw;
+          const float* df = ds + (sb * g.f + f) * ps;
           const float* xc = xs + (sb * g.c + c) * cs + (i - g.pad) * rs + (j - g.pad);
           for (int oy = oy0; oy < oy1; ++oy) {
             const float* xr = xc + oy * g.s * rs;
@@ -554,10 +640,11 @@ __global__ void __launch_bounds__(DTHREADS) conv_direct_kernel(const hnn_conv_pr
 // Shared-memory bytes a problem needs on the direct path (host and device agree on this).
 __host__ __device__ inline int conv_direct_smem(int op, int c, int h, int w, int f, int k, int oh, int ow) {
   const int ckk = c * k * k;
-  if (op == HNN_FWD) return 4 * (c * h * w + f * ckk);
+  const DirectLayout lay(c, h, w, k, oh, ow);
+  if (op == HNN_FWD) return 4 * (((c * lay.cs + 3) & ~3) + ((f + 7) & ~7) * ckk);  // (filters padded: blocked path)
   if (op == HNN_DGRAD) return 4 * (f * oh * ow + f * ckk);
   // staged samples + the blocked stride-1 path's row-group partials (G <= 8 groups of f*c*k*k)
-  return 4 * HNN_CONV_DIRECT_BCHUNK * (c * (h * (w + 1) + 1) + f * oh * ow) + 4 * 8 * f * c * k * k;
+  return 4 * HNN_CONV_DIRECT_BCHUNK * (c * lay.cs + f * lay.ps) + 4 * 8 * f * c * k * k;
 }
 
 }  // namespace hnn
