@@ -294,6 +294,12 @@ int hnn_grouped_conv(int op, const hnn_conv_problem* probs, int nprob, int total
 int hnn_conv_direct_smem(int op, int c, int h, int w, int f, int k, int oh, int ow);
 int hnn_grouped_conv_direct(int op, const hnn_conv_problem* probs, int nprob, int total_blocks, int smem,
                             const hnn_step_row* cur, const hnn_model_status* status, void* stream);
+/* Threads per CTA the direct kernels want for a layer (128 when a stride-1 forward / input gradient
+ * has at most 128 register-blocked work items per sample, else 256), and the launch taking it
+ * (`threads` = max over the launch's problems; hnn_grouped_conv_direct launches 256). */
+int hnn_conv_direct_threads(int op, int c, int h, int w, int f, int k, int oh, int ow);
+int hnn_grouped_conv_direct_ex(int op, const hnn_conv_problem* probs, int nprob, int total_blocks, int smem,
+                               int threads, const hnn_step_row* cur, const hnn_model_status* status, void* stream);
 
 /* dw[f,:] = sum_s partial[s,f,:C*k*k] and db[f] = sum_s partial[s,f,C*k*k] in split order. */
 int hnn_conv_wgrad_reduce(const hnn_conv_problem* probs, int nprob, int total_blocks, const hnn_step_row* cur,

@@ -130,6 +130,8 @@ SIGNATURES = {
     "hnn_conv_wgrad_reduce": [P, C.c_int, C.c_int, P, P, VP],
     "hnn_grouped_conv_direct": [C.c_int, P, C.c_int, C.c_int, C.c_int, P, P, VP],
     "hnn_conv_direct_smem": [C.c_int] * 8,
+    "hnn_conv_direct_threads": [C.c_int] * 8,
+    "hnn_grouped_conv_direct_ex": [C.c_int, P, C.c_int, C.c_int, C.c_int, C.c_int, P, P, VP],
     "hnn_grouped_maxpool": [C.c_int, P, C.c_int, C.c_int, P, P, VP],
     "hnn_grouped_relu": [C.c_int, P, C.c_int, C.c_int, P, P, VP],
     "hnn_sce_fused": [P, C.c_int, C.c_int, C.c_int, P, P, C.c_int, P, P, VP],
@@ -197,6 +199,10 @@ def conv_tile_shape(op: int) -> tuple:
 
 def conv_direct_smem(op, c, h, w, f, k, oh, ow) -> int:
     return int(load().hnn_conv_direct_smem(op, c, h, w, f, k, oh, ow))
+
+
+def conv_direct_threads(op, c, h, w, f, k, oh, ow) -> int:
+    return int(load().hnn_conv_direct_threads(op, c, h, w, f, k, oh, ow))
 
 
 def conv_direct_ok(c, h, w, f, k, oh, ow) -> bool:

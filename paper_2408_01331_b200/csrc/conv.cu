@@ -358,41 +358,72 @@ __device__ __forceinline__ int fwd_fg(const ConvGeom& g) {
   return ((g.f + 7) / 8) * g.oh * q >= 128 ? 8 : 4;
 }
 
-template <int K>
-__device__ __forceinline__ void direct_dgrad_blocked(const hnn_conv_problem& p, const ConvGeom& g, const float* ds,
-                                                     const float* ws, float* dxb, const float* mb) {
+// Input gradient, stride 1 (the transposed convolution in gather form): a thread computes CG
+// channels x RB consecutive inputs of one row from a zero-padded copy of dy (K - 1 zeros around
+// every plane: no bounds tests in the loop) and tap-major float4 weights (wt[(f*K + i)*K + j][c],
+// channels innermost, CP = C rounded up to 8), CG * RB FMAs per weight load.
+struct DgradLayout {
+  int pd, rows, rs, plane, cp;  // pad, padded rows, row stride, plane stride, padded channels
+  __host__ __device__ DgradLayout(int c, int h, int w, int k, int pad, int oh, int ow) {
+    pd = k - 1;
+    rows = oh + 2 * pd;
+    const int need = ((w + RB - 1) / RB) * RB + pad + k - 1;  // last quad's segment end
+    rs = max(ow + 2 * pd, need) | 1;                          // odd: rows spread over banks
+    plane = rows * rs;
+    cp = (c + 7) & ~7;
+  }
+};
+
+template <int K, int CG>
+__device__ __forceinline__ void direct_dgrad_blocked(const hnn_conv_problem& p, const ConvGeom& g, const DgradLayout& L,
+                                                     const float* dp, const float* wt, float* dxb, const float* mb) {
   const int qblocks = (g.w + RB - 1) / RB;
-  for (int e = threadIdx.x; e < g.c * g.h * qblocks; e += blockDim.x) {
-    const int c = e / (g.h * qblocks), rq = e - c * g.h * qblocks, y = rq / qblocks, x0 = (rq - y * qblocks) * RB;
-    float acc[RB] = {0.0f, 0.0f, 0.0f, 0.0f};
+  const int groups = (g.c + CG - 1) / CG;
+  for (int e = threadIdx.x; e < groups * g.h * qblocks; e += blockDim.x) {
+    const int cg = e / (g.h * qblocks), rq = e - cg * g.h * qblocks, y = rq / qblocks, x0 = (rq - y * qblocks) * RB;
+    const int c0 = cg * CG;
+    float acc[CG][RB];
+#pragma unroll
+    for (int cc = 0; cc < CG; ++cc)
+#pragma unroll
+      for (int q = 0; q < RB; ++q) acc[cc][q] = 0.0f;
     for (int f = 0; f < g.f; ++f) {
 #pragma unroll
       for (int i = 0; i < K; ++i) {
-        const int oy = y + g.pad - i;
-        if (oy < 0 || oy >= g.oh) continue;
-        const float* dr = ds + (f * g.oh + oy) * g.ow;
-        // dx[x] gets dy[x + pad - j] * w[j]; seg[t] = dy[x0 + pad - (K - 1) + t]
+        // dx[x] gets dy[x + pad - j] * w[j]: seg[t] = dy[y + pad - i][x0 + pad - (K - 1) + t], padded
+        const float* dr = dp + f * L.plane + (y + g.pad - i + L.pd) * L.rs + x0 + g.pad;
         float seg[RB + K - 1];
 #pragma unroll
-        for (int t = 0; t < RB + K - 1; ++t) {
-          const int ox = x0 + g.pad - (K - 1) + t;
-          seg[t] = (ox >= 0 && ox < g.ow) ? dr[ox] : 0.0f;
-        }
-        const float* wr = ws + ((f * g.c + c) * K + i) * K;
+        for (int t = 0; t < RB + K - 1; ++t) seg[t] = dr[t];
+        const float* wr = wt + size_t((f * K + i) * K) * L.cp + c0;
 #pragma unroll
         for (int j = 0; j < K; ++j) {
-          const float w = wr[j];
 #pragma unroll
-          for (int q = 0; q < RB; ++q) acc[q] = fmaf(seg[q + K - 1 - j], w, acc[q]);
+          for (int c4 = 0; c4 < CG / 4; ++c4) {
+            const float4 w = *reinterpret_cast<const float4*>(wr + j * L.cp + 4 * c4);
+#pragma unroll
+            for (int q = 0; q < RB; ++q) {
+              const float d = seg[q + K - 1 - j];
+              acc[4 * c4 + 0][q] = fmaf(d, w.x, acc[4 * c4 + 0][q]);
+              acc[4 * c4 + 1][q] = fmaf(d, w.y, acc[4 * c4 + 1][q]);
+              acc[4 * c4 + 2][q] = fmaf(d, w.z, acc[4 * c4 + 2][q]);
+              acc[4 * c4 + 3][q] = fmaf(d, w.w, acc[4 * c4 + 3][q]);
+            }
+          }
         }
       }
     }
 #pragma unroll
-    for (int q = 0; q < RB; ++q) {
-      const int x = x0 + q;
-      if (x >= g.w) break;
-      const int o = (c * g.h + y) * g.w + x;
-      dxb[o] = mb ? np_mask(acc[q], mb[o]) : acc[q];
+    for (int cc = 0; cc < CG; ++cc) {
+      const int c = c0 + cc;
+      if (c >= g.c) break;
+#pragma unroll
+      for (int q = 0; q < RB; ++q) {
+        const int x = x0 + q;
+        if (x >= g.w) break;
+        const int o = (c * g.h + y) * g.w + x;
+        dxb[o] = mb ? np_mask(acc[cc][q], mb[o]) : acc[cc][q];
+      }
     }
   }
 }
@@ -534,14 +565,31 @@ __global__ void __launch_bounds__(DTHREADS, 3) conv_direct_kernel(const hnn_conv
       for (int e = threadIdx.x; e < g.c * g.hw; e += blockDim.x) dxb[e] = 0.0f;
       return;
     }
+    const float* mb = p.mask ? p.mask + size_t(b) * g.c * g.hw : nullptr;
+    if (g.s == 1 && (g.k == 5 || g.k == 3) && g.pad <= g.k - 1) {
+      const DgradLayout L(g.c, g.h, g.w, g.k, g.pad, g.oh, g.ow);
+      float* dp = sm;                                    // [F][rows][rs] zero-padded dy planes
+      float* wt = sm + ((g.f * L.plane + 3) & ~3);       // [F*k*k][cp] tap-major weights
+      for (int e = threadIdx.x; e < g.f * L.plane; e += blockDim.x) dp[e] = 0.0f;
+      for (int e = threadIdx.x; e < g.f * g.k * g.k * L.cp; e += blockDim.x) {
+        const int t = e / L.cp, c = e - t * L.cp, f = t / (g.k * g.k), ij = t - f * g.k * g.k;
+        wt[e] = c < g.c ? __ldg(p.weight + (size_t(f) * g.c + c) * g.k * g.k + ij) : 0.0f;
+      }
+      __syncthreads();
+      stage_rows(dp + L.pd * L.rs + L.pd, p.dy + size_t(b) * g.f * g.ohw, g.f * g.oh, g.ow, g.oh, L.rs, L.plane);
+      __syncthreads();
+      const int groups8 = (g.c + 7) / 8, qb = (g.w + RB - 1) / RB;
+      const bool cg8 = groups8 * g.h * qb >= 128;
+      if (g.k == 5) return cg8 ? direct_dgrad_blocked<5, 8>(p, g, L, dp, wt, dxb, mb)
+                               : direct_dgrad_blocked<5, 4>(p, g, L, dp, wt, dxb, mb);
+      return cg8 ? direct_dgrad_blocked<3, 8>(p, g, L, dp, wt, dxb, mb)
+                 : direct_dgrad_blocked<3, 4>(p, g, L, dp, wt, dxb, mb);
+    }
     float* ds = sm;                  // [F][OH][OW]
     float* ws = sm + g.f * g.ohw;    // [F][C][k][k]
     stage(ds, p.dy + size_t(b) * g.f * g.ohw, g.f * g.ohw);
     stage(ws, p.weight, g.f * g.ckk);
     __syncthreads();
-    const float* mb = p.mask ? p.mask + size_t(b) * g.c * g.hw : nullptr;
-    if (g.s == 1 && g.k == 5) return direct_dgrad_blocked<5>(p, g, ds, ws, dxb, mb);
-    if (g.s == 1 && g.k == 3) return direct_dgrad_blocked<3>(p, g, ds, ws, dxb, mb);
     for (int e = threadIdx.x; e < g.c * g.hw; e += blockDim.x) {
       const int c = e / g.hw, pix = e - c * g.hw;
       const int y = pix / g.w, x = pix - y * g.w;
@@ -642,7 +690,14 @@ __host__ __device__ inline int conv_direct_smem(int op, int c, int h, int w, int
   const int ckk = c * k * k;
   const DirectLayout lay(c, h, w, k, oh, ow);
   if (op == HNN_FWD) return 4 * (((c * lay.cs + 3) & ~3) + ((f + 7) & ~7) * ckk);  // (filters padded: blocked path)
-  if (op == HNN_DGRAD) return 4 * (f * oh * ow + f * ckk);
+  if (op == HNN_DGRAD) {
+    const int pad = (h - oh + k - 1) / 2;  // stride 1: h = oh + k - 1 - 2 * pad
+    if (k == 5 || k == 3) {  // (the blocked path needs the padded layout; otherwise the plain one fits)
+      const DgradLayout L(c, h, w, k, pad, oh, ow);
+      return 4 * max(((f * L.plane + 3) & ~3) + f * k * k * L.cp, f * oh * ow + f * ckk);
+    }
+    return 4 * (f * oh * ow + f * ckk);
+  }
   // staged samples + the blocked stride-1 path's row-group partials (G <= 8 groups of f*c*k*k)
   return 4 * HNN_CONV_DIRECT_BCHUNK * (c * lay.cs + f * lay.ps) + 4 * 8 * f * c * k * k;
 }
@@ -653,9 +708,34 @@ extern "C" int hnn_conv_direct_smem(int op, int c, int h, int w, int f, int k, i
   return hnn::conv_direct_smem(op, c, h, w, f, k, oh, ow);
 }
 
+// Threads per CTA the direct kernel wants for a layer: 128 when the register-blocked stride-1 forward /
+// input gradient has at most 128 work items per sample (LeNet conv2: 120 / 112), so that twice as
+// many samples share an SM; 256 otherwise.
+extern "C" int hnn_conv_direct_threads(int op, int c, int h, int w, int f, int k, int oh, int ow) {
+  const int pad2 = oh - h + k - 1;  // 2 * padding of a stride-1 layer (the blocked paths)
+  const bool blocked = (k == 5 || k == 3) && pad2 >= 0 && pad2 % 2 == 0 && pad2 / 2 <= k - 1;
+  if (!blocked || op == HNN_WGRAD) return hnn::DTHREADS;
+  const int rows = op == HNN_FWD ? oh : h, qb = ((op == HNN_FWD ? ow : w) + hnn::RB - 1) / hnn::RB;
+  const int ch = op == HNN_FWD ? f : c;  // filters (forward) / channels (input gradient) per thread block
+  const int g8 = ((ch + 7) / 8) * rows * qb;
+  const int items = g8 >= 128 ? g8 : ((ch + 3) / 4) * rows * qb;
+  return items <= 128 ? 128 : hnn::DTHREADS;
+}
+
+extern "C" int hnn_grouped_conv_direct_ex(int op, const hnn_conv_problem* probs, int nprob, int total_blocks, int smem,
+                                          int threads, const hnn_step_row* cur, const hnn_model_status* status,
+                                          void* stream);
+
 extern "C" int hnn_grouped_conv_direct(int op, const hnn_conv_problem* probs, int nprob, int total_blocks, int smem,
                                        const hnn_step_row* cur, const hnn_model_status* status, void* stream) {
+  return hnn_grouped_conv_direct_ex(op, probs, nprob, total_blocks, smem, hnn::DTHREADS, cur, status, stream);
+}
+
+extern "C" int hnn_grouped_conv_direct_ex(int op, const hnn_conv_problem* probs, int nprob, int total_blocks, int smem,
+                                          int threads, const hnn_step_row* cur, const hnn_model_status* status,
+                                          void* stream) {
   HNN_REQUIRE(probs && cur && nprob > 0 && total_blocks > 0, "hnn_grouped_conv_direct", "bad arguments");
+  HNN_REQUIRE(threads >= 32 && threads <= hnn::DTHREADS && threads % 32 == 0, "hnn_grouped_conv_direct", "bad block size");
   HNN_REQUIRE(smem > 0 && smem <= 200 * 1024, "hnn_grouped_conv_direct", "layer too large for the direct path");
   cudaStream_t s = hnn::as_stream(stream);
   static int configured[3] = {0, 0, 0};
@@ -664,19 +744,19 @@ extern "C" int hnn_grouped_conv_direct(int op, const hnn_conv_problem* probs, in
       cudaFuncSetAttribute(hnn::conv_direct_kernel<HNN_FWD>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
       configured[0] = 200 * 1024;
     }
-    hnn::launch_pdl(hnn::conv_direct_kernel<HNN_FWD>, dim3(total_blocks), dim3(hnn::DTHREADS), smem, s, probs, nprob, cur, status);
+    hnn::launch_pdl(hnn::conv_direct_kernel<HNN_FWD>, dim3(total_blocks), dim3(threads), smem, s, probs, nprob, cur, status);
   } else if (op == HNN_DGRAD) {
     if (smem > configured[1]) {
       cudaFuncSetAttribute(hnn::conv_direct_kernel<HNN_DGRAD>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
       configured[1] = 200 * 1024;
     }
-    hnn::launch_pdl(hnn::conv_direct_kernel<HNN_DGRAD>, dim3(total_blocks), dim3(hnn::DTHREADS), smem, s, probs, nprob, cur, status);
+    hnn::launch_pdl(hnn::conv_direct_kernel<HNN_DGRAD>, dim3(total_blocks), dim3(threads), smem, s, probs, nprob, cur, status);
   } else if (op == HNN_WGRAD) {
     if (smem > configured[2]) {
       cudaFuncSetAttribute(hnn::conv_direct_kernel<HNN_WGRAD>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
       configured[2] = 200 * 1024;
     }
-    hnn::launch_pdl(hnn::conv_direct_kernel<HNN_WGRAD>, dim3(total_blocks), dim3(hnn::DTHREADS), smem, s, probs, nprob, cur, status);
+    hnn::launch_pdl(hnn::conv_direct_kernel<HNN_WGRAD>, dim3(total_blocks), dim3(threads), smem, s, probs, nprob, cur, status);
   } else {
     hnn::set_error("hnn_grouped_conv_direct", "unknown op");
     return HNN_ERR_INVALID;

@@ -261,6 +261,7 @@ GEMM_FAMILY = {N.PREC_SIMT: "gemm/simt", N.PREC_SIMT_SKINNY: "gemm/skinny", N.PR
 ENTRY_FAMILY = {"hnn_multi_tensor_adam": "optimizer", "hnn_multi_tensor_sgd": "optimizer", "hnn_sce_fused": "sce",
                 "hnn_gather_rows": "gather", "hnn_splitk_epilogue": "splitk_epilogue",
                 "hnn_grouped_conv": "conv/simt", "hnn_grouped_conv_direct": "conv/direct",
+                "hnn_grouped_conv_direct_ex": "conv/direct",
                 "hnn_conv_wgrad_reduce": "conv/wgrad_reduce", "hnn_embedding": "embed",
                 "hnn_grouped_maxpool": "pool", "hnn_grouped_relu": "relu", "hnn_conv_tc_aux": "conv/tc_aux"}
 
@@ -1275,7 +1276,7 @@ class DeviceHybrid:
     def _conv_group(self, op, items, label, direct):
         tm, tn = N.conv_tile_shape(op)
         probs, base, red, rbase = [], 0, [], 0
-        flops = smem = 0
+        flops = smem = threads = 0
         for s, st in items:
             c, h, w = st.in_shape
             f, oh, ow = self._conv_out(st)
@@ -1293,6 +1294,7 @@ class DeviceHybrid:
                 tiles_n = 1
                 tiles = st.splits if op == N.HNN_WGRAD else s.batch_size
                 smem = max(smem, N.conv_direct_smem(op, c, h, w, f, k, oh, ow))
+                threads = max(threads, N.conv_direct_threads(op, c, h, w, f, k, oh, ow))
             elif op == N.HNN_FWD:
                 tiles_n = -(-f // tn)
                 tiles = -(-(s.batch_size * oh * ow) // tm) * tiles_n
@@ -1310,8 +1312,8 @@ class DeviceHybrid:
             flops += 2 * s.batch_size * oh * ow * f * c * k * k
         t = _dev_table(N.ConvProblem, probs, self.device)
         if direct:
-            args = (op, _ptr(t), len(probs), base, smem, _ptr(self.cur), _ptr(self.status))
-            out = [Launch("hnn_grouped_conv_direct", args, t, label, flops=flops)]
+            args = (op, _ptr(t), len(probs), base, smem, threads, _ptr(self.cur), _ptr(self.status))
+            out = [Launch("hnn_grouped_conv_direct_ex", args, t, label, flops=flops)]
         else:
             out = [Launch("hnn_grouped_conv", (op, _ptr(t), len(probs), base, _ptr(self.cur), _ptr(self.status)), t,
                           label, flops=flops)]
