@@ -247,6 +247,13 @@ int hnn_gemm_tc_encode(int op, const hnn_gemm_problem* host_probs, int nprob, vo
  * ops.py:46-48).  Table fields: a = partials (lda = partial row stride), c = y (ldc), bias, relu,
  * m, n, ksplit, model; tile_base / tiles_n = the problem's first block and block count.
  */
+/* The logits layer's input and weight gradients in one pass over its input X (gemm_skinny.cu):
+ * wgrad_probs[i] / dgrad_probs[i] are the HNN_WGRAD / HNN_DGRAD problems of the same dense layer
+ * (tile_base / tiles_n in wgrad_probs: 128-column tiles), m <= 10 output units, no fused optimizer
+ * (W is read by every tile).  Results equal hnn_grouped_gemm's two skinny launches bit for bit. */
+int hnn_skinny_backward(const hnn_gemm_problem* wgrad_probs, const hnn_gemm_problem* dgrad_probs, int nprob,
+                        int total_tiles, const hnn_step_row* cur, const hnn_model_status* status, void* stream);
+
 int hnn_splitk_epilogue(const hnn_gemm_problem* probs, int nprob, int total_blocks, const hnn_step_row* cur,
                         const hnn_model_status* status, void* stream);
 int hnn_gemm_bf16_encode(int op, const hnn_gemm_problem* host_probs, int nprob, void* host_maps);

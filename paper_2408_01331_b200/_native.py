@@ -122,6 +122,7 @@ SIGNATURES = {
     "hnn_gemm_tile_shape": [C.c_int, C.c_int, C.POINTER(I), C.POINTER(I)],
     "hnn_gemm_chunk_terms": [C.c_int, C.POINTER(I)],
     "hnn_grouped_gemm": [C.c_int, C.c_int, P, C.c_int, C.c_int, P, P, VP],
+    "hnn_skinny_backward": [P, P, C.c_int, C.c_int, P, P, VP],
     "hnn_splitk_epilogue": [P, C.c_int, C.c_int, P, P, VP],
     "hnn_gemm_tc_encode": [C.c_int, C.c_void_p, C.c_int, C.c_void_p],
     "hnn_gemm_bf16_encode": [C.c_int, C.c_void_p, C.c_int, C.c_void_p],

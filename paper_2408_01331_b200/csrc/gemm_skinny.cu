@@ -318,6 +318,120 @@ __global__ void __launch_bounds__(KTHREADS) skinny_wgrad_kernel(const hnn_gemm_p
   else wgrad_tile<16>(p, cur[p.model], col, active, q, qd, dys, red, bias_thread);
 }
 
+// ------------------------------------------------------------------------ fused DGRAD + WGRAD
+// The logits layer's backward in one pass over its input X (the WGRAD operand and the DGRAD relu
+// mask are the same tensor): CTA = the WGRAD tile above (128 columns x 8 row groups); per row a
+// thread loads its X quad once, adds dY[r, :]^T x into its weight-gradient partial, and writes
+// dX[r, quad] = (dY[r, :] W[:, quad]) * (X > 0) with the DGRAD kernel's FMA order (bit-identical
+// to the two separate launches).  Only for problems without a fused optimizer: W must not change
+// while any CTA still reads it.  wp / dp: the WGRAD and DGRAD problems of the same layers, in the
+// same order (tile_base in wp); at most 10 output units (the host routes wider layers to the two
+// separate launches: 16 units' W quads and partials would not fit two CTAs' registers).
+template <int MJ>
+__device__ __forceinline__ void bwd_tile(const hnn_gemm_problem& p, const hnn_gemm_problem& d, const hnn_step_row& row,
+                                         int col, bool active, int q, int qd, float* dys, float* red, bool bias_thread) {
+  const int rows = row.rows;
+  float part[MJ][4];
+#pragma unroll
+  for (int j = 0; j < MJ; ++j) part[j][0] = part[j][1] = part[j][2] = part[j][3] = 0.0f;
+  float4 w[MJ];
+#pragma unroll
+  for (int j = 0; j < MJ; ++j) w[j] = (active && j < d.k) ? ldg4(d.b + size_t(j) * d.ldb + col) : make_float4(0, 0, 0, 0);
+  const bool own_mask = d.mask != nullptr && d.mask != p.b;  // (a mask other than X: loaded separately)
+  float bsum = -0.0f;
+  for (int base = 0; base < rows; base += WG_CHUNK) {
+    const int n = min(WG_CHUNK, rows - base);
+    __syncthreads();
+    for (int e = threadIdx.x; e < WG_CHUNK * 16; e += KTHREADS) {
+      const int r = e >> 4, j = e & 15;
+      dys[e] = (j < p.m && r < n) ? __ldg(p.a + size_t(base + r) * p.lda + j) : 0.0f;
+    }
+    __syncthreads();
+    if (bias_thread)  // numpy's axis-0 sum: sequential row order per column
+      for (int r = 0; r < n; ++r) bsum = __fadd_rn(bsum, dys[r * 16 + threadIdx.x]);
+    if (active) {
+      const int r_lo = base + (n * q) / WG_GROUPS, r_hi = base + (n * (q + 1)) / WG_GROUPS;
+      const float* x = p.b + col;
+#pragma unroll 4
+      for (int r = r_lo; r < r_hi; ++r) {
+        const float4 xv = ldg4(x + size_t(r) * p.ldb);
+        const float* dr = dys + (r - base) * 16;
+        float4 o = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
+#pragma unroll
+        for (int j = 0; j < MJ; ++j) {
+          const float dj = dr[j];
+          part[j][0] = fmaf(dj, xv.x, part[j][0]);
+          part[j][1] = fmaf(dj, xv.y, part[j][1]);
+          part[j][2] = fmaf(dj, xv.z, part[j][2]);
+          part[j][3] = fmaf(dj, xv.w, part[j][3]);
+          o.x = fmaf(dj, w[j].x, o.x);
+          o.y = fmaf(dj, w[j].y, o.y);
+          o.z = fmaf(dj, w[j].z, o.z);
+          o.w = fmaf(dj, w[j].w, o.w);
+        }
+        if (d.mask) {
+          const float4 mk = own_mask ? ldg4(d.mask + size_t(r) * d.ldc + col) : xv;
+          o.x = np_mask(o.x, mk.x);
+          o.y = np_mask(o.y, mk.y);
+          o.z = np_mask(o.z, mk.z);
+          o.w = np_mask(o.w, mk.w);
+        }
+        *reinterpret_cast<float4*>(d.c + size_t(r) * d.ldc + col) = o;
+      }
+    }
+  }
+  if (active)  // rows past this step's batch: exact zeros (as the DGRAD kernel writes them)
+    for (int r = rows + q; r < d.m; r += WG_GROUPS)
+      *reinterpret_cast<float4*>(d.c + size_t(r) * d.ldc + col) = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
+  if (bias_thread && p.dbias) p.dbias[threadIdx.x] = bsum;
+  if (q > 0) {
+    float* dst = red + (size_t(q - 1) * WG_QUADS + qd) * 64;
+#pragma unroll
+    for (int j = 0; j < MJ; ++j)
+      *reinterpret_cast<float4*>(dst + j * 4) = make_float4(part[j][0], part[j][1], part[j][2], part[j][3]);
+  }
+  __syncthreads();
+  if (q != 0 || !active) return;
+  for (int g = 0; g < WG_GROUPS - 1; ++g) {  // row groups summed in fixed order 0 + 1 + ... + 7
+    const float* src = red + (size_t(g) * WG_QUADS + qd) * 64;
+#pragma unroll
+    for (int j = 0; j < MJ; ++j) {
+      const float4 v = *reinterpret_cast<const float4*>(src + j * 4);
+      part[j][0] += v.x;
+      part[j][1] += v.y;
+      part[j][2] += v.z;
+      part[j][3] += v.w;
+    }
+  }
+#pragma unroll
+  for (int j = 0; j < MJ; ++j) {
+    if (j >= p.m) break;
+    if (p.c) *reinterpret_cast<float4*>(p.c + size_t(j) * p.ldc + col) = make_float4(part[j][0], part[j][1], part[j][2], part[j][3]);
+  }
+}
+
+__global__ void __launch_bounds__(KTHREADS, 2) skinny_bwd_kernel(const hnn_gemm_problem* __restrict__ wprobs,
+                                                                 const hnn_gemm_problem* __restrict__ dprobs, int nprob,
+                                                                 const hnn_step_row* __restrict__ cur,
+                                                                 const hnn_model_status* __restrict__ status) {
+  hnn::pdl_wait();
+  extern __shared__ __align__(16) float wg_smem[];
+  float* dys = wg_smem;
+  float* red = wg_smem + WG_CHUNK * 16;
+  const int pi = find_problem(wprobs, nprob, blockIdx.x, [](const hnn_gemm_problem& q) { return q.tile_base; });
+  const hnn_gemm_problem& p = wprobs[pi];
+  const hnn_gemm_problem& d = dprobs[pi];
+  if (!live(cur, status, p.model)) return;
+  const int n0 = (blockIdx.x - p.tile_base) * (4 * WG_QUADS);
+  const int qd = threadIdx.x % WG_QUADS, q = threadIdx.x / WG_QUADS;
+  const int col = n0 + qd * 4;
+  const bool active = col < p.n;
+  const bool bias_thread = n0 == 0 && threadIdx.x < p.m && p.dbias;
+  if (p.m <= 4) bwd_tile<4>(p, d, cur[p.model], col, active, q, qd, dys, red, bias_thread);
+  else if (p.m <= 8) bwd_tile<8>(p, d, cur[p.model], col, active, q, qd, dys, red, bias_thread);
+  else bwd_tile<10>(p, d, cur[p.model], col, active, q, qd, dys, red, bias_thread);  // (host: m <= 10)
+}
+
 int skinny_tile_shape(int op, int32_t* tm, int32_t* tn) {
   if (op == HNN_FWD) { *tm = 8 * FWD_ROWS; *tn = 16; }
   else if (op == HNN_DGRAD) { *tm = 8 * DG_ROWS; *tn = 128; }
@@ -344,3 +458,18 @@ int grouped_gemm_skinny(int op, const hnn_gemm_problem* probs, int nprob, int to
 }
 
 }  // namespace hnn
+
+extern "C" int hnn_skinny_backward(const hnn_gemm_problem* wgrad_probs, const hnn_gemm_problem* dgrad_probs, int nprob,
+                                   int total_tiles, const hnn_step_row* cur, const hnn_model_status* status,
+                                   void* stream) {
+  HNN_REQUIRE(wgrad_probs && dgrad_probs && cur && nprob > 0 && total_tiles > 0, "hnn_skinny_backward", "bad arguments");
+  constexpr int smem = (hnn::WG_CHUNK * 16 + (hnn::WG_GROUPS - 1) * hnn::WG_QUADS * 64) * 4;  // 72 KB
+  static bool configured = false;
+  if (!configured) {
+    cudaFuncSetAttribute(hnn::skinny_bwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    configured = true;
+  }
+  hnn::launch_pdl(hnn::skinny_bwd_kernel, dim3(total_tiles), dim3(hnn::KTHREADS), smem, hnn::as_stream(stream),
+                  wgrad_probs, dgrad_probs, nprob, cur, status);
+  return hnn::check_launch("hnn_skinny_backward");
+}

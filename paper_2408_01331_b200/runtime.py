@@ -261,7 +261,7 @@ GEMM_FAMILY = {N.PREC_SIMT: "gemm/simt", N.PREC_SIMT_SKINNY: "gemm/skinny", N.PR
 ENTRY_FAMILY = {"hnn_multi_tensor_adam": "optimizer", "hnn_multi_tensor_sgd": "optimizer", "hnn_sce_fused": "sce",
                 "hnn_gather_rows": "gather", "hnn_splitk_epilogue": "splitk_epilogue",
                 "hnn_grouped_conv": "conv/simt", "hnn_grouped_conv_direct": "conv/direct",
-                "hnn_grouped_conv_direct_ex": "conv/direct",
+                "hnn_grouped_conv_direct_ex": "conv/direct", "hnn_skinny_backward": "gemm/skinny",
                 "hnn_conv_wgrad_reduce": "conv/wgrad_reduce", "hnn_embedding": "embed",
                 "hnn_grouped_maxpool": "pool", "hnn_grouped_relu": "relu", "hnn_conv_tc_aux": "conv/tc_aux"}
 
@@ -722,6 +722,60 @@ class DeviceHybrid:
         """items: list of (slot, stage).  Splits into SIMT / 3xTF32 launches."""
         groups = {N.PREC_SIMT: [], N.PREC_SIMT_SKINNY: [], N.PREC_3XTF32: [], N.PREC_3XTF32_PAIR: []}
         for s, st in items:
+            d = self._gemm_problem(op, s, st)
+            groups[self._gemm_prec(op, d)].append((s, d))
+        out = []
+        for prec, rows in groups.items():
+            if rows:
+                out += self._emit_gemm(op, prec, rows, label)
+        return out
+
+    def _gemm_prec(self, op, d) -> int:
+        if self.use_tc and self._route_tc(op, d):
+            # CTA-pair 256x256 tiles (one launch per wave, LPT-scheduled); HNN_TC_PAIR=0
+            # selects the single-CTA 128x128 kernel
+            return N.PREC_3XTF32_PAIR if self.use_pairs else N.PREC_3XTF32
+        if self._route_skinny(op, d):
+            return N.PREC_SIMT_SKINNY
+        return N.PREC_SIMT
+
+    def _skinny_backward(self, items):
+        """Dense layers of a backward wave whose input gradient and weight gradient both take the
+        skinny kernels (the <= 10-class logits layer), without a fused optimizer: one fused launch
+        (hnn_skinny_backward) reads their input once for both.  Returns (launches, fused items)."""
+        if os.environ.get("HNN_SKINNY_FUSED", "1") == "0":
+            return [], []
+        pairs = []
+        for s, st in items:
+            if st.kind != "dense" or not st.needs_dx:
+                continue
+            dg, wg = self._gemm_problem(N.HNN_DGRAD, s, st), self._gemm_problem(N.HNN_WGRAD, s, st)
+            if (self._gemm_prec(N.HNN_DGRAD, dg) == N.PREC_SIMT_SKINNY and self._gemm_prec(N.HNN_WGRAD, wg)
+                    == N.PREC_SIMT_SKINNY and not wg.get("opt_w") and wg["m"] <= 10 and dg["k"] == wg["m"]):
+                pairs.append((s, st, dg, wg))
+        if not pairs:
+            return [], []
+        tn = 4 * 32  # columns per CTA (gemm_skinny.cu WG_QUADS float4 quads)
+        wp, dp, base = [], [], 0
+        for s, st, dg, wg in sorted(pairs, key=lambda t: -t[3]["n"]):
+            tiles = -(-wg["n"] // tn)
+            wp.append(N.GemmProblem(tile_base=base, tiles_n=tiles, model=s.index, **wg))
+            dp.append(N.GemmProblem(tile_base=base, tiles_n=tiles, model=s.index, **dg))
+            base += tiles
+        t = _dev_table(N.GemmProblem, wp + dp, self.device)
+        import ctypes
+
+        size = ctypes.sizeof(N.GemmProblem)
+        nbytes = sum(4 * (2 * d["m"] * d["n"] + w["k"] * w["m"] * 2 + w["m"] * w["n"]) for _, _, d, w in pairs)
+        flops = sum(4 * w["m"] * w["n"] * w["k"] for _, _, _, w in pairs)
+        label = "dense/skinny_bwd"
+        launch = Launch("hnn_skinny_backward", (_ptr(t), _ptr(t) + size * len(wp), len(wp), base, _ptr(self.cur),
+                                                _ptr(self.status)), t, label, flops=flops, nbytes=nbytes)
+        return [launch], [(s, st) for s, st, _, _ in pairs]
+
+    def _gemm_problem(self, op, s, st) -> dict:
+        """The grouped-GEMM problem dict of dense stage st of slot s for op."""
+        if True:
             cap = s.batch_size
             K, U = int(np.prod(st.in_shape)), st.out_shape[0]
             w = self.pview(self.params, s.index, st.params[0])
@@ -748,20 +802,7 @@ class DeviceHybrid:
                              opt_wv=arena(self.m2, st.params[0]) if kind == N.OPT_ADAM else 0,
                              opt_bv=arena(self.m2, st.params[1]) if kind == N.OPT_ADAM else 0,
                              opt_kind=kind, opt_momentum=float(np.float32(s.momentum)))
-            if self.use_tc and self._route_tc(op, d):
-                # CTA-pair 256x256 tiles (one launch per wave, LPT-scheduled); HNN_TC_PAIR=0
-                # selects the single-CTA 128x128 kernel
-                prec = N.PREC_3XTF32_PAIR if self.use_pairs else N.PREC_3XTF32
-            elif self._route_skinny(op, d):
-                prec = N.PREC_SIMT_SKINNY
-            else:
-                prec = N.PREC_SIMT
-            groups[prec].append((s, d))
-        out = []
-        for prec, rows in groups.items():
-            if rows:
-                out += self._emit_gemm(op, prec, rows, label)
-        return out
+            return d
 
     def _pair_tile_cap(self, op, rows, tm) -> int:
         """Widest pair-tile width (256 / 128 / 64) for one launch: narrower tiles put more CTA pairs
@@ -1509,11 +1550,16 @@ class DeviceHybrid:
             # input gradients first: with optimizer fusion the weight-gradient launch updates W in
             # place, and this wave's DGRAD must still read the pre-update W (src/engine.py:120-151
             # computes every gradient before apply_update)
-            dg = [(s, st) for s, st in items if st.needs_dx]
+            fused_l, fused = self._skinny_backward(items)
+            for l in fused_l:
+                l.label = f"bwd{w}/dense/skinny_bwd"
+            done = {id(st) for _, st in fused}
+            dg = [(s, st) for s, st in items if st.needs_dx and id(st) not in done]
             if dg:
                 bwd += self._wave_launches(N.HNN_DGRAD, dg, f"bwd{w}")
+            bwd += fused_l
             for kind in ("dense", "conv", "embed"):
-                grp = [(s, st) for s, st in items if st.kind == kind]
+                grp = [(s, st) for s, st in items if st.kind == kind and id(st) not in done]
                 if grp:
                     if kind == "dense":
                         bwd += self._gemm_launch(N.HNN_WGRAD, grp, f"bwd{w}/dense/wgrad")

@@ -1007,6 +1007,35 @@ def test_split_k_forward_is_bit_identical(pkg, monkeypatch):
             assert np.array_equal(a[k], b[k]), k
 
 
+def test_fused_skinny_backward_is_bit_identical(pkg, monkeypatch):
+    """C3's logits layers (784-h-h-10, Adam: no optimizer fused into the weight gradient) take one
+    hnn_skinny_backward launch for their input and weight gradients; 3 steps end bit-identical (params,
+    gradients, Adam moments) to the two separate skinny launches (src/ops.py:51-55)."""
+    import torch
+
+    import bench
+
+    device = torch.device("cuda", 0)
+    outs = []
+    for fused in ("1", "0"):
+        monkeypatch.setenv("HNN_SKINNY_FUSED", fused)
+        _, jobs, hy, dev, ddev, ds, comm = bench.build_rank("c3", 0, 1, device)
+        labels = [l.label for l in dev.train_plan]
+        assert any(l.endswith("/skinny_bwd") for l in labels) == (fused == "1"), labels
+        rows = bench.schedule(jobs, ds, 3)
+        bench.upload_perms(dev, jobs, ds)
+        dev.load_schedule(rows)
+        dev.train_steps(3, use_graph=True)
+        torch.cuda.synchronize()
+        outs.append([(dev.download_params(m), dev.download_grads(m), dev.download_moments(m)[1])
+                     for m in (0, 13, 31)])
+    for (pa, ga, va), (pb, gb, vb) in zip(*outs):
+        for k in pa:
+            assert np.array_equal(pa[k], pb[k]), k
+            assert np.array_equal(ga[k], gb[k]), k
+            assert np.array_equal(va[k], vb[k]), k
+
+
 def test_tf32_truncation_selftest(pkg):
     """The load-time check behind the 3xTF32 split (gemm_tc2.cu:11-13): raw fp32 operands are
     truncated to tf32 by the tensor core, so hi + lo reproduce x; the probe GEMM then misses only
