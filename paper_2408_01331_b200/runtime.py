@@ -1064,7 +1064,7 @@ class DeviceHybrid:
         of whole 64-element K blocks, raw partial sums stacked [S, m rounded to 32, n] and finished
         in order by HNN_CONVTC_SPLITK_FWD (+ bias, relu, NCHW, NHWC copy, relu mask).  Returns
         (problem dict, finish description or None)."""
-        if not st.bf16 or os.environ.get("HNN_CONV_SPLITK", "1") == "0":
+        if not st.bf16 or os.environ.get("HNN_CONV_SPLITK", "0") == "0":  # measured slower on every C4 layer (off)
             return d, None
         M, F, K = d["m"], d["n"], d["k"]
         tn = 64 if F <= 64 else (128 if F <= 128 else 256)
