@@ -667,6 +667,8 @@ class DeviceHybrid:
         """Dense problems big and aligned enough for the tcgen05 tiles go to the 3xTF32 kernels.
         The CTA-pair kernel takes short batches too (64 rows: a quarter of its 256-row tile still
         beats the FFMA path 3x on C5's first layer); the single-CTA kernel needs 128 rows."""
+        # (the 10-class logits forward on the pair kernel at tile width 64 measured slower than the
+        # streaming skinny kernel: C3 39 -> 67 us, profiles/r02/narrow_fwd_ab_v7.txt)
         if d["m"] < (32 if self.use_pairs else 128) or d["n"] < 64 or d["k"] < 64:
             return False
         if op == N.HNN_WGRAD and d["m"] > 4096:
