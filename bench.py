@@ -338,6 +338,15 @@ def roofline(dev, per_launch_ms, workload):
                     "peak_source": (f"{kind} bf16 burst (MEASURED_PEAKS.json)" if bf16 else
                                     f"3xTF32 useful-FLOP ceiling = measured tf32 tcgen05 rate {TF32_RATE} TF/s / 3 "
                                     "(profiles/r01/mma_rate_micro.txt)")})
+    elif f["flops"] and not f["nbytes"]:
+        # CUDA-core FP32 kernels (the direct convolutions of LeNet-class layers): the FFMA roofline,
+        # nominal (148 SMs x 128 FMA lanes x 2 FLOP x the 1965 MHz max clock; no measured figure)
+        peak = round(148 * 128 * 2 * 1.965e9 / 1e12, 1)
+        achieved = f["flops"] / sec / 1e12
+        out.update({"bound": "fp32-fma", "achieved": round(achieved, 2), "peak": peak, "unit": "TFLOP/s",
+                    "frac": round(achieved / peak, 4), "traffic": traffic,
+                    "algorithmic": f"{f['flops']} useful FLOP per step (2*B*OH*OW*F*C*k*k per conv)",
+                    "peak_source": "nominal FFMA peak, 148 SMs x 128 lanes x 2 x 1.965 GHz"})
     else:
         achieved = f["nbytes"] / sec / 1e9
         out.update({"bound": "hbm", "achieved": round(achieved, 1), "peak": hbm, "unit": "GB/s",
