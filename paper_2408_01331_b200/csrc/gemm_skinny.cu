@@ -10,6 +10,8 @@
 //                                                 quarter of the rows, quarters reduced in order;
 //                                                 bias gradient and the fused optimizer included
 // Tiling is a fixed function of each problem's shape (bit-exact isolation); no atomics.
+#include <cstdlib>
+
 #include "common.cuh"
 
 namespace hnn {
@@ -113,6 +115,143 @@ __global__ void __launch_bounds__(KTHREADS) skinny_fwd_kernel(const hnn_gemm_pro
   const int r0 = (blockIdx.x - p.tile_base) * (8 * FWD_ROWS) + warp * FWD_ROWS;
   if (r0 >= p.m) return;
   // CTA-uniform dispatch on the column count: loads and FMAs carry no per-column branches
+  if (p.n <= 4) rowdot_rows<4>(p, r0, rows, lane);
+  else if (p.n <= 8) rowdot_rows<8>(p, r0, rows, lane);
+  else if (p.n <= 10) rowdot_rows<10>(p, r0, rows, lane);
+  else if (p.n <= 12) rowdot_rows<12>(p, r0, rows, lane);
+  else rowdot_rows<16>(p, r0, rows, lane);
+}
+
+// FWD, bulk-copy form (problems with 16-byte rows and K % 128 == 0: the C1 / C3 / C5 logits
+// layers): the same 16-row tile, its x rows and the n <= 16 W rows streamed through a 4-stage
+// shared-memory ring in 128-float K chunks by a producer warp (cp.async.bulk, one row per lane), 256
+// update threads = 16 rows x 16 K-slices (float4 each), slices combined by a fixed xor tree.  The
+// per-warp streaming form walked each row's whole K as a chain of dependent L2 / HBM round trips
+// at 24 warps per SM (C3: 39 us for 35.6 MB, ncu long-scoreboard bound).  Other problems take the
+// per-warp form inside the same launch (the tile shape is shared).
+constexpr int FB_KC = 128, FB_STAGES = 4, FB_THREADS = KTHREADS + 32;
+constexpr int FB_STAGE_BYTES = 2 * 16 * FB_KC * 4;  // 16 x rows + 16 W rows
+constexpr int FB_SMEM = FB_STAGES * FB_STAGE_BYTES + 256;
+
+__device__ __forceinline__ bool fwd_bulk_ok(const hnn_gemm_problem& p) {
+  return p.n <= 16 && (p.k % FB_KC) == 0 && (p.lda & 3) == 0 && (p.ldb & 3) == 0 &&
+         (reinterpret_cast<uintptr_t>(p.a) & 15) == 0 && (reinterpret_cast<uintptr_t>(p.b) & 15) == 0;
+}
+
+template <int NJ>
+__device__ __forceinline__ void fwd_bulk_tile(const hnn_gemm_problem& p, int r0, int rows, uint8_t* smem) {
+  const uint32_t ring = static_cast<uint32_t>(__cvta_generic_to_shared(smem));
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + FB_STAGES * FB_STAGE_BYTES);
+  auto bar = [&](int i) { return static_cast<uint32_t>(__cvta_generic_to_shared(bars + i)); };
+  auto wait = [&](uint32_t b, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred P1;\n"
+        "FB_WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+        "@!P1 bra FB_WAIT_%=;\n\t}" ::"r"(b),
+        "r"(parity)
+        : "memory");
+  };
+  const int nchunks = p.k / FB_KC;
+  const int xrows = min(16, p.m - r0);  // rows of this tile inside the buffer (cap)
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  if (warp == KTHREADS / 32) {
+    // ---------------- producer warp: lanes 0..15 copy x rows, lanes 16..31 W rows
+    const uint32_t bytes = uint32_t(xrows + p.n) * FB_KC * 4;
+    for (int c = 0; c < nchunks; ++c) {
+      const int st = c % FB_STAGES;
+      if (c >= FB_STAGES) wait(bar(FB_STAGES + st), ((c / FB_STAGES) - 1) & 1);
+      if (lane == 0)
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar(st)), "r"(bytes) : "memory");
+      __syncwarp();
+      const uint32_t dst = ring + st * FB_STAGE_BYTES;
+      const float* src = nullptr;
+      uint32_t d = 0;
+      if (lane < 16 && lane < xrows) {
+        src = p.a + size_t(r0 + lane) * p.lda + c * FB_KC;
+        d = dst + lane * FB_KC * 4;
+      } else if (lane >= 16 && lane - 16 < p.n) {
+        src = p.b + size_t(lane - 16) * p.ldb + c * FB_KC;
+        d = dst + (16 + lane - 16) * FB_KC * 4;
+      }
+      if (src)
+        asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(d),
+                     "l"(src), "r"(FB_KC * 4), "r"(bar(st))
+                     : "memory");
+    }
+    return;
+  }
+  // ---------------- 16 rows x 16 K-slices
+  const int r = threadIdx.x / 16, sl = threadIdx.x % 16;
+  float acc[NJ];
+#pragma unroll
+  for (int j = 0; j < NJ; ++j) acc[j] = 0.0f;
+  for (int c = 0; c < nchunks; ++c) {
+    const int st = c % FB_STAGES;
+    wait(bar(st), (c / FB_STAGES) & 1);
+    const float* xs = reinterpret_cast<const float*>(smem + st * FB_STAGE_BYTES) + r * FB_KC;
+    const float* ws = reinterpret_cast<const float*>(smem + st * FB_STAGE_BYTES) + 16 * FB_KC;
+#pragma unroll
+    for (int i = 0; i < FB_KC / 64; ++i) {
+      const int k = (sl + 16 * i) * 4;
+      const float4 u = *reinterpret_cast<const float4*>(xs + k);
+#pragma unroll
+      for (int j = 0; j < NJ; ++j) acc[j] = dot4(u, *reinterpret_cast<const float4*>(ws + j * FB_KC + k), acc[j]);
+    }
+    asm volatile("bar.sync 1, %0;" ::"n"(KTHREADS) : "memory");  // every slice has read stage st
+    if (threadIdx.x == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar(FB_STAGES + st)) : "memory");
+  }
+  // fixed xor tree over the 16 slices of a row (lanes 16 apart never mix: offsets < 16)
+#pragma unroll
+  for (int j = 0; j < NJ; ++j)
+#pragma unroll
+    for (int o = 8; o > 0; o >>= 1) acc[j] += __shfl_xor_sync(0xffffffffu, acc[j], o);
+  const int row = r0 + r;
+  if (row >= p.m) return;
+  // slice lane sl writes column sl (sl < n): lane-local select of acc[sl]
+  float v = 0.0f;
+#pragma unroll
+  for (int j = 0; j < NJ; ++j)
+    if (j == sl) v = acc[j];
+  if (sl >= p.n) return;
+  float y = 0.0f;
+  if (row < rows) {
+    y = __fadd_rn(v, __ldg(p.bias + sl));
+    if (p.relu) y = np_relu(y);
+  }
+  p.c[size_t(row) * p.ldc + sl] = y;
+}
+
+__global__ void __launch_bounds__(FB_THREADS) skinny_fwd_bulk_kernel(const hnn_gemm_problem* __restrict__ probs,
+                                                                     int nprob, const hnn_step_row* __restrict__ cur,
+                                                                     const hnn_model_status* __restrict__ status) {
+  hnn::pdl_wait();
+  extern __shared__ __align__(128) uint8_t fb_smem[];
+  const int pi = find_problem(probs, nprob, blockIdx.x, [](const hnn_gemm_problem& q) { return q.tile_base; });
+  const hnn_gemm_problem& p = probs[pi];
+  if (!live(cur, status, p.model)) return;
+  const int rows = cur[p.model].rows;
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const int t0 = (blockIdx.x - p.tile_base) * (8 * FWD_ROWS);
+  if (t0 >= p.m) return;
+  if (fwd_bulk_ok(p)) {
+    if (threadIdx.x == 0) {
+      uint64_t* bars = reinterpret_cast<uint64_t*>(fb_smem + FB_STAGES * FB_STAGE_BYTES);
+      for (int i = 0; i < 2 * FB_STAGES; ++i)
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(static_cast<uint32_t>(__cvta_generic_to_shared(bars + i))));
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    if (p.n <= 4) fwd_bulk_tile<4>(p, t0, rows, fb_smem);
+    else if (p.n <= 8) fwd_bulk_tile<8>(p, t0, rows, fb_smem);
+    else if (p.n <= 10) fwd_bulk_tile<10>(p, t0, rows, fb_smem);
+    else if (p.n <= 12) fwd_bulk_tile<12>(p, t0, rows, fb_smem);
+    else fwd_bulk_tile<16>(p, t0, rows, fb_smem);
+    return;
+  }
+  if (warp >= KTHREADS / 32) return;  // (the per-warp form: 8 warps x FWD_ROWS rows)
+  const int r0 = t0 + warp * FWD_ROWS;
+  if (r0 >= p.m) return;
   if (p.n <= 4) rowdot_rows<4>(p, r0, rows, lane);
   else if (p.n <= 8) rowdot_rows<8>(p, r0, rows, lane);
   else if (p.n <= 10) rowdot_rows<10>(p, r0, rows, lane);
@@ -442,7 +581,16 @@ int skinny_tile_shape(int op, int32_t* tm, int32_t* tn) {
 int grouped_gemm_skinny(int op, const hnn_gemm_problem* probs, int nprob, int total_tiles, const hnn_step_row* cur,
                         const hnn_model_status* status, cudaStream_t s) {
   if (op == HNN_FWD) {
-    hnn::launch_pdl(skinny_fwd_kernel, dim3(total_tiles), dim3(KTHREADS), 0, s, probs, nprob, cur, status);
+    static int bulk = -1;
+    if (bulk < 0) {
+      const char* e = getenv("HNN_SKINNY_FWD_BULK");
+      bulk = e ? atoi(e) : 1;
+      if (bulk) cudaFuncSetAttribute(skinny_fwd_bulk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, FB_SMEM);
+    }
+    if (bulk)
+      hnn::launch_pdl(skinny_fwd_bulk_kernel, dim3(total_tiles), dim3(FB_THREADS), FB_SMEM, s, probs, nprob, cur, status);
+    else
+      hnn::launch_pdl(skinny_fwd_kernel, dim3(total_tiles), dim3(KTHREADS), 0, s, probs, nprob, cur, status);
   } else if (op == HNN_DGRAD) {
     hnn::launch_pdl(skinny_dgrad_kernel, dim3(total_tiles), dim3(KTHREADS), 0, s, probs, nprob, cur, status);
   } else {
