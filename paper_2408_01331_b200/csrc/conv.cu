@@ -428,60 +428,77 @@ __device__ __forceinline__ void direct_dgrad_blocked(const hnn_conv_problem& p, 
   }
 }
 
-// Weight gradient of one staged sample, stride 1: a thread owns (f, c, i) and the K taps j of that
-// filter row, sweeping the output rows of its row group; per 4 outputs it loads 4 dy values and
-// one 4 + K - 1 input segment for 4 * K FMAs.  G row groups (fixed) are combined in order.
-template <int K>
+// Weight gradient of one staged sample, stride 1: a thread owns FG filters x one input row (c, i)
+// and the K taps j of those filter rows, sweeping the output rows of its row group; per 4 outputs it
+// loads one 4 + K - 1 input segment and 4 dy values per filter for FG * 4 * K FMAs (one filter per
+// thread loaded the segment once per 4 * K FMAs: issue-bound, FMA pipe 27%, profiles/r02).  G row
+// groups (fixed) are combined in order.
+template <int K, int FG>
 __device__ __forceinline__ void direct_wgrad_blocked(const hnn_conv_problem& p, const ConvGeom& g, const float* xs,
                                                      int cs, int rs, const float* ds, int ps, int nb, float* red,
                                                      float* out) {
-  const int nrow = g.f * g.c * K;  // (f, c, i) filter rows
+  const int fgroups = (g.f + FG - 1) / FG;
+  const int nrow = fgroups * g.c * K;  // (filter group, c, i) work rows
   const int G = max(1, min(8, int(blockDim.x) / nrow));
   const int cols = g.ckk + 1;
+  const int frow = g.f * g.c * K;      // (f, c, i) filter rows of the partial layout
   const int qblocks = (g.ow + RB - 1) / RB;
   for (int t = threadIdx.x; t < nrow * G; t += blockDim.x) {
     const int grp = t / nrow, rrow = t - grp * nrow;
-    const int f = rrow / (g.c * K), ci = rrow - f * g.c * K, c = ci / K, i = ci - c * K;
-    float acc[K];
+    const int fg = rrow / (g.c * K), ci = rrow - fg * g.c * K, c = ci / K, i = ci - c * K;
+    const int f0 = fg * FG;
+    float acc[FG][K];
 #pragma unroll
-    for (int j = 0; j < K; ++j) acc[j] = 0.0f;
+    for (int ff = 0; ff < FG; ++ff)
+#pragma unroll
+      for (int j = 0; j < K; ++j) acc[ff][j] = 0.0f;
     for (int sb = 0; sb < nb; ++sb) {
-      const float* df = ds + (sb * g.f + f) * ps;
       const float* xc = xs + (sb * g.c + c) * cs;
       for (int oy = grp; oy < g.oh; oy += G) {
         const int y = oy - g.pad + i;
         if (y < 0 || y >= g.h) continue;
         const float* xr = xc + y * rs;
-        const float* dr = df + oy * g.ow;
         for (int qb = 0; qb < qblocks; ++qb) {
           const int ox0 = qb * RB;
-          float d[RB], seg[RB + K - 1];
-#pragma unroll
-          for (int q = 0; q < RB; ++q) d[q] = ox0 + q < g.ow ? dr[ox0 + q] : 0.0f;
+          float seg[RB + K - 1];
 #pragma unroll
           for (int u = 0; u < RB + K - 1; ++u) {
             const int x = ox0 - g.pad + u;
             seg[u] = (x >= 0 && x < g.w) ? xr[x] : 0.0f;
           }
 #pragma unroll
-          for (int j = 0; j < K; ++j)
+          for (int ff = 0; ff < FG; ++ff) {
+            const int f = min(f0 + ff, g.f - 1);  // (a padded filter recomputes the last: discarded)
+            const float* dr = ds + (sb * g.f + f) * ps + oy * g.ow;
+            float d[RB];
 #pragma unroll
-            for (int q = 0; q < RB; ++q) acc[j] = fmaf(d[q], seg[q + j], acc[j]);
+            for (int q = 0; q < RB; ++q) d[q] = ox0 + q < g.ow ? dr[ox0 + q] : 0.0f;
+#pragma unroll
+            for (int j = 0; j < K; ++j)
+#pragma unroll
+              for (int q = 0; q < RB; ++q) acc[ff][j] = fmaf(d[q], seg[q + j], acc[ff][j]);
+          }
         }
       }
     }
     // group 0 -> slot G-1, group g > 0 -> slot g-1 (combined in group order after the barrier)
     const int slot = grp > 0 ? grp - 1 : G - 1;
 #pragma unroll
-    for (int j = 0; j < K; ++j) red[(slot * nrow + rrow) * K + j] = acc[j];
+    for (int ff = 0; ff < FG; ++ff) {
+      const int f = f0 + ff;
+      if (f >= g.f) break;
+      const int fr = (f * g.c + c) * K + i;
+#pragma unroll
+      for (int j = 0; j < K; ++j) red[(slot * frow + fr) * K + j] = acc[ff][j];
+    }
   }
   __syncthreads();
-  for (int rrow = threadIdx.x; rrow < nrow; rrow += blockDim.x) {
-    const int f = rrow / (g.c * K), ci = rrow - f * g.c * K, c = ci / K, i = ci - c * K;
+  for (int fr = threadIdx.x; fr < frow; fr += blockDim.x) {
+    const int f = fr / (g.c * K), ci = fr - f * g.c * K, c = ci / K, i = ci - c * K;
 #pragma unroll
     for (int j = 0; j < K; ++j) {
-      float a = red[((G - 1) * nrow + rrow) * K + j];  // group 0
-      for (int grp = 1; grp < G; ++grp) a = __fadd_rn(a, red[((grp - 1) * nrow + rrow) * K + j]);
+      float a = red[((G - 1) * frow + fr) * K + j];  // group 0
+      for (int grp = 1; grp < G; ++grp) a = __fadd_rn(a, red[((grp - 1) * frow + fr) * K + j]);
       out[f * cols + c * K * K + i * K + j] = a;
     }
   }
@@ -494,6 +511,13 @@ __device__ __forceinline__ void direct_wgrad_blocked(const hnn_conv_problem& p, 
     }
     out[f * cols + g.ckk] = a;
   }
+}
+
+// FG for the blocked weight gradient: as many filters per thread (<= 4) as keep >= 2 row groups
+__device__ __forceinline__ int wgrad_fg(const ConvGeom& g, int threads) {
+  for (int fg = 4; fg > 1; --fg)
+    if (((g.f + fg - 1) / fg) * g.c * g.k * 2 <= threads) return fg;
+  return 1;
 }
 
 template <int OP>
@@ -630,8 +654,18 @@ __global__ void __launch_bounds__(DTHREADS, 3) conv_direct_kernel(const hnn_conv
     if (g.s == 1 && (g.k == 5 || g.k == 3)) {
       float* red = ds + HNN_CONV_DIRECT_BCHUNK * g.f * ps;  // [G][f*c*k][k] group partials
       float* out = p.partial + size_t(unit) * nw;
-      if (g.k == 5) direct_wgrad_blocked<5>(p, g, xs, cs, rs, ds, ps, nb, red, out);
-      else direct_wgrad_blocked<3>(p, g, xs, cs, rs, ds, ps, nb, red, out);
+      const int fg = wgrad_fg(g, blockDim.x);
+      if (g.k == 5) {
+        if (fg == 4) direct_wgrad_blocked<5, 4>(p, g, xs, cs, rs, ds, ps, nb, red, out);
+        else if (fg == 3) direct_wgrad_blocked<5, 3>(p, g, xs, cs, rs, ds, ps, nb, red, out);
+        else if (fg == 2) direct_wgrad_blocked<5, 2>(p, g, xs, cs, rs, ds, ps, nb, red, out);
+        else direct_wgrad_blocked<5, 1>(p, g, xs, cs, rs, ds, ps, nb, red, out);
+      } else {
+        if (fg == 4) direct_wgrad_blocked<3, 4>(p, g, xs, cs, rs, ds, ps, nb, red, out);
+        else if (fg == 3) direct_wgrad_blocked<3, 3>(p, g, xs, cs, rs, ds, ps, nb, red, out);
+        else if (fg == 2) direct_wgrad_blocked<3, 2>(p, g, xs, cs, rs, ds, ps, nb, red, out);
+        else direct_wgrad_blocked<3, 1>(p, g, xs, cs, rs, ds, ps, nb, red, out);
+      }
       return;
     }
     float acc[MAXW];
