@@ -14,15 +14,23 @@
  *   hnn_grouped_gemm            dense fwd / bwd  _dense_fwd, _dense_bwd (ops.py:46-55) with
  *                               relu fwd/bwd fused (ops.py:62-67); fp32 SIMT or tcgen05 3xTF32
  *   hnn_gemm_tc_encode          host-side TMA descriptors for the tcgen05 path
- *   hnn_grouped_conv            conv2d fwd / bwd _conv2d_fwd, _conv2d_bwd (ops.py:100-130), implicit GEMM
- *   hnn_grouped_conv_direct     the same for small channel counts, direct (one thread per output)
+ *   hnn_grouped_conv            conv2d fwd / bwd _conv2d_fwd, _conv2d_bwd (ops.py:100-130): a SIMT
+ *                               implicit-GEMM fallback (64x32 tiles); the planner routes LeNet-class
+ *                               layers to hnn_grouped_conv_direct[_ex] and wide ones to hnn_conv_tc_aux
+ *                               + the tcgen05 GEMMs, so the default routes never launch it
+ *   hnn_grouped_conv_direct     the same for small channel counts, direct (register-blocked over
+ *                               filters / channels x 4 outputs; _ex takes the block size)
+ *   hnn_conv_tc_aux             im2col / NHWC copies / dy transposes / weight layouts / split reduce
+ *                               around the tensor-core conv GEMMs (ops.py:100-130)
  *   hnn_conv_wgrad_reduce       the fixed-order finish of the conv weight/bias gradient
+ *   hnn_skinny_backward         the <= 10-unit logits layer's input + weight gradient in one pass
  *   hnn_grouped_maxpool         maxpool2d fwd / bwd (ops.py:149-174), relu mask fused
  *   hnn_grouped_relu            stand-alone relu fwd / bwd (ops.py:62-67)
  *   hnn_sce_fused               softmax_cross_entropy + argmax accuracy + non-finite abort
  *                               (ops.py:220-251, train.py:239-243,252-255)
  *   hnn_multi_tensor_sgd        optim.apply_update, SGD / momentum branch (optim.py:59-71)
- *   hnn_multi_tensor_adam       optim.apply_update, Adam branch (optim.py:73-87)
+ *   hnn_multi_tensor_adam       optim.apply_update, Adam branch (optim.py:73-87); both run the bulk-
+ *                               copy multi-tensor kernel (HNN_OPT_BULK=0: the per-thread one)
  *   hnn_last_error              error text for the last nonzero status on this thread
  *
  * Conventions (every entry point):

@@ -1,4 +1,4 @@
-"""Two eager training steps of a small mixed hybrid for compute-sanitizer (racecheck / synccheck /
+"""Three eager training steps (the last on a ragged batch) of a small mixed hybrid for compute-sanitizer (racecheck / synccheck /
 memcheck): an fp32 MLP on the CTA-pair 3xTF32 GEMMs (fwd / dgrad / wgrad, Adam), a LeNet-style CNN
 on the direct conv + pool kernels, and a bf16 conv net on the tensor-core conv path (implicit-GEMM
 forward, stride-2 parity-class input gradient, weight-gradient reduce).
@@ -35,15 +35,15 @@ h = merge(jobs)
 dev = h.materialize(dev_t, conv_precision=prec)
 dev.bind_datasets([DeviceDataset(d, dev_t) for d in data], 128)
 dev.build_plans()
-rows = np.zeros((2, len(jobs)), dtype=STEP_DTYPE)
+rows = np.zeros((3, len(jobs)), dtype=STEP_DTYPE)
 for m, j in enumerate(jobs):
     B = j.hypers.batch_size
-    for t in range(2):
-        rows[t, m] = (1, B, t * B, 0, t, t + 1, j.hypers.learning_rate, 0.1, 0.001, (0, 0, 0))
+    for t in range(3):  # (step 3: a ragged batch, rows < capacity)
+        rows[t, m] = (1, B if t < 2 else B - 5, t * B, 0, t, t + 1, j.hypers.learning_rate, 0.1, 0.001, (0, 0, 0))
     d = data[m]
     dev.perm_upload(m, rng.permutation(d.sample_count, "shuffle", d.content_hash, j.hypers.seed, 0))
 dev.load_schedule(rows)
-dev.train_steps(2, use_graph=False)
+dev.train_steps(3, use_graph=False)
 torch.cuda.synchronize()
 print("labels:", [l.label for l in dev.train_plan])
 print("losses:", dev.loss_out.cpu().numpy())
