@@ -11,6 +11,7 @@
  *   hnn_gather_rows             Batch(x=train_x[idx], y=train_y[idx])   (store.py:77-80)
  *   hnn_host_gather_rows        the same gather on the host (data loader of the host-fed step)
  *   hnn_host_gather_batch       one step's host gather for all models, split over host threads
+ *   hnn_hostfed_step            the host-fed step's copies + graph launch as one native call
  *   hnn_grouped_gemm            dense fwd / bwd  _dense_fwd, _dense_bwd (ops.py:46-55) with
  *                               relu fwd/bwd fused (ops.py:62-67); fp32 SIMT or tcgen05 3xTF32
  *   hnn_gemm_tc_encode          host-side TMA descriptors for the tcgen05 path
@@ -150,6 +151,32 @@ typedef struct hnn_host_gather_item {
 } hnn_host_gather_item;
 
 int hnn_host_gather_batch(const hnn_host_gather_item* items, int n_items, int threads);
+
+/* The host-fed step (train.HostFedStepper) as one native call: on `copy_stream`, wait until staging
+ * slot `slot` (0 / 1) is free (its previous batch moved out), H2D host_x / host_y (pinned) into it,
+ * record the slot's ready event; on `compute_stream`, wait for it, copy the staged batch into the
+ * arenas, record the slot's free event, launch `graph_exec` (the captured host-fed step graph, a
+ * cudaGraphExec_t), then D2H out_dev[i] -> out_host[i] (per-model loss / correct).  *copied_event =
+ * the ready event: once it completes the host buffers may be refilled (hnn_event_synchronize). */
+typedef struct hnn_hostfed_io {
+  const void* host_x;
+  void* stage_x;
+  void* arena_x;
+  int64_t x_bytes;
+  const void* host_y;
+  void* stage_y;
+  void* arena_y;
+  int64_t y_bytes;
+  const void* out_dev[2];
+  void* out_host[2];
+  int64_t out_bytes[2];
+} hnn_hostfed_io;
+
+int hnn_hostfed_create(void** ctx_out);
+int hnn_hostfed_destroy(void* ctx);
+int hnn_hostfed_step(void* ctx, int slot, const hnn_hostfed_io* io, void* graph_exec, void* compute_stream,
+                     void* copy_stream, void** copied_event);
+int hnn_event_synchronize(void* event);
 
 /*
  * Row-major grouped GEMM problem.  Let R = cur[model].rows.

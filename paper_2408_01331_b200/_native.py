@@ -100,6 +100,12 @@ class HostGatherItem(C.Structure):
                 ("ld_src", C.c_int64), ("cols", C.c_int64), ("n", C.c_int64), ("cap", C.c_int64)]
 
 
+class HostFedIO(C.Structure):
+    _fields_ = [("host_x", P), ("stage_x", P), ("arena_x", P), ("x_bytes", C.c_int64), ("host_y", P), ("stage_y", P),
+                ("arena_y", P), ("y_bytes", C.c_int64), ("out_dev", P * 2), ("out_host", P * 2),
+                ("out_bytes", C.c_int64 * 2)]
+
+
 class OptSegment(C.Structure):
     _fields_ = [("param", P), ("grad", P), ("m", P), ("v", P), ("count", C.c_int64), ("model", I), ("kind", I),
                 ("momentum", C.c_float), ("chunk_base", I), ("chunks", I), ("reserved", I)]
@@ -109,7 +115,7 @@ STRUCTS = {
     "hnn_step_row": StepRow, "hnn_model_status": ModelStatus, "hnn_gather_problem": GatherProblem,
     "hnn_gemm_problem": GemmProblem, "hnn_conv_problem": ConvProblem, "hnn_pool_problem": PoolProblem,
     "hnn_relu_problem": ReluProblem, "hnn_convtc_problem": ConvTcProblem, "hnn_embed_problem": EmbedProblem, "hnn_sce_problem": SceProblem, "hnn_opt_segment": OptSegment,
-    "hnn_host_gather_item": HostGatherItem,
+    "hnn_host_gather_item": HostGatherItem, "hnn_hostfed_io": HostFedIO,
 }
 
 # every symbol include/hnn_b200.h declares, with its ctypes signature
@@ -119,6 +125,10 @@ SIGNATURES = {
     "hnn_gather_rows": [P, C.c_int, C.c_int, P, VP],
     "hnn_host_gather_rows": [VP, C.c_int64, VP, VP, C.c_int64, VP, VP, C.c_int64, C.c_int64],
     "hnn_host_gather_batch": [VP, C.c_int, C.c_int],
+    "hnn_hostfed_create": [C.POINTER(VP)],
+    "hnn_hostfed_destroy": [VP],
+    "hnn_hostfed_step": [VP, C.c_int, VP, VP, VP, VP, C.POINTER(VP)],
+    "hnn_event_synchronize": [VP],
     "hnn_gemm_tile_shape": [C.c_int, C.c_int, C.POINTER(I), C.POINTER(I)],
     "hnn_gemm_chunk_terms": [C.c_int, C.POINTER(I)],
     "hnn_grouped_gemm": [C.c_int, C.c_int, P, C.c_int, C.c_int, P, P, VP],

@@ -106,6 +106,7 @@ int hnn_struct_size(const char* name) {
   if (!strcmp(name, "hnn_sce_problem")) return sizeof(hnn_sce_problem);
   if (!strcmp(name, "hnn_opt_segment")) return sizeof(hnn_opt_segment);
   if (!strcmp(name, "hnn_host_gather_item")) return sizeof(hnn_host_gather_item);
+  if (!strcmp(name, "hnn_hostfed_io")) return sizeof(hnn_hostfed_io);
   if (!strcmp(name, "hnn_convtc_problem")) return sizeof(hnn_convtc_problem);
   if (!strcmp(name, "hnn_embed_problem")) return sizeof(hnn_embed_problem);
   return -1;
@@ -181,6 +182,83 @@ int hnn_host_gather_batch(const hnn_host_gather_item* items, int n_items, int th
   for (int t = 1; t < nt; ++t) pool.emplace_back(work, total * t / nt, total * (t + 1) / nt);
   work(0, total / nt);
   for (auto& th : pool) th.join();
+  return HNN_OK;
+}
+
+// ---------------------------------------------------------------- host-fed step (one native call)
+// The public host-fed step's stream work without per-step Python (train.HostFedStepper, fast path):
+// copy stream: wait until staging slot k is free, H2D of the pinned batch into it, record ready[k];
+// compute stream: wait ready[k], move the staged batch into the arenas, record free[k], launch the
+// captured step graph, D2H the per-model outputs.  Events live in the context.
+struct HostFed {
+  cudaEvent_t ready[2], free_[2];
+  bool used[2];
+};
+
+int hnn_hostfed_create(void** out) {
+  HNN_REQUIRE(out, "hnn_hostfed_create", "null output");
+  HostFed* h = new HostFed();
+  for (int k = 0; k < 2; ++k) {
+    if (cudaEventCreateWithFlags(&h->ready[k], cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&h->free_[k], cudaEventDisableTiming) != cudaSuccess) {
+      hnn::set_error("hnn_hostfed_create", "cudaEventCreate failed");
+      delete h;
+      return HNN_ERR_CUDA;
+    }
+    h->used[k] = false;
+  }
+  *out = h;
+  return HNN_OK;
+}
+
+int hnn_hostfed_destroy(void* ctx) {
+  HostFed* h = static_cast<HostFed*>(ctx);
+  if (!h) return HNN_OK;
+  for (int k = 0; k < 2; ++k) {
+    cudaEventDestroy(h->ready[k]);
+    cudaEventDestroy(h->free_[k]);
+  }
+  delete h;
+  return HNN_OK;
+}
+
+int hnn_hostfed_step(void* ctx, int slot, const hnn_hostfed_io* io, void* graph_exec, void* compute_stream,
+                     void* copy_stream, void** copied_event) {
+  HostFed* h = static_cast<HostFed*>(ctx);
+  HNN_REQUIRE(h && io && graph_exec && (slot == 0 || slot == 1), "hnn_hostfed_step", "bad arguments");
+  cudaStream_t cs = hnn::as_stream(compute_stream), xs = hnn::as_stream(copy_stream);
+  cudaError_t e = cudaSuccess;
+  auto ok = [&](cudaError_t r) {
+    if (e == cudaSuccess) e = r;
+  };
+  if (h->used[slot]) ok(cudaStreamWaitEvent(xs, h->free_[slot], 0));  // step t-2 moved its batch out
+  ok(cudaMemcpyAsync(io->stage_x, io->host_x, size_t(io->x_bytes), cudaMemcpyHostToDevice, xs));
+  ok(cudaMemcpyAsync(io->stage_y, io->host_y, size_t(io->y_bytes), cudaMemcpyHostToDevice, xs));
+  ok(cudaEventRecord(h->ready[slot], xs));
+  ok(cudaStreamWaitEvent(cs, h->ready[slot], 0));
+  ok(cudaMemcpyAsync(io->arena_x, io->stage_x, size_t(io->x_bytes), cudaMemcpyDeviceToDevice, cs));
+  ok(cudaMemcpyAsync(io->arena_y, io->stage_y, size_t(io->y_bytes), cudaMemcpyDeviceToDevice, cs));
+  ok(cudaEventRecord(h->free_[slot], cs));
+  h->used[slot] = true;
+  ok(cudaGraphLaunch(static_cast<cudaGraphExec_t>(graph_exec), cs));
+  for (int i = 0; i < 2; ++i)
+    if (io->out_bytes[i] > 0)
+      ok(cudaMemcpyAsync(io->out_host[i], io->out_dev[i], size_t(io->out_bytes[i]), cudaMemcpyDeviceToHost, cs));
+  if (copied_event) *copied_event = h->ready[slot];
+  if (e != cudaSuccess) {
+    hnn::set_error("hnn_hostfed_step", cudaGetErrorString(e));
+    return HNN_ERR_CUDA;
+  }
+  return HNN_OK;
+}
+
+int hnn_event_synchronize(void* event) {
+  HNN_REQUIRE(event, "hnn_event_synchronize", "null event");
+  const cudaError_t e = cudaEventSynchronize(static_cast<cudaEvent_t>(event));
+  if (e != cudaSuccess) {
+    hnn::set_error("hnn_event_synchronize", cudaGetErrorString(e));
+    return HNN_ERR_CUDA;
+  }
   return HNN_OK;
 }
 

@@ -17,6 +17,8 @@ float64 (:419-426) and the test split evaluated in order at completion
 """
 from __future__ import annotations
 
+import os
+
 import time
 from dataclasses import dataclass, field
 from functools import lru_cache
@@ -572,6 +574,52 @@ class HostFedStepper:
         self.staging_free = [None, None]
         self.steps_issued = 0
         self.dev.train_steps(0, use_graph=use_graph, host_fed=True)  # capture the step graph up front
+        # graph-replayed steps go through one native call per step (hnn_hostfed_step: the staged
+        # copies, the graph launch and the output D2H), the per-step Python of the stream-context
+        # path below being the bound of the small configs' end-to-end step (C5: 0.3 ms)
+        self._ctx = None
+        if use_graph and os.environ.get("HNN_HOSTFED_NATIVE", "1") == "1":
+            import ctypes
+
+            from . import _native as N
+
+            ctx = ctypes.c_void_p()
+            N.call("hnn_hostfed_create", ctypes.byref(ctx))
+            self._ctx = ctx
+            self._io = N.HostFedIO()
+            self._io.x_bytes = self.dev.batch_arena.numel() * 4
+            self._io.y_bytes = self.dev.label_arena.numel() * 4
+            self._io.arena_x = self.dev.batch_arena.data_ptr()
+            self._io.arena_y = self.dev.label_arena.data_ptr()
+            self._io.out_dev[0], self._io.out_host[0] = self.dev.loss_out.data_ptr(), self.loss_host.data_ptr()
+            self._io.out_dev[1], self._io.out_host[1] = self.dev.correct_out.data_ptr(), self.hits_host.data_ptr()
+            self._io.out_bytes[0], self._io.out_bytes[1] = self.dev.n * 4, self.dev.n * 4
+
+    def __del__(self):
+        if getattr(self, "_ctx", None) is not None:
+            from . import _native as N
+
+            try:
+                torch_sync = __import__("torch").cuda.synchronize
+                torch_sync(self.dev.device)
+                N.call("hnn_hostfed_destroy", self._ctx)
+            except Exception:
+                pass
+            self._ctx = None
+
+    def _graph_exec(self) -> int:
+        g = self.dev.__dict__.get("_graphs", {}).get(True)
+        if g is None:  # (re-planned device: capture again)
+            self.dev.train_steps(0, use_graph=True, host_fed=True)
+            g = self.dev._graphs[True]
+        h = g.raw_cuda_graph_exec()
+        if not isinstance(h, int):  # a capsule on some builds
+            import ctypes
+
+            ctypes.pythonapi.PyCapsule_GetPointer.restype = ctypes.c_void_p
+            ctypes.pythonapi.PyCapsule_GetPointer.argtypes = [ctypes.py_object, ctypes.c_char_p]
+            h = ctypes.pythonapi.PyCapsule_GetPointer(h, None)
+        return h
 
     def stage_epoch_batches(self, rows, count: int = 2, host_datasets: dict | None = None) -> list:
         """Pinned host copies of the first `count` steps' batches (store.batches order, src/store.py:68-81),
@@ -593,6 +641,22 @@ class HostFedStepper:
         x, y = host_batch[0], host_batch[1]
         k = self.steps_issued % 2
         sx, sy = self.staging[k]
+        if self._ctx is not None:
+            import ctypes
+
+            from . import _native as N
+
+            io = self._io
+            io.host_x, io.host_y = x.data_ptr(), y.data_ptr()
+            io.stage_x, io.stage_y = sx.data_ptr(), sy.data_ptr()
+            ev = ctypes.c_void_p()
+            N.call("hnn_hostfed_step", self._ctx, k, ctypes.byref(io), self._graph_exec(),
+                   torch.cuda.current_stream(self.dev.device).cuda_stream, self.copy_stream.cuda_stream,
+                   ctypes.byref(ev))
+            self.steps_issued += 1
+            if isinstance(host_batch, LoadedBatch):
+                host_batch.release(_NativeEvent(ev.value))
+            return
         compute = torch.cuda.current_stream(self.dev.device)
         with torch.cuda.stream(self.copy_stream):
             if self.staging_free[k] is not None:  # step t-2 has moved its batch out
@@ -713,6 +777,18 @@ class _BatchAssembler:
                    np.ascontiguousarray(d.train_y, dtype=np.float32))
             self._src[job_id] = got
         return got
+
+
+class _NativeEvent:
+    """A CUDA event owned by the native host-fed context (hnn_hostfed_step's copied event)."""
+
+    def __init__(self, handle: int):
+        self.handle = handle
+
+    def synchronize(self) -> None:
+        from . import _native as N
+
+        N.call("hnn_event_synchronize", self.handle)
 
 
 class LoadedBatch(tuple):
