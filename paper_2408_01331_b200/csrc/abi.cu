@@ -1,6 +1,10 @@
 // C-ABI plumbing: error state, the per-step schedule prologue and the batch gather.
 #include <cstring>
 #include <algorithm>
+#include <atomic>
+#include <condition_variable>
+#include <functional>
+#include <mutex>
 #include <thread>
 #include <vector>
 
@@ -141,6 +145,69 @@ int hnn_host_gather_rows(float* dst_x, int64_t ld_dst, int32_t* dst_y, const flo
   return HNN_OK;
 }
 
+}  // extern "C"
+
+// Persistent host worker pool for the loader's per-step gather: spawning and joining threads per
+// call cost ~0.1 ms per step (the bound of the small configs' end-to-end step).  One job at a time
+// (a mutex serialises callers); the caller runs piece 0..n-1 alongside the workers.
+namespace {
+struct HostPool {
+  std::mutex run_m, m;
+  std::condition_variable cv, done_cv;
+  std::vector<std::thread> workers;
+  std::function<void(int)> job;
+  int pieces = 0, remaining = 0;
+  std::atomic<int> next{0};
+  uint64_t gen = 0;
+
+  void pieces_loop() {
+    for (int i; (i = next.fetch_add(1)) < pieces;) {
+      job(i);
+      std::lock_guard<std::mutex> lk(m);
+      if (--remaining == 0) done_cv.notify_all();
+    }
+  }
+  void worker() {
+    uint64_t seen = 0;
+    std::unique_lock<std::mutex> lk(m);
+    for (;;) {
+      cv.wait(lk, [&] { return gen != seen; });
+      seen = gen;
+      lk.unlock();
+      pieces_loop();
+      lk.lock();
+    }
+  }
+  void run(int n, const std::function<void(int)>& fn) {
+    std::lock_guard<std::mutex> serial(run_m);
+    {
+      std::unique_lock<std::mutex> lk(m);
+      while (int(workers.size()) < n - 1) {
+        workers.emplace_back([this] { worker(); });
+        workers.back().detach();  // (never joined: idle workers must not block process exit)
+      }
+      job = fn;
+      pieces = n;
+      remaining = n;
+      next.store(0);
+      ++gen;
+    }
+    cv.notify_all();
+    pieces_loop();
+    std::unique_lock<std::mutex> lk(m);
+    done_cv.wait(lk, [&] { return remaining == 0; });
+  }
+};
+HostPool& host_pool() {
+  static HostPool* p = new HostPool();  // (leaked on purpose: no destructor runs at exit)
+  return *p;
+}
+}  // namespace
+
+static void host_pool_run(int n, const std::function<void(int)>& fn) { host_pool().run(n, fn); }
+
+extern "C" {
+
 int hnn_host_gather_batch(const hnn_host_gather_item* items, int n_items, int threads) {
   HNN_REQUIRE(items && n_items >= 0 && threads >= 1 && threads <= 64, "hnn_host_gather_batch", "bad arguments");
   std::vector<int64_t> start(size_t(n_items) + 1, 0);  // prefix sums of the rows each item writes
@@ -177,11 +244,7 @@ int hnn_host_gather_batch(const hnn_host_gather_item* items, int n_items, int th
     work(0, total);
     return HNN_OK;
   }
-  std::vector<std::thread> pool;
-  pool.reserve(nt - 1);
-  for (int t = 1; t < nt; ++t) pool.emplace_back(work, total * t / nt, total * (t + 1) / nt);
-  work(0, total / nt);
-  for (auto& th : pool) th.join();
+  host_pool_run(nt, [&](int t) { work(total * t / nt, total * (t + 1) / nt); });
   return HNN_OK;
 }
 

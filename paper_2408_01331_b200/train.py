@@ -745,16 +745,40 @@ class _BatchAssembler:
 
     def items(self, x, y, row, perms: dict) -> np.ndarray:
         """The step's item table for buffers (x, y): model m gathers its `rows` indices of `perms[m]`
-        from perm_base on (inactive models: no item rows)."""
+        from perm_base on (inactive models: no item rows).  Vectorised (per-step Python is the bound
+        of the small configs' end-to-end step)."""
         it = self.static.copy()
         it["dst_x"] += np.uint64(x.data_ptr())
         it["dst_y"] += np.uint64(y.data_ptr())
         active = row["active"].astype(bool)
         it["n"] = np.where(active, row["rows"], 0)
         it["cap"] = np.where(active, self.caps, 0)
+        base = np.zeros(len(it), dtype=np.uint64)
         for m, p in perms.items():
-            it[m]["idx"] = p.ctypes.data + 8 * int(row[m]["perm_base"])
+            base[m] = p.ctypes.data
+        it["idx"] = np.where(active, base + 8 * row["perm_base"].astype(np.uint64), 0)
         return it
+
+    def step_items(self, x, y, row) -> np.ndarray:
+        """items() for a schedule row, with the per-model permutation pointers cached across steps
+        (recomputed only for models whose epoch changed): no per-model Python on ordinary steps."""
+        n = self.dev.n
+        if not hasattr(self, "_ptr"):
+            self._ptr = np.zeros(n, dtype=np.uint64)
+            self._ep = np.full(n, -1, dtype=np.int64)
+            self._keep = [None] * n
+        active = row["active"].astype(bool)
+        epochs = row["epoch"].astype(np.int64)
+        for m in np.nonzero(active & (epochs != self._ep))[0]:
+            p = self.perm(self.dev.slots[int(m)], int(epochs[m]))
+            self._keep[m], self._ptr[m], self._ep[m] = p, p.ctypes.data, epochs[m]
+        it = self.static.copy()
+        it["dst_x"] += np.uint64(x.data_ptr())
+        it["dst_y"] += np.uint64(y.data_ptr())
+        it["n"] = np.where(active, row["rows"], 0)
+        it["cap"] = np.where(active, self.caps, 0)
+        it["idx"] = np.where(active, self._ptr + 8 * row["perm_base"].astype(np.uint64), 0)
+        return it, list(self._keep)  # (the permutation arrays the raw pointers refer to)
 
     def gather(self, items: np.ndarray, threads: int) -> None:
         from . import _native as N
@@ -829,15 +853,14 @@ class HostBatchLoader:
             self.pending[k] = None
             return
         row = self.rows[t]
-        dev = self.asm.dev
-        perms = {m: self.asm.perm(dev.slots[m], int(row[m]["epoch"])) for m in range(dev.n) if row[m]["active"]}
         x, y = self.bufs[k]
-        items = self.asm.items(x, y, row, perms)
+        items, keep = self.asm.step_items(x, y, row)
 
         def job():
             if after is not None:
                 after.synchronize()
             self.asm.gather(items, self.threads)
+            del keep[:]  # (kept alive until the gather has read them)
 
         self.pending[k] = [self.pool.submit(job)]
 
