@@ -126,7 +126,7 @@ __global__ void __launch_bounds__(STHREADS) gemm_simt_kernel(const hnn_gemm_prob
       const Update u = make_update(cur[p.model], p.opt_kind, p.opt_momentum);
       const int i = m0 + tid;
       float w = p.opt_b[i], m = p.opt_bm ? p.opt_bm[i] : 0.0f, v = p.opt_bv ? p.opt_bv[i] : 0.0f;
-      update_one(u, w, bsum, m, v);
+      update_sgd(u, w, bsum, m);
       p.opt_b[i] = w;
       if (p.opt_bm) p.opt_bm[i] = m;
       if (p.opt_bv) p.opt_bv[i] = v;
@@ -145,7 +145,7 @@ __global__ void __launch_bounds__(STHREADS) gemm_simt_kernel(const hnn_gemm_prob
         if (gn >= p.n) continue;
         const size_t off = size_t(gm) * p.ldc + gn;
         float w = p.opt_w[off], m = p.opt_wm ? p.opt_wm[off] : 0.0f, v = p.opt_wv ? p.opt_wv[off] : 0.0f;
-        update_one(u, w, acc[i][j], m, v);
+        update_sgd(u, w, acc[i][j], m);
         p.opt_w[off] = w;
         if (p.opt_wm) p.opt_wm[off] = m;
         if (p.opt_wv) p.opt_wv[off] = v;

@@ -343,6 +343,21 @@ __global__ void __launch_bounds__(KTHREADS) skinny_dgrad_kernel(const hnn_gemm_p
 constexpr int WG_CHUNK = 256;  // dy rows staged in shared memory per pass ([256][16] floats)
 constexpr int WG_GROUPS = KTHREADS / WG_QUADS;
 
+// dy rows [base, base + n) x 16 columns (zero padded) into shared memory: every thread's 16 loads
+// are issued before its stores (a load -> store per element serialised 16 round trips per thread:
+// most of the tiny-batch weight-gradient launches' time)
+__device__ __forceinline__ void stage_dy(const hnn_gemm_problem& p, int base, int n, float* dys) {
+  constexpr int PER = WG_CHUNK * 16 / KTHREADS;
+  float v[PER];
+#pragma unroll
+  for (int u = 0; u < PER; ++u) {
+    const int e = threadIdx.x + u * KTHREADS, r = e >> 4, j = e & 15;
+    v[u] = (j < p.m && r < n) ? __ldg(p.a + size_t(base + r) * p.lda + j) : 0.0f;
+  }
+#pragma unroll
+  for (int u = 0; u < PER; ++u) dys[threadIdx.x + u * KTHREADS] = v[u];
+}
+
 template <int MJ>
 __device__ __forceinline__ void colacc(const hnn_gemm_problem& p, int col, int r_lo, int r_hi, int base,
                                        float (&part)[MJ][4], const float* dys) {
@@ -373,10 +388,7 @@ __device__ __forceinline__ void wgrad_tile(const hnn_gemm_problem& p, const hnn_
   for (int base = 0; base < rows; base += WG_CHUNK) {
     const int n = min(WG_CHUNK, rows - base);
     __syncthreads();
-    for (int e = threadIdx.x; e < WG_CHUNK * 16; e += KTHREADS) {
-      const int r = e >> 4, j = e & 15;
-      dys[e] = (j < p.m && r < n) ? __ldg(p.a + size_t(base + r) * p.lda + j) : 0.0f;
-    }
+    stage_dy(p, base, n, dys);
     __syncthreads();
     if (bias_thread)  // numpy's axis-0 sum: sequential row order per column
       for (int r = 0; r < n; ++r) bsum = __fadd_rn(bsum, dys[r * 16 + threadIdx.x]);
@@ -388,7 +400,7 @@ __device__ __forceinline__ void wgrad_tile(const hnn_gemm_problem& p, const hnn_
       const Update u = make_update(row, p.opt_kind, p.opt_momentum);
       const int i = threadIdx.x;
       float w = p.opt_b[i], m = p.opt_bm ? p.opt_bm[i] : 0.0f, v = p.opt_bv ? p.opt_bv[i] : 0.0f;
-      update_one(u, w, bsum, m, v);
+      update_sgd(u, w, bsum, m);
       p.opt_b[i] = w;
       if (p.opt_bm) p.opt_bm[i] = m;
       if (p.opt_bv) p.opt_bv[i] = v;
@@ -424,10 +436,10 @@ __device__ __forceinline__ void wgrad_tile(const hnn_gemm_problem& p, const hnn_
       float4 w = *reinterpret_cast<float4*>(p.opt_w + off);
       float4 m = p.opt_wm ? *reinterpret_cast<float4*>(p.opt_wm + off) : make_float4(0, 0, 0, 0);
       float4 v = p.opt_wv ? *reinterpret_cast<float4*>(p.opt_wv + off) : make_float4(0, 0, 0, 0);
-      update_one(u, w.x, part[j][0], m.x, v.x);
-      update_one(u, w.y, part[j][1], m.y, v.y);
-      update_one(u, w.z, part[j][2], m.z, v.z);
-      update_one(u, w.w, part[j][3], m.w, v.w);
+      update_sgd(u, w.x, part[j][0], m.x);
+      update_sgd(u, w.y, part[j][1], m.y);
+      update_sgd(u, w.z, part[j][2], m.z);
+      update_sgd(u, w.w, part[j][3], m.w);
       *reinterpret_cast<float4*>(p.opt_w + off) = w;
       if (p.opt_wm) *reinterpret_cast<float4*>(p.opt_wm + off) = m;
       if (p.opt_wv) *reinterpret_cast<float4*>(p.opt_wv + off) = v;
@@ -481,10 +493,7 @@ __device__ __forceinline__ void bwd_tile(const hnn_gemm_problem& p, const hnn_ge
   for (int base = 0; base < rows; base += WG_CHUNK) {
     const int n = min(WG_CHUNK, rows - base);
     __syncthreads();
-    for (int e = threadIdx.x; e < WG_CHUNK * 16; e += KTHREADS) {
-      const int r = e >> 4, j = e & 15;
-      dys[e] = (j < p.m && r < n) ? __ldg(p.a + size_t(base + r) * p.lda + j) : 0.0f;
-    }
+    stage_dy(p, base, n, dys);
     __syncthreads();
     if (bias_thread)  // numpy's axis-0 sum: sequential row order per column
       for (int r = 0; r < n; ++r) bsum = __fadd_rn(bsum, dys[r * 16 + threadIdx.x]);

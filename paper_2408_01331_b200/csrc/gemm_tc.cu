@@ -299,7 +299,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
               const float g = lds32(stg + rr * 128 + ((((lane >> 2) ^ (rr & 7))) << 4) + ((lane & 3) << 2));
               const size_t off = size_t(r) * p->ldc + n;
               float w = p->opt_w[off], mm = p->opt_wm ? p->opt_wm[off] : 0.0f, vv = p->opt_wv ? p->opt_wv[off] : 0.0f;
-              update_one(u, w, g, mm, vv);
+              update_sgd(u, w, g, mm);
               p->opt_w[off] = w;
               if (p->opt_wm) p->opt_wm[off] = mm;
               if (p->opt_wv) p->opt_wv[off] = vv;
@@ -387,7 +387,7 @@ __global__ void __launch_bounds__(COLSUM_THREADS) colsum_kernel(const hnn_gemm_p
   if (p.opt_b) {
     const Update u = make_update(cur[p.model], p.opt_kind, p.opt_momentum);
     float w = p.opt_b[i], m = p.opt_bm ? p.opt_bm[i] : 0.0f, v = p.opt_bv ? p.opt_bv[i] : 0.0f;
-    update_one(u, w, acc, m, v);
+    update_sgd(u, w, acc, m);
     p.opt_b[i] = w;
     if (p.opt_bm) p.opt_bm[i] = m;
     if (p.opt_bv) p.opt_bv[i] = v;
