@@ -26,6 +26,13 @@ constexpr int FWD_ROWS = HNN_SKINNY_FWD_ROWS;  // rows per warp; tile = 8 warps 
 #endif
 constexpr int DG_ROWS = HNN_SKINNY_DG_ROWS;  // DGRAD rows per thread; tile = 8 row groups x 8 rows x 128 columns
 constexpr int WG_QUADS = 32; // WGRAD column quads per CTA; tile = 128 columns, 8 row groups
+#ifndef HNN_SKBWD_UNROLL
+#define HNN_SKBWD_UNROLL 4
+#endif
+#ifndef HNN_SKBWD_WSMEM
+#define HNN_SKBWD_WSMEM 0
+#endif
+constexpr int SKBWD_UNROLL = HNN_SKBWD_UNROLL;
 
 __device__ __forceinline__ float4 ldg4(const float* p) { return __ldg(reinterpret_cast<const float4*>(p)); }
 
@@ -129,7 +136,13 @@ __global__ void __launch_bounds__(KTHREADS) skinny_fwd_kernel(const hnn_gemm_pro
 // per-warp streaming form walked each row's whole K as a chain of dependent L2 / HBM round trips
 // at 24 warps per SM (C3: 39 us for 35.6 MB, ncu long-scoreboard bound).  Other problems take the
 // per-warp form inside the same launch (the tile shape is shared).
-constexpr int FB_KC = 128, FB_STAGES = 4, FB_THREADS = KTHREADS + 32;
+#ifndef HNN_FB_KC
+#define HNN_FB_KC 128
+#endif
+#ifndef HNN_FB_STAGES
+#define HNN_FB_STAGES 4
+#endif
+constexpr int FB_KC = HNN_FB_KC, FB_STAGES = HNN_FB_STAGES, FB_THREADS = KTHREADS + 32;
 constexpr int FB_STAGE_BYTES = 2 * 16 * FB_KC * 4;  // 16 x rows + 16 W rows
 constexpr int FB_SMEM = FB_STAGES * FB_STAGE_BYTES + 256;
 
@@ -358,6 +371,21 @@ __device__ __forceinline__ void stage_dy(const hnn_gemm_problem& p, int base, in
   for (int u = 0; u < PER; ++u) dys[threadIdx.x + u * KTHREADS] = v[u];
 }
 
+// numpy's axis-0 sum of column j of the staged dy rows: sequential in row order, eight rows' shared
+// loads issued ahead of their dependent adds
+__device__ __forceinline__ float colsum_rows(const float* dys, int n, int j, float acc) {
+  int r = 0;
+  for (; r + 8 <= n; r += 8) {
+    float v[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) v[u] = dys[(r + u) * 16 + j];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) acc = __fadd_rn(acc, v[u]);
+  }
+  for (; r < n; ++r) acc = __fadd_rn(acc, dys[r * 16 + j]);
+  return acc;
+}
+
 template <int MJ>
 __device__ __forceinline__ void colacc(const hnn_gemm_problem& p, int col, int r_lo, int r_hi, int base,
                                        float (&part)[MJ][4], const float* dys) {
@@ -390,8 +418,7 @@ __device__ __forceinline__ void wgrad_tile(const hnn_gemm_problem& p, const hnn_
     __syncthreads();
     stage_dy(p, base, n, dys);
     __syncthreads();
-    if (bias_thread)  // numpy's axis-0 sum: sequential row order per column
-      for (int r = 0; r < n; ++r) bsum = __fadd_rn(bsum, dys[r * 16 + threadIdx.x]);
+    if (bias_thread) bsum = colsum_rows(dys, n, threadIdx.x, bsum);  // numpy's axis-0 order
     if (active) colacc<MJ>(p, col, base + (n * q) / WG_GROUPS, base + (n * (q + 1)) / WG_GROUPS, base, part, dys);
   }
   if (bias_thread) {
@@ -485,9 +512,20 @@ __device__ __forceinline__ void bwd_tile(const hnn_gemm_problem& p, const hnn_ge
   float part[MJ][4];
 #pragma unroll
   for (int j = 0; j < MJ; ++j) part[j][0] = part[j][1] = part[j][2] = part[j][3] = 0.0f;
+#if HNN_SKBWD_WSMEM
+  // W quads of the CTA's 128 columns in shared memory (the registers hold the partials and more rows
+  // of X in flight instead)
+  float4* wq = reinterpret_cast<float4*>(red + (WG_GROUPS - 1) * WG_QUADS * 64);  // [MJ][WG_QUADS]
+  if (q == 0)
+    for (int j = 0; j < MJ; ++j)
+      wq[j * WG_QUADS + qd] = (active && j < d.k) ? ldg4(d.b + size_t(j) * d.ldb + col) : make_float4(0, 0, 0, 0);
+#define SKBWD_W(j) wq[(j) * WG_QUADS + qd]
+#else
   float4 w[MJ];
 #pragma unroll
   for (int j = 0; j < MJ; ++j) w[j] = (active && j < d.k) ? ldg4(d.b + size_t(j) * d.ldb + col) : make_float4(0, 0, 0, 0);
+#define SKBWD_W(j) w[j]
+#endif
   const bool own_mask = d.mask != nullptr && d.mask != p.b;  // (a mask other than X: loaded separately)
   float bsum = -0.0f;
   for (int base = 0; base < rows; base += WG_CHUNK) {
@@ -495,12 +533,11 @@ __device__ __forceinline__ void bwd_tile(const hnn_gemm_problem& p, const hnn_ge
     __syncthreads();
     stage_dy(p, base, n, dys);
     __syncthreads();
-    if (bias_thread)  // numpy's axis-0 sum: sequential row order per column
-      for (int r = 0; r < n; ++r) bsum = __fadd_rn(bsum, dys[r * 16 + threadIdx.x]);
+    if (bias_thread) bsum = colsum_rows(dys, n, threadIdx.x, bsum);  // numpy's axis-0 order
     if (active) {
       const int r_lo = base + (n * q) / WG_GROUPS, r_hi = base + (n * (q + 1)) / WG_GROUPS;
       const float* x = p.b + col;
-#pragma unroll 4
+#pragma unroll SKBWD_UNROLL
       for (int r = r_lo; r < r_hi; ++r) {
         const float4 xv = ldg4(x + size_t(r) * p.ldb);
         const float* dr = dys + (r - base) * 16;
@@ -508,14 +545,15 @@ __device__ __forceinline__ void bwd_tile(const hnn_gemm_problem& p, const hnn_ge
 #pragma unroll
         for (int j = 0; j < MJ; ++j) {
           const float dj = dr[j];
+          const float4 wj = SKBWD_W(j);
           part[j][0] = fmaf(dj, xv.x, part[j][0]);
           part[j][1] = fmaf(dj, xv.y, part[j][1]);
           part[j][2] = fmaf(dj, xv.z, part[j][2]);
           part[j][3] = fmaf(dj, xv.w, part[j][3]);
-          o.x = fmaf(dj, w[j].x, o.x);
-          o.y = fmaf(dj, w[j].y, o.y);
-          o.z = fmaf(dj, w[j].z, o.z);
-          o.w = fmaf(dj, w[j].w, o.w);
+          o.x = fmaf(dj, wj.x, o.x);
+          o.y = fmaf(dj, wj.y, o.y);
+          o.z = fmaf(dj, wj.z, o.z);
+          o.w = fmaf(dj, wj.w, o.w);
         }
         if (d.mask) {
           const float4 mk = own_mask ? ldg4(d.mask + size_t(r) * d.ldc + col) : xv;
@@ -557,6 +595,8 @@ __device__ __forceinline__ void bwd_tile(const hnn_gemm_problem& p, const hnn_ge
     if (p.c) *reinterpret_cast<float4*>(p.c + size_t(j) * p.ldc + col) = make_float4(part[j][0], part[j][1], part[j][2], part[j][3]);
   }
 }
+
+#undef SKBWD_W
 
 __global__ void __launch_bounds__(KTHREADS, 2) skinny_bwd_kernel(const hnn_gemm_problem* __restrict__ wprobs,
                                                                  const hnn_gemm_problem* __restrict__ dprobs, int nprob,
@@ -620,7 +660,7 @@ extern "C" int hnn_skinny_backward(const hnn_gemm_problem* wgrad_probs, const hn
                                    int total_tiles, const hnn_step_row* cur, const hnn_model_status* status,
                                    void* stream) {
   HNN_REQUIRE(wgrad_probs && dgrad_probs && cur && nprob > 0 && total_tiles > 0, "hnn_skinny_backward", "bad arguments");
-  constexpr int smem = (hnn::WG_CHUNK * 16 + (hnn::WG_GROUPS - 1) * hnn::WG_QUADS * 64) * 4;  // 72 KB
+  constexpr int smem = (hnn::WG_CHUNK * 16 + (hnn::WG_GROUPS - 1) * hnn::WG_QUADS * 64 + 10 * hnn::WG_QUADS * 4) * 4;
   static bool configured = false;
   if (!configured) {
     cudaFuncSetAttribute(hnn::skinny_bwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
