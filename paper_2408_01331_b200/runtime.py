@@ -810,16 +810,21 @@ class DeviceHybrid:
     def _pair_tile_cap(self, op, rows, tm) -> int:
         """Widest pair-tile width (256 / 128 / 64) for one launch: narrower tiles put more CTA pairs
         to work when a launch has fewer tiles than pairs (C5's 32 batch-64 forward GEMMs: 32
-        tiles at 256 columns, 64 at 128).  Cost model per tile: 0.5 + 0.5 * width / 256 (the A
-        operand streams whatever the width); makespan = max(total / pairs, largest tile)."""
+        tiles at 256 columns, 64 at 128).  Cost model per tile: K blocks * (0.5 + 0.5 * width / 256)
+        + 3 (the A operand streams whatever the width; the _pair_schedule model); makespan =
+        max(total / pairs, largest tile).  The width never changes a tile's per-element arithmetic."""
         pairs = self._sm_count() // 2
         best, best_cost = 256, None
         for cap in (256, 128, 64):
             total, largest = 0.0, 0.0
             for _, d in rows:
                 w = min(cap, 64 if d["n"] <= 64 else (128 if d["n"] <= 128 else 256))
-                cost = 0.5 + 0.5 * w / 256
-                n_tiles = -(-d["m"] // tm) * -(-d["n"] // w) * (d.get("ksplit", 1) if op == N.HNN_WGRAD else 1)
+                # a tile's time scales with its K blocks (the long-K tiles of a sparse launch set its
+                # makespan: C3 on 8 GPUs, 4 models per launch, K up to 2048)
+                split = d.get("ksplit", 1) if op == N.HNN_WGRAD else 1
+                kb = -(-(d["ksplit_len"] if split > 1 else d["k"]) // 32)
+                cost = kb * (0.5 + 0.5 * w / 256) + 3
+                n_tiles = -(-d["m"] // tm) * -(-d["n"] // w) * split
                 total += n_tiles * cost
                 largest = max(largest, cost)
             c = max(total / pairs, largest)

@@ -1,5 +1,5 @@
 """Per-launch times of one C3 step for a given library build (debug tool).
-usage: python tools/plan_times.py [path/to/libhnn_b200.so] [workload]"""
+usage: python tools/plan_times.py [path/to/libhnn_b200.so] [workload] [R/N: rank R's shard of an N-GPU run]"""
 import sys
 from pathlib import Path
 
@@ -14,7 +14,8 @@ import bench
 
 wl = sys.argv[2] if len(sys.argv) > 2 else "c3"
 torch.cuda.set_device(0)
-_, jobs, hy, dev, ddev, ds, comm = bench.build_rank(wl, 0, 1, torch.device("cuda", 0))
+shard = tuple(int(v) for v in sys.argv[3].split("/")) if len(sys.argv) > 3 else None
+_, jobs, hy, dev, ddev, ds, comm = bench.build_rank(wl, 0, 1, torch.device("cuda", 0), shard)
 meta = ds
 rows = bench.schedule(jobs, meta, 200)
 bench.upload_perms(dev, jobs, meta)
