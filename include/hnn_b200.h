@@ -27,6 +27,7 @@
  *   hnn_skinny_backward         the <= 10-unit logits layer's input + weight gradient in one pass
  *   hnn_grouped_maxpool         maxpool2d fwd / bwd (ops.py:149-174), relu mask fused
  *   hnn_grouped_relu            stand-alone relu fwd / bwd (ops.py:62-67)
+ *   hnn_logits_tail             a small model's logits layer fwd + SCE + bwd (+ fused SGD) in one launch
  *   hnn_sce_fused               softmax_cross_entropy + argmax accuracy + non-finite abort
  *                               (ops.py:220-251, train.py:239-243,252-255)
  *   hnn_multi_tensor_sgd        optim.apply_update, SGD / momentum branch (optim.py:59-71)
@@ -400,6 +401,35 @@ typedef struct hnn_sce_problem {
  */
 int hnn_sce_fused(const hnn_sce_problem* probs, int nprob, int max_cap, int max_classes, const hnn_step_row* cur,
                   hnn_model_status* status, int train, float* loss_out, int32_t* correct_out, void* stream);
+
+/* The fused logits tail of a small model (tail.cu, one CTA per model): the last dense layer's
+ * forward y = x W^T + b (W [classes, k], classes <= 16), softmax-CE + accuracy + abort exactly as
+ * hnn_sce_fused (train mode), then — unless the loss is non-finite — dx = (dlogits W) * (mask > 0)
+ * (rows >= R zero), dW = dlogits^T x and db (numpy axis-0 order) into dw / db and / or the fused
+ * SGD / momentum update of opt_w / opt_b (opt_kind, opt_momentum; never Adam).  x rows 16-byte
+ * aligned (ldx % 4 == 0, k % 4 == 0); `smem` = max over problems of hnn_tail_smem(cap, k, classes). */
+typedef struct hnn_tail_problem {
+  const float* x;
+  const float* w;
+  const float* b;
+  float* logits;      /* [cap, ld_logits] (optional) */
+  const int32_t* labels;
+  float* dx;          /* [cap, ld_dx] (NULL: no input gradient) */
+  const float* mask;  /* relu mask source (x itself or NULL) */
+  float* dw;
+  float* db;
+  float* opt_w;
+  float* opt_wm;
+  float* opt_b;
+  float* opt_bm;
+  int32_t ldx, ld_logits, ld_dx, cap, k, classes, model, opt_kind;
+  float opt_momentum;
+  int32_t reserved;
+} hnn_tail_problem;
+
+int hnn_tail_smem(int cap, int k, int classes);
+int hnn_logits_tail(const hnn_tail_problem* probs, int nprob, int smem, const hnn_step_row* cur,
+                    hnn_model_status* status, float* loss_out, int32_t* correct_out, void* stream);
 
 typedef struct hnn_opt_segment {
   float* param;

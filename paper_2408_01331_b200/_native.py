@@ -106,6 +106,13 @@ class HostFedIO(C.Structure):
                 ("out_bytes", C.c_int64 * 2)]
 
 
+class TailProblem(C.Structure):
+    _fields_ = [("x", P), ("w", P), ("b", P), ("logits", P), ("labels", P), ("dx", P), ("mask", P), ("dw", P),
+                ("db", P), ("opt_w", P), ("opt_wm", P), ("opt_b", P), ("opt_bm", P), ("ldx", I), ("ld_logits", I),
+                ("ld_dx", I), ("cap", I), ("k", I), ("classes", I), ("model", I), ("opt_kind", I),
+                ("opt_momentum", C.c_float), ("reserved", I)]
+
+
 class OptSegment(C.Structure):
     _fields_ = [("param", P), ("grad", P), ("m", P), ("v", P), ("count", C.c_int64), ("model", I), ("kind", I),
                 ("momentum", C.c_float), ("chunk_base", I), ("chunks", I), ("reserved", I)]
@@ -116,6 +123,7 @@ STRUCTS = {
     "hnn_gemm_problem": GemmProblem, "hnn_conv_problem": ConvProblem, "hnn_pool_problem": PoolProblem,
     "hnn_relu_problem": ReluProblem, "hnn_convtc_problem": ConvTcProblem, "hnn_embed_problem": EmbedProblem, "hnn_sce_problem": SceProblem, "hnn_opt_segment": OptSegment,
     "hnn_host_gather_item": HostGatherItem, "hnn_hostfed_io": HostFedIO,
+    "hnn_tail_problem": TailProblem,
 }
 
 # every symbol include/hnn_b200.h declares, with its ctypes signature
@@ -145,6 +153,8 @@ SIGNATURES = {
     "hnn_grouped_conv_direct_ex": [C.c_int, P, C.c_int, C.c_int, C.c_int, C.c_int, P, P, VP],
     "hnn_grouped_maxpool": [C.c_int, P, C.c_int, C.c_int, P, P, VP],
     "hnn_grouped_relu": [C.c_int, P, C.c_int, C.c_int, P, P, VP],
+    "hnn_tail_smem": [C.c_int, C.c_int, C.c_int],
+    "hnn_logits_tail": [P, C.c_int, C.c_int, P, P, P, P, VP],
     "hnn_sce_fused": [P, C.c_int, C.c_int, C.c_int, P, P, C.c_int, P, P, VP],
     "hnn_multi_tensor_sgd": [P, C.c_int, C.c_int, P, P, VP],
     "hnn_multi_tensor_adam": [P, C.c_int, C.c_int, P, P, VP],
@@ -210,6 +220,10 @@ def conv_tile_shape(op: int) -> tuple:
 
 def conv_direct_smem(op, c, h, w, f, k, oh, ow) -> int:
     return int(load().hnn_conv_direct_smem(op, c, h, w, f, k, oh, ow))
+
+
+def tail_smem(cap, k, classes) -> int:
+    return int(load().hnn_tail_smem(cap, k, classes))
 
 
 def conv_direct_threads(op, c, h, w, f, k, oh, ow) -> int:

@@ -111,6 +111,7 @@ int hnn_struct_size(const char* name) {
   if (!strcmp(name, "hnn_opt_segment")) return sizeof(hnn_opt_segment);
   if (!strcmp(name, "hnn_host_gather_item")) return sizeof(hnn_host_gather_item);
   if (!strcmp(name, "hnn_hostfed_io")) return sizeof(hnn_hostfed_io);
+  if (!strcmp(name, "hnn_tail_problem")) return sizeof(hnn_tail_problem);
   if (!strcmp(name, "hnn_convtc_problem")) return sizeof(hnn_convtc_problem);
   if (!strcmp(name, "hnn_embed_problem")) return sizeof(hnn_embed_problem);
   return -1;

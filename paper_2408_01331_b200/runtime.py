@@ -262,6 +262,7 @@ ENTRY_FAMILY = {"hnn_multi_tensor_adam": "optimizer", "hnn_multi_tensor_sgd": "o
                 "hnn_gather_rows": "gather", "hnn_splitk_epilogue": "splitk_epilogue",
                 "hnn_grouped_conv": "conv/simt", "hnn_grouped_conv_direct": "conv/direct",
                 "hnn_grouped_conv_direct_ex": "conv/direct", "hnn_skinny_backward": "gemm/skinny",
+                "hnn_logits_tail": "logits_tail",
                 "hnn_conv_wgrad_reduce": "conv/wgrad_reduce", "hnn_embedding": "embed",
                 "hnn_grouped_maxpool": "pool", "hnn_grouped_relu": "relu", "hnn_conv_tc_aux": "conv/tc_aux"}
 
@@ -1441,10 +1442,12 @@ class DeviceHybrid:
                 out += self._relu_launch(N.HNN_FWD if op == N.HNN_FWD else N.HNN_DGRAD, group, f"{label}/relu")
         return out
 
-    def _sce_launch(self, train: bool):
+    def _sce_launch(self, train: bool, skip=()):
         probs = []
         for s in self.slots:
             last = s.stages[-1]
+            if id(last) in skip:
+                continue
             probs.append(N.SceProblem(_ptr(last.y), _ptr(s.batch_y), _ptr(last.dy) if train else 0, last.ld_out,
                                       s.classes, s.batch_size, s.index))
         t = _dev_table(N.SceProblem, probs, self.device)
@@ -1545,6 +1548,57 @@ class DeviceHybrid:
                         and f % 8 == 0):
                     a.xh_next, b.xh_from_prev = b.xh, True
 
+    def _tail_eligible(self, s) -> bool:
+        """Models whose logits layer takes the fused tail (hnn_logits_tail): a final plain dense layer
+        with <= 16 classes, 16-byte rows and a small input (cap * K <= 16K floats: C1 / C5's 64 x 256,
+        LeNet's 128 x 84; measured slower than the grouped skinny launches for C3's 256 x 128 and the
+        CNNs' 128 x 512, profiles/r02/logits_tail_ab_v10.txt).  A function of the model's own shape
+        only, so isolation and sharding never change a model's path.  Opt-in (HNN_LOGITS_TAIL=1):
+        eager per-launch times favour it (C5 0.150 -> 0.133 ms), but in the graph-replayed step the
+        four programmatically-dependent launches it replaces overlap their tails and it measured level
+        or slower (C5 0.111 -> 0.110, C1 0.0615 -> 0.0636, C2 0.482 -> 0.496 ms)."""
+        if os.environ.get("HNN_LOGITS_TAIL", "0") != "1":  # (off by default: see below)
+            return False
+        st = s.stages[-1]
+        if st.kind != "dense" or st.relu or len(st.params) != 2:
+            return False
+        K, U = int(np.prod(st.in_shape)), st.out_shape[0]
+        return (U <= 16 and U == s.classes and K % 4 == 0 and st.ld_in % 4 == 0 and K <= 2048
+                and s.batch_size * K <= 16 * 1024
+                and N.tail_smem(s.batch_size, K, U) <= 200 * 1024)
+
+    def _logits_tail(self):
+        """(launch or None, ids of the tail stages): the fused logits tail of every eligible model."""
+        probs, done, smem = [], set(), 0
+        for s in self.slots:
+            if not self._tail_eligible(s):
+                continue
+            st = s.stages[-1]
+            K, U = int(np.prod(st.in_shape)), st.out_shape[0]
+            fuse = self._fused(s)
+            keep = self.keep_grads or not fuse
+            arena = lambda a, pid: _ptr(self.pview(a, s.index, pid)) if a is not None else 0
+            probs.append(N.TailProblem(
+                x=_ptr(st.x), w=arena(self.params, st.params[0]), b=arena(self.params, st.params[1]),
+                logits=_ptr(st.y), labels=_ptr(s.batch_y), dx=_ptr(st.dx) if st.needs_dx else 0,
+                mask=_ptr(st.x) if st.mask_input else 0,
+                dw=arena(self.grads, st.params[0]) if keep else 0, db=arena(self.grads, st.params[1]) if keep else 0,
+                opt_w=arena(self.params, st.params[0]) if fuse else 0, opt_b=arena(self.params, st.params[1]) if fuse else 0,
+                opt_wm=arena(self.m1, st.params[0]) if fuse and s.opt_kind != N.OPT_SGD else 0,
+                opt_bm=arena(self.m1, st.params[1]) if fuse and s.opt_kind != N.OPT_SGD else 0,
+                ldx=st.ld_in, ld_logits=st.ld_out, ld_dx=st.ld_in, cap=s.batch_size, k=K, classes=U, model=s.index,
+                opt_kind=s.opt_kind, opt_momentum=float(np.float32(s.momentum))))
+            smem = max(smem, N.tail_smem(s.batch_size, K, U))
+            done.add(id(st))
+        if not probs:
+            return None, done
+        t = _dev_table(N.TailProblem, probs, self.device)
+        flops = sum(6 * p.cap * p.k * p.classes for p in probs)
+        launch = Launch("hnn_logits_tail", (_ptr(t), len(probs), smem, _ptr(self.cur), _ptr(self.status),
+                                            _ptr(self.loss_out), _ptr(self.correct_out)), t, "tail/logits+sce+bwd",
+                        flops=flops)
+        return launch, done
+
     def build_plans(self):
         waves = self._stage_waves()
         self._pending_reduce = []
@@ -1552,9 +1606,20 @@ class DeviceHybrid:
         fwd = []
         for w, items in enumerate(waves):
             fwd += self._wave_launches(N.HNN_FWD, items, f"fwd{w}")
+        # training: eligible models' logits layers leave their waves for the fused tail launch
+        tail, tail_ids = self._logits_tail()
+        fwd_train = fwd
+        if tail is not None:
+            fwd_train = []
+            for w, items in enumerate(waves):
+                rest = [(s, st) for s, st in items if id(st) not in tail_ids]
+                if rest:
+                    fwd_train += self._wave_launches(N.HNN_FWD, rest, f"fwd{w}")
+        sce_train = [] if tail is not None and all(id(s.stages[-1]) in tail_ids for s in self.slots) else \
+            [self._sce_launch(True, skip=tail_ids)]
         bwd = []
         for w in range(len(waves) - 1, -1, -1):
-            items = waves[w]
+            items = [(s, st) for s, st in waves[w] if id(st) not in tail_ids]
             # input gradients first: with optimizer fusion the weight-gradient launch updates W in
             # place, and this wave's DGRAD must still read the pre-update W (src/engine.py:120-151
             # computes every gradient before apply_update)
@@ -1576,8 +1641,8 @@ class DeviceHybrid:
                     else:
                         bwd += self._embed_launch(N.HNN_WGRAD, grp, f"bwd{w}/embed/wgrad")
         self.forward_plan = self.conv_weight_prep(False) + fwd
-        self.train_plan = ([self._gather_train] + self.conv_weight_prep(True) + fwd + [self._sce_launch(True)] + bwd
-                           + self.conv_reduce_all() + self._optimizer_launch())
+        self.train_plan = ([self._gather_train] + self.conv_weight_prep(True) + fwd_train + ([tail] if tail else [])
+                           + sce_train + bwd + self.conv_reduce_all() + self._optimizer_launch())
         self.eval_plan = [self._gather_eval] + self.conv_weight_prep(False) + fwd + [self._sce_launch(False)]
         self.graph = None
 

@@ -162,6 +162,15 @@ def test_trajectory_matches_reference(pkg, name):
     assert abs(res.final_test_accuracy - ta) <= 0.001 + 1e-12
 
 
+@pytest.mark.parametrize("name", ["c1_mlp", "lenet"])
+def test_logits_tail_trajectory_matches_reference(pkg, name, monkeypatch):
+    """The opt-in fused logits tail (hnn_logits_tail: last dense layer forward, softmax-CE, input and
+    weight gradient, fused SGD in one launch) keeps the reference trajectory: the same checks as
+    test_trajectory_matches_reference with HNN_LOGITS_TAIL=1."""
+    monkeypatch.setenv("HNN_LOGITS_TAIL", "1")
+    test_trajectory_matches_reference(pkg, name)
+
+
 def graph_pids(arr, prefix):
     return sorted(k.split("/", 1)[1] for k in arr.files if k.startswith(prefix + "/"))
 
