@@ -317,6 +317,18 @@ def roofline(dev, per_launch_ms, workload):
         f["launches"] += 1
         f["tensor"] = f["tensor"] or launch.family.startswith("gemm/tc2") or launch.family.startswith("gemm/tc")
     total = float(per_launch_ms.sum())
+
+    def frac_of(fname, fam):  # each family against its own roofline (reported next to the dominant one)
+        sec_ = fam["ms"] / 1e3
+        if fam["tensor"] and fam["flops"]:
+            pk = tf_burst if fname.endswith("bf16") else TRIPLE_TF32_PEAK
+            return {"bound": "tensor", "achieved": round(fam["flops"] / sec_ / 1e12, 2), "peak": pk, "unit": "TFLOP/s",
+                    "frac": round(fam["flops"] / sec_ / 1e12 / pk, 4), "share_of_step": round(fam["ms"] / total, 4)}
+        if fam["nbytes"]:
+            return {"bound": "hbm", "achieved": round(fam["nbytes"] / sec_ / 1e9, 1), "peak": hbm, "unit": "GB/s",
+                    "frac": round(fam["nbytes"] / sec_ / 1e9 / hbm, 4), "share_of_step": round(fam["ms"] / total, 4)}
+        return None
+
     name, f = max(fams.items(), key=lambda kv: kv[1]["ms"])
     sec = f["ms"] / 1e3
     rec, src = traffic_record(workload)
@@ -324,8 +336,10 @@ def roofline(dev, per_launch_ms, workload):
     if rec is not None and name in rec.get("families", {}):
         traffic = rec["families"][name]["dram_bytes_per_step"]
     shares = {k: round(v["ms"] / total, 4) for k, v in sorted(fams.items(), key=lambda kv: -kv[1]["ms"])}
+    others = {k: frac_of(k, v) for k, v in sorted(fams.items(), key=lambda kv: -kv[1]["ms"])[:4] if k != name}
     out = {"kernel": name, "launches_per_step": f["launches"], "share_of_step": round(f["ms"] / total, 4),
            "ms_per_step": round(f["ms"], 4), "family_shares": shares,
+           "other_families": {k: v for k, v in others.items() if v is not None},
            "traffic_unit": "DRAM bytes per step of this family (ncu --set full, one eager step)",
            "traffic_source": src}
     if f["tensor"] and f["flops"]:
