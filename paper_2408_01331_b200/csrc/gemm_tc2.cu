@@ -58,13 +58,9 @@ constexpr int TC2_STAGES = 3;  // ring bytes = 2 * TC2_STAGES * 32 KB (raw A | r
 #endif
 constexpr int TC2_RAW = HNN_TC2_RAW_STAGES, TC2_LO = 2 * TC2_STAGES - TC2_RAW;
 static_assert(TC2_RAW >= 2 && TC2_LO >= 2, "raw / lo ring depths");
-// HNN_TC2_WG3 = 1: a fourth warpgroup (warps 12-15) adds two converter warps (12, 13; 14, 15 idle), so
-// narrow tiles, whose per-K-block work is dominated by converting the A tile, convert twice as fast
-#ifndef HNN_TC2_WG3
-#define HNN_TC2_WG3 0
-#endif
-constexpr int TC2_CONV_WARPS = HNN_TC2_WG3 ? 4 : 2;
-constexpr int TC2_THREADS = HNN_TC2_WG3 ? 512 : 384;
+constexpr int TC2_CONV_WARPS = 2;  // (a fourth warpgroup with two more converter warps measured no gain:
+                                   //  profiles/r02/wg3_converters_ab_v9.txt)
+constexpr int TC2_THREADS = 384;
 #ifndef HNN_TC2_CHUNK_KB
 #define HNN_TC2_CHUNK_KB 2
 #endif
@@ -77,10 +73,10 @@ constexpr int TC2_CHUNK_KB = HNN_TC2_CHUNK_KB;
 #endif
 constexpr int TC2_PROMO_COLS = HNN_TC2_PROMO_COLS;
 #ifndef HNN_TC2_REGS_ACC
-#define HNN_TC2_REGS_ACC (HNN_TC2_WG3 ? 200 : 216)  // 0: no setmaxnreg split
+#define HNN_TC2_REGS_ACC 216  // 0: no setmaxnreg split
 #endif
 #ifndef HNN_TC2_REGS_LO
-#define HNN_TC2_REGS_LO (HNN_TC2_WG3 ? 56 : 72)
+#define HNN_TC2_REGS_LO 72
 #endif  // accumulator columns per TMEM load in the promotion
 // K blocks per TMEM accumulation chunk of one tile: a fused-SGD weight-gradient tile whose whole K
 // fits 4 blocks keeps one chunk (its epilogue reads the finished sums straight from TMEM)
@@ -334,7 +330,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC2_THREADS, 1)
   static_assert((TC2_THREADS - 256) * HNN_TC2_REGS_LO + 256 * HNN_TC2_REGS_ACC <= TC2_THREADS * ((65536 / TC2_THREADS) & ~7),
                 "register split");
 #endif
-  if (warp < 4 || warp >= 12) {
+  if (warp < 4) {
 #if HNN_TC2_REGS_ACC
   asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(HNN_TC2_REGS_LO));
 #endif
@@ -522,10 +518,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC2_THREADS, 1)
         }
       }
     }
-  } else if (warp < 4 + 2 * HNN_TC2_WG3 + 8 * HNN_TC2_WG3) {
+  } else {
     // ---------------- converters (both CTAs): lo = rna_tf32(x - trunc_tf32(x)); raw stays as hi
-    // (warps 2, 3 and, with the fourth warpgroup, 12, 13; warps 14, 15 idle)
-    const int ct = (warp < 4 ? warp - 2 : warp - 10) * 32 + lane;
+    const int ct = threadIdx.x - 64;
     constexpr int CT = 32 * TC2_CONV_WARPS, PER = TC2_STAGE / 16 / CT, NPART = 4, PART = PER / NPART;
     const uint32_t lo_full_leader = map_cluster(bar(LO_FULL), 0);
     uint32_t kg = 0, iseq = 0;

@@ -701,13 +701,12 @@ class DeviceHybrid:
         sms = torch.cuda.get_device_properties(self.device).multi_processor_count
         npairs = max(1, min(total_tiles, sms // 2))
         costs = []
-        ca, cb, ce = (float(v) for v in os.environ.get("HNN_LPT_COST", "0.5,0.5,3").split(","))
         for pr, (s, d) in zip(probs, rows):
             split = d.get("ksplit", 1) if d.get("ksplit_len") else 1
             kb = -(-(d["ksplit_len"] if split > 1 else d["k"]) // 32)
             tiles = pr.tiles_n * -(-d["m"] // tm) * split
             width = pr.tile_n / 256  # MMA and operand time scale with the tile's columns
-            costs += [(kb * (ca + cb * width) + ce, pr.tile_base + i) for i in range(tiles)]
+            costs += [(kb * (0.5 + 0.5 * width) + 3, pr.tile_base + i) for i in range(tiles)]
         costs.sort(key=lambda c: (-c[0], c[1]))
         import heapq
 
