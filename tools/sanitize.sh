@@ -4,7 +4,7 @@ for prec in f32 bf16; do
   for tool in memcheck racecheck synccheck; do
     timeout 900 compute-sanitizer --tool $tool --print-limit 20 python tools/sanitize_step.py $prec > /tmp/san.log 2>&1
     echo "rc=$?" >> /tmp/san.log
-    (head -40 /tmp/san.log; echo "[...]"; tail -25 /tmp/san.log) > gpurun_out/san/${tool}_${prec}_v7.log
+    (head -40 /tmp/san.log; echo "[...]"; tail -25 /tmp/san.log) > gpurun_out/san/${tool}_${prec}_v13.log
   done
 done
 echo done
