@@ -40,6 +40,8 @@
 // and the lo slot's previous MMAs are done (up to TC2_LO - 1 K blocks ahead of the MMAs).
 // Barriers: raw full/empty, acc full: per CTA (the leader's commits multicast to both);
 // lo full and acc empty: in the leader, arrived on by both CTAs.
+#include <algorithm>
+#include <cstdlib>
 #include <cuda_bf16.h>
 
 #include "tc_common.cuh"
@@ -949,7 +951,8 @@ int launch_tc2(int op, const hnn_gemm_problem* probs, int nprob, int total_tiles
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   }
-  const int pairs = total_tiles < sms / 2 ? total_tiles : sms / 2;
+  int pairs = total_tiles < sms / 2 ? total_tiles : sms / 2;
+  if (const char* g = getenv("HNN_TC2_PAIRS")) pairs = std::max(1, std::min(pairs, atoi(g)));  // (probe: SM share)
   const int grid = 2 * pairs;
   if (op == HNN_FWD)
     hnn::launch_pdl(gemm_tc2_kernel<HNN_FWD, KIND>, dim3(grid), dim3(TC2_THREADS), TC2_SMEM_BYTES, s, probs, nprob, total_tiles, cur, status);

@@ -7,6 +7,7 @@
 // explicit round-to-nearest intrinsics (numpy never contracts to FMA), so
 // given the same gradients the update is bit-identical to apply_update.
 #include <cstdlib>
+#include <algorithm>
 
 #include "common.cuh"
 
@@ -290,7 +291,8 @@ int launch_multi_tensor(const char* who, const hnn_opt_segment* segs, int nseg, 
   }
   if (bulk) {
     const int units = total_chunks * (OPT_CHUNK / OPTB_E);
-    const int grid = units < OPTB_CTAS * sms ? units : OPTB_CTAS * sms;
+    int grid = units < OPTB_CTAS * sms ? units : OPTB_CTAS * sms;
+    if (const char* g = getenv("HNN_OPT_GRID")) grid = std::max(1, std::min(grid, atoi(g)));  // (probe: SM share)
     hnn::launch_pdl(multi_tensor_bulk_kernel, dim3(grid), dim3(OPTB_THREADS), OPTB_SMEM, as_stream(stream), segs, nseg,
                     units, cur, status);
     return check_launch(who);
