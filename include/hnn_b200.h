@@ -359,11 +359,19 @@ typedef struct hnn_pool_problem {
   int32_t model;
   int32_t block_base;
   int32_t blocks;
-  int32_t reserved;
+  /* HNN_POOL_ELEMENTWISE: one thread per output (FWD) / input element (DGRAD), 256 per block.
+   * HNN_POOL_WINDOWS_2X2 (k = stride = 2, h and w even): one unit per 2 x 2 window for both ops,
+   * HNN_POOL_WINDOWS_PER_BLOCK windows per block, row pairs moved as float2 */
+  int32_t mode;
   /* FWD: when non-NULL, the output is also written as NHWC bf16 rows [cap * oh * ow, c] (zeros
    * past the batch): the next layer's implicit-GEMM input */
   void* xh;
 } hnn_pool_problem;
+#define HNN_POOL_ELEMENTWISE 0
+#define HNN_POOL_WINDOWS_2X2 1
+#ifndef HNN_POOL_WINDOWS_PER_BLOCK
+#define HNN_POOL_WINDOWS_PER_BLOCK 1024
+#endif
 
 int hnn_grouped_maxpool(int op, const hnn_pool_problem* probs, int nprob, int total_blocks,
                         const hnn_step_row* cur, const hnn_model_status* status, void* stream);

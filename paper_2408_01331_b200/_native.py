@@ -83,7 +83,26 @@ class EmbedProblem(C.Structure):
 class PoolProblem(C.Structure):
     _fields_ = [("x", P), ("y", P), ("idx", P), ("dy", P), ("dx", P), ("mask", P),
                 ("cap", I), ("c", I), ("h", I), ("w", I), ("k", I), ("stride", I), ("oh", I), ("ow", I),
-                ("model", I), ("block_base", I), ("blocks", I), ("reserved", I), ("xh", P)]
+                ("model", I), ("block_base", I), ("blocks", I), ("mode", I), ("xh", P)]
+
+
+POOL_ELEMENTWISE, POOL_WINDOWS_2X2 = 0, 1  # (hnn_b200.h)
+# HNN_POOL_WINDOWS_PER_BLOCK: the library's build constant (the override is for variant builds only)
+POOL_WINDOWS_PER_BLOCK = int(os.environ.get("HNN_POOL_WINDOWS_PER_BLOCK", "1024"))
+
+
+def pool_mode_blocks(op: int, cap: int, c: int, h: int, w: int, k: int, stride: int, oh: int, ow: int,
+                     ptrs=()):
+    """(mode, blocks) of one hnn_pool_problem: 2 x 2 / stride 2 windows on even planes run in window
+    mode (HNN_POOL_WINDOWS_PER_BLOCK windows per block, both directions); other pools one element per
+    thread, 256 per block.  ptrs: the plane-sized tensors the window form moves as float2 (8-byte
+    aligned or elementwise).  HNN_POOL_WINDOWS=0 forces the elementwise form (A/B, tests)."""
+    import os
+
+    if (k == 2 and stride == 2 and h % 2 == 0 and w % 2 == 0 and all(p % 8 == 0 for p in ptrs)
+            and os.environ.get("HNN_POOL_WINDOWS", "1") != "0"):
+        return POOL_WINDOWS_2X2, -(-(cap * c * oh * ow) // POOL_WINDOWS_PER_BLOCK)
+    return POOL_ELEMENTWISE, -(-(cap * c * (oh * ow if op == HNN_FWD else h * w)) // 256)
 
 
 class ReluProblem(C.Structure):

@@ -1,7 +1,8 @@
 // Grouped max-pool (fwd/bwd, relu mask fused into bwd) and stand-alone relu
-// (pkg/src/hybridnn/ops.py:62-67, 149-174).  HBM-bound elementwise kernels:
-// one thread per output (fwd) or per input element (bwd, gather form, so the
-// reference's np.add.at scatter becomes a fixed-order sum with no atomics).
+// (pkg/src/hybridnn/ops.py:62-67, 149-174).  HBM-bound elementwise kernels.  Per problem
+// (hnn_pool_problem.mode): 2 x 2 / stride 2 pools on even planes run one thread per four windows
+// (both directions); other windows one thread per output (fwd) or per input element (bwd,
+// gather form, so the reference's np.add.at scatter becomes a fixed-order sum with no atomics).
 #include <cuda_bf16.h>
 
 #include "common.cuh"
@@ -10,6 +11,122 @@ namespace hnn {
 
 constexpr int PTHREADS = 256;
 
+// ------------------------------------------------------------- 2 x 2 windows (HNN_POOL_WINDOWS_2X2)
+// One unit per window for both directions, PW windows per thread with every load issued before
+// the first compare: the elementwise form (one 256-element CTA per block, ~5 dependent round trips
+// per CTA: problem search, problem, batch rows, data, store) ran 16 waves of latency-bound CTAs
+// per SM (C2's first pool gradient: 46 us for 45 MB).  h and w are even, so a window's two row
+// pairs are aligned float2 and (DGRAD) every input element lies in exactly one window.
+constexpr int PW = HNN_POOL_WINDOWS_PER_BLOCK / PTHREADS;
+static_assert(PW * PTHREADS == HNN_POOL_WINDOWS_PER_BLOCK, "whole windows per thread");
+
+struct WinPos {
+  int plane, b, pix;  // pix: the window's top-left input element within its plane
+};
+
+__device__ __forceinline__ WinPos win_pos(const hnn_pool_problem& p, int e) {
+  const int ohw = p.oh * p.ow;
+  WinPos r;
+  r.plane = e / ohw;
+  const int o = e - r.plane * ohw, oy = o / p.ow, ox = o - oy * p.ow;
+  r.b = r.plane / p.c;
+  r.pix = (2 * oy) * p.w + 2 * ox;
+  return r;
+}
+
+__device__ __forceinline__ void maxpool2_fwd(const hnn_pool_problem& p, int rows) {
+  const int total = p.cap * p.c * p.oh * p.ow, hw = p.h * p.w;
+  const int e0 = (blockIdx.x - p.block_base) * HNN_POOL_WINDOWS_PER_BLOCK + threadIdx.x;
+  float2 r0[PW], r1[PW];
+#pragma unroll
+  for (int u = 0; u < PW; ++u) {
+    const int e = e0 + u * PTHREADS;
+    r0[u] = r1[u] = make_float2(0.0f, 0.0f);
+    if (e < total) {
+      const WinPos q = win_pos(p, e);
+      if (q.b < rows) {
+        const float* s0 = p.x + size_t(q.plane) * hw + q.pix;
+        r0[u] = *reinterpret_cast<const float2*>(s0);
+        r1[u] = *reinterpret_cast<const float2*>(s0 + p.w);
+      }
+    }
+  }
+  __nv_bfloat16* xh = reinterpret_cast<__nv_bfloat16*>(p.xh);  // NHWC bf16 copy: [(b, o), c]
+#pragma unroll
+  for (int u = 0; u < PW; ++u) {
+    const int e = e0 + u * PTHREADS;
+    if (e >= total) break;
+    const WinPos q = win_pos(p, e);
+    // numpy argmax over (0,0) (0,1) (1,0) (1,1): first max wins, first NaN wins outright
+    float best = r0[u].x;
+    int best_i = 0;
+    if (best == best) {
+      const float vs[3] = {r0[u].y, r1[u].x, r1[u].y};
+#pragma unroll
+      for (int k = 1; k < 4; ++k) {
+        const float v = vs[k - 1];
+        if (!(v <= best)) {
+          best = v;
+          best_i = k;
+          if (v != v) break;
+        }
+      }
+    }
+    if (q.b >= rows) best = 0.0f, best_i = 0;  // rows past the batch: zeros (loads skipped)
+    p.y[e] = best;
+    p.idx[e] = (uint8_t)best_i;
+    if (xh) {
+      const int ohw = p.oh * p.ow, o = e - q.plane * ohw;
+      xh[(size_t(q.b) * ohw + o) * p.c + (q.plane - q.b * p.c)] = __float2bfloat16_rn(best);
+    }
+  }
+}
+
+__device__ __forceinline__ void maxpool2_bwd(const hnn_pool_problem& p, int rows) {
+  const int total = p.cap * p.c * p.oh * p.ow, hw = p.h * p.w;
+  const int e0 = (blockIdx.x - p.block_base) * HNN_POOL_WINDOWS_PER_BLOCK + threadIdx.x;
+  float d[PW];
+  int ix[PW];
+  float2 m0[PW], m1[PW];
+#pragma unroll
+  for (int u = 0; u < PW; ++u) {
+    const int e = e0 + u * PTHREADS;
+    d[u] = 0.0f;
+    ix[u] = -1;  // (no window element selected: rows past the batch)
+    m0[u] = m1[u] = make_float2(1.0f, 1.0f);
+    if (e < total) {
+      const WinPos q = win_pos(p, e);
+      if (q.b < rows) {
+        d[u] = p.dy[e];
+        ix[u] = p.idx[e];
+        if (p.mask) {
+          const float* mk = p.mask + size_t(q.plane) * hw + q.pix;
+          m0[u] = *reinterpret_cast<const float2*>(mk);
+          m1[u] = *reinterpret_cast<const float2*>(mk + p.w);
+        }
+      }
+    }
+  }
+#pragma unroll
+  for (int u = 0; u < PW; ++u) {
+    const int e = e0 + u * PTHREADS;
+    if (e >= total) break;
+    const WinPos q = win_pos(p, e);
+    float g[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) g[k] = __fadd_rn(0.0f, ix[u] == k ? d[u] : 0.0f);  // np.add.at into zeros
+    if (p.mask && ix[u] >= 0) {
+      g[0] = np_mask(g[0], m0[u].x);
+      g[1] = np_mask(g[1], m0[u].y);
+      g[2] = np_mask(g[2], m1[u].x);
+      g[3] = np_mask(g[3], m1[u].y);
+    }
+    float* dx = p.dx + size_t(q.plane) * hw + q.pix;
+    *reinterpret_cast<float2*>(dx) = make_float2(g[0], g[1]);
+    *reinterpret_cast<float2*>(dx + p.w) = make_float2(g[2], g[3]);
+  }
+}
+
 __global__ void __launch_bounds__(PTHREADS) maxpool_fwd_kernel(const hnn_pool_problem* __restrict__ probs, int nprob,
                                                                const hnn_step_row* __restrict__ cur,
                                                                const hnn_model_status* __restrict__ status) {
@@ -17,6 +134,7 @@ __global__ void __launch_bounds__(PTHREADS) maxpool_fwd_kernel(const hnn_pool_pr
   const int pi = find_problem(probs, nprob, blockIdx.x, [](const hnn_pool_problem& q) { return q.block_base; });
   const hnn_pool_problem p = probs[pi];
   if (!live(cur, status, p.model)) return;
+  if (p.mode == HNN_POOL_WINDOWS_2X2) return maxpool2_fwd(p, cur[p.model].rows);
   // 32-bit index arithmetic (the host keeps cap*c*h*w < 2^31): 64-bit divisions made these
   // elementwise kernels issue-bound (0.12 ms for a 33 MB pool gradient)
   const int e = (blockIdx.x - p.block_base) * PTHREADS + threadIdx.x;
@@ -78,6 +196,7 @@ __global__ void __launch_bounds__(PTHREADS) maxpool_bwd_kernel(const hnn_pool_pr
   const int pi = find_problem(probs, nprob, blockIdx.x, [](const hnn_pool_problem& q) { return q.block_base; });
   const hnn_pool_problem p = probs[pi];
   if (!live(cur, status, p.model)) return;
+  if (p.mode == HNN_POOL_WINDOWS_2X2) return maxpool2_bwd(p, cur[p.model].rows);
   const int e = (blockIdx.x - p.block_base) * PTHREADS + threadIdx.x;
   const int total = p.cap * p.c * p.h * p.w;
   if (e >= total) return;

@@ -119,10 +119,9 @@ def _pool(op, x, y, idx, dy, dx, attrs):
     k = attrs["kernel"]
     s = attrs.get("stride", k)
     oh, ow = conv_extent(h, k, s, 0), conv_extent(w, k, s, 0)
-    total = n * c * (oh * ow if op == N.HNN_FWD else h * w)
-    blocks = -(-total // 256)
+    mode, blocks = N.pool_mode_blocks(op, n, c, h, w, k, s, oh, ow, (_ptr(x), _ptr(dx)) if op != N.HNN_FWD else (_ptr(x),))
     prob = N.PoolProblem(_ptr(x), _ptr(y), _ptr(idx), _ptr(dy), _ptr(dx), 0, n, c, h, w, k, s, oh, ow, 0, 0,
-                         blocks, 0)
+                         blocks, mode)
     t = _dev_table(N.PoolProblem, [prob], x.device)
     N.call("hnn_grouped_maxpool", op, _ptr(t), 1, blocks, _ptr(_cur(n)), 0, _stream())
     _torch().cuda.current_stream().synchronize()

@@ -1394,13 +1394,13 @@ class DeviceHybrid:
             k = st.attrs["kernel"]
             stride = st.attrs.get("stride", k)
             oh, ow = conv_extent(h, k, stride, 0), conv_extent(w, k, stride, 0)
-            total = s.batch_size * c * (oh * ow if op == N.HNN_FWD else h * w)
             if s.batch_size * c * h * w >= 2 ** 31:  # (the pool kernels index in 32 bits)
                 raise UnsupportedGraphError(f"{st.node_id}: pooled tensor above 2^31 elements")
-            blocks = -(-total // 256)
+            mode, blocks = N.pool_mode_blocks(op, s.batch_size, c, h, w, k, stride, oh, ow,
+                                              (_ptr(st.x), _ptr(st.dx)) if op != N.HNN_FWD else (_ptr(st.x),))
             probs.append(N.PoolProblem(_ptr(st.x), _ptr(st.y), _ptr(st.idx), _ptr(st.dy), _ptr(st.dx),
                                        _ptr(st.x) if st.mask_input else 0, s.batch_size, c, h, w, k, stride, oh,
-                                       ow, s.index, base, blocks, 0,
+                                       ow, s.index, base, blocks, mode,
                                        _ptr(st.xh_next) if op == N.HNN_FWD else 0))
             base += blocks
         nbytes = sum(4 * p.cap * p.c * (p.h * p.w + p.oh * p.ow) + p.cap * p.c * p.oh * p.ow for p in probs)

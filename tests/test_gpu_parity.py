@@ -72,6 +72,31 @@ def test_ops_match_reference_registry(pkg):
     assert np.array_equal(dp["bias"], arr["dense/d_bias"])
 
 
+@pytest.mark.parametrize("shape", [(3, 6, 28, 28), (2, 16, 10, 10), (5, 4, 2, 2), (2, 3, 8, 6), (2, 2, 9, 8)])
+@pytest.mark.parametrize("windows", ["1", "0"])
+def test_maxpool_k2_window_and_elementwise_forms_are_bit_exact(pkg, shape, windows, monkeypatch):
+    """2 x 2 max-pool through the plugin path in both kernel forms (pool_relu.cu: window mode, four
+    windows per thread; elementwise mode, one element per thread; (9, 8) planes always take the
+    elementwise form) vs the oracle's numpy argmax / np.add.at (src/ops.py:149-174) bit for bit, on
+    values with many ties, NaNs and signed zeros."""
+    monkeypatch.setenv("HNN_POOL_WINDOWS", windows)
+    g = np.random.default_rng(sum(shape))
+    x = (np.round(g.normal(size=shape) * 2) / 2).astype(np.float32)  # (ties in most windows)
+    flat = x.reshape(-1)
+    flat[g.choice(flat.size, flat.size // 50 + 1, replace=False)] = np.nan
+    flat[g.choice(flat.size, flat.size // 20 + 1, replace=False)] = -0.0
+    kind, attrs = pkg.OP_KINDS["maxpool2d"], {"kernel": 2}
+    y, aux = kind.forward(x, {}, attrs)
+    ry, saved = oracle.op_forward("maxpool2d", x, {}, attrs)
+    assert np.array_equal(y, ry, equal_nan=True)
+    assert np.array_equal(np.signbit(y), np.signbit(ry))
+    dy = g.normal(size=y.shape).astype(np.float32)
+    dy.reshape(-1)[:: 7] = -0.0
+    dx, _ = kind.backward(dy, aux, {}, attrs)
+    rdx, _ = oracle.op_backward("maxpool2d", dy, saved, {}, attrs)
+    assert np.array_equal(dx, rdx) and np.array_equal(np.signbit(dx), np.signbit(rdx))
+
+
 @pytest.mark.parametrize("rows,units,feats", [(200, 100, 96), (256, 256, 128), (37, 64, 64)])
 def test_dense_bias_gradient_column_sum_is_bit_exact(pkg, rows, units, feats):
     """The plugin path's dense bias gradient equals numpy's axis-0 float32 sum of dY bit for bit
