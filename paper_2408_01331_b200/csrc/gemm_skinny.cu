@@ -131,8 +131,8 @@ __global__ void __launch_bounds__(KTHREADS) skinny_fwd_kernel(const hnn_gemm_pro
 
 // FWD, bulk-copy form (problems with 16-byte rows and K % 128 == 0: the C1 / C3 / C5 logits
 // layers): the same 16-row tile, its x rows and the n <= 16 W rows streamed through a 4-stage
-// shared-memory ring in 128-float K chunks by a producer warp (cp.async.bulk, one row per lane), 256
-// update threads = 16 rows x 16 K-slices (float4 each), slices combined by a fixed xor tree.  The
+// shared-memory ring in 128-float K chunks by a producer warp (cp.async.bulk, one row per lane), 8
+// update warps = 2 rows each x 32 K-slices (float4 each), slices combined by a fixed xor tree.  The
 // per-warp streaming form walked each row's whole K as a chain of dependent L2 / HBM round trips
 // at 24 warps per SM (C3: 39 us for 35.6 MB, ncu long-scoreboard bound).  Other problems take the
 // per-warp form inside the same launch (the tile shape is shared).
@@ -145,6 +145,7 @@ __global__ void __launch_bounds__(KTHREADS) skinny_fwd_kernel(const hnn_gemm_pro
 constexpr int FB_KC = HNN_FB_KC, FB_STAGES = HNN_FB_STAGES, FB_THREADS = KTHREADS + 32;
 constexpr int FB_STAGE_BYTES = 2 * 16 * FB_KC * 4;  // 16 x rows + 16 W rows
 constexpr int FB_SMEM = FB_STAGES * FB_STAGE_BYTES + 256;
+static_assert(FB_KC % 128 == 0 && 8 * FWD_ROWS == 16, "lane = float4 slice of each 128-wide K block; 16-row tiles");
 
 __device__ __forceinline__ bool fwd_bulk_ok(const hnn_gemm_problem& p) {
   return p.n <= 16 && (p.k % FB_KC) == 0 && (p.lda & 3) == 0 && (p.ldb & 3) == 0 &&
@@ -194,45 +195,60 @@ __device__ __forceinline__ void fwd_bulk_tile(const hnn_gemm_problem& p, int r0,
     }
     return;
   }
-  // ---------------- 16 rows x 16 K-slices
-  const int r = threadIdx.x / 16, sl = threadIdx.x % 16;
-  float acc[NJ];
+  // ---------------- 8 warps x FWD_ROWS rows, lane = K-slice: lane l holds float4 l of every 128
+  // K-wide block, exactly the per-warp form's assignment (rowdot_rows), so both forms add every dot
+  // product in the same order (and the same 32-lane xor tree); each W float4 read from shared
+  // memory serves the warp's FWD_ROWS rows (16 K-slices x 16 rows re-read the W rows once per row:
+  // shared-memory bound, 31 us on C3)
+  float acc[FWD_ROWS][NJ];
 #pragma unroll
-  for (int j = 0; j < NJ; ++j) acc[j] = 0.0f;
+  for (int i = 0; i < FWD_ROWS; ++i)
+#pragma unroll
+    for (int j = 0; j < NJ; ++j) acc[i][j] = 0.0f;
   for (int c = 0; c < nchunks; ++c) {
     const int st = c % FB_STAGES;
     wait(bar(st), (c / FB_STAGES) & 1);
-    const float* xs = reinterpret_cast<const float*>(smem + st * FB_STAGE_BYTES) + r * FB_KC;
+    const float* xs = reinterpret_cast<const float*>(smem + st * FB_STAGE_BYTES) + warp * FWD_ROWS * FB_KC;
     const float* ws = reinterpret_cast<const float*>(smem + st * FB_STAGE_BYTES) + 16 * FB_KC;
 #pragma unroll
-    for (int i = 0; i < FB_KC / 64; ++i) {
-      const int k = (sl + 16 * i) * 4;
-      const float4 u = *reinterpret_cast<const float4*>(xs + k);
+    for (int h = 0; h < FB_KC / 128; ++h) {
+      const int k = (lane + 32 * h) * 4;
+      float4 u[FWD_ROWS];
 #pragma unroll
-      for (int j = 0; j < NJ; ++j) acc[j] = dot4(u, *reinterpret_cast<const float4*>(ws + j * FB_KC + k), acc[j]);
+      for (int i = 0; i < FWD_ROWS; ++i) u[i] = *reinterpret_cast<const float4*>(xs + i * FB_KC + k);
+#pragma unroll
+      for (int j = 0; j < NJ; ++j) {
+        const float4 w = *reinterpret_cast<const float4*>(ws + j * FB_KC + k);
+#pragma unroll
+        for (int i = 0; i < FWD_ROWS; ++i) acc[i][j] = dot4(u[i], w, acc[i][j]);
+      }
     }
-    asm volatile("bar.sync 1, %0;" ::"n"(KTHREADS) : "memory");  // every slice has read stage st
+    asm volatile("bar.sync 1, %0;" ::"n"(KTHREADS) : "memory");  // every warp has read stage st
     if (threadIdx.x == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar(FB_STAGES + st)) : "memory");
   }
-  // fixed xor tree over the 16 slices of a row (lanes 16 apart never mix: offsets < 16)
 #pragma unroll
-  for (int j = 0; j < NJ; ++j)
+  for (int i = 0; i < FWD_ROWS; ++i)
 #pragma unroll
-    for (int o = 8; o > 0; o >>= 1) acc[j] += __shfl_xor_sync(0xffffffffu, acc[j], o);
-  const int row = r0 + r;
-  if (row >= p.m) return;
-  // slice lane sl writes column sl (sl < n): lane-local select of acc[sl]
-  float v = 0.0f;
+    for (int j = 0; j < NJ; ++j)
 #pragma unroll
-  for (int j = 0; j < NJ; ++j)
-    if (j == sl) v = acc[j];
-  if (sl >= p.n) return;
-  float y = 0.0f;
-  if (row < rows) {
-    y = __fadd_rn(v, __ldg(p.bias + sl));
-    if (p.relu) y = np_relu(y);
+      for (int o = 16; o > 0; o >>= 1) acc[i][j] += __shfl_xor_sync(0xffffffffu, acc[i][j], o);
+  if (lane >= p.n) return;
+  const float b = __ldg(p.bias + lane);
+#pragma unroll
+  for (int i = 0; i < FWD_ROWS; ++i) {
+    const int row = r0 + warp * FWD_ROWS + i;
+    if (row >= p.m) break;
+    float v = 0.0f;
+#pragma unroll
+    for (int j = 0; j < NJ; ++j)
+      if (j == lane) v = acc[i][j];
+    float y = 0.0f;
+    if (row < rows) {
+      y = __fadd_rn(v, b);
+      if (p.relu) y = np_relu(y);
+    }
+    p.c[size_t(row) * p.ldc + lane] = y;
   }
-  p.c[size_t(row) * p.ldc + sl] = y;
 }
 
 __global__ void __launch_bounds__(FB_THREADS) skinny_fwd_bulk_kernel(const hnn_gemm_problem* __restrict__ probs,
@@ -630,12 +646,13 @@ int skinny_tile_shape(int op, int32_t* tm, int32_t* tn) {
 int grouped_gemm_skinny(int op, const hnn_gemm_problem* probs, int nprob, int total_tiles, const hnn_step_row* cur,
                         const hnn_model_status* status, cudaStream_t s) {
   if (op == HNN_FWD) {
-    static int bulk = -1;
-    if (bulk < 0) {
-      const char* e = getenv("HNN_SKINNY_FWD_BULK");
-      bulk = e ? atoi(e) : 1;
-      if (bulk) cudaFuncSetAttribute(skinny_fwd_bulk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, FB_SMEM);
+    static bool configured = false;
+    if (!configured) {
+      cudaFuncSetAttribute(skinny_fwd_bulk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, FB_SMEM);
+      configured = true;
     }
+    const char* e = getenv("HNN_SKINNY_FWD_BULK");  // (0: the per-warp form, A/B and the bit-identity test)
+    const bool bulk = e ? atoi(e) != 0 : true;
     if (bulk)
       hnn::launch_pdl(skinny_fwd_bulk_kernel, dim3(total_tiles), dim3(FB_THREADS), FB_SMEM, s, probs, nprob, cur, status);
     else

@@ -1119,6 +1119,31 @@ def test_fused_skinny_backward_is_bit_identical(pkg, monkeypatch):
             assert np.array_equal(va[k], vb[k]), k
 
 
+def test_skinny_forward_bulk_and_per_warp_forms_are_bit_identical(pkg, monkeypatch):
+    """The logits forward's bulk-copy form (gemm_skinny.cu fwd_bulk_tile: rows streamed through a
+    shared-memory ring) and its per-warp streaming form give every lane the same K slices and the same
+    xor tree: 3 C3 steps end bit-identical (params, gradients) either way (src/ops.py:46-48)."""
+    import torch
+
+    import bench
+
+    device = torch.device("cuda", 0)
+    outs = []
+    for bulk in ("1", "0"):
+        monkeypatch.setenv("HNN_SKINNY_FWD_BULK", bulk)
+        _, jobs, hy, dev, ddev, ds, comm = bench.build_rank("c3", 0, 1, device)
+        rows = bench.schedule(jobs, ds, 3)
+        bench.upload_perms(dev, jobs, ds)
+        dev.load_schedule(rows)
+        dev.train_steps(3, use_graph=False)
+        torch.cuda.synchronize()
+        outs.append([(dev.download_params(m), dev.download_grads(m)) for m in (0, 7, 13, 31)])
+    for (pa, ga), (pb, gb) in zip(*outs):
+        for k in pa:
+            assert np.array_equal(pa[k], pb[k]), k
+            assert np.array_equal(ga[k], gb[k]), k
+
+
 def test_tf32_truncation_selftest(pkg):
     """The load-time check behind the 3xTF32 split (gemm_tc2.cu:11-13): raw fp32 operands are
     truncated to tf32 by the tensor core, so hi + lo reproduce x; the probe GEMM then misses only
