@@ -478,6 +478,9 @@ int hnn_multi_tensor_adam(const hnn_opt_segment* segs, int nseg, int total_chunk
  */
 #define HNN_CONVTC_IM2COL 0
 #define HNN_CONVTC_TRANSPOSE_DY 1
+/* HNN_CONVTC_TRANSPOSE_DY blocks: ceil(cap * ceil(oh*ow / 32) / HNN_CONVTC_TRANSPOSE_HW_TILES) * ceil(f / 32)
+ * (one block = 32 channels x HNN_CONVTC_TRANSPOSE_HW_TILES consecutive (sample, 32-pixel run) units) */
+#define HNN_CONVTC_TRANSPOSE_HW_TILES 4
 #define HNN_CONVTC_COL2IM 2
 #define HNN_CONVTC_WGRAD_REDUCE 3
 #define HNN_CONVTC_PAD_WEIGHTS 4  /* wpad[f, kk'] = w[f, kk] (kk' < kkp, zero pad): when C*k*k % 4 != 0 */

@@ -17,6 +17,13 @@ LIB_PATH = Path(__file__).resolve().parent / "_lib" / "libhnn_b200.so"
 HNN_FWD, HNN_DGRAD, HNN_WGRAD = 0, 1, 2
 PREC_SIMT, PREC_3XTF32, PREC_SIMT_SKINNY, PREC_3XTF32_PAIR, PREC_BF16_PAIR = 0, 1, 2, 3, 4
 CONVTC_IM2COL, CONVTC_TRANSPOSE_DY, CONVTC_COL2IM, CONVTC_WGRAD_REDUCE, CONVTC_PAD_WEIGHTS = 0, 1, 2, 3, 4
+CONVTC_TRANSPOSE_HW_TILES = 4  # (hnn_b200.h)
+
+
+def transpose_blocks(cap: int, hw: int, f: int) -> int:
+    """Blocks of one HNN_CONVTC_TRANSPOSE_DY problem: 32 channels x CONVTC_TRANSPOSE_HW_TILES
+    consecutive (sample, 32-pixel run) units per block."""
+    return -(-(cap * -(-hw // 32)) // CONVTC_TRANSPOSE_HW_TILES) * -(-f // 32)
 CONVTC_FLIP_WEIGHTS, CONVTC_WT_WEIGHTS, CONVTC_PAD_WEIGHTS_RSC, CONVTC_FLIP_WEIGHTS_RSC = 5, 6, 7, 8
 CONVTC_PARITY_WEIGHTS, CONVTC_SPLITK_FWD = 9, 10
 OPT_SGD, OPT_SGD_MOMENTUM, OPT_ADAM = 0, 1, 2

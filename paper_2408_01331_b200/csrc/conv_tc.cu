@@ -195,59 +195,77 @@ __global__ void __launch_bounds__(CT_THREADS) im2col_kernel(const hnn_convtc_pro
 
 int im2col_smem_bytes(int k) { return IC_PIX * (IC_CH * k * k + 1) * 4; }
 
-// dyT[m, f] = dy[b, f, hw] (m = b*HW + hw) through a 32 x 32 shared-memory tile per (b, hw, f)
-// block; bpart[b, th, f] = sum over the tile's 32 pixels of dy[b, f, hw] (bias gradient partials).
+// dyT[m, f] = dy[b, f, hw] (m = b*HW + hw) through 32 x 32 shared-memory tiles; one CTA = 32
+// channels x TR_TILES consecutive (sample, 32-pixel run) units, every thread's 4 * TR_TILES loads issued
+// before the first store (one 32 x 32 tile per CTA: a few dependent round trips per 4 KB, 1.4-2 TB/s
+// on C4); bpart[b, th, f] = sum over pixel run th of dy[b, f, hw] (bias gradient partials).
+constexpr int TR_TILES = HNN_CONVTC_TRANSPOSE_HW_TILES;
 __global__ void __launch_bounds__(CT_THREADS) transpose_dy_kernel(const hnn_convtc_problem* __restrict__ probs,
                                                                  int nprob, const hnn_step_row* __restrict__ cur,
                                                                  const hnn_model_status* __restrict__ status) {
   hnn::pdl_wait();
-  __shared__ float tile[32][33];
+  __shared__ float tile[TR_TILES][32][33];
   const hnn_convtc_problem& p = ct_problem(probs, nprob, blockIdx.x);
   if (!live(cur, status, p.model)) return;
   const int rows = cur[p.model].rows;
   const int hw_n = p.oh * p.ow;
   const int tiles_hw = (hw_n + 31) / 32, tiles_f = (p.f + 31) / 32;
   const int t = blockIdx.x - p.block_base;
-  const int b = t / (tiles_hw * tiles_f), r = t - b * tiles_hw * tiles_f;
-  const int th = r / tiles_f, tf = r - th * tiles_f;
-  if (b >= rows) return;  // rows beyond the batch are never read by the GEMMs
+  // units q = (sample, pixel run) in row-major order, TR_TILES consecutive units per CTA (several
+  // samples per CTA when a plane has fewer than TR_TILES runs)
+  const int q0 = (t / tiles_f) * TR_TILES, tf = t - (t / tiles_f) * tiles_f, nq = rows * tiles_hw;
   const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // 32 x 8
-  // all four loads first (a store consuming each loaded value right away serialised the loads:
-  // the compiler cannot move a load of dy above a store to dyk)
-  float v[4];
+  int ub[TR_TILES], uh[TR_TILES];  // unit's sample and first pixel (ub = -1: past the batch)
 #pragma unroll
-  for (int i = 0; i < 4; ++i) {
-    const int f = tf * 32 + ty + 8 * i, hw = th * 32 + tx;
-    v[i] = (f < p.f && hw < hw_n) ? __ldg(p.dy + (size_t(b) * p.f + f) * hw_n + hw) : 0.0f;
+  for (int u = 0; u < TR_TILES; ++u) {
+    const int q = q0 + u, b = q / tiles_hw;
+    ub[u] = q < nq ? b : -1;  // rows beyond the batch are never read by the GEMMs
+    uh[u] = (q - b * tiles_hw) * 32;
   }
+  if (ub[0] < 0) return;
+  float v[TR_TILES][4];
 #pragma unroll
-  for (int i = 0; i < 4; ++i) {
-    const int j = ty + 8 * i, f = tf * 32 + j, hw = th * 32 + tx;
-    tile[j][tx] = v[i];
-    if (p.bf16 && p.dyk && f < p.f && hw < hw_n)  // dyk[f, b*HW + hw]: filter-major, pixel-contiguous
-      reinterpret_cast<__nv_bfloat16*>(p.dyk)[size_t(f) * p.pix_ld + size_t(b) * hw_n + hw] = __float2bfloat16_rn(v[i]);
-  }
+  for (int u = 0; u < TR_TILES; ++u)
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int f = tf * 32 + ty + 8 * i, hw = uh[u] + tx;
+      v[u][i] = (ub[u] >= 0 && f < p.f && hw < hw_n) ? __ldg(p.dy + (size_t(ub[u]) * p.f + f) * hw_n + hw) : 0.0f;
+    }
+#pragma unroll
+  for (int u = 0; u < TR_TILES; ++u)
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int j = ty + 8 * i, f = tf * 32 + j, hw = uh[u] + tx;
+      tile[u][j][tx] = v[u][i];
+      if (p.bf16 && p.dyk && ub[u] >= 0 && f < p.f && hw < hw_n)  // dyk[f, b*HW + hw]: filter-major, pixel-contiguous
+        reinterpret_cast<__nv_bfloat16*>(p.dyk)[size_t(f) * p.pix_ld + size_t(ub[u]) * hw_n + hw] =
+            __float2bfloat16_rn(v[u][i]);
+    }
   __syncthreads();
   const int fld = p.bf16 ? (p.f + 7) & ~7 : (p.f + 3) & ~3;  // dyt rows padded to 16 bytes (TMA)
-  if (p.dyt)
-    for (int j = ty; j < 32; j += 8) {
-      const int hw = th * 32 + j, f = tf * 32 + tx;
-      if (hw < hw_n && f < p.f) {
-        const size_t o = (size_t(b) * hw_n + hw) * fld + f;
-        if (p.bf16) reinterpret_cast<__nv_bfloat16*>(p.dyt)[o] = __float2bfloat16_rn(tile[tx][j]);
-        else p.dyt[o] = tile[tx][j];
-      }
-    }
-  // bias partial of this tile: bpart[b, th, f] = sum over the tile's 32 pixels of dy[b, f, hw]
-  // (fixed order; the reduce adds the tiles in (b, th) order).  A per-(b, f) sequential sum over all
-  // HW pixels was a 1024-long dependent chain per thread (0.1-0.16 ms per C4 layer).
-  if (ty == 0 && p.bpart) {
+  if (p.dyt) {
     const int f = tf * 32 + tx;
-    if (f < p.f) {
+#pragma unroll
+    for (int u = 0; u < TR_TILES; ++u)
+      for (int j = ty; j < 32; j += 8) {
+        const int hw = uh[u] + j;
+        if (ub[u] >= 0 && hw < hw_n && f < p.f) {
+          const size_t o = (size_t(ub[u]) * hw_n + hw) * fld + f;
+          if (p.bf16) reinterpret_cast<__nv_bfloat16*>(p.dyt)[o] = __float2bfloat16_rn(tile[u][tx][j]);
+          else p.dyt[o] = tile[u][tx][j];
+        }
+      }
+  }
+  // bias partial of each pixel run: bpart[b, th, f] = sum over its 32 pixels of dy[b, f, hw]
+  // (fixed order; the reduce adds the runs in (b, th) order).  A per-(b, f) sequential sum over all
+  // HW pixels was a 1024-long dependent chain per thread (0.1-0.16 ms per C4 layer).
+  if (ty < TR_TILES && p.bpart) {
+    const int f = tf * 32 + tx, q = q0 + ty;
+    if (f < p.f && q < nq) {
       float acc = 0.0f;
 #pragma unroll 8
-      for (int j = 0; j < 32; ++j) acc = __fadd_rn(acc, tile[tx][j]);  // pixels th*32 + j (0 past HW)
-      p.bpart[(size_t(b) * tiles_hw + th) * p.f + f] = acc;
+      for (int j = 0; j < 32; ++j) acc = __fadd_rn(acc, tile[ty][tx][j]);  // pixels th*32 + j (0 past HW)
+      p.bpart[size_t(q) * p.f + f] = acc;  // (q = b * tiles_hw + th)
     }
   }
 }

@@ -1010,8 +1010,9 @@ class DeviceHybrid:
         imp = [(s, st) for s, st in items if st.im_dg]
         if imp:  # NHWC dy (+ the weight-gradient copies and bias partials of the same transpose)
             out.append(self._convtc_aux(N.CONVTC_TRANSPOSE_DY, imp, f"{label}/tc/transpose",
-                                        lambda s, st: (s.batch_size * -(-(self._conv_out(st)[1] * self._conv_out(st)[2]) // 32)
-                                                       * -(-self._conv_out(st)[0] // 32))))
+                                        lambda s, st: N.transpose_blocks(s.batch_size,
+                                                                         self._conv_out(st)[1] * self._conv_out(st)[2],
+                                                                         self._conv_out(st)[0])))
         for s, st in items:
             if st.im_dg:
                 continue
@@ -1148,7 +1149,7 @@ class DeviceHybrid:
                     probs.append((s, N.ConvTcProblem(dy=_ptr(st.x), dyt=_ptr(st.xh), cap=s.batch_size, f=c, oh=h,
                                                      ow=w, model=s.index, bf16=1)))
                 out.append(self._aux_table(N.CONVTC_TRANSPOSE_DY, probs, f"{label}/tc/nhwc",
-                                           lambda pr: pr.cap * -(-(pr.oh * pr.ow) // 32) * -(-pr.f // 32), 3))
+                                           lambda pr: N.transpose_blocks(pr.cap, pr.oh * pr.ow, pr.f), 3))
             # (no im2col at all for a layer whose NHWC input came from the previous epilogue and
             # whose weight gradient is implicit too)
             cols_items = [(s, st) for s, st in items if not (st.xh_from_prev and st.im_wg)]
@@ -1178,7 +1179,7 @@ class DeviceHybrid:
             if fins:
                 out.append(self._splitk_finish(fins, f"{label}/tc/splitk"))
             return out
-        tiles_t = lambda s, st: (s.batch_size * -(-(geo(st)[4] * geo(st)[5]) // 32) * -(-geo(st)[3] // 32))
+        tiles_t = lambda s, st: N.transpose_blocks(s.batch_size, geo(st)[4] * geo(st)[5], geo(st)[3])
         if op == N.HNN_DGRAD:
             # (only stages whose input gradient is needed reach here)
             fw = [(s, st) for s, st in items if st.dg_fwd]
