@@ -319,6 +319,18 @@ typedef struct hnn_conv_problem {
   int32_t tiles_n;
   int32_t splits;     /* WGRAD: number of fixed K chunks */
   int32_t split_len;  /* WGRAD: GEMM-K elements per chunk (multiple of OH*OW not required) */
+  /* Direct path only, may be NULL (max-pools folded into a direct conv instead of their own launch):
+   * DGRAD / WGRAD: the layer's output feeds a 2 x 2 / stride-2 max-pool (OH, OW even) whose backward
+   *   is folded into this layer's dy staging: dy[b, f, oy, ox] = np_mask(0 + (pool_idx[w] == (oy&1)*2
+   *   + (ox&1) ? pool_dy[w] : 0), pool_mask[b, f, oy, ox]) with w = (b, f, oy/2, ox/2) -- exactly
+   *   hnn_grouped_maxpool's DGRAD (pool_mask NULL: no relu mask); `dy` is never written or read.
+   * FWD: the layer's input x is the output of a 2 x 2 / stride-2 max-pool of pool_x [cap, C, 2H, 2W]
+   *   computed while staging (hnn_grouped_maxpool's FWD arithmetic), which also writes the pool's
+   *   outputs x (= pool_y) and pool_idx, zeros for rows past the batch. */
+  const float* pool_dy;   /* DGRAD / WGRAD: [cap, F, OH/2, OW/2] */
+  uint8_t* pool_idx;      /* [cap, F, OH/2, OW/2] (DGRAD / WGRAD, read) / [cap, C, H, W] (FWD, written) */
+  const float* pool_mask; /* DGRAD / WGRAD: [cap, F, OH, OW] or NULL */
+  const float* pool_x;    /* FWD: the pool's input [cap, C, 2H, 2W] */
 } hnn_conv_problem;
 
 int hnn_conv_tile_shape(int op, int32_t* tile_m, int32_t* tile_n);
@@ -341,6 +353,8 @@ int hnn_grouped_conv_direct(int op, const hnn_conv_problem* probs, int nprob, in
  * has at most 128 register-blocked work items per sample, else 256), and the launch taking it
  * (`threads` = max over the launch's problems; hnn_grouped_conv_direct launches 256). */
 int hnn_conv_direct_threads(int op, int c, int h, int w, int f, int k, int oh, int ow);
+/* hnn_grouped_conv_direct_ex op for a forward whose problems may carry pool_x (folded max-pools). */
+#define HNN_CONV_DIRECT_FWD_POOLED 16
 int hnn_grouped_conv_direct_ex(int op, const hnn_conv_problem* probs, int nprob, int total_blocks, int smem,
                                int threads, const hnn_step_row* cur, const hnn_model_status* status, void* stream);
 

@@ -70,7 +70,8 @@ class ConvProblem(C.Structure):
                 ("partial", P), ("dw", P), ("db", P),
                 ("cap", I), ("c", I), ("h", I), ("w", I), ("f", I), ("k", I), ("stride", I), ("pad", I),
                 ("oh", I), ("ow", I), ("model", I), ("relu", I), ("tile_base", I), ("tiles_n", I),
-                ("splits", I), ("split_len", I)]
+                ("splits", I), ("split_len", I), ("pool_dy", P), ("pool_idx", P), ("pool_mask", P),
+                ("pool_x", P)]
 
 
 class ConvTcProblem(C.Structure):
@@ -94,6 +95,7 @@ class PoolProblem(C.Structure):
 
 
 POOL_ELEMENTWISE, POOL_WINDOWS_2X2 = 0, 1  # (hnn_b200.h)
+CONV_DIRECT_FWD_POOLED = 16  # (hnn_b200.h: hnn_grouped_conv_direct_ex op, forward with folded max-pools)
 # HNN_POOL_WINDOWS_PER_BLOCK: the library's build constant (the override is for variant builds only)
 POOL_WINDOWS_PER_BLOCK = int(os.environ.get("HNN_POOL_WINDOWS_PER_BLOCK", "1024"))
 

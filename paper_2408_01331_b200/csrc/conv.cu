@@ -293,6 +293,109 @@ __device__ __forceinline__ void stage_rows(float* dst, const float* __restrict__
   }
 }
 
+// dy of nplanes (sample, filter) planes starting at plane pl0 of a layer whose 2 x 2 / stride-2
+// max-pool backward is folded into the staging (hnn_conv_problem.pool_*): one unit per pool window
+// (its gradient, argmax and the relu mask's two row pairs loaded together, every unit's loads issued
+// before the first store), maxpool2_bwd's arithmetic (pool_relu.cu), so the staged values are
+// bit-identical to the pool launch's dx.  Element (plane, oy, ox) goes to dst[plane * PS + oy * RS + ox].
+__device__ __forceinline__ void stage_dy_pooled(float* dst, const hnn_conv_problem& p, size_t pl0, int nplanes,
+                                                int PS, int RS) {
+  const int pw = p.ow >> 1, pohw = (p.oh >> 1) * pw, ohw = p.oh * p.ow;
+  const int total = nplanes * pohw;
+  constexpr int U = 4;
+  for (int e0 = threadIdx.x; e0 < total; e0 += U * blockDim.x) {
+    float d[U];
+    int ix[U];
+    float2 m0[U], m1[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int e = e0 + u * blockDim.x;
+      d[u] = 0.0f;
+      ix[u] = -1;
+      m0[u] = m1[u] = make_float2(1.0f, 1.0f);
+      if (e < total) {
+        const int pl = e / pohw, t = e - pl * pohw, wy = t / pw, wx = t - wy * pw;
+        const size_t o = pl0 * pohw + e;
+        d[u] = __ldg(p.pool_dy + o);
+        ix[u] = __ldg(p.pool_idx + o);
+        if (p.pool_mask) {
+          const float* mk = p.pool_mask + (pl0 + pl) * ohw + (2 * wy) * p.ow + 2 * wx;
+          m0[u] = __ldg(reinterpret_cast<const float2*>(mk));
+          m1[u] = __ldg(reinterpret_cast<const float2*>(mk + p.ow));
+        }
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int e = e0 + u * blockDim.x;
+      if (e >= total) break;
+      const int pl = e / pohw, t = e - pl * pohw, wy = t / pw, wx = t - wy * pw;
+      float g[4];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) g[k] = __fadd_rn(0.0f, ix[u] == k ? d[u] : 0.0f);  // np.add.at into zeros
+      if (p.pool_mask) {
+        g[0] = np_mask(g[0], m0[u].x);
+        g[1] = np_mask(g[1], m0[u].y);
+        g[2] = np_mask(g[2], m1[u].x);
+        g[3] = np_mask(g[3], m1[u].y);
+      }
+      float* o = dst + pl * PS + (2 * wy) * RS + 2 * wx;
+      o[0] = g[0];
+      o[1] = g[1];
+      o[RS] = g[2];
+      o[RS + 1] = g[3];
+    }
+  }
+}
+
+// Forward staging of sample b's input when x is a folded 2 x 2 / stride-2 max-pool of p.pool_x:
+// every pooled element is computed once (maxpool2_fwd's numpy-argmax scan, pool_relu.cu), staged,
+// and written out as the pool's y (= p.x) and argmax (p.pool_idx) for the backward.
+__device__ __forceinline__ void stage_pooled_x(float* dst, const hnn_conv_problem& p, int b, int c, int h, int w,
+                                               int rs, int cs) {
+  const int hw = h * w, total = c * hw, w2 = 2 * w;
+  const float* src = p.pool_x + size_t(b) * c * 4 * hw;
+  float* y = const_cast<float*>(p.x) + size_t(b) * total;
+  uint8_t* idx = p.pool_idx + size_t(b) * total;
+  for (int e0 = threadIdx.x; e0 < total; e0 += 4 * blockDim.x) {
+    float2 r0[4], r1[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int e = e0 + u * blockDim.x;
+      r0[u] = r1[u] = make_float2(0.0f, 0.0f);
+      if (e < total) {
+        const int pl = e / hw, t = e - pl * hw, oy = t / w, ox = t - oy * w;
+        const float* s0 = src + size_t(pl) * 4 * hw + (2 * oy) * w2 + 2 * ox;
+        r0[u] = __ldg(reinterpret_cast<const float2*>(s0));
+        r1[u] = __ldg(reinterpret_cast<const float2*>(s0 + w2));
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int e = e0 + u * blockDim.x;
+      if (e >= total) break;
+      // numpy argmax over (0,0) (0,1) (1,0) (1,1): first max wins, first NaN wins outright
+      float best = r0[u].x;
+      int best_i = 0;
+      bool stop = best != best;
+      const auto scan = [&](float v, int k) {
+        if (!stop && !(v <= best)) {
+          best = v;
+          best_i = k;
+          stop = v != v;
+        }
+      };
+      scan(r0[u].y, 1);
+      scan(r1[u].x, 2);
+      scan(r1[u].y, 3);
+      const int pl = e / hw, t = e - pl * hw, oy = t / w, ox = t - oy * w;
+      dst[pl * cs + oy * rs + ox] = best;
+      y[e] = best;
+      idx[e] = (uint8_t)best_i;
+    }
+  }
+}
+
 // Register-blocked stride-1 paths (LeNet-class layers): a thread computes 4 consecutive outputs of
 // one row, so each staged input row segment (4 + K - 1 values) and each weight are loaded from
 // shared memory once for 4 * K FMAs (the one-output-per-thread loop issued 2 shared loads per
@@ -532,8 +635,10 @@ __device__ __forceinline__ int wgrad_fg(const ConvGeom& g, int threads) {
   return 1;
 }
 
-template <int OP>
-__global__ void __launch_bounds__(DTHREADS, 3) conv_direct_kernel(const hnn_conv_problem* __restrict__ probs, int nprob,
+// POOLX (FWD only): problems may carry a folded max-pool of their input (hnn_conv_problem.pool_x); a
+// separate instantiation because the staging branch alone made ptxas spill in the compute paths.
+template <int OP, bool POOLX = false>
+__global__ void __launch_bounds__(DTHREADS, POOLX ? 2 : 3) conv_direct_kernel(const hnn_conv_problem* __restrict__ probs, int nprob,
                                                                const hnn_step_row* __restrict__ cur,
                                                                const hnn_model_status* __restrict__ status) {
   hnn::pdl_wait();
@@ -549,12 +654,18 @@ __global__ void __launch_bounds__(DTHREADS, 3) conv_direct_kernel(const hnn_conv
     float* yb = p.y + size_t(b) * g.f * g.ohw;
     if (b >= rows) {
       for (int e = threadIdx.x; e < g.f * g.ohw; e += blockDim.x) yb[e] = 0.0f;
+      if (POOLX && p.pool_x)  // (the folded pool's outputs for rows past the batch: zeros, like its own launch)
+        for (int e = threadIdx.x; e < g.c * g.hw; e += blockDim.x) {
+          const_cast<float*>(p.x)[size_t(b) * g.c * g.hw + e] = 0.0f;
+          p.pool_idx[size_t(b) * g.c * g.hw + e] = 0;
+        }
       return;
     }
     const DirectLayout lay(g.c, g.h, g.w, g.k, g.oh, g.ow);
     float* xs = sm;                 // [C][H][rs], channel stride cs
     float* ws = sm + ((g.c * lay.cs + 3) & ~3);  // [F][C*k*k] (generic) / [C*k*k][fp] (blocked; float4 rows)
-    stage_rows(xs, p.x + size_t(b) * g.c * g.hw, g.c * g.h, g.w, g.h, lay.rs, lay.cs);
+    if (POOLX && p.pool_x) stage_pooled_x(xs, p, b, g.c, g.h, g.w, lay.rs, lay.cs);
+    else stage_rows(xs, p.x + size_t(b) * g.c * g.hw, g.c * g.h, g.w, g.h, lay.rs, lay.cs);
     if (g.s == 1 && (g.k == 5 || g.k == 3)) {
       const int fp = (g.f + 3) & ~3;
       for (int e = threadIdx.x; e < g.ckk * fp; e += blockDim.x) {  // tap-major, filters innermost
@@ -612,7 +723,8 @@ __global__ void __launch_bounds__(DTHREADS, 3) conv_direct_kernel(const hnn_conv
         wt[e] = c < g.c ? __ldg(p.weight + (size_t(f) * g.c + c) * g.k * g.k + ij) : 0.0f;
       }
       __syncthreads();
-      stage_rows(dp + L.pd * L.rs + L.pd, p.dy + size_t(b) * g.f * g.ohw, g.f * g.oh, g.ow, g.oh, L.rs, L.plane);
+      if (p.pool_idx) stage_dy_pooled(dp + L.pd * L.rs + L.pd, p, size_t(b) * g.f, g.f, L.plane, L.rs);
+      else stage_rows(dp + L.pd * L.rs + L.pd, p.dy + size_t(b) * g.f * g.ohw, g.f * g.oh, g.ow, g.oh, L.rs, L.plane);
       __syncthreads();
       const int groups8 = (g.c + 7) / 8, qb = (g.w + RB - 1) / RB;
       const bool cg8 = groups8 * g.h * qb >= 128;
@@ -623,7 +735,8 @@ __global__ void __launch_bounds__(DTHREADS, 3) conv_direct_kernel(const hnn_conv
     }
     float* ds = sm;                  // [F][OH][OW]
     float* ws = sm + g.f * g.ohw;    // [F][C][k][k]
-    stage(ds, p.dy + size_t(b) * g.f * g.ohw, g.f * g.ohw);
+    if (p.pool_idx) stage_dy_pooled(ds, p, size_t(b) * g.f, g.f, g.ohw, g.ow);
+    else stage(ds, p.dy + size_t(b) * g.f * g.ohw, g.f * g.ohw);
     stage(ws, p.weight, g.f * g.ckk);
     __syncthreads();
     for (int e = threadIdx.x; e < g.c * g.hw; e += blockDim.x) {
@@ -661,7 +774,8 @@ __global__ void __launch_bounds__(DTHREADS, 3) conv_direct_kernel(const hnn_conv
     float* xs = sm;                                            // [nb][C] x (H x rs), channel stride cs
     float* ds = sm + HNN_CONV_DIRECT_BCHUNK * g.c * cs;        // [nb][F] dy planes (OH x OW), stride ps
     stage_rows(xs, p.x + size_t(b0) * g.c * g.hw, nb * g.c * g.h, g.w, g.h, rs, cs);
-    stage_rows(ds, p.dy + size_t(b0) * g.f * g.ohw, nb * g.f, g.ohw, 1, g.ohw, ps);
+    if (p.pool_idx) stage_dy_pooled(ds, p, size_t(b0) * g.f, nb * g.f, ps, g.ow);
+    else stage_rows(ds, p.dy + size_t(b0) * g.f * g.ohw, nb * g.f, g.ohw, 1, g.ohw, ps);
     __syncthreads();
     if (g.s == 1 && (g.k == 5 || g.k == 3)) {
       float* red = ds + HNN_CONV_DIRECT_BCHUNK * g.f * ps;  // [G][f*c*k][k] group partials
@@ -784,8 +898,14 @@ extern "C" int hnn_grouped_conv_direct_ex(int op, const hnn_conv_problem* probs,
   HNN_REQUIRE(threads >= 32 && threads <= hnn::DTHREADS && threads % 32 == 0, "hnn_grouped_conv_direct", "bad block size");
   HNN_REQUIRE(smem > 0 && smem <= 200 * 1024, "hnn_grouped_conv_direct", "layer too large for the direct path");
   cudaStream_t s = hnn::as_stream(stream);
-  static int configured[3] = {0, 0, 0};
-  if (op == HNN_FWD) {
+  static int configured[4] = {0, 0, 0, 0};
+  if (op == HNN_CONV_DIRECT_FWD_POOLED) {
+    if (smem > configured[3]) {
+      cudaFuncSetAttribute(hnn::conv_direct_kernel<HNN_FWD, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+      configured[3] = 200 * 1024;
+    }
+    hnn::launch_pdl(hnn::conv_direct_kernel<HNN_FWD, true>, dim3(total_blocks), dim3(threads), smem, s, probs, nprob, cur, status);
+  } else if (op == HNN_FWD) {
     if (smem > configured[0]) {
       cudaFuncSetAttribute(hnn::conv_direct_kernel<HNN_FWD>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
       configured[0] = 200 * 1024;

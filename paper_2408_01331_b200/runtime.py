@@ -1340,6 +1340,13 @@ class DeviceHybrid:
                           f=f, k=k, stride=st.attrs.get("stride", 1), pad=st.attrs.get("padding", 0), oh=oh, ow=ow,
                           model=s.index, relu=int(st.relu), splits=st.splits, split_len=CONV_SPLIT_LEN)
             cols = c * k * k + 1
+            fold = getattr(st, "pool_fold", None)
+            if direct and fold is not None and op != N.HNN_FWD:  # (the pool's backward in the dy staging)
+                common.update(pool_dy=_ptr(fold.dy), pool_idx=_ptr(fold.idx),
+                              pool_mask=_ptr(fold.x) if fold.mask_input else 0)
+            pfwd = getattr(st, "pool_fwd", None)
+            if direct and pfwd is not None and op == N.HNN_FWD:  # (the pool's forward in the x staging)
+                common.update(pool_x=_ptr(pfwd.x), pool_idx=_ptr(pfwd.idx))
             if direct:
                 tiles_n = 1
                 tiles = st.splits if op == N.HNN_WGRAD else s.batch_size
@@ -1362,7 +1369,9 @@ class DeviceHybrid:
             flops += 2 * s.batch_size * oh * ow * f * c * k * k
         t = _dev_table(N.ConvProblem, probs, self.device)
         if direct:
-            args = (op, _ptr(t), len(probs), base, smem, threads, _ptr(self.cur), _ptr(self.status))
+            pooled = op == N.HNN_FWD and any(getattr(st, "pool_fwd", None) is not None for _, st in items)
+            args = (N.CONV_DIRECT_FWD_POOLED if pooled else op, _ptr(t), len(probs), base, smem, threads,
+                    _ptr(self.cur), _ptr(self.status))
             out = [Launch("hnn_grouped_conv_direct_ex", args, t, label, flops=flops)]
         else:
             out = [Launch("hnn_grouped_conv", (op, _ptr(t), len(probs), base, _ptr(self.cur), _ptr(self.status)), t,
@@ -1434,7 +1443,10 @@ class DeviceHybrid:
             elif kind == "conv":
                 out += self._conv_launch(op, group, f"{label}/conv")
             elif kind == "pool":
-                out += self._pool_launch(N.HNN_FWD if op == N.HNN_FWD else N.HNN_DGRAD, group, f"{label}/pool")
+                if op == N.HNN_FWD:  # (pools folded into the next direct conv's input staging: no launch)
+                    group = [(s, st) for s, st in group if not getattr(st, "fwd_folded", False)]
+                if group:
+                    out += self._pool_launch(N.HNN_FWD if op == N.HNN_FWD else N.HNN_DGRAD, group, f"{label}/pool")
             elif kind == "embed":
                 if op == N.HNN_FWD:  # (an embedding never needs an input gradient: it reads the input)
                     out += self._embed_launch(N.HNN_FWD, group, f"{label}/embed")
@@ -1548,6 +1560,41 @@ class DeviceHybrid:
                         and f % 8 == 0):
                     a.xh_next, b.xh_from_prev = b.xh, True
 
+    def _link_pool_folds(self):
+        """A direct (LeNet-class) conv whose output feeds a 2 x 2 / stride-2 max-pool on even planes
+        stages its dy through the pool's backward (hnn_conv_problem.pool_*: argmax select + relu mask,
+        maxpool2_bwd's arithmetic, so bit-identical) and the pool's backward launch is dropped (C2's
+        first pool gradient alone was a 45 us launch).  The conv then reads the pool's dy, which
+        lives in the ping-pong buffer its own dx would overwrite, so a conv that needs dx gets a
+        dx buffer of its own (and the stage below reads its dy from there).  Forward: a direct conv
+        whose input is such a pool's output computes the pool while staging its input (writing the
+        pool's y and argmax) and the pool's forward launch is dropped.  HNN_POOL_FOLD=0: off; =bwd:
+        backward folds only."""
+        torch = _torch()
+        mode = os.environ.get("HNN_POOL_FOLD", "1")
+        even22 = lambda b: (b.attrs["kernel"] == 2 and b.attrs.get("stride", 2) == 2
+                            and b.in_shape[1] % 2 == 0 and b.in_shape[2] % 2 == 0)
+        for s in self.slots:
+            for st in s.stages:
+                st.pool_fold, st.folded, st.pool_fwd, st.fwd_folded = None, False, None, False
+            if mode == "0":
+                continue
+            for a, b in zip(s.stages, s.stages[1:]):
+                if (mode != "bwd" and a.kind == "pool" and b.kind == "conv" and getattr(b, "direct", False)
+                        and b.x is a.y and even22(a) and getattr(a, "xh_next", None) is None):
+                    b.pool_fwd, a.fwd_folded = a, True
+            for k, (a, b) in enumerate(zip(s.stages, s.stages[1:])):
+                if not (a.kind == "conv" and getattr(a, "direct", False) and b.kind == "pool" and b.x is a.y):
+                    continue
+                if not even22(b):
+                    continue
+                a.pool_fold, b.folded = b, True
+                if a.needs_dx and getattr(a, "fold_dx", None) is None:
+                    cap = s.batch_size
+                    a.fold_dx = torch.zeros(cap * a.ld_in, dtype=torch.float32, device=self.device)
+                    a.dx = a.fold_dx.view(cap, a.ld_in)
+                    s.stages[k - 1].dy = a.dx
+
     def _tail_eligible(self, s) -> bool:
         """Models whose logits layer takes the fused tail (hnn_logits_tail): a final plain dense layer
         with <= 16 classes, 16-byte rows and a small input (cap * K <= 16K floats: C1 / C5's 64 x 256,
@@ -1603,6 +1650,7 @@ class DeviceHybrid:
         waves = self._stage_waves()
         self._pending_reduce = []
         self._link_nhwc_producers()
+        self._link_pool_folds()
         fwd = []
         for w, items in enumerate(waves):
             fwd += self._wave_launches(N.HNN_FWD, items, f"fwd{w}")
@@ -1627,7 +1675,7 @@ class DeviceHybrid:
             for l in fused_l:
                 l.label = f"bwd{w}/dense/skinny_bwd"
             done = {id(st) for _, st in fused}
-            dg = [(s, st) for s, st in items if st.needs_dx and id(st) not in done]
+            dg = [(s, st) for s, st in items if st.needs_dx and id(st) not in done and not st.folded]
             if dg:
                 bwd += self._wave_launches(N.HNN_DGRAD, dg, f"bwd{w}")
             bwd += fused_l

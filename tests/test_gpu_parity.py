@@ -1090,6 +1090,39 @@ def test_split_k_forward_is_bit_identical(pkg, monkeypatch):
             assert np.array_equal(a[k], b[k]), k
 
 
+@pytest.mark.parametrize("workload", ["c2", "c4"])
+def test_pool_backward_folded_into_direct_conv_is_bit_identical(pkg, monkeypatch, workload):
+    """LeNet's 2 x 2 max-pool gradients folded into the preceding direct conv's dy staging and the
+    first pool's forward into conv2's input staging (hnn_conv_problem.pool_*; no pool launch, conv2
+    writes its dx to a buffer of its own) reproduce the pool launches exactly: 3 steps end
+    bit-identical (params, gradients, last step's per-model losses) to the unfolded plan
+    (src/ops.py:149-174, 91-130).  C4 mixes the folded LeNets with tensor-core CNNs."""
+    import torch
+
+    import bench
+
+    device = torch.device("cuda", 0)
+    outs, losses = [], []
+    for fold in ("1", "0"):
+        monkeypatch.setenv("HNN_POOL_FOLD", fold)
+        _, jobs, hy, dev, ddev, ds, comm = bench.build_rank(workload, 0, 1, device)
+        pools = [l.label for l in dev.train_plan if l.label.endswith("/pool")]
+        if workload == "c2":  # (LeNet: both pool gradients and the first pool's forward folded)
+            assert pools == (["fwd3/pool"] if fold == "1" else ["fwd1/pool", "fwd3/pool", "bwd3/pool", "bwd1/pool"]), pools
+        rows = bench.schedule(jobs, ds, 3)
+        bench.upload_perms(dev, jobs, ds)
+        dev.load_schedule(rows)
+        dev.train_steps(3, use_graph=True)
+        torch.cuda.synchronize()
+        outs.append([(dev.download_params(m), dev.download_grads(m)) for m in range(len(jobs))])
+        losses.append(dev.loss_out.cpu().numpy())
+    assert np.array_equal(*losses)
+    for (pa, ga), (pb, gb) in zip(*outs):
+        for k in pa:
+            assert np.array_equal(pa[k], pb[k]), k
+            assert np.array_equal(ga[k], gb[k]), k
+
+
 def test_fused_skinny_backward_is_bit_identical(pkg, monkeypatch):
     """C3's logits layers (784-h-h-10, Adam: no optimizer fused into the weight gradient) take one
     hnn_skinny_backward launch for their input and weight gradients; 3 steps end bit-identical (params,
