@@ -348,6 +348,16 @@ __device__ __forceinline__ void stage_dy_pooled(float* dst, const hnn_conv_probl
   }
 }
 
+// pooled elements per thread per round (loads in flight) and the pooled forward's CTAs-per-SM bound:
+// 1 unit at 3 CTAs per SM (80 registers, no spills) measured C2 0.4245 ms against 0.4264 for 2, 4
+// or 8 units at 2 CTAs per SM (4 units at 3 CTAs spilled 700 bytes), profiles/r02/pool_fold_ab_v15.txt
+#ifndef HNN_POOLX_UNITS
+#define HNN_POOLX_UNITS 1
+#endif
+#ifndef HNN_POOLX_MINB
+#define HNN_POOLX_MINB 3
+#endif
+constexpr int PXU = HNN_POOLX_UNITS;
 // Forward staging of sample b's input when x is a folded 2 x 2 / stride-2 max-pool of p.pool_x:
 // every pooled element is computed once (maxpool2_fwd's numpy-argmax scan, pool_relu.cu), staged,
 // and written out as the pool's y (= p.x) and argmax (p.pool_idx) for the backward.
@@ -357,10 +367,10 @@ __device__ __forceinline__ void stage_pooled_x(float* dst, const hnn_conv_proble
   const float* src = p.pool_x + size_t(b) * c * 4 * hw;
   float* y = const_cast<float*>(p.x) + size_t(b) * total;
   uint8_t* idx = p.pool_idx + size_t(b) * total;
-  for (int e0 = threadIdx.x; e0 < total; e0 += 4 * blockDim.x) {
-    float2 r0[4], r1[4];
+  for (int e0 = threadIdx.x; e0 < total; e0 += PXU * blockDim.x) {
+    float2 r0[PXU], r1[PXU];
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {
+    for (int u = 0; u < PXU; ++u) {
       const int e = e0 + u * blockDim.x;
       r0[u] = r1[u] = make_float2(0.0f, 0.0f);
       if (e < total) {
@@ -371,7 +381,7 @@ __device__ __forceinline__ void stage_pooled_x(float* dst, const hnn_conv_proble
       }
     }
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {
+    for (int u = 0; u < PXU; ++u) {
       const int e = e0 + u * blockDim.x;
       if (e >= total) break;
       // numpy argmax over (0,0) (0,1) (1,0) (1,1): first max wins, first NaN wins outright
@@ -638,7 +648,7 @@ __device__ __forceinline__ int wgrad_fg(const ConvGeom& g, int threads) {
 // POOLX (FWD only): problems may carry a folded max-pool of their input (hnn_conv_problem.pool_x); a
 // separate instantiation because the staging branch alone made ptxas spill in the compute paths.
 template <int OP, bool POOLX = false>
-__global__ void __launch_bounds__(DTHREADS, POOLX ? 2 : 3) conv_direct_kernel(const hnn_conv_problem* __restrict__ probs, int nprob,
+__global__ void __launch_bounds__(DTHREADS, POOLX ? HNN_POOLX_MINB : 3) conv_direct_kernel(const hnn_conv_problem* __restrict__ probs, int nprob,
                                                                const hnn_step_row* __restrict__ cur,
                                                                const hnn_model_status* __restrict__ status) {
   hnn::pdl_wait();
