@@ -86,6 +86,9 @@ template <int OP>
 static __device__ __forceinline__ int tc2_chunk_kb(const hnn_gemm_problem* p, int nkb) {
   return (OP == HNN_WGRAD && p->opt_w != nullptr && p->opt_wm == nullptr && nkb <= 4) ? 4 : TC2_CHUNK_KB;
 }
+#ifndef HNN_TC2_NARROW_LAST
+#define HNN_TC2_NARROW_LAST 1
+#endif
 constexpr int TC2_A_BYTES = TC2_BM * TC2_BK * 4;        // 16 KB
 constexpr int TC2_B_BYTES = (TC2_BN / 2) * TC2_BK * 4;  // 16 KB (this CTA's half)
 constexpr int TC2_STAGE = TC2_A_BYTES + TC2_B_BYTES;
@@ -297,6 +300,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC2_THREADS, 1)
     tn = p->tile_n > 0 ? p->tile_n : TC2_BN;  // pair tile columns: 64, 128 or 256
     m0 = (t / p->tiles_n) * (2 * TC2_BM);
     n0 = (t % p->tiles_n) * tn;
+    if (HNN_TC2_NARROW_LAST && !BF16 && B_MN) {
+      // the last column tile of a ragged n takes the narrowest width covering the rest (n = 784:
+      // 3 x 256 + one 64-wide tile instead of a fourth 256-wide one with 16 useful columns); each
+      // output column's sum is independent of the MMA's N, so results are unchanged.  (fp32
+      // input / weight gradients only: their B tiles load in 32-column boxes, so the TMA bytes
+      // follow tn; the K-major forward B box is fixed per problem by its tensor map.)
+      const int rem = p->n - n0;
+      if (rem < tn) tn = rem <= 64 ? 64 : (rem <= 128 ? 128 : tn);
+    }
     nkb = ktot > 0 ? (ktot + KBE - 1) / KBE : 0;
     return nkb > 0;
   };

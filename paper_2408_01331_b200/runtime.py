@@ -692,11 +692,13 @@ class DeviceHybrid:
         ptrs = ("b", "c", "mask") if op == N.HNN_DGRAD else ("b", "c", "opt_w", "opt_wm", "opt_wv")
         return all(d.get(k, 0) % 16 == 0 for k in ptrs)
 
-    def _pair_schedule(self, probs, rows, total_tiles, tm) -> bytes:
+    def _pair_schedule(self, probs, rows, total_tiles, tm, narrow=False) -> bytes:
         """Longest-processing-time assignment of a CTA-pair launch's tiles to its pairs (the
         table trailer read by gemm_tc2.cu): int32 npairs, offsets[npairs + 1], tile ids.
         Cost of a tile = its 32-wide K blocks + a fixed epilogue share.  Which pair computes a
-        tile never changes the tile's arithmetic (bit-exact isolation)."""
+        tile never changes the tile's arithmetic (bit-exact isolation).  narrow: the kernel gives a
+        ragged n's last column tile the narrowest width covering the rest (fp32 input / weight
+        gradients, gemm_tc2.cu tile_info), so its cost uses that width."""
         torch = _torch()
         sms = torch.cuda.get_device_properties(self.device).multi_processor_count
         npairs = max(1, min(total_tiles, sms // 2))
@@ -705,8 +707,13 @@ class DeviceHybrid:
             split = d.get("ksplit", 1) if d.get("ksplit_len") else 1
             kb = -(-(d["ksplit_len"] if split > 1 else d["k"]) // 32)
             tiles = pr.tiles_n * -(-d["m"] // tm) * split
-            width = pr.tile_n / 256  # MMA and operand time scale with the tile's columns
-            costs += [(kb * (0.5 + 0.5 * width) + 3, pr.tile_base + i) for i in range(tiles)]
+            for i in range(tiles):
+                tn = pr.tile_n  # MMA and operand time scale with the tile's columns
+                if narrow:
+                    rem = d["n"] - ((i // split) % pr.tiles_n) * pr.tile_n
+                    if rem < tn:
+                        tn = 64 if rem <= 64 else (128 if rem <= 128 else tn)
+                costs.append((kb * (0.5 + 0.5 * tn / 256) + 3, pr.tile_base + i))
         costs.sort(key=lambda c: (-c[0], c[1]))
         import heapq
 
@@ -877,7 +884,8 @@ class DeviceHybrid:
                     pr.tmap_xh = _ptr(keep) + 512 * i + 384
             extra = b""
             if prec in (N.PREC_3XTF32_PAIR, N.PREC_BF16_PAIR):
-                extra = self._pair_schedule(probs, rows, base, tm)
+                extra = self._pair_schedule(probs, rows, base, tm,
+                                            narrow=prec == N.PREC_3XTF32_PAIR and op != N.HNN_FWD)
             t = _dev_table(N.GemmProblem, probs, self.device, extra)
             flops = sum(2 * d["m"] * d["n"] * d["k"] for _, d in rows)
             # bytes: A + B read once, C written once (fp32); a fused optimizer adds its p/m/v traffic
